@@ -1,0 +1,218 @@
+/*
+ * mpf.h — C ABI of libmpf: single-pass whole-image training of MaxPooling
+ * Convolutional Networks with MaxPoolingFragment (MPF) layers on B200 (sm_100a).
+ *
+ * Method: arxiv 1302.1690.  "processes each training image in a single
+ * pass": a whole image is forward-propagated through C, MPF and FC
+ * layers into an output image x_hat whose every pixel equals the net applied to
+ * the patch at that pixel (§3.2); the loss derivative w.r.t. x_hat
+ * is back-propagated through MPF layers (Alg. 4) and through C/FC
+ * layers over all fragments, summing parameter gradients over fragments (Alg. 2,
+ * PAPER.md:131-140); weights are updated by SGD.
+ *
+ * Conventions (all calls):
+ *   - Every call returns mpf_status; nothing throws or aborts across the ABI.  On a
+ *     non-OK status mpf_last_error() returns a thread-local message.
+ *   - Device pointers ("d_") are CUDA global-memory pointers owned by the caller
+ *     (typically torch tensors).  Host pointers ("h_") are ordinary host memory;
+ *     pinned memory makes the host copies asynchronous.
+ *   - `stream` is a cudaStream_t passed as void*.  Every device call is enqueued on
+ *     it and returns without synchronising (except mpf_check and the host-buffer
+ *     step, which document their syncs).
+ *   - The net owns only host metadata.  All device memory (parameters, gradients,
+ *     tape, scratch) is allocated by the caller with the sizes mpf_net_memory
+ *     reports and attached with mpf_net_bind.
+ *   - Layout of every activation on the device is fragment-major NHWC fp32
+ *     [n_images * F_l, rows, cols, C_l], fragment index
+ *     f_l = f_{l-1} * k^2 + (r * k + c) with the image outermost (reading R2).
+ *   - Parameters/gradients are one flat fp32 vector in the canonical order of
+ *     layer order; W[out][in][kr][kc] row-major, then b[out].
+ */
+#ifndef MPF_H
+#define MPF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPF_VERSION 1
+#define MPF_MAX_LAYERS 24
+
+typedef enum {
+  MPF_OK = 0,
+  MPF_ERR_ARG = 1,      /* NULL / out-of-range argument */
+  MPF_ERR_CONFIG = 2,   /* invalid architecture or geometry */
+  MPF_ERR_DATA = 3,     /* bad labels (>= classes and != 255) or image count */
+  MPF_ERR_INTERNAL = 4, /* consistency failure */
+  MPF_ERR_CUDA = 5,     /* a CUDA runtime/driver call failed */
+  MPF_ERR_STATE = 6     /* call order violated (e.g. backward before forward, unbound net) */
+} mpf_status;
+
+/* layer kinds (§2) */
+enum { MPF_CONV = 0, MPF_POOL = 1, MPF_FC = 2 };
+/* activations ("tanh or logistic"); the last FC must be MPF_IDENTITY (softmax head) */
+enum { MPF_TANH = 0, MPF_IDENTITY = 1, MPF_LOGISTIC = 2 };
+/* precision of the tensor-core convolutions */
+enum { MPF_PREC_TF32 = 0, /* TF32 operands rounded to nearest, fp32 accumulate (north_star) */
+       MPF_PREC_FP32 = 1  /* fp32 CUDA-core convolutions everywhere (reference mode, slow) */ };
+
+/*
+ * One layer.  CONV: k x k valid cross-correlation with n_out maps, full connectivity
+ * (PAPER.md:197), + bias, + act.  POOL: k x k max pooling, realised as an MPF layer
+ * (Alg. 3; n_out, act ignored).  FC: fully-connected over the k x k x C volume left at
+ * that depth in patch mode (k = 1 after the first FC), evaluated over fragments as a
+ * k x k convolution (north_star; reading R12).
+ */
+typedef struct {
+  int32_t kind, k, n_out, act;
+} mpf_layer;
+
+typedef struct {
+  int32_t in_channels;  /* maps of the input image (1 for the BASELINE configs) */
+  int32_t patch;        /* P: square patch = receptive field; must reduce to 1x1 exactly */
+  int32_t image_rows;   /* H */
+  int32_t image_cols;   /* W */
+  int32_t max_images;   /* largest n passed to forward/backward */
+  int32_t precision;    /* MPF_PREC_* */
+  int32_t deterministic;/* reserved: every reduction is already fixed-order */
+  int32_t debug_keep;   /* 1: keep every conv output on the tape (mpf_debug_tape), for parity tests */
+} mpf_config;
+
+/* Geometry of the padded uniform-fragment layout.
+ * Activation l = 0..n_layers (a[0] = zero-padded image, a[l+1] = output of layer l). */
+typedef struct {
+  int32_t n_layers, n_levels, classes;
+  int32_t stride;                 /* S = prod of pooling factors */
+  int32_t n_fragments;            /* fragments per image at the output */
+  int32_t out_rows, out_cols;     /* O = H - P + 1: valid outputs (R7) */
+  int32_t padded_rows, padded_cols; /* H' = P - 1 + S * ceil(O / S) */
+  int32_t frag_rows, frag_cols;   /* output grid per fragment (S * frag_rows >= out_rows) */
+  int64_t n_params;
+  int32_t frag[MPF_MAX_LAYERS + 1]; /* fragments per image of a[l] */
+  int32_t rows[MPF_MAX_LAYERS + 1]; /* valid rows of a[l] per fragment */
+  int32_t cols[MPF_MAX_LAYERS + 1];
+  int32_t chans[MPF_MAX_LAYERS + 1];
+  int64_t w_offset[MPF_MAX_LAYERS]; /* offset of W of layer l in the flat params, -1 for POOL */
+  int64_t b_offset[MPF_MAX_LAYERS];
+} mpf_geometry;
+
+typedef struct mpf_net mpf_net; /* opaque */
+
+/* Library version (MPF_VERSION). */
+int32_t mpf_version(void);
+
+/* Thread-local description of the last error (never NULL). */
+const char* mpf_last_error(void);
+
+/*
+ * validate_arch + plan_geometry (with valid outputs instead of
+ * mirror padding): checks that P reduces to 1x1 exactly at the last layer, that the
+ * last layer is an FC with identity activation, and plans the padded layout.  No
+ * device memory is touched.  MPF_ERR_CONFIG on an invalid architecture.
+ */
+mpf_status mpf_net_create(const mpf_config* cfg, const mpf_layer* layers, int32_t n_layers,
+                          mpf_net** out);
+void mpf_net_destroy(mpf_net* net);
+
+mpf_status mpf_net_geometry(const mpf_net* net, mpf_geometry* out);
+
+/*
+ * Device bytes the caller must provide for n_images images (n_images <= max_images):
+ * params and grads (n_params fp32 each), the tape (pooled fragments + argmax +
+ * FC activations kept from forward to backward) and scratch (transient conv
+ * outputs, deltas, packed weights, reduction partials, staging for host inputs).
+ * Every buffer must be 256-byte aligned (torch allocations are).
+ */
+mpf_status mpf_net_memory(const mpf_net* net, int32_t n_images, uint64_t* params_bytes,
+                          uint64_t* grads_bytes, uint64_t* tape_bytes, uint64_t* scratch_bytes);
+
+/* Attach caller-owned device buffers sized by mpf_net_memory(net, n_images, ...). */
+mpf_status mpf_net_bind(mpf_net* net, void* d_params, void* d_grads, void* d_tape, void* d_scratch,
+                        int32_t n_images);
+
+/*
+ * Whole-image forward (Alg. 1 per layer, Alg. 3 for MPF) of n images
+ * d_images [n, in_channels, H, W] fp32 (read again by mpf_backward_image: keep it
+ * alive and unchanged until then).  The image is zero-padded to H' x W' on the fly
+ * (padded outputs are ignored by the loss).  If d_probs is not NULL, the softmax
+ * output of every fragment position is written to d_probs
+ * [n * n_fragments, frag_rows, frag_cols, classes] (use mpf_fragments_to_pixels to
+ * reassemble x_hat).  Overwrites the tape.
+ */
+mpf_status mpf_forward_image(mpf_net* net, const float* d_images, int32_t n, float* d_probs,
+                             void* stream);
+
+/*
+ * Loss and back-propagation for the images of the last forward.
+ * d_labels [n, out_rows, out_cols] uint8 on the output grid (reading R7), 255 = ignore.
+ * h_class_w: `classes` host floats (NULL = all 1; "MCCE per class").
+ * Per image: loss = mean over labelled pixels of -w_t log p_t (R8), written to
+ * d_loss[n] (device, may be NULL); gradients of that per-image mean are ADDED to the
+ * bound gradient buffer (Alg. 2 accumulation; micro-batches sum).  Labels >= classes
+ * other than 255 are ignored and raise a device flag reported by mpf_check.
+ */
+mpf_status mpf_backward_image(mpf_net* net, const uint8_t* d_labels, const float* h_class_w,
+                              float* d_loss, void* stream);
+
+/* SGD: theta <- theta - lr * grad_scale * g ; g <- 0. */
+mpf_status mpf_sgd_step(mpf_net* net, float lr, float grad_scale, void* stream);
+
+/*
+ * One end-to-end step on HOST buffers: async copy h_images [n, in_channels, H, W]
+ * and h_labels [n, out_rows, out_cols] into the bound staging area, forward,
+ * backward, and an async copy of the per-image losses to h_loss[n].  If apply_sgd,
+ * also mpf_sgd_step(lr, grad_scale).  h_loss is valid after the stream is synchronised.
+ */
+mpf_status mpf_train_step_host(mpf_net* net, const float* h_images, const uint8_t* h_labels,
+                               int32_t n, const float* h_class_w, float* h_loss, int32_t apply_sgd,
+                               float lr, float grad_scale, void* stream);
+
+/*
+ * Defragmentation (lineage_to_pixel SPEC.md:71-79): d_frag
+ * [n * n_fragments, frag_rows, frag_cols, channels] -> d_pixels [n, channels,
+ * out_rows, out_cols], out(y, x) = frag[f(y, x), i(y), j(x)] with the mixed-radix
+ * decode y = r1 + k1 (r2 + k2 (... + kL i)).  Padded positions are dropped.
+ */
+mpf_status mpf_fragments_to_pixels(const mpf_net* net, const float* d_frag, float* d_pixels,
+                                   int32_t n, int32_t channels, void* stream);
+
+/* Copy a tape tensor of the last forward (for parity tests), compact layout:
+ * what = MPF_TAPE_VALUE: a[layer+1] fp32 [n*F, rows, cols, C] (POOL layers: pooled
+ *        values; CONV/FC layers whose output is kept on the tape — every conv output
+ *        when the net was created with debug_keep = 1)
+ * what = MPF_TAPE_ARGMAX: uint8 [n*F, rows, cols, C], index dy*k + dx (POOL layers).
+ * MPF_ERR_ARG if the tensor is not on the tape. */
+enum { MPF_TAPE_VALUE = 0, MPF_TAPE_ARGMAX = 1 };
+mpf_status mpf_debug_tape(const mpf_net* net, int32_t layer, int32_t what, void* d_dst,
+                          void* stream);
+
+/* Synchronise `stream` and report device-side data errors (bad labels) and CUDA errors. */
+mpf_status mpf_check(mpf_net* net, void* stream);
+
+/*
+ * Live kernel timing (for bench.py's roofline): between mpf_profile_begin and
+ * mpf_profile_end every kernel libmpf launches is bracketed by CUDA events recorded on
+ * its own stream.  max_launches bounds the event pool (launches beyond it are not
+ * timed).  mpf_profile_end synchronises the events and returns one record per
+ * (kernel, layer): launch count, summed device milliseconds, and the ALGORITHMIC
+ * flops and bytes of ONE launch (valid positions only, each
+ * tensor read/written once, fp32 = 4 B, argmax/labels = 1 B).
+ */
+typedef struct {
+  char name[40];
+  int32_t layer;
+  int32_t launches;
+  double total_ms;
+  double flops;  /* per launch */
+  double bytes;  /* per launch */
+} mpf_kernel_stat;
+mpf_status mpf_profile_begin(mpf_net* net, int32_t max_launches);
+mpf_status mpf_profile_end(mpf_net* net, mpf_kernel_stat* out, int32_t capacity, int32_t* n_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPF_H */

@@ -1,0 +1,46 @@
+// conv_tc.h — tensor-core (tcgen05 / TMEM, kind::tf32) implicit-GEMM convolutions.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+namespace mpf {
+
+constexpr int kMaxSplits = 296;  // split-K partial slots of the weight-gradient GEMMs (2 x 148 SMs)
+
+// Forward conv and dgrad (a forward correlation of the delta with the rotated pack).
+// x: [n_frag][gr][gc][cin] (NHWC, all grid positions readable; dgrad: delta with zero padding)
+// out: [n_frag][gr][gc][cout] (same grid); valid region out_vr x out_vc
+// out(y, x) = act(bias + sum_{ky,kx,ci} w[co][ky][kx][ci] * x(y + shift + ky, x + shift + kx))
+// with x(.) = 0 outside the fragment.
+struct TcConvArgs {
+  const float* x;
+  int n_frag, gr, gc, cin;
+  const float* w;     // [cout][k][k][cin], tf32-rounded
+  const float* bias;  // nullable
+  int k, cout;
+  float* out;
+  int out_vr, out_vc;
+  int act;
+  int shift;          // 0 (forward) or -(k-1) (dgrad)
+  int round_out;      // round the stored result to tf32 (operand of the next MMA)
+  int zero_pad;       // write zeros at grid positions outside the valid region
+  const float* mul_dact;  // nullable: multiply by act'(mul_dact[same position])
+  int dact;
+};
+
+// Weight gradient: part[s][co][(ky*k+kx)*cin+ci] = sum_{p in split s} dy[p][co] * x[p+(ky,kx)][ci]
+// followed by part_b[s][co] at part + splits*cout*K.
+struct TcWgradArgs {
+  const float* x;
+  const float* dy;    // [n_frag][gr][gc][cout], zero outside the valid region
+  int n_frag, gr, gc, vr_out, vc_out;
+  int cin, cout, k;
+  float* part;
+  size_t part_cap_floats;
+};
+
+bool tc_supported(int cin, int cout, int k);
+cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s);
+cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits, cudaStream_t s);
+
+}  // namespace mpf

@@ -1,0 +1,617 @@
+// kernels.cu — bandwidth-bound kernels of the MPF training path and the CUDA-core
+// (SIMT) convolutions used for narrow layers and as the fp32 reference mode.
+//
+// Paper references: C layer §2 (54-55); MPF forward Alg. 3 (157-172);
+// MPF backward Alg. 4 (174-186) with accumulation of shared maxima (Fig. 2, 143-145);
+// gradient accumulation over fragments Alg. 2 (131-140); MCCE per pixel (197);
+// class-weighted MCCE (252); SGD (210).  Readings R1-R19: DESIGN.md.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "mpf_internal.h"
+
+namespace mpf {
+
+static inline long long mpf_min_ll(long long a, long long b) { return a < b ? a : b; }
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__device__ __forceinline__ float act_fwd(int act, float v) {
+  if (act == MPF_TANH) return tanhf(v);
+  if (act == MPF_LOGISTIC) return 1.f / (1.f + expf(-v));
+  return v;
+}
+
+// derivative of the activation from its output
+__device__ __forceinline__ float act_der(int act, float y) {
+  if (act == MPF_TANH) return 1.f - y * y;
+  if (act == MPF_LOGISTIC) return y * (1.f - y);
+  return 1.f;
+}
+
+// ============================================================================ conv (SIMT)
+// out[f][y][x][co] = act(bias[co] + sum_{ky,kx,ci} w[co][ky][kx][ci] * in[f][y+oy+ky][x+ox+kx][ci])
+// Used for: forward of narrow layers (C_in = 1 first layers), dgrad (with the rotated
+// pack and oy = ox = -(k-1)), and everything in MPF_PREC_FP32 mode.
+constexpr int kTW = 16, kTH = 16, kCOT = 8, kCIC = 8;
+
+template <int IMG>
+__global__ void __launch_bounds__(256) conv_simt_kernel(ConvArgs a, int tiles_x) {
+  extern __shared__ float sm[];
+  const int k = a.k;
+  const int IW = kTW + k - 1, IH = kTH + k - 1;
+  float* s_in = sm;                      // [CIC][IH][IW]
+  float* s_w = sm + kCIC * IH * IW;      // [COT][k*k][CIC]
+  const int bx = blockIdx.x % tiles_x, cg = blockIdx.x / tiles_x;
+  const int co0 = cg * kCOT;
+  const int y0 = blockIdx.y * kTH, x0 = bx * kTW;
+  const long long f = blockIdx.z;
+  const int tx = threadIdx.x % kTW, ty = threadIdx.x / kTW;
+  float acc[kCOT];
+#pragma unroll
+  for (int o = 0; o < kCOT; ++o) acc[o] = 0.f;
+  const int cin = a.cin, cout = a.cout, kk = k * k;
+  for (int ci0 = 0; ci0 < cin; ci0 += kCIC) {
+    for (int e = threadIdx.x; e < IH * IW * kCIC; e += blockDim.x) {
+      const int c = e % kCIC, t = e / kCIC, ix = t % IW, iy = t / IW;
+      const int gy = y0 + a.off_y + iy, gx = x0 + a.off_x + ix, ci = ci0 + c;
+      float v = 0.f;
+      if (ci < cin && gy >= 0 && gy < a.in_vr && gx >= 0 && gx < a.in_vc) {
+        if (IMG)
+          v = a.in[((f * cin + ci) * a.in_gr + gy) * a.in_gc + gx];
+        else
+          v = a.in[((f * a.in_gr + gy) * a.in_gc + gx) * cin + ci];
+      }
+      s_in[(c * IH + iy) * IW + ix] = v;
+    }
+    for (int e = threadIdx.x; e < kCOT * kk * kCIC; e += blockDim.x) {
+      const int c = e % kCIC, t = e / kCIC, q = t % kk, o = t / kk;
+      const int co = co0 + o, ci = ci0 + c;
+      s_w[e] = (co < cout && ci < cin) ? a.w[((long long)co * kk + q) * cin + ci] : 0.f;
+    }
+    __syncthreads();
+    for (int ky = 0; ky < k; ++ky)
+      for (int kx = 0; kx < k; ++kx) {
+        const int q = ky * k + kx;
+#pragma unroll
+        for (int c = 0; c < kCIC; ++c) {
+          const float v = s_in[(c * IH + ty + ky) * IW + tx + kx];
+#pragma unroll
+          for (int o = 0; o < kCOT; ++o) acc[o] += v * s_w[(o * kk + q) * kCIC + c];
+        }
+      }
+    __syncthreads();
+  }
+  const int y = y0 + ty, x = x0 + tx;
+  if (y >= a.out_gr || x >= a.out_gc) return;
+  const bool valid = y < a.out_vr && x < a.out_vc;
+  if (!valid && !a.zero_pad) return;
+  const long long base = ((f * a.out_gr + y) * a.out_gc + x) * cout;
+#pragma unroll
+  for (int o = 0; o < kCOT; ++o) {
+    const int co = co0 + o;
+    if (co >= cout) break;
+    float v = 0.f;
+    if (valid) {
+      v = acc[o] + (a.bias ? a.bias[co] : 0.f);
+      v = act_fwd(a.act, v);
+      if (a.mul_dact) v *= act_der(a.dact, a.mul_dact[base + co]);
+      if (a.round_tf32) v = tf32_rna(v);
+    }
+    a.out[base + co] = v;
+  }
+}
+
+cudaError_t launch_conv_simt(const ConvArgs& a, cudaStream_t s) {
+  const int tiles_x = (a.out_gc + kTW - 1) / kTW;
+  const int groups = (a.cout + kCOT - 1) / kCOT;
+  dim3 grid(tiles_x * groups, (a.out_gr + kTH - 1) / kTH, a.n_frag_total);
+  const int IW = kTW + a.k - 1, IH = kTH + a.k - 1;
+  const size_t smem = sizeof(float) * (kCIC * IH * IW + kCOT * a.k * a.k * kCIC);
+  if (a.image_mode) {
+    cudaFuncSetAttribute(conv_simt_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    conv_simt_kernel<1><<<grid, 256, smem, s>>>(a, tiles_x);
+  } else {
+    cudaFuncSetAttribute(conv_simt_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    conv_simt_kernel<0><<<grid, 256, smem, s>>>(a, tiles_x);
+  }
+  return cudaGetLastError();
+}
+
+// ============================================================================ wgrad (SIMT)
+// part_w[s][co][(ky*k+kx)*cin+ci] = sum_{p in chunk s} dy[p][co] * x[p + (ky,kx)][ci]
+// part_b[s][co] = sum_{p in chunk s} dy[p][co]
+// Alg. 2: the sum over all fragments and positions is the K-reduction of this GEMM.
+constexpr int kWP = 32;  // positions per smem stage
+
+template <int IMG>
+__global__ void __launch_bounds__(256) wgrad_simt_kernel(WgradArgs a, long long chunk, int co_tiles,
+                                                          long long P_total) {
+  __shared__ float s_d[kWP][17];
+  __shared__ float s_x[kWP][17];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int cot = blockIdx.x % co_tiles, kt = blockIdx.x / co_tiles;
+  const int co = cot * 16 + ty;
+  const int K = a.k * a.k * a.cin;
+  const int kidx = kt * 16 + tx;
+  int ky = 0, kx = 0, ci = 0;
+  if (kidx < K) {
+    ci = kidx % a.cin;
+    const int q = kidx / a.cin;
+    ky = q / a.k;
+    kx = q % a.k;
+  }
+  const long long p0 = (long long)blockIdx.y * chunk;
+  const long long p1 = (P_total < p0 + chunk) ? P_total : p0 + chunk;
+  const long long per_frag = (long long)a.y_vr * a.y_vc;
+  float acc = 0.f, accb = 0.f;
+  for (long long pb = p0; pb < p1; pb += kWP) {
+    // stage deltas [kWP][16 co] and shifted inputs [kWP][16 K]
+    for (int e = threadIdx.x; e < kWP * 16; e += 256) {
+      const int j = e / 16, c = e % 16;
+      const long long p = pb + j;
+      float dv = 0.f, xv = 0.f;
+      if (p < p1) {
+        const long long f = p / per_frag;
+        const int r = (int)(p % per_frag);
+        const int y = r / a.y_vc, x = r % a.y_vc;
+        const int cc = cot * 16 + c;
+        if (cc < a.cout) dv = a.dy[((f * a.y_gr + y) * a.y_gc + x) * a.cout + cc];
+        const int kq = kt * 16 + c;
+        if (kq < K) {
+          const int ci2 = kq % a.cin, q2 = kq / a.cin;
+          const int yy = y + q2 / a.k, xx = x + q2 % a.k;
+          if (yy < a.x_vr && xx < a.x_vc) {
+            if (IMG)
+              xv = a.x[((f * a.cin + ci2) * a.x_gr + yy) * a.x_gc + xx];
+            else
+              xv = a.x[((f * a.x_gr + yy) * a.x_gc + xx) * a.cin + ci2];
+          }
+        }
+      }
+      s_d[j][c] = dv;
+      s_x[j][c] = xv;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int j = 0; j < kWP; ++j) {
+      const float d = s_d[j][ty];
+      acc += d * s_x[j][tx];
+      accb += d;
+    }
+    __syncthreads();
+  }
+  (void)ky; (void)kx; (void)ci;
+  if (co < a.cout && kidx < K) a.part_w[((long long)blockIdx.y * a.cout + co) * K + kidx] = acc;
+  if (kt == 0 && tx == 0 && co < a.cout) a.part_b[(long long)blockIdx.y * a.cout + co] = accb;
+}
+
+int wgrad_simt_splits(long long positions) {
+  long long s = (positions + 4095) / 4096;
+  if (s < 1) s = 1;
+  if (s > 256) s = 256;
+  return (int)s;
+}
+
+cudaError_t launch_wgrad_simt(const WgradArgs& a, cudaStream_t s) {
+  const long long P_total = (long long)a.n_frag_total * a.y_vr * a.y_vc;
+  const int K = a.k * a.k * a.cin;
+  const int co_tiles = (a.cout + 15) / 16, k_tiles = (K + 15) / 16;
+  const long long chunk = (P_total + a.n_split - 1) / a.n_split;
+  dim3 grid(co_tiles * k_tiles, a.n_split);
+  if (a.image_mode)
+    wgrad_simt_kernel<1><<<grid, 256, 0, s>>>(a, chunk, co_tiles, P_total);
+  else
+    wgrad_simt_kernel<0><<<grid, 256, 0, s>>>(a, chunk, co_tiles, P_total);
+  return cudaGetLastError();
+}
+
+__global__ void wgrad_reduce_kernel(const float* __restrict__ pw, const float* __restrict__ pb, int n_split,
+                                    int cout, int cin, int k, float* gw, float* gb) {
+  const int K = k * k * cin;
+  const long long total = (long long)cout * K + cout;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    if (e < (long long)cout * K) {
+      const int co = (int)(e / K), kidx = (int)(e % K);
+      float s = 0.f;
+      for (int i = 0; i < n_split; ++i) s += pw[((long long)i * cout + co) * K + kidx];  // fixed order
+      const int ci = kidx % cin, q = kidx / cin;
+      const int ky = q / k, kx = q % k;
+      gw[(((long long)co * cin + ci) * k + ky) * k + kx] += s;
+    } else {
+      const int co = (int)(e - (long long)cout * K);
+      float s = 0.f;
+      for (int i = 0; i < n_split; ++i) s += pb[(long long)i * cout + co];
+      gb[co] += s;
+    }
+  }
+}
+
+cudaError_t launch_wgrad_reduce(const float* pw, const float* pb, int n_split, int cout, int cin, int k,
+                                float* gw, float* gb, cudaStream_t s) {
+  const long long total = (long long)cout * k * k * cin + cout;
+  int blocks = (int)mpf_min_ll((total + 255) / 256, 4096);
+  wgrad_reduce_kernel<<<blocks, 256, 0, s>>>(pw, pb, n_split, cout, cin, k, gw, gb);
+  return cudaGetLastError();
+}
+
+// ============================================================================ MPF forward
+// Alg. 3: input fragment g, offset (r,c) (row-major, R2) ->
+// output fragment g*k^2 + r*k + c; cell (i,j) = max of the k x k block with top-left
+// (r + k i, c + k j) in the fragment; argmax = first maximum in row-major scan (R6).
+template <int V>
+__global__ void mpf_fwd_kernel(MpfArgs a, long long total) {
+  const int k = a.k, kk = k * k;
+  const int CV = a.C / V;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int cv = (int)(e % CV);
+    long long t = e / CV;
+    const int j = (int)(t % a.m_c);
+    t /= a.m_c;
+    const int i = (int)(t % a.m_r);
+    const long long go = t / a.m_r;     // output fragment
+    const long long g = go / kk;        // source fragment (findSourceFragment)
+    const int rc = (int)(go % kk), r = rc / k, c = rc % k;
+    const int y0 = r + k * i, x0 = c + k * j;
+    const float* src = a.y + ((g * a.gr + y0) * a.gc + x0) * a.C + cv * V;
+    float best[V];
+    uint8_t arg[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) { best[v] = src[v]; arg[v] = 0; }
+    for (int dy = 0; dy < k; ++dy)
+      for (int dx = 0; dx < k; ++dx) {
+        if (dy == 0 && dx == 0) continue;
+        const float* p = src + ((long long)dy * a.gc + dx) * a.C;
+        float val[V];
+        if constexpr (V == 4) {
+          const float4 q = *reinterpret_cast<const float4*>(p);
+          val[0] = q.x; val[1] = q.y; val[2] = q.z; val[3] = q.w;
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v) val[v] = p[v];
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+          if (val[v] > best[v]) { best[v] = val[v]; arg[v] = (uint8_t)(dy * k + dx); }
+      }
+    const long long o = e * V;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      a.out[o + v] = a.round_tf32 ? tf32_rna(best[v]) : best[v];
+      a.idx[o + v] = arg[v];
+    }
+  }
+}
+
+cudaError_t launch_mpf_fwd(const MpfArgs& a, cudaStream_t s) {
+  const bool vec = (a.C % 4) == 0;
+  const long long total = (long long)a.n_frag_in * a.k * a.k * a.m_r * a.m_c * (a.C / (vec ? 4 : 1));
+  const int blocks = (int)mpf_min_ll((total + 255) / 256, 148LL * 64);
+  if (vec)
+    mpf_fwd_kernel<4><<<blocks, 256, 0, s>>>(a, total);
+  else
+    mpf_fwd_kernel<1><<<blocks, 256, 0, s>>>(a, total);
+  return cudaGetLastError();
+}
+
+// ============================================================================ MPF backward
+// Alg. 4 as a deterministic gather: every element p of the conv
+// output sums, in fixed (dy,dx) order, the deltas of all pooled cells whose recorded
+// argmax is p — an element that is the maximum for several offsets receives the SUM
+// (Fig. 2).  Times act'(y_p), with y_p = the pooled value of any
+// cell that selected p (that cell's value IS y_p).  Zero outside the valid region.
+template <int V>
+__global__ void mpf_bwd_kernel(MpfBwdArgs a, long long total) {
+  const int k = a.k, kk = k * k;
+  const int CV = a.C / V;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int cv = (int)(e % CV);
+    long long t = e / CV;
+    const int x = (int)(t % a.gc);
+    t /= a.gc;
+    const int y = (int)(t % a.gr);
+    const long long g = t / a.gr;
+    float acc[V], val[V];
+    bool hit[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) { acc[v] = 0.f; val[v] = 0.f; hit[v] = false; }
+    if (y < a.vr && x < a.vc) {
+      for (int dy = 0; dy < k; ++dy) {
+        const int ty = y - dy;
+        if (ty < 0) break;
+        const int r = ty % k, i = ty / k;
+        if (i >= a.m_r) continue;
+        for (int dx = 0; dx < k; ++dx) {
+          const int tx = x - dx;
+          if (tx < 0) break;
+          const int c = tx % k, j = tx / k;
+          if (j >= a.m_c) continue;
+          const long long cell = (((g * kk + r * k + c) * a.m_r + i) * a.m_c + j) * a.C + cv * V;
+          const uint8_t want = (uint8_t)(dy * k + dx);
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            if (a.idx[cell + v] == want) {
+              acc[v] += a.dout[cell + v];
+              val[v] = a.pooled[cell + v];
+              hit[v] = true;
+            }
+          }
+        }
+      }
+    }
+    const long long o = e * V;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      float d = hit[v] ? acc[v] * act_der(a.act, val[v]) : 0.f;
+      if (a.round_tf32) d = tf32_rna(d);
+      a.din[o + v] = d;
+    }
+  }
+}
+
+cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s) {
+  const bool vec = (a.C % 4) == 0;
+  const long long total = (long long)a.n_frag_in * a.gr * a.gc * (a.C / (vec ? 4 : 1));
+  const int blocks = (int)mpf_min_ll((total + 255) / 256, 148LL * 64);
+  if (vec)
+    mpf_bwd_kernel<4><<<blocks, 256, 0, s>>>(a, total);
+  else
+    mpf_bwd_kernel<1><<<blocks, 256, 0, s>>>(a, total);
+  return cudaGetLastError();
+}
+
+// ============================================================================ head
+// Last FC (1x1, linear) + per-pixel softmax + class-weighted MCCE (
+// R8: per-image mean over labelled pixels) + dL/dlogits = w_t (p - onehot)/n_lab +
+// dh = (W^T dlogits) * act'(h).  Labels are fetched through the fragment -> pixel map
+// (mixed radix, R2/R7); positions outside the O_H x O_W output grid are ignored.
+constexpr int kHeadThreads = 256;
+
+__global__ void __launch_bounds__(kHeadThreads) head_kernel(HeadArgs a, int parts) {
+  extern __shared__ float s_w[];  // [C][Ch] then b[C]
+  __shared__ float s_red[kHeadThreads / 32];
+  const int C = a.C, Ch = a.Ch;
+  for (int e = threadIdx.x; e < C * Ch; e += blockDim.x) s_w[e] = a.w[e];
+  for (int e = threadIdx.x; e < C; e += blockDim.x) s_w[C * Ch + e] = a.b[e];
+  __syncthreads();
+  const int img = blockIdx.y;
+  const long long per_img = (long long)a.F * a.gr * a.gc;
+  const long long pos = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  float lossv = 0.f;
+  if (pos < per_img) {
+    const int gl = (int)(pos / ((long long)a.gr * a.gc));
+    const int rem = (int)(pos % ((long long)a.gr * a.gc));
+    const int i = rem / a.gc, j = rem % a.gc;
+    const long long g = (long long)img * a.F + gl;
+    const long long hb = ((g * a.gr + i) * a.gc + j);
+    const bool valid = i < a.vr && j < a.vc;
+    if (valid) {
+      const float* h = a.h + hb * Ch;
+      float z[16];
+      for (int c = 0; c < C; ++c) z[c] = s_w[C * Ch + c];
+      for (int ch = 0; ch < Ch; ++ch) {
+        const float hv = h[ch];
+        for (int c = 0; c < C; ++c) z[c] += s_w[c * Ch + ch] * hv;
+      }
+      float mx = z[0];
+      for (int c = 1; c < C; ++c) mx = fmaxf(mx, z[c]);
+      float se = 0.f;
+      for (int c = 0; c < C; ++c) se += expf(z[c] - mx);
+      const float lse = mx + logf(se);
+      float p[16];
+      for (int c = 0; c < C; ++c) p[c] = expf(z[c] - lse);
+      if (a.probs) {
+        const long long pb = ((g * a.vr + i) * a.vc + j) * C;
+        for (int c = 0; c < C; ++c) a.probs[pb + c] = p[c];
+      }
+      if (a.dlogits) {
+        // label through the fragment -> pixel map: y = r1 + k1 (r2 + k2 (... + kL i))
+        int yy = i, xx = j, rem_f = gl;
+        for (int l = a.n_levels - 1; l >= 0; --l) {
+          const int kq = a.pool_k[l];
+          const int d = rem_f % (kq * kq);
+          rem_f /= kq * kq;
+          yy = d / kq + kq * yy;
+          xx = d % kq + kq * xx;
+        }
+        int t = 255;
+        if (a.labels && yy < a.O_H && xx < a.O_W) t = a.labels[((long long)img * a.O_H + yy) * a.O_W + xx];
+        float dl[16];
+        for (int c = 0; c < C; ++c) dl[c] = 0.f;
+        if (t != 255 && t >= C) atomicOr(a.err, 1);
+        const int nl = a.nlab[img];
+        if (t < C && nl > 0) {
+          const float wt = a.cw[t];
+          lossv = -wt * (z[t] - lse);
+          const float inv = 1.f / (float)nl;
+          for (int c = 0; c < C; ++c) dl[c] = wt * (p[c] - (c == t ? 1.f : 0.f)) * inv;
+        }
+        float* dlo = a.dlogits + hb * C;
+        for (int c = 0; c < C; ++c) dlo[c] = a.round_tf32 ? tf32_rna(dl[c]) : dl[c];
+        float* dh = a.dh + hb * Ch;
+        for (int ch = 0; ch < Ch; ++ch) {
+          float s = 0.f;
+          for (int c = 0; c < C; ++c) s += s_w[c * Ch + ch] * dl[c];
+          s *= act_der(a.hidden_act, h[ch]);
+          dh[ch] = a.round_tf32 ? tf32_rna(s) : s;
+        }
+      }
+    } else if (a.dlogits) {
+      for (int c = 0; c < C; ++c) a.dlogits[hb * C + c] = 0.f;
+      for (int ch = 0; ch < Ch; ++ch) a.dh[hb * Ch + ch] = 0.f;
+    }
+  }
+  // fixed-order block reduction of the loss
+  float v = lossv;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int w = 0; w < kHeadThreads / 32; ++w) s += s_red[w];
+    if (a.loss_part) a.loss_part[(long long)img * parts + blockIdx.x] = s;
+  }
+}
+
+cudaError_t launch_head(const HeadArgs& a, int* parts_out, cudaStream_t s) {
+  const long long per_img = (long long)a.F * a.gr * a.gc;
+  const int parts = (int)((per_img + kHeadThreads - 1) / kHeadThreads);
+  if (parts_out) *parts_out = parts;
+  dim3 grid(parts, a.n);
+  const size_t smem = sizeof(float) * (a.C * a.Ch + a.C);
+  cudaFuncSetAttribute(head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  head_kernel<<<grid, kHeadThreads, smem, s>>>(a, parts);
+  return cudaGetLastError();
+}
+
+// ============================================================================ small kernels
+__global__ void label_count_kernel(const uint8_t* __restrict__ labels, int hw, int classes, int* nlab) {
+  __shared__ int s_red[32];
+  const int img = blockIdx.x;
+  int c = 0;
+  for (int e = threadIdx.x; e < hw; e += blockDim.x) c += labels[(long long)img * hw + e] < classes;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) s += s_red[w];
+    nlab[img] = s;
+  }
+}
+
+cudaError_t launch_label_count(const uint8_t* labels, int n, int hw, int classes, int* nlab, cudaStream_t s) {
+  label_count_kernel<<<n, 1024, 0, s>>>(labels, hw, classes, nlab);
+  return cudaGetLastError();
+}
+
+__global__ void loss_finalize_kernel(const float* __restrict__ part, int parts, const int* __restrict__ nlab,
+                                     int n, float* loss) {
+  const int img = blockIdx.x * blockDim.x + threadIdx.x;
+  if (img >= n) return;
+  float s = 0.f;
+  for (int i = 0; i < parts; ++i) s += part[(long long)img * parts + i];
+  loss[img] = nlab[img] > 0 ? s / (float)nlab[img] : 0.f;
+}
+
+cudaError_t launch_loss_finalize(const float* part, int parts, const int* nlab, int n, float* loss,
+                                 cudaStream_t s) {
+  loss_finalize_kernel<<<(n + 127) / 128, 128, 0, s>>>(part, parts, nlab, n, loss);
+  return cudaGetLastError();
+}
+
+__global__ void sgd_kernel(float* __restrict__ p, float* __restrict__ g, long long n, float step) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    p[e] -= step * g[e];
+    g[e] = 0.f;
+  }
+}
+
+cudaError_t launch_sgd(float* params, float* grads, long long n, float lr, float scale, cudaStream_t s) {
+  const int blocks = (int)mpf_min_ll((n + 255) / 256, 1024);
+  sgd_kernel<<<blocks, 256, 0, s>>>(params, grads, n, lr * scale);
+  return cudaGetLastError();
+}
+
+// canonical W[co][ci][ky][kx] -> fwd pack [co][ky][kx][ci], dgrad pack [ci][k-1-ky][k-1-kx][co]
+__global__ void pack_kernel(const float* __restrict__ w, int cout, int cin, int k, float* wp, float* dp,
+                            int round_tf32) {
+  const long long n = (long long)cout * cin * k * k;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int kx = (int)(e % k);
+    long long t = e / k;
+    const int ky = (int)(t % k);
+    t /= k;
+    const int ci = (int)(t % cin);
+    const int co = (int)(t / cin);
+    float v = w[e];
+    if (round_tf32) v = tf32_rna(v);
+    wp[(((long long)co * k + ky) * k + kx) * cin + ci] = v;
+    if (dp) dp[(((long long)ci * k + (k - 1 - ky)) * k + (k - 1 - kx)) * cout + co] = v;
+  }
+}
+
+cudaError_t launch_pack_weights(const float* w, int cout, int cin, int k, float* wp, float* dp, int round_tf32,
+                                cudaStream_t s) {
+  const long long n = (long long)cout * cin * k * k;
+  const int blocks = (int)mpf_min_ll((n + 255) / 256, 1024);
+  pack_kernel<<<blocks, 256, 0, s>>>(w, cout, cin, k, wp, dp, round_tf32);
+  return cudaGetLastError();
+}
+
+// Defragmentation: pix[n][c][y][x] = frag[n*F + f(y,x)][i(y)][j(x)][c]
+struct Frag2PixArgs {
+  const float* frag;
+  float* pix;
+  int n, C, F, fr, fc, O_H, O_W, L;
+  int k[kMaxL];
+};
+
+__global__ void frag2pix_kernel(Frag2PixArgs a, long long total) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(e % a.O_W);
+    long long t = e / a.O_W;
+    const int y = (int)(t % a.O_H);
+    t /= a.O_H;
+    const int c = (int)(t % a.C);
+    const long long img = t / a.C;
+    int yy = y, xx = x, g = 0;
+    for (int l = 0; l < a.L; ++l) {  // level 1 is the most significant digit (R2)
+      const int kq = a.k[l];
+      const int r = yy % kq, cc = xx % kq;
+      yy /= kq;
+      xx /= kq;
+      g = g * kq * kq + r * kq + cc;
+    }
+    a.pix[e] = a.frag[(((img * a.F + g) * a.fr + yy) * a.fc + xx) * a.C + c];
+  }
+}
+
+cudaError_t launch_frag2pix(const float* frag, float* pix, int n, int C, int F, int fr, int fc, int O_H, int O_W,
+                            int n_levels, const int* pool_k, cudaStream_t s) {
+  Frag2PixArgs a;
+  a.frag = frag; a.pix = pix; a.n = n; a.C = C; a.F = F; a.fr = fr; a.fc = fc; a.O_H = O_H; a.O_W = O_W;
+  a.L = n_levels;
+  for (int l = 0; l < n_levels; ++l) a.k[l] = pool_k[l];
+  const long long total = (long long)n * C * O_H * O_W;
+  if (total == 0) return cudaSuccess;
+  const int blocks = (int)mpf_min_ll((total + 255) / 256, 148LL * 32);
+  frag2pix_kernel<<<blocks, 256, 0, s>>>(a, total);
+  return cudaGetLastError();
+}
+
+__global__ void compact_kernel(const float* __restrict__ src, int gr, int gc, int vr, int vc, int C,
+                               long long total, float* dst) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e % C);
+    long long t = e / C;
+    const int x = (int)(t % vc);
+    t /= vc;
+    const int y = (int)(t % vr);
+    const long long f = t / vr;
+    dst[e] = src[((f * gr + y) * gc + x) * C + c];
+  }
+}
+
+cudaError_t launch_compact_copy(const float* src, int gr, int gc, int vr, int vc, int C, long long nf,
+                                float* dst, cudaStream_t s) {
+  const long long total = nf * vr * vc * C;
+  if (total == 0) return cudaSuccess;
+  const int blocks = (int)mpf_min_ll((total + 255) / 256, 148LL * 32);
+  compact_kernel<<<blocks, 256, 0, s>>>(src, gr, gc, vr, vc, C, total, dst);
+  return cudaGetLastError();
+}
+
+}  // namespace mpf

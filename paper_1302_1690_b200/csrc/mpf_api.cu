@@ -1,0 +1,721 @@
+// mpf_api.cu — host side of libmpf: the C ABI declared in include/mpf.h.
+//
+// Geometry planning (validate_arch + plan_geometry, SPEC.md:241-258 with valid
+// outputs), memory plan, and the per-step launch sequence:
+//   forward  (Alg. 1 per layer, Alg. 3 for MPF)
+//   loss     (MCCE per pixel, dL/dx_hat first)
+//   backward (Alg. 4 for MPF, Alg. 2 accumulation)
+//   SGD
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+
+#include "conv_tc.h"
+#include "mpf_internal.h"
+
+namespace mpf {
+
+static thread_local std::string g_err = "no error";
+void set_error(const std::string& m) { g_err = m; }
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+#define MPF_CUDA(call)                                                                  \
+  do {                                                                                  \
+    cudaError_t _e = (call);                                                            \
+    if (_e != cudaSuccess) {                                                            \
+      set_error(std::string(#call) + ": " + cudaGetErrorString(_e));                    \
+      return MPF_ERR_CUDA;                                                              \
+    }                                                                                   \
+  } while (0)
+
+static mpf_status fail(mpf_status s, const std::string& m) {
+  set_error(m);
+  return s;
+}
+
+// ------------------------------------------------------------------ live kernel timing
+static int prof_mark(Net* N, cudaStream_t s) {
+  Prof& P = N->prof;
+  if (!P.on || P.used + 2 > (int)P.ev.size()) return -1;
+  cudaEventRecord(P.ev[P.used], s);
+  return P.used++;
+}
+static void prof_rec(Net* N, cudaStream_t s, int e0, const char* name, int layer, double flops, double bytes) {
+  Prof& P = N->prof;
+  if (e0 < 0) return;
+  cudaEventRecord(P.ev[P.used], s);
+  P.recs.push_back(ProfRec{name, layer, flops, bytes, e0, P.used});
+  P.used++;
+}
+// every kernel launch of the path goes through LAUNCH (timed when profiling is on)
+#define LAUNCH(N, s, name, layer, flops, bytes, call)            \
+  do {                                                           \
+    const int _e0 = prof_mark((N), (s));                         \
+    MPF_CUDA(call);                                              \
+    prof_rec((N), (s), _e0, (name), (layer), (flops), (bytes));  \
+  } while (0)
+
+// ------------------------------------------------------------------ geometry plan
+static mpf_status plan(Net* N) {
+  const mpf_config& c = N->cfg;
+  const int nl = N->n_layers;
+  if (nl < 2 || nl > kMaxL) return fail(MPF_ERR_CONFIG, "n_layers must be in [2, MPF_MAX_LAYERS]");
+  if (c.in_channels < 1 || c.patch < 1 || c.max_images < 1)
+    return fail(MPF_ERR_CONFIG, "in_channels, patch and max_images must be >= 1");
+  if (c.image_rows < c.patch || c.image_cols < c.patch)
+    return fail(MPF_ERR_CONFIG, "image smaller than the patch");
+  // patch-mode shape chain: exact divisibility, FC sees the whole remaining volume
+  int sz = c.patch, ch = c.in_channels;
+  long long off = 0;
+  N->n_levels = 0;
+  N->S = 1;
+  for (int l = 0; l < nl; ++l) {
+    const mpf_layer& L = N->lp[l].L;
+    LayerPlan& P = N->lp[l];
+    if (L.k < 1) return fail(MPF_ERR_CONFIG, "layer " + std::to_string(l) + ": k < 1");
+    if (L.kind == MPF_POOL) {
+      if (sz % L.k) return fail(MPF_ERR_CONFIG, "layer " + std::to_string(l) + ": pooling does not divide the patch-mode size");
+      if (L.k > 15) return fail(MPF_ERR_CONFIG, "pool factor > 15");
+      sz /= L.k;
+      P.cin = P.cout = ch;
+      N->pool_k[N->n_levels++] = L.k;
+      N->S *= L.k;
+    } else if (L.kind == MPF_CONV || L.kind == MPF_FC) {
+      if (L.n_out < 1 || L.k > sz) return fail(MPF_ERR_CONFIG, "layer " + std::to_string(l) + ": bad kernel/maps");
+      if (L.kind == MPF_FC && L.k != sz)
+        return fail(MPF_ERR_CONFIG, "layer " + std::to_string(l) + ": FC kernel must equal the remaining spatial size");
+      if (L.act != MPF_TANH && L.act != MPF_IDENTITY && L.act != MPF_LOGISTIC)
+        return fail(MPF_ERR_CONFIG, "unknown activation");
+      P.cin = ch;
+      P.cout = L.n_out;
+      P.w_off = off;
+      off += (long long)L.n_out * ch * L.k * L.k;
+      P.b_off = off;
+      off += L.n_out;
+      ch = L.n_out;
+      sz = sz - L.k + 1;
+    } else {
+      return fail(MPF_ERR_CONFIG, "unknown layer kind");
+    }
+  }
+  if (sz != 1) return fail(MPF_ERR_CONFIG, "the layer list does not reduce the patch to 1x1");
+  const mpf_layer& last = N->lp[nl - 1].L;
+  if (last.kind != MPF_FC || last.k != 1 || last.act != MPF_IDENTITY)
+    return fail(MPF_ERR_CONFIG, "the last layer must be a 1x1 FC with identity activation (softmax head)");
+  const mpf_layer& prev = N->lp[nl - 2].L;
+  if (prev.kind == MPF_POOL) return fail(MPF_ERR_CONFIG, "the layer before the softmax FC must be CONV/FC");
+  if (last.n_out > 16 || last.n_out < 2) return fail(MPF_ERR_CONFIG, "2..16 classes supported");
+  N->classes = last.n_out;
+  N->n_params = off;
+  // dense geometry: valid outputs O = H - P + 1, padded so every fragment has equal size
+  N->O_H = c.image_rows - c.patch + 1;
+  N->O_W = c.image_cols - c.patch + 1;
+  const int fr = (N->O_H + N->S - 1) / N->S, fc = (N->O_W + N->S - 1) / N->S;
+  int r = fr, q = fc;
+  for (int l = nl - 1; l >= 0; --l) {
+    const mpf_layer& L = N->lp[l].L;
+    if (L.kind == MPF_POOL) { r = r * L.k + L.k - 1; q = q * L.k + L.k - 1; }
+    else { r += L.k - 1; q += L.k - 1; }
+  }
+  N->Hp = r;
+  N->Wp = q;
+  // forward chain of activations
+  Act a0;
+  a0.F = 1; a0.vr = a0.gr = N->Hp; a0.vc = a0.gc = N->Wp; a0.C = c.in_channels;
+  N->a[0] = a0;
+  for (int l = 0; l < nl; ++l) {
+    const mpf_layer& L = N->lp[l].L;
+    const Act& in = N->a[l];
+    Act o;
+    if (L.kind == MPF_POOL) {
+      const int nr = in.vr - L.k + 1, nc = in.vc - L.k + 1;
+      if (nr % L.k || nc % L.k) return fail(MPF_ERR_INTERNAL, "non-uniform fragments (planner bug)");
+      o.F = in.F * L.k * L.k; o.vr = o.gr = nr / L.k; o.vc = o.gc = nc / L.k; o.C = in.C;
+    } else {
+      o.F = in.F; o.vr = in.vr - L.k + 1; o.vc = in.vc - L.k + 1; o.gr = in.gr; o.gc = in.gc; o.C = L.n_out;
+    }
+    if (o.vr < 1 || o.vc < 1) return fail(MPF_ERR_INTERNAL, "empty activation (planner bug)");
+    N->a[l + 1] = o;
+  }
+  if (N->a[nl].vr != fr || N->a[nl].vc != fc) return fail(MPF_ERR_INTERNAL, "output grid mismatch (planner bug)");
+  // where every layer output lives
+  for (int l = 0; l < nl; ++l) {
+    const mpf_layer& L = N->lp[l].L;
+    if (l == nl - 1) N->lp[l].out_where = Where::None;                 // logits: fused in the head
+    else if (L.kind == MPF_POOL) N->lp[l].out_where = Where::Tape;     // pooled values + argmax
+    else if (N->lp[l + 1].L.kind == MPF_POOL && !c.debug_keep) N->lp[l].out_where = Where::ScratchY;  // consumed by MPF
+    else N->lp[l].out_where = Where::Tape;                             // input of a CONV/FC + act'
+  }
+  return MPF_OK;
+}
+
+static void layout_memory(Net* N, int n) {
+  size_t tape = 0;
+  long long maxY = 0, maxD = 0;
+  for (int l = 0; l < N->n_layers; ++l) {
+    LayerPlan& P = N->lp[l];
+    const Act& o = N->a[l + 1];
+    const long long e = o.elems_per_image() * n;
+    P.tape_val_off = P.tape_idx_off = -1;
+    if (P.out_where == Where::Tape) {
+      P.tape_val_off = (long long)tape;
+      tape = align256(tape + sizeof(float) * e);
+      if (P.L.kind == MPF_POOL) {
+        P.tape_idx_off = (long long)tape;
+        tape = align256(tape + e);
+      }
+    } else if (P.out_where == Where::ScratchY) {
+      maxY = std::max(maxY, e);
+    }
+    if (l < N->n_layers - 1) maxD = std::max(maxD, e);
+  }
+  N->tape_bytes = std::max<size_t>(tape, 256);
+  size_t s = 0;
+  N->off_Y = s; s = align256(s + sizeof(float) * maxY);
+  N->off_dA = s; s = align256(s + sizeof(float) * maxD);
+  N->off_dB = s; s = align256(s + sizeof(float) * maxD);
+  N->off_dlog = s; s = align256(s + sizeof(float) * N->a[N->n_layers].elems_per_image() * n);
+  // weight packs
+  N->off_wpack = s;
+  long long wp = 0;
+  size_t max_part = 0;
+  for (int l = 0; l < N->n_layers; ++l) {
+    LayerPlan& P = N->lp[l];
+    if (P.L.kind == MPF_POOL) continue;
+    const long long nw = (long long)P.cout * P.cin * P.L.k * P.L.k;
+    P.wpack_off = wp; wp += (nw + 63) / 64 * 64;
+    P.dpack_off = wp; wp += (nw + 63) / 64 * 64;
+    max_part = std::max<size_t>(max_part, (size_t)(nw + P.cout));
+  }
+  s = align256(s + sizeof(float) * wp);
+  N->off_part = s;
+  N->part_floats = max_part * (size_t)kMaxSplits;
+  s = align256(s + sizeof(float) * N->part_floats);
+  N->off_nlab = s; s = align256(s + sizeof(int) * n);
+  // loss partials: head blocks per image
+  const Act& h = N->a[N->n_layers - 1];
+  N->loss_parts = (int)((h.elems_per_image() / h.C + 255) / 256);
+  N->off_lossp = s; s = align256(s + sizeof(float) * (size_t)N->loss_parts * n);
+  N->off_err = s; s = align256(s + 256);
+  N->off_stage_img = s; s = align256(s + sizeof(float) * (size_t)n * N->cfg.in_channels * N->cfg.image_rows * N->cfg.image_cols);
+  N->off_stage_lab = s; s = align256(s + (size_t)n * N->O_H * N->O_W);
+  N->off_stage_loss = s; s = align256(s + sizeof(float) * n);
+  N->scratch_bytes = s;
+  N->n_cap = n;
+}
+
+static float* tape_val(const Net* N, int l) { return (float*)(N->tape + N->lp[l].tape_val_off); }
+static uint8_t* tape_idx(const Net* N, int l) { return (uint8_t*)(N->tape + N->lp[l].tape_idx_off); }
+static float* scr(const Net* N, size_t off) { return (float*)(N->scratch + off); }
+
+// pointer to activation a[l] (l >= 1) as produced in the last forward
+static const float* act_ptr(const Net* N, int l) {
+  const LayerPlan& P = N->lp[l - 1];
+  if (P.out_where == Where::Tape) return tape_val(N, l - 1);
+  if (P.out_where == Where::ScratchY) return scr(N, N->off_Y);
+  return nullptr;
+}
+
+static bool use_tc(const Net* N, const LayerPlan& P, bool dgrad) {
+  if (N->cfg.precision != MPF_PREC_TF32) return false;
+  return tc_supported(dgrad ? P.cout : P.cin, dgrad ? P.cin : P.cout, P.L.k);
+}
+
+}  // namespace mpf
+
+using namespace mpf;
+
+extern "C" {
+
+int32_t mpf_version(void) { return MPF_VERSION; }
+const char* mpf_last_error(void) { return g_err.c_str(); }
+
+mpf_status mpf_net_create(const mpf_config* cfg, const mpf_layer* layers, int32_t n_layers, mpf_net** out) {
+  if (!cfg || !layers || !out) return fail(MPF_ERR_ARG, "NULL argument");
+  *out = nullptr;
+  if (n_layers < 2 || n_layers > kMaxL) return fail(MPF_ERR_CONFIG, "n_layers out of range");
+  mpf_net* N = new mpf_net();
+  N->cfg = *cfg;
+  N->n_layers = n_layers;
+  for (int l = 0; l < n_layers; ++l) N->lp[l].L = layers[l];
+  mpf_status st = plan(N);
+  if (st != MPF_OK) {
+    delete N;
+    return st;
+  }
+  layout_memory(N, cfg->max_images);
+  *out = N;
+  return MPF_OK;
+}
+
+void mpf_net_destroy(mpf_net* net) {
+  if (!net) return;
+  for (cudaEvent_t e : net->prof.ev) cudaEventDestroy(e);
+  delete net;
+}
+
+mpf_status mpf_profile_begin(mpf_net* N, int32_t max_launches) {
+  if (!N || max_launches < 1) return fail(MPF_ERR_ARG, "bad argument");
+  Prof& P = N->prof;
+  const int need = 2 * max_launches;
+  while ((int)P.ev.size() < need) {
+    cudaEvent_t e;
+    MPF_CUDA(cudaEventCreate(&e));
+    P.ev.push_back(e);
+  }
+  P.used = 0;
+  P.recs.clear();
+  P.on = true;
+  return MPF_OK;
+}
+
+mpf_status mpf_profile_end(mpf_net* N, mpf_kernel_stat* out, int32_t cap, int32_t* n_out) {
+  if (!N) return fail(MPF_ERR_ARG, "NULL net");
+  Prof& P = N->prof;
+  P.on = false;
+  std::vector<mpf_kernel_stat> agg;
+  for (const ProfRec& r : P.recs) {
+    MPF_CUDA(cudaEventSynchronize(P.ev[r.e1]));
+    float ms = 0.f;
+    MPF_CUDA(cudaEventElapsedTime(&ms, P.ev[r.e0], P.ev[r.e1]));
+    mpf_kernel_stat* hit = nullptr;
+    for (auto& a : agg)
+      if (a.layer == r.layer && strncmp(a.name, r.name.c_str(), sizeof(a.name)) == 0) hit = &a;
+    if (!hit) {
+      mpf_kernel_stat z;
+      memset(&z, 0, sizeof(z));
+      strncpy(z.name, r.name.c_str(), sizeof(z.name) - 1);
+      z.layer = r.layer;
+      z.flops = r.flops;
+      z.bytes = r.bytes;
+      agg.push_back(z);
+      hit = &agg.back();
+    }
+    hit->launches += 1;
+    hit->total_ms += ms;
+  }
+  if (n_out) *n_out = (int32_t)agg.size();
+  if (out)
+    for (int i = 0; i < (int)agg.size() && i < cap; ++i) out[i] = agg[i];
+  P.recs.clear();
+  P.used = 0;
+  return MPF_OK;
+}
+
+mpf_status mpf_net_geometry(const mpf_net* N, mpf_geometry* g) {
+  if (!N || !g) return fail(MPF_ERR_ARG, "NULL argument");
+  memset(g, 0, sizeof(*g));
+  g->n_layers = N->n_layers;
+  g->n_levels = N->n_levels;
+  g->classes = N->classes;
+  g->stride = N->S;
+  g->n_fragments = N->a[N->n_layers].F;
+  g->out_rows = N->O_H;
+  g->out_cols = N->O_W;
+  g->padded_rows = N->Hp;
+  g->padded_cols = N->Wp;
+  g->frag_rows = N->a[N->n_layers].vr;
+  g->frag_cols = N->a[N->n_layers].vc;
+  g->n_params = N->n_params;
+  for (int l = 0; l <= N->n_layers; ++l) {
+    g->frag[l] = N->a[l].F;
+    g->rows[l] = N->a[l].vr;
+    g->cols[l] = N->a[l].vc;
+    g->chans[l] = N->a[l].C;
+  }
+  for (int l = 0; l < N->n_layers; ++l) {
+    g->w_offset[l] = N->lp[l].w_off;
+    g->b_offset[l] = N->lp[l].b_off;
+  }
+  return MPF_OK;
+}
+
+mpf_status mpf_net_memory(const mpf_net* N, int32_t n, uint64_t* pb, uint64_t* gb, uint64_t* tb, uint64_t* sb) {
+  if (!N) return fail(MPF_ERR_ARG, "NULL net");
+  if (n < 1 || n > N->cfg.max_images) return fail(MPF_ERR_ARG, "n_images must be in [1, max_images]");
+  Net tmp = *N;
+  layout_memory(&tmp, n);
+  if (pb) *pb = sizeof(float) * (uint64_t)N->n_params;
+  if (gb) *gb = sizeof(float) * (uint64_t)N->n_params;
+  if (tb) *tb = tmp.tape_bytes;
+  if (sb) *sb = tmp.scratch_bytes;
+  return MPF_OK;
+}
+
+mpf_status mpf_net_bind(mpf_net* N, void* p, void* g, void* t, void* s, int32_t n) {
+  if (!N || !p || !g || !t || !s) return fail(MPF_ERR_ARG, "NULL buffer");
+  if (n < 1 || n > N->cfg.max_images) return fail(MPF_ERR_ARG, "n_images must be in [1, max_images]");
+  if (((uintptr_t)t | (uintptr_t)s) & 255) return fail(MPF_ERR_ARG, "tape/scratch must be 256-byte aligned");
+  if (((uintptr_t)p | (uintptr_t)g) & 15) return fail(MPF_ERR_ARG, "params/grads must be 16-byte aligned");
+  layout_memory(N, n);
+  N->params = (float*)p;
+  N->grads = (float*)g;
+  N->tape = (char*)t;
+  N->scratch = (char*)s;
+  N->bound = true;
+  N->have_fwd = false;
+  MPF_CUDA(cudaMemset(N->scratch + N->off_err, 0, 256));
+  return MPF_OK;
+}
+
+mpf_status mpf_forward_image(mpf_net* N, const float* d_images, int32_t n, float* d_probs, void* stream) {
+  if (!N || !d_images) return fail(MPF_ERR_ARG, "NULL argument");
+  if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound (mpf_net_bind)");
+  if (n < 1 || n > N->n_cap) return fail(MPF_ERR_DATA, "n must be in [1, bound n_images]");
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool tf32 = N->cfg.precision == MPF_PREC_TF32;
+  float* wpack = scr(N, N->off_wpack);
+  // 1. weight packs (tf32-rounded for the tensor-core path)
+  for (int l = 0; l < N->n_layers; ++l) {
+    const LayerPlan& P = N->lp[l];
+    if (P.L.kind == MPF_POOL) continue;
+    const double nw = (double)P.cout * P.cin * P.L.k * P.L.k;
+    LAUNCH(N, s, "pack_weights", l, 0.0, 12.0 * nw,
+           launch_pack_weights(N->params + P.w_off, P.cout, P.cin, P.L.k, wpack + P.wpack_off,
+                               wpack + P.dpack_off, tf32 ? 1 : 0, s));
+  }
+  // 2. layers (Alg. 1; Alg. 3 for MPF)
+  for (int l = 0; l < N->n_layers - 1; ++l) {
+    const LayerPlan& P = N->lp[l];
+    const Act& in = N->a[l];
+    const Act& o = N->a[l + 1];
+    // the consumer of this output rounds? (TF32 operand of a tensor-core conv)
+    const bool next_tc = (l + 1 < N->n_layers - 1) && N->lp[l + 1].L.kind != MPF_POOL && use_tc(N, N->lp[l + 1], false);
+    if (P.L.kind == MPF_POOL) {
+      const Act& y = in;
+      MpfArgs m;
+      m.y = act_ptr(N, l);
+      m.gr = y.gr; m.gc = y.gc; m.vr = y.vr; m.vc = y.vc; m.C = y.C; m.k = P.L.k;
+      m.n_frag_in = n * y.F;
+      m.out = tape_val(N, l);
+      m.idx = tape_idx(N, l);
+      m.m_r = o.vr; m.m_c = o.vc;
+      m.round_tf32 = (l + 1 < N->n_layers - 1 && use_tc(N, N->lp[l + 1], false)) ? 1 : 0;
+      const double ein = (double)n * y.F * y.vr * y.vc * y.C, eout = (double)n * o.F * o.vr * o.vc * o.C;
+      LAUNCH(N, s, "mpf_fwd", l, 0.0, 4.0 * ein + 5.0 * eout, launch_mpf_fwd(m, s));
+    } else {
+      float* out = P.out_where == Where::Tape ? tape_val(N, l) : scr(N, N->off_Y);
+      const float* x = (l == 0) ? d_images : act_ptr(N, l);
+      const double pos_out = (double)n * o.F * o.vr * o.vc;
+      const double cflops = 2.0 * pos_out * P.cout * P.L.k * P.L.k * P.cin;
+      const double in_e = (l == 0) ? (double)n * N->cfg.in_channels * N->cfg.image_rows * N->cfg.image_cols
+                                   : (double)n * in.F * in.vr * in.vc * in.C;
+      const double cbytes = 4.0 * (in_e + pos_out * P.cout);
+      if (l > 0 && use_tc(N, P, false)) {
+        TcConvArgs t{};
+        t.x = x; t.n_frag = n * in.F; t.gr = in.gr; t.gc = in.gc; t.cin = P.cin;
+        t.w = wpack + P.wpack_off; t.bias = N->params + P.b_off; t.k = P.L.k; t.cout = P.cout;
+        t.out = out; t.out_vr = o.vr; t.out_vc = o.vc; t.act = P.L.act; t.shift = 0;
+        t.round_out = next_tc ? 1 : 0; t.zero_pad = 0; t.mul_dact = nullptr;
+        LAUNCH(N, s, "conv_fwd_tc", l, cflops, cbytes, launch_conv_tc(t, s));
+      } else {
+        ConvArgs c{};
+        c.in = x;
+        c.in_F = in.F;
+        c.image_mode = l == 0;
+        if (l == 0) {
+          c.in_gr = N->cfg.image_rows; c.in_gc = N->cfg.image_cols;
+          c.in_vr = N->cfg.image_rows; c.in_vc = N->cfg.image_cols;
+        } else {
+          c.in_gr = in.gr; c.in_gc = in.gc; c.in_vr = in.vr; c.in_vc = in.vc;
+        }
+        c.off_y = c.off_x = 0;
+        c.cin = P.cin;
+        c.w = wpack + P.wpack_off;
+        c.bias = N->params + P.b_off;
+        c.k = P.L.k;
+        c.cout = P.cout;
+        c.out = out;
+        c.out_gr = o.gr; c.out_gc = o.gc; c.out_vr = o.vr; c.out_vc = o.vc;
+        c.act = P.L.act;
+        c.mul_dact = nullptr;
+        c.dact = 0;
+        c.zero_pad = 0;
+        c.round_tf32 = next_tc ? 1 : 0;
+        c.n_frag_total = n * in.F;
+        LAUNCH(N, s, "conv_fwd_simt", l, cflops, cbytes, launch_conv_simt(c, s));
+      }
+    }
+  }
+  N->images = d_images;
+  N->n_fwd = n;
+  N->have_fwd = true;
+  // 3. optional softmax output
+  if (d_probs) {
+    const int L = N->n_layers - 1;
+    const Act& h = N->a[L];
+    HeadArgs hd{};
+    hd.h = act_ptr(N, L);
+    hd.gr = h.gr; hd.gc = h.gc; hd.vr = h.vr; hd.vc = h.vc; hd.Ch = h.C; hd.F = h.F;
+    hd.w = N->params + N->lp[L].w_off;
+    hd.b = N->params + N->lp[L].b_off;
+    hd.C = N->classes;
+    hd.hidden_act = N->lp[L - 1].L.act;
+    hd.probs = d_probs;
+    hd.n = n;
+    hd.err = (int*)(N->scratch + N->off_err);
+    hd.loss_part = nullptr;
+    const double pos = (double)n * h.F * h.vr * h.vc;
+    LAUNCH(N, s, "head_probs", L, 2.0 * pos * h.C * N->classes, pos * (4.0 * h.C + 4.0 * N->classes),
+           launch_head(hd, nullptr, s));
+  }
+  return MPF_OK;
+}
+
+static mpf_status wgrad(Net* N, int l, const float* x, const float* dy, int n, cudaStream_t s) {
+  const LayerPlan& P = N->lp[l];
+  const Act& in = N->a[l];
+  const Act& o = N->a[l + 1];
+  float* part = scr(N, N->off_part);
+  const long long positions = (long long)n * o.F * o.vr * o.vc;
+  const double Kd = (double)P.L.k * P.L.k * P.cin;
+  const double wflops = 2.0 * positions * P.cout * Kd;
+  const double in_e = (l == 0) ? (double)n * N->cfg.in_channels * N->cfg.image_rows * N->cfg.image_cols
+                               : (double)n * in.F * in.vr * in.vc * in.C;
+  const double wbytes = 4.0 * (in_e + (double)positions * P.cout);
+  if (l > 0 && use_tc(N, P, false)) {
+    TcWgradArgs t{};
+    t.x = x; t.dy = dy; t.n_frag = n * in.F; t.gr = in.gr; t.gc = in.gc; t.vr_out = o.vr; t.vc_out = o.vc;
+    t.cin = P.cin; t.cout = P.cout; t.k = P.L.k;
+    t.part = part;
+    t.part_cap_floats = N->part_floats;
+    int splits = 0;
+    LAUNCH(N, s, "wgrad_tc", l, wflops, wbytes, launch_wgrad_tc(t, &splits, s));
+    const long long K = (long long)P.L.k * P.L.k * P.cin;
+    LAUNCH(N, s, "wgrad_reduce", l, 0.0, 4.0 * (splits + 2.0) * (P.cout * Kd + P.cout),
+           launch_wgrad_reduce(part, part + (size_t)splits * P.cout * K, splits, P.cout, P.cin, P.L.k,
+                               N->grads + P.w_off, N->grads + P.b_off, s));
+    return MPF_OK;
+  }
+  WgradArgs w{};
+  w.x = x;
+  w.image_mode = l == 0;
+  if (l == 0) {
+    w.x_gr = N->cfg.image_rows; w.x_gc = N->cfg.image_cols; w.x_vr = N->cfg.image_rows; w.x_vc = N->cfg.image_cols;
+  } else {
+    w.x_gr = in.gr; w.x_gc = in.gc; w.x_vr = in.vr; w.x_vc = in.vc;
+  }
+  w.dy = dy;
+  w.y_gr = o.gr; w.y_gc = o.gc; w.y_vr = o.vr; w.y_vc = o.vc;
+  w.n_frag_total = n * in.F;
+  w.cin = P.cin; w.cout = P.cout; w.k = P.L.k;
+  const long long K = (long long)P.L.k * P.L.k * P.cin;
+  int splits = wgrad_simt_splits(positions);
+  while (splits > 1 && (size_t)splits * (P.cout * K + P.cout) > N->part_floats) --splits;
+  w.n_split = splits;
+  w.part_w = part;
+  w.part_b = part + (size_t)splits * P.cout * K;
+  LAUNCH(N, s, "wgrad_simt", l, wflops, wbytes, launch_wgrad_simt(w, s));
+  LAUNCH(N, s, "wgrad_reduce", l, 0.0, 4.0 * (splits + 2.0) * (P.cout * Kd + P.cout),
+         launch_wgrad_reduce(w.part_w, w.part_b, splits, P.cout, P.cin, P.L.k, N->grads + P.w_off,
+                             N->grads + P.b_off, s));
+  return MPF_OK;
+}
+
+mpf_status mpf_backward_image(mpf_net* N, const uint8_t* d_labels, const float* h_class_w, float* d_loss,
+                              void* stream) {
+  if (!N || !d_labels) return fail(MPF_ERR_ARG, "NULL argument");
+  if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound");
+  if (!N->have_fwd) return fail(MPF_ERR_STATE, "mpf_backward_image before mpf_forward_image");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int n = N->n_fwd;
+  const bool tf32 = N->cfg.precision == MPF_PREC_TF32;
+  const int L = N->n_layers - 1;  // the softmax FC
+  int* nlab = (int*)(N->scratch + N->off_nlab);
+  float* lossp = scr(N, N->off_lossp);
+  LAUNCH(N, s, "label_count", -1, 0.0, (double)n * N->O_H * N->O_W,
+         launch_label_count(d_labels, n, N->O_H * N->O_W, N->classes, nlab, s));
+  // head: dL/dx_hat (first step of back-propagation) and dh
+  const Act& h = N->a[L];
+  float* dcur = scr(N, N->off_dA);
+  float* dother = scr(N, N->off_dB);
+  float* dlog = scr(N, N->off_dlog);
+  HeadArgs hd{};
+  hd.h = act_ptr(N, L);
+  hd.gr = h.gr; hd.gc = h.gc; hd.vr = h.vr; hd.vc = h.vc; hd.Ch = h.C; hd.F = h.F;
+  hd.w = N->params + N->lp[L].w_off;
+  hd.b = N->params + N->lp[L].b_off;
+  hd.C = N->classes;
+  hd.hidden_act = N->lp[L - 1].L.act;
+  hd.labels = d_labels;
+  hd.O_H = N->O_H; hd.O_W = N->O_W;
+  hd.n_levels = N->n_levels;
+  for (int i = 0; i < N->n_levels; ++i) hd.pool_k[i] = N->pool_k[i];
+  hd.nlab = nlab;
+  for (int c = 0; c < 16; ++c) hd.cw[c] = (h_class_w && c < N->classes) ? h_class_w[c] : 1.f;
+  hd.probs = nullptr;
+  hd.dlogits = dlog;
+  hd.dh = dcur;
+  hd.loss_part = lossp;
+  hd.err = (int*)(N->scratch + N->off_err);
+  hd.n = n;
+  hd.round_tf32 = tf32 ? 1 : 0;
+  int parts = 0;
+  {
+    const double pos = (double)n * h.F * h.vr * h.vc;
+    LAUNCH(N, s, "head_loss_delta", L, 4.0 * pos * h.C * N->classes,
+           pos * (8.0 * h.C + 4.0 * N->classes + 1.0), launch_head(hd, &parts, s));
+  }
+  if (d_loss)
+    LAUNCH(N, s, "loss_finalize", L, 0.0, 4.0 * (double)parts * n, launch_loss_finalize(lossp, parts, nlab, n, d_loss, s));
+  // gradient of the softmax FC (1x1 conv over h): Alg. 2 accumulation
+  {
+    mpf_status st = wgrad(N, L, hd.h, dlog, n, s);
+    if (st != MPF_OK) return st;
+  }
+  // remaining layers in reverse.  Invariant: dcur holds the delta of a[l+1] at the
+  // pre-activation (CONV/FC output) or the value (pooled output).
+  float* wpack = scr(N, N->off_wpack);
+  for (int l = L - 1; l >= 0; --l) {
+    const LayerPlan& P = N->lp[l];
+    const Act& in = N->a[l];
+    const Act& o = N->a[l + 1];
+    if (P.L.kind == MPF_POOL) {
+      // Alg. 4: route deltas through mpIDXS, accumulate shared maxima; times act' of the conv
+      MpfBwdArgs m{};
+      m.dout = dcur;
+      m.pooled = tape_val(N, l);
+      m.idx = tape_idx(N, l);
+      m.gr = in.gr; m.gc = in.gc; m.vr = in.vr; m.vc = in.vc; m.C = in.C; m.k = P.L.k;
+      m.m_r = o.vr; m.m_c = o.vc;
+      m.n_frag_in = n * in.F;
+      m.act = N->lp[l - 1].L.act;
+      m.din = dother;
+      m.round_tf32 = tf32 ? 1 : 0;
+      const double ein = (double)n * in.F * in.vr * in.vc * in.C, eout = (double)n * o.F * o.vr * o.vc * o.C;
+      LAUNCH(N, s, "mpf_bwd", l, 0.0, 9.0 * eout + 4.0 * ein, launch_mpf_bwd(m, s));
+      std::swap(dcur, dother);
+      continue;
+    }
+    const float* x = (l == 0) ? N->images : act_ptr(N, l);
+    mpf_status st = wgrad(N, l, x, dcur, n, s);
+    if (st != MPF_OK) return st;
+    if (l == 0) break;
+    // dgrad: delta of a[l] = full correlation of dcur with the rotated kernel
+    const bool in_is_conv = N->lp[l - 1].L.kind != MPF_POOL;
+    const double pos_out = (double)n * o.F * o.vr * o.vc, pos_in = (double)n * in.F * in.vr * in.vc;
+    const double dflops = 2.0 * pos_out * P.cout * P.L.k * P.L.k * P.cin;
+    const double dbytes = 4.0 * (pos_out * P.cout + pos_in * P.cin) + (in_is_conv ? 4.0 * pos_in * P.cin : 0.0);
+    if (use_tc(N, P, true)) {
+      TcConvArgs t{};
+      t.x = dcur; t.n_frag = n * in.F; t.gr = in.gr; t.gc = in.gc; t.cin = P.cout;
+      t.w = wpack + P.dpack_off; t.bias = nullptr; t.k = P.L.k; t.cout = P.cin;
+      t.out = dother; t.out_vr = in.vr; t.out_vc = in.vc; t.act = MPF_IDENTITY; t.shift = -(P.L.k - 1);
+      t.round_out = tf32 ? 1 : 0; t.zero_pad = 1;
+      t.mul_dact = in_is_conv ? act_ptr(N, l) : nullptr;
+      t.dact = in_is_conv ? N->lp[l - 1].L.act : 0;
+      LAUNCH(N, s, "dgrad_tc", l, dflops, dbytes, launch_conv_tc(t, s));
+    } else {
+      ConvArgs c{};
+      c.in = dcur;
+      c.in_F = in.F;
+      c.image_mode = 0;
+      c.in_gr = o.gr; c.in_gc = o.gc; c.in_vr = o.vr; c.in_vc = o.vc;
+      c.off_y = c.off_x = -(P.L.k - 1);
+      c.cin = P.cout;
+      c.w = wpack + P.dpack_off;
+      c.bias = nullptr;
+      c.k = P.L.k;
+      c.cout = P.cin;
+      c.out = dother;
+      c.out_gr = in.gr; c.out_gc = in.gc; c.out_vr = in.vr; c.out_vc = in.vc;
+      c.act = MPF_IDENTITY;
+      c.mul_dact = in_is_conv ? act_ptr(N, l) : nullptr;
+      c.dact = in_is_conv ? N->lp[l - 1].L.act : 0;
+      c.zero_pad = 1;
+      c.round_tf32 = tf32 ? 1 : 0;
+      c.n_frag_total = n * in.F;
+      LAUNCH(N, s, "dgrad_simt", l, dflops, dbytes, launch_conv_simt(c, s));
+    }
+    std::swap(dcur, dother);
+  }
+  return MPF_OK;
+}
+
+mpf_status mpf_sgd_step(mpf_net* N, float lr, float scale, void* stream) {
+  if (!N) return fail(MPF_ERR_ARG, "NULL net");
+  if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound");
+  cudaStream_t s = (cudaStream_t)stream;
+  LAUNCH(N, s, "sgd", -1, 2.0 * N->n_params, 16.0 * N->n_params,
+         launch_sgd(N->params, N->grads, N->n_params, lr, scale, s));
+  return MPF_OK;
+}
+
+mpf_status mpf_train_step_host(mpf_net* N, const float* h_images, const uint8_t* h_labels, int32_t n,
+                               const float* h_class_w, float* h_loss, int32_t apply_sgd, float lr, float scale,
+                               void* stream) {
+  if (!N || !h_images || !h_labels) return fail(MPF_ERR_ARG, "NULL argument");
+  if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound");
+  if (n < 1 || n > N->n_cap) return fail(MPF_ERR_DATA, "n must be in [1, bound n_images]");
+  cudaStream_t s = (cudaStream_t)stream;
+  float* d_img = scr(N, N->off_stage_img);
+  uint8_t* d_lab = (uint8_t*)(N->scratch + N->off_stage_lab);
+  float* d_loss = scr(N, N->off_stage_loss);
+  const size_t ib = sizeof(float) * (size_t)n * N->cfg.in_channels * N->cfg.image_rows * N->cfg.image_cols;
+  const size_t lb = (size_t)n * N->O_H * N->O_W;
+  MPF_CUDA(cudaMemcpyAsync(d_img, h_images, ib, cudaMemcpyHostToDevice, s));
+  MPF_CUDA(cudaMemcpyAsync(d_lab, h_labels, lb, cudaMemcpyHostToDevice, s));
+  mpf_status st = mpf_forward_image(N, d_img, n, nullptr, stream);
+  if (st != MPF_OK) return st;
+  st = mpf_backward_image(N, d_lab, h_class_w, d_loss, stream);
+  if (st != MPF_OK) return st;
+  if (apply_sgd) {
+    st = mpf_sgd_step(N, lr, scale, stream);
+    if (st != MPF_OK) return st;
+  }
+  if (h_loss) MPF_CUDA(cudaMemcpyAsync(h_loss, d_loss, sizeof(float) * n, cudaMemcpyDeviceToHost, s));
+  return MPF_OK;
+}
+
+mpf_status mpf_fragments_to_pixels(const mpf_net* N, const float* d_frag, float* d_pix, int32_t n, int32_t C,
+                                   void* stream) {
+  if (!N || !d_frag || !d_pix) return fail(MPF_ERR_ARG, "NULL argument");
+  if (n < 1 || C < 1) return fail(MPF_ERR_ARG, "n and channels must be >= 1");
+  const Act& o = N->a[N->n_layers];
+  cudaStream_t s = (cudaStream_t)stream;
+  Net* Nm = const_cast<mpf_net*>(N);
+  LAUNCH(Nm, s, "frag2pix", -1, 0.0, 8.0 * n * C * N->O_H * N->O_W,
+         launch_frag2pix(d_frag, d_pix, n, C, o.F, o.vr, o.vc, N->O_H, N->O_W, N->n_levels, N->pool_k, s));
+  return MPF_OK;
+}
+
+mpf_status mpf_debug_tape(const mpf_net* N, int32_t layer, int32_t what, void* dst, void* stream) {
+  if (!N || !dst) return fail(MPF_ERR_ARG, "NULL argument");
+  if (!N->have_fwd) return fail(MPF_ERR_STATE, "no forward yet");
+  if (layer < 0 || layer >= N->n_layers) return fail(MPF_ERR_ARG, "layer out of range");
+  const LayerPlan& P = N->lp[layer];
+  const Act& o = N->a[layer + 1];
+  cudaStream_t s = (cudaStream_t)stream;
+  const long long nf = (long long)N->n_fwd * o.F;
+  if (what == MPF_TAPE_ARGMAX) {
+    if (P.L.kind != MPF_POOL) return fail(MPF_ERR_ARG, "argmax exists only for POOL layers");
+    MPF_CUDA(cudaMemcpyAsync(dst, tape_idx(N, layer), (size_t)nf * o.vr * o.vc * o.C, cudaMemcpyDeviceToDevice, s));
+    return MPF_OK;
+  }
+  if (what != MPF_TAPE_VALUE) return fail(MPF_ERR_ARG, "unknown tape item");
+  if (P.out_where != Where::Tape) return fail(MPF_ERR_ARG, "this layer's output is not kept on the tape");
+  MPF_CUDA(launch_compact_copy(tape_val(N, layer), o.gr, o.gc, o.vr, o.vc, o.C, nf, (float*)dst, s));
+  return MPF_OK;
+}
+
+mpf_status mpf_check(mpf_net* N, void* stream) {
+  if (!N) return fail(MPF_ERR_ARG, "NULL net");
+  cudaStream_t s = (cudaStream_t)stream;
+  MPF_CUDA(cudaStreamSynchronize(s));
+  MPF_CUDA(cudaGetLastError());
+  if (N->bound) {
+    int err = 0;
+    MPF_CUDA(cudaMemcpy(&err, N->scratch + N->off_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (err) {
+      MPF_CUDA(cudaMemset(N->scratch + N->off_err, 0, sizeof(int)));
+      return fail(MPF_ERR_DATA, "a label >= classes (and != 255) was found; it was ignored");
+    }
+  }
+  return MPF_OK;
+}
+
+}  // extern "C"

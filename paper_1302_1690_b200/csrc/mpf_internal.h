@@ -1,0 +1,195 @@
+// mpf_internal.h — internal declarations of libmpf (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/mpf.h"
+
+namespace mpf {
+
+constexpr int kMaxL = MPF_MAX_LAYERS;
+
+// One activation a[l] in the padded uniform-fragment layout.
+//   F      fragments per image
+//   vr,vc  valid rows/cols per fragment (logical size)
+//   gr,gc  storage grid per fragment (row pitch gc*C floats).  A CONV/FC output is
+//          stored in its *input's* grid (gr,gc of the input): positions past the valid
+//          region are padding ("garbage" in forward, always zero in delta buffers).
+//          Pooled outputs are compact (gr == vr).
+//   C      channels (innermost)
+struct Act {
+  int F = 1, vr = 0, vc = 0, gr = 0, gc = 0, C = 0;
+  long long elems_per_image() const { return (long long)F * gr * gc * C; }
+};
+
+enum class Where : int { None = 0, Tape = 1, ScratchY = 2 };
+
+struct LayerPlan {
+  mpf_layer L{};
+  int cin = 0, cout = 0;          // channels in / out
+  long long w_off = -1, b_off = -1; // canonical param offsets
+  long long wpack_off = -1;       // fwd pack [co][k][k][ci]  (floats, scratch)
+  long long dpack_off = -1;       // dgrad pack [ci][k][k][co] rotated
+  Where out_where = Where::None;  // where a[l+1] lives
+  long long tape_val_off = -1;    // bytes in tape (values)   (n_cap images)
+  long long tape_idx_off = -1;    // bytes in tape (argmax, POOL)
+};
+
+// live kernel timing (mpf_profile_begin/end)
+struct ProfRec {
+  std::string name;
+  int layer;
+  double flops, bytes;
+  int e0, e1;
+};
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;
+  int used = 0;
+  std::vector<ProfRec> recs;
+};
+
+struct Net {
+  mpf_config cfg{};
+  Prof prof;
+  int n_layers = 0;
+  LayerPlan lp[kMaxL];
+  Act a[kMaxL + 1];
+  int n_levels = 0, S = 1, classes = 0;
+  int O_H = 0, O_W = 0, Hp = 0, Wp = 0;
+  int pool_k[kMaxL];  // pool factors in order (levels)
+  long long n_params = 0;
+  // memory plan for n_cap images (bytes)
+  int n_cap = 0;
+  size_t tape_bytes = 0, scratch_bytes = 0;
+  size_t off_Y = 0, off_dA = 0, off_dB = 0, off_dlog = 0, off_wpack = 0, off_part = 0,
+         off_nlab = 0, off_lossp = 0, off_err = 0, off_stage_img = 0, off_stage_lab = 0,
+         off_stage_loss = 0;
+  size_t part_floats = 0;  // capacity of the wgrad partial buffer (floats)
+  int loss_parts = 0;      // loss partials per image
+  // bound memory
+  float* params = nullptr;
+  float* grads = nullptr;
+  char* tape = nullptr;
+  char* scratch = nullptr;
+  bool bound = false;
+  // state of the last forward
+  const float* images = nullptr;
+  int n_fwd = 0;
+  bool have_fwd = false;
+};
+
+// ---------------------------------------------------------------- kernels (launchers)
+// All launchers enqueue on `s` and return cudaGetLastError().
+
+struct ConvArgs {
+  // input
+  const float* in;
+  int in_F;              // fragments per image of the input (grid z = n*in_F)
+  int in_gr, in_gc;      // input storage grid
+  int in_vr, in_vc;      // readable region (elements outside read as 0)
+  int image_mode;        // 1: input is the raw image [n][Cin][H][W] (NCHW), grid (in_gr,in_gc) = (H,W)
+  int off_y, off_x;      // input coordinate of output (0,0) tap (0,0): in(y+off_y+ky, x+off_x+kx)
+  int cin;
+  // weights [cout][k][k][cin] and bias (nullable)
+  const float* w;
+  const float* bias;
+  int k, cout;
+  // output
+  float* out;
+  int out_gr, out_gc;    // output storage grid (covered fully)
+  int out_vr, out_vc;    // valid region; positions outside are written as 0 when zero_pad
+  int act;               // activation applied in the epilogue
+  const float* mul_dact; // nullable: multiply by act'(mul_dact[out position]) (deltas)
+  int dact;              // activation whose derivative is applied with mul_dact
+  int zero_pad;
+  int round_tf32;
+  int n_frag_total;      // n * in_F
+};
+cudaError_t launch_conv_simt(const ConvArgs& a, cudaStream_t s);
+
+struct WgradArgs {
+  const float* x;        // layer input
+  int image_mode;        // x is the raw image (NCHW, zero outside H,W)
+  int x_gr, x_gc, x_vr, x_vc;
+  const float* dy;       // delta at pre-activation of the layer output, grid (y_gr, y_gc)
+  int y_gr, y_gc, y_vr, y_vc;
+  int n_frag_total;
+  int cin, cout, k;
+  float* part_w;         // [n_split][cout][k*k*cin]
+  float* part_b;         // [n_split][cout]
+  int n_split;
+};
+cudaError_t launch_wgrad_simt(const WgradArgs& a, cudaStream_t s);
+int wgrad_simt_splits(long long positions);
+
+// grads_canon[w_off + ((co*cin+ci)*k+ky)*k+kx] += sum_s part_w[s][co][(ky*k+kx)*cin+ci]; bias likewise.
+cudaError_t launch_wgrad_reduce(const float* part_w, const float* part_b, int n_split, int cout, int cin,
+                                int k, float* grad_w, float* grad_b, cudaStream_t s);
+
+struct MpfArgs {
+  const float* y;        // conv output, grid (gr,gc), valid vr x vc, C channels
+  int gr, gc, vr, vc, C, k;
+  int n_frag_in;         // n * F_in
+  float* out;            // pooled [n*F_in*k*k][m][m][C], m = (vr-k+1)/k (uniform)
+  uint8_t* idx;          // argmax dy*k+dx
+  int m_r, m_c;
+  int round_tf32;
+};
+cudaError_t launch_mpf_fwd(const MpfArgs& a, cudaStream_t s);
+
+struct MpfBwdArgs {
+  const float* dout;     // delta of the pooled output [n*F_in*k*k][m][m][C]
+  const float* pooled;   // pooled values (for act')
+  const uint8_t* idx;
+  int gr, gc, vr, vc, C, k, m_r, m_c;
+  int n_frag_in;
+  int act;               // activation of the conv that produced y
+  float* din;            // delta at pre-activation of y, grid (gr,gc); zero outside valid
+  int round_tf32;
+};
+cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s);
+
+struct HeadArgs {
+  const float* h;        // last hidden activation, grid (gr,gc), valid (vr,vc), Ch channels
+  int gr, gc, vr, vc, Ch, F; // F fragments per image
+  const float* w;        // last FC weights canonical [C][Ch] (1x1)
+  const float* b;        // [C]
+  int C;
+  int hidden_act;        // activation of h (for act')
+  const uint8_t* labels; // [n][O_H][O_W] or null (forward only)
+  int O_H, O_W;
+  int n_levels;
+  int pool_k[kMaxL];
+  const int* nlab;       // [n]
+  float cw[16];          // class weights
+  float* probs;          // nullable: [n*F][vr][vc][C] compact
+  float* dlogits;        // nullable: [n*F][gr][gc][C]
+  float* dh;             // nullable: [n*F][gr][gc][Ch]
+  float* loss_part;      // [n][parts]
+  int* err;
+  int n;
+  int round_tf32;
+};
+cudaError_t launch_head(const HeadArgs& a, int* parts_per_image, cudaStream_t s);
+
+cudaError_t launch_label_count(const uint8_t* labels, int n, int hw, int classes, int* nlab, cudaStream_t s);
+cudaError_t launch_loss_finalize(const float* loss_part, int parts, const int* nlab, int n, float* loss,
+                                 cudaStream_t s);
+cudaError_t launch_sgd(float* params, float* grads, long long n, float lr, float scale, cudaStream_t s);
+cudaError_t launch_pack_weights(const float* w_canon, int cout, int cin, int k, float* wpack, float* dpack,
+                                int round_tf32, cudaStream_t s);
+cudaError_t launch_frag2pix(const float* frag, float* pix, int n, int C, int F, int fr, int fc, int O_H,
+                            int O_W, int n_levels, const int* pool_k, cudaStream_t s);
+cudaError_t launch_compact_copy(const float* src, int gr, int gc, int vr, int vc, int C, long long nf,
+                                float* dst, cudaStream_t s);
+
+// thread-local error text
+void set_error(const std::string& msg);
+
+}  // namespace mpf
+
+struct mpf_net : public mpf::Net {};

@@ -1,0 +1,199 @@
+"""Thin Python wrapper over the libmpf C ABI (marshalling only).
+
+PyTorch provides device memory and streams; every step of the training path runs
+in libmpf's CUDA kernels.  There is no CPU path: constructing an ``MPFNet`` without
+a CUDA device, or without the built library, raises.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+
+def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[ctypes.c_void_p]:
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+@dataclass
+class Geometry:
+    n_layers: int
+    n_levels: int
+    classes: int
+    stride: int
+    n_fragments: int
+    out_rows: int
+    out_cols: int
+    padded_rows: int
+    padded_cols: int
+    frag_rows: int
+    frag_cols: int
+    n_params: int
+    frag: list
+    rows: list
+    cols: list
+    chans: list
+    w_offset: list
+    b_offset: list
+
+
+def layers_to_c(layers) -> "ctypes.Array":
+    arr = (L.MpfLayer * len(layers))()
+    for i, ly in enumerate(layers):
+        arr[i].kind, arr[i].k, arr[i].n_out, arr[i].act = int(ly.kind), int(ly.k), int(ly.n_out), int(ly.act)
+    return arr
+
+
+class MPFNet:
+    """One network bound to PyTorch-allocated device buffers.
+
+    layers: sequence with .kind/.k/.n_out/.act (mpf_synth.Layer); patch = P.
+    """
+
+    def __init__(self, layers: Sequence, patch: int, image_rows: int, image_cols: int, max_images: int,
+                 in_channels: int = 1, precision: str = "tf32", device: Optional[torch.device] = None,
+                 debug_keep: bool = False):
+        if not torch.cuda.is_available():
+            raise RuntimeError("MPFNet needs a CUDA device (there is no CPU fallback)")
+        self.lib = L.lib()
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        cfg = L.MpfConfig(in_channels, patch, image_rows, image_cols, max_images,
+                          L.MPF_PREC_TF32 if precision == "tf32" else L.MPF_PREC_FP32, 1,
+                          1 if debug_keep else 0)
+        self.layers = tuple(layers)
+        self.patch = patch
+        self.in_channels = in_channels
+        self.image_rows, self.image_cols = image_rows, image_cols
+        self.max_images = max_images
+        h = ctypes.c_void_p()
+        L.check(self.lib.mpf_net_create(ctypes.byref(cfg), layers_to_c(self.layers), len(self.layers),
+                                        ctypes.byref(h)), "mpf_net_create")
+        self.h = h
+        g = L.MpfGeometry()
+        L.check(self.lib.mpf_net_geometry(self.h, ctypes.byref(g)), "mpf_net_geometry")
+        nl = g.n_layers
+        self.geom = Geometry(g.n_layers, g.n_levels, g.classes, g.stride, g.n_fragments, g.out_rows, g.out_cols,
+                             g.padded_rows, g.padded_cols, g.frag_rows, g.frag_cols, g.n_params,
+                             list(g.frag[:nl + 1]), list(g.rows[:nl + 1]), list(g.cols[:nl + 1]),
+                             list(g.chans[:nl + 1]), list(g.w_offset[:nl]), list(g.b_offset[:nl]))
+        pb, gb, tb, sb = (ctypes.c_uint64() for _ in range(4))
+        L.check(self.lib.mpf_net_memory(self.h, max_images, ctypes.byref(pb), ctypes.byref(gb), ctypes.byref(tb),
+                                        ctypes.byref(sb)), "mpf_net_memory")
+        self.bytes = dict(params=pb.value, grads=gb.value, tape=tb.value, scratch=sb.value)
+        with torch.cuda.device(self.device):
+            self.params = torch.zeros(self.geom.n_params, dtype=torch.float32, device=self.device)
+            self.grads = torch.zeros(self.geom.n_params, dtype=torch.float32, device=self.device)
+            self.tape = torch.empty(tb.value, dtype=torch.uint8, device=self.device)
+            self.scratch = torch.empty(sb.value, dtype=torch.uint8, device=self.device)
+        L.check(self.lib.mpf_net_bind(self.h, _ptr(self.params), _ptr(self.grads), _ptr(self.tape),
+                                      _ptr(self.scratch), max_images), "mpf_net_bind")
+        self._images = None
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            try:
+                self.lib.mpf_net_destroy(h)
+            except Exception:
+                pass
+            self.h = None
+
+    # ------------------------------------------------------------------ parameters
+    def set_params(self, flat) -> None:
+        t = torch.as_tensor(np.asarray(flat, np.float32) if not torch.is_tensor(flat) else flat)
+        if t.numel() != self.geom.n_params:
+            raise ValueError(f"expected {self.geom.n_params} parameters, got {t.numel()}")
+        self.params.copy_(t.reshape(-1).to(self.device, torch.float32))
+
+    def get_params(self) -> torch.Tensor:
+        return self.params.clone()
+
+    def zero_grads(self) -> None:
+        self.grads.zero_()
+
+    # ------------------------------------------------------------------ the path
+    def forward(self, images: torch.Tensor, want_probs: bool = False, stream=None) -> Optional[torch.Tensor]:
+        """images: cuda float32 [n, in_channels, H, W] (kept alive until backward)."""
+        if images.dtype != torch.float32 or not images.is_cuda or not images.is_contiguous():
+            raise ValueError("images must be a contiguous cuda float32 tensor")
+        n = images.shape[0]
+        probs = None
+        if want_probs:
+            g = self.geom
+            probs = torch.empty((n * g.n_fragments, g.frag_rows, g.frag_cols, g.classes), dtype=torch.float32,
+                                device=self.device)
+        L.check(self.lib.mpf_forward_image(self.h, _ptr(images), n, _ptr(probs), _stream_ptr(stream)),
+                "mpf_forward_image")
+        self._images = images
+        return probs
+
+    def backward(self, labels: torch.Tensor, class_w=None, stream=None) -> torch.Tensor:
+        """labels: cuda uint8 [n, out_rows, out_cols] (255 = ignore); returns per-image losses [n]."""
+        if labels.dtype != torch.uint8 or not labels.is_cuda or not labels.is_contiguous():
+            raise ValueError("labels must be a contiguous cuda uint8 tensor")
+        n = labels.shape[0]
+        loss = torch.empty(n, dtype=torch.float32, device=self.device)
+        cw = None
+        if class_w is not None:
+            arr = (ctypes.c_float * self.geom.classes)(*[float(v) for v in class_w])
+            cw = arr
+        L.check(self.lib.mpf_backward_image(self.h, _ptr(labels), cw, _ptr(loss), _stream_ptr(stream)),
+                "mpf_backward_image")
+        return loss
+
+    def sgd_step(self, lr: float, grad_scale: float = 1.0, stream=None) -> None:
+        L.check(self.lib.mpf_sgd_step(self.h, float(lr), float(grad_scale), _stream_ptr(stream)), "mpf_sgd_step")
+
+    def train_step_host(self, h_images: torch.Tensor, h_labels: torch.Tensor, h_loss: torch.Tensor,
+                        apply_sgd: bool = True, lr: float = 0.01, grad_scale: float = 1.0, class_w=None,
+                        stream=None) -> None:
+        """Host (pinned) buffers in, loss copied back to h_loss; async on `stream`."""
+        n = h_images.shape[0]
+        cw = None
+        if class_w is not None:
+            cw = (ctypes.c_float * self.geom.classes)(*[float(v) for v in class_w])
+        L.check(self.lib.mpf_train_step_host(self.h, _ptr(h_images), _ptr(h_labels), n, cw, _ptr(h_loss),
+                                             1 if apply_sgd else 0, float(lr), float(grad_scale),
+                                             _stream_ptr(stream)), "mpf_train_step_host")
+
+    def fragments_to_pixels(self, frag: torch.Tensor, n: int, channels: int, stream=None) -> torch.Tensor:
+        g = self.geom
+        out = torch.empty((n, channels, g.out_rows, g.out_cols), dtype=torch.float32, device=self.device)
+        L.check(self.lib.mpf_fragments_to_pixels(self.h, _ptr(frag), _ptr(out), n, channels, _stream_ptr(stream)),
+                "mpf_fragments_to_pixels")
+        return out
+
+    def debug_tape(self, layer: int, what: int, n: int) -> torch.Tensor:
+        g = self.geom
+        shape = (n * g.frag[layer + 1], g.rows[layer + 1], g.cols[layer + 1], g.chans[layer + 1])
+        dt = torch.uint8 if what == L.MPF_TAPE_ARGMAX else torch.float32
+        out = torch.empty(shape, dtype=dt, device=self.device)
+        L.check(self.lib.mpf_debug_tape(self.h, layer, what, _ptr(out), _stream_ptr(None)), "mpf_debug_tape")
+        return out
+
+    def profile_begin(self, max_launches: int = 100000) -> None:
+        L.check(self.lib.mpf_profile_begin(self.h, max_launches), "mpf_profile_begin")
+
+    def profile_end(self) -> list:
+        """Per (kernel, layer): launches, total_ms, algorithmic flops/bytes per launch."""
+        cap = 512
+        arr = (L.MpfKernelStat * cap)()
+        n = ctypes.c_int32()
+        L.check(self.lib.mpf_profile_end(self.h, arr, cap, ctypes.byref(n)), "mpf_profile_end")
+        return [dict(name=arr[i].name.decode(), layer=arr[i].layer, launches=arr[i].launches,
+                     total_ms=arr[i].total_ms, flops=arr[i].flops, bytes=arr[i].bytes) for i in range(n.value)]
+
+    def check(self, stream=None) -> None:
+        L.check(self.lib.mpf_check(self.h, _stream_ptr(stream)), "mpf_check")

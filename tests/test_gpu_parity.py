@@ -1,0 +1,269 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element.
+
+Bars (BASELINE.json north_star): pooling argmax indices and the fragment -> pixel
+permutation bit-exact; outputs, loss and every gradient tensor within relative L2
+5e-3 (TF32 tensor cores, fp32 accumulate; reading R17: per tensor).
+"""
+import numpy as np
+import pytest
+
+import mpf_synth as S
+import oracle
+from oracle import o2
+from tests.gpu_common import (TOL_FP32, TOL_TF32, compare_step, gpu_step, oracle_step, param_slices,
+                              rel_l2)
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1302_1690_b200 import MPF_TAPE_ARGMAX, MPF_TAPE_VALUE, MpfError  # noqa: E402
+from paper_1302_1690_b200.net import MPFNet  # noqa: E402
+
+PRECS = [("fp32", TOL_FP32), ("tf32", TOL_TF32)]
+
+
+@pytest.mark.parametrize("prec,tol", PRECS)
+def test_cfg1_full_image_vs_o1(prec, tol):
+    """configs[0]: every one of the 361 pixels through the patch-by-patch oracle."""
+    cfg = S.CONFIGS["cfg1"]
+    images, labels = S.make_batch(cfg, [0])
+    params = S.init_params(cfg)
+    g = gpu_step(cfg.layers, cfg.P, images, labels, params, prec)
+    o = oracle_step(cfg.layers, cfg.P, images.astype(np.float64), labels, params, engine="o1")
+    o["probs"] = [pr.reshape(cfg.out_rows, cfg.out_cols, cfg.classes).transpose(2, 0, 1) for pr in o["probs"]]
+    compare_step(cfg.layers, g, o, tol, "cfg1")
+    # SGD update theta <- theta - lr * mean gradient
+    d_gpu = g["params1"].astype(np.float64) - g["params0"]
+    assert rel_l2(d_gpu, -cfg.lr * o["grad_sum"]) <= max(tol, 1e-4)
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("prec,tol", PRECS)
+def test_random_archs_vs_o2(seed, prec, tol):
+    rng = np.random.default_rng(500 + seed)
+    layers, P = S.random_arch_case(rng)
+    n = int(rng.integers(1, 4))
+    H = int(rng.integers(P, P + 30))
+    W = int(rng.integers(P, P + 30))
+    images = rng.standard_normal((n, 1, H, W)).astype(np.float32)
+    C = layers[-1].n_out
+    labels = S.random_labels(rng, n, H - P + 1, W - P + 1, C)
+    params = S.init_params(layers, seed) * 1.5
+    g = gpu_step(layers, P, images, labels, params, prec)
+    o = oracle_step(layers, P, images.astype(np.float64), labels, params, engine="o2")
+    compare_step(layers, g, o, tol, f"random arch seed {seed}")
+
+
+def test_cfg2_batch_vs_o2():
+    """configs[1]: 8 images of 128^2, one SGD step on the batch mean, TF32."""
+    cfg = S.CONFIGS["cfg2"]
+    images, labels = S.make_batch(cfg, range(8))
+    params = S.init_params(cfg)
+    g = gpu_step(cfg.layers, cfg.P, images, labels, params, "tf32")
+    o = oracle_step(cfg.layers, cfg.P, images.astype(np.float64), labels, params, engine="o2")
+    errs = compare_step(cfg.layers, g, o, TOL_TF32, "cfg2")
+    print("cfg2 rel L2:", {k: f"{v:.2e}" for k, v in errs.items()})
+    d_gpu = g["params1"].astype(np.float64) - g["params0"]
+    assert rel_l2(d_gpu, -cfg.lr * o["grad_sum"] / 8) <= TOL_TF32
+
+
+@pytest.mark.parametrize("name,H", [("cfg1", 32), ("cfg2", 100), ("cfg5", 120)])
+@pytest.mark.parametrize("prec", ["fp32", "tf32"])
+def test_argmax_bit_exact_on_identical_inputs(name, H, prec):
+    """MPF forward (Alg. 3) on the GPU's own fp32 conv output, promoted exactly to fp64,
+    through the oracle's MP_fwd: argmax indices must match bit for bit (R6, R16)."""
+    cfg = S.CONFIGS[name]
+    rng = np.random.default_rng(3)
+    n = 2
+    images = rng.standard_normal((n, 1, H, H)).astype(np.float32)
+    params = S.init_params(cfg)
+    net = MPFNet(cfg.layers, cfg.P, H, H, max_images=n, precision=prec, debug_keep=True)
+    net.set_params(params.astype(np.float32))
+    net.forward(torch.tensor(images, device="cuda"))
+    torch.cuda.synchronize()
+    for l, ly in enumerate(cfg.layers):
+        if ly.kind != S.POOL:
+            continue
+        Y = net.debug_tape(l - 1, MPF_TAPE_VALUE, n).cpu().numpy().astype(np.float64)  # [nF, vr, vc, C]
+        pooled = net.debug_tape(l, MPF_TAPE_VALUE, n).cpu().numpy()
+        idx = net.debug_tape(l, MPF_TAPE_ARGMAX, n).cpu().numpy()
+        storage = [o2.Fragment(Y[g].transpose(2, 0, 1)) for g in range(Y.shape[0])]
+        F_out, mpidx = o2.mpf_fwd(storage, ly.k)
+        assert len(F_out) == idx.shape[0]
+        want_idx = np.stack([m.transpose(1, 2, 0) for m in mpidx])
+        want_val = np.stack([f.maps.transpose(1, 2, 0) for f in F_out])
+        assert np.array_equal(idx, want_idx.astype(np.uint8)), f"layer {l}: argmax mismatch"
+        if prec == "fp32":
+            assert np.array_equal(pooled.astype(np.float64), want_val), f"layer {l}: pooled values differ"
+        else:  # pooled values are stored rounded to tf32 (operand of the next MMA)
+            assert np.max(np.abs(pooled - want_val) / np.maximum(np.abs(want_val), 1e-30)) <= 2.0 ** -11
+
+
+@pytest.mark.parametrize("name,H", [("cfg1", 32), ("cfg2", 128), ("cfg5", 160)])
+def test_fragments_to_pixels_permutation_bit_exact(name, H):
+    """G8 against the oracle's lineage (O2 fragment enumeration, R2)."""
+    cfg = S.CONFIGS[name]
+    net = MPFNet(cfg.layers, cfg.P, H, H, max_images=2)
+    g = net.geom
+    n, C = 2, 3
+    shape = (n * g.n_fragments, g.frag_rows, g.frag_cols, C)
+    iota = torch.arange(int(np.prod(shape)), dtype=torch.float32, device="cuda").reshape(shape)
+    assert iota.numel() < 2 ** 24
+    pix = net.fragments_to_pixels(iota, n, C).cpu().numpy()
+    # the oracle's fragment lineages on the padded image (uniform fragments)
+    tape, _ = o2.forward_dense(cfg.layers, S.init_params(cfg), np.zeros((g.padded_rows, g.padded_cols)))
+    final = tape[-1]
+    assert len(final) == g.n_fragments
+    want = np.full((n, C, g.out_rows, g.out_cols), -1.0)
+    hits = np.zeros((g.out_rows, g.out_cols), int)
+    for f, frag in enumerate(final):
+        assert frag.maps.shape[1:] == (g.frag_rows, g.frag_cols)
+        for m in range(g.frag_rows):
+            for q in range(g.frag_cols):
+                y, x = o2.lineage_to_pixel(frag.lineage, m, q)
+                if y < g.out_rows and x < g.out_cols:
+                    hits[y, x] += 1
+                    for img in range(n):
+                        base = (((img * g.n_fragments + f) * g.frag_rows + m) * g.frag_cols + q) * C
+                        want[img, :, y, x] = base + np.arange(C)
+    assert np.all(hits == 1)
+    assert np.array_equal(pix, want)
+
+
+def _full_size_case(name, n_pix, seed):
+    cfg = S.CONFIGS[name]
+    images, labels = S.make_batch(cfg, [seed])
+    rng = np.random.default_rng(seed)
+    O = cfg.out_rows
+    pix = np.sort(rng.choice(O * O, n_pix, replace=False)).astype(np.int32)
+    sparse = np.full_like(labels, 255)
+    sparse.reshape(1, -1)[0, pix] = labels.reshape(1, -1)[0, pix]
+    return cfg, images, labels, sparse, pix
+
+
+@pytest.mark.parametrize("name,n_pix", [("cfg3", 256), ("cfg5", 128), ("cfg4", 24)])
+def test_full_size_sampled_outputs_and_sparse_gradient(name, n_pix):
+    """BASELINE.json full sizes (one image, the launch configuration of bench.py): outputs
+    at sampled pixels vs O1 computed one by one; the gradient with only those pixels
+    labelled vs O1 on the same pixels (fp32 path: exact-arithmetic reference mode)."""
+    cfg, images, labels, sparse, pix = _full_size_case(name, n_pix, 7)
+    params = S.init_params(cfg)
+    o = oracle_step(cfg.layers, cfg.P, images.astype(np.float64), sparse, params, engine="o1", pix=[pix])
+    for prec, tol in [("tf32", TOL_TF32), ("fp32", TOL_FP32 * 10)]:
+        g = gpu_step(cfg.layers, cfg.P, images, sparse, params, prec)
+        gp = g["probs"][0].reshape(cfg.classes, -1)[:, pix].T
+        e_p = rel_l2(gp, o["probs"][0])
+        assert e_p <= tol, (prec, e_p)
+        if prec == "fp32":
+            errs = compare_step(cfg.layers, g, {"probs": [None], "loss": o["loss"], "grad_sum": o["grad_sum"]},
+                                tol, f"{name} sparse")
+            print(name, "sparse-label grads (fp32):", {k: f"{v:.1e}" for k, v in errs.items()})
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg5", "cfg4"])
+def test_full_size_properties(name):
+    """Properties that hold at any size, checked on the full BASELINE image: softmax rows
+    sum to 1; the GPU loss equals the mean -w log p recomputed (fp64) from the GPU's own
+    outputs; the bias gradient of the softmax layer equals mean_t w_t (p - onehot_t)."""
+    cfg = S.CONFIGS[name]
+    images, labels = S.make_batch(cfg, [3])
+    params = S.init_params(cfg)
+    g = gpu_step(cfg.layers, cfg.P, images, labels, params, "tf32")
+    p = g["probs"][0].astype(np.float64)           # [C, O, O]
+    assert np.max(np.abs(p.sum(0) - 1)) < 1e-5
+    lab = labels[0].astype(np.int64)
+    m = lab != 255
+    pt = np.take_along_axis(p, np.where(m, lab, 0)[None], 0)[0]
+    loss = -np.log(pt[m]).mean()
+    assert abs(g["loss"][0] - loss) <= 1e-4 * abs(loss)
+    onehot = np.zeros_like(p)
+    np.put_along_axis(onehot, np.where(m, lab, 0)[None], 1.0, 0)
+    db = ((p - onehot) * m[None]).sum((1, 2)) / m.sum()
+    sl = param_slices(cfg.layers)[-1][1]
+    assert rel_l2(g["grad_sum"][sl], db) <= 1e-4
+
+
+# ----------------------------------------------------------------- edge cases
+
+def test_all_labels_ignored_gives_zero_loss_and_grad():
+    cfg = S.CONFIGS["cfg1"]
+    images, labels = S.make_batch(cfg, [0])
+    labels[:] = 255
+    g = gpu_step(cfg.layers, cfg.P, images, labels, S.init_params(cfg), "tf32")
+    assert g["loss"][0] == 0.0
+    assert np.all(g["grad_sum"] == 0.0)
+
+
+def test_bad_label_is_reported():
+    cfg = S.CONFIGS["cfg1"]
+    images, labels = S.make_batch(cfg, [0])
+    labels[0, 3, 3] = 7
+    with pytest.raises(MpfError) as e:
+        gpu_step(cfg.layers, cfg.P, images, labels, S.init_params(cfg), "tf32")
+    assert e.value.status == 3
+
+
+def test_class_weights_vs_o1():
+    cfg = S.CONFIGS["cfg1"]
+    images, labels = S.make_batch(cfg, [1])
+    params = S.init_params(cfg)
+    cw = [0.3, 2.5]
+    g = gpu_step(cfg.layers, cfg.P, images, labels, params, "fp32", class_w=cw)
+    o = oracle_step(cfg.layers, cfg.P, images.astype(np.float64), labels, params, engine="o1", class_w=cw)
+    o["probs"] = [pr.reshape(19, 19, 2).transpose(2, 0, 1) for pr in o["probs"]]
+    compare_step(cfg.layers, g, o, TOL_FP32, "class weights")
+
+
+def test_microbatch_accumulation_and_determinism():
+    """backward accumulates (Alg. 2): grads of [A] + grads of [B] == grads of [A, B];
+    reruns are bitwise identical (fixed-order reductions)."""
+    cfg = S.CONFIGS["cfg2"]
+    images, labels = S.make_batch(cfg, [0, 1])
+    params = S.init_params(cfg).astype(np.float32)
+    net = MPFNet(cfg.layers, cfg.P, 128, 128, max_images=2)
+    net.set_params(params)
+
+    def run(sel):
+        net.zero_grads()
+        for s in sel:
+            im = torch.tensor(images[s], device="cuda").contiguous()
+            lb = torch.tensor(labels[s], device="cuda").contiguous()
+            net.forward(im)
+            net.backward(lb)
+        torch.cuda.synchronize()
+        return net.grads.clone().cpu().numpy()
+
+    both = run([slice(0, 2)])
+    both2 = run([slice(0, 2)])
+    assert np.array_equal(both, both2)
+    split = run([slice(0, 1), slice(1, 2)])
+    assert rel_l2(split, both) <= 1e-5
+
+
+def test_host_buffer_step_matches_device_step():
+    cfg = S.CONFIGS["cfg2"]
+    images, labels = S.make_batch(cfg, [4, 5])
+    params = S.init_params(cfg).astype(np.float32)
+    g = gpu_step(cfg.layers, cfg.P, images, labels, params, "tf32")
+    net = MPFNet(cfg.layers, cfg.P, 128, 128, max_images=2)
+    net.set_params(params)
+    h_img = torch.tensor(images).pin_memory()
+    h_lab = torch.tensor(labels).pin_memory()
+    h_loss = torch.zeros(2).pin_memory()
+    net.train_step_host(h_img, h_lab, h_loss, apply_sgd=True, lr=cfg.lr, grad_scale=0.5)
+    torch.cuda.synchronize()
+    assert np.array_equal(h_loss.numpy(), g["loss"])
+    assert np.array_equal(net.params.cpu().numpy(), g["params1"])
+
+
+def test_fewer_images_than_capacity():
+    cfg = S.CONFIGS["cfg1"]
+    images, labels = S.make_batch(cfg, [0, 1, 2])
+    params = S.init_params(cfg)
+    net = MPFNet(cfg.layers, cfg.P, 32, 32, max_images=4)
+    g = gpu_step(cfg.layers, cfg.P, images, labels, params, "tf32", net=net)
+    o = oracle_step(cfg.layers, cfg.P, images.astype(np.float64), labels, params, engine="o2")
+    compare_step(cfg.layers, g, o, TOL_TF32, "n < capacity")
