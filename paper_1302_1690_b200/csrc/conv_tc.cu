@@ -1,10 +1,536 @@
-// conv_tc.cu — tcgen05 implicit-GEMM convolutions (placeholder until the kernels land).
+// conv_tc.cu — tcgen05 (kind::tf32, TMEM accumulators, TMA-fed) implicit-GEMM
+// convolution over all fragments at once: forward of C/FC layers (Alg. 1 applied to
+// every fragment) and the delta propagation (dgrad) of the backward.
+//
+// GEMM view.  Positions are flattened over (image, fragment, row, col) of the storage
+// grid (row pitch gc): p = ((f * gr) + y) * gc + x.  A valid k x k correlation is a
+// sum over k^2 taps t = (ky, kx) of a position shift:
+//     D[p, co] = sum_t sum_ci X[p + base + ky*gc + kx, ci] * W[co, t, ci]
+// with base = 0 (forward) or -(k-1)(gc+1) (dgrad, rotated weights).  Positions whose
+// window leaves the fragment are garbage and are never used; reads outside the tensor
+// are zero-filled by TMA.  Delta tensors are zero outside their valid region, which
+// makes the dgrad "full correlation" exact with the same 1-D formulation.
+//
+// Kernel.  One CTA computes M_cta = NACC x 128 consecutive positions, all output
+// channels (N = cout padded to 16), into NACC TMEM accumulators of 128 x N fp32.
+// K loop over stages (ky, 32-channel chunk): one TMA "slab" of M_cta + 8 input rows
+// (128 B = 32 fp32 per row, SWIZZLE_128B) is reused for all k taps kx of that row by
+// offsetting the UMMA descriptor start by kx rows; the weights of each tap are a
+// separate TMA tile [N x 32].  Warp roles: warp 0 TMA producer, warp 1 TMEM allocator
+// + single-thread MMA issuer, warps 2-5 epilogue (TMEM -> registers -> bias/act ->
+// global).  Two mbarrier rings (A slabs, B taps) with full/empty phases.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <mutex>
+
 #include "conv_tc.h"
+#include "tc_ptx.cuh"
+#include "mpf_internal.h"
 
 namespace mpf {
 
-bool tc_supported(int, int, int) { return false; }
-cudaError_t launch_conv_tc(const TcConvArgs&, cudaStream_t) { return cudaErrorNotSupported; }
-cudaError_t launch_wgrad_tc(const TcWgradArgs&, int*, cudaStream_t) { return cudaErrorNotSupported; }
+namespace {
+
+constexpr int kThreads = 192;  // 6 warps
+constexpr int kKC = 32;        // fp32 channels per 128-byte row
+
+struct ConvTcParams {
+  int P_tot, gr, gc, out_vr, out_vc;
+  int cin, cout, npad, k, shift_rows, n_cc;
+  int act, round_out, zero_pad, dact;
+  const float* bias;
+  float* out;
+  const float* mul_dact;
+  int box_rows, nbox;
+  uint32_t a_slot_bytes, b_slot_bytes;
+  int n_bslots;
+  int base_mode;
+  uint32_t tmem_cols;
+};
+
+__device__ __forceinline__ float tf32r(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ float act_f(int act, float v) {
+  if (act == MPF_TANH) return tanhf(v);
+  if (act == MPF_LOGISTIC) return 1.f / (1.f + expf(-v));
+  return v;
+}
+__device__ __forceinline__ float act_d(int act, float y) {
+  if (act == MPF_TANH) return 1.f - y * y;
+  if (act == MPF_LOGISTIC) return y * (1.f - y);
+  return 1.f;
+}
+
+template <int NACC>
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, ConvTcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-B aligned carve-up
+  const uint32_t sbase = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t sA = sbase;                                   // 2 A slabs
+  const uint32_t sB = sA + 2 * p.a_slot_bytes;                 // n_bslots weight taps
+  const uint32_t sBar = sB + p.n_bslots * p.b_slot_bytes;      // barriers
+  const uint32_t barAfull = sBar, barAempty = sBar + 16;
+  const uint32_t barBfull = sBar + 32, barBempty = barBfull + 8 * p.n_bslots;
+  const uint32_t barTfull = barBempty + 8 * p.n_bslots;
+  const uint32_t sTmemSlot = barTfull + 8;
+  uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (sTmemSlot - ptx::smem_u32(smem_raw)));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p0 = blockIdx.x * (NACC * 128);
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(barAfull + 8 * i, 1);
+      ptx::mbar_init(barAempty + 8 * i, 1);
+    }
+    for (int i = 0; i < p.n_bslots; ++i) {
+      ptx::mbar_init(barBfull + 8 * i, 1);
+      ptx::mbar_init(barBempty + 8 * i, 1);
+    }
+    ptx::mbar_init(barTfull, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(sTmemSlot, p.tmem_cols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot_ptr;
+
+  const int k = p.k;
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int a_it = 0, b_it = 0;
+      for (int ky = 0; ky < k; ++ky) {
+        for (int cc = 0; cc < p.n_cc; ++cc) {
+          const int as = a_it & 1;
+          ptx::mbar_wait(barAempty + 8 * as, ((a_it >> 1) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(barAfull + 8 * as, p.a_slot_bytes);
+          const int row0 = p0 + p.shift_rows + ky * p.gc;
+          for (int b = 0; b < p.nbox; ++b)
+            ptx::tma_load_2d(sA + as * p.a_slot_bytes + b * p.box_rows * 128, &tmA, barAfull + 8 * as, cc * kKC,
+                             row0 + b * p.box_rows);
+          ++a_it;
+          for (int kx = 0; kx < k; ++kx) {
+            const int bs = b_it % p.n_bslots;
+            ptx::mbar_wait(barBempty + 8 * bs, ((b_it / p.n_bslots) & 1) ^ 1);
+            ptx::mbar_arrive_expect_tx(barBfull + 8 * bs, p.b_slot_bytes);
+            ptx::tma_load_2d(sB + bs * p.b_slot_bytes, &tmB, barBfull + 8 * bs, (ky * k + kx) * p.cin + cc * kKC, 0);
+            ++b_it;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    const uint32_t idesc = ptx::idesc_tf32(128, p.npad);
+    int a_it = 0, b_it = 0;
+    for (int ky = 0; ky < k; ++ky) {
+      for (int cc = 0; cc < p.n_cc; ++cc) {
+        const int as = a_it & 1;
+        ptx::mbar_wait(barAfull + 8 * as, (a_it >> 1) & 1);
+        for (int kx = 0; kx < k; ++kx) {
+          const int bs = b_it % p.n_bslots;
+          ptx::mbar_wait(barBfull + 8 * bs, (b_it / p.n_bslots) & 1);
+          ptx::tc_fence_after();
+          if (lane == 0) {
+#pragma unroll
+            for (int acc = 0; acc < NACC; ++acc) {
+#pragma unroll
+              for (int k8 = 0; k8 < 4; ++k8) {
+                const uint32_t aaddr = sA + as * p.a_slot_bytes + (acc * 128 + kx) * 128 + k8 * 32;
+                const uint32_t baddr = sB + bs * p.b_slot_bytes + k8 * 32;
+                const uint32_t accum = (ky | cc | kx | k8) != 0;
+                ptx::mma_tf32(tmem + acc * p.npad, ptx::sdesc_k_sw128(aaddr, p.base_mode),
+                              ptx::sdesc_k_sw128(baddr, p.base_mode), idesc, accum);
+              }
+            }
+            ptx::mma_commit(barBempty + 8 * bs);
+          }
+          __syncwarp();
+          ++b_it;
+        }
+        if (lane == 0) ptx::mma_commit(barAempty + 8 * as);
+        __syncwarp();
+        ++a_it;
+      }
+    }
+    if (lane == 0) ptx::mma_commit(barTfull);
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------ epilogue (warps 2..5)
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = q * 32 + lane;
+    ptx::mbar_wait(barTfull, 0);
+    ptx::tc_fence_after();
+    const int per_frag = p.gr * p.gc;
+    for (int acc = 0; acc < NACC; ++acc) {
+      const int pos = p0 + acc * 128 + row;
+      const bool inb = pos < p.P_tot;
+      int y = 0, x = 0;
+      if (inb) {
+        const int r = pos % per_frag;
+        y = r / p.gc;
+        x = r % p.gc;
+      }
+      const bool valid = inb && y < p.out_vr && x < p.out_vc;
+      const bool write = valid || (inb && p.zero_pad);
+      float* dst = p.out + (long long)pos * p.cout;
+      const float* md = p.mul_dact ? p.mul_dact + (long long)pos * p.cout : nullptr;
+      for (int c0 = 0; c0 < p.cout; c0 += 16) {
+        float v[16];
+        ptx::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * p.npad + c0, v);
+        if (write) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int co = c0 + j;
+            if (co < p.cout) {
+              float o = 0.f;
+              if (valid) {
+                o = v[j] + (p.bias ? p.bias[co] : 0.f);
+                o = act_f(p.act, o);
+                if (md) o *= act_d(p.dact, md[co]);
+                if (p.round_out) o = tf32r(o);
+              }
+              dst[co] = o;
+            }
+          }
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) ptx::tmem_dealloc(tmem, p.tmem_cols);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_once;
+
+cudaError_t get_encoder() {
+  cudaError_t err = cudaSuccess;
+  std::call_once(g_once, [&]() {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    err = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (err == cudaSuccess && q == cudaDriverEntryPointSuccess) g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  });
+  if (!g_encode) return cudaErrorNotSupported;
+  return cudaSuccess;
+}
+
+// 2-D fp32 tensor [rows][cols] (cols contiguous), box {32 cols, box_rows}, SW128.
+cudaError_t make_map(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+  cudaError_t e = get_encoder();
+  if (e != cudaSuccess) return e;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 4};
+  cuuint32_t box[2] = {(cuuint32_t)kKC, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+int base_mode() {
+  const char* e = getenv("MPF_TC_BASE_MODE");
+  return e ? atoi(e) : 0;  // measured: the swizzle is address-based, base offset 0
+}
+
+template <int NACC>
+cudaError_t launch_nacc(const CUtensorMap& A, const CUtensorMap& B, ConvTcParams& p, size_t smem, int tiles,
+                        cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  conv_tc_kernel<NACC><<<tiles, kThreads, smem, s>>>(A, B, p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool tc_supported(int cin, int cout, int k) {
+  if (getenv("MPF_DISABLE_TC")) return false;
+  return cin % 4 == 0 && cin >= 24 && cout >= 1 && cout <= 256 && k >= 1 && k <= 8;
+}
+
+cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s) {
+  ConvTcParams p{};
+  p.P_tot = a.n_frag * a.gr * a.gc;
+  p.gr = a.gr;
+  p.gc = a.gc;
+  p.out_vr = a.out_vr;
+  p.out_vc = a.out_vc;
+  p.cin = a.cin;
+  p.cout = a.cout;
+  p.npad = (a.cout + 15) / 16 * 16;
+  p.k = a.k;
+  p.shift_rows = a.shift * (a.gc + 1);
+  p.n_cc = (a.cin + kKC - 1) / kKC;
+  p.act = a.act;
+  p.round_out = a.round_out;
+  p.zero_pad = a.zero_pad;
+  p.dact = a.dact;
+  p.bias = a.bias;
+  p.out = a.out;
+  p.mul_dact = a.mul_dact;
+  p.base_mode = base_mode();
+  int nacc = 512 / p.npad;
+  if (nacc > 4) nacc = 4;
+  if (nacc < 1) nacc = 1;
+  const int m_cta = nacc * 128;
+  const int rows_needed = m_cta + a.k - 1;
+  p.nbox = (rows_needed + 255) / 256;
+  p.box_rows = ((rows_needed + p.nbox - 1) / p.nbox + 7) / 8 * 8;
+  p.a_slot_bytes = (uint32_t)(p.nbox * p.box_rows * 128);
+  p.b_slot_bytes = (uint32_t)(p.npad * 128);
+  const size_t budget = 225 * 1024 - 1024 - 256;
+  int nb = (int)((budget - 2 * (size_t)p.a_slot_bytes) / p.b_slot_bytes);
+  if (nb > 6) nb = 6;
+  if (nb < 2) return cudaErrorInvalidConfiguration;
+  p.n_bslots = nb;
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(nacc * p.npad)) cols <<= 1;
+  p.tmem_cols = cols;
+  const size_t smem = 1024 + 2 * (size_t)p.a_slot_bytes + (size_t)nb * p.b_slot_bytes + 256;
+  CUtensorMap A, B;
+  cudaError_t e = make_map(&A, a.x, (uint64_t)a.cin, (uint64_t)p.P_tot, (uint32_t)p.box_rows);
+  if (e != cudaSuccess) return e;
+  e = make_map(&B, a.w, (uint64_t)a.k * a.k * a.cin, (uint64_t)a.cout, (uint32_t)p.npad);
+  if (e != cudaSuccess) return e;
+  const int tiles = (p.P_tot + m_cta - 1) / m_cta;
+  switch (nacc) {
+    case 1: return launch_nacc<1>(A, B, p, smem, tiles, s);
+    case 2: return launch_nacc<2>(A, B, p, smem, tiles, s);
+    case 3: return launch_nacc<3>(A, B, p, smem, tiles, s);
+    default: return launch_nacc<4>(A, B, p, smem, tiles, s);
+  }
+}
+
+// ============================================================================ wgrad
+// dW[co][(ky,kx,ci)] = sum_p dY[p][co] * X[p + ky*gc + kx][ci]  (Alg. 2: the sum over
+// every fragment and position is the K-reduction of this GEMM).
+//
+// M = 128 output channels (A = dY tile, MN-major: co contiguous, one TMA box of 32 co x R
+// positions per 32-channel atom), N = 32 k (B = one X "slab" of R + 8 positions x 32
+// input channels for one (ky, ci chunk); the k taps kx are k MN-atoms of that same slab,
+// one row (128 B) apart: LBO = 128 B), K = positions, 8 per instruction.  A CTA owns G
+// such (ky, ci-chunk) groups (G * 32k <= 512 TMEM columns) of one 128-channel tile, and
+// one contiguous split of the positions; its partial sums go to part[split] and a
+// fixed-order reduction adds them to the gradient (deterministic, no atomics).
+namespace {
+
+constexpr int kWR = 64;  // positions per stage
+
+struct WgTcParams {
+  int P_tot, gc, cin, cout, k, n_cc, n_groups, G, n_sets, m_tiles;
+  int chunk_stages;      // stages (of kWR positions) per split
+  float* part;           // [splits][cout][k*k*cin]
+  uint32_t a_bytes, b_bytes, stage_bytes;
+  int n_stages_ring;
+  uint32_t tmem_cols;
+};
+
+template <int dummy>
+__global__ void __launch_bounds__(kThreads, 1)
+    wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX, WgTcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t sbase = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t sBar = sbase + p.n_stages_ring * p.stage_bytes;
+  const uint32_t barFull = sBar, barEmpty = sBar + 8 * p.n_stages_ring, barT = sBar + 16 * p.n_stages_ring;
+  const uint32_t sTmemSlot = barT + 8;
+  uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (sTmemSlot - ptx::smem_u32(smem_raw)));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // block -> (m tile, group set, split); neighbouring blocks share a split (L2 reuse)
+  const int mt = blockIdx.x % p.m_tiles;
+  const int set = (blockIdx.x / p.m_tiles) % p.n_sets;
+  const int split = blockIdx.x / (p.m_tiles * p.n_sets);
+  const int g0 = set * p.G;
+  const int G = min(p.G, p.n_groups - g0);
+  const int N = 32 * p.k;
+  const long long pbeg = (long long)split * p.chunk_stages * kWR;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmD);
+    ptx::prefetch_tmap(&tmX);
+    for (int i = 0; i < p.n_stages_ring; ++i) {
+      ptx::mbar_init(barFull + 8 * i, 1);
+      ptx::mbar_init(barEmpty + 8 * i, 1);
+    }
+    ptx::mbar_init(barT, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(sTmemSlot, p.tmem_cols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot_ptr;
+  const int n_st = p.chunk_stages;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int st = 0; st < n_st; ++st) {
+        const int slot = st % p.n_stages_ring;
+        ptx::mbar_wait(barEmpty + 8 * slot, ((st / p.n_stages_ring) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(barFull + 8 * slot, p.a_bytes + G * p.b_bytes);
+        const uint32_t sa = sbase + slot * p.stage_bytes;
+        const int row = (int)(pbeg + (long long)st * kWR);
+        for (int j = 0; j < 4; ++j)  // 4 atoms of 32 output channels
+          ptx::tma_load_2d(sa + j * kWR * 128, &tmD, barFull + 8 * slot, mt * 128 + j * 32, row);
+        for (int g = 0; g < G; ++g) {
+          const int ng = g0 + g, ky = ng / p.n_cc, cc = ng % p.n_cc;
+          ptx::tma_load_2d(sa + p.a_bytes + g * p.b_bytes, &tmX, barFull + 8 * slot, cc * kKC, row + ky * p.gc);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = ptx::idesc_tf32_mn(128, N);
+    for (int st = 0; st < n_st; ++st) {
+      const int slot = st % p.n_stages_ring;
+      ptx::mbar_wait(barFull + 8 * slot, (st / p.n_stages_ring) & 1);
+      ptx::tc_fence_after();
+      if (lane == 0) {
+        const uint32_t sa = sbase + slot * p.stage_bytes;
+        for (int g = 0; g < G; ++g) {
+          const uint32_t sb = sa + p.a_bytes + g * p.b_bytes;
+#pragma unroll
+          for (int r8 = 0; r8 < kWR / 8; ++r8) {
+            const uint64_t ad = ptx::sdesc_mn_sw128_32b(sa + r8 * 1024, kWR * 128, 512);
+            const uint64_t bd = ptx::sdesc_mn_sw128_32b(sb + r8 * 1024, 128, 512);
+            ptx::mma_tf32(tmem + g * N, ad, bd, idesc, (st | r8) != 0);
+          }
+        }
+        ptx::mma_commit(barEmpty + 8 * slot);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) ptx::mma_commit(barT);
+    __syncwarp();
+  } else {
+    const int q = warp & 3;
+    const int co = mt * 128 + q * 32 + lane;
+    ptx::mbar_wait(barT, 0);
+    ptx::tc_fence_after();
+    const int K = p.k * p.k * p.cin;
+    float* dst = p.part + ((long long)split * p.cout + co) * K;
+    for (int g = 0; g < G; ++g) {
+      const int ng = g0 + g, ky = ng / p.n_cc, cc = ng % p.n_cc;
+      for (int c0 = 0; c0 < N; c0 += 16) {
+        float v[16];
+        ptx::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + g * N + c0, v);
+        if (co < p.cout) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int n = c0 + j, kx = n / 32, ci = cc * kKC + (n % 32);
+            if (ci < p.cin) dst[(ky * p.k + kx) * p.cin + ci] = n_st > 0 ? v[j] : 0.f;
+          }
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) ptx::tmem_dealloc(tmem, p.tmem_cols);
+}
+
+// part_b[s][co] = sum over the rows of split s of dY[p][co] (fixed order)
+__global__ void channel_sum_kernel(const float* __restrict__ dy, long long P, int C, long long rows_per_split,
+                                   float* part_b) {
+  __shared__ float red[256];
+  const int s = blockIdx.x;
+  const long long r0 = (long long)s * rows_per_split;
+  const long long r1 = min(P, r0 + rows_per_split);
+  const int lanes_per_row = C;  // one thread per channel, rows strided by the row-groups
+  const int groups = max(1, 256 / lanes_per_row);
+  const int c = threadIdx.x % C, grp = threadIdx.x / C;
+  float acc = 0.f;
+  if (grp < groups)
+    for (long long r = r0 + grp; r < r1; r += groups) acc += dy[r * C + c];
+  red[threadIdx.x] = (grp < groups) ? acc : 0.f;
+  __syncthreads();
+  if (threadIdx.x < C) {
+    float t = 0.f;
+    for (int g = 0; g < groups; ++g) t += red[g * C + threadIdx.x];
+    part_b[(long long)s * C + threadIdx.x] = t;
+  }
+}
+
+}  // namespace
+
+bool tc_wgrad_supported(int cin, int cout, int k) {
+  if (getenv("MPF_DISABLE_TC")) return false;
+  return cin % 4 == 0 && cin >= 8 && cout % 4 == 0 && cout <= 256 && k >= 1 && k <= 8;
+}
+
+cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits_out, cudaStream_t s) {
+  WgTcParams p{};
+  p.P_tot = a.n_frag * a.gr * a.gc;
+  p.gc = a.gc;
+  p.cin = a.cin;
+  p.cout = a.cout;
+  p.k = a.k;
+  p.n_cc = (a.cin + kKC - 1) / kKC;
+  p.n_groups = a.k * p.n_cc;
+  const int N = 32 * a.k;
+  p.G = 512 / N;
+  if (p.G > p.n_groups) p.G = p.n_groups;
+  p.n_sets = (p.n_groups + p.G - 1) / p.G;
+  p.m_tiles = (a.cout + 127) / 128;
+  p.a_bytes = 4 * kWR * 128;
+  p.b_bytes = (kWR + 8) * 128;
+  p.stage_bytes = p.a_bytes + p.G * p.b_bytes;
+  const size_t budget = 225 * 1024 - 1024 - 256;
+  p.n_stages_ring = (int)(budget / p.stage_bytes);
+  if (p.n_stages_ring > 4) p.n_stages_ring = 4;
+  if (p.n_stages_ring < 2) {  // shrink G until two stages fit
+    while (p.G > 1 && 2 * (p.a_bytes + p.G * p.b_bytes) > budget) --p.G;
+    p.n_sets = (p.n_groups + p.G - 1) / p.G;
+    p.stage_bytes = p.a_bytes + p.G * p.b_bytes;
+    p.n_stages_ring = 2;
+  }
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(p.G * N)) cols <<= 1;
+  p.tmem_cols = cols;
+  const long long total_stages = (p.P_tot + kWR - 1) / kWR;
+  const int per_split_blocks = p.m_tiles * p.n_sets;
+  int splits = (int)((2 * 148 + per_split_blocks - 1) / per_split_blocks);
+  if (splits > kMaxSplits) splits = kMaxSplits;
+  if (splits < 1) splits = 1;
+  const size_t K = (size_t)a.k * a.k * a.cin;
+  while (splits > 1 && (size_t)splits * (a.cout * K + a.cout) > a.part_cap_floats) --splits;
+  if (splits > total_stages) splits = (int)total_stages;
+  p.chunk_stages = (int)((total_stages + splits - 1) / splits);
+  splits = (int)((total_stages + p.chunk_stages - 1) / p.chunk_stages);
+  p.part = a.part;
+  *splits_out = splits;
+  CUtensorMap D, X;
+  cudaError_t e = make_map(&D, a.dy, (uint64_t)a.cout, (uint64_t)p.P_tot, (uint32_t)kWR,
+                           CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  if (e != cudaSuccess) return e;
+  e = make_map(&X, a.x, (uint64_t)a.cin, (uint64_t)p.P_tot, (uint32_t)(kWR + 8), CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  if (e != cudaSuccess) return e;
+  const size_t smem = 1024 + (size_t)p.n_stages_ring * p.stage_bytes + 256;
+  e = cudaFuncSetAttribute(wgrad_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  wgrad_tc_kernel<0><<<splits * per_split_blocks, kThreads, smem, s>>>(D, X, p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  // bias partials over the same splits
+  const long long rows_per_split = (long long)p.chunk_stages * kWR;
+  channel_sum_kernel<<<splits, 256, 0, s>>>(a.dy, (long long)p.P_tot, a.cout, rows_per_split,
+                                            a.part + (size_t)splits * a.cout * K);
+  return cudaGetLastError();
+}
 
 }  // namespace mpf

@@ -40,6 +40,7 @@ struct TcWgradArgs {
 };
 
 bool tc_supported(int cin, int cout, int k);
+bool tc_wgrad_supported(int cin, int cout, int k);
 cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s);
 cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits, cudaStream_t s);
 

@@ -8,6 +8,7 @@
 //   SGD
 #include <cuda_runtime.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -220,7 +221,10 @@ static const float* act_ptr(const Net* N, int l) {
   return nullptr;
 }
 
+static bool fwd_round_off() { return getenv("MPF_DEBUG_FWD_FP32") != nullptr; }
+
 static bool use_tc(const Net* N, const LayerPlan& P, bool dgrad) {
+  if (!dgrad && fwd_round_off()) return false;
   if (N->cfg.precision != MPF_PREC_TF32) return false;
   return tc_supported(dgrad ? P.cout : P.cin, dgrad ? P.cin : P.cout, P.L.k);
 }
@@ -376,7 +380,7 @@ mpf_status mpf_forward_image(mpf_net* N, const float* d_images, int32_t n, float
     const double nw = (double)P.cout * P.cin * P.L.k * P.L.k;
     LAUNCH(N, s, "pack_weights", l, 0.0, 12.0 * nw,
            launch_pack_weights(N->params + P.w_off, P.cout, P.cin, P.L.k, wpack + P.wpack_off,
-                               wpack + P.dpack_off, tf32 ? 1 : 0, s));
+                               wpack + P.dpack_off, (tf32 && !fwd_round_off()) ? 1 : 0, s));
   }
   // 2. layers (Alg. 1; Alg. 3 for MPF)
   for (int l = 0; l < N->n_layers - 1; ++l) {
@@ -410,7 +414,8 @@ mpf_status mpf_forward_image(mpf_net* N, const float* d_images, int32_t n, float
         t.x = x; t.n_frag = n * in.F; t.gr = in.gr; t.gc = in.gc; t.cin = P.cin;
         t.w = wpack + P.wpack_off; t.bias = N->params + P.b_off; t.k = P.L.k; t.cout = P.cout;
         t.out = out; t.out_vr = o.vr; t.out_vc = o.vc; t.act = P.L.act; t.shift = 0;
-        t.round_out = next_tc ? 1 : 0; t.zero_pad = 0; t.mul_dact = nullptr;
+        t.round_out = next_tc ? 1 : 0; t.mul_dact = nullptr;
+        t.zero_pad = P.out_where == Where::Tape ? 1 : 0;  // tape tensors are read whole by the TC wgrad
         LAUNCH(N, s, "conv_fwd_tc", l, cflops, cbytes, launch_conv_tc(t, s));
       } else {
         ConvArgs c{};
@@ -434,7 +439,7 @@ mpf_status mpf_forward_image(mpf_net* N, const float* d_images, int32_t n, float
         c.act = P.L.act;
         c.mul_dact = nullptr;
         c.dact = 0;
-        c.zero_pad = 0;
+        c.zero_pad = P.out_where == Where::Tape ? 1 : 0;
         c.round_tf32 = next_tc ? 1 : 0;
         c.n_frag_total = n * in.F;
         LAUNCH(N, s, "conv_fwd_simt", l, cflops, cbytes, launch_conv_simt(c, s));
@@ -477,7 +482,7 @@ static mpf_status wgrad(Net* N, int l, const float* x, const float* dy, int n, c
   const double in_e = (l == 0) ? (double)n * N->cfg.in_channels * N->cfg.image_rows * N->cfg.image_cols
                                : (double)n * in.F * in.vr * in.vc * in.C;
   const double wbytes = 4.0 * (in_e + (double)positions * P.cout);
-  if (l > 0 && use_tc(N, P, false)) {
+  if (l > 0 && N->cfg.precision == MPF_PREC_TF32 && tc_wgrad_supported(P.cin, P.cout, P.L.k)) {
     TcWgradArgs t{};
     t.x = x; t.dy = dy; t.n_frag = n * in.F; t.gr = in.gr; t.gc = in.gc; t.vr_out = o.vr; t.vc_out = o.vc;
     t.cin = P.cin; t.cout = P.cout; t.k = P.L.k;
