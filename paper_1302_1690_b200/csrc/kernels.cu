@@ -524,7 +524,7 @@ cudaError_t launch_sgd(float* params, float* grads, long long n, float lr, float
 
 // canonical W[co][ci][ky][kx] -> fwd pack [co][ky][kx][ci], dgrad pack [ci][k-1-ky][k-1-kx][co]
 __global__ void pack_kernel(const float* __restrict__ w, int cout, int cin, int k, float* wp, float* dp,
-                            int round_tf32) {
+                            int round_fwd, int round_dgrad) {
   const long long n = (long long)cout * cin * k * k;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
        e += (long long)gridDim.x * blockDim.x) {
@@ -534,18 +534,17 @@ __global__ void pack_kernel(const float* __restrict__ w, int cout, int cin, int 
     t /= k;
     const int ci = (int)(t % cin);
     const int co = (int)(t / cin);
-    float v = w[e];
-    if (round_tf32) v = tf32_rna(v);
-    wp[(((long long)co * k + ky) * k + kx) * cin + ci] = v;
-    if (dp) dp[(((long long)ci * k + (k - 1 - ky)) * k + (k - 1 - kx)) * cout + co] = v;
+    const float v = w[e];
+    wp[(((long long)co * k + ky) * k + kx) * cin + ci] = round_fwd ? tf32_rna(v) : v;
+    if (dp) dp[(((long long)ci * k + (k - 1 - ky)) * k + (k - 1 - kx)) * cout + co] = round_dgrad ? tf32_rna(v) : v;
   }
 }
 
-cudaError_t launch_pack_weights(const float* w, int cout, int cin, int k, float* wp, float* dp, int round_tf32,
-                                cudaStream_t s) {
+cudaError_t launch_pack_weights(const float* w, int cout, int cin, int k, float* wp, float* dp, int round_fwd,
+                                int round_dgrad, cudaStream_t s) {
   const long long n = (long long)cout * cin * k * k;
   const int blocks = (int)mpf_min_ll((n + 255) / 256, 1024);
-  pack_kernel<<<blocks, 256, 0, s>>>(w, cout, cin, k, wp, dp, round_tf32);
+  pack_kernel<<<blocks, 256, 0, s>>>(w, cout, cin, k, wp, dp, round_fwd, round_dgrad);
   return cudaGetLastError();
 }
 

@@ -378,9 +378,12 @@ mpf_status mpf_forward_image(mpf_net* N, const float* d_images, int32_t n, float
     const LayerPlan& P = N->lp[l];
     if (P.L.kind == MPF_POOL) continue;
     const double nw = (double)P.cout * P.cin * P.L.k * P.L.k;
+    // tf32-round a pack only when a tensor-core kernel consumes it; CUDA-core convs use fp32
+    const int rf = (l > 0 && l < N->n_layers - 1 && use_tc(N, P, false)) ? 1 : 0;
+    const int rd = (l > 0 && use_tc(N, P, true)) ? 1 : 0;
     LAUNCH(N, s, "pack_weights", l, 0.0, 12.0 * nw,
            launch_pack_weights(N->params + P.w_off, P.cout, P.cin, P.L.k, wpack + P.wpack_off,
-                               wpack + P.dpack_off, (tf32 && !fwd_round_off()) ? 1 : 0, s));
+                               wpack + P.dpack_off, rf, rd, s));
   }
   // 2. layers (Alg. 1; Alg. 3 for MPF)
   for (int l = 0; l < N->n_layers - 1; ++l) {

@@ -181,7 +181,7 @@ cudaError_t launch_loss_finalize(const float* loss_part, int parts, const int* n
                                  cudaStream_t s);
 cudaError_t launch_sgd(float* params, float* grads, long long n, float lr, float scale, cudaStream_t s);
 cudaError_t launch_pack_weights(const float* w_canon, int cout, int cin, int k, float* wpack, float* dpack,
-                                int round_tf32, cudaStream_t s);
+                                int round_fwd, int round_dgrad, cudaStream_t s);
 cudaError_t launch_frag2pix(const float* frag, float* pix, int n, int C, int F, int fr, int fc, int O_H,
                             int O_W, int n_levels, const int* pool_k, cudaStream_t s);
 cudaError_t launch_compact_copy(const float* src, int gr, int gc, int vr, int vc, int C, long long nf,
