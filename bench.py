@@ -188,6 +188,7 @@ def main():
 
     import torch
     import torch.distributed as dist
+    from paper_1302_1690_b200 import dist as D
     from paper_1302_1690_b200.net import MPFNet
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -202,7 +203,7 @@ def main():
     # two global batches of this rank's shard, resident in HBM (inputs cycle between steps)
     pools = []
     for b in range(2):
-        idx = [b * B + rank * per + i for i in range(per)]
+        idx = D.batch_indices(b, B, world, rank)
         im, lb = S.make_batch(cfg, idx)
         pools.append((torch.tensor(im, device=dev).contiguous(), torch.tensor(lb, device=dev).contiguous(), im, lb))
     counts = []  # labelled pixels of each global batch (all ranks)
@@ -217,8 +218,7 @@ def main():
         im, lb = pools[i % 2][0], pools[i % 2][1]
         net.forward(im)
         net.backward(lb)
-        if world > 1:
-            dist.all_reduce(net.grads)
+        D.allreduce_grads(net.grads)
         net.sgd_step(cfg.lr, 1.0 / B)
 
     for i in range(args.warmup):
@@ -265,7 +265,7 @@ def main():
             hi, hl = h_pools[i % 2]
             net.train_step_host(hi, hl, h_loss, apply_sgd=(world == 1), lr=cfg.lr, grad_scale=1.0 / B)
             if world > 1:
-                dist.all_reduce(net.grads)
+                D.allreduce_grads(net.grads)
                 net.sgd_step(cfg.lr, 1.0 / B)
 
         for i in range(max(1, args.warmup)):
