@@ -1,0 +1,288 @@
+// conv_first.cu — the first convolution layer (one input map: the raw image), forward
+// and weight gradient, on CUDA cores in fp32.
+//
+// Alg. 1 for the first layer: the input storage holds a single
+// fragment, the zero-padded image (reading R7 padding), so the first layer
+// is one valid k x k cross-correlation (R10) per image, + bias + tanh.
+// With C_in = 1 the GEMM K dimension is only k^2 (9..49), far too thin for the tensor
+// cores to pay; the layer is bound by its fp32 output stream (forward) and its delta
+// stream (wgrad), so both kernels stage the image tile in shared memory and use
+// register-blocked outer products (4 positions x 8 maps forward; 8 maps x 4 taps
+// wgrad) to stay near the FFMA/HBM ceilings.
+//
+// Weight gradient (Alg. 2): dW[co][ky][kx] = sum over every position
+// p of the image of dY[p][co] * img[p + (ky, kx)], with dY zero outside the valid
+// region.  Persistent CTAs accumulate in registers over their tiles and write one
+// partial per CTA; a fixed-order reduction finishes the sum (deterministic).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "mpf_internal.h"
+
+namespace mpf {
+
+namespace {
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__device__ __forceinline__ float act_fwd(int act, float v) {
+  if (act == MPF_TANH) return tanhf(v);
+  if (act == MPF_LOGISTIC) return 1.f / (1.f + expf(-v));
+  return v;
+}
+
+constexpr int kFTH = 16, kFTW = 16;  // forward tile (positions)
+constexpr int kFPX = 4;              // positions per thread (horizontal strip)
+constexpr int kFCO = 8;              // maps per thread
+
+// blockDim.x = 64 strips x n_cog channel groups
+template <int K>
+__global__ void __launch_bounds__(256) conv_first_fwd_kernel(FirstConvArgs a) {
+  extern __shared__ float sm[];
+  constexpr int IW = kFTW + K - 1, IH = kFTH + K - 1;
+  const int coutp = a.n_cog * kFCO;
+  constexpr int IMG = (IH * IW + 3) / 4 * 4;  // keep the float4 tiles 16-B aligned
+  float* s_img = sm;                 // [IH][IW]
+  float* s_w = sm + IMG;             // [K*K][coutp]
+  float* s_b = s_w + K * K * coutp;  // [coutp]
+  const int img = blockIdx.z;
+  const int y0 = blockIdx.y * kFTH, x0 = blockIdx.x * kFTW;
+  for (int e = threadIdx.x; e < IH * IW; e += blockDim.x) {
+    const int iy = e / IW, ix = e % IW;
+    const int gy = y0 + iy, gx = x0 + ix;
+    float v = 0.f;
+    if (gy < a.H && gx < a.W) v = a.img[((size_t)img * a.H + gy) * a.W + gx];
+    s_img[e] = v;
+  }
+  for (int e = threadIdx.x; e < K * K * coutp; e += blockDim.x) {
+    const int co = e % coutp, t = e / coutp;
+    s_w[e] = co < a.cout ? a.w[co * K * K + t] : 0.f;  // canonical W[co][0][ky][kx]
+  }
+  for (int e = threadIdx.x; e < coutp; e += blockDim.x) s_b[e] = e < a.cout ? a.bias[e] : 0.f;
+  __syncthreads();
+  const int cog = threadIdx.x % a.n_cog, strip = threadIdx.x / a.n_cog;
+  const int ty = strip / (kFTW / kFPX), tx = (strip % (kFTW / kFPX)) * kFPX;
+  float acc[kFPX][kFCO];
+#pragma unroll
+  for (int q = 0; q < kFPX; ++q)
+#pragma unroll
+    for (int o = 0; o < kFCO; ++o) acc[q][o] = 0.f;
+#pragma unroll
+  for (int ky = 0; ky < K; ++ky) {
+    float row[kFPX + K - 1];
+#pragma unroll
+    for (int i = 0; i < kFPX + K - 1; ++i) row[i] = s_img[(ty + ky) * IW + tx + i];
+#pragma unroll
+    for (int kx = 0; kx < K; ++kx) {
+      const float4* wp = reinterpret_cast<const float4*>(s_w + (ky * K + kx) * coutp + cog * kFCO);
+      const float4 w0 = wp[0], w1 = wp[1];
+      const float wv[kFCO] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+      for (int q = 0; q < kFPX; ++q)
+#pragma unroll
+        for (int o = 0; o < kFCO; ++o) acc[q][o] = fmaf(row[q + kx], wv[o], acc[q][o]);
+    }
+  }
+  const int y = y0 + ty;
+  if (y >= a.out_gr) return;
+#pragma unroll
+  for (int q = 0; q < kFPX; ++q) {
+    const int x = x0 + tx + q;
+    if (x >= a.out_gc) continue;
+    const bool valid = y < a.out_vr && x < a.out_vc;
+    if (!valid && !a.zero_pad) continue;
+    float* dst = a.out + (((size_t)img * a.out_gr + y) * a.out_gc + x) * a.cout + cog * kFCO;
+    float v[kFCO];
+#pragma unroll
+    for (int o = 0; o < kFCO; ++o) {
+      float t = 0.f;
+      if (valid) {
+        t = act_fwd(a.act, acc[q][o] + s_b[cog * kFCO + o]);
+        if (a.round_tf32) t = tf32_rna(t);
+      }
+      v[o] = t;
+    }
+    if (a.cout % kFCO == 0) {
+      reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
+      reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
+    } else {
+#pragma unroll
+      for (int o = 0; o < kFCO; ++o)
+        if (cog * kFCO + o < a.cout) dst[o] = v[o];
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------ wgrad
+constexpr int kWTH = 8, kWTW = 32;  // wgrad tile: 256 positions
+constexpr int kWCO = 8, kWT = 4;    // accumulators per thread: 8 maps x 4 taps
+
+template <int K>
+__global__ void __launch_bounds__(256) conv_first_wgrad_kernel(FirstWgradArgs a) {
+  extern __shared__ float sm[];
+  constexpr int IW = kWTW + K - 1, IH = kWTH + K - 1;
+  constexpr int NT = (K * K + kWT - 1) / kWT;  // tap groups
+  const int coutp = a.n_cog * kWCO;
+  constexpr int IMG = (IH * IW + 3) / 4 * 4;
+  float* s_img = sm;             // [IH][IW]
+  float* s_dy = sm + IMG;        // [kWTH*kWTW][coutp]
+  float* s_red = s_dy;           // end-of-kernel reduction (aliases the delta tile)
+  const int per_stream = a.n_cog * NT;
+  const int n_streams = blockDim.x / per_stream;
+  const int stream = threadIdx.x / per_stream, r = threadIdx.x % per_stream;
+  const int cog = r % a.n_cog, tg = r / a.n_cog;
+  const bool active = stream < n_streams;
+  int toff[kWT];
+#pragma unroll
+  for (int u = 0; u < kWT; ++u) {
+    const int t = tg * kWT + u;
+    toff[u] = t < K * K ? (t / K) * IW + (t % K) : 0;
+  }
+  float acc[kWCO][kWT];
+#pragma unroll
+  for (int o = 0; o < kWCO; ++o)
+#pragma unroll
+    for (int u = 0; u < kWT; ++u) acc[o][u] = 0.f;
+  const int tiles_x = (a.gc + kWTW - 1) / kWTW, tiles_y = (a.gr + kWTH - 1) / kWTH;
+  const long long total = (long long)a.n * tiles_x * tiles_y;
+  for (long long tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    const int tx_ = (int)(tile % tiles_x);
+    const long long t2 = tile / tiles_x;
+    const int ty_ = (int)(t2 % tiles_y), img = (int)(t2 / tiles_y);
+    const int y0 = ty_ * kWTH, x0 = tx_ * kWTW;
+    __syncthreads();
+    for (int e = threadIdx.x; e < IH * IW; e += blockDim.x) {
+      const int iy = e / IW, ix = e % IW;
+      const int gy = y0 + iy, gx = x0 + ix;
+      float v = 0.f;
+      if (gy < a.H && gx < a.W) v = a.img[((size_t)img * a.H + gy) * a.W + gx];
+      s_img[e] = v;
+    }
+    // delta tile [256 positions][cout] (zero outside the grid); rows of cout floats
+    for (int e = threadIdx.x; e < kWTH * kWTW * coutp; e += blockDim.x) {
+      const int co = e % coutp, p = e / coutp;
+      const int y = y0 + p / kWTW, x = x0 + p % kWTW;
+      float v = 0.f;
+      if (co < a.cout && y < a.gr && x < a.gc) v = a.dy[(((size_t)img * a.gr + y) * a.gc + x) * a.cout + co];
+      s_dy[e] = v;
+    }
+    __syncthreads();
+    if (active) {
+      for (int p = stream; p < kWTH * kWTW; p += n_streams) {
+        const int py = p / kWTW, px = p % kWTW;
+        const float4* dp = reinterpret_cast<const float4*>(s_dy + p * coutp + cog * kWCO);
+        const float4 d0 = dp[0], d1 = dp[1];
+        const float dv[kWCO] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+        const float* ib = s_img + py * IW + px;
+        float iv[kWT];
+#pragma unroll
+        for (int u = 0; u < kWT; ++u) iv[u] = ib[toff[u]];
+#pragma unroll
+        for (int o = 0; o < kWCO; ++o)
+#pragma unroll
+          for (int u = 0; u < kWT; ++u) acc[o][u] = fmaf(dv[o], iv[u], acc[o][u]);
+      }
+    }
+  }
+  // fixed-order reduction over streams, then one partial per CTA: part[blk][co][tap]
+  __syncthreads();
+  const int KK = K * K;
+  if (active) {
+#pragma unroll
+    for (int o = 0; o < kWCO; ++o)
+#pragma unroll
+      for (int u = 0; u < kWT; ++u) {
+        const int co = cog * kWCO + o, t = tg * kWT + u;
+        if (t < KK) s_red[(stream * coutp + co) * KK + t] = acc[o][u];
+      }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < a.cout * KK; e += blockDim.x) {
+    float s = 0.f;
+    for (int q = 0; q < n_streams; ++q) s += s_red[q * coutp * KK + e];
+    a.part[(size_t)blockIdx.x * a.cout * KK + e] = s;
+  }
+}
+
+template <int K>
+size_t fwd_smem(int coutp) {
+  return sizeof(float) * (((kFTH + K - 1) * (kFTW + K - 1) + 3) / 4 * 4 + K * K * coutp + coutp);
+}
+
+template <int K>
+cudaError_t fwd_k(const FirstConvArgs& a, cudaStream_t s) {
+  const int coutp = a.n_cog * kFCO;
+  const size_t smem = fwd_smem<K>(coutp);
+  cudaError_t e = cudaFuncSetAttribute(conv_first_fwd_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((a.out_gc + kFTW - 1) / kFTW, (a.out_gr + kFTH - 1) / kFTH, a.n);
+  conv_first_fwd_kernel<K><<<grid, 64 * a.n_cog, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int K>
+size_t wgrad_smem(int n_cog) {
+  const int coutp = n_cog * kWCO;
+  constexpr int NT = (K * K + kWT - 1) / kWT;
+  const int n_streams = 256 / (n_cog * NT);
+  const size_t tile = (size_t)kWTH * kWTW * coutp;
+  const size_t red = (size_t)n_streams * coutp * K * K;
+  return sizeof(float) * (((kWTH + K - 1) * (kWTW + K - 1) + 3) / 4 * 4 + (tile > red ? tile : red));
+}
+
+template <int K>
+cudaError_t wgrad_k(const FirstWgradArgs& a, cudaStream_t s) {
+  const size_t smem = wgrad_smem<K>(a.n_cog);
+  cudaError_t e = cudaFuncSetAttribute(conv_first_wgrad_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  conv_first_wgrad_kernel<K><<<a.n_blocks, 256, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool first_conv_supported(int cin, int cout, int k) {
+  if (cin != 1 || cout < 1 || cout > 32 || k < 2 || k > 8) return false;
+  const int n_cog = (cout + kFCO - 1) / kFCO;
+  const int NT = (k * k + kWT - 1) / kWT;
+  return n_cog * NT <= 256;
+}
+
+int first_wgrad_blocks() { return 148 * 2; }
+
+cudaError_t launch_first_conv(FirstConvArgs a, cudaStream_t s) {
+  a.n_cog = (a.cout + kFCO - 1) / kFCO;
+  switch (a.k) {
+    case 2: return fwd_k<2>(a, s);
+    case 3: return fwd_k<3>(a, s);
+    case 4: return fwd_k<4>(a, s);
+    case 5: return fwd_k<5>(a, s);
+    case 6: return fwd_k<6>(a, s);
+    case 7: return fwd_k<7>(a, s);
+    case 8: return fwd_k<8>(a, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_first_wgrad(FirstWgradArgs a, cudaStream_t s) {
+  a.n_cog = (a.cout + kWCO - 1) / kWCO;
+  switch (a.k) {
+    case 2: return wgrad_k<2>(a, s);
+    case 3: return wgrad_k<3>(a, s);
+    case 4: return wgrad_k<4>(a, s);
+    case 5: return wgrad_k<5>(a, s);
+    case 6: return wgrad_k<6>(a, s);
+    case 7: return wgrad_k<7>(a, s);
+    case 8: return wgrad_k<8>(a, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace mpf

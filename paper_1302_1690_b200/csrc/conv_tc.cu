@@ -444,28 +444,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) ptx::tmem_dealloc(tmem, p.tmem_cols);
 }
 
-// part_b[s][co] = sum over the rows of split s of dY[p][co] (fixed order)
-__global__ void channel_sum_kernel(const float* __restrict__ dy, long long P, int C, long long rows_per_split,
-                                   float* part_b) {
-  __shared__ float red[256];
-  const int s = blockIdx.x;
-  const long long r0 = (long long)s * rows_per_split;
-  const long long r1 = min(P, r0 + rows_per_split);
-  const int lanes_per_row = C;  // one thread per channel, rows strided by the row-groups
-  const int groups = max(1, 256 / lanes_per_row);
-  const int c = threadIdx.x % C, grp = threadIdx.x / C;
-  float acc = 0.f;
-  if (grp < groups)
-    for (long long r = r0 + grp; r < r1; r += groups) acc += dy[r * C + c];
-  red[threadIdx.x] = (grp < groups) ? acc : 0.f;
-  __syncthreads();
-  if (threadIdx.x < C) {
-    float t = 0.f;
-    for (int g = 0; g < groups; ++g) t += red[g * C + threadIdx.x];
-    part_b[(long long)s * C + threadIdx.x] = t;
-  }
-}
-
 }  // namespace
 
 bool tc_wgrad_supported(int cin, int cout, int k) {
@@ -524,12 +502,6 @@ cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits_out, cudaStream_t 
   e = cudaFuncSetAttribute(wgrad_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   wgrad_tc_kernel<0><<<splits * per_split_blocks, kThreads, smem, s>>>(D, X, p);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  // bias partials over the same splits
-  const long long rows_per_split = (long long)p.chunk_stages * kWR;
-  channel_sum_kernel<<<splits, 256, 0, s>>>(a.dy, (long long)p.P_tot, a.cout, rows_per_split,
-                                            a.part + (size_t)splits * a.cout * K);
   return cudaGetLastError();
 }
 

@@ -29,7 +29,6 @@ struct TcConvArgs {
 };
 
 // Weight gradient: part[s][co][(ky*k+kx)*cin+ci] = sum_{p in split s} dy[p][co] * x[p+(ky,kx)][ci]
-// followed by part_b[s][co] at part + splits*cout*K.
 struct TcWgradArgs {
   const float* x;
   const float* dy;    // [n_frag][gr][gc][cout], zero outside the valid region

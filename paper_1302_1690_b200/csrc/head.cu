@@ -1,0 +1,325 @@
+// head.cu — the softmax FC (1x1, linear) + per-pixel softmax + class-weighted MCCE +
+// dL/dx_hat, and the whole back-propagation through that layer, in one pass over the
+// last hidden activation h ("first dL/dx_hat", 197 MCCE per pixel,
+// 252 per-class weights; readings R8, R9, R15).
+//
+// Per position p (fragment-major; the label is fetched through the fragment -> pixel
+// map, R2/R7; positions outside the O_H x O_W output grid and label 255 are ignored):
+//     z = W_L h + b_L,  p = softmax(z),  loss += w_t (lse - z_t)
+//     dz = w_t (p - onehot_t) / n_lab(img)
+//     dh = (W_L^T dz) * act'(h)                 -> written (delta of the previous layer)
+//     dW_L += dz h^T,  db_L += dz,  db_prev += dh   (Alg. 2: sums over all fragments)
+// The three sums are per-block register partials finished by a fixed-order reduction,
+// so the softmax layer needs no separate weight-gradient pass and the previous layer
+// needs no separate bias pass.
+//
+// Schedule: persistent CTAs (one per SM slot) walk tiles of TP positions.  A tile of h
+// is TP*Ch contiguous floats: one TMA bulk copy into a double-buffered shared buffer,
+// issued one tile ahead.  Phase A: one warp per position, lanes split the Ch-long dot
+// products and combine them with an xor butterfly (bit-identical on every lane).
+// Phase B: thread = (channel ch, position stream); W_L[:, ch] sits in registers, dh is
+// written coalesced and the dW/db partials accumulate in registers.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "mpf_internal.h"
+#include "tc_ptx.cuh"
+
+namespace mpf {
+
+namespace {
+
+constexpr int kTP = 64;       // positions per tile
+constexpr int kThr = 256;
+constexpr int kMaxC = 16;
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__device__ __forceinline__ float act_der(int act, float y) {
+  if (act == MPF_TANH) return 1.f - y * y;
+  if (act == MPF_LOGISTIC) return y * (1.f - y);
+  return 1.f;
+}
+
+// bytes of region0: two h tiles, or the end-of-kernel reduction area if larger
+__host__ __device__ inline size_t head_region0(int C, int Ch) {
+  const int nstreams = kThr / Ch;
+  const size_t red = sizeof(float) * ((size_t)nstreams * Ch * (C + 1) + (size_t)nstreams * kMaxC);
+  const size_t tiles = 2 * (size_t)kTP * Ch * sizeof(float);
+  return ((red > tiles ? red : tiles) + 127) / 128 * 128;
+}
+
+template <bool TRAIN>
+__global__ void __launch_bounds__(kThr) head_kernel(HeadArgs a) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  const int C = a.C, Ch = a.Ch;
+  const size_t tile_bytes = (size_t)kTP * Ch * sizeof(float);
+  // [2 mbarriers | pad | region0: two h tiles, later the reduction area | W | b | dl | valid | loss]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+  float* hb0 = reinterpret_cast<float*>(smem_raw + 128);
+  float* hb1 = reinterpret_cast<float*>(smem_raw + 128 + tile_bytes);
+  float* s_w = reinterpret_cast<float*>(smem_raw + 128 + head_region0(C, Ch));
+  float* s_b = s_w + C * Ch;
+  float* s_dl = s_b + kMaxC;
+  int* s_valid = reinterpret_cast<int*>(s_dl + kTP * kMaxC);
+  float* s_loss = reinterpret_cast<float*>(s_valid + kTP);  // [kThr/32]
+  const uint32_t bar0 = ptx::smem_u32(&bars[0]), bar1 = ptx::smem_u32(&bars[1]);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  for (int e = tid; e < C * Ch; e += kThr) s_w[e] = a.w[e];
+  for (int e = tid; e < C; e += kThr) s_b[e] = a.b[e];
+  const long long per_img = (long long)a.F * a.gr * a.gc;
+  const int tpi = a.tiles_per_img;
+  const long long total = (long long)a.n * tpi;
+  if (tid == 0) {
+    ptx::mbar_init(bar0, 1);
+    ptx::mbar_init(bar1, 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto issue = [&](long long tile, int buf) {
+    const int img = (int)(tile / tpi), tt = (int)(tile % tpi);
+    const long long p0 = (long long)tt * kTP;
+    const long long np = min((long long)kTP, per_img - p0);
+    const uint32_t bytes = (uint32_t)(np * Ch * sizeof(float));
+    const uint32_t bar = buf ? bar1 : bar0;
+    ptx::mbar_arrive_expect_tx(bar, bytes);
+    ptx::bulk_load(ptx::smem_u32(buf ? hb1 : hb0), a.h + ((long long)img * per_img + p0) * Ch, bytes, bar);
+  };
+
+  // phase-B mapping: thread -> (channel, stream)
+  const int nstreams = kThr / Ch;  // >= 1 (Ch <= 256)
+  const int my_ch = tid % Ch, my_stream = tid / Ch;
+  const bool b_active = my_stream < nstreams;
+  float wreg[kMaxC];
+#pragma unroll
+  for (int c = 0; c < kMaxC; ++c) wreg[c] = (c < C && b_active) ? s_w[c * Ch + my_ch] : 0.f;
+  float accW[kMaxC], accL[kMaxC], accP = 0.f;
+#pragma unroll
+  for (int c = 0; c < kMaxC; ++c) { accW[c] = 0.f; accL[c] = 0.f; }
+
+  // TMA bulk copies need 16-byte granules: Ch % 4 == 0; otherwise a plain cooperative copy
+  const bool bulk = (Ch % 4) == 0;
+  if (bulk && tid == 0 && blockIdx.x < total) issue(blockIdx.x, 0);
+  int it = 0;
+  for (long long tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+    const int cur = it & 1;
+    const int img = (int)(tile / tpi), tt = (int)(tile % tpi);
+    const long long p0 = (long long)tt * kTP;
+    if (bulk) {
+      ptx::mbar_wait(cur ? bar1 : bar0, (it >> 1) & 1);
+      if (tid == 0 && tile + gridDim.x < total) issue(tile + gridDim.x, cur ^ 1);
+    } else {
+      float* dst = cur ? hb1 : hb0;
+      const long long np = min((long long)kTP, per_img - p0);
+      const float* src = a.h + ((long long)img * per_img + p0) * Ch;
+      for (int e = tid; e < np * Ch; e += kThr) dst[e] = src[e];
+      __syncthreads();
+    }
+    const float* hs = cur ? hb1 : hb0;
+    float lossv = 0.f;
+    // ---------------------------------------------------------------- phase A
+    for (int p = warp; p < kTP; p += kThr / 32) {
+      const long long pos = p0 + p;
+      const bool inimg = pos < per_img;
+      int gl = 0, i = 0, j = 0;
+      if (inimg) {
+        gl = (int)(pos / ((long long)a.gr * a.gc));
+        const int rem = (int)(pos - (long long)gl * a.gr * a.gc);
+        i = rem / a.gc;
+        j = rem % a.gc;
+      }
+      const bool valid = inimg && i < a.vr && j < a.vc;
+      if (!valid) {  // warp-uniform
+        if (lane < kMaxC) s_dl[p * kMaxC + lane] = 0.f;
+        if (lane == 0) s_valid[p] = inimg ? 0 : -1;
+        continue;
+      }
+      float z[kMaxC];
+#pragma unroll
+      for (int c = 0; c < kMaxC; ++c) z[c] = 0.f;
+      const float* hrow = hs + p * Ch;
+      for (int ch = lane; ch < Ch; ch += 32) {
+        const float hv = hrow[ch];
+#pragma unroll
+        for (int c = 0; c < kMaxC; ++c)
+          if (c < C) z[c] = fmaf(s_w[c * Ch + ch], hv, z[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < kMaxC; ++c) {
+        if (c < C) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) z[c] += __shfl_xor_sync(0xffffffffu, z[c], o);
+          z[c] += s_b[c];
+        }
+      }
+      float mx = z[0];
+#pragma unroll
+      for (int c = 1; c < kMaxC; ++c)
+        if (c < C) mx = fmaxf(mx, z[c]);
+      float se = 0.f;
+#pragma unroll
+      for (int c = 0; c < kMaxC; ++c)
+        if (c < C) se += expf(z[c] - mx);
+      const float lse = mx + logf(se);
+      if (!TRAIN) {
+        if (lane < C) {
+          float pc = 0.f;
+#pragma unroll
+          for (int c = 0; c < kMaxC; ++c)
+            if (c == lane) pc = expf(z[c] - lse);
+          const long long g = (long long)img * a.F + gl;
+          a.probs[((g * a.vr + i) * a.vc + j) * C + lane] = pc;
+        }
+        continue;
+      }
+      // label through the fragment -> pixel map: y = r1 + k1 (r2 + k2 (... + kL i))
+      int yy = i, xx = j, rf = gl;
+      for (int l = a.n_levels - 1; l >= 0; --l) {
+        const int kq = a.pool_k[l];
+        const int d = rf % (kq * kq);
+        rf /= kq * kq;
+        yy = d / kq + kq * yy;
+        xx = d % kq + kq * xx;
+      }
+      int t = 255;
+      if (yy < a.O_H && xx < a.O_W) t = a.labels[((long long)img * a.O_H + yy) * a.O_W + xx];
+      if (t != 255 && t >= C && lane == 0) atomicOr(a.err, 1);
+      const int nl = a.nlab[img];
+      float dlv = 0.f;
+      if (t < C && nl > 0) {
+        const float wt = a.cw[t];
+        float zt = 0.f;
+#pragma unroll
+        for (int c = 0; c < kMaxC; ++c)
+          if (c == t) zt = z[c];
+        if (lane == 0) lossv += wt * (lse - zt);
+        if (lane < C) {
+          float zl = 0.f;
+#pragma unroll
+          for (int c = 0; c < kMaxC; ++c)
+            if (c == lane) zl = z[c];
+          dlv = wt * (expf(zl - lse) - (lane == t ? 1.f : 0.f)) / (float)nl;
+        }
+      }
+      if (lane < kMaxC) s_dl[p * kMaxC + lane] = lane < C ? dlv : 0.f;
+      if (lane == 0) s_valid[p] = 1;
+    }
+    if (TRAIN) {
+      // per-tile loss: fixed-order block sum
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) lossv += __shfl_xor_sync(0xffffffffu, lossv, o);
+      if (lane == 0) s_loss[warp] = lossv;
+    }
+    __syncthreads();
+    if (TRAIN) {
+      if (tid == 0) {
+        float s = 0.f;
+        for (int w = 0; w < kThr / 32; ++w) s += s_loss[w];
+        a.loss_part[(long long)img * tpi + tt] = s;
+      }
+      // -------------------------------------------------------------- phase B
+      if (b_active) {
+        float* dh_img = a.dh + ((long long)img * per_img + p0) * Ch;
+        for (int p = my_stream; p < kTP; p += nstreams) {
+          const int vflag = s_valid[p];
+          if (vflag < 0) continue;          // past the end of the image
+          float d = 0.f;
+          if (vflag > 0) {
+            const float hv = hs[p * Ch + my_ch];
+            float dl[kMaxC];
+#pragma unroll
+            for (int c = 0; c < kMaxC; ++c) dl[c] = s_dl[p * kMaxC + c];
+            float sacc = 0.f;
+#pragma unroll
+            for (int c = 0; c < kMaxC; ++c) {
+              sacc = fmaf(wreg[c], dl[c], sacc);
+              accW[c] = fmaf(dl[c], hv, accW[c]);
+              accL[c] += dl[c];
+            }
+            d = sacc * act_der(a.hidden_act, hv);
+            accP += d;
+          }
+          dh_img[(long long)p * Ch + my_ch] = a.round_tf32 ? tf32_rna(d) : d;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (!TRAIN) return;
+  // ------------------------------------------------------------------ block partials
+  // red[stream][ch][0..C) = accW, red[..][C] = accP, and accL from ch == 0 threads
+  float* red = hb0;  // tiles are no longer needed
+  const int RW = C + 1;
+  if (b_active) {
+#pragma unroll
+    for (int c = 0; c < kMaxC; ++c)
+      if (c < C) red[(my_stream * Ch + my_ch) * RW + c] = accW[c];
+    red[(my_stream * Ch + my_ch) * RW + C] = accP;
+  }
+  float* redL = red + nstreams * Ch * RW;
+  if (b_active && my_ch == 0) {
+#pragma unroll
+    for (int c = 0; c < kMaxC; ++c)
+      if (c < C) redL[my_stream * kMaxC + c] = accL[c];
+  }
+  __syncthreads();
+  const int E = C * Ch + C + Ch;
+  float* out = a.part + (size_t)blockIdx.x * E;
+  for (int e = tid; e < E; e += kThr) {
+    float s = 0.f;
+    if (e < C * Ch) {
+      const int c = e / Ch, ch = e % Ch;
+      for (int q = 0; q < nstreams; ++q) s += red[(q * Ch + ch) * RW + c];
+    } else if (e < C * Ch + C) {
+      const int c = e - C * Ch;
+      for (int q = 0; q < nstreams; ++q) s += redL[q * kMaxC + c];
+    } else {
+      const int ch = e - C * Ch - C;
+      for (int q = 0; q < nstreams; ++q) s += red[(q * Ch + ch) * RW + C];
+    }
+    out[e] = s;
+  }
+}
+
+size_t head_smem(int C, int Ch) {
+  return 128 + head_region0(C, Ch) + sizeof(float) * (C * Ch + kMaxC + kTP * kMaxC) + sizeof(int) * kTP +
+         sizeof(float) * (kThr / 32);
+}
+
+}  // namespace
+
+int head_tiles_per_image(long long per_img) { return (int)((per_img + kTP - 1) / kTP); }
+
+int head_blocks(long long total_tiles) {
+  long long nb = 148LL * 2;
+  if (nb > total_tiles) nb = total_tiles;
+  return (int)(nb < 1 ? 1 : nb);
+}
+
+bool head_supported(int C, int Ch) {
+  return C >= 2 && C <= kMaxC && Ch >= 1 && Ch <= kThr && head_smem(C, Ch) <= 200 * 1024;
+}
+
+cudaError_t launch_head2(const HeadArgs& a, cudaStream_t s) {
+  const int nb = a.n_blocks;
+  const size_t smem = head_smem(a.C, a.Ch);
+  if (a.probs) {
+    cudaError_t e = cudaFuncSetAttribute(head_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    head_kernel<false><<<nb, kThr, smem, s>>>(a);
+  } else {
+    cudaError_t e = cudaFuncSetAttribute(head_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    head_kernel<true><<<nb, kThr, smem, s>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace mpf

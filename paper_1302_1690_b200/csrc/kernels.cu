@@ -214,7 +214,7 @@ cudaError_t launch_wgrad_simt(const WgradArgs& a, cudaStream_t s) {
 __global__ void wgrad_reduce_kernel(const float* __restrict__ pw, const float* __restrict__ pb, int n_split,
                                     int cout, int cin, int k, float* gw, float* gb) {
   const int K = k * k * cin;
-  const long long total = (long long)cout * K + cout;
+  const long long total = (long long)cout * K + (pb ? cout : 0);
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     if (e < (long long)cout * K) {
@@ -235,240 +235,9 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ pw, const float* _
 
 cudaError_t launch_wgrad_reduce(const float* pw, const float* pb, int n_split, int cout, int cin, int k,
                                 float* gw, float* gb, cudaStream_t s) {
-  const long long total = (long long)cout * k * k * cin + cout;
+  const long long total = (long long)cout * k * k * cin + (pb ? cout : 0);
   int blocks = (int)mpf_min_ll((total + 255) / 256, 4096);
   wgrad_reduce_kernel<<<blocks, 256, 0, s>>>(pw, pb, n_split, cout, cin, k, gw, gb);
-  return cudaGetLastError();
-}
-
-// ============================================================================ MPF forward
-// Alg. 3: input fragment g, offset (r,c) (row-major, R2) ->
-// output fragment g*k^2 + r*k + c; cell (i,j) = max of the k x k block with top-left
-// (r + k i, c + k j) in the fragment; argmax = first maximum in row-major scan (R6).
-template <int V>
-__global__ void mpf_fwd_kernel(MpfArgs a, long long total) {
-  const int k = a.k, kk = k * k;
-  const int CV = a.C / V;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int cv = (int)(e % CV);
-    long long t = e / CV;
-    const int j = (int)(t % a.m_c);
-    t /= a.m_c;
-    const int i = (int)(t % a.m_r);
-    const long long go = t / a.m_r;     // output fragment
-    const long long g = go / kk;        // source fragment (findSourceFragment)
-    const int rc = (int)(go % kk), r = rc / k, c = rc % k;
-    const int y0 = r + k * i, x0 = c + k * j;
-    const float* src = a.y + ((g * a.gr + y0) * a.gc + x0) * a.C + cv * V;
-    float best[V];
-    uint8_t arg[V];
-#pragma unroll
-    for (int v = 0; v < V; ++v) { best[v] = src[v]; arg[v] = 0; }
-    for (int dy = 0; dy < k; ++dy)
-      for (int dx = 0; dx < k; ++dx) {
-        if (dy == 0 && dx == 0) continue;
-        const float* p = src + ((long long)dy * a.gc + dx) * a.C;
-        float val[V];
-        if constexpr (V == 4) {
-          const float4 q = *reinterpret_cast<const float4*>(p);
-          val[0] = q.x; val[1] = q.y; val[2] = q.z; val[3] = q.w;
-        } else {
-#pragma unroll
-          for (int v = 0; v < V; ++v) val[v] = p[v];
-        }
-#pragma unroll
-        for (int v = 0; v < V; ++v)
-          if (val[v] > best[v]) { best[v] = val[v]; arg[v] = (uint8_t)(dy * k + dx); }
-      }
-    const long long o = e * V;
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      a.out[o + v] = a.round_tf32 ? tf32_rna(best[v]) : best[v];
-      a.idx[o + v] = arg[v];
-    }
-  }
-}
-
-cudaError_t launch_mpf_fwd(const MpfArgs& a, cudaStream_t s) {
-  const bool vec = (a.C % 4) == 0;
-  const long long total = (long long)a.n_frag_in * a.k * a.k * a.m_r * a.m_c * (a.C / (vec ? 4 : 1));
-  const int blocks = (int)mpf_min_ll((total + 255) / 256, 148LL * 64);
-  if (vec)
-    mpf_fwd_kernel<4><<<blocks, 256, 0, s>>>(a, total);
-  else
-    mpf_fwd_kernel<1><<<blocks, 256, 0, s>>>(a, total);
-  return cudaGetLastError();
-}
-
-// ============================================================================ MPF backward
-// Alg. 4 as a deterministic gather: every element p of the conv
-// output sums, in fixed (dy,dx) order, the deltas of all pooled cells whose recorded
-// argmax is p — an element that is the maximum for several offsets receives the SUM
-// (Fig. 2).  Times act'(y_p), with y_p = the pooled value of any
-// cell that selected p (that cell's value IS y_p).  Zero outside the valid region.
-template <int V>
-__global__ void mpf_bwd_kernel(MpfBwdArgs a, long long total) {
-  const int k = a.k, kk = k * k;
-  const int CV = a.C / V;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int cv = (int)(e % CV);
-    long long t = e / CV;
-    const int x = (int)(t % a.gc);
-    t /= a.gc;
-    const int y = (int)(t % a.gr);
-    const long long g = t / a.gr;
-    float acc[V], val[V];
-    bool hit[V];
-#pragma unroll
-    for (int v = 0; v < V; ++v) { acc[v] = 0.f; val[v] = 0.f; hit[v] = false; }
-    if (y < a.vr && x < a.vc) {
-      for (int dy = 0; dy < k; ++dy) {
-        const int ty = y - dy;
-        if (ty < 0) break;
-        const int r = ty % k, i = ty / k;
-        if (i >= a.m_r) continue;
-        for (int dx = 0; dx < k; ++dx) {
-          const int tx = x - dx;
-          if (tx < 0) break;
-          const int c = tx % k, j = tx / k;
-          if (j >= a.m_c) continue;
-          const long long cell = (((g * kk + r * k + c) * a.m_r + i) * a.m_c + j) * a.C + cv * V;
-          const uint8_t want = (uint8_t)(dy * k + dx);
-#pragma unroll
-          for (int v = 0; v < V; ++v) {
-            if (a.idx[cell + v] == want) {
-              acc[v] += a.dout[cell + v];
-              val[v] = a.pooled[cell + v];
-              hit[v] = true;
-            }
-          }
-        }
-      }
-    }
-    const long long o = e * V;
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      float d = hit[v] ? acc[v] * act_der(a.act, val[v]) : 0.f;
-      if (a.round_tf32) d = tf32_rna(d);
-      a.din[o + v] = d;
-    }
-  }
-}
-
-cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s) {
-  const bool vec = (a.C % 4) == 0;
-  const long long total = (long long)a.n_frag_in * a.gr * a.gc * (a.C / (vec ? 4 : 1));
-  const int blocks = (int)mpf_min_ll((total + 255) / 256, 148LL * 64);
-  if (vec)
-    mpf_bwd_kernel<4><<<blocks, 256, 0, s>>>(a, total);
-  else
-    mpf_bwd_kernel<1><<<blocks, 256, 0, s>>>(a, total);
-  return cudaGetLastError();
-}
-
-// ============================================================================ head
-// Last FC (1x1, linear) + per-pixel softmax + class-weighted MCCE (
-// R8: per-image mean over labelled pixels) + dL/dlogits = w_t (p - onehot)/n_lab +
-// dh = (W^T dlogits) * act'(h).  Labels are fetched through the fragment -> pixel map
-// (mixed radix, R2/R7); positions outside the O_H x O_W output grid are ignored.
-constexpr int kHeadThreads = 256;
-
-__global__ void __launch_bounds__(kHeadThreads) head_kernel(HeadArgs a, int parts) {
-  extern __shared__ float s_w[];  // [C][Ch] then b[C]
-  __shared__ float s_red[kHeadThreads / 32];
-  const int C = a.C, Ch = a.Ch;
-  for (int e = threadIdx.x; e < C * Ch; e += blockDim.x) s_w[e] = a.w[e];
-  for (int e = threadIdx.x; e < C; e += blockDim.x) s_w[C * Ch + e] = a.b[e];
-  __syncthreads();
-  const int img = blockIdx.y;
-  const long long per_img = (long long)a.F * a.gr * a.gc;
-  const long long pos = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  float lossv = 0.f;
-  if (pos < per_img) {
-    const int gl = (int)(pos / ((long long)a.gr * a.gc));
-    const int rem = (int)(pos % ((long long)a.gr * a.gc));
-    const int i = rem / a.gc, j = rem % a.gc;
-    const long long g = (long long)img * a.F + gl;
-    const long long hb = ((g * a.gr + i) * a.gc + j);
-    const bool valid = i < a.vr && j < a.vc;
-    if (valid) {
-      const float* h = a.h + hb * Ch;
-      float z[16];
-      for (int c = 0; c < C; ++c) z[c] = s_w[C * Ch + c];
-      for (int ch = 0; ch < Ch; ++ch) {
-        const float hv = h[ch];
-        for (int c = 0; c < C; ++c) z[c] += s_w[c * Ch + ch] * hv;
-      }
-      float mx = z[0];
-      for (int c = 1; c < C; ++c) mx = fmaxf(mx, z[c]);
-      float se = 0.f;
-      for (int c = 0; c < C; ++c) se += expf(z[c] - mx);
-      const float lse = mx + logf(se);
-      float p[16];
-      for (int c = 0; c < C; ++c) p[c] = expf(z[c] - lse);
-      if (a.probs) {
-        const long long pb = ((g * a.vr + i) * a.vc + j) * C;
-        for (int c = 0; c < C; ++c) a.probs[pb + c] = p[c];
-      }
-      if (a.dlogits) {
-        // label through the fragment -> pixel map: y = r1 + k1 (r2 + k2 (... + kL i))
-        int yy = i, xx = j, rem_f = gl;
-        for (int l = a.n_levels - 1; l >= 0; --l) {
-          const int kq = a.pool_k[l];
-          const int d = rem_f % (kq * kq);
-          rem_f /= kq * kq;
-          yy = d / kq + kq * yy;
-          xx = d % kq + kq * xx;
-        }
-        int t = 255;
-        if (a.labels && yy < a.O_H && xx < a.O_W) t = a.labels[((long long)img * a.O_H + yy) * a.O_W + xx];
-        float dl[16];
-        for (int c = 0; c < C; ++c) dl[c] = 0.f;
-        if (t != 255 && t >= C) atomicOr(a.err, 1);
-        const int nl = a.nlab[img];
-        if (t < C && nl > 0) {
-          const float wt = a.cw[t];
-          lossv = -wt * (z[t] - lse);
-          const float inv = 1.f / (float)nl;
-          for (int c = 0; c < C; ++c) dl[c] = wt * (p[c] - (c == t ? 1.f : 0.f)) * inv;
-        }
-        float* dlo = a.dlogits + hb * C;
-        for (int c = 0; c < C; ++c) dlo[c] = a.round_tf32 ? tf32_rna(dl[c]) : dl[c];
-        float* dh = a.dh + hb * Ch;
-        for (int ch = 0; ch < Ch; ++ch) {
-          float s = 0.f;
-          for (int c = 0; c < C; ++c) s += s_w[c * Ch + ch] * dl[c];
-          s *= act_der(a.hidden_act, h[ch]);
-          dh[ch] = a.round_tf32 ? tf32_rna(s) : s;
-        }
-      }
-    } else if (a.dlogits) {
-      for (int c = 0; c < C; ++c) a.dlogits[hb * C + c] = 0.f;
-      for (int ch = 0; ch < Ch; ++ch) a.dh[hb * Ch + ch] = 0.f;
-    }
-  }
-  // fixed-order block reduction of the loss
-  float v = lossv;
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float s = 0.f;
-    for (int w = 0; w < kHeadThreads / 32; ++w) s += s_red[w];
-    if (a.loss_part) a.loss_part[(long long)img * parts + blockIdx.x] = s;
-  }
-}
-
-cudaError_t launch_head(const HeadArgs& a, int* parts_out, cudaStream_t s) {
-  const long long per_img = (long long)a.F * a.gr * a.gc;
-  const int parts = (int)((per_img + kHeadThreads - 1) / kHeadThreads);
-  if (parts_out) *parts_out = parts;
-  dim3 grid(parts, a.n);
-  const size_t smem = sizeof(float) * (a.C * a.Ch + a.C);
-  cudaFuncSetAttribute(head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  head_kernel<<<grid, kHeadThreads, smem, s>>>(a, parts);
   return cudaGetLastError();
 }
 

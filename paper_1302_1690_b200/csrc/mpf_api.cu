@@ -110,6 +110,9 @@ static mpf_status plan(Net* N) {
   const mpf_layer& prev = N->lp[nl - 2].L;
   if (prev.kind == MPF_POOL) return fail(MPF_ERR_CONFIG, "the layer before the softmax FC must be CONV/FC");
   if (last.n_out > 16 || last.n_out < 2) return fail(MPF_ERR_CONFIG, "2..16 classes supported");
+  if (!head_supported(last.n_out, N->lp[nl - 2].L.n_out))
+    return fail(MPF_ERR_CONFIG, "the layer before the softmax FC must have <= 256 maps");
+  if (N->lp[0].L.kind == MPF_POOL) return fail(MPF_ERR_CONFIG, "the first layer must be a CONV layer");
   N->classes = last.n_out;
   N->n_params = off;
   // dense geometry: valid outputs O = H - P + 1, padded so every fragment has equal size
@@ -179,7 +182,6 @@ static void layout_memory(Net* N, int n) {
   N->off_Y = s; s = align256(s + sizeof(float) * maxY);
   N->off_dA = s; s = align256(s + sizeof(float) * maxD);
   N->off_dB = s; s = align256(s + sizeof(float) * maxD);
-  N->off_dlog = s; s = align256(s + sizeof(float) * N->a[N->n_layers].elems_per_image() * n);
   // weight packs
   N->off_wpack = s;
   long long wp = 0;
@@ -197,9 +199,25 @@ static void layout_memory(Net* N, int n) {
   N->part_floats = max_part * (size_t)kMaxSplits;
   s = align256(s + sizeof(float) * N->part_floats);
   N->off_nlab = s; s = align256(s + sizeof(int) * n);
-  // loss partials: head blocks per image
+  // bias / head partials (fixed-order two-level reductions)
   const Act& h = N->a[N->n_layers - 1];
-  N->loss_parts = (int)((h.elems_per_image() / h.C + 255) / 256);
+  const long long h_pos = h.elems_per_image() / h.C;
+  N->loss_parts = head_tiles_per_image(h_pos);
+  size_t bp = (size_t)head_blocks((long long)N->loss_parts * n) * ((size_t)N->classes * h.C + N->classes + h.C);
+  for (int l = 0; l < N->n_layers - 1; ++l) {
+    const LayerPlan& P = N->lp[l];
+    const Act& in = N->a[l];
+    if (P.L.kind == MPF_POOL) {
+      MpfBwdArgs m{};
+      m.gr = in.gr; m.gc = in.gc; m.C = in.C; m.n_frag_in = n * in.F;
+      bp = std::max(bp, (size_t)mpf_bwd_partials(m) * in.C);
+    } else {
+      const Act& o = N->a[l + 1];
+      bp = std::max(bp, (size_t)channel_partials((long long)n * o.F * o.gr * o.gc) * o.C);
+    }
+  }
+  N->bpart_floats = bp;
+  N->off_bpart = s; s = align256(s + sizeof(float) * bp);
   N->off_lossp = s; s = align256(s + sizeof(float) * (size_t)N->loss_parts * n);
   N->off_err = s; s = align256(s + 256);
   N->off_stage_img = s; s = align256(s + sizeof(float) * (size_t)n * N->cfg.in_channels * N->cfg.image_rows * N->cfg.image_cols);
@@ -412,7 +430,14 @@ mpf_status mpf_forward_image(mpf_net* N, const float* d_images, int32_t n, float
       const double in_e = (l == 0) ? (double)n * N->cfg.in_channels * N->cfg.image_rows * N->cfg.image_cols
                                    : (double)n * in.F * in.vr * in.vc * in.C;
       const double cbytes = 4.0 * (in_e + pos_out * P.cout);
-      if (l > 0 && use_tc(N, P, false)) {
+      if (l == 0 && first_conv_supported(N->cfg.in_channels, P.cout, P.L.k) && !getenv("MPF_DISABLE_FIRST")) {
+        FirstConvArgs f{};
+        f.img = d_images; f.n = n; f.H = N->cfg.image_rows; f.W = N->cfg.image_cols;
+        f.w = N->params + P.w_off; f.bias = N->params + P.b_off; f.k = P.L.k; f.cout = P.cout;
+        f.out = out; f.out_gr = o.gr; f.out_gc = o.gc; f.out_vr = o.vr; f.out_vc = o.vc;
+        f.act = P.L.act; f.zero_pad = P.out_where == Where::Tape ? 1 : 0; f.round_tf32 = next_tc ? 1 : 0;
+        LAUNCH(N, s, "conv_first_fwd", l, cflops, cbytes, launch_first_conv(f, s));
+      } else if (l > 0 && use_tc(N, P, false)) {
         TcConvArgs t{};
         t.x = x; t.n_frag = n * in.F; t.gr = in.gr; t.gc = in.gc; t.cin = P.cin;
         t.w = wpack + P.wpack_off; t.bias = N->params + P.b_off; t.k = P.L.k; t.cout = P.cout;
@@ -466,10 +491,11 @@ mpf_status mpf_forward_image(mpf_net* N, const float* d_images, int32_t n, float
     hd.probs = d_probs;
     hd.n = n;
     hd.err = (int*)(N->scratch + N->off_err);
-    hd.loss_part = nullptr;
+    hd.tiles_per_img = head_tiles_per_image((long long)h.F * h.gr * h.gc);
+    hd.n_blocks = head_blocks((long long)hd.tiles_per_img * n);
     const double pos = (double)n * h.F * h.vr * h.vc;
     LAUNCH(N, s, "head_probs", L, 2.0 * pos * h.C * N->classes, pos * (4.0 * h.C + 4.0 * N->classes),
-           launch_head(hd, nullptr, s));
+           launch_head2(hd, s));
   }
   return MPF_OK;
 }
@@ -485,6 +511,17 @@ static mpf_status wgrad(Net* N, int l, const float* x, const float* dy, int n, c
   const double in_e = (l == 0) ? (double)n * N->cfg.in_channels * N->cfg.image_rows * N->cfg.image_cols
                                : (double)n * in.F * in.vr * in.vc * in.C;
   const double wbytes = 4.0 * (in_e + (double)positions * P.cout);
+  if (l == 0 && first_conv_supported(N->cfg.in_channels, P.cout, P.L.k) && !getenv("MPF_DISABLE_FIRST")) {
+    FirstWgradArgs f{};
+    f.img = x; f.n = n; f.H = N->cfg.image_rows; f.W = N->cfg.image_cols;
+    f.dy = dy; f.gr = o.gr; f.gc = o.gc; f.k = P.L.k; f.cout = P.cout;
+    f.part = part; f.n_blocks = first_wgrad_blocks();
+    const int E = P.cout * P.L.k * P.L.k;
+    LAUNCH(N, s, "wgrad_first", l, wflops, wbytes, launch_first_wgrad(f, s));
+    LAUNCH(N, s, "wgrad_reduce", l, 0.0, 4.0 * (f.n_blocks + 1.0) * E,
+           launch_partial_reduce(part, f.n_blocks, E, N->grads + P.w_off, nullptr, E, s));
+    return MPF_OK;
+  }
   if (l > 0 && N->cfg.precision == MPF_PREC_TF32 && tc_wgrad_supported(P.cin, P.cout, P.L.k)) {
     TcWgradArgs t{};
     t.x = x; t.dy = dy; t.n_frag = n * in.F; t.gr = in.gr; t.gc = in.gc; t.vr_out = o.vr; t.vc_out = o.vc;
@@ -494,9 +531,8 @@ static mpf_status wgrad(Net* N, int l, const float* x, const float* dy, int n, c
     int splits = 0;
     LAUNCH(N, s, "wgrad_tc", l, wflops, wbytes, launch_wgrad_tc(t, &splits, s));
     const long long K = (long long)P.L.k * P.L.k * P.cin;
-    LAUNCH(N, s, "wgrad_reduce", l, 0.0, 4.0 * (splits + 2.0) * (P.cout * Kd + P.cout),
-           launch_wgrad_reduce(part, part + (size_t)splits * P.cout * K, splits, P.cout, P.cin, P.L.k,
-                               N->grads + P.w_off, N->grads + P.b_off, s));
+    LAUNCH(N, s, "wgrad_reduce", l, 0.0, 4.0 * (splits + 2.0) * (P.cout * Kd),
+           launch_wgrad_reduce(part, nullptr, splits, P.cout, P.cin, P.L.k, N->grads + P.w_off, nullptr, s));
     return MPF_OK;
   }
   WgradArgs w{};
@@ -518,9 +554,16 @@ static mpf_status wgrad(Net* N, int l, const float* x, const float* dy, int n, c
   w.part_w = part;
   w.part_b = part + (size_t)splits * P.cout * K;
   LAUNCH(N, s, "wgrad_simt", l, wflops, wbytes, launch_wgrad_simt(w, s));
-  LAUNCH(N, s, "wgrad_reduce", l, 0.0, 4.0 * (splits + 2.0) * (P.cout * Kd + P.cout),
-         launch_wgrad_reduce(w.part_w, w.part_b, splits, P.cout, P.cin, P.L.k, N->grads + P.w_off,
-                             N->grads + P.b_off, s));
+  LAUNCH(N, s, "wgrad_reduce", l, 0.0, 4.0 * (splits + 2.0) * (P.cout * Kd),
+         launch_wgrad_reduce(w.part_w, nullptr, splits, P.cout, P.cin, P.L.k, N->grads + P.w_off, nullptr, s));
+  return MPF_OK;
+}
+
+// bias gradient of conv layer l from per-block partials [nb][C] (fixed order)
+static mpf_status bias_reduce(Net* N, int l, const float* part, long long nb, cudaStream_t s) {
+  const LayerPlan& P = N->lp[l];
+  LAUNCH(N, s, "bias_reduce", l, 0.0, 4.0 * (double)nb * P.cout,
+         launch_partial_reduce(part, (int)nb, P.cout, N->grads + P.b_off, nullptr, P.cout, s));
   return MPF_OK;
 }
 
@@ -535,13 +578,14 @@ mpf_status mpf_backward_image(mpf_net* N, const uint8_t* d_labels, const float* 
   const int L = N->n_layers - 1;  // the softmax FC
   int* nlab = (int*)(N->scratch + N->off_nlab);
   float* lossp = scr(N, N->off_lossp);
+  float* bpart = scr(N, N->off_bpart);
   LAUNCH(N, s, "label_count", -1, 0.0, (double)n * N->O_H * N->O_W,
          launch_label_count(d_labels, n, N->O_H * N->O_W, N->classes, nlab, s));
-  // head: dL/dx_hat (first step of back-propagation) and dh
+  // head: dL/dx_hat first, dh, and the softmax FC's gradient + the
+  // previous layer's bias gradient as block partials
   const Act& h = N->a[L];
   float* dcur = scr(N, N->off_dA);
   float* dother = scr(N, N->off_dB);
-  float* dlog = scr(N, N->off_dlog);
   HeadArgs hd{};
   hd.h = act_ptr(N, L);
   hd.gr = h.gr; hd.gc = h.gc; hd.vr = h.vr; hd.vc = h.vc; hd.Ch = h.C; hd.F = h.F;
@@ -556,34 +600,38 @@ mpf_status mpf_backward_image(mpf_net* N, const uint8_t* d_labels, const float* 
   hd.nlab = nlab;
   for (int c = 0; c < 16; ++c) hd.cw[c] = (h_class_w && c < N->classes) ? h_class_w[c] : 1.f;
   hd.probs = nullptr;
-  hd.dlogits = dlog;
   hd.dh = dcur;
   hd.loss_part = lossp;
+  hd.part = bpart;
+  hd.tiles_per_img = head_tiles_per_image((long long)h.F * h.gr * h.gc);
+  hd.n_blocks = head_blocks((long long)hd.tiles_per_img * n);
   hd.err = (int*)(N->scratch + N->off_err);
   hd.n = n;
   hd.round_tf32 = tf32 ? 1 : 0;
-  int parts = 0;
   {
     const double pos = (double)n * h.F * h.vr * h.vc;
-    LAUNCH(N, s, "head_loss_delta", L, 4.0 * pos * h.C * N->classes,
-           pos * (8.0 * h.C + 4.0 * N->classes + 1.0), launch_head(hd, &parts, s));
+    LAUNCH(N, s, "head_loss_delta", L, 6.0 * pos * h.C * N->classes, pos * (8.0 * h.C + 1.0),
+           launch_head2(hd, s));
+    const int E = N->classes * h.C + N->classes + h.C;
+    // [dW_L | db_L] are contiguous in the canonical order; db of layer L-1 follows
+    LAUNCH(N, s, "head_reduce", L, 0.0, 4.0 * (double)hd.n_blocks * E,
+           launch_partial_reduce(bpart, hd.n_blocks, E, N->grads + N->lp[L].w_off, N->grads + N->lp[L - 1].b_off,
+                                 N->classes * h.C + N->classes, s));
   }
   if (d_loss)
-    LAUNCH(N, s, "loss_finalize", L, 0.0, 4.0 * (double)parts * n, launch_loss_finalize(lossp, parts, nlab, n, d_loss, s));
-  // gradient of the softmax FC (1x1 conv over h): Alg. 2 accumulation
-  {
-    mpf_status st = wgrad(N, L, hd.h, dlog, n, s);
-    if (st != MPF_OK) return st;
-  }
+    LAUNCH(N, s, "loss_finalize", L, 0.0, 4.0 * (double)hd.tiles_per_img * n,
+           launch_loss_finalize(lossp, hd.tiles_per_img, nlab, n, d_loss, s));
   // remaining layers in reverse.  Invariant: dcur holds the delta of a[l+1] at the
   // pre-activation (CONV/FC output) or the value (pooled output).
+  bool bias_done = true;  // layer L-1's bias came from the head
   float* wpack = scr(N, N->off_wpack);
   for (int l = L - 1; l >= 0; --l) {
     const LayerPlan& P = N->lp[l];
     const Act& in = N->a[l];
     const Act& o = N->a[l + 1];
     if (P.L.kind == MPF_POOL) {
-      // Alg. 4: route deltas through mpIDXS, accumulate shared maxima; times act' of the conv
+      // Alg. 4: route deltas through mpIDXS, accumulate shared maxima; times act' of the
+      // conv; the same pass sums the bias gradient of that conv (layer l-1)
       MpfBwdArgs m{};
       m.dout = dcur;
       m.pooled = tape_val(N, l);
@@ -594,11 +642,23 @@ mpf_status mpf_backward_image(mpf_net* N, const uint8_t* d_labels, const float* 
       m.act = N->lp[l - 1].L.act;
       m.din = dother;
       m.round_tf32 = tf32 ? 1 : 0;
+      m.bias_part = bpart;
       const double ein = (double)n * in.F * in.vr * in.vc * in.C, eout = (double)n * o.F * o.vr * o.vc * o.C;
       LAUNCH(N, s, "mpf_bwd", l, 0.0, 9.0 * eout + 4.0 * ein, launch_mpf_bwd(m, s));
+      mpf_status st = bias_reduce(N, l - 1, bpart, mpf_bwd_partials(m), s);
+      if (st != MPF_OK) return st;
+      bias_done = true;
       std::swap(dcur, dother);
       continue;
     }
+    if (!bias_done) {  // delta came from a dgrad (conv followed by conv)
+      const long long Pp = (long long)n * o.F * o.gr * o.gc;
+      LAUNCH(N, s, "bias_partial", l, 0.0, 4.0 * (double)Pp * P.cout,
+             launch_channel_partial(dcur, Pp, P.cout, bpart, s));
+      mpf_status st = bias_reduce(N, l, bpart, channel_partials(Pp), s);
+      if (st != MPF_OK) return st;
+    }
+    bias_done = false;
     const float* x = (l == 0) ? N->images : act_ptr(N, l);
     mpf_status st = wgrad(N, l, x, dcur, n, s);
     if (st != MPF_OK) return st;

@@ -65,10 +65,11 @@ struct Net {
   // memory plan for n_cap images (bytes)
   int n_cap = 0;
   size_t tape_bytes = 0, scratch_bytes = 0;
-  size_t off_Y = 0, off_dA = 0, off_dB = 0, off_dlog = 0, off_wpack = 0, off_part = 0,
+  size_t off_Y = 0, off_dA = 0, off_dB = 0, off_bpart = 0, off_wpack = 0, off_part = 0,
          off_nlab = 0, off_lossp = 0, off_err = 0, off_stage_img = 0, off_stage_lab = 0,
          off_stage_loss = 0;
   size_t part_floats = 0;  // capacity of the wgrad partial buffer (floats)
+  size_t bpart_floats = 0; // capacity of the bias / head partial buffer (floats)
   int loss_parts = 0;      // loss partials per image
   // bound memory
   float* params = nullptr;
@@ -150,31 +151,44 @@ struct MpfBwdArgs {
   int act;               // activation of the conv that produced y
   float* din;            // delta at pre-activation of y, grid (gr,gc); zero outside valid
   int round_tf32;
+  float* bias_part;      // nullable: [mpf_bwd_partials(a)][C] per-block sums of din (bias gradient)
 };
 cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s);
+long long mpf_bwd_partials(const MpfBwdArgs& a);
+
+// per-channel partial sums of a [P][C] tensor: part[channel_partials(P)][C]
+long long channel_partials(long long P);
+cudaError_t launch_channel_partial(const float* dy, long long P, int C, float* part, cudaStream_t s);
+// dst[e] += sum_b part[b][e] for e < split_at, dst2[e - split_at] += ... beyond (fixed order)
+cudaError_t launch_partial_reduce(const float* part, int nb, int E, float* dst, float* dst2, int split_at,
+                                  cudaStream_t s);
 
 struct HeadArgs {
   const float* h;        // last hidden activation, grid (gr,gc), valid (vr,vc), Ch channels
   int gr, gc, vr, vc, Ch, F; // F fragments per image
-  const float* w;        // last FC weights canonical [C][Ch] (1x1)
+  const float* w;        // softmax FC weights canonical [C][Ch] (1x1)
   const float* b;        // [C]
   int C;
   int hidden_act;        // activation of h (for act')
-  const uint8_t* labels; // [n][O_H][O_W] or null (forward only)
+  const uint8_t* labels; // [n][O_H][O_W] (training)
   int O_H, O_W;
   int n_levels;
   int pool_k[kMaxL];
   const int* nlab;       // [n]
   float cw[16];          // class weights
-  float* probs;          // nullable: [n*F][vr][vc][C] compact
-  float* dlogits;        // nullable: [n*F][gr][gc][C]
-  float* dh;             // nullable: [n*F][gr][gc][Ch]
-  float* loss_part;      // [n][parts]
+  float* probs;          // forward-only mode when non-null: [n*F][vr][vc][C] compact
+  float* dh;             // training: [n*F][gr][gc][Ch] delta of the previous layer (zero off-valid)
+  float* loss_part;      // training: [n][tiles_per_img]
+  float* part;           // training: [n_blocks][C*Ch + C + Ch] (dW_L, db_L, db_prev)
+  int tiles_per_img, n_blocks;
   int* err;
   int n;
   int round_tf32;
 };
-cudaError_t launch_head(const HeadArgs& a, int* parts_per_image, cudaStream_t s);
+int head_tiles_per_image(long long per_img);
+int head_blocks(long long total_tiles);
+bool head_supported(int C, int Ch);
+cudaError_t launch_head2(const HeadArgs& a, cudaStream_t s);
 
 cudaError_t launch_label_count(const uint8_t* labels, int n, int hw, int classes, int* nlab, cudaStream_t s);
 cudaError_t launch_loss_finalize(const float* loss_part, int parts, const int* nlab, int n, float* loss,
@@ -186,6 +200,33 @@ cudaError_t launch_frag2pix(const float* frag, float* pix, int n, int C, int F, 
                             int O_W, int n_levels, const int* pool_k, cudaStream_t s);
 cudaError_t launch_compact_copy(const float* src, int gr, int gc, int vr, int vc, int C, long long nf,
                                 float* dst, cudaStream_t s);
+
+// First layer (one input map, the raw image [n][H][W]) on CUDA cores, fp32.
+struct FirstConvArgs {
+  const float* img;
+  int n, H, W;
+  const float* w;        // canonical W[co][0][ky][kx]
+  const float* bias;
+  int k, cout;
+  float* out;            // [n][out_gr][out_gc][cout]
+  int out_gr, out_gc, out_vr, out_vc;
+  int act, zero_pad, round_tf32;
+  int n_cog;             // set by the launcher
+};
+struct FirstWgradArgs {
+  const float* img;
+  int n, H, W;
+  const float* dy;       // [n][gr][gc][cout], zero outside the valid region
+  int gr, gc;
+  int k, cout;
+  float* part;           // [n_blocks][cout][k*k]
+  int n_blocks;
+  int n_cog;             // set by the launcher
+};
+bool first_conv_supported(int cin, int cout, int k);
+int first_wgrad_blocks();
+cudaError_t launch_first_conv(FirstConvArgs a, cudaStream_t s);
+cudaError_t launch_first_wgrad(FirstWgradArgs a, cudaStream_t s);
 
 // thread-local error text
 void set_error(const std::string& msg);

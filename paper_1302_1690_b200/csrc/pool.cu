@@ -1,0 +1,403 @@
+// pool.cu — MaxPoolingFragment forward / backward (HBM-bound) and the deterministic
+// per-channel reductions that produce bias gradients.
+//
+// MPF forward, Alg. 3.  For input fragment g and offset (r, c)
+// (row-major, reading R2) output fragment g*k^2 + r*k + c holds, at cell (i, j), the
+// max of the k x k block with top-left (r + k i, c + k j) and its argmax (first maximum
+// in row-major scan, R6).  Every block position Y = r + k i, X = c + k j is a distinct
+// point of the stride-1 "window grid" [0, k m_r) x [0, k m_c), so the kernel walks that
+// grid: one thread owns a column X and one 4-channel vector and slides down a band of
+// rows keeping the k horizontal row maxima in registers — each input element comes
+// from HBM once and from L1 k times (instead of k^2).
+//
+// MPF backward, Alg. 4 (reading R3) as a gather: conv-output element
+// (Y', X') sums, in fixed (dy, dx) order, the deltas of every window (Y'-dy, X'-dx)
+// whose recorded argmax is (dy, dx) — shared maxima ADD (Fig. 2) —
+// times act'(y) taken from the pooled value of a selecting window (it equals y at
+// (Y', X')).  Deterministic, no atomics.  The same pass adds the delta into a
+// per-block, per-channel partial sum: the bias gradient of the conv that produced y
+// (Alg. 2: the sum over all fragments and positions), finished by bias_reduce in a
+// fixed order.
+//
+// All index arithmetic is 32-bit per fragment; only final offsets are 64-bit.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "mpf_internal.h"
+
+namespace mpf {
+
+namespace {
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__device__ __forceinline__ float act_der(int act, float y) {
+  if (act == MPF_TANH) return 1.f - y * y;
+  if (act == MPF_LOGISTIC) return y * (1.f - y);
+  return 1.f;
+}
+
+template <int V>
+struct Vec {
+  float v[V];
+};
+
+template <int V>
+__device__ __forceinline__ Vec<V> ldv(const float* p) {
+  Vec<V> r;
+  if constexpr (V == 4) {
+    const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+    r.v[0] = q.x; r.v[1] = q.y; r.v[2] = q.z; r.v[3] = q.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i) r.v[i] = __ldg(p + i);
+  }
+  return r;
+}
+
+template <int V>
+__device__ __forceinline__ void stv(float* p, const float (&v)[V]) {
+  if constexpr (V == 4) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i) p[i] = v[i];
+  }
+}
+
+template <int V>
+__device__ __forceinline__ void stidx(uint8_t* p, const uint8_t (&a)[V]) {
+  if constexpr (V == 4) {
+    *reinterpret_cast<uchar4*>(p) = make_uchar4(a[0], a[1], a[2], a[3]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i) p[i] = a[i];
+  }
+}
+
+constexpr int kBand = 16;  // window rows per thread (forward) / output rows per thread (backward)
+
+int block_dims(int C, int V, dim3* blk) {
+  const int CV = C / V;
+  int ty = 256 / CV;
+  if (ty < 1) ty = 1;
+  *blk = dim3(CV, ty, 1);
+  return ty;
+}
+
+// ----------------------------------------------------------------------------- forward
+template <int K, int V>
+__global__ void __launch_bounds__(256) mpf_fwd_kernel(MpfArgs a) {
+  const int cv = threadIdx.x;
+  const int X = blockIdx.x * blockDim.y + threadIdx.y;
+  const int Xw = K * a.m_c, Yw = K * a.m_r;
+  if (X >= Xw) return;
+  const int y0 = blockIdx.y * kBand;
+  const int y1 = min(y0 + kBand, Yw);
+  const int c = X % K, j = X / K;
+  const int C = a.C;
+  for (int g = blockIdx.z; g < a.n_frag_in; g += gridDim.z) {
+    const float* src = a.y + ((size_t)g * a.gr * a.gc + X) * C + cv * V;
+    // horizontal max of row r over dx = 0..K-1 (first maximum)
+    auto hrow = [&](int r, float (&hv)[V], uint8_t (&ha)[V]) {
+      const float* p = src + (size_t)r * a.gc * C;
+      Vec<V> q = ldv<V>(p);
+#pragma unroll
+      for (int v = 0; v < V; ++v) { hv[v] = q.v[v]; ha[v] = 0; }
+#pragma unroll
+      for (int dx = 1; dx < K; ++dx) {
+        q = ldv<V>(p + dx * C);
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+          if (q.v[v] > hv[v]) { hv[v] = q.v[v]; ha[v] = (uint8_t)dx; }
+      }
+    };
+    float hm[K][V];
+    uint8_t ha[K][V];
+#pragma unroll
+    for (int d = 1; d < K; ++d) hrow(y0 + d - 1, hm[d], ha[d]);
+    const size_t frag_base = (size_t)g * K * K;
+    for (int Y = y0; Y < y1; ++Y) {
+#pragma unroll
+      for (int d = 0; d < K - 1; ++d) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) { hm[d][v] = hm[d + 1][v]; ha[d][v] = ha[d + 1][v]; }
+      }
+      hrow(Y + K - 1, hm[K - 1], ha[K - 1]);
+      float best[V];
+      uint8_t arg[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) { best[v] = hm[0][v]; arg[v] = ha[0][v]; }
+#pragma unroll
+      for (int d = 1; d < K; ++d)
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+          if (hm[d][v] > best[v]) { best[v] = hm[d][v]; arg[v] = (uint8_t)(d * K + ha[d][v]); }
+      const int r = Y % K, i = Y / K;
+      const size_t o = (((frag_base + r * K + c) * a.m_r + i) * a.m_c + j) * C + cv * V;
+      if (a.round_tf32) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) best[v] = tf32_rna(best[v]);
+      }
+      stv<V>(a.out + o, best);
+      stidx<V>(a.idx + o, arg);
+    }
+  }
+}
+
+template <int K, int V>
+cudaError_t fwd_launch(const MpfArgs& a, cudaStream_t s) {
+  dim3 blk;
+  const int ty = block_dims(a.C, V, &blk);
+  const int Xw = K * a.m_c, Yw = K * a.m_r;
+  dim3 grid((Xw + ty - 1) / ty, (Yw + kBand - 1) / kBand, a.n_frag_in < 65535 ? a.n_frag_in : 65535);
+  mpf_fwd_kernel<K, V><<<grid, blk, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// generic k (any pooling factor): plain k x k scan per window
+template <int V>
+__global__ void __launch_bounds__(256) mpf_fwd_generic_kernel(MpfArgs a) {
+  const int cv = threadIdx.x;
+  const int K = a.k;
+  const int X = blockIdx.x * blockDim.y + threadIdx.y;
+  const int Xw = K * a.m_c, Yw = K * a.m_r;
+  if (X >= Xw) return;
+  const int y0 = blockIdx.y * kBand, y1 = min(y0 + kBand, Yw);
+  const int c = X % K, j = X / K;
+  for (int g = blockIdx.z; g < a.n_frag_in; g += gridDim.z) {
+    for (int Y = y0; Y < y1; ++Y) {
+      const float* src = a.y + (((size_t)g * a.gr + Y) * a.gc + X) * a.C + cv * V;
+      float best[V];
+      uint8_t arg[V];
+      Vec<V> q = ldv<V>(src);
+#pragma unroll
+      for (int v = 0; v < V; ++v) { best[v] = q.v[v]; arg[v] = 0; }
+      for (int dy = 0; dy < K; ++dy)
+        for (int dx = 0; dx < K; ++dx) {
+          if (dy == 0 && dx == 0) continue;
+          q = ldv<V>(src + ((size_t)dy * a.gc + dx) * a.C);
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+            if (q.v[v] > best[v]) { best[v] = q.v[v]; arg[v] = (uint8_t)(dy * K + dx); }
+        }
+      const int r = Y % K, i = Y / K;
+      const size_t o = ((((size_t)g * K * K + r * K + c) * a.m_r + i) * a.m_c + j) * a.C + cv * V;
+      if (a.round_tf32) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) best[v] = tf32_rna(best[v]);
+      }
+      stv<V>(a.out + o, best);
+      stidx<V>(a.idx + o, arg);
+    }
+  }
+}
+
+template <int V>
+cudaError_t fwd_dispatch(const MpfArgs& a, cudaStream_t s) {
+  if (a.k == 2) return fwd_launch<2, V>(a, s);
+  if (a.k == 3) return fwd_launch<3, V>(a, s);
+  if (a.k == 4) return fwd_launch<4, V>(a, s);
+  dim3 blk;
+  const int ty = block_dims(a.C, V, &blk);
+  const int Xw = a.k * a.m_c, Yw = a.k * a.m_r;
+  dim3 grid((Xw + ty - 1) / ty, (Yw + kBand - 1) / kBand, a.n_frag_in < 65535 ? a.n_frag_in : 65535);
+  mpf_fwd_generic_kernel<V><<<grid, blk, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------- backward
+template <int V>
+__global__ void __launch_bounds__(256) mpf_bwd_kernel(MpfBwdArgs a) {
+  extern __shared__ float s_red[];  // [blockDim.y][C]
+  const int cv = threadIdx.x;
+  const int K = a.k, KK = K * K;
+  const int X = blockIdx.x * blockDim.y + threadIdx.y;
+  const int Xw = K * a.m_c, Yw = K * a.m_r;
+  const int y0 = blockIdx.y * kBand, y1 = min(y0 + kBand, a.gr);
+  const int C = a.C;
+  float bsum[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) bsum[v] = 0.f;
+  if (X < a.gc) {
+    for (int g = blockIdx.z; g < a.n_frag_in; g += gridDim.z) {
+      const size_t cell_frag0 = (size_t)g * KK;
+      for (int Y = y0; Y < y1; ++Y) {
+        float acc[V], val[V];
+        bool hit[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) { acc[v] = 0.f; val[v] = 0.f; hit[v] = false; }
+        if (Y < a.vr && X < a.vc) {
+          for (int dy = 0; dy < K; ++dy) {
+            const int wy = Y - dy;
+            if (wy < 0) break;
+            if (wy >= Yw) continue;
+            const int r = wy % K, i = wy / K;
+            for (int dx = 0; dx < K; ++dx) {
+              const int wx = X - dx;
+              if (wx < 0) break;
+              if (wx >= Xw) continue;
+              const int c = wx % K, j = wx / K;
+              const size_t cell = (((cell_frag0 + r * K + c) * a.m_r + i) * a.m_c + j) * C + cv * V;
+              const uint8_t want = (uint8_t)(dy * K + dx);
+              uint8_t id[V];
+              if constexpr (V == 4) {
+                const uchar4 q = __ldg(reinterpret_cast<const uchar4*>(a.idx + cell));
+                id[0] = q.x; id[1] = q.y; id[2] = q.z; id[3] = q.w;
+              } else {
+#pragma unroll
+                for (int v = 0; v < V; ++v) id[v] = __ldg(a.idx + cell + v);
+              }
+              bool any = false;
+#pragma unroll
+              for (int v = 0; v < V; ++v) any |= (id[v] == want);
+              if (any) {
+                const Vec<V> d = ldv<V>(a.dout + cell);
+                const Vec<V> pv = ldv<V>(a.pooled + cell);
+#pragma unroll
+                for (int v = 0; v < V; ++v)
+                  if (id[v] == want) { acc[v] += d.v[v]; val[v] = pv.v[v]; hit[v] = true; }
+              }
+            }
+          }
+        }
+        float o[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const float dv = hit[v] ? acc[v] * act_der(a.act, val[v]) : 0.f;
+          bsum[v] += dv;
+          o[v] = a.round_tf32 ? tf32_rna(dv) : dv;
+        }
+        stv<V>(a.din + (((size_t)g * a.gr + Y) * a.gc + X) * C + cv * V, o);
+      }
+    }
+  }
+  if (a.bias_part == nullptr) return;
+  // fixed-order block reduction of the bias partials over threadIdx.y
+#pragma unroll
+  for (int v = 0; v < V; ++v) s_red[threadIdx.y * C + cv * V + v] = bsum[v];
+  __syncthreads();
+  if (threadIdx.y == 0) {
+    const size_t blin = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      float t = 0.f;
+      for (int q = 0; q < (int)blockDim.y; ++q) t += s_red[q * C + cv * V + v];
+      a.bias_part[blin * C + cv * V + v] = t;
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------- channel sums
+// Generic per-channel partials of a [P][C] tensor (bias gradient of a conv whose delta
+// comes from a dgrad, i.e. a conv followed by another conv).
+template <int V>
+__global__ void __launch_bounds__(256) channel_partial_kernel(const float* __restrict__ dy, long long P, int C,
+                                                              long long rows_per_block, float* part) {
+  extern __shared__ float s_red[];
+  const int cv = threadIdx.x;
+  const long long r0 = (long long)blockIdx.x * rows_per_block;
+  const long long r1 = min(P, r0 + rows_per_block);
+  float acc[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) acc[v] = 0.f;
+  for (long long r = r0 + threadIdx.y; r < r1; r += blockDim.y) {
+    const Vec<V> q = ldv<V>(dy + r * C + cv * V);
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] += q.v[v];
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v) s_red[threadIdx.y * C + cv * V + v] = acc[v];
+  __syncthreads();
+  if (threadIdx.y == 0) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      float t = 0.f;
+      for (int q = 0; q < (int)blockDim.y; ++q) t += s_red[q * C + cv * V + v];
+      part[(size_t)blockIdx.x * C + cv * V + v] = t;
+    }
+  }
+}
+
+// dst[e] += sum_{b < nb} part[b][e], e < E, in a fixed order (deterministic).
+__global__ void __launch_bounds__(256) partial_reduce_kernel(const float* __restrict__ part, int nb, int E,
+                                                             float* dst, float* dst2, int split_at) {
+  __shared__ float s[256];
+  const int e = blockIdx.x;
+  float t = 0.f;
+  for (int b = threadIdx.x; b < nb; b += 256) t += part[(size_t)b * E + e];
+  s[threadIdx.x] = t;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (e < split_at) dst[e] += s[0];
+    else dst2[e - split_at] += s[0];
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_mpf_fwd(const MpfArgs& a, cudaStream_t s) {
+  if (a.C % 4 == 0) return fwd_dispatch<4>(a, s);
+  return fwd_dispatch<1>(a, s);
+}
+
+static void bwd_geometry(const MpfBwdArgs& a, int V, dim3* grid, dim3* blk) {
+  const int ty = block_dims(a.C, V, blk);
+  *grid = dim3((a.gc + ty - 1) / ty, (a.gr + kBand - 1) / kBand, a.n_frag_in < 65535 ? a.n_frag_in : 65535);
+}
+
+long long mpf_bwd_partials(const MpfBwdArgs& a) {
+  dim3 g, b;
+  bwd_geometry(a, a.C % 4 == 0 ? 4 : 1, &g, &b);
+  return (long long)g.x * g.y * g.z;
+}
+
+cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s) {
+  const int V = a.C % 4 == 0 ? 4 : 1;
+  dim3 grid, blk;
+  bwd_geometry(a, V, &grid, &blk);
+  const size_t smem = sizeof(float) * blk.y * a.C;
+  if (V == 4)
+    mpf_bwd_kernel<4><<<grid, blk, smem, s>>>(a);
+  else
+    mpf_bwd_kernel<1><<<grid, blk, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+long long channel_partials(long long P) {
+  long long nb = (P + 4095) / 4096;
+  if (nb > 148 * 8) nb = 148 * 8;
+  if (nb < 1) nb = 1;
+  return nb;
+}
+
+cudaError_t launch_channel_partial(const float* dy, long long P, int C, float* part, cudaStream_t s) {
+  const long long nb = channel_partials(P);
+  const long long rows = (P + nb - 1) / nb;
+  const int V = C % 4 == 0 ? 4 : 1;
+  dim3 blk;
+  block_dims(C, V, &blk);
+  const size_t smem = sizeof(float) * blk.y * C;
+  if (V == 4)
+    channel_partial_kernel<4><<<(unsigned)nb, blk, smem, s>>>(dy, P, C, rows, part);
+  else
+    channel_partial_kernel<1><<<(unsigned)nb, blk, smem, s>>>(dy, P, C, rows, part);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_partial_reduce(const float* part, int nb, int E, float* dst, float* dst2, int split_at,
+                                  cudaStream_t s) {
+  if (E <= 0) return cudaSuccess;
+  partial_reduce_kernel<<<E, 256, 0, s>>>(part, nb, E, dst, dst2, split_at);
+  return cudaGetLastError();
+}
+
+}  // namespace mpf
