@@ -7,18 +7,21 @@
 // sum over k^2 taps t = (ky, kx) of a position shift:
 //     D[p, co] = sum_t sum_ci X[p + base + ky*gc + kx, ci] * W[co, t, ci]
 // with base = 0 (forward) or -(k-1)(gc+1) (dgrad, rotated weights).  Positions whose
-// window leaves the fragment are garbage and are never used; reads outside the tensor
-// are zero-filled by TMA.  Delta tensors are zero outside their valid region, which
-// makes the dgrad "full correlation" exact with the same 1-D formulation.
+// window leaves the fragment are garbage and are written as 0.  Reads outside the
+// tensor are zero-filled by TMA.  Delta tensors are zero outside their valid region,
+// which makes the dgrad "full correlation" exact with the same 1-D formulation.
 //
-// Kernel.  One CTA computes M_cta = NACC x 128 consecutive positions, all output
-// channels (N = cout padded to 16), into NACC TMEM accumulators of 128 x N fp32.
-// K loop over stages (ky, 32-channel chunk): one TMA "slab" of M_cta + 8 input rows
-// (128 B = 32 fp32 per row, SWIZZLE_128B) is reused for all k taps kx of that row by
-// offsetting the UMMA descriptor start by kx rows; the weights of each tap are a
-// separate TMA tile [N x 32].  Warp roles: warp 0 TMA producer, warp 1 TMEM allocator
-// + single-thread MMA issuer, warps 2-5 epilogue (TMEM -> registers -> bias/act ->
-// global).  Two mbarrier rings (A slabs, B taps) with full/empty phases.
+// Kernel (persistent, one CTA per SM).  A tile is M_cta = NACC x 128 consecutive
+// positions x all output channels (N = cout padded to 16) held in NACC TMEM
+// accumulators of 128 x N fp32; two such accumulator sets alternate so the epilogue
+// of tile i overlaps the MMAs of tile i+1.  K loop over stages (ky, 32-channel chunk):
+// one TMA "slab" of M_cta + k - 1 input rows (128 B = 32 fp32 per row, SWIZZLE_128B)
+// serves all k taps kx of that row — each tap only offsets the UMMA descriptor start
+// by kx rows; the weights of each tap are a separate TMA tile [N x 32].
+// Warp roles: warp 0 TMA producer, warp 1 TMEM allocator + single-thread MMA issuer,
+// warps 2-5 epilogue: TMEM -> registers -> bias/act/act'/tf32 rounding -> swizzled
+// shared staging -> TMA tile store (the output tile rows are consecutive positions,
+// so every store is a dense [32 rows x 32 channels] box).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -37,19 +40,20 @@ namespace {
 
 constexpr int kThreads = 192;  // 6 warps
 constexpr int kKC = 32;        // fp32 channels per 128-byte row
+constexpr uint32_t kStageBytes = 32 * 128;  // one epilogue store box: 32 rows x 32 fp32
 
 struct ConvTcParams {
   int P_tot, gr, gc, out_vr, out_vc;
   int cin, cout, npad, k, shift_rows, n_cc;
-  int act, round_out, zero_pad, dact;
+  int act, round_out, dact;
   const float* bias;
-  float* out;
   const float* mul_dact;
   int box_rows, nbox;
   uint32_t a_slot_bytes, b_slot_bytes;
-  int n_bslots;
+  int n_aslots, n_bslots;
   int base_mode;
   uint32_t tmem_cols;
+  int n_tiles;
 };
 
 __device__ __forceinline__ float tf32r(float x) {
@@ -70,26 +74,32 @@ __device__ __forceinline__ float act_d(int act, float y) {
 
 template <int NACC>
 __global__ void __launch_bounds__(kThreads, 1)
-    conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, ConvTcParams p) {
+    conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmO, ConvTcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B aligned carve-up
   const uint32_t sbase = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
-  const uint32_t sA = sbase;                                   // 2 A slabs
-  const uint32_t sB = sA + 2 * p.a_slot_bytes;                 // n_bslots weight taps
-  const uint32_t sBar = sB + p.n_bslots * p.b_slot_bytes;      // barriers
-  const uint32_t barAfull = sBar, barAempty = sBar + 16;
-  const uint32_t barBfull = sBar + 32, barBempty = barBfull + 8 * p.n_bslots;
-  const uint32_t barTfull = barBempty + 8 * p.n_bslots;
-  const uint32_t sTmemSlot = barTfull + 8;
-  uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (sTmemSlot - ptx::smem_u32(smem_raw)));
+  const uint32_t sA = sbase;                                   // A slabs
+  const uint32_t sB = sA + p.n_aslots * p.a_slot_bytes;        // weight taps
+  const uint32_t sC = sB + p.n_bslots * p.b_slot_bytes;        // epilogue staging: 4 warps x 2 boxes
+  const uint32_t sBias = sC + 8 * kStageBytes;                 // [npad] fp32
+  const uint32_t sBar = sBias + 4 * 256;
+  const uint32_t barAfull = sBar, barAempty = barAfull + 8 * p.n_aslots;
+  const uint32_t barBfull = barAempty + 8 * p.n_aslots, barBempty = barBfull + 8 * p.n_bslots;
+  const uint32_t barTfull = barBempty + 8 * p.n_bslots, barTempty = barTfull + 16;
+  const uint32_t sTmemSlot = barTempty + 16;
+  uint8_t* gen = smem_raw - ptx::smem_u32(smem_raw);  // generic pointer of shared address 0
+  uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(gen + sTmemSlot);
+  float* s_bias = reinterpret_cast<float*>(gen + sBias);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int p0 = blockIdx.x * (NACC * 128);
+  constexpr int M_CTA = NACC * 128;
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
-    for (int i = 0; i < 2; ++i) {
+    ptx::prefetch_tmap(&tmO);
+    for (int i = 0; i < p.n_aslots; ++i) {
       ptx::mbar_init(barAfull + 8 * i, 1);
       ptx::mbar_init(barAempty + 8 * i, 1);
     }
@@ -97,10 +107,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(barBfull + 8 * i, 1);
       ptx::mbar_init(barBempty + 8 * i, 1);
     }
-    ptx::mbar_init(barTfull, 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(barTfull + 8 * i, 1);
+      ptx::mbar_init(barTempty + 8 * i, 4);  // one arrive per epilogue warp
+    }
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc(sTmemSlot, p.tmem_cols);
+  for (int c = threadIdx.x; c < p.npad; c += kThreads) s_bias[c] = (p.bias && c < p.cout) ? p.bias[c] : 0.f;
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -111,22 +125,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       int a_it = 0, b_it = 0;
-      for (int ky = 0; ky < k; ++ky) {
-        for (int cc = 0; cc < p.n_cc; ++cc) {
-          const int as = a_it & 1;
-          ptx::mbar_wait(barAempty + 8 * as, ((a_it >> 1) & 1) ^ 1);
-          ptx::mbar_arrive_expect_tx(barAfull + 8 * as, p.a_slot_bytes);
-          const int row0 = p0 + p.shift_rows + ky * p.gc;
-          for (int b = 0; b < p.nbox; ++b)
-            ptx::tma_load_2d(sA + as * p.a_slot_bytes + b * p.box_rows * 128, &tmA, barAfull + 8 * as, cc * kKC,
-                             row0 + b * p.box_rows);
-          ++a_it;
-          for (int kx = 0; kx < k; ++kx) {
-            const int bs = b_it % p.n_bslots;
-            ptx::mbar_wait(barBempty + 8 * bs, ((b_it / p.n_bslots) & 1) ^ 1);
-            ptx::mbar_arrive_expect_tx(barBfull + 8 * bs, p.b_slot_bytes);
-            ptx::tma_load_2d(sB + bs * p.b_slot_bytes, &tmB, barBfull + 8 * bs, (ky * k + kx) * p.cin + cc * kKC, 0);
-            ++b_it;
+      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+        const int p0 = tile * M_CTA;
+        for (int ky = 0; ky < k; ++ky) {
+          for (int cc = 0; cc < p.n_cc; ++cc) {
+            const int as = a_it % p.n_aslots;
+            ptx::mbar_wait(barAempty + 8 * as, ((a_it / p.n_aslots) & 1) ^ 1);
+            ptx::mbar_arrive_expect_tx(barAfull + 8 * as, p.a_slot_bytes);
+            const int row0 = p0 + p.shift_rows + ky * p.gc;
+            for (int b = 0; b < p.nbox; ++b)
+              ptx::tma_load_2d(sA + as * p.a_slot_bytes + b * p.box_rows * 128, &tmA, barAfull + 8 * as, cc * kKC,
+                               row0 + b * p.box_rows);
+            ++a_it;
+            for (int kx = 0; kx < k; ++kx) {
+              const int bs = b_it % p.n_bslots;
+              ptx::mbar_wait(barBempty + 8 * bs, ((b_it / p.n_bslots) & 1) ^ 1);
+              ptx::mbar_arrive_expect_tx(barBfull + 8 * bs, p.b_slot_bytes);
+              ptx::tma_load_2d(sB + bs * p.b_slot_bytes, &tmB, barBfull + 8 * bs, (ky * k + kx) * p.cin + cc * kKC, 0);
+              ++b_it;
+            }
           }
         }
       }
@@ -134,80 +151,143 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     const uint32_t idesc = ptx::idesc_tf32(128, p.npad);
-    int a_it = 0, b_it = 0;
-    for (int ky = 0; ky < k; ++ky) {
-      for (int cc = 0; cc < p.n_cc; ++cc) {
-        const int as = a_it & 1;
-        ptx::mbar_wait(barAfull + 8 * as, (a_it >> 1) & 1);
-        for (int kx = 0; kx < k; ++kx) {
-          const int bs = b_it % p.n_bslots;
-          ptx::mbar_wait(barBfull + 8 * bs, (b_it / p.n_bslots) & 1);
-          ptx::tc_fence_after();
-          if (lane == 0) {
+    int a_it = 0, b_it = 0, lt = 0;
+    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++lt) {
+      const int buf = lt & 1;
+      ptx::mbar_wait(barTempty + 8 * buf, ((lt >> 1) & 1) ^ 1);  // the epilogue drained this set
+      ptx::tc_fence_after();
+      const uint32_t dbase = tmem + buf * (NACC * p.npad);
+      for (int ky = 0; ky < k; ++ky) {
+        for (int cc = 0; cc < p.n_cc; ++cc) {
+          const int as = a_it % p.n_aslots;
+          ptx::mbar_wait(barAfull + 8 * as, (a_it / p.n_aslots) & 1);
+          for (int kx = 0; kx < k; ++kx) {
+            const int bs = b_it % p.n_bslots;
+            ptx::mbar_wait(barBfull + 8 * bs, (b_it / p.n_bslots) & 1);
+            ptx::tc_fence_after();
+            if (lane == 0) {
 #pragma unroll
-            for (int acc = 0; acc < NACC; ++acc) {
+              for (int acc = 0; acc < NACC; ++acc) {
 #pragma unroll
-              for (int k8 = 0; k8 < 4; ++k8) {
-                const uint32_t aaddr = sA + as * p.a_slot_bytes + (acc * 128 + kx) * 128 + k8 * 32;
-                const uint32_t baddr = sB + bs * p.b_slot_bytes + k8 * 32;
-                const uint32_t accum = (ky | cc | kx | k8) != 0;
-                ptx::mma_tf32(tmem + acc * p.npad, ptx::sdesc_k_sw128(aaddr, p.base_mode),
-                              ptx::sdesc_k_sw128(baddr, p.base_mode), idesc, accum);
+                for (int k8 = 0; k8 < 4; ++k8) {
+                  const uint32_t aaddr = sA + as * p.a_slot_bytes + (acc * 128 + kx) * 128 + k8 * 32;
+                  const uint32_t baddr = sB + bs * p.b_slot_bytes + k8 * 32;
+                  const uint32_t accum = (ky | cc | kx | k8) != 0;
+                  ptx::mma_tf32(dbase + acc * p.npad, ptx::sdesc_k_sw128(aaddr, p.base_mode),
+                                ptx::sdesc_k_sw128(baddr, p.base_mode), idesc, accum);
+                }
               }
+              ptx::mma_commit(barBempty + 8 * bs);
             }
-            ptx::mma_commit(barBempty + 8 * bs);
+            __syncwarp();
+            ++b_it;
           }
+          if (lane == 0) ptx::mma_commit(barAempty + 8 * as);
           __syncwarp();
-          ++b_it;
+          ++a_it;
         }
-        if (lane == 0) ptx::mma_commit(barAempty + 8 * as);
-        __syncwarp();
-        ++a_it;
       }
+      if (lane == 0) ptx::mma_commit(barTfull + 8 * buf);
+      __syncwarp();
     }
-    if (lane == 0) ptx::mma_commit(barTfull);
-    __syncwarp();
   } else {
     // ------------------------------------------------------------ epilogue (warps 2..5)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int row = q * 32 + lane;
-    ptx::mbar_wait(barTfull, 0);
-    ptx::tc_fence_after();
     const int per_frag = p.gr * p.gc;
-    for (int acc = 0; acc < NACC; ++acc) {
-      const int pos = p0 + acc * 128 + row;
-      const bool inb = pos < p.P_tot;
-      int y = 0, x = 0;
-      if (inb) {
-        const int r = pos % per_frag;
-        y = r / p.gc;
-        x = r % p.gc;
-      }
-      const bool valid = inb && y < p.out_vr && x < p.out_vc;
-      const bool write = valid || (inb && p.zero_pad);
-      float* dst = p.out + (long long)pos * p.cout;
-      const float* md = p.mul_dact ? p.mul_dact + (long long)pos * p.cout : nullptr;
-      for (int c0 = 0; c0 < p.cout; c0 += 16) {
-        float v[16];
-        ptx::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * p.npad + c0, v);
-        if (write) {
+    int lt = 0, sb = 0;
+    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++lt) {
+      const int buf = lt & 1;
+      ptx::mbar_wait(barTfull + 8 * buf, (lt >> 1) & 1);
+      ptx::tc_fence_after();
+      const int p0 = tile * M_CTA;
+      for (int acc = 0; acc < NACC; ++acc) {
+        const int row0 = p0 + acc * 128 + q * 32;
+        const int pos = row0 + lane;
+        bool valid = false;
+        if (pos < p.P_tot) {
+          const int r = pos % per_frag;
+          const int y = r / p.gc, x = r - (r / p.gc) * p.gc;
+          valid = y < p.out_vr && x < p.out_vc;
+        }
+        const float* md = (p.mul_dact && valid) ? p.mul_dact + (size_t)pos * p.cout : nullptr;
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + buf * (NACC * p.npad) + acc * p.npad;
+        for (int c0 = 0; c0 < p.npad; c0 += 32) {
+          uint32_t r[32];
+          const bool two = c0 + 16 < p.npad;
+          {
+            uint32_t* r0 = r;
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                : "=r"(r0[0]), "=r"(r0[1]), "=r"(r0[2]), "=r"(r0[3]), "=r"(r0[4]), "=r"(r0[5]), "=r"(r0[6]),
+                  "=r"(r0[7]), "=r"(r0[8]), "=r"(r0[9]), "=r"(r0[10]), "=r"(r0[11]), "=r"(r0[12]), "=r"(r0[13]),
+                  "=r"(r0[14]), "=r"(r0[15])
+                : "r"(taddr + c0));
+          }
+          if (two) {
+            uint32_t* r1 = r + 16;
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                : "=r"(r1[0]), "=r"(r1[1]), "=r"(r1[2]), "=r"(r1[3]), "=r"(r1[4]), "=r"(r1[5]), "=r"(r1[6]),
+                  "=r"(r1[7]), "=r"(r1[8]), "=r"(r1[9]), "=r"(r1[10]), "=r"(r1[11]), "=r"(r1[12]), "=r"(r1[13]),
+                  "=r"(r1[14]), "=r"(r1[15])
+                : "r"(taddr + c0 + 16));
+          } else {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int co = c0 + j;
-            if (co < p.cout) {
-              float o = 0.f;
-              if (valid) {
-                o = v[j] + (p.bias ? p.bias[co] : 0.f);
-                o = act_f(p.act, o);
-                if (md) o *= act_d(p.dact, md[co]);
-                if (p.round_out) o = tf32r(o);
+            for (int j = 16; j < 32; ++j) r[j] = 0u;
+          }
+          // operand of the act' multiply (dgrad), 32 contiguous floats of this row
+          float mdv[32];
+          if (md) {
+            if (c0 + 32 <= p.cout) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float4 t = __ldg(reinterpret_cast<const float4*>(md + c0) + j);
+                mdv[4 * j] = t.x; mdv[4 * j + 1] = t.y; mdv[4 * j + 2] = t.z; mdv[4 * j + 3] = t.w;
               }
-              dst[co] = o;
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) mdv[j] = (c0 + j < p.cout) ? __ldg(md + c0 + j) : 0.f;
             }
           }
+          ptx::tmem_ld_wait();
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float o = 0.f;
+            if (valid) {
+              o = act_f(p.act, __uint_as_float(r[j]) + s_bias[(c0 + j) & 255]);
+              if (md) o *= act_d(p.dact, mdv[j]);
+              if (p.round_out) o = tf32r(o);
+            }
+            v[j] = o;
+          }
+          // staging box (swizzled like the TMA SWIZZLE_128B pattern): 16-B chunk jj of
+          // row `lane` lives at lane*128 + ((jj ^ (lane & 7)) * 16)
+          const uint32_t sbuf = sC + (q * 2 + sb) * kStageBytes;
+          if (lane == 0) ptx::bulk_wait_read<1>();  // the store issued from this box 2 stores ago
+          __syncwarp();
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            const uint32_t a = sbuf + lane * 128 + ((jj ^ (lane & 7)) * 16);
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v[4 * jj]), "f"(v[4 * jj + 1]),
+                         "f"(v[4 * jj + 2]), "f"(v[4 * jj + 3])
+                         : "memory");
+          }
+          ptx::fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::tma_store_2d(&tmO, sbuf, c0, row0);
+            ptx::bulk_commit();
+          }
+          sb ^= 1;
         }
       }
+      // every TMEM read of this accumulator set is complete: hand it back to the MMA warp
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(barTempty + 8 * buf);
     }
+    if (lane == 0) ptx::bulk_wait<0>();
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -249,12 +329,24 @@ int base_mode() {
   return e ? atoi(e) : 0;  // measured: the swizzle is address-based, base offset 0
 }
 
+int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
 template <int NACC>
-cudaError_t launch_nacc(const CUtensorMap& A, const CUtensorMap& B, ConvTcParams& p, size_t smem, int tiles,
-                        cudaStream_t s) {
+cudaError_t launch_nacc(const CUtensorMap& A, const CUtensorMap& B, const CUtensorMap& O, ConvTcParams& p,
+                        size_t smem, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  conv_tc_kernel<NACC><<<tiles, kThreads, smem, s>>>(A, B, p);
+  const int grid = p.n_tiles < num_sms() ? p.n_tiles : num_sms();
+  conv_tc_kernel<NACC><<<grid, kThreads, smem, s>>>(A, B, O, p);
   return cudaGetLastError();
 }
 
@@ -262,7 +354,7 @@ cudaError_t launch_nacc(const CUtensorMap& A, const CUtensorMap& B, ConvTcParams
 
 bool tc_supported(int cin, int cout, int k) {
   if (getenv("MPF_DISABLE_TC")) return false;
-  return cin % 4 == 0 && cin >= 24 && cout >= 1 && cout <= 256 && k >= 1 && k <= 8;
+  return cin % 4 == 0 && cin >= 16 && cout % 4 == 0 && cout >= 4 && cout <= 256 && k >= 1 && k <= 8;
 }
 
 cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s) {
@@ -280,13 +372,11 @@ cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s) {
   p.n_cc = (a.cin + kKC - 1) / kKC;
   p.act = a.act;
   p.round_out = a.round_out;
-  p.zero_pad = a.zero_pad;
   p.dact = a.dact;
   p.bias = a.bias;
-  p.out = a.out;
   p.mul_dact = a.mul_dact;
   p.base_mode = base_mode();
-  int nacc = 512 / p.npad;
+  int nacc = 256 / p.npad;  // two accumulator sets in 512 TMEM columns
   if (nacc > 4) nacc = 4;
   if (nacc < 1) nacc = 1;
   const int m_cta = nacc * 128;
@@ -295,26 +385,32 @@ cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s) {
   p.box_rows = ((rows_needed + p.nbox - 1) / p.nbox + 7) / 8 * 8;
   p.a_slot_bytes = (uint32_t)(p.nbox * p.box_rows * 128);
   p.b_slot_bytes = (uint32_t)(p.npad * 128);
-  const size_t budget = 225 * 1024 - 1024 - 256;
-  int nb = (int)((budget - 2 * (size_t)p.a_slot_bytes) / p.b_slot_bytes);
-  if (nb > 6) nb = 6;
+  const size_t fixed = 1024 + 8 * kStageBytes + 4 * 256 + 512;
+  const size_t budget = 227 * 1024 - fixed;
+  int na = 3;
+  while (na > 2 && na * (size_t)p.a_slot_bytes + 4 * (size_t)p.b_slot_bytes > budget) --na;
+  int nb = (int)((budget - na * (size_t)p.a_slot_bytes) / p.b_slot_bytes);
+  if (nb > 8) nb = 8;
   if (nb < 2) return cudaErrorInvalidConfiguration;
+  p.n_aslots = na;
   p.n_bslots = nb;
   uint32_t cols = 32;
-  while (cols < (uint32_t)(nacc * p.npad)) cols <<= 1;
+  while (cols < (uint32_t)(2 * nacc * p.npad)) cols <<= 1;
   p.tmem_cols = cols;
-  const size_t smem = 1024 + 2 * (size_t)p.a_slot_bytes + (size_t)nb * p.b_slot_bytes + 256;
-  CUtensorMap A, B;
+  p.n_tiles = (p.P_tot + m_cta - 1) / m_cta;
+  const size_t smem = fixed + (size_t)na * p.a_slot_bytes + (size_t)nb * p.b_slot_bytes;
+  CUtensorMap A, B, O;
   cudaError_t e = make_map(&A, a.x, (uint64_t)a.cin, (uint64_t)p.P_tot, (uint32_t)p.box_rows);
   if (e != cudaSuccess) return e;
   e = make_map(&B, a.w, (uint64_t)a.k * a.k * a.cin, (uint64_t)a.cout, (uint32_t)p.npad);
   if (e != cudaSuccess) return e;
-  const int tiles = (p.P_tot + m_cta - 1) / m_cta;
+  e = make_map(&O, a.out, (uint64_t)a.cout, (uint64_t)p.P_tot, 32u);
+  if (e != cudaSuccess) return e;
   switch (nacc) {
-    case 1: return launch_nacc<1>(A, B, p, smem, tiles, s);
-    case 2: return launch_nacc<2>(A, B, p, smem, tiles, s);
-    case 3: return launch_nacc<3>(A, B, p, smem, tiles, s);
-    default: return launch_nacc<4>(A, B, p, smem, tiles, s);
+    case 1: return launch_nacc<1>(A, B, O, p, smem, s);
+    case 2: return launch_nacc<2>(A, B, O, p, smem, s);
+    case 3: return launch_nacc<3>(A, B, O, p, smem, s);
+    default: return launch_nacc<4>(A, B, O, p, smem, s);
   }
 }
 

@@ -23,7 +23,7 @@ struct TcConvArgs {
   int act;
   int shift;          // 0 (forward) or -(k-1) (dgrad)
   int round_out;      // round the stored result to tf32 (operand of the next MMA)
-  int zero_pad;       // write zeros at grid positions outside the valid region
+  int zero_pad;       // (SIMT path) write zeros outside the valid region; the TC path always does
   const float* mul_dact;  // nullable: multiply by act'(mul_dact[same position])
   int dact;
 };

@@ -13,12 +13,14 @@
 // so the softmax layer needs no separate weight-gradient pass and the previous layer
 // needs no separate bias pass.
 //
-// Schedule: persistent CTAs (one per SM slot) walk tiles of TP positions.  A tile of h
-// is TP*Ch contiguous floats: one TMA bulk copy into a double-buffered shared buffer,
-// issued one tile ahead.  Phase A: one warp per position, lanes split the Ch-long dot
-// products and combine them with an xor butterfly (bit-identical on every lane).
-// Phase B: thread = (channel ch, position stream); W_L[:, ch] sits in registers, dh is
-// written coalesced and the dW/db partials accumulate in registers.
+// Schedule: persistent CTAs walk tiles of TP = 64 positions.  A tile of h is TP*Ch
+// contiguous floats: one TMA bulk copy into a double-buffered shared buffer, issued one
+// tile ahead; the labels of the tile are gathered while it lands.  Phase A: a warp
+// computes 8 positions at once (4 lanes per position split the Ch-long dot products,
+// rotated per position so the 8 rows hit distinct banks, and combine them with an xor
+// butterfly that is bit-identical on the 4 lanes).  Phase B: thread = (channel ch,
+// position stream); W_L[:, ch] sits in registers, dh is written coalesced and the
+// dW/db partials accumulate in registers.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -30,9 +32,10 @@ namespace mpf {
 
 namespace {
 
-constexpr int kTP = 64;       // positions per tile
+constexpr int kTP = 64;  // positions per tile
 constexpr int kThr = 256;
 constexpr int kMaxC = 16;
+constexpr int kLabBeyond = -1, kLabPad = -2;
 
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
@@ -54,26 +57,27 @@ __host__ __device__ inline size_t head_region0(int C, int Ch) {
   return ((red > tiles ? red : tiles) + 127) / 128 * 128;
 }
 
-template <bool TRAIN>
-__global__ void __launch_bounds__(kThr) head_kernel(HeadArgs a) {
+template <int NC, bool TRAIN>
+__global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int C = a.C, Ch = a.Ch;
   const size_t tile_bytes = (size_t)kTP * Ch * sizeof(float);
-  // [2 mbarriers | pad | region0: two h tiles, later the reduction area | W | b | dl | valid | loss]
+  // [2 mbarriers | pad | region0: two h tiles, later the reduction area | W | b | dl | lab | loss]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
   float* hb0 = reinterpret_cast<float*>(smem_raw + 128);
   float* hb1 = reinterpret_cast<float*>(smem_raw + 128 + tile_bytes);
   float* s_w = reinterpret_cast<float*>(smem_raw + 128 + head_region0(C, Ch));
   float* s_b = s_w + C * Ch;
-  float* s_dl = s_b + kMaxC;
-  int* s_valid = reinterpret_cast<int*>(s_dl + kTP * kMaxC);
-  float* s_loss = reinterpret_cast<float*>(s_valid + kTP);  // [kThr/32]
+  float* s_dl = s_b + kMaxC;                                  // [kTP][NC]
+  int* s_lab = reinterpret_cast<int*>(s_dl + kTP * kMaxC);     // [kTP]
+  float* s_loss = reinterpret_cast<float*>(s_lab + kTP);       // [kThr/32]
   const uint32_t bar0 = ptx::smem_u32(&bars[0]), bar1 = ptx::smem_u32(&bars[1]);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   for (int e = tid; e < C * Ch; e += kThr) s_w[e] = a.w[e];
   for (int e = tid; e < C; e += kThr) s_b[e] = a.b[e];
   const long long per_img = (long long)a.F * a.gr * a.gc;
+  const int frag_sz = a.gr * a.gc;
   const int tpi = a.tiles_per_img;
   const long long total = (long long)a.n * tpi;
   if (tid == 0) {
@@ -93,16 +97,20 @@ __global__ void __launch_bounds__(kThr) head_kernel(HeadArgs a) {
     ptx::bulk_load(ptx::smem_u32(buf ? hb1 : hb0), a.h + ((long long)img * per_img + p0) * Ch, bytes, bar);
   };
 
+  // phase-A mapping: 8 positions per warp, 4 lanes per position
+  const int pa = warp * 8 + (lane >> 2), qa = lane & 3;
+  const int M = Ch >> 2;  // channels per lane (Ch % 4 == 0 path)
+  const int rot = pa % (M > 0 ? M : 1);
   // phase-B mapping: thread -> (channel, stream)
   const int nstreams = kThr / Ch;  // >= 1 (Ch <= 256)
   const int my_ch = tid % Ch, my_stream = tid / Ch;
   const bool b_active = my_stream < nstreams;
-  float wreg[kMaxC];
+  float wreg[NC];
 #pragma unroll
-  for (int c = 0; c < kMaxC; ++c) wreg[c] = (c < C && b_active) ? s_w[c * Ch + my_ch] : 0.f;
-  float accW[kMaxC], accL[kMaxC], accP = 0.f;
+  for (int c = 0; c < NC; ++c) wreg[c] = (c < C && b_active) ? s_w[c * Ch + my_ch] : 0.f;
+  float accW[NC], accL[NC], accP = 0.f;
 #pragma unroll
-  for (int c = 0; c < kMaxC; ++c) { accW[c] = 0.f; accL[c] = 0.f; }
+  for (int c = 0; c < NC; ++c) { accW[c] = 0.f; accL[c] = 0.f; }
 
   // TMA bulk copies need 16-byte granules: Ch % 4 == 0; otherwise a plain cooperative copy
   const bool bulk = (Ch % 4) == 0;
@@ -112,6 +120,36 @@ __global__ void __launch_bounds__(kThr) head_kernel(HeadArgs a) {
     const int cur = it & 1;
     const int img = (int)(tile / tpi), tt = (int)(tile % tpi);
     const long long p0 = (long long)tt * kTP;
+    // ---------------------------------------------------------- phase 0: labels
+    if (tid < kTP) {
+      const long long pos = p0 + tid;
+      int lab = kLabBeyond;
+      if (pos < per_img) {
+        const int gl = (int)(pos / frag_sz);
+        const int rem = (int)(pos - (long long)gl * frag_sz);
+        const int i = rem / a.gc, j = rem - (rem / a.gc) * a.gc;
+        lab = kLabPad;
+        if (i < a.vr && j < a.vc) {
+          lab = 255;
+          if (TRAIN) {
+            // label through the fragment -> pixel map: y = r1 + k1 (r2 + k2 (... + kL i))
+            int yy = i, xx = j, rf = gl;
+            for (int l = a.n_levels - 1; l >= 0; --l) {
+              const int kq = a.pool_k[l];
+              const int d = rf % (kq * kq);
+              rf /= kq * kq;
+              yy = d / kq + kq * yy;
+              xx = d % kq + kq * xx;
+            }
+            if (yy < a.O_H && xx < a.O_W) lab = a.labels[((long long)img * a.O_H + yy) * a.O_W + xx];
+            if (lab != 255 && lab >= C) atomicOr(a.err, 1);
+          } else {
+            lab = 0;
+          }
+        }
+      }
+      s_lab[tid] = lab;
+    }
     if (bulk) {
       ptx::mbar_wait(cur ? bar1 : bar0, (it >> 1) & 1);
       if (tid == 0 && tile + gridDim.x < total) issue(tile + gridDim.x, cur ^ 1);
@@ -120,96 +158,81 @@ __global__ void __launch_bounds__(kThr) head_kernel(HeadArgs a) {
       const long long np = min((long long)kTP, per_img - p0);
       const float* src = a.h + ((long long)img * per_img + p0) * Ch;
       for (int e = tid; e < np * Ch; e += kThr) dst[e] = src[e];
-      __syncthreads();
     }
+    __syncthreads();
     const float* hs = cur ? hb1 : hb0;
     float lossv = 0.f;
     // ---------------------------------------------------------------- phase A
-    for (int p = warp; p < kTP; p += kThr / 32) {
-      const long long pos = p0 + p;
-      const bool inimg = pos < per_img;
-      int gl = 0, i = 0, j = 0;
-      if (inimg) {
-        gl = (int)(pos / ((long long)a.gr * a.gc));
-        const int rem = (int)(pos - (long long)gl * a.gr * a.gc);
-        i = rem / a.gc;
-        j = rem % a.gc;
-      }
-      const bool valid = inimg && i < a.vr && j < a.vc;
-      if (!valid) {  // warp-uniform
-        if (lane < kMaxC) s_dl[p * kMaxC + lane] = 0.f;
-        if (lane == 0) s_valid[p] = inimg ? 0 : -1;
-        continue;
-      }
-      float z[kMaxC];
+    {
+      const int lab = s_lab[pa];
+      const bool need = lab >= 0 && lab < C;
+      float z[NC];
 #pragma unroll
-      for (int c = 0; c < kMaxC; ++c) z[c] = 0.f;
-      const float* hrow = hs + p * Ch;
-      for (int ch = lane; ch < Ch; ch += 32) {
-        const float hv = hrow[ch];
+      for (int c = 0; c < NC; ++c) z[c] = 0.f;
+      if (need) {  // uniform over the 4 lanes of a position
+        const float* hrow = hs + pa * Ch;
+        if (bulk) {
+          for (int m = 0; m < M; ++m) {
+            int mm = m + rot;
+            if (mm >= M) mm -= M;
+            const int ch = qa + 4 * mm;
+            const float hv = hrow[ch];
 #pragma unroll
-        for (int c = 0; c < kMaxC; ++c)
-          if (c < C) z[c] = fmaf(s_w[c * Ch + ch], hv, z[c]);
-      }
+            for (int c = 0; c < NC; ++c)
+              if (c < C) z[c] = fmaf(s_w[c * Ch + ch], hv, z[c]);
+          }
+        } else {
+          for (int ch = qa; ch < Ch; ch += 4) {
+            const float hv = hrow[ch];
 #pragma unroll
-      for (int c = 0; c < kMaxC; ++c) {
-        if (c < C) {
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) z[c] += __shfl_xor_sync(0xffffffffu, z[c], o);
-          z[c] += s_b[c];
+            for (int c = 0; c < NC; ++c)
+              if (c < C) z[c] = fmaf(s_w[c * Ch + ch], hv, z[c]);
+          }
         }
       }
-      float mx = z[0];
+      // 4-lane butterfly (the lanes of one position are lane^1, lane^2: same group);
+      // executed by every lane of the warp
 #pragma unroll
-      for (int c = 1; c < kMaxC; ++c)
-        if (c < C) mx = fmaxf(mx, z[c]);
-      float se = 0.f;
+      for (int c = 0; c < NC; ++c) {
+        z[c] += __shfl_xor_sync(0xffffffffu, z[c], 1);
+        z[c] += __shfl_xor_sync(0xffffffffu, z[c], 2);
+        z[c] += (c < C) ? s_b[c] : 0.f;
+      }
+      if (need) {
+        float mx = z[0];
 #pragma unroll
-      for (int c = 0; c < kMaxC; ++c)
-        if (c < C) se += expf(z[c] - mx);
-      const float lse = mx + logf(se);
-      if (!TRAIN) {
-        if (lane < C) {
-          float pc = 0.f;
+        for (int c = 1; c < NC; ++c)
+          if (c < C) mx = fmaxf(mx, z[c]);
+        float se = 0.f;
 #pragma unroll
-          for (int c = 0; c < kMaxC; ++c)
-            if (c == lane) pc = expf(z[c] - lse);
+        for (int c = 0; c < NC; ++c)
+          if (c < C) se += expf(z[c] - mx);
+        const float lse = mx + logf(se);
+        if (!TRAIN) {
+          const long long pos = p0 + pa;
+          const int gl = (int)(pos / frag_sz);
+          const int rem = (int)(pos - (long long)gl * frag_sz);
+          const int i = rem / a.gc, j = rem - (rem / a.gc) * a.gc;
           const long long g = (long long)img * a.F + gl;
-          a.probs[((g * a.vr + i) * a.vc + j) * C + lane] = pc;
-        }
-        continue;
-      }
-      // label through the fragment -> pixel map: y = r1 + k1 (r2 + k2 (... + kL i))
-      int yy = i, xx = j, rf = gl;
-      for (int l = a.n_levels - 1; l >= 0; --l) {
-        const int kq = a.pool_k[l];
-        const int d = rf % (kq * kq);
-        rf /= kq * kq;
-        yy = d / kq + kq * yy;
-        xx = d % kq + kq * xx;
-      }
-      int t = 255;
-      if (yy < a.O_H && xx < a.O_W) t = a.labels[((long long)img * a.O_H + yy) * a.O_W + xx];
-      if (t != 255 && t >= C && lane == 0) atomicOr(a.err, 1);
-      const int nl = a.nlab[img];
-      float dlv = 0.f;
-      if (t < C && nl > 0) {
-        const float wt = a.cw[t];
-        float zt = 0.f;
+          float* pr = a.probs + ((g * a.vr + i) * a.vc + j) * C;
 #pragma unroll
-        for (int c = 0; c < kMaxC; ++c)
-          if (c == t) zt = z[c];
-        if (lane == 0) lossv += wt * (lse - zt);
-        if (lane < C) {
-          float zl = 0.f;
+          for (int c = 0; c < NC; ++c)
+            if (c < C && (c & 3) == qa) pr[c] = expf(z[c] - lse);
+        } else {
+          const int nl = a.nlab[img];
+          const float wt = a.cw[lab];
+          float zt = 0.f;
 #pragma unroll
-          for (int c = 0; c < kMaxC; ++c)
-            if (c == lane) zl = z[c];
-          dlv = wt * (expf(zl - lse) - (lane == t ? 1.f : 0.f)) / (float)nl;
+          for (int c = 0; c < NC; ++c)
+            if (c == lab) zt = z[c];
+          if (qa == 0) lossv = wt * (lse - zt);
+          const float inv = nl > 0 ? wt / (float)nl : 0.f;
+#pragma unroll
+          for (int c = 0; c < NC; ++c)
+            if ((c & 3) == qa)
+              s_dl[pa * NC + c] = (c < C) ? inv * (expf(z[c] - lse) - (c == lab ? 1.f : 0.f)) : 0.f;
         }
       }
-      if (lane < kMaxC) s_dl[p * kMaxC + lane] = lane < C ? dlv : 0.f;
-      if (lane == 0) s_valid[p] = 1;
     }
     if (TRAIN) {
       // per-tile loss: fixed-order block sum
@@ -228,17 +251,17 @@ __global__ void __launch_bounds__(kThr) head_kernel(HeadArgs a) {
       if (b_active) {
         float* dh_img = a.dh + ((long long)img * per_img + p0) * Ch;
         for (int p = my_stream; p < kTP; p += nstreams) {
-          const int vflag = s_valid[p];
-          if (vflag < 0) continue;          // past the end of the image
+          const int lab = s_lab[p];
+          if (lab == kLabBeyond) continue;  // past the end of the image
           float d = 0.f;
-          if (vflag > 0) {
+          if (lab >= 0 && lab < C) {
             const float hv = hs[p * Ch + my_ch];
-            float dl[kMaxC];
+            float dl[NC];
 #pragma unroll
-            for (int c = 0; c < kMaxC; ++c) dl[c] = s_dl[p * kMaxC + c];
+            for (int c = 0; c < NC; ++c) dl[c] = s_dl[p * NC + c];
             float sacc = 0.f;
 #pragma unroll
-            for (int c = 0; c < kMaxC; ++c) {
+            for (int c = 0; c < NC; ++c) {
               sacc = fmaf(wreg[c], dl[c], sacc);
               accW[c] = fmaf(dl[c], hv, accW[c]);
               accL[c] += dl[c];
@@ -259,14 +282,14 @@ __global__ void __launch_bounds__(kThr) head_kernel(HeadArgs a) {
   const int RW = C + 1;
   if (b_active) {
 #pragma unroll
-    for (int c = 0; c < kMaxC; ++c)
+    for (int c = 0; c < NC; ++c)
       if (c < C) red[(my_stream * Ch + my_ch) * RW + c] = accW[c];
     red[(my_stream * Ch + my_ch) * RW + C] = accP;
   }
   float* redL = red + nstreams * Ch * RW;
   if (b_active && my_ch == 0) {
 #pragma unroll
-    for (int c = 0; c < kMaxC; ++c)
+    for (int c = 0; c < NC; ++c)
       if (c < C) redL[my_stream * kMaxC + c] = accL[c];
   }
   __syncthreads();
@@ -293,6 +316,22 @@ size_t head_smem(int C, int Ch) {
          sizeof(float) * (kThr / 32);
 }
 
+template <int NC>
+cudaError_t launch_nc(const HeadArgs& a, size_t smem, cudaStream_t s) {
+  if (a.probs) {
+    cudaError_t e =
+        cudaFuncSetAttribute(head_kernel<NC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    head_kernel<NC, false><<<a.n_blocks, kThr, smem, s>>>(a);
+  } else {
+    cudaError_t e =
+        cudaFuncSetAttribute(head_kernel<NC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    head_kernel<NC, true><<<a.n_blocks, kThr, smem, s>>>(a);
+  }
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 int head_tiles_per_image(long long per_img) { return (int)((per_img + kTP - 1) / kTP); }
@@ -308,18 +347,11 @@ bool head_supported(int C, int Ch) {
 }
 
 cudaError_t launch_head2(const HeadArgs& a, cudaStream_t s) {
-  const int nb = a.n_blocks;
   const size_t smem = head_smem(a.C, a.Ch);
-  if (a.probs) {
-    cudaError_t e = cudaFuncSetAttribute(head_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    head_kernel<false><<<nb, kThr, smem, s>>>(a);
-  } else {
-    cudaError_t e = cudaFuncSetAttribute(head_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    head_kernel<true><<<nb, kThr, smem, s>>>(a);
-  }
-  return cudaGetLastError();
+  if (a.C <= 2) return launch_nc<2>(a, smem, s);
+  if (a.C <= 4) return launch_nc<4>(a, smem, s);
+  if (a.C <= 8) return launch_nc<8>(a, smem, s);
+  return launch_nc<16>(a, smem, s);
 }
 
 }  // namespace mpf

@@ -242,38 +242,52 @@ cudaError_t launch_wgrad_reduce(const float* pw, const float* pb, int n_split, i
 }
 
 // ============================================================================ small kernels
+// labelled pixels per image: integer partial counts combined with integer atomics
+// (exact, order-independent)
 __global__ void label_count_kernel(const uint8_t* __restrict__ labels, int hw, int classes, int* nlab) {
   __shared__ int s_red[32];
-  const int img = blockIdx.x;
+  const int img = blockIdx.y;
   int c = 0;
-  for (int e = threadIdx.x; e < hw; e += blockDim.x) c += labels[(long long)img * hw + e] < classes;
+  const uint8_t* L = labels + (long long)img * hw;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < hw; e += gridDim.x * blockDim.x) c += L[e] < classes;
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = c;
   __syncthreads();
   if (threadIdx.x == 0) {
-    int s = 0;
-    for (int w = 0; w < (int)(blockDim.x / 32); ++w) s += s_red[w];
-    nlab[img] = s;
+    int t = 0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) t += s_red[w];
+    atomicAdd(nlab + img, t);
   }
 }
 
 cudaError_t launch_label_count(const uint8_t* labels, int n, int hw, int classes, int* nlab, cudaStream_t s) {
-  label_count_kernel<<<n, 1024, 0, s>>>(labels, hw, classes, nlab);
+  cudaError_t e = cudaMemsetAsync(nlab, 0, sizeof(int) * n, s);
+  if (e != cudaSuccess) return e;
+  int bx = (hw + 256 * 16 - 1) / (256 * 16);
+  if (bx > 64) bx = 64;
+  label_count_kernel<<<dim3(bx, n), 256, 0, s>>>(labels, hw, classes, nlab);
   return cudaGetLastError();
 }
 
+// per-image loss = (sum of the per-tile partials, fixed tree order) / n_lab
 __global__ void loss_finalize_kernel(const float* __restrict__ part, int parts, const int* __restrict__ nlab,
-                                     int n, float* loss) {
-  const int img = blockIdx.x * blockDim.x + threadIdx.x;
-  if (img >= n) return;
-  float s = 0.f;
-  for (int i = 0; i < parts; ++i) s += part[(long long)img * parts + i];
-  loss[img] = nlab[img] > 0 ? s / (float)nlab[img] : 0.f;
+                                     float* loss) {
+  __shared__ float s[256];
+  const int img = blockIdx.x;
+  float t = 0.f;
+  for (int i = threadIdx.x; i < parts; i += 256) t += part[(long long)img * parts + i];
+  s[threadIdx.x] = t;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) loss[img] = nlab[img] > 0 ? s[0] / (float)nlab[img] : 0.f;
 }
 
 cudaError_t launch_loss_finalize(const float* part, int parts, const int* nlab, int n, float* loss,
                                  cudaStream_t s) {
-  loss_finalize_kernel<<<(n + 127) / 128, 128, 0, s>>>(part, parts, nlab, n, loss);
+  loss_finalize_kernel<<<n, 256, 0, s>>>(part, parts, nlab, loss);
   return cudaGetLastError();
 }
 
