@@ -38,7 +38,8 @@ namespace mpf {
 
 namespace {
 
-constexpr int kThreads = 192;  // 6 warps
+constexpr int kEpiWarps = 8;   // two per TMEM lane quarter, splitting the column chunks
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kKC = 32;        // fp32 channels per 128-byte row
 constexpr uint32_t kStageBytes = 32 * 128;  // one epilogue store box: 32 rows x 32 fp32
 
@@ -61,9 +62,12 @@ __device__ __forceinline__ float tf32r(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
+// tanh(v) = 1 - 2 / (exp(2v) + 1): two MUFU ops, absolute error ~1e-7 (far below the
+// TF32 rounding of every tensor-core operand), saturates correctly at +-inf.
+__device__ __forceinline__ float fast_tanh(float v) { return 1.f - __fdividef(2.f, __expf(2.f * v) + 1.f); }
 __device__ __forceinline__ float act_f(int act, float v) {
-  if (act == MPF_TANH) return tanhf(v);
-  if (act == MPF_LOGISTIC) return 1.f / (1.f + expf(-v));
+  if (act == MPF_TANH) return fast_tanh(v);
+  if (act == MPF_LOGISTIC) return __fdividef(1.f, 1.f + __expf(-v));
   return v;
 }
 __device__ __forceinline__ float act_d(int act, float y) {
@@ -81,8 +85,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sbase = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
   const uint32_t sA = sbase;                                   // A slabs
   const uint32_t sB = sA + p.n_aslots * p.a_slot_bytes;        // weight taps
-  const uint32_t sC = sB + p.n_bslots * p.b_slot_bytes;        // epilogue staging: 4 warps x 2 boxes
-  const uint32_t sBias = sC + 8 * kStageBytes;                 // [npad] fp32
+  const uint32_t sC = sB + p.n_bslots * p.b_slot_bytes;        // epilogue staging: 2 boxes per warp
+  const uint32_t sBias = sC + 2 * kEpiWarps * kStageBytes;     // [npad] fp32
   const uint32_t sBar = sBias + 4 * 256;
   const uint32_t barAfull = sBar, barAempty = barAfull + 8 * p.n_aslots;
   const uint32_t barBfull = barAempty + 8 * p.n_aslots, barBempty = barBfull + 8 * p.n_bslots;
@@ -109,7 +113,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(barTfull + 8 * i, 1);
-      ptx::mbar_init(barTempty + 8 * i, 4);  // one arrive per epilogue warp
+      ptx::mbar_init(barTempty + 8 * i, kEpiWarps);  // one arrive per epilogue warp
     }
     ptx::fence_mbar_init();
   }
@@ -191,8 +195,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
     }
   } else {
-    // ------------------------------------------------------------ epilogue (warps 2..5)
+    // ------------------------------------------------------------ epilogue (warps 2..)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;  // which alternate 32-column chunks this warp stores
+    const int ew = warp - 2;
     const int per_frag = p.gr * p.gc;
     int lt = 0, sb = 0;
     for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++lt) {
@@ -211,7 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const float* md = (p.mul_dact && valid) ? p.mul_dact + (size_t)pos * p.cout : nullptr;
         const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + buf * (NACC * p.npad) + acc * p.npad;
-        for (int c0 = 0; c0 < p.npad; c0 += 32) {
+        for (int c0 = 32 * half; c0 < p.npad; c0 += 64) {
           uint32_t r[32];
           const bool two = c0 + 16 < p.npad;
           {
@@ -255,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 32; ++j) {
             float o = 0.f;
             if (valid) {
-              o = act_f(p.act, __uint_as_float(r[j]) + s_bias[(c0 + j) & 255]);
+              o = act_f(p.act, __uint_as_float(r[j]) + s_bias[c0 + j]);
               if (md) o *= act_d(p.dact, mdv[j]);
               if (p.round_out) o = tf32r(o);
             }
@@ -263,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           // staging box (swizzled like the TMA SWIZZLE_128B pattern): 16-B chunk jj of
           // row `lane` lives at lane*128 + ((jj ^ (lane & 7)) * 16)
-          const uint32_t sbuf = sC + (q * 2 + sb) * kStageBytes;
+          const uint32_t sbuf = sC + (ew * 2 + sb) * kStageBytes;
           if (lane == 0) ptx::bulk_wait_read<1>();  // the store issued from this box 2 stores ago
           __syncwarp();
 #pragma unroll
@@ -385,7 +391,7 @@ cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s) {
   p.box_rows = ((rows_needed + p.nbox - 1) / p.nbox + 7) / 8 * 8;
   p.a_slot_bytes = (uint32_t)(p.nbox * p.box_rows * 128);
   p.b_slot_bytes = (uint32_t)(p.npad * 128);
-  const size_t fixed = 1024 + 8 * kStageBytes + 4 * 256 + 512;
+  const size_t fixed = 1024 + 2 * kEpiWarps * kStageBytes + 4 * 256 + 512;
   const size_t budget = 227 * 1024 - fixed;
   int na = 3;
   while (na > 2 && na * (size_t)p.a_slot_bytes + 4 * (size_t)p.b_slot_bytes > budget) --na;
