@@ -348,10 +348,13 @@ bool head_supported(int C, int Ch) {
 
 cudaError_t launch_head2(const HeadArgs& a, cudaStream_t s) {
   const size_t smem = head_smem(a.C, a.Ch);
-  if (a.C <= 2) return launch_nc<2>(a, smem, s);
-  if (a.C <= 4) return launch_nc<4>(a, smem, s);
-  if (a.C <= 8) return launch_nc<8>(a, smem, s);
-  return launch_nc<16>(a, smem, s);
+  switch (a.C) {  // exact class counts of the common heads; padded beyond
+    case 2: return launch_nc<2>(a, smem, s);
+    case 3: return launch_nc<3>(a, smem, s);
+    case 4: return launch_nc<4>(a, smem, s);
+    case 5: return launch_nc<5>(a, smem, s);
+    default: return a.C <= 8 ? launch_nc<8>(a, smem, s) : launch_nc<16>(a, smem, s);
+  }
 }
 
 }  // namespace mpf

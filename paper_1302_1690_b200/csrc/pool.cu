@@ -22,6 +22,7 @@
 // All index arithmetic is 32-bit per fragment; only final offsets are 64-bit.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "mpf_internal.h"
 
@@ -292,6 +293,123 @@ __global__ void __launch_bounds__(256) mpf_bwd_kernel(MpfBwdArgs a) {
   }
 }
 
+// Sliding-window gather for K in {2,3,4} and 4-channel vectors: a thread keeps the
+// argmax bytes of the K window rows that can select its current row (K x K uchar4 in
+// registers), loads one new window row per output row, and fetches delta + pooled
+// value only for matching windows with predicated loads (no branches between the
+// independent loads).
+__device__ __forceinline__ float4 ldg4_pred(const float* p, bool pred) {
+  float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+      "@q ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];\n\t}"
+      : "+f"(r.x), "+f"(r.y), "+f"(r.z), "+f"(r.w)
+      : "l"(p), "r"((int)pred));
+  return r;
+}
+__device__ __forceinline__ uint32_t ldg_u32_pred(const uint8_t* p, bool pred) {
+  uint32_t r = 0xFFFFFFFFu;  // matches no window index (indices < K^2 <= 16)
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+      "@q ld.global.nc.u32 %0, [%1];\n\t}"
+      : "+r"(r)
+      : "l"(p), "r"((int)pred));
+  return r;
+}
+
+constexpr int kBandB = 32;  // output rows per thread (backward, sliding)
+
+template <int K>
+__global__ void __launch_bounds__(256) mpf_bwd_slide_kernel(MpfBwdArgs a) {
+  extern __shared__ float s_red[];  // [blockDim.y][C]
+  const int cv = threadIdx.x;
+  const int X = blockIdx.x * blockDim.y + threadIdx.y;
+  const int Xw = K * a.m_c, Yw = K * a.m_r;
+  const int y0 = blockIdx.y * kBandB, y1 = min(y0 + kBandB, a.gr);
+  const int C = a.C;
+  const int MM = a.m_r * a.m_c;  // cells per output fragment
+  float bsum[4] = {0.f, 0.f, 0.f, 0.f};
+  if (X < a.gc) {
+    // column part of the cell index for each dx (window column wx = X - dx)
+    int colpart[K];
+    bool cval[K];
+#pragma unroll
+    for (int dx = 0; dx < K; ++dx) {
+      const int wx = X - dx;
+      cval[dx] = wx >= 0 && wx < Xw;
+      colpart[dx] = cval[dx] ? (wx % K) * MM + wx / K : 0;
+    }
+    for (int g = blockIdx.z; g < a.n_frag_in; g += gridDim.z) {
+      const size_t fbase = (size_t)g * K * K * MM;  // first cell of the input fragment's k^2 outputs
+      auto rowpart = [&](int wy) { return (wy % K) * K * MM + (wy / K) * a.m_c; };
+      auto load_row = [&](int wy, uint32_t (&idr)[K]) {
+        const bool rv = wy >= 0 && wy < Yw;
+        const int rp = rv ? rowpart(wy) : 0;
+#pragma unroll
+        for (int dx = 0; dx < K; ++dx)
+          idr[dx] = ldg_u32_pred(a.idx + (fbase + rp + colpart[dx]) * C + cv * 4, rv && cval[dx]);
+      };
+      uint32_t id[K][K];  // id[dy][dx]: window row Y - dy (pre-filled one row behind: the loop shifts first)
+#pragma unroll
+      for (int dy = 1; dy < K; ++dy) load_row(y0 - dy, id[dy - 1]);
+      for (int Y = y0; Y < y1; ++Y) {
+#pragma unroll
+        for (int dy = K - 1; dy > 0; --dy)
+#pragma unroll
+          for (int dx = 0; dx < K; ++dx) id[dy][dx] = id[dy - 1][dx];
+        load_row(Y, id[0]);
+        float acc[4] = {0.f, 0.f, 0.f, 0.f}, val[4] = {0.f, 0.f, 0.f, 0.f};
+        bool hit[4] = {false, false, false, false};
+#pragma unroll
+        for (int dy = 0; dy < K; ++dy) {
+          const int wy = Y - dy;
+          const int rp = (wy >= 0) ? rowpart(wy) : 0;
+#pragma unroll
+          for (int dx = 0; dx < K; ++dx) {
+            const uint32_t want = (uint32_t)(dy * K + dx);
+            const uint32_t w = id[dy][dx];
+            bool m[4];
+            bool any = false;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              m[v] = ((w >> (8 * v)) & 0xFFu) == want;
+              any |= m[v];
+            }
+            const size_t cell = (fbase + rp + colpart[dx]) * C + cv * 4;
+            const float4 d = ldg4_pred(a.dout + cell, any);
+            const float4 pv = ldg4_pred(a.pooled + cell, any);
+            const float dd[4] = {d.x, d.y, d.z, d.w}, pp[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+              if (m[v]) { acc[v] += dd[v]; val[v] = pp[v]; hit[v] = true; }
+          }
+        }
+        float o[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const float dv = hit[v] ? acc[v] * act_der(a.act, val[v]) : 0.f;
+          bsum[v] += dv;
+          o[v] = a.round_tf32 ? tf32_rna(dv) : dv;
+        }
+        stv<4>(a.din + (((size_t)g * a.gr + Y) * a.gc + X) * C + cv * 4, o);
+      }
+    }
+  }
+  if (a.bias_part == nullptr) return;
+#pragma unroll
+  for (int v = 0; v < 4; ++v) s_red[threadIdx.y * C + cv * 4 + v] = bsum[v];
+  __syncthreads();
+  if (threadIdx.y == 0) {
+    const size_t blin = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      float t = 0.f;
+      for (int q = 0; q < (int)blockDim.y; ++q) t += s_red[q * C + cv * 4 + v];
+      a.bias_part[blin * C + cv * 4 + v] = t;
+    }
+  }
+}
+
 // ----------------------------------------------------------------------------- channel sums
 // Generic per-channel partials of a [P][C] tensor (bias gradient of a conv whose delta
 // comes from a dgrad, i.e. a conv followed by another conv).
@@ -349,9 +467,12 @@ cudaError_t launch_mpf_fwd(const MpfArgs& a, cudaStream_t s) {
   return fwd_dispatch<1>(a, s);
 }
 
+static bool bwd_slide(const MpfBwdArgs& a) { return a.C % 4 == 0 && a.k >= 2 && a.k <= 4; }
+
 static void bwd_geometry(const MpfBwdArgs& a, int V, dim3* grid, dim3* blk) {
   const int ty = block_dims(a.C, V, blk);
-  *grid = dim3((a.gc + ty - 1) / ty, (a.gr + kBand - 1) / kBand, a.n_frag_in < 65535 ? a.n_frag_in : 65535);
+  const int band = bwd_slide(a) ? kBandB : kBand;
+  *grid = dim3((a.gc + ty - 1) / ty, (a.gr + band - 1) / band, a.n_frag_in < 65535 ? a.n_frag_in : 65535);
 }
 
 long long mpf_bwd_partials(const MpfBwdArgs& a) {
@@ -365,7 +486,11 @@ cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s) {
   dim3 grid, blk;
   bwd_geometry(a, V, &grid, &blk);
   const size_t smem = sizeof(float) * blk.y * a.C;
-  if (V == 4)
+  if (bwd_slide(a) && !getenv("MPF_BWD_GENERIC")) {
+    if (a.k == 2) mpf_bwd_slide_kernel<2><<<grid, blk, smem, s>>>(a);
+    else if (a.k == 3) mpf_bwd_slide_kernel<3><<<grid, blk, smem, s>>>(a);
+    else mpf_bwd_slide_kernel<4><<<grid, blk, smem, s>>>(a);
+  } else if (V == 4)
     mpf_bwd_kernel<4><<<grid, blk, smem, s>>>(a);
   else
     mpf_bwd_kernel<1><<<grid, blk, smem, s>>>(a);
