@@ -51,8 +51,8 @@ __device__ __forceinline__ float act_der(int act, float y) {
 
 // bytes of region0: two h tiles, or the end-of-kernel reduction area if larger
 __host__ __device__ inline size_t head_region0(int C, int Ch) {
-  const int nstreams = kThr / Ch;
-  const size_t red = sizeof(float) * ((size_t)nstreams * Ch * (C + 1) + (size_t)nstreams * kMaxC);
+  const int nw = kThr / 32;
+  const size_t red = sizeof(float) * ((size_t)nw * Ch * (C + 1) + (size_t)nw * kMaxC);
   const size_t tiles = 2 * (size_t)kTP * Ch * sizeof(float);
   return ((red > tiles ? red : tiles) + 127) / 128 * 128;
 }
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int C = a.C, Ch = a.Ch;
   const size_t tile_bytes = (size_t)kTP * Ch * sizeof(float);
-  // [2 mbarriers | pad | region0: two h tiles, later the reduction area | W | b | dl | lab | loss]
+  // [2 mbarriers | pad | region0: two h tiles, later the reduction area | W | b | dl | lab]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
   float* hb0 = reinterpret_cast<float*>(smem_raw + 128);
   float* hb1 = reinterpret_cast<float*>(smem_raw + 128 + tile_bytes);
@@ -70,7 +70,6 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
   float* s_b = s_w + C * Ch;
   float* s_dl = s_b + kMaxC;                                  // [kTP][NC]
   int* s_lab = reinterpret_cast<int*>(s_dl + kTP * kMaxC);     // [kTP]
-  float* s_loss = reinterpret_cast<float*>(s_lab + kTP);       // [kThr/32]
   const uint32_t bar0 = ptx::smem_u32(&bars[0]), bar1 = ptx::smem_u32(&bars[1]);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
@@ -97,20 +96,22 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
     ptx::bulk_load(ptx::smem_u32(buf ? hb1 : hb0), a.h + ((long long)img * per_img + p0) * Ch, bytes, bar);
   };
 
-  // phase-A mapping: 8 positions per warp, 4 lanes per position
-  const int pa = warp * 8 + (lane >> 2), qa = lane & 3;
-  const int M = Ch >> 2;  // channels per lane (Ch % 4 == 0 path)
+  // Every warp owns 8 positions of a tile: phase A maps 4 lanes to a position, phase B
+  // maps lanes to channels; only the tile-buffer hand-off needs the whole block.
+  const int pw0 = warp * 8;                       // first position of this warp
+  const int pa = pw0 + (lane >> 2), qa = lane & 3;
+  const int M = Ch >> 2;  // channels per lane in phase A (Ch % 4 == 0 path)
   const int rot = pa % (M > 0 ? M : 1);
-  // phase-B mapping: thread -> (channel, stream)
-  const int nstreams = kThr / Ch;  // >= 1 (Ch <= 256)
-  const int my_ch = tid % Ch, my_stream = tid / Ch;
-  const bool b_active = my_stream < nstreams;
-  float wreg[NC];
+  constexpr int kMC = 8;  // channel slots per lane in phase B (Ch <= 256)
+  float accW[kMC][NC], accP[kMC], accL[NC];
 #pragma unroll
-  for (int c = 0; c < NC; ++c) wreg[c] = (c < C && b_active) ? s_w[c * Ch + my_ch] : 0.f;
-  float accW[NC], accL[NC], accP = 0.f;
+  for (int m = 0; m < kMC; ++m) {
+    accP[m] = 0.f;
 #pragma unroll
-  for (int c = 0; c < NC; ++c) { accW[c] = 0.f; accL[c] = 0.f; }
+    for (int c = 0; c < NC; ++c) accW[m][c] = 0.f;
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) accL[c] = 0.f;
 
   // TMA bulk copies need 16-byte granules: Ch % 4 == 0; otherwise a plain cooperative copy
   const bool bulk = (Ch % 4) == 0;
@@ -120,9 +121,9 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
     const int cur = it & 1;
     const int img = (int)(tile / tpi), tt = (int)(tile % tpi);
     const long long p0 = (long long)tt * kTP;
-    // ---------------------------------------------------------- phase 0: labels
-    if (tid < kTP) {
-      const long long pos = p0 + tid;
+    // ---------------------------------------------------------- phase 0: labels (lanes 0..7)
+    if (lane < 8) {
+      const long long pos = p0 + pw0 + lane;
       int lab = kLabBeyond;
       if (pos < per_img) {
         const int gl = (int)(pos / frag_sz);
@@ -148,18 +149,18 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
           }
         }
       }
-      s_lab[tid] = lab;
+      s_lab[pw0 + lane] = lab;
     }
     if (bulk) {
       ptx::mbar_wait(cur ? bar1 : bar0, (it >> 1) & 1);
       if (tid == 0 && tile + gridDim.x < total) issue(tile + gridDim.x, cur ^ 1);
     } else {
-      float* dst = cur ? hb1 : hb0;
-      const long long np = min((long long)kTP, per_img - p0);
-      const float* src = a.h + ((long long)img * per_img + p0) * Ch;
-      for (int e = tid; e < np * Ch; e += kThr) dst[e] = src[e];
+      float* dst = (cur ? hb1 : hb0) + pw0 * Ch;
+      const long long np = min(8LL, per_img - p0 - pw0);
+      const float* src = a.h + ((long long)img * per_img + p0 + pw0) * Ch;
+      for (int e = lane; e < np * Ch; e += 32) dst[e] = src[e];
     }
-    __syncthreads();
+    __syncwarp();
     const float* hs = cur ? hb1 : hb0;
     float lossv = 0.f;
     // ---------------------------------------------------------------- phase A
@@ -235,62 +236,68 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
       }
     }
     if (TRAIN) {
-      // per-tile loss: fixed-order block sum
+      // per-(tile, warp) loss: fixed-order warp sum
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) lossv += __shfl_xor_sync(0xffffffffu, lossv, o);
-      if (lane == 0) s_loss[warp] = lossv;
-    }
-    __syncthreads();
-    if (TRAIN) {
-      if (tid == 0) {
-        float s = 0.f;
-        for (int w = 0; w < kThr / 32; ++w) s += s_loss[w];
-        a.loss_part[(long long)img * tpi + tt] = s;
-      }
+      if (lane == 0) a.loss_part[((long long)img * tpi + tt) * (kThr / 32) + warp] = lossv;
+      __syncwarp();
       // -------------------------------------------------------------- phase B
-      if (b_active) {
-        float* dh_img = a.dh + ((long long)img * per_img + p0) * Ch;
-        for (int p = my_stream; p < kTP; p += nstreams) {
-          const int lab = s_lab[p];
-          if (lab == kLabBeyond) continue;  // past the end of the image
-          float d = 0.f;
-          if (lab >= 0 && lab < C) {
-            const float hv = hs[p * Ch + my_ch];
-            float dl[NC];
+      float* dh_img = a.dh + ((long long)img * per_img + p0) * Ch;
+      for (int q = 0; q < 8; ++q) {
+        const int p = pw0 + q;
+        const int lab = s_lab[p];  // warp-uniform
+        if (lab == kLabBeyond) break;  // past the end of the image (and so are the rest)
+        const bool act = lab >= 0 && lab < C;
+        float dl[NC];
 #pragma unroll
-            for (int c = 0; c < NC; ++c) dl[c] = s_dl[p * NC + c];
-            float sacc = 0.f;
+        for (int c = 0; c < NC; ++c) dl[c] = act ? s_dl[p * NC + c] : 0.f;
+        if (act && lane == 0) {
 #pragma unroll
-            for (int c = 0; c < NC; ++c) {
-              sacc = fmaf(wreg[c], dl[c], sacc);
-              accW[c] = fmaf(dl[c], hv, accW[c]);
-              accL[c] += dl[c];
+          for (int c = 0; c < NC; ++c) accL[c] += dl[c];
+        }
+#pragma unroll
+        for (int m = 0; m < kMC; ++m) {
+          const int ch = lane + 32 * m;
+          if (ch < Ch) {
+            float d = 0.f;
+            if (act) {
+              const float hv = hs[p * Ch + ch];
+              float sacc = 0.f;
+#pragma unroll
+              for (int c = 0; c < NC; ++c) {
+                sacc = fmaf(s_w[c * Ch + ch], dl[c], sacc);
+                accW[m][c] = fmaf(dl[c], hv, accW[m][c]);
+              }
+              d = sacc * act_der(a.hidden_act, hv);
+              accP[m] += d;
             }
-            d = sacc * act_der(a.hidden_act, hv);
-            accP += d;
+            dh_img[(long long)p * Ch + ch] = a.round_tf32 ? tf32_rna(d) : d;
           }
-          dh_img[(long long)p * Ch + my_ch] = a.round_tf32 ? tf32_rna(d) : d;
         }
       }
     }
-    __syncthreads();
+    __syncthreads();  // every warp is done with this tile buffer before it is refilled
   }
   if (!TRAIN) return;
   // ------------------------------------------------------------------ block partials
-  // red[stream][ch][0..C) = accW, red[..][C] = accP, and accL from ch == 0 threads
+  // red[warp][ch][0..C) = accW, red[warp][ch][C] = accP; redL[warp][c] = accL (lane 0)
   float* red = hb0;  // tiles are no longer needed
   const int RW = C + 1;
-  if (b_active) {
 #pragma unroll
-    for (int c = 0; c < NC; ++c)
-      if (c < C) red[(my_stream * Ch + my_ch) * RW + c] = accW[c];
-    red[(my_stream * Ch + my_ch) * RW + C] = accP;
+  for (int m = 0; m < kMC; ++m) {
+    const int ch = lane + 32 * m;
+    if (ch < Ch) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        if (c < C) red[(warp * Ch + ch) * RW + c] = accW[m][c];
+      red[(warp * Ch + ch) * RW + C] = accP[m];
+    }
   }
-  float* redL = red + nstreams * Ch * RW;
-  if (b_active && my_ch == 0) {
+  float* redL = red + (kThr / 32) * Ch * RW;
+  if (lane == 0) {
 #pragma unroll
     for (int c = 0; c < NC; ++c)
-      if (c < C) redL[my_stream * kMaxC + c] = accL[c];
+      if (c < C) redL[warp * kMaxC + c] = accL[c];
   }
   __syncthreads();
   const int E = C * Ch + C + Ch;
@@ -299,21 +306,20 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
     float s = 0.f;
     if (e < C * Ch) {
       const int c = e / Ch, ch = e % Ch;
-      for (int q = 0; q < nstreams; ++q) s += red[(q * Ch + ch) * RW + c];
+      for (int q = 0; q < kThr / 32; ++q) s += red[(q * Ch + ch) * RW + c];
     } else if (e < C * Ch + C) {
       const int c = e - C * Ch;
-      for (int q = 0; q < nstreams; ++q) s += redL[q * kMaxC + c];
+      for (int q = 0; q < kThr / 32; ++q) s += redL[q * kMaxC + c];
     } else {
       const int ch = e - C * Ch - C;
-      for (int q = 0; q < nstreams; ++q) s += red[(q * Ch + ch) * RW + C];
+      for (int q = 0; q < kThr / 32; ++q) s += red[(q * Ch + ch) * RW + C];
     }
     out[e] = s;
   }
 }
 
 size_t head_smem(int C, int Ch) {
-  return 128 + head_region0(C, Ch) + sizeof(float) * (C * Ch + kMaxC + kTP * kMaxC) + sizeof(int) * kTP +
-         sizeof(float) * (kThr / 32);
+  return 128 + head_region0(C, Ch) + sizeof(float) * (C * Ch + kMaxC + kTP * kMaxC) + sizeof(int) * kTP;
 }
 
 template <int NC>
@@ -335,6 +341,7 @@ cudaError_t launch_nc(const HeadArgs& a, size_t smem, cudaStream_t s) {
 }  // namespace
 
 int head_tiles_per_image(long long per_img) { return (int)((per_img + kTP - 1) / kTP); }
+int head_loss_parts_per_tile() { return kThr / 32; }
 
 int head_blocks(long long total_tiles) {
   long long nb = 148LL * 2;

@@ -202,8 +202,9 @@ static void layout_memory(Net* N, int n) {
   // bias / head partials (fixed-order two-level reductions)
   const Act& h = N->a[N->n_layers - 1];
   const long long h_pos = h.elems_per_image() / h.C;
-  N->loss_parts = head_tiles_per_image(h_pos);
-  size_t bp = (size_t)head_blocks((long long)N->loss_parts * n) * ((size_t)N->classes * h.C + N->classes + h.C);
+  N->loss_parts = head_tiles_per_image(h_pos) * head_loss_parts_per_tile();
+  size_t bp = (size_t)head_blocks((long long)head_tiles_per_image(h_pos) * n) *
+              ((size_t)N->classes * h.C + N->classes + h.C);
   for (int l = 0; l < N->n_layers - 1; ++l) {
     const LayerPlan& P = N->lp[l];
     const Act& in = N->a[l];
@@ -619,8 +620,8 @@ mpf_status mpf_backward_image(mpf_net* N, const uint8_t* d_labels, const float* 
                                  N->classes * h.C + N->classes, s));
   }
   if (d_loss)
-    LAUNCH(N, s, "loss_finalize", L, 0.0, 4.0 * (double)hd.tiles_per_img * n,
-           launch_loss_finalize(lossp, hd.tiles_per_img, nlab, n, d_loss, s));
+    LAUNCH(N, s, "loss_finalize", L, 0.0, 4.0 * (double)N->loss_parts * n,
+           launch_loss_finalize(lossp, hd.tiles_per_img * head_loss_parts_per_tile(), nlab, n, d_loss, s));
   // remaining layers in reverse.  Invariant: dcur holds the delta of a[l+1] at the
   // pre-activation (CONV/FC output) or the value (pooled output).
   bool bias_done = true;  // layer L-1's bias came from the head

@@ -178,7 +178,7 @@ struct HeadArgs {
   float cw[16];          // class weights
   float* probs;          // forward-only mode when non-null: [n*F][vr][vc][C] compact
   float* dh;             // training: [n*F][gr][gc][Ch] delta of the previous layer (zero off-valid)
-  float* loss_part;      // training: [n][tiles_per_img]
+  float* loss_part;      // training: [n][tiles_per_img][head_loss_parts_per_tile()]
   float* part;           // training: [n_blocks][C*Ch + C + Ch] (dW_L, db_L, db_prev)
   int tiles_per_img, n_blocks;
   int* err;
@@ -186,6 +186,7 @@ struct HeadArgs {
   int round_tf32;
 };
 int head_tiles_per_image(long long per_img);
+int head_loss_parts_per_tile();
 int head_blocks(long long total_tiles);
 bool head_supported(int C, int Ch);
 cudaError_t launch_head2(const HeadArgs& a, cudaStream_t s);

@@ -349,15 +349,13 @@ __global__ void __launch_bounds__(256) mpf_bwd_slide_kernel(MpfBwdArgs a) {
         for (int dx = 0; dx < K; ++dx)
           idr[dx] = ldg_u32_pred(a.idx + (fbase + rp + colpart[dx]) * C + cv * 4, rv && cval[dx]);
       };
-      uint32_t id[K][K];  // id[dy][dx]: window row Y - dy (pre-filled one row behind: the loop shifts first)
+      uint32_t id[K][K];  // id[dy][dx]: window row Y - dy
 #pragma unroll
-      for (int dy = 1; dy < K; ++dy) load_row(y0 - dy, id[dy - 1]);
+      for (int dy = 0; dy < K; ++dy) load_row(y0 - dy, id[dy]);
       for (int Y = y0; Y < y1; ++Y) {
-#pragma unroll
-        for (int dy = K - 1; dy > 0; --dy)
-#pragma unroll
-          for (int dx = 0; dx < K; ++dx) id[dy][dx] = id[dy - 1][dx];
-        load_row(Y, id[0]);
+        // prefetch the argmax row of the next output row while this row's deltas load
+        uint32_t nxt[K];
+        load_row(Y + 1, nxt);
         float acc[4] = {0.f, 0.f, 0.f, 0.f}, val[4] = {0.f, 0.f, 0.f, 0.f};
         bool hit[4] = {false, false, false, false};
 #pragma unroll
@@ -392,6 +390,12 @@ __global__ void __launch_bounds__(256) mpf_bwd_slide_kernel(MpfBwdArgs a) {
           o[v] = a.round_tf32 ? tf32_rna(dv) : dv;
         }
         stv<4>(a.din + (((size_t)g * a.gr + Y) * a.gc + X) * C + cv * 4, o);
+#pragma unroll
+        for (int dy = K - 1; dy > 0; --dy)
+#pragma unroll
+          for (int dx = 0; dx < K; ++dx) id[dy][dx] = id[dy - 1][dx];
+#pragma unroll
+        for (int dx = 0; dx < K; ++dx) id[0][dx] = nxt[dx];
       }
     }
   }
