@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include <mutex>
 
@@ -50,12 +51,27 @@ struct ConvTcParams {
   const float* bias;
   const float* mul_dact;
   int box_rows, nbox;
-  uint32_t a_slot_bytes, b_slot_bytes;
-  int n_aslots, n_bslots;
+  uint32_t a_slot_bytes, b_slot_bytes;  // per stage: one A slab + k weight taps of b_slot_bytes
+  uint32_t stage_bytes;
+  int n_stages;
+  int n_stage;  // epilogue staging boxes per warp (1 or 2)
   int base_mode;
   uint32_t tmem_cols;
-  int n_tiles;
+  int n_tiles;   // tiles of M_CTA (single) or 2 x M_CTA (pair) positions
+  int b_rows;    // weight rows per B slot (npad, or npad/2 per CTA of a pair)
+  unsigned long long* prof;  // optional role-timing counters (MPF_TC_PROF)
 };
+
+// mbarrier wait that adds the cycles spent waiting to a counter when profiling
+__device__ __forceinline__ void twait(uint32_t bar, uint32_t parity, unsigned long long& acc, bool on) {
+  if (!on) {
+    ptx::mbar_wait(bar, parity);
+    return;
+  }
+  const long long t0 = clock64();
+  ptx::mbar_wait(bar, parity);
+  acc += (unsigned long long)(clock64() - t0);
+}
 
 __device__ __forceinline__ float tf32r(float x) {
   uint32_t r;
@@ -76,123 +92,138 @@ __device__ __forceinline__ float act_d(int act, float y) {
   return 1.f;
 }
 
-template <int NACC>
+// PAIR: a cluster of two CTAs on one TPC runs tcgen05 cta_group::2 MMAs (M = 256):
+// each CTA stages its own positions (A) and HALF of every weight tile (B), the leader
+// issues the MMAs, every accumulator lands in the TMEM of the CTA that owns its rows.
+template <int NACC, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmO, ConvTcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B aligned carve-up
   const uint32_t sbase = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
-  const uint32_t sA = sbase;                                   // A slabs
-  const uint32_t sB = sA + p.n_aslots * p.a_slot_bytes;        // weight taps
-  const uint32_t sC = sB + p.n_bslots * p.b_slot_bytes;        // epilogue staging: 2 boxes per warp
-  const uint32_t sBias = sC + 2 * kEpiWarps * kStageBytes;     // [npad] fp32
+  // stage s: [A slab | k weight taps], one full/empty barrier pair per stage
+  const uint32_t sS = sbase;
+  const uint32_t sC = sS + p.n_stages * p.stage_bytes;         // epilogue staging boxes
+  const uint32_t sBias = sC + p.n_stage * kEpiWarps * kStageBytes;  // [npad] fp32
   const uint32_t sBar = sBias + 4 * 256;
-  const uint32_t barAfull = sBar, barAempty = barAfull + 8 * p.n_aslots;
-  const uint32_t barBfull = barAempty + 8 * p.n_aslots, barBempty = barBfull + 8 * p.n_bslots;
-  const uint32_t barTfull = barBempty + 8 * p.n_bslots, barTempty = barTfull + 16;
+  const uint32_t barFull = sBar, barEmpty = barFull + 8 * p.n_stages;
+  const uint32_t barTfull = barEmpty + 8 * p.n_stages, barTempty = barTfull + 16;
   const uint32_t sTmemSlot = barTempty + 16;
   uint8_t* gen = smem_raw - ptx::smem_u32(smem_raw);  // generic pointer of shared address 0
   uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(gen + sTmemSlot);
   float* s_bias = reinterpret_cast<float*>(gen + sBias);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index via a shuffle: provably warp-uniform, so role branches stay convergent and
+  // the MMA warp's descriptor arithmetic lives in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   constexpr int M_CTA = NACC * 128;
+  const uint32_t rank = PAIR ? ptx::cluster_rank() : 0u;
+  const bool leader = rank == 0;
+  // tiles: one per CTA, or one per pair (2 x M_CTA positions, CTA r owns the r-th half)
+  const int unit0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int n_units = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int tile_pos = PAIR ? 2 * M_CTA : M_CTA;
+  const int my_off = (int)rank * M_CTA;
+  // the pair's full barriers and the TMEM-empty barriers live in the leader
+  const uint32_t barFullL = PAIR ? ptx::mapa(barFull, 0) : barFull;
+  const uint32_t barTemptyL = PAIR ? ptx::mapa(barTempty, 0) : barTempty;
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
     ptx::prefetch_tmap(&tmO);
-    for (int i = 0; i < p.n_aslots; ++i) {
-      ptx::mbar_init(barAfull + 8 * i, 1);
-      ptx::mbar_init(barAempty + 8 * i, 1);
-    }
-    for (int i = 0; i < p.n_bslots; ++i) {
-      ptx::mbar_init(barBfull + 8 * i, 1);
-      ptx::mbar_init(barBempty + 8 * i, 1);
+    for (int i = 0; i < p.n_stages; ++i) {
+      ptx::mbar_init(barFull + 8 * i, 1);
+      ptx::mbar_init(barEmpty + 8 * i, 1);
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(barTfull + 8 * i, 1);
-      ptx::mbar_init(barTempty + 8 * i, kEpiWarps);  // one arrive per epilogue warp
+      ptx::mbar_init(barTempty + 8 * i, (PAIR ? 2 : 1) * kEpiWarps);  // one arrive per epilogue warp
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 1) ptx::tmem_alloc(sTmemSlot, p.tmem_cols);
+  if (warp == 1) {
+    if (PAIR) ptx::tmem_alloc_pair(sTmemSlot, p.tmem_cols);
+    else ptx::tmem_alloc(sTmemSlot, p.tmem_cols);
+  }
   for (int c = threadIdx.x; c < p.npad; c += kThreads) s_bias[c] = (p.bias && c < p.cout) ? p.bias[c] : 0.f;
   ptx::tc_fence_before();
-  __syncthreads();
+  if (PAIR) ptx::cluster_sync_all();  // barrier inits and TMEM allocation visible to the peer
+  else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot_ptr;
 
   const int k = p.k;
+  const bool prof_on = p.prof != nullptr;
+  unsigned long long pc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  const long long t_start = clock64();
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      int a_it = 0, b_it = 0;
-      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
-        const int p0 = tile * M_CTA;
+      int it = 0;
+      const uint32_t npair = PAIR ? 2u : 1u;
+      for (int tile = unit0; tile < p.n_tiles; tile += n_units) {
+        const int p0 = tile * tile_pos + my_off;
         for (int ky = 0; ky < k; ++ky) {
-          for (int cc = 0; cc < p.n_cc; ++cc) {
-            const int as = a_it % p.n_aslots;
-            ptx::mbar_wait(barAempty + 8 * as, ((a_it / p.n_aslots) & 1) ^ 1);
-            ptx::mbar_arrive_expect_tx(barAfull + 8 * as, p.a_slot_bytes);
+          for (int cc = 0; cc < p.n_cc; ++cc, ++it) {
+            const int st = it % p.n_stages;
+            twait(barEmpty + 8 * st, ((it / p.n_stages) & 1) ^ 1, pc[0], prof_on);
+            if (leader) ptx::mbar_arrive_expect_tx(barFull + 8 * st, npair * (p.a_slot_bytes + k * p.b_slot_bytes));
+            const uint32_t bar = (PAIR ? barFullL : barFull) + 8 * st;
+            const uint32_t sa = sS + st * p.stage_bytes;
             const int row0 = p0 + p.shift_rows + ky * p.gc;
-            for (int b = 0; b < p.nbox; ++b)
-              ptx::tma_load_2d(sA + as * p.a_slot_bytes + b * p.box_rows * 128, &tmA, barAfull + 8 * as, cc * kKC,
-                               row0 + b * p.box_rows);
-            ++a_it;
+            for (int b = 0; b < p.nbox; ++b) {
+              if (PAIR) ptx::tma_load_2d_pair(sa + b * p.box_rows * 128, &tmA, bar, cc * kKC, row0 + b * p.box_rows);
+              else ptx::tma_load_2d(sa + b * p.box_rows * 128, &tmA, bar, cc * kKC, row0 + b * p.box_rows);
+            }
             for (int kx = 0; kx < k; ++kx) {
-              const int bs = b_it % p.n_bslots;
-              ptx::mbar_wait(barBempty + 8 * bs, ((b_it / p.n_bslots) & 1) ^ 1);
-              ptx::mbar_arrive_expect_tx(barBfull + 8 * bs, p.b_slot_bytes);
-              ptx::tma_load_2d(sB + bs * p.b_slot_bytes, &tmB, barBfull + 8 * bs, (ky * k + kx) * p.cin + cc * kKC, 0);
-              ++b_it;
+              const uint32_t sb = sa + p.a_slot_bytes + kx * p.b_slot_bytes;
+              const int c0 = (ky * k + kx) * p.cin + cc * kKC;
+              if (PAIR) ptx::tma_load_2d_pair(sb, &tmB, bar, c0, (int)rank * p.b_rows);
+              else ptx::tma_load_2d(sb, &tmB, bar, c0, 0);
             }
           }
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    const uint32_t idesc = ptx::idesc_tf32(128, p.npad);
-    int a_it = 0, b_it = 0, lt = 0;
-    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++lt) {
+    // ------------------------------------------------------------ MMA issuer (leader)
+    const uint32_t idesc = ptx::idesc_tf32(PAIR ? 256 : 128, p.npad);
+    int it = 0, lt = 0;
+    for (int tile = unit0; leader && tile < p.n_tiles; tile += n_units, ++lt) {
       const int buf = lt & 1;
-      ptx::mbar_wait(barTempty + 8 * buf, ((lt >> 1) & 1) ^ 1);  // the epilogue drained this set
+      twait(barTempty + 8 * buf, ((lt >> 1) & 1) ^ 1, pc[3], prof_on);  // the epilogue drained this set
       ptx::tc_fence_after();
       const uint32_t dbase = tmem + buf * (NACC * p.npad);
       for (int ky = 0; ky < k; ++ky) {
-        for (int cc = 0; cc < p.n_cc; ++cc) {
-          const int as = a_it % p.n_aslots;
-          ptx::mbar_wait(barAfull + 8 * as, (a_it / p.n_aslots) & 1);
+        for (int cc = 0; cc < p.n_cc; ++cc, ++it) {
+          const int st = it % p.n_stages;
+          twait(barFull + 8 * st, (it / p.n_stages) & 1, pc[4], prof_on);
+          ptx::tc_fence_after();
+          const uint32_t sa = sS + st * p.stage_bytes;
+          const uint64_t adesc0 = ptx::sdesc_k_sw128(sa, p.base_mode);
+          const uint64_t bdesc0 = ptx::sdesc_k_sw128(sa + p.a_slot_bytes, p.base_mode);
           for (int kx = 0; kx < k; ++kx) {
-            const int bs = b_it % p.n_bslots;
-            ptx::mbar_wait(barBfull + 8 * bs, (b_it / p.n_bslots) & 1);
-            ptx::tc_fence_after();
-            if (lane == 0) {
 #pragma unroll
-              for (int acc = 0; acc < NACC; ++acc) {
+            for (int acc = 0; acc < NACC; ++acc) {
 #pragma unroll
-                for (int k8 = 0; k8 < 4; ++k8) {
-                  const uint32_t aaddr = sA + as * p.a_slot_bytes + (acc * 128 + kx) * 128 + k8 * 32;
-                  const uint32_t baddr = sB + bs * p.b_slot_bytes + k8 * 32;
-                  const uint32_t accum = (ky | cc | kx | k8) != 0;
-                  ptx::mma_tf32(dbase + acc * p.npad, ptx::sdesc_k_sw128(aaddr, p.base_mode),
-                                ptx::sdesc_k_sw128(baddr, p.base_mode), idesc, accum);
-                }
+              for (int k8 = 0; k8 < 4; ++k8) {
+                // descriptor start-address field is (addr >> 4) in the low bits
+                const uint64_t ad = adesc0 + (uint64_t)((((acc * 128 + kx) * 128) + k8 * 32) >> 4);
+                const uint64_t bd = bdesc0 + (uint64_t)((kx * p.b_slot_bytes + k8 * 32) >> 4);
+                const uint32_t accum = (ky | cc | kx | k8) != 0;
+                if (PAIR) ptx::mma_tf32_pair_elect(dbase + acc * p.npad, ad, bd, idesc, accum);
+                else ptx::mma_tf32_elect(dbase + acc * p.npad, ad, bd, idesc, accum);
               }
-              ptx::mma_commit(barBempty + 8 * bs);
             }
-            __syncwarp();
-            ++b_it;
           }
-          if (lane == 0) ptx::mma_commit(barAempty + 8 * as);
-          __syncwarp();
-          ++a_it;
+          if (PAIR) ptx::mma_commit_pair_elect(barEmpty + 8 * st, 3);  // frees the stage in both CTAs
+          else ptx::mma_commit_elect(barEmpty + 8 * st);
         }
       }
-      if (lane == 0) ptx::mma_commit(barTfull + 8 * buf);
-      __syncwarp();
+      if (PAIR) ptx::mma_commit_pair_elect(barTfull + 8 * buf, 3);
+      else ptx::mma_commit_elect(barTfull + 8 * buf);
     }
   } else {
     // ------------------------------------------------------------ epilogue (warps 2..)
@@ -201,11 +232,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ew = warp - 2;
     const int per_frag = p.gr * p.gc;
     int lt = 0, sb = 0;
-    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++lt) {
+    for (int tile = unit0; tile < p.n_tiles; tile += n_units, ++lt) {
       const int buf = lt & 1;
-      ptx::mbar_wait(barTfull + 8 * buf, (lt >> 1) & 1);
+      twait(barTfull + 8 * buf, (lt >> 1) & 1, pc[7], prof_on);
       ptx::tc_fence_after();
-      const int p0 = tile * M_CTA;
+      const int p0 = tile * tile_pos + my_off;
       for (int acc = 0; acc < NACC; ++acc) {
         const int row0 = p0 + acc * 128 + q * 32;
         const int pos = row0 + lane;
@@ -269,8 +300,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           // staging box (swizzled like the TMA SWIZZLE_128B pattern): 16-B chunk jj of
           // row `lane` lives at lane*128 + ((jj ^ (lane & 7)) * 16)
-          const uint32_t sbuf = sC + (ew * 2 + sb) * kStageBytes;
-          if (lane == 0) ptx::bulk_wait_read<1>();  // the store issued from this box 2 stores ago
+          const uint32_t sbuf = sC + (ew * p.n_stage + sb) * kStageBytes;
+          if (lane == 0) {  // the store that last used this box has finished reading it
+            if (p.n_stage == 2) ptx::bulk_wait_read<1>();
+            else ptx::bulk_wait_read<0>();
+          }
           __syncwarp();
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj) {
@@ -285,19 +319,32 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tma_store_2d(&tmO, sbuf, c0, row0);
             ptx::bulk_commit();
           }
-          sb ^= 1;
+          sb = (sb + 1 == p.n_stage) ? 0 : sb + 1;
         }
       }
       // every TMEM read of this accumulator set is complete: hand it back to the MMA warp
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(barTempty + 8 * buf);
+      if (lane == 0) {
+        if (PAIR) ptx::mbar_arrive_cluster(barTemptyL + 8 * buf);
+        else ptx::mbar_arrive(barTempty + 8 * buf);
+      }
     }
     if (lane == 0) ptx::bulk_wait<0>();
   }
+  if (prof_on && (warp >= 2 || lane == 0)) {
+    const int slot_total = warp == 0 ? 2 : (warp == 1 ? 6 : 8);
+    pc[slot_total] = (unsigned long long)(clock64() - t_start);
+    for (int i = 0; i < 10; ++i)
+      if (pc[i]) atomicAdd(p.prof + i, pc[i]);
+  }
   ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 1) ptx::tmem_dealloc(tmem, p.tmem_cols);
+  if (PAIR) ptx::cluster_sync_all();  // the peer may still signal our barriers until here
+  else __syncthreads();
+  if (warp == 1) {
+    if (PAIR) ptx::tmem_dealloc_pair(tmem, p.tmem_cols);
+    else ptx::tmem_dealloc(tmem, p.tmem_cols);
+  }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -346,14 +393,61 @@ int num_sms() {
   return g_num_sms;
 }
 
-template <int NACC>
+unsigned long long* g_prof = nullptr;
+unsigned long long* prof_counters() {
+  if (!getenv("MPF_TC_PROF")) return nullptr;
+  if (!g_prof && cudaMalloc(&g_prof, 16 * sizeof(unsigned long long)) != cudaSuccess) g_prof = nullptr;
+  if (g_prof) cudaMemset(g_prof, 0, 16 * sizeof(unsigned long long));
+  return g_prof;
+}
+void prof_report(const ConvTcParams& p, int nacc, bool pair, int grid) {
+  if (!p.prof) return;
+  unsigned long long h[16];
+  cudaDeviceSynchronize();
+  cudaMemcpy(h, p.prof, sizeof(h), cudaMemcpyDeviceToHost);
+  const double ctas = grid;
+  fprintf(stderr,
+          "[tc-prof] cin=%d cout=%d k=%d nacc=%d pair=%d tiles=%d grid=%d | per CTA Mcyc: prod total %.2f wAempty %.2f "
+          "wBempty %.2f | mma total %.2f wTempty %.2f wAfull %.2f wBfull %.2f | epi(sum of %d warps) total %.2f wTfull %.2f\n",
+          p.cin, p.cout, p.k, nacc, pair ? 1 : 0, p.n_tiles, grid, h[2] / ctas / 1e6, h[0] / ctas / 1e6,
+          h[1] / ctas / 1e6, h[6] / ctas / 1e6, h[3] / ctas / 1e6, h[4] / ctas / 1e6, h[5] / ctas / 1e6, kEpiWarps,
+          h[8] / ctas / 1e6, h[7] / ctas / 1e6);
+}
+
+template <int NACC, bool PAIR>
 cudaError_t launch_nacc(const CUtensorMap& A, const CUtensorMap& B, const CUtensorMap& O, ConvTcParams& p,
                         size_t smem, cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = conv_tc_kernel<NACC, PAIR>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int grid = p.n_tiles < num_sms() ? p.n_tiles : num_sms();
-  conv_tc_kernel<NACC><<<grid, kThreads, smem, s>>>(A, B, O, p);
+  if (!PAIR) {
+    const int grid = p.n_tiles < num_sms() ? p.n_tiles : num_sms();
+    kern<<<grid, kThreads, smem, s>>>(A, B, O, p);
+    prof_report(p, NACC, PAIR, grid);
+    return cudaGetLastError();
+  }
+  const int pairs = p.n_tiles < num_sms() / 2 ? p.n_tiles : num_sms() / 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, A, B, O, p);
+  if (e != cudaSuccess) return e;
+  prof_report(p, NACC, PAIR, 2 * pairs);
   return cudaGetLastError();
+}
+
+bool use_pair() {
+  const char* e = getenv("MPF_TC_PAIR");
+  return e ? atoi(e) != 0 : true;
 }
 
 }  // namespace
@@ -382,41 +476,66 @@ cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s) {
   p.bias = a.bias;
   p.mul_dact = a.mul_dact;
   p.base_mode = base_mode();
+  p.prof = prof_counters();
   int nacc = 256 / p.npad;  // two accumulator sets in 512 TMEM columns
   if (nacc > 4) nacc = 4;
   if (nacc < 1) nacc = 1;
+  if (const char* e = getenv("MPF_TC_NACC_MAX")) {  // tuning knob
+    const int m = atoi(e);
+    if (m >= 1 && nacc > m) nacc = m;
+  }
   const int m_cta = nacc * 128;
   const int rows_needed = m_cta + a.k - 1;
   p.nbox = (rows_needed + 255) / 256;
   p.box_rows = ((rows_needed + p.nbox - 1) / p.nbox + 7) / 8 * 8;
+  const bool pair = use_pair();
   p.a_slot_bytes = (uint32_t)(p.nbox * p.box_rows * 128);
-  p.b_slot_bytes = (uint32_t)(p.npad * 128);
-  const size_t fixed = 1024 + 2 * kEpiWarps * kStageBytes + 4 * 256 + 512;
-  const size_t budget = 227 * 1024 - fixed;
-  int na = 3;
-  while (na > 2 && na * (size_t)p.a_slot_bytes + 4 * (size_t)p.b_slot_bytes > budget) --na;
-  int nb = (int)((budget - na * (size_t)p.a_slot_bytes) / p.b_slot_bytes);
-  if (nb > 8) nb = 8;
-  if (nb < 2) return cudaErrorInvalidConfiguration;
-  p.n_aslots = na;
-  p.n_bslots = nb;
+  p.b_rows = pair ? p.npad / 2 : p.npad;  // a CTA of a pair stages half of every weight tile
+  p.b_slot_bytes = (uint32_t)(p.b_rows * 128);
+  // shared memory: stages of [A slab | k weight taps] (2..4, as many as fit), epilogue
+  // staging (two boxes per warp when 3 stages still fit, else one)
+  p.stage_bytes = p.a_slot_bytes + (uint32_t)a.k * p.b_slot_bytes;
+  const size_t base_fixed = 1024 + 4 * 256 + 512;
+  const size_t total = 227 * 1024;
+  int ns = 0, nst = 0;
+  for (int cand_ns = 2; cand_ns >= 1 && !ns; --cand_ns) {
+    const size_t budget = total - base_fixed - (size_t)cand_ns * kEpiWarps * kStageBytes;
+    int cand = (int)(budget / p.stage_bytes);
+    if (cand > 4) cand = 4;
+    if (cand >= 3 || (cand_ns == 1 && cand >= 2)) {
+      ns = cand_ns;
+      nst = cand;
+    }
+  }
+  if (!ns) return cudaErrorInvalidConfiguration;
+  const size_t fixed = base_fixed + (size_t)ns * kEpiWarps * kStageBytes;
+  p.n_stage = ns;
+  p.n_stages = nst;
   uint32_t cols = 32;
   while (cols < (uint32_t)(2 * nacc * p.npad)) cols <<= 1;
   p.tmem_cols = cols;
-  p.n_tiles = (p.P_tot + m_cta - 1) / m_cta;
-  const size_t smem = fixed + (size_t)na * p.a_slot_bytes + (size_t)nb * p.b_slot_bytes;
+  p.n_tiles = (p.P_tot + (pair ? 2 : 1) * m_cta - 1) / ((pair ? 2 : 1) * m_cta);
+  const size_t smem = fixed + (size_t)nst * p.stage_bytes;
   CUtensorMap A, B, O;
   cudaError_t e = make_map(&A, a.x, (uint64_t)a.cin, (uint64_t)p.P_tot, (uint32_t)p.box_rows);
   if (e != cudaSuccess) return e;
-  e = make_map(&B, a.w, (uint64_t)a.k * a.k * a.cin, (uint64_t)a.cout, (uint32_t)p.npad);
+  e = make_map(&B, a.w, (uint64_t)a.k * a.k * a.cin, (uint64_t)a.cout, (uint32_t)p.b_rows);
   if (e != cudaSuccess) return e;
   e = make_map(&O, a.out, (uint64_t)a.cout, (uint64_t)p.P_tot, 32u);
   if (e != cudaSuccess) return e;
+  if (pair) {
+    switch (nacc) {
+      case 1: return launch_nacc<1, true>(A, B, O, p, smem, s);
+      case 2: return launch_nacc<2, true>(A, B, O, p, smem, s);
+      case 3: return launch_nacc<3, true>(A, B, O, p, smem, s);
+      default: return launch_nacc<4, true>(A, B, O, p, smem, s);
+    }
+  }
   switch (nacc) {
-    case 1: return launch_nacc<1>(A, B, O, p, smem, s);
-    case 2: return launch_nacc<2>(A, B, O, p, smem, s);
-    case 3: return launch_nacc<3>(A, B, O, p, smem, s);
-    default: return launch_nacc<4>(A, B, O, p, smem, s);
+    case 1: return launch_nacc<1, false>(A, B, O, p, smem, s);
+    case 2: return launch_nacc<2, false>(A, B, O, p, smem, s);
+    case 3: return launch_nacc<3, false>(A, B, O, p, smem, s);
+    default: return launch_nacc<4, false>(A, B, O, p, smem, s);
   }
 }
 
