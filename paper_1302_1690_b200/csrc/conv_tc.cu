@@ -80,17 +80,21 @@ __device__ __forceinline__ float tf32r(float x) {
 }
 // tanh(v) = 1 - 2 / (exp(2v) + 1): two MUFU ops, absolute error ~1e-7 (far below the
 // TF32 rounding of every tensor-core operand), saturates correctly at +-inf.
-__device__ __forceinline__ float fast_tanh(float v) { return 1.f - __fdividef(2.f, __expf(2.f * v) + 1.f); }
-__device__ __forceinline__ float act_f(int act, float v) {
-  if (act == MPF_TANH) return fast_tanh(v);
-  if (act == MPF_LOGISTIC) return __fdividef(1.f, 1.f + __expf(-v));
-  return v;
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
-__device__ __forceinline__ float act_d(int act, float y) {
-  if (act == MPF_TANH) return 1.f - y * y;
-  if (act == MPF_LOGISTIC) return y * (1.f - y);
-  return 1.f;
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
+// branch-free SFU tanh: 1 - 2 / (2^(2 v log2 e) + 1); saturates to +-1 at +-inf
+__device__ __forceinline__ float fast_tanh(float v) {
+  return fmaf(-2.f, rcp_approx(ex2_approx(2.8853900817779268f * v) + 1.f), 1.f);
+}
+__device__ __forceinline__ float fast_logistic(float v) { return rcp_approx(1.f + ex2_approx(-1.4426950408889634f * v)); }
 
 // PAIR: a cluster of two CTAs on one TPC runs tcgen05 cta_group::2 MMAs (M = 256):
 // each CTA stages its own positions (A) and HALF of every weight tile (B), the leader
@@ -156,7 +160,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int k = p.k;
   const bool prof_on = p.prof != nullptr;
-  unsigned long long pc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long pc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   const long long t_start = clock64();
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -249,6 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float* md = (p.mul_dact && valid) ? p.mul_dact + (size_t)pos * p.cout : nullptr;
         const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + buf * (NACC * p.npad) + acc * p.npad;
         for (int c0 = 32 * half; c0 < p.npad; c0 += 64) {
+          const long long e0 = prof_on ? clock64() : 0;
           uint32_t r[32];
           const bool two = c0 + 16 < p.npad;
           {
@@ -287,20 +292,40 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           ptx::tmem_ld_wait();
+          const long long e1 = prof_on ? clock64() : 0;
+          // every branch below is warp-uniform (kernel parameters) except `valid`, taken
+          // once per row: no per-element control flow
           float v[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            float o = 0.f;
-            if (valid) {
-              o = act_f(p.act, __uint_as_float(r[j]) + s_bias[c0 + j]);
-              if (md) o *= act_d(p.dact, mdv[j]);
-              if (p.round_out) o = tf32r(o);
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) + s_bias[c0 + j];
+          if (p.act == MPF_TANH) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = fast_tanh(v[j]);
+          } else if (p.act == MPF_LOGISTIC) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = fast_logistic(v[j]);
+          }
+          if (md) {
+            if (p.dact == MPF_TANH) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] *= fmaf(-mdv[j], mdv[j], 1.f);
+            } else if (p.dact == MPF_LOGISTIC) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] *= mdv[j] * (1.f - mdv[j]);
             }
-            v[j] = o;
+          }
+          if (p.round_out) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = tf32r(v[j]);
+          }
+          if (!valid) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0.f;
           }
           // staging box (swizzled like the TMA SWIZZLE_128B pattern): 16-B chunk jj of
           // row `lane` lives at lane*128 + ((jj ^ (lane & 7)) * 16)
           const uint32_t sbuf = sC + (ew * p.n_stage + sb) * kStageBytes;
+          const long long e2 = prof_on ? clock64() : 0;
           if (lane == 0) {  // the store that last used this box has finished reading it
             if (p.n_stage == 2) ptx::bulk_wait_read<1>();
             else ptx::bulk_wait_read<0>();
@@ -320,6 +345,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::bulk_commit();
           }
           sb = (sb + 1 == p.n_stage) ? 0 : sb + 1;
+          if (prof_on) {
+            const long long e3 = clock64();
+            pc[1] += (unsigned long long)(e1 - e0);   // TMEM loads (+ act' operand loads)
+            pc[5] += (unsigned long long)(e2 - e1);   // epilogue math
+            pc[9] += (unsigned long long)(e3 - e2);   // staging wait + st.shared + fence + store issue
+          }
         }
       }
       // every TMEM read of this accumulator set is complete: hand it back to the MMA warp
@@ -335,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (prof_on && (warp >= 2 || lane == 0)) {
     const int slot_total = warp == 0 ? 2 : (warp == 1 ? 6 : 8);
     pc[slot_total] = (unsigned long long)(clock64() - t_start);
-    for (int i = 0; i < 10; ++i)
+    for (int i = 0; i < 12; ++i)
       if (pc[i]) atomicAdd(p.prof + i, pc[i]);
   }
   ptx::tc_fence_before();
@@ -412,6 +443,8 @@ void prof_report(const ConvTcParams& p, int nacc, bool pair, int grid) {
           p.cin, p.cout, p.k, nacc, pair ? 1 : 0, p.n_tiles, grid, h[2] / ctas / 1e6, h[0] / ctas / 1e6,
           h[1] / ctas / 1e6, h[6] / ctas / 1e6, h[3] / ctas / 1e6, h[4] / ctas / 1e6, h[5] / ctas / 1e6, kEpiWarps,
           h[8] / ctas / 1e6, h[7] / ctas / 1e6);
+  fprintf(stderr, "[tc-prof]   epi per thread Mcyc: tmem-ld %.2f math %.2f stage+store %.2f (of total %.2f)\n",
+          h[1] / ctas / 256e6, h[5] / ctas / 256e6, h[9] / ctas / 256e6, h[8] / ctas / 256e6);
 }
 
 template <int NACC, bool PAIR>
@@ -572,7 +605,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t barFull = sBar, barEmpty = sBar + 8 * p.n_stages_ring, barT = sBar + 16 * p.n_stages_ring;
   const uint32_t sTmemSlot = barT + 8;
   uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (sTmemSlot - ptx::smem_u32(smem_raw)));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   // block -> (m tile, group set, split); neighbouring blocks share a split (L2 reuse)
   const int mt = blockIdx.x % p.m_tiles;
   const int set = (blockIdx.x / p.m_tiles) % p.n_sets;
@@ -621,23 +654,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int slot = st % p.n_stages_ring;
       ptx::mbar_wait(barFull + 8 * slot, (st / p.n_stages_ring) & 1);
       ptx::tc_fence_after();
-      if (lane == 0) {
-        const uint32_t sa = sbase + slot * p.stage_bytes;
-        for (int g = 0; g < G; ++g) {
-          const uint32_t sb = sa + p.a_bytes + g * p.b_bytes;
+      const uint32_t sa = sbase + slot * p.stage_bytes;
+      const uint64_t ad0 = ptx::sdesc_mn_sw128_32b(sa, kWR * 128, 512);
+      const uint64_t bd0 = ptx::sdesc_mn_sw128_32b(sa + p.a_bytes, 128, 512);
+      for (int g = 0; g < G; ++g) {
 #pragma unroll
-          for (int r8 = 0; r8 < kWR / 8; ++r8) {
-            const uint64_t ad = ptx::sdesc_mn_sw128_32b(sa + r8 * 1024, kWR * 128, 512);
-            const uint64_t bd = ptx::sdesc_mn_sw128_32b(sb + r8 * 1024, 128, 512);
-            ptx::mma_tf32(tmem + g * N, ad, bd, idesc, (st | r8) != 0);
-          }
+        for (int r8 = 0; r8 < kWR / 8; ++r8) {
+          const uint64_t ad = ad0 + (uint64_t)((r8 * 1024) >> 4);
+          const uint64_t bd = bd0 + (uint64_t)((g * p.b_bytes + r8 * 1024) >> 4);
+          ptx::mma_tf32_elect(tmem + g * N, ad, bd, idesc, (st | r8) != 0);
         }
-        ptx::mma_commit(barEmpty + 8 * slot);
       }
-      __syncwarp();
+      ptx::mma_commit_elect(barEmpty + 8 * slot);
     }
-    if (lane == 0) ptx::mma_commit(barT);
-    __syncwarp();
+    ptx::mma_commit_elect(barT);
   } else {
     const int q = warp & 3;
     const int co = mt * 128 + q * 32 + lane;

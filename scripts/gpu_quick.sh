@@ -8,4 +8,4 @@ timeout 120 python scripts/run_step.py --workload cfg4 > gpurun_out/quick_cfg4.l
 timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo tests $? >> gpurun_out/status.txt
 for w in cfg4 cfg5 cfg3; do timeout 300 python bench.py --workload $w --no-cpu-baseline --profile-json gpurun_out/prof_$w.json > gpurun_out/bench_$w.log 2>&1; echo bench_$w $? >> gpurun_out/status.txt; done
 MPF_TC_PROF=1 timeout 300 python scripts/run_step.py --workload cfg4 --warmup 1 > gpurun_out/tcprof_cfg4.log 2>&1
-MPF_TC_PAIR=0 timeout 300 python bench.py --workload cfg4 --steps 3 --no-e2e --no-cpu-baseline --profile-json gpurun_out/prof_cfg4_single.json > gpurun_out/bench_cfg4_single.log 2>&1
+MPF_TC_PROF=1 timeout 300 python scripts/run_step.py --workload cfg5 --warmup 1 > gpurun_out/tcprof_cfg5.log 2>&1
