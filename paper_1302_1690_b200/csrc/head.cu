@@ -57,7 +57,7 @@ __host__ __device__ inline size_t head_region0(int C, int Ch) {
   return ((red > tiles ? red : tiles) + 127) / 128 * 128;
 }
 
-template <int NC, bool TRAIN>
+template <int NC, bool TRAIN, bool TANH>
 __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int C = a.C, Ch = a.Ch;
@@ -66,14 +66,16 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
   float* hb0 = reinterpret_cast<float*>(smem_raw + 128);
   float* hb1 = reinterpret_cast<float*>(smem_raw + 128 + tile_bytes);
-  float* s_w = reinterpret_cast<float*>(smem_raw + 128 + head_region0(C, Ch));
-  float* s_b = s_w + C * Ch;
+  // W_L [C][Ch] (canonical): phase A reads it with 4 distinct addresses per warp, phase B
+  // with consecutive channels per lane (conflict-free)
+  float* s_w2 = reinterpret_cast<float*>(smem_raw + 128 + head_region0(C, Ch));
+  float* s_b = s_w2 + C * Ch;
   float* s_dl = s_b + kMaxC;                                  // [kTP][NC]
   int* s_lab = reinterpret_cast<int*>(s_dl + kTP * kMaxC);     // [kTP]
   const uint32_t bar0 = ptx::smem_u32(&bars[0]), bar1 = ptx::smem_u32(&bars[1]);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  for (int e = tid; e < C * Ch; e += kThr) s_w[e] = a.w[e];
+  for (int e = tid; e < C * Ch; e += kThr) s_w2[e] = a.w[e];
   for (int e = tid; e < C; e += kThr) s_b[e] = a.b[e];
   const long long per_img = (long long)a.F * a.gr * a.gc;
   const int frag_sz = a.gr * a.gc;
@@ -104,6 +106,9 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
   const int rot = pa % (M > 0 ? M : 1);
   constexpr int kMC = 8;  // channel slots per lane in phase B (Ch <= 256)
   float accW[kMC][NC], accP[kMC], accL[NC];
+  // W_L[:, ch] of this lane's phase-B channels, held in registers (constant over tiles)
+  constexpr bool kWReg = NC <= 4;
+  float wreg[kWReg ? kMC : 1][kWReg ? NC : 1];
 #pragma unroll
   for (int m = 0; m < kMC; ++m) {
     accP[m] = 0.f;
@@ -112,6 +117,15 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
   }
 #pragma unroll
   for (int c = 0; c < NC; ++c) accL[c] = 0.f;
+  __syncthreads();  // s_w is filled (the barrier init sync above precedes nothing else)
+  if constexpr (kWReg) {
+#pragma unroll
+    for (int m = 0; m < kMC; ++m) {
+      const int ch = lane + 32 * m;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) wreg[m][c] = ch < Ch ? s_w2[c * Ch + ch] : 0.f;
+    }
+  }
 
   // TMA bulk copies need 16-byte granules: Ch % 4 == 0; otherwise a plain cooperative copy
   const bool bulk = (Ch % 4) == 0;
@@ -179,15 +193,13 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
             const int ch = qa + 4 * mm;
             const float hv = hrow[ch];
 #pragma unroll
-            for (int c = 0; c < NC; ++c)
-              if (c < C) z[c] = fmaf(s_w[c * Ch + ch], hv, z[c]);
+            for (int c = 0; c < NC; ++c) z[c] = fmaf(s_w2[c * Ch + ch], hv, z[c]);
           }
         } else {
           for (int ch = qa; ch < Ch; ch += 4) {
             const float hv = hrow[ch];
 #pragma unroll
-            for (int c = 0; c < NC; ++c)
-              if (c < C) z[c] = fmaf(s_w[c * Ch + ch], hv, z[c]);
+            for (int c = 0; c < NC; ++c) z[c] = fmaf(s_w2[c * Ch + ch], hv, z[c]);
           }
         }
       }
@@ -255,23 +267,28 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
 #pragma unroll
           for (int c = 0; c < NC; ++c) accL[c] += dl[c];
         }
+        float* dh_row = dh_img + (long long)p * Ch;
+        if (!act) {  // warp-uniform: padding position or ignored label -> zero delta
+#pragma unroll
+          for (int m = 0; m < kMC; ++m)
+            if (lane + 32 * m < Ch) dh_row[lane + 32 * m] = 0.f;
+          continue;
+        }
 #pragma unroll
         for (int m = 0; m < kMC; ++m) {
           const int ch = lane + 32 * m;
           if (ch < Ch) {
-            float d = 0.f;
-            if (act) {
-              const float hv = hs[p * Ch + ch];
-              float sacc = 0.f;
+            const float hv = hs[p * Ch + ch];
+            float sacc = 0.f;
 #pragma unroll
-              for (int c = 0; c < NC; ++c) {
-                sacc = fmaf(s_w[c * Ch + ch], dl[c], sacc);
-                accW[m][c] = fmaf(dl[c], hv, accW[m][c]);
-              }
-              d = sacc * act_der(a.hidden_act, hv);
-              accP[m] += d;
+            for (int c = 0; c < NC; ++c) {
+              const float w = kWReg ? wreg[kWReg ? m : 0][kWReg ? c : 0] : s_w2[c * Ch + ch];
+              sacc = fmaf(w, dl[c], sacc);
+              accW[m][c] = fmaf(dl[c], hv, accW[m][c]);
             }
-            dh_img[(long long)p * Ch + ch] = a.round_tf32 ? tf32_rna(d) : d;
+            const float d = sacc * (TANH ? fmaf(-hv, hv, 1.f) : act_der(a.hidden_act, hv));
+            accP[m] += d;
+            dh_row[ch] = a.round_tf32 ? tf32_rna(d) : d;
           }
         }
       }
@@ -322,20 +339,20 @@ size_t head_smem(int C, int Ch) {
   return 128 + head_region0(C, Ch) + sizeof(float) * (C * Ch + kMaxC + kTP * kMaxC) + sizeof(int) * kTP;
 }
 
+template <int NC, bool TRAIN, bool TANH>
+cudaError_t launch_k(const HeadArgs& a, size_t smem, cudaStream_t s) {
+  cudaError_t e =
+      cudaFuncSetAttribute(head_kernel<NC, TRAIN, TANH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  head_kernel<NC, TRAIN, TANH><<<a.n_blocks, kThr, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 template <int NC>
 cudaError_t launch_nc(const HeadArgs& a, size_t smem, cudaStream_t s) {
-  if (a.probs) {
-    cudaError_t e =
-        cudaFuncSetAttribute(head_kernel<NC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    head_kernel<NC, false><<<a.n_blocks, kThr, smem, s>>>(a);
-  } else {
-    cudaError_t e =
-        cudaFuncSetAttribute(head_kernel<NC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    head_kernel<NC, true><<<a.n_blocks, kThr, smem, s>>>(a);
-  }
-  return cudaGetLastError();
+  if (a.probs) return launch_k<NC, false, true>(a, smem, s);  // forward: activation unused
+  if (a.hidden_act == MPF_TANH) return launch_k<NC, true, true>(a, smem, s);
+  return launch_k<NC, true, false>(a, smem, s);
 }
 
 }  // namespace

@@ -625,6 +625,7 @@ mpf_status mpf_backward_image(mpf_net* N, const uint8_t* d_labels, const float* 
   // remaining layers in reverse.  Invariant: dcur holds the delta of a[l+1] at the
   // pre-activation (CONV/FC output) or the value (pooled output).
   bool bias_done = true;  // layer L-1's bias came from the head
+  bool premul = false;    // dcur already carries act' of the conv feeding the next pool
   float* wpack = scr(N, N->off_wpack);
   for (int l = L - 1; l >= 0; --l) {
     const LayerPlan& P = N->lp[l];
@@ -644,8 +645,10 @@ mpf_status mpf_backward_image(mpf_net* N, const uint8_t* d_labels, const float* 
       m.din = dother;
       m.round_tf32 = tf32 ? 1 : 0;
       m.bias_part = bpart;
+      m.premul = premul ? 1 : 0;
+      premul = false;
       const double ein = (double)n * in.F * in.vr * in.vc * in.C, eout = (double)n * o.F * o.vr * o.vc * o.C;
-      LAUNCH(N, s, "mpf_bwd", l, 0.0, 9.0 * eout + 4.0 * ein, launch_mpf_bwd(m, s));
+      LAUNCH(N, s, "mpf_bwd", l, 0.0, (m.premul ? 5.0 : 9.0) * eout + 4.0 * ein, launch_mpf_bwd(m, s));
       mpf_status st = bias_reduce(N, l - 1, bpart, mpf_bwd_partials(m), s);
       if (st != MPF_OK) return st;
       bias_done = true;
@@ -664,19 +667,26 @@ mpf_status mpf_backward_image(mpf_net* N, const uint8_t* d_labels, const float* 
     mpf_status st = wgrad(N, l, x, dcur, n, s);
     if (st != MPF_OK) return st;
     if (l == 0) break;
-    // dgrad: delta of a[l] = full correlation of dcur with the rotated kernel
+    // dgrad: delta of a[l] = full correlation of dcur with the rotated kernel.  When a[l]
+    // is a pooled tensor, the epilogue already multiplies by act'(pooled value) of the conv
+    // before that pool (= act'(y) at every element the pool selected), so the MPF backward
+    // only routes and sums (premul).
     const bool in_is_conv = N->lp[l - 1].L.kind != MPF_POOL;
+    const bool in_is_pool = !in_is_conv && l >= 2 && N->lp[l - 2].L.kind != MPF_POOL;
+    const float* md = in_is_conv ? act_ptr(N, l) : (in_is_pool ? act_ptr(N, l) : nullptr);
+    const int mdact = in_is_conv ? N->lp[l - 1].L.act : (in_is_pool ? N->lp[l - 2].L.act : 0);
     const double pos_out = (double)n * o.F * o.vr * o.vc, pos_in = (double)n * in.F * in.vr * in.vc;
     const double dflops = 2.0 * pos_out * P.cout * P.L.k * P.L.k * P.cin;
-    const double dbytes = 4.0 * (pos_out * P.cout + pos_in * P.cin) + (in_is_conv ? 4.0 * pos_in * P.cin : 0.0);
+    const double dbytes = 4.0 * (pos_out * P.cout + pos_in * P.cin) + (md ? 4.0 * pos_in * P.cin : 0.0);
     if (use_tc(N, P, true)) {
       TcConvArgs t{};
       t.x = dcur; t.n_frag = n * in.F; t.gr = in.gr; t.gc = in.gc; t.cin = P.cout;
       t.w = wpack + P.dpack_off; t.bias = nullptr; t.k = P.L.k; t.cout = P.cin;
       t.out = dother; t.out_vr = in.vr; t.out_vc = in.vc; t.act = MPF_IDENTITY; t.shift = -(P.L.k - 1);
-      t.round_out = tf32 ? 1 : 0; t.zero_pad = 1;
-      t.mul_dact = in_is_conv ? act_ptr(N, l) : nullptr;
-      t.dact = in_is_conv ? N->lp[l - 1].L.act : 0;
+      t.round_out = (tf32 && !in_is_pool) ? 1 : 0;  // a pooled delta feeds the MPF backward, not an MMA
+      t.zero_pad = 1;
+      t.mul_dact = md;
+      t.dact = mdact;
       LAUNCH(N, s, "dgrad_tc", l, dflops, dbytes, launch_conv_tc(t, s));
     } else {
       ConvArgs c{};
@@ -693,13 +703,14 @@ mpf_status mpf_backward_image(mpf_net* N, const uint8_t* d_labels, const float* 
       c.out = dother;
       c.out_gr = in.gr; c.out_gc = in.gc; c.out_vr = in.vr; c.out_vc = in.vc;
       c.act = MPF_IDENTITY;
-      c.mul_dact = in_is_conv ? act_ptr(N, l) : nullptr;
-      c.dact = in_is_conv ? N->lp[l - 1].L.act : 0;
+      c.mul_dact = md;
+      c.dact = mdact;
       c.zero_pad = 1;
-      c.round_tf32 = tf32 ? 1 : 0;
+      c.round_tf32 = (tf32 && !in_is_pool) ? 1 : 0;
       c.n_frag_total = n * in.F;
       LAUNCH(N, s, "dgrad_simt", l, dflops, dbytes, launch_conv_simt(c, s));
     }
+    premul = in_is_pool;
     std::swap(dcur, dother);
   }
   return MPF_OK;

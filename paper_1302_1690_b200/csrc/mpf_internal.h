@@ -152,6 +152,7 @@ struct MpfBwdArgs {
   float* din;            // delta at pre-activation of y, grid (gr,gc); zero outside valid
   int round_tf32;
   float* bias_part;      // nullable: [mpf_bwd_partials(a)][C] per-block sums of din (bias gradient)
+  int premul;            // 1: dout already carries act'(y) (the producing dgrad applied it); pooled unused
 };
 cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s);
 long long mpf_bwd_partials(const MpfBwdArgs& a);

@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(256) mpf_bwd_kernel(MpfBwdArgs a) {
               for (int v = 0; v < V; ++v) any |= (id[v] == want);
               if (any) {
                 const Vec<V> d = ldv<V>(a.dout + cell);
-                const Vec<V> pv = ldv<V>(a.pooled + cell);
+                const Vec<V> pv = a.premul ? d : ldv<V>(a.pooled + cell);
 #pragma unroll
                 for (int v = 0; v < V; ++v)
                   if (id[v] == want) { acc[v] += d.v[v]; val[v] = pv.v[v]; hit[v] = true; }
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(256) mpf_bwd_kernel(MpfBwdArgs a) {
         float o[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-          const float dv = hit[v] ? acc[v] * act_der(a.act, val[v]) : 0.f;
+          const float dv = hit[v] ? (a.premul ? acc[v] : acc[v] * act_der(a.act, val[v])) : 0.f;
           bsum[v] += dv;
           o[v] = a.round_tf32 ? tf32_rna(dv) : dv;
         }
@@ -375,7 +375,8 @@ __global__ void __launch_bounds__(256) mpf_bwd_slide_kernel(MpfBwdArgs a) {
             }
             const size_t cell = (fbase + rp + colpart[dx]) * C + cv * 4;
             const float4 d = ldg4_pred(a.dout + cell, any);
-            const float4 pv = ldg4_pred(a.pooled + cell, any);
+            // premul: the delta already carries act'(y) (applied by the producing dgrad)
+            const float4 pv = ldg4_pred(a.pooled + cell, any && !a.premul);
             const float dd[4] = {d.x, d.y, d.z, d.w}, pp[4] = {pv.x, pv.y, pv.z, pv.w};
 #pragma unroll
             for (int v = 0; v < 4; ++v)
@@ -385,7 +386,7 @@ __global__ void __launch_bounds__(256) mpf_bwd_slide_kernel(MpfBwdArgs a) {
         float o[4];
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
-          const float dv = hit[v] ? acc[v] * act_der(a.act, val[v]) : 0.f;
+          const float dv = hit[v] ? (a.premul ? acc[v] : acc[v] * act_der(a.act, val[v])) : 0.f;
           bsum[v] += dv;
           o[v] = a.round_tf32 ? tf32_rna(dv) : dv;
         }
