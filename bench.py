@@ -90,6 +90,18 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def _ncu_traffic(workload, kernel, layer):
+    """DRAM bytes (read + write) per launch of `kernel` at `layer`, from the committed
+    `ncu --set full` capture summary (profiles/ncu_traffic.json, written by
+    scripts/ncu_traffic.py from the same kernel at the same config), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            table = json.load(f)
+        return table.get(f"{workload}:{kernel}:{layer}")
+    except Exception:
+        return None
+
+
 def cpu_baseline(cfg, seconds=12.0, seed=0):
     """The oracle O1 (naive patch-by-patch fp64, as it stands) on a bounded pixel sample
     of one image of the same workload, on this host's cores."""
@@ -305,7 +317,7 @@ def main():
         roof = {"bound": "hbm", "achieved": dom["bytes"] / avg_ms / 1e6, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "peak_source": f"{src} hbm_gbs"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
+    roof["traffic"] = _ncu_traffic(cfg.name, name, dom["layer"])
     roof["kernel"] = f"{name}[layer {dom['layer']}]"
     roof["share_of_step"] = dom["total_ms"] / ms
     roof["algorithmic_per_launch"] = dom["flops"] if roof["bound"] != "hbm" else dom["bytes"]

@@ -610,8 +610,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int mt = blockIdx.x % p.m_tiles;
   const int set = (blockIdx.x / p.m_tiles) % p.n_sets;
   const int split = blockIdx.x / (p.m_tiles * p.n_sets);
-  const int g0 = set * p.G;
-  const int G = min(p.G, p.n_groups - g0);
+  // groups are spread evenly over the sets (equal MMA work per CTA keeps the sets of a
+  // split in lockstep, so their shared dY / X tiles are L2 hits)
+  const int g0 = (int)((long long)set * p.n_groups / p.n_sets);
+  const int G = (int)((long long)(set + 1) * p.n_groups / p.n_sets) - g0;
   const int N = 32 * p.k;
   const long long pbeg = (long long)split * p.chunk_stages * kWR;
 
@@ -733,7 +735,7 @@ cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits_out, cudaStream_t 
   p.tmem_cols = cols;
   const long long total_stages = (p.P_tot + kWR - 1) / kWR;
   const int per_split_blocks = p.m_tiles * p.n_sets;
-  int splits = (int)((2 * 148 + per_split_blocks - 1) / per_split_blocks);
+  int splits = num_sms() / per_split_blocks;  // one wave of co-resident CTAs
   if (splits > kMaxSplits) splits = kMaxSplits;
   if (splits < 1) splits = 1;
   const size_t K = (size_t)a.k * a.k * a.cin;

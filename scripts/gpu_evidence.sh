@@ -1,0 +1,14 @@
+# round evidence: default bench line, launch list (ncu timing only) and a full ncu capture of one step
+set -x
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke $? >> gpurun_out/status.txt
+timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1; echo bench $? >> gpurun_out/status.txt
+timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_reference.log 2>&1; echo ref $? >> gpurun_out/status.txt
+timeout 600 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/plain.log 2>&1 &&
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg4.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo launches $? >> gpurun_out/status.txt
+for w in cfg4 cfg5; do
+  timeout 300 python scripts/run_step.py --workload $w --order-json gpurun_out/order_$w.json > gpurun_out/order_$w.log 2>&1
+  timeout 300 python scripts/run_step.py --workload $w > gpurun_out/plain_$w.log 2>&1 &&
+  timeout 1500 ncu -f --set full --clock-control none --profile-from-start off -o /tmp/ncu_$w python scripts/run_step.py --workload $w > gpurun_out/ncu_$w.log 2>&1; echo ncu_$w $? >> gpurun_out/status.txt
+  ncu -i /tmp/ncu_$w.ncu-rep --page raw --csv 2>/dev/null | gzip > gpurun_out/ncu_${w}_raw.csv.gz
+done

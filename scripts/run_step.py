@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--images", type=int, default=0, help="0 = the config's global batch")
     ap.add_argument("--precision", default="tf32")
+    ap.add_argument("--order-json", default="", help="write the (kernel, layer) launch order of one step here")
     a = ap.parse_args()
     cfg = S.CONFIGS[a.workload]
     n = a.images or cfg.global_batch
@@ -43,6 +44,14 @@ def main():
     for _ in range(a.warmup):
         step()
     net.check()
+    torch.cuda.synchronize()
+    if a.order_json:  # one extra step through the library's own launch timer (not profiled)
+        import json
+        net.profile_begin(1000)
+        step()
+        recs = net.profile_end()
+        with open(a.order_json, "w") as f:
+            json.dump([[r["name"], r["layer"], r["total_ms"], r["flops"], r["bytes"]] for r in recs], f)
     torch.cuda.synchronize()
     torch.cuda.cudart().cudaProfilerStart()
     step()
