@@ -210,8 +210,11 @@ static void layout_memory(Net* N, int n) {
     const Act& in = N->a[l];
     if (P.L.kind == MPF_POOL) {
       MpfBwdArgs m{};
-      m.gr = in.gr; m.gc = in.gc; m.C = in.C; m.n_frag_in = n * in.F;
-      bp = std::max(bp, (size_t)mpf_bwd_partials(m) * in.C);
+      m.gr = in.gr; m.gc = in.gc; m.C = in.C; m.n_frag_in = n * in.F; m.k = P.L.k;
+      for (int pm = 0; pm <= 1; ++pm) {  // both kernel variants (premultiplied or not)
+        m.premul = pm;
+        bp = std::max(bp, (size_t)mpf_bwd_partials(m) * in.C);
+      }
     } else {
       const Act& o = N->a[l + 1];
       bp = std::max(bp, (size_t)channel_partials((long long)n * o.F * o.gr * o.gc) * o.C);

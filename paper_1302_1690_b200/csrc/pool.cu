@@ -415,6 +415,99 @@ __global__ void __launch_bounds__(256) mpf_bwd_slide_kernel(MpfBwdArgs a) {
   }
 }
 
+// Shared-memory tiled gather (premul deltas, 4-channel vectors, any K <= 4).  A CTA owns
+// a TY x TX tile of conv-output positions of one input fragment and walks down the
+// fragment's rows tile by tile.  Per tile it first stages, with fully coalesced and
+// mutually independent loads, the argmax bytes and deltas of every window that can
+// select a tile element ((TY+K-1) x (TX+K-1) windows, absent windows marked 0xFF), then
+// every element gathers its K^2 candidates from shared memory in the same fixed (dy, dx)
+// order as the other MPF backward kernels (bitwise-identical results).  No dependent
+// global-load chains remain; the halo re-reads hit L2.
+constexpr int kTBY = 8, kTBX = 8;
+
+template <int K>
+__global__ void __launch_bounds__(256) mpf_bwd_tile_kernel(MpfBwdArgs a, int rows_per_cta) {
+  extern __shared__ __align__(16) uint8_t sm_raw[];
+  constexpr int WY = kTBY + K - 1, WX = kTBX + K - 1;
+  const int C = a.C, CV = C / 4;
+  uint32_t* s_id = reinterpret_cast<uint32_t*>(sm_raw);                   // [WY][WX][CV]
+  float4* s_d = reinterpret_cast<float4*>(sm_raw + ((size_t)WY * WX * CV * 4 + 15) / 16 * 16);  // [WY][WX][CV]
+  float* s_red = reinterpret_cast<float*>(s_d + WY * WX * CV);            // [256 / CV][C]
+  const int Xw = K * a.m_c, Yw = K * a.m_r;
+  const int MM = a.m_r * a.m_c;
+  const int X0 = blockIdx.x * kTBX;
+  const int tid = threadIdx.x;
+  const int cv = tid % CV, pt = tid / CV, npt = 256 / CV;  // compute mapping (pt < npt)
+  float bsum[4] = {0.f, 0.f, 0.f, 0.f};
+  const int ybeg = blockIdx.y * rows_per_cta, yend = min(ybeg + rows_per_cta, a.gr);
+  for (int g = blockIdx.z; g < a.n_frag_in; g += gridDim.z) {
+    const size_t fbase = (size_t)g * K * K * MM;
+    for (int Y0 = ybeg; Y0 < yend; Y0 += kTBY) {
+      __syncthreads();  // previous tile's shared data fully consumed
+      // ---- stage windows wy in [Y0-K+1, Y0+kTBY), wx in [X0-K+1, X0+kTBX)
+      for (int e = tid; e < WY * WX * CV; e += 256) {
+        const int c4 = e % CV, t = e / CV, wxl = t % WX, wyl = t / WX;
+        const int wy = Y0 - K + 1 + wyl, wx = X0 - K + 1 + wxl;
+        uint32_t idv = 0xFFFFFFFFu;
+        float4 dv = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (wy >= 0 && wy < Yw && wx >= 0 && wx < Xw) {
+          const size_t cell = (fbase + (size_t)((wy % K) * K + (wx % K)) * MM + (wy / K) * a.m_c + wx / K) * C + c4 * 4;
+          idv = __ldg(reinterpret_cast<const uint32_t*>(a.idx + cell));
+          dv = __ldg(reinterpret_cast<const float4*>(a.dout + cell));
+        }
+        s_id[e] = idv;
+        s_d[e] = dv;
+      }
+      __syncthreads();
+      // ---- gather: element (Y0+ty, X0+tx) sums window (ty+K-1-dy, tx+K-1-dx) where idx == dy*K+dx
+      if (pt < npt) {
+        for (int q = pt; q < kTBY * kTBX; q += npt) {
+          const int ty = q / kTBX, tx = q % kTBX;
+          const int Y = Y0 + ty, X = X0 + tx;
+          if (Y >= yend || X >= a.gc) continue;
+          float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int dy = 0; dy < K; ++dy)
+#pragma unroll
+            for (int dx = 0; dx < K; ++dx) {
+              const int w = ((ty + K - 1 - dy) * WX + (tx + K - 1 - dx)) * CV + cv;
+              const uint32_t id = s_id[w];
+              const uint32_t want = (uint32_t)(dy * K + dx);
+              const float4 d = s_d[w];
+              if (((id) & 0xFFu) == want) acc[0] += d.x;
+              if (((id >> 8) & 0xFFu) == want) acc[1] += d.y;
+              if (((id >> 16) & 0xFFu) == want) acc[2] += d.z;
+              if (((id >> 24) & 0xFFu) == want) acc[3] += d.w;
+            }
+          float o[4];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            bsum[v] += acc[v];
+            o[v] = a.round_tf32 ? tf32_rna(acc[v]) : acc[v];
+          }
+          stv<4>(a.din + (((size_t)g * a.gr + Y) * a.gc + X) * C + cv * 4, o);
+        }
+      }
+    }
+  }
+  if (a.bias_part == nullptr) return;
+  __syncthreads();
+  if (pt < npt) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v) s_red[pt * C + cv * 4 + v] = bsum[v];
+  }
+  __syncthreads();
+  if (tid < CV) {
+    const size_t blin = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      float t = 0.f;
+      for (int q2 = 0; q2 < npt; ++q2) t += s_red[q2 * C + tid * 4 + v];
+      a.bias_part[blin * C + tid * 4 + v] = t;
+    }
+  }
+}
+
 // ----------------------------------------------------------------------------- channel sums
 // Generic per-channel partials of a [P][C] tensor (bias gradient of a conv whose delta
 // comes from a dgrad, i.e. a conv followed by another conv).
@@ -472,9 +565,24 @@ cudaError_t launch_mpf_fwd(const MpfArgs& a, cudaStream_t s) {
   return fwd_dispatch<1>(a, s);
 }
 
+static bool bwd_tile(const MpfBwdArgs& a) {
+  return a.premul && a.C % 4 == 0 && a.C <= 1024 && a.k >= 2 && a.k <= 4 && !getenv("MPF_BWD_SLIDE");
+}
 static bool bwd_slide(const MpfBwdArgs& a) { return a.C % 4 == 0 && a.k >= 2 && a.k <= 4; }
+constexpr int kTileRows = 64;  // conv-output rows per CTA of the tiled kernel (partials per CTA)
+
+static size_t tile_smem(const MpfBwdArgs& a) {
+  const int CV = a.C / 4, WY = kTBY + a.k - 1, WX = kTBX + a.k - 1;
+  return ((size_t)WY * WX * CV * 4 + 15) / 16 * 16 + (size_t)WY * WX * CV * 16 + sizeof(float) * (256 / CV) * a.C;
+}
 
 static void bwd_geometry(const MpfBwdArgs& a, int V, dim3* grid, dim3* blk) {
+  if (bwd_tile(a)) {
+    *blk = dim3(256, 1, 1);
+    *grid = dim3((a.gc + kTBX - 1) / kTBX, (a.gr + kTileRows - 1) / kTileRows,
+                 a.n_frag_in < 65535 ? a.n_frag_in : 65535);
+    return;
+  }
   const int ty = block_dims(a.C, V, blk);
   const int band = bwd_slide(a) ? kBandB : kBand;
   *grid = dim3((a.gc + ty - 1) / ty, (a.gr + band - 1) / band, a.n_frag_in < 65535 ? a.n_frag_in : 65535);
@@ -490,6 +598,22 @@ cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s) {
   const int V = a.C % 4 == 0 ? 4 : 1;
   dim3 grid, blk;
   bwd_geometry(a, V, &grid, &blk);
+  if (bwd_tile(a)) {
+    const size_t sm = tile_smem(a);
+    cudaError_t e = cudaSuccess;
+    if (a.k == 2) {
+      e = cudaFuncSetAttribute(mpf_bwd_tile_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      mpf_bwd_tile_kernel<2><<<grid, blk, sm, s>>>(a, kTileRows);
+    } else if (a.k == 3) {
+      e = cudaFuncSetAttribute(mpf_bwd_tile_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      mpf_bwd_tile_kernel<3><<<grid, blk, sm, s>>>(a, kTileRows);
+    } else {
+      e = cudaFuncSetAttribute(mpf_bwd_tile_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      mpf_bwd_tile_kernel<4><<<grid, blk, sm, s>>>(a, kTileRows);
+    }
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+  }
   const size_t smem = sizeof(float) * blk.y * a.C;
   if (bwd_slide(a) && !getenv("MPF_BWD_GENERIC")) {
     if (a.k == 2) mpf_bwd_slide_kernel<2><<<grid, blk, smem, s>>>(a);
