@@ -123,7 +123,7 @@ constexpr int kWTH = 8, kWTW = 32;  // wgrad tile: 256 positions
 constexpr int kWCO = 8, kWT = 4;    // accumulators per thread: 8 maps x 4 taps
 
 template <int K>
-__global__ void __launch_bounds__(256) conv_first_wgrad_kernel(FirstWgradArgs a) {
+__global__ void __launch_bounds__(256, 3) conv_first_wgrad_kernel(FirstWgradArgs a) {
   extern __shared__ float sm[];
   constexpr int IW = kWTW + K - 1, IH = kWTH + K - 1;
   constexpr int NT = (K * K + kWT - 1) / kWT;  // tap groups
@@ -255,7 +255,7 @@ bool first_conv_supported(int cin, int cout, int k) {
   return n_cog * NT <= 256;
 }
 
-int first_wgrad_blocks() { return 148 * 2; }
+int first_wgrad_blocks() { return 148 * 3; }  // 3 co-resident CTAs per SM overlap staging with compute
 
 cudaError_t launch_first_conv(FirstConvArgs a, cudaStream_t s) {
   a.n_cog = (a.cout + kFCO - 1) / kFCO;

@@ -197,6 +197,10 @@ static void layout_memory(Net* N, int n) {
   s = align256(s + sizeof(float) * wp);
   N->off_part = s;
   N->part_floats = max_part * (size_t)kMaxSplits;
+  {  // the first layer's CUDA-core weight gradient writes one partial per CTA
+    const LayerPlan& P0 = N->lp[0];
+    N->part_floats = std::max(N->part_floats, (size_t)first_wgrad_blocks() * P0.cout * P0.L.k * P0.L.k);
+  }
   s = align256(s + sizeof(float) * N->part_floats);
   N->off_nlab = s; s = align256(s + sizeof(int) * n);
   // bias / head partials (fixed-order two-level reductions)

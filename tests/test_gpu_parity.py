@@ -267,3 +267,71 @@ def test_fewer_images_than_capacity():
     g = gpu_step(cfg.layers, cfg.P, images, labels, params, "tf32", net=net)
     o = oracle_step(cfg.layers, cfg.P, images.astype(np.float64), labels, params, engine="o2")
     compare_step(cfg.layers, g, o, TOL_TF32, "n < capacity")
+
+
+# ----------------------------------------------------------------- full images, kernel variants
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg5"])
+def test_full_image_all_pixels_vs_o2(name):
+    """One whole BASELINE image (512^2 / 768^2), every output pixel labelled, TF32 path (the
+    bench configuration) against the literal whole-image oracle O2 in fp64: outputs, loss
+    and every weight/bias gradient within rel L2 5e-3 (R17)."""
+    cfg = S.CONFIGS[name]
+    images, labels = S.make_batch(cfg, [11])
+    params = S.init_params(cfg)
+    g = gpu_step(cfg.layers, cfg.P, images, labels, params, "tf32")
+    o = oracle_step(cfg.layers, cfg.P, images.astype(np.float64), labels, params, engine="o2")
+    errs = compare_step(cfg.layers, g, o, TOL_TF32, f"{name} full image")
+    print(name, "full-image rel L2:", {k: f"{v:.1e}" for k, v in errs.items()})
+
+
+def _run_variant(env, name="cfg2", n=2, prec="tf32"):
+    import os
+    cfg = S.CONFIGS[name]
+    images, labels = S.make_batch(cfg, list(range(n)))
+    params = S.init_params(cfg)
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        g = gpu_step(cfg.layers, cfg.P, images, labels, params, prec)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    return cfg, g
+
+
+def test_cta_pair_matches_single_cta_mma():
+    """The cta_group::2 (M = 256) and single-CTA (M = 128) tensor-core convolutions compute
+    the same sums in the same K order: identical results up to fp32 accumulation order
+    inside the tensor core."""
+    cfg, a = _run_variant({"MPF_TC_PAIR": "1"})
+    _, b = _run_variant({"MPF_TC_PAIR": "0"})
+    assert rel_l2(a["probs"], b["probs"]) <= 1e-6
+    for nm, sl in param_slices(cfg.layers):
+        assert rel_l2(a["grad_sum"][sl], b["grad_sum"][sl]) <= 1e-5, nm
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg5s"])
+def test_mpf_backward_tiled_equals_sliding_bitwise(name):
+    """Shared-memory tiled and register-sliding MPF backward gather the same candidates in
+    the same fixed (dy, dx) order: bitwise-identical gradients."""
+    if name == "cfg5s":  # k = 3 pools on a reduced 168^2 image of the cfg5 net
+        import dataclasses
+        cfg5 = S.CONFIGS["cfg5"]
+        S.CONFIGS["cfg5s"] = dataclasses.replace(cfg5, name="cfg5s", H=168, W=168)
+    try:
+        cfg, a = _run_variant({}, name=name)
+        _, b = _run_variant({"MPF_BWD_SLIDE": "1"}, name=name)
+    finally:
+        S.CONFIGS.pop("cfg5s", None)
+    # the routed deltas are bitwise equal, hence every weight gradient; bias sums are
+    # reduced over differently shaped blocks (fixed order each), so only to rounding
+    for nm, sl in param_slices(cfg.layers):
+        if nm.startswith("W"):
+            assert np.array_equal(a["grad_sum"][sl], b["grad_sum"][sl]), nm
+        else:
+            assert rel_l2(a["grad_sum"][sl], b["grad_sum"][sl]) <= 1e-5, nm
+    assert np.array_equal(a["loss"], b["loss"])
