@@ -478,9 +478,13 @@ cudaError_t launch_nacc(const CUtensorMap& A, const CUtensorMap& B, const CUtens
   return cudaGetLastError();
 }
 
-bool use_pair() {
-  const char* e = getenv("MPF_TC_PAIR");
-  return e ? atoi(e) != 0 : true;
+// CTA-pair policy: the pair halves the weight stream per SM, which pays only for wide,
+// deep layers (N >= 192, or N >= 128 with K >= 1536); everywhere else the single-CTA MMA
+// measured as fast or faster (per-layer A/B on cfg4/cfg5).
+// MPF_TC_PAIR=1/0 forces a mode.
+bool want_pair(int npad, int K) {
+  if (const char* e = getenv("MPF_TC_PAIR")) return atoi(e) != 0;
+  return npad >= 192 || (npad >= 128 && K >= 1536);
 }
 
 }  // namespace
@@ -521,26 +525,33 @@ cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s) {
   const int rows_needed = m_cta + a.k - 1;
   p.nbox = (rows_needed + 255) / 256;
   p.box_rows = ((rows_needed + p.nbox - 1) / p.nbox + 7) / 8 * 8;
-  const bool pair = use_pair();
   p.a_slot_bytes = (uint32_t)(p.nbox * p.box_rows * 128);
-  p.b_rows = pair ? p.npad / 2 : p.npad;  // a CTA of a pair stages half of every weight tile
-  p.b_slot_bytes = (uint32_t)(p.b_rows * 128);
   // shared memory: stages of [A slab | k weight taps] (2..4, as many as fit), epilogue
   // staging (two boxes per warp when 3 stages still fit, else one)
-  p.stage_bytes = p.a_slot_bytes + (uint32_t)a.k * p.b_slot_bytes;
   const size_t base_fixed = 1024 + 4 * 256 + 512;
   const size_t total = 227 * 1024;
   int ns = 0, nst = 0;
-  for (int cand_ns = 2; cand_ns >= 1 && !ns; --cand_ns) {
-    const size_t budget = total - base_fixed - (size_t)cand_ns * kEpiWarps * kStageBytes;
-    int cand = (int)(budget / p.stage_bytes);
-    if (cand > 4) cand = 4;
-    if (cand >= 3 || (cand_ns == 1 && cand >= 2)) {
-      ns = cand_ns;
-      nst = cand;
+  auto plan_smem = [&](bool pr) {
+    p.b_rows = pr ? p.npad / 2 : p.npad;  // a CTA of a pair stages half of every weight tile
+    p.b_slot_bytes = (uint32_t)(p.b_rows * 128);
+    p.stage_bytes = p.a_slot_bytes + (uint32_t)a.k * p.b_slot_bytes;
+    ns = nst = 0;
+    for (int cand_ns = 2; cand_ns >= 1 && !ns; --cand_ns) {
+      const size_t budget = total - base_fixed - (size_t)cand_ns * kEpiWarps * kStageBytes;
+      int cand = (int)(budget / p.stage_bytes);
+      if (cand > 4) cand = 4;
+      if (cand >= 3 || (cand_ns == 1 && cand >= 2)) {
+        ns = cand_ns;
+        nst = cand;
+      }
     }
+    return ns != 0;
+  };
+  bool pair = want_pair(p.npad, a.k * a.k * a.cin);
+  if (!plan_smem(pair)) {  // the other mode may fit (a pair stages half the weights)
+    pair = !pair;
+    if (!plan_smem(pair)) return cudaErrorInvalidConfiguration;
   }
-  if (!ns) return cudaErrorInvalidConfiguration;
   const size_t fixed = base_fixed + (size_t)ns * kEpiWarps * kStageBytes;
   p.n_stage = ns;
   p.n_stages = nst;
