@@ -57,7 +57,9 @@ __host__ __device__ inline size_t head_region0(int C, int Ch) {
   return ((red > tiles ? red : tiles) + 127) / 128 * 128;
 }
 
-template <int NC, bool TRAIN, bool TANH>
+// VEC (Ch % 4 == 0): both phases work on float4 channel groups (LDS.128 / STG.128, one
+// W_L row fetch per 4 channels), which halves the instruction count per element.
+template <int NC, bool TRAIN, bool TANH, bool VEC>
 __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int C = a.C, Ch = a.Ch;
@@ -105,12 +107,22 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
   const int M = Ch >> 2;  // channels per lane in phase A (Ch % 4 == 0 path)
   const int rot = pa % (M > 0 ? M : 1);
   constexpr int kMC = 8;  // channel slots per lane in phase B (Ch <= 256)
-  float accW[kMC][NC], accP[kMC], accL[NC];
+  constexpr int kMG = 2;  // float4 channel groups per lane in phase B (VEC; Ch <= 256)
+  float accW[VEC ? 1 : kMC][NC], accP[VEC ? 1 : kMC], accL[NC];
+  float accW4[VEC ? kMG : 1][NC][4], accP4[VEC ? kMG : 1][4];
+#pragma unroll
+  for (int m = 0; m < (VEC ? kMG : 1); ++m)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      accP4[m][u] = 0.f;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) accW4[m][c][u] = 0.f;
+    }
   // W_L[:, ch] of this lane's phase-B channels, held in registers (constant over tiles)
-  constexpr bool kWReg = NC <= 4;
+  constexpr bool kWReg = !VEC && NC <= 4;
   float wreg[kWReg ? kMC : 1][kWReg ? NC : 1];
 #pragma unroll
-  for (int m = 0; m < kMC; ++m) {
+  for (int m = 0; m < (VEC ? 1 : kMC); ++m) {
     accP[m] = 0.f;
 #pragma unroll
     for (int c = 0; c < NC; ++c) accW[m][c] = 0.f;
@@ -184,7 +196,18 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
       float z[NC];
 #pragma unroll
       for (int c = 0; c < NC; ++c) z[c] = 0.f;
-      if (need) {  // uniform over the 4 lanes of a position
+      if (need && VEC) {  // float4 channel groups g = qa, qa + 4, ...
+        const float4* hrow4 = reinterpret_cast<const float4*>(hs + pa * Ch);
+        const int G4 = Ch >> 2;
+        for (int g = qa; g < G4; g += 4) {
+          const float4 hv = hrow4[g];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            const float4 w = reinterpret_cast<const float4*>(s_w2 + c * Ch)[g];
+            z[c] = fmaf(w.x, hv.x, fmaf(w.y, hv.y, fmaf(w.z, hv.z, fmaf(w.w, hv.w, z[c]))));
+          }
+        }
+      } else if (need) {  // uniform over the 4 lanes of a position
         const float* hrow = hs + pa * Ch;
         if (bulk) {
           for (int m = 0; m < M; ++m) {
@@ -274,6 +297,36 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
             if (lane + 32 * m < Ch) dh_row[lane + 32 * m] = 0.f;
           continue;
         }
+        if constexpr (VEC) {
+#pragma unroll
+          for (int m = 0; m < kMG; ++m) {
+            const int g = lane + 32 * m;
+            if (4 * g < Ch) {
+              const float4 hv = reinterpret_cast<const float4*>(hs + p * Ch)[g];
+              const float hh[4] = {hv.x, hv.y, hv.z, hv.w};
+              float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+              for (int c = 0; c < NC; ++c) {
+                const float4 w = reinterpret_cast<const float4*>(s_w2 + c * Ch)[g];
+                const float ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  sacc[u] = fmaf(ww[u], dl[c], sacc[u]);
+                  accW4[m][c][u] = fmaf(dl[c], hh[u], accW4[m][c][u]);
+                }
+              }
+              float d[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                d[u] = sacc[u] * (TANH ? fmaf(-hh[u], hh[u], 1.f) : act_der(a.hidden_act, hh[u]));
+                accP4[m][u] += d[u];
+                if (a.round_tf32) d[u] = tf32_rna(d[u]);
+              }
+              reinterpret_cast<float4*>(dh_row)[g] = make_float4(d[0], d[1], d[2], d[3]);
+            }
+          }
+          continue;
+        }
 #pragma unroll
         for (int m = 0; m < kMC; ++m) {
           const int ch = lane + 32 * m;
@@ -284,10 +337,10 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
             for (int c = 0; c < NC; ++c) {
               const float w = kWReg ? wreg[kWReg ? m : 0][kWReg ? c : 0] : s_w2[c * Ch + ch];
               sacc = fmaf(w, dl[c], sacc);
-              accW[m][c] = fmaf(dl[c], hv, accW[m][c]);
+              accW[VEC ? 0 : m][c] = fmaf(dl[c], hv, accW[VEC ? 0 : m][c]);
             }
             const float d = sacc * (TANH ? fmaf(-hv, hv, 1.f) : act_der(a.hidden_act, hv));
-            accP[m] += d;
+            accP[VEC ? 0 : m] += d;
             dh_row[ch] = a.round_tf32 ? tf32_rna(d) : d;
           }
         }
@@ -300,14 +353,30 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
   // red[warp][ch][0..C) = accW, red[warp][ch][C] = accP; redL[warp][c] = accL (lane 0)
   float* red = hb0;  // tiles are no longer needed
   const int RW = C + 1;
+  if constexpr (VEC) {
 #pragma unroll
-  for (int m = 0; m < kMC; ++m) {
-    const int ch = lane + 32 * m;
-    if (ch < Ch) {
+    for (int m = 0; m < kMG; ++m) {
+      const int g = lane + 32 * m;
+      if (4 * g < Ch) {
 #pragma unroll
-      for (int c = 0; c < NC; ++c)
-        if (c < C) red[(warp * Ch + ch) * RW + c] = accW[m][c];
-      red[(warp * Ch + ch) * RW + C] = accP[m];
+        for (int u = 0; u < 4; ++u) {
+#pragma unroll
+          for (int c = 0; c < NC; ++c)
+            if (c < C) red[(warp * Ch + 4 * g + u) * RW + c] = accW4[m][c][u];
+          red[(warp * Ch + 4 * g + u) * RW + C] = accP4[m][u];
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int m = 0; m < kMC; ++m) {
+      const int ch = lane + 32 * m;
+      if (ch < Ch) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+          if (c < C) red[(warp * Ch + ch) * RW + c] = accW[m][c];
+        red[(warp * Ch + ch) * RW + C] = accP[m];
+      }
     }
   }
   float* redL = red + (kThr / 32) * Ch * RW;
@@ -341,10 +410,10 @@ size_t head_smem(int C, int Ch) {
 
 template <int NC, bool TRAIN, bool TANH>
 cudaError_t launch_k(const HeadArgs& a, size_t smem, cudaStream_t s) {
-  cudaError_t e =
-      cudaFuncSetAttribute(head_kernel<NC, TRAIN, TANH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = (a.Ch % 4 == 0) ? head_kernel<NC, TRAIN, TANH, true> : head_kernel<NC, TRAIN, TANH, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  head_kernel<NC, TRAIN, TANH><<<a.n_blocks, kThr, smem, s>>>(a);
+  kern<<<a.n_blocks, kThr, smem, s>>>(a);
   return cudaGetLastError();
 }
 
