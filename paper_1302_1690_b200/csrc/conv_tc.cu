@@ -521,11 +521,13 @@ cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s) {
     const int m = atoi(e);
     if (m >= 1 && nacc > m) nacc = m;
   }
-  const int m_cta = nacc * 128;
-  const int rows_needed = m_cta + a.k - 1;
-  p.nbox = (rows_needed + 255) / 256;
-  p.box_rows = ((rows_needed + p.nbox - 1) / p.nbox + 7) / 8 * 8;
-  p.a_slot_bytes = (uint32_t)(p.nbox * p.box_rows * 128);
+  auto set_nacc = [&](int na) {
+    const int rows_needed = na * 128 + a.k - 1;
+    p.nbox = (rows_needed + 255) / 256;
+    p.box_rows = ((rows_needed + p.nbox - 1) / p.nbox + 7) / 8 * 8;
+    p.a_slot_bytes = (uint32_t)(p.nbox * p.box_rows * 128);
+  };
+  set_nacc(nacc);
   // shared memory: stages of [A slab | k weight taps] (2..4, as many as fit), epilogue
   // staging (two boxes per warp when 3 stages still fit, else one)
   const size_t base_fixed = 1024 + 4 * 256 + 512;
@@ -547,11 +549,27 @@ cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s) {
     }
     return ns != 0;
   };
+  // keep the preferred mode and give up accumulator depth first (a smaller A slab lets two
+  // stages fit: measured faster than switching mode); then try the other mode
   bool pair = want_pair(p.npad, a.k * a.k * a.cin);
-  if (!plan_smem(pair)) {  // the other mode may fit (a pair stages half the weights)
-    pair = !pair;
-    if (!plan_smem(pair)) return cudaErrorInvalidConfiguration;
+  bool ok = false;
+  for (int na = nacc; na >= 1 && !ok; --na) {
+    set_nacc(na);
+    if (plan_smem(pair)) {
+      nacc = na;
+      ok = true;
+    }
   }
+  for (int na = nacc; na >= 1 && !ok; --na) {
+    set_nacc(na);
+    if (plan_smem(!pair)) {
+      nacc = na;
+      pair = !pair;
+      ok = true;
+    }
+  }
+  if (!ok) return cudaErrorInvalidConfiguration;
+  const int m_cta = nacc * 128;
   const size_t fixed = base_fixed + (size_t)ns * kEpiWarps * kStageBytes;
   p.n_stage = ns;
   p.n_stages = nst;
