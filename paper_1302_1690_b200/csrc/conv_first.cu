@@ -129,9 +129,10 @@ __global__ void __launch_bounds__(256, 3) conv_first_wgrad_kernel(FirstWgradArgs
   constexpr int NT = (K * K + kWT - 1) / kWT;  // tap groups
   const int coutp = a.n_cog * kWCO;
   constexpr int IMG = (IH * IW + 3) / 4 * 4;
-  float* s_img = sm;             // [IH][IW]
-  float* s_dy = sm + IMG;        // [kWTH*kWTW][coutp]
-  float* s_red = s_dy;           // end-of-kernel reduction (aliases the delta tile)
+  // two buffers of [image tile | delta tile], filled with cp.async one tile ahead
+  const int buf_floats = IMG + kWTH * kWTW * coutp;
+  float* s_red = sm;             // end-of-kernel reduction (aliases buffer 0)
+  const bool async = coutp == a.cout;  // delta rows are whole 16-B vectors (cout % 8 == 0)
   const int per_stream = a.n_cog * NT;
   const int n_streams = blockDim.x / per_stream;
   const int stream = threadIdx.x / per_stream, r = threadIdx.x % per_stream;
@@ -150,28 +151,58 @@ __global__ void __launch_bounds__(256, 3) conv_first_wgrad_kernel(FirstWgradArgs
     for (int u = 0; u < kWT; ++u) acc[o][u] = 0.f;
   const int tiles_x = (a.gc + kWTW - 1) / kWTW, tiles_y = (a.gr + kWTH - 1) / kWTH;
   const long long total = (long long)a.n * tiles_x * tiles_y;
-  for (long long tile = blockIdx.x; tile < total; tile += gridDim.x) {
+  // stage tile `tile` into buffer `b`: image tile (zero outside H x W) and delta tile
+  // [256 positions][cout] (zero outside the grid)
+  auto stage = [&](long long tile, int b) {
+    float* s_img = sm + b * buf_floats;
+    float* s_dy = s_img + IMG;
     const int tx_ = (int)(tile % tiles_x);
     const long long t2 = tile / tiles_x;
     const int ty_ = (int)(t2 % tiles_y), img = (int)(t2 / tiles_y);
     const int y0 = ty_ * kWTH, x0 = tx_ * kWTW;
-    __syncthreads();
     for (int e = threadIdx.x; e < IH * IW; e += blockDim.x) {
       const int iy = e / IW, ix = e % IW;
       const int gy = y0 + iy, gx = x0 + ix;
-      float v = 0.f;
-      if (gy < a.H && gx < a.W) v = a.img[((size_t)img * a.H + gy) * a.W + gx];
-      s_img[e] = v;
+      const bool in = gy < a.H && gx < a.W;
+      const float* src = a.img + (in ? ((size_t)img * a.H + gy) * a.W + gx : 0);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(s_img + e)),
+                   "l"(src), "r"(in ? 4 : 0)
+                   : "memory");
     }
-    // delta tile [256 positions][cout] (zero outside the grid); rows of cout floats
-    for (int e = threadIdx.x; e < kWTH * kWTW * coutp; e += blockDim.x) {
-      const int co = e % coutp, p = e / coutp;
-      const int y = y0 + p / kWTW, x = x0 + p % kWTW;
-      float v = 0.f;
-      if (co < a.cout && y < a.gr && x < a.gc) v = a.dy[(((size_t)img * a.gr + y) * a.gc + x) * a.cout + co];
-      s_dy[e] = v;
+    if (async) {
+      const int vec = coutp / 4;
+      for (int e = threadIdx.x; e < kWTH * kWTW * vec; e += blockDim.x) {
+        const int v4 = e % vec, p = e / vec;
+        const int y = y0 + p / kWTW, x = x0 + p % kWTW;
+        const bool in = y < a.gr && x < a.gc;
+        const float* src = a.dy + (in ? (((size_t)img * a.gr + y) * a.gc + x) * a.cout + 4 * v4 : 0);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(s_dy + p * coutp + 4 * v4)),
+                     "l"(src), "r"(in ? 16 : 0)
+                     : "memory");
+      }
+    } else {
+      for (int e = threadIdx.x; e < kWTH * kWTW * coutp; e += blockDim.x) {
+        const int co = e % coutp, p = e / coutp;
+        const int y = y0 + p / kWTW, x = x0 + p % kWTW;
+        float v = 0.f;
+        if (co < a.cout && y < a.gr && x < a.gc) v = a.dy[(((size_t)img * a.gr + y) * a.gc + x) * a.cout + co];
+        s_dy[e] = v;
+      }
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (blockIdx.x < total) stage(blockIdx.x, 0);
+  int it = 0;
+  for (long long tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+    const int tx_ = (int)(tile % tiles_x);
+    (void)tx_;
+    if (tile + gridDim.x < total) stage(tile + gridDim.x, (it + 1) & 1);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // this tile's group has landed
     __syncthreads();
+    const float* s_img = sm + (it & 1) * buf_floats;
+    const float* s_dy = s_img + IMG;
     if (active) {
       for (int p = stream; p < kWTH * kWTW; p += n_streams) {
         const int py = p / kWTW, px = p % kWTW;
@@ -188,7 +219,9 @@ __global__ void __launch_bounds__(256, 3) conv_first_wgrad_kernel(FirstWgradArgs
           for (int u = 0; u < kWT; ++u) acc[o][u] = fmaf(dv[o], iv[u], acc[o][u]);
       }
     }
+    __syncthreads();  // this buffer is free for the stage issued next iteration
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   // fixed-order reduction over streams, then one partial per CTA: part[blk][co][tap]
   __syncthreads();
   const int KK = K * K;
@@ -233,7 +266,8 @@ size_t wgrad_smem(int n_cog) {
   const int n_streams = 256 / (n_cog * NT);
   const size_t tile = (size_t)kWTH * kWTW * coutp;
   const size_t red = (size_t)n_streams * coutp * K * K;
-  return sizeof(float) * (((kWTH + K - 1) * (kWTW + K - 1) + 3) / 4 * 4 + (tile > red ? tile : red));
+  const size_t bufs = 2 * ((((kWTH + K - 1) * (kWTW + K - 1) + 3) / 4 * 4) + tile);
+  return sizeof(float) * (bufs > red ? bufs : red);
 }
 
 template <int K>
