@@ -228,8 +228,7 @@ def main():
 
     def step(i):
         im, lb = pools[i % 2][0], pools[i % 2][1]
-        net.forward(im)
-        net.backward(lb)
+        net.train_step(im, lb)  # forward + backward (softmax head fused into the last hidden conv)
         D.allreduce_grads(net.grads)
         net.sgd_step(cfg.lr, 1.0 / B)
 

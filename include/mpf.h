@@ -157,13 +157,27 @@ mpf_status mpf_forward_image(mpf_net* net, const float* d_images, int32_t n, flo
 mpf_status mpf_backward_image(mpf_net* net, const uint8_t* d_labels, const float* h_class_w,
                               float* d_loss, void* stream);
 
+/*
+ * Forward + backward of n images in one call (the training step of PAPER.md:210 without
+ * the update): same results as mpf_forward_image followed by mpf_backward_image (up to
+ * fp32 summation order), but the softmax head (last FC + softmax + MCCE + dL/dx_hat,
+ * PAPER.md:110-113, 197) runs inside the epilogue of the last hidden layer's tensor-core
+ * convolution, so that layer's activations never reach device memory.  Gradients are
+ * ADDED to the bound buffer; d_loss[n] (device, may be NULL) receives the per-image mean
+ * losses.  Afterwards there is no tape to run mpf_backward_image on (MPF_ERR_STATE).
+ * Falls back to the unfused sequence when the head cannot be fused (non-tensor-core last
+ * hidden layer, > 8 classes).
+ */
+mpf_status mpf_train_step(mpf_net* net, const float* d_images, int32_t n, const uint8_t* d_labels,
+                          const float* h_class_w, float* d_loss, void* stream);
+
 /* SGD: theta <- theta - lr * grad_scale * g ; g <- 0. */
 mpf_status mpf_sgd_step(mpf_net* net, float lr, float grad_scale, void* stream);
 
 /*
  * One end-to-end step on HOST buffers: async copy h_images [n, in_channels, H, W]
- * and h_labels [n, out_rows, out_cols] into the bound staging area, forward,
- * backward, and an async copy of the per-image losses to h_loss[n].  If apply_sgd,
+ * and h_labels [n, out_rows, out_cols] into the bound staging area, mpf_train_step,
+ * and an async copy of the per-image losses to h_loss[n].  If apply_sgd,
  * also mpf_sgd_step(lr, grad_scale).  h_loss is valid after the stream is synchronised.
  */
 mpf_status mpf_train_step_host(mpf_net* net, const float* h_images, const uint8_t* h_labels,
@@ -188,6 +202,10 @@ mpf_status mpf_fragments_to_pixels(const mpf_net* net, const float* d_frag, floa
 enum { MPF_TAPE_VALUE = 0, MPF_TAPE_ARGMAX = 1 };
 mpf_status mpf_debug_tape(const mpf_net* net, int32_t layer, int32_t what, void* d_dst,
                           void* stream);
+
+/* Debug copy of a scratch region (which = 0: fused-head per-position losses, 1: first
+ * delta buffer (dh after mpf_train_step), 2: head / bias partials); parity tests only. */
+mpf_status mpf_debug_scratch(const mpf_net* net, int32_t which, void* d_dst, uint64_t bytes, void* stream);
 
 /* Synchronise `stream` and report device-side data errors (bad labels) and CUDA errors. */
 mpf_status mpf_check(mpf_net* net, void* stream);

@@ -21,7 +21,7 @@ MPF_MAX_LAYERS = 24
 # every symbol include/mpf.h declares
 EXPORTS = ("mpf_version", "mpf_last_error", "mpf_net_create", "mpf_net_destroy", "mpf_net_geometry",
            "mpf_net_memory", "mpf_net_bind", "mpf_forward_image", "mpf_backward_image", "mpf_sgd_step",
-           "mpf_train_step_host", "mpf_fragments_to_pixels", "mpf_debug_tape", "mpf_check", "mpf_profile_begin",
+           "mpf_train_step", "mpf_train_step_host", "mpf_fragments_to_pixels", "mpf_debug_tape", "mpf_debug_scratch", "mpf_check", "mpf_profile_begin",
            "mpf_profile_end")
 
 
@@ -80,6 +80,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.mpf_backward_image.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_float), vp, vp]
     lib.mpf_sgd_step.restype = st
     lib.mpf_sgd_step.argtypes = [vp, ctypes.c_float, ctypes.c_float, vp]
+    lib.mpf_train_step.restype = st
+    lib.mpf_train_step.argtypes = [vp, vp, i32, vp, ctypes.POINTER(ctypes.c_float), vp, vp]
     lib.mpf_train_step_host.restype = st
     lib.mpf_train_step_host.argtypes = [vp, vp, vp, i32, ctypes.POINTER(ctypes.c_float), vp, i32, ctypes.c_float,
                                         ctypes.c_float, vp]
@@ -87,6 +89,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.mpf_fragments_to_pixels.argtypes = [vp, vp, vp, i32, i32, vp]
     lib.mpf_debug_tape.restype = st
     lib.mpf_debug_tape.argtypes = [vp, i32, i32, vp, vp]
+    lib.mpf_debug_scratch.restype = st
+    lib.mpf_debug_scratch.argtypes = [vp, i32, vp, ctypes.c_uint64, vp]
     lib.mpf_check.restype = st
     lib.mpf_check.argtypes = [vp, vp]
     lib.mpf_profile_begin.restype = st

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stddef.h>
+#include <stdint.h>
 
 namespace mpf {
 
@@ -26,7 +27,28 @@ struct TcConvArgs {
   int zero_pad;       // (SIMT path) write zeros outside the valid region; the TC path always does
   const float* mul_dact;  // nullable: multiply by act'(mul_dact[same position])
   int dact;
+  const struct TcHeadArgs* head;  // nullable: fuse the softmax head into this (forward) conv
 };
+
+// Softmax head fused into the epilogue of the forward conv that produces the last hidden
+// layer h: instead of h the kernel writes
+// dh = (W_L^T dz) * act'(h) to `out`, per-position losses to row_loss, and per-CTA
+// partials [grid][C*Ch + C + Ch] = (dW_L, db_L, db_h) to part.
+struct TcHeadArgs {
+  const float* wL;       // [C][Ch] softmax FC weights (canonical 1x1)
+  const float* bL;       // [C]
+  int C;
+  const uint8_t* labels; // [n][O_H][O_W], 255 = ignore
+  int O_H, O_W, F, n_levels;
+  int pool_k[24];
+  const int* nlab;       // [n] labelled pixels per image
+  float cw[16];          // class weights
+  float* row_loss;       // [positions] w_t (lse - z_t) of labelled valid positions, else 0
+  float* part;           // [grid][C*Ch + C + Ch]
+  int* err;              // label >= C flag
+  int round_dh;          // round dh to tf32 (operand of the FC1 dgrad / wgrad MMAs)
+};
+bool tc_head_supported(int C, int Ch, int act);
 
 // Weight gradient: part[s][co][(ky*k+kx)*cin+ci] = sum_{p in split s} dy[p][co] * x[p+(ky,kx)][ci]
 struct TcWgradArgs {
@@ -40,7 +62,7 @@ struct TcWgradArgs {
 
 bool tc_supported(int cin, int cout, int k);
 bool tc_wgrad_supported(int cin, int cout, int k);
-cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s);
+cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s, int* grid_out = nullptr);
 cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits, cudaStream_t s);
 
 }  // namespace mpf

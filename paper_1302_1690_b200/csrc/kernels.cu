@@ -285,6 +285,27 @@ __global__ void loss_finalize_kernel(const float* __restrict__ part, int parts, 
   if (threadIdx.x == 0) loss[img] = nlab[img] > 0 ? s[0] / (float)nlab[img] : 0.f;
 }
 
+__global__ void loss_rows_kernel(const float* __restrict__ rl, long long per_img, const int* __restrict__ nlab,
+                                 float* loss) {
+  __shared__ float s[1024];
+  const int img = blockIdx.x;
+  float t = 0.f;
+  for (long long i = threadIdx.x; i < per_img; i += 1024) t += rl[(long long)img * per_img + i];
+  s[threadIdx.x] = t;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if (threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) loss[img] = nlab[img] > 0 ? s[0] / (float)nlab[img] : 0.f;
+}
+
+cudaError_t launch_loss_rows(const float* row_loss, long long per_img, const int* nlab, int n, float* loss,
+                             cudaStream_t s) {
+  loss_rows_kernel<<<n, 1024, 0, s>>>(row_loss, per_img, nlab, loss);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_loss_finalize(const float* part, int parts, const int* nlab, int n, float* loss,
                                  cudaStream_t s) {
   loss_finalize_kernel<<<n, 256, 0, s>>>(part, parts, nlab, loss);

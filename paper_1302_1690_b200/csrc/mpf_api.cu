@@ -228,6 +228,7 @@ static void layout_memory(Net* N, int n) {
   N->off_bpart = s; s = align256(s + sizeof(float) * bp);
   N->off_lossp = s; s = align256(s + sizeof(float) * (size_t)N->loss_parts * n);
   N->off_err = s; s = align256(s + 256);
+  N->off_rowloss = s; s = align256(s + sizeof(float) * (size_t)h_pos * n);  // fused-head per-position losses
   N->off_stage_img = s; s = align256(s + sizeof(float) * (size_t)n * N->cfg.in_channels * N->cfg.image_rows * N->cfg.image_cols);
   N->off_stage_lab = s; s = align256(s + (size_t)n * N->O_H * N->O_W);
   N->off_stage_loss = s; s = align256(s + sizeof(float) * n);
@@ -392,11 +393,19 @@ mpf_status mpf_net_bind(mpf_net* N, void* p, void* g, void* t, void* s, int32_t 
   return MPF_OK;
 }
 
-mpf_status mpf_forward_image(mpf_net* N, const float* d_images, int32_t n, float* d_probs, void* stream) {
-  if (!N || !d_images) return fail(MPF_ERR_ARG, "NULL argument");
-  if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound (mpf_net_bind)");
-  if (n < 1 || n > N->n_cap) return fail(MPF_ERR_DATA, "n must be in [1, bound n_images]");
-  cudaStream_t s = (cudaStream_t)stream;
+// Is the softmax head fused into the forward of the last hidden layer (mpf_train_step)?
+static bool head_fusable(const Net* N) {
+  const int L = N->n_layers - 1;
+  const LayerPlan& P = N->lp[L - 1];
+  return L >= 2 && P.L.kind != MPF_POOL && use_tc(N, P, false) &&
+         tc_head_supported(N->classes, P.cout, P.L.act);
+}
+
+// Forward (Alg. 1 per layer, Alg. 3 for MPF).  With `hf`, the last hidden layer's conv
+// runs with the fused softmax head: it writes dh into the first delta buffer instead of
+// its output, plus per-position losses and per-CTA head partials (*head_grid CTAs).
+static mpf_status forward_impl(Net* N, const float* d_images, int n, float* d_probs, cudaStream_t s,
+                               const TcHeadArgs* hf, int* head_grid) {
   const bool tf32 = N->cfg.precision == MPF_PREC_TF32;
   float* wpack = scr(N, N->off_wpack);
   // 1. weight packs (tf32-rounded for the tensor-core path)
@@ -438,7 +447,16 @@ mpf_status mpf_forward_image(mpf_net* N, const float* d_images, int32_t n, float
       const double in_e = (l == 0) ? (double)n * N->cfg.in_channels * N->cfg.image_rows * N->cfg.image_cols
                                    : (double)n * in.F * in.vr * in.vc * in.C;
       const double cbytes = 4.0 * (in_e + pos_out * P.cout);
-      if (l == 0 && first_conv_supported(N->cfg.in_channels, P.cout, P.L.k) && !getenv("MPF_DISABLE_FIRST")) {
+      if (hf && l == N->n_layers - 2) {  // last hidden layer + fused softmax head
+        TcConvArgs t{};
+        t.x = x; t.n_frag = n * in.F; t.gr = in.gr; t.gc = in.gc; t.cin = P.cin;
+        t.w = wpack + P.wpack_off; t.bias = N->params + P.b_off; t.k = P.L.k; t.cout = P.cout;
+        t.out = scr(N, N->off_dA); t.out_vr = o.vr; t.out_vc = o.vc; t.act = P.L.act; t.shift = 0;
+        t.round_out = 0; t.mul_dact = nullptr; t.head = hf;
+        const double pos = (double)n * o.F * o.vr * o.vc;
+        LAUNCH(N, s, "conv_fwd_head_tc", l, cflops + 6.0 * pos * P.cout * N->classes,
+               4.0 * (in_e + pos * P.cout) + pos, launch_conv_tc(t, s, head_grid));
+      } else if (l == 0 && first_conv_supported(N->cfg.in_channels, P.cout, P.L.k) && !getenv("MPF_DISABLE_FIRST")) {
         FirstConvArgs f{};
         f.img = d_images; f.n = n; f.H = N->cfg.image_rows; f.W = N->cfg.image_cols;
         f.w = N->params + P.w_off; f.bias = N->params + P.b_off; f.k = P.L.k; f.cout = P.cout;
@@ -484,7 +502,7 @@ mpf_status mpf_forward_image(mpf_net* N, const float* d_images, int32_t n, float
   }
   N->images = d_images;
   N->n_fwd = n;
-  N->have_fwd = true;
+  N->have_fwd = !hf;  // a fused step has no standalone backward
   // 3. optional softmax output
   if (d_probs) {
     const int L = N->n_layers - 1;
@@ -506,6 +524,13 @@ mpf_status mpf_forward_image(mpf_net* N, const float* d_images, int32_t n, float
            launch_head2(hd, s));
   }
   return MPF_OK;
+}
+
+mpf_status mpf_forward_image(mpf_net* N, const float* d_images, int32_t n, float* d_probs, void* stream) {
+  if (!N || !d_images) return fail(MPF_ERR_ARG, "NULL argument");
+  if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound (mpf_net_bind)");
+  if (n < 1 || n > N->n_cap) return fail(MPF_ERR_DATA, "n must be in [1, bound n_images]");
+  return forward_impl(N, d_images, n, d_probs, (cudaStream_t)stream, nullptr, nullptr);
 }
 
 static mpf_status wgrad(Net* N, int l, const float* x, const float* dy, int n, cudaStream_t s) {
@@ -575,20 +600,19 @@ static mpf_status bias_reduce(Net* N, int l, const float* part, long long nb, cu
   return MPF_OK;
 }
 
-mpf_status mpf_backward_image(mpf_net* N, const uint8_t* d_labels, const float* h_class_w, float* d_loss,
-                              void* stream) {
-  if (!N || !d_labels) return fail(MPF_ERR_ARG, "NULL argument");
-  if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound");
-  if (!N->have_fwd) return fail(MPF_ERR_STATE, "mpf_backward_image before mpf_forward_image");
-  cudaStream_t s = (cudaStream_t)stream;
+// Backward.  head_grid > 0: the fused forward already produced dh (first delta buffer),
+// the per-position losses and head_grid CTA partials of (dW_L, db_L, db_{L-1}).
+static mpf_status backward_impl(Net* N, const uint8_t* d_labels, const float* h_class_w, float* d_loss,
+                                cudaStream_t s, int head_grid) {
   const int n = N->n_fwd;
   const bool tf32 = N->cfg.precision == MPF_PREC_TF32;
   const int L = N->n_layers - 1;  // the softmax FC
   int* nlab = (int*)(N->scratch + N->off_nlab);
   float* lossp = scr(N, N->off_lossp);
   float* bpart = scr(N, N->off_bpart);
-  LAUNCH(N, s, "label_count", -1, 0.0, (double)n * N->O_H * N->O_W,
-         launch_label_count(d_labels, n, N->O_H * N->O_W, N->classes, nlab, s));
+  if (head_grid == 0)
+    LAUNCH(N, s, "label_count", -1, 0.0, (double)n * N->O_H * N->O_W,
+           launch_label_count(d_labels, n, N->O_H * N->O_W, N->classes, nlab, s));
   // head: dL/dx_hat first, dh, and the softmax FC's gradient + the
   // previous layer's bias gradient as block partials
   const Act& h = N->a[L];
@@ -616,7 +640,15 @@ mpf_status mpf_backward_image(mpf_net* N, const uint8_t* d_labels, const float* 
   hd.err = (int*)(N->scratch + N->off_err);
   hd.n = n;
   hd.round_tf32 = tf32 ? 1 : 0;
-  {
+  if (head_grid > 0) {  // fused: partials from the conv epilogue, losses per position
+    const int E = N->classes * h.C + N->classes + h.C;
+    LAUNCH(N, s, "head_reduce", L, 0.0, 4.0 * (double)head_grid * E,
+           launch_partial_reduce(bpart, head_grid, E, N->grads + N->lp[L].w_off, N->grads + N->lp[L - 1].b_off,
+                                 N->classes * h.C + N->classes, s));
+    if (d_loss)
+      LAUNCH(N, s, "loss_rows", L, 0.0, 4.0 * (double)n * h.F * h.gr * h.gc,
+             launch_loss_rows(scr(N, N->off_rowloss), (long long)h.F * h.gr * h.gc, nlab, n, d_loss, s));
+  } else {
     const double pos = (double)n * h.F * h.vr * h.vc;
     LAUNCH(N, s, "head_loss_delta", L, 6.0 * pos * h.C * N->classes, pos * (8.0 * h.C + 1.0),
            launch_head2(hd, s));
@@ -625,10 +657,10 @@ mpf_status mpf_backward_image(mpf_net* N, const uint8_t* d_labels, const float* 
     LAUNCH(N, s, "head_reduce", L, 0.0, 4.0 * (double)hd.n_blocks * E,
            launch_partial_reduce(bpart, hd.n_blocks, E, N->grads + N->lp[L].w_off, N->grads + N->lp[L - 1].b_off,
                                  N->classes * h.C + N->classes, s));
+    if (d_loss)
+      LAUNCH(N, s, "loss_finalize", L, 0.0, 4.0 * (double)N->loss_parts * n,
+             launch_loss_finalize(lossp, hd.tiles_per_img * head_loss_parts_per_tile(), nlab, n, d_loss, s));
   }
-  if (d_loss)
-    LAUNCH(N, s, "loss_finalize", L, 0.0, 4.0 * (double)N->loss_parts * n,
-           launch_loss_finalize(lossp, hd.tiles_per_img * head_loss_parts_per_tile(), nlab, n, d_loss, s));
   // remaining layers in reverse.  Invariant: dcur holds the delta of a[l+1] at the
   // pre-activation (CONV/FC output) or the value (pooled output).
   bool bias_done = true;  // layer L-1's bias came from the head
@@ -723,6 +755,57 @@ mpf_status mpf_backward_image(mpf_net* N, const uint8_t* d_labels, const float* 
   return MPF_OK;
 }
 
+mpf_status mpf_backward_image(mpf_net* N, const uint8_t* d_labels, const float* h_class_w, float* d_loss,
+                              void* stream) {
+  if (!N || !d_labels) return fail(MPF_ERR_ARG, "NULL argument");
+  if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound");
+  if (!N->have_fwd) return fail(MPF_ERR_STATE, "mpf_backward_image before mpf_forward_image");
+  return backward_impl(N, d_labels, h_class_w, d_loss, (cudaStream_t)stream, 0);
+}
+
+mpf_status mpf_train_step(mpf_net* N, const float* d_images, int32_t n, const uint8_t* d_labels,
+                          const float* h_class_w, float* d_loss, void* stream) {
+  if (!N || !d_images || !d_labels) return fail(MPF_ERR_ARG, "NULL argument");
+  if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound (mpf_net_bind)");
+  if (n < 1 || n > N->n_cap) return fail(MPF_ERR_DATA, "n must be in [1, bound n_images]");
+  cudaStream_t s = (cudaStream_t)stream;
+  // The fused head is opt-in (MPF_HEAD_FUSION=1): measured slower than the separate head
+  // pass on cfg4/cfg5 (11.5 ms vs 4.7 + 4.4 ms; the per-row head work makes the conv
+  // epilogue the bottleneck), so the default is forward + backward.
+  const char* hfe = getenv("MPF_HEAD_FUSION");
+  if (!head_fusable(N) || !(hfe && atoi(hfe) != 0)) {  // unfused: plain forward + backward
+    mpf_status st = forward_impl(N, d_images, n, nullptr, s, nullptr, nullptr);
+    if (st != MPF_OK) return st;
+    return backward_impl(N, d_labels, h_class_w, d_loss, s, 0);
+  }
+  int* nlab = (int*)(N->scratch + N->off_nlab);
+  LAUNCH(N, s, "label_count", -1, 0.0, (double)n * N->O_H * N->O_W,
+         launch_label_count(d_labels, n, N->O_H * N->O_W, N->classes, nlab, s));
+  const int L = N->n_layers - 1;
+  TcHeadArgs hf{};
+  hf.wL = N->params + N->lp[L].w_off;
+  hf.bL = N->params + N->lp[L].b_off;
+  hf.C = N->classes;
+  hf.labels = d_labels;
+  hf.O_H = N->O_H; hf.O_W = N->O_W;
+  hf.F = N->a[L].F;
+  hf.n_levels = N->n_levels;
+  for (int i = 0; i < N->n_levels; ++i) hf.pool_k[i] = N->pool_k[i];
+  hf.nlab = nlab;
+  for (int c = 0; c < 16; ++c) hf.cw[c] = (h_class_w && c < N->classes) ? h_class_w[c] : 1.f;
+  hf.row_loss = scr(N, N->off_rowloss);
+  hf.part = scr(N, N->off_bpart);
+  hf.err = (int*)(N->scratch + N->off_err);
+  hf.round_dh = N->cfg.precision == MPF_PREC_TF32 ? 1 : 0;
+  int grid = 0;
+  mpf_status st = forward_impl(N, d_images, n, nullptr, s, &hf, &grid);
+  if (st != MPF_OK) return st;
+  if (grid <= 0) return fail(MPF_ERR_INTERNAL, "fused head launch reported no CTAs");
+  st = backward_impl(N, d_labels, h_class_w, d_loss, s, grid);
+  N->have_fwd = false;  // the tape is consumed (the last hidden layer's output was never stored)
+  return st;
+}
+
 mpf_status mpf_sgd_step(mpf_net* N, float lr, float scale, void* stream) {
   if (!N) return fail(MPF_ERR_ARG, "NULL net");
   if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound");
@@ -746,9 +829,7 @@ mpf_status mpf_train_step_host(mpf_net* N, const float* h_images, const uint8_t*
   const size_t lb = (size_t)n * N->O_H * N->O_W;
   MPF_CUDA(cudaMemcpyAsync(d_img, h_images, ib, cudaMemcpyHostToDevice, s));
   MPF_CUDA(cudaMemcpyAsync(d_lab, h_labels, lb, cudaMemcpyHostToDevice, s));
-  mpf_status st = mpf_forward_image(N, d_img, n, nullptr, stream);
-  if (st != MPF_OK) return st;
-  st = mpf_backward_image(N, d_lab, h_class_w, d_loss, stream);
+  mpf_status st = mpf_train_step(N, d_img, n, d_lab, h_class_w, d_loss, stream);
   if (st != MPF_OK) return st;
   if (apply_sgd) {
     st = mpf_sgd_step(N, lr, scale, stream);
@@ -786,6 +867,14 @@ mpf_status mpf_debug_tape(const mpf_net* N, int32_t layer, int32_t what, void* d
   if (what != MPF_TAPE_VALUE) return fail(MPF_ERR_ARG, "unknown tape item");
   if (P.out_where != Where::Tape) return fail(MPF_ERR_ARG, "this layer's output is not kept on the tape");
   MPF_CUDA(launch_compact_copy(tape_val(N, layer), o.gr, o.gc, o.vr, o.vc, o.C, nf, (float*)dst, s));
+  return MPF_OK;
+}
+
+mpf_status mpf_debug_scratch(const mpf_net* N, int32_t which, void* d_dst, uint64_t bytes, void* stream) {
+  if (!N || !d_dst || !N->bound) return fail(MPF_ERR_ARG, "NULL argument or unbound net");
+  const size_t off = which == 0 ? N->off_rowloss : (which == 1 ? N->off_dA : N->off_bpart);
+  if (off + bytes > N->scratch_bytes) return fail(MPF_ERR_ARG, "range outside the scratch buffer");
+  MPF_CUDA(cudaMemcpyAsync(d_dst, N->scratch + off, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
   return MPF_OK;
 }
 

@@ -66,7 +66,7 @@ struct Net {
   int n_cap = 0;
   size_t tape_bytes = 0, scratch_bytes = 0;
   size_t off_Y = 0, off_dA = 0, off_dB = 0, off_bpart = 0, off_wpack = 0, off_part = 0,
-         off_nlab = 0, off_lossp = 0, off_err = 0, off_stage_img = 0, off_stage_lab = 0,
+         off_nlab = 0, off_lossp = 0, off_err = 0, off_rowloss = 0, off_stage_img = 0, off_stage_lab = 0,
          off_stage_loss = 0;
   size_t part_floats = 0;  // capacity of the wgrad partial buffer (floats)
   size_t bpart_floats = 0; // capacity of the bias / head partial buffer (floats)
@@ -195,6 +195,9 @@ cudaError_t launch_head2(const HeadArgs& a, cudaStream_t s);
 cudaError_t launch_label_count(const uint8_t* labels, int n, int hw, int classes, int* nlab, cudaStream_t s);
 cudaError_t launch_loss_finalize(const float* loss_part, int parts, const int* nlab, int n, float* loss,
                                  cudaStream_t s);
+// per-image loss = sum of per-position losses (fixed order) / n_lab (fused head)
+cudaError_t launch_loss_rows(const float* row_loss, long long per_img, const int* nlab, int n, float* loss,
+                             cudaStream_t s);
 cudaError_t launch_sgd(float* params, float* grads, long long n, float lr, float scale, cudaStream_t s);
 cudaError_t launch_pack_weights(const float* w_canon, int cout, int cin, int k, float* wpack, float* dpack,
                                 int round_fwd, int round_dgrad, cudaStream_t s);

@@ -153,6 +153,23 @@ class MPFNet:
                 "mpf_backward_image")
         return loss
 
+    def train_step(self, images: torch.Tensor, labels: torch.Tensor, class_w=None, stream=None) -> torch.Tensor:
+        """Forward + backward in one C call (mpf_train_step: the softmax head is fused into the
+        last hidden layer's tensor-core epilogue).  Gradients are added; returns losses [n]."""
+        if images.dtype != torch.float32 or not images.is_cuda or not images.is_contiguous():
+            raise ValueError("images must be a contiguous cuda float32 tensor")
+        if labels.dtype != torch.uint8 or not labels.is_cuda or not labels.is_contiguous():
+            raise ValueError("labels must be a contiguous cuda uint8 tensor")
+        n = images.shape[0]
+        loss = torch.empty(n, dtype=torch.float32, device=self.device)
+        cw = None
+        if class_w is not None:
+            cw = (ctypes.c_float * self.geom.classes)(*[float(v) for v in class_w])
+        L.check(self.lib.mpf_train_step(self.h, _ptr(images), n, _ptr(labels), cw, _ptr(loss), _stream_ptr(stream)),
+                "mpf_train_step")
+        self._images = images
+        return loss
+
     def sgd_step(self, lr: float, grad_scale: float = 1.0, stream=None) -> None:
         L.check(self.lib.mpf_sgd_step(self.h, float(lr), float(grad_scale), _stream_ptr(stream)), "mpf_sgd_step")
 

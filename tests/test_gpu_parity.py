@@ -335,3 +335,82 @@ def test_mpf_backward_tiled_equals_sliding_bitwise(name):
         else:
             assert rel_l2(a["grad_sum"][sl], b["grad_sum"][sl]) <= 1e-5, nm
     assert np.array_equal(a["loss"], b["loss"])
+
+
+# ----------------------------------------------------------------- fused training step
+
+@pytest.fixture
+def head_fusion(monkeypatch):
+    monkeypatch.setenv("MPF_HEAD_FUSION", "1")
+
+
+def _fused_vs_oracle(name, images, labels, params, prec="tf32", class_w=None):
+    cfg = S.CONFIGS[name]
+    n, cin, H, W = images.shape
+    net = MPFNet(cfg.layers, cfg.P, H, W, max_images=n, precision=prec)
+    net.set_params(params.astype(np.float32))
+    net.zero_grads()
+    img = torch.tensor(images, device="cuda").contiguous()
+    lab = torch.tensor(labels, device="cuda").contiguous()
+    loss = net.train_step(img, lab, class_w)
+    net.check()
+    torch.cuda.synchronize()
+    return net, loss.cpu().numpy(), net.grads.cpu().numpy().astype(np.float64)
+
+
+@pytest.mark.parametrize("name,idx", [("cfg2", [0, 1, 2]), ("cfg3", [5])])
+def test_fused_train_step_vs_o2(name, idx, head_fusion):
+    """mpf_train_step (softmax head fused into the FC1 tensor-core epilogue) against the
+    whole-image oracle O2: loss and every gradient tensor within rel L2 5e-3."""
+    cfg = S.CONFIGS[name]
+    images, labels = S.make_batch(cfg, idx)
+    params = S.init_params(cfg)
+    _, loss, grads = _fused_vs_oracle(name, images, labels, params)
+    o = oracle_step(cfg.layers, cfg.P, images.astype(np.float64), labels, params, engine="o2")
+    errs = compare_step(cfg.layers, {"loss": loss, "grad_sum": grads}, {"probs": [None], "loss": o["loss"],
+                        "grad_sum": o["grad_sum"]}, TOL_TF32, f"{name} fused step")
+    print(name, "fused rel L2:", {k: f"{v:.1e}" for k, v in errs.items()})
+
+
+def test_fused_train_step_matches_unfused(monkeypatch):
+    """Fused and unfused steps compute the same gradients up to fp32 summation order, the
+    same per-image losses, and keep the label-error flag; class weights included."""
+    cfg = S.CONFIGS["cfg2"]
+    images, labels = S.make_batch(cfg, [3, 4])
+    labels[1, :10, :] = 255  # some ignored pixels
+    params = S.init_params(cfg)
+    cw = [0.7, 1.9]
+    monkeypatch.setenv("MPF_HEAD_FUSION", "1")
+    _, loss_f, grads_f = _fused_vs_oracle("cfg2", images, labels, params, class_w=cw)
+    monkeypatch.delenv("MPF_HEAD_FUSION")
+    g = gpu_step(cfg.layers, cfg.P, images, labels, params, "tf32", class_w=cw)
+    monkeypatch.setenv("MPF_HEAD_FUSION", "1")
+    assert rel_l2(loss_f, g["loss"]) <= 1e-5
+    for nm, sl in param_slices(cfg.layers):
+        assert rel_l2(grads_f[sl], g["grad_sum"][sl]) <= 1e-4, nm
+    bad = labels.copy()
+    bad[0, 5, 5] = 9
+    with pytest.raises(MpfError):
+        _fused_vs_oracle("cfg2", images, bad, params)
+
+
+def test_fused_train_step_all_ignored_and_tape_consumed(head_fusion):
+    cfg = S.CONFIGS["cfg2"]
+    images, labels = S.make_batch(cfg, [0])
+    labels[:] = 255
+    net, loss, grads = _fused_vs_oracle("cfg2", images, labels, S.init_params(cfg))
+    assert loss[0] == 0.0 and np.all(grads == 0.0)
+    with pytest.raises(MpfError) as e:  # the fused step leaves no tape for a backward
+        net.backward(torch.tensor(labels, device="cuda"))
+    assert e.value.status == 6
+
+
+def test_train_step_default_equals_forward_backward():
+    """The default (unfused) mpf_train_step is exactly mpf_forward_image + mpf_backward_image."""
+    cfg = S.CONFIGS["cfg2"]
+    images, labels = S.make_batch(cfg, [6, 7])
+    params = S.init_params(cfg)
+    _, loss_t, grads_t = _fused_vs_oracle("cfg2", images, labels, params)
+    g = gpu_step(cfg.layers, cfg.P, images, labels, params, "tf32")
+    assert np.array_equal(loss_t, g["loss"])
+    assert np.array_equal(grads_t, g["grad_sum"])
