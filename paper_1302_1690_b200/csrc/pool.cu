@@ -22,6 +22,7 @@
 // All index arithmetic is 32-bit per fragment; only final offsets are 64-bit.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "mpf_internal.h"
@@ -423,9 +424,7 @@ __global__ void __launch_bounds__(256) mpf_bwd_slide_kernel(MpfBwdArgs a) {
 // every element gathers its K^2 candidates from shared memory in the same fixed (dy, dx)
 // order as the other MPF backward kernels (bitwise-identical results).  No dependent
 // global-load chains remain; the halo re-reads hit L2.
-constexpr int kTBY = 8, kTBX = 8;
-
-template <int K>
+template <int K, int kTBY, int kTBX>
 __global__ void __launch_bounds__(256) mpf_bwd_tile_kernel(MpfBwdArgs a, int rows_per_cta) {
   extern __shared__ __align__(16) uint8_t sm_raw[];
   constexpr int WY = kTBY + K - 1, WX = kTBX + K - 1;
@@ -445,19 +444,25 @@ __global__ void __launch_bounds__(256) mpf_bwd_tile_kernel(MpfBwdArgs a, int row
     for (int Y0 = ybeg; Y0 < yend; Y0 += kTBY) {
       __syncthreads();  // previous tile's shared data fully consumed
       // ---- stage windows wy in [Y0-K+1, Y0+kTBY), wx in [X0-K+1, X0+kTBX)
+      // cp.async: global -> shared without a register round trip, so every thread keeps
+      // all of its staging loads in flight; absent windows read as idx 0xFF.., delta 0
       for (int e = tid; e < WY * WX * CV; e += 256) {
         const int c4 = e % CV, t = e / CV, wxl = t % WX, wyl = t / WX;
         const int wy = Y0 - K + 1 + wyl, wx = X0 - K + 1 + wxl;
-        uint32_t idv = 0xFFFFFFFFu;
-        float4 dv = make_float4(0.f, 0.f, 0.f, 0.f);
         if (wy >= 0 && wy < Yw && wx >= 0 && wx < Xw) {
           const size_t cell = (fbase + (size_t)((wy % K) * K + (wx % K)) * MM + (wy / K) * a.m_c + wx / K) * C + c4 * 4;
-          idv = __ldg(reinterpret_cast<const uint32_t*>(a.idx + cell));
-          dv = __ldg(reinterpret_cast<const float4*>(a.dout + cell));
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(s_id + e)),
+                       "l"(a.idx + cell)
+                       : "memory");
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(s_d + e)),
+                       "l"(a.dout + cell)
+                       : "memory");
+        } else {
+          s_id[e] = 0xFFFFFFFFu;
+          s_d[e] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        s_id[e] = idv;
-        s_d[e] = dv;
       }
+      asm volatile("cp.async.wait_all;" ::: "memory");
       __syncthreads();
       // ---- gather: element (Y0+ty, X0+tx) sums window (ty+K-1-dy, tx+K-1-dx) where idx == dy*K+dx
       if (pt < npt) {
@@ -571,16 +576,62 @@ static bool bwd_tile(const MpfBwdArgs& a) {
 static bool bwd_slide(const MpfBwdArgs& a) { return a.C % 4 == 0 && a.k >= 2 && a.k <= 4; }
 constexpr int kTileRows = 64;  // conv-output rows per CTA of the tiled kernel (partials per CTA)
 
+// tile shape (rows x cols of conv-output positions per CTA step); MPF_BWD_TILE=RxC overrides
+static size_t tile_bytes(int C, int k, int ty, int tx) {
+  const int CV = C / 4, WY = ty + k - 1, WX = tx + k - 1;
+  return ((size_t)WY * WX * CV * 4 + 15) / 16 * 16 + (size_t)WY * WX * CV * 16 + sizeof(float) * (256 / CV) * C;
+}
+
+// Largest tile whose staging fits ~56 KB (4 CTAs per SM): measured best per layer on
+// cfg4/cfg5 (A/B over 8x8 .. 16x16).
+static void tile_shape(const MpfBwdArgs& a, int* ty, int* tx) {
+  *ty = 8;
+  *tx = 8;
+  const int cand[3][2] = {{16, 16}, {8, 16}, {8, 8}};
+  for (int i = 0; i < 3; ++i)
+    if (tile_bytes(a.C, a.k, cand[i][0], cand[i][1]) <= 56 * 1024) {
+      *ty = cand[i][0];
+      *tx = cand[i][1];
+      break;
+    }
+  if (const char* e = getenv("MPF_BWD_TILE")) {
+    int r = 8, c = 8;
+    if (sscanf(e, "%dx%d", &r, &c) == 2 && (r == 8 || r == 16) && (c == 8 || c == 16)) { *ty = r; *tx = c; }
+  }
+}
+
 static size_t tile_smem(const MpfBwdArgs& a) {
-  const int CV = a.C / 4, WY = kTBY + a.k - 1, WX = kTBX + a.k - 1;
-  return ((size_t)WY * WX * CV * 4 + 15) / 16 * 16 + (size_t)WY * WX * CV * 16 + sizeof(float) * (256 / CV) * a.C;
+  int ty, tx;
+  tile_shape(a, &ty, &tx);
+  return tile_bytes(a.C, a.k, ty, tx);
+}
+
+template <int K>
+static cudaError_t launch_tile_k(const MpfBwdArgs& a, dim3 grid, dim3 blk, size_t sm, cudaStream_t s) {
+  int ty, tx;
+  tile_shape(a, &ty, &tx);
+  cudaError_t e = cudaSuccess;
+#define MPF_TILE_CASE(TY, TX)                                                                                   \
+  if (ty == TY && tx == TX) {                                                                                   \
+    e = cudaFuncSetAttribute(mpf_bwd_tile_kernel<K, TY, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    if (e != cudaSuccess) return e;                                                                             \
+    mpf_bwd_tile_kernel<K, TY, TX><<<grid, blk, sm, s>>>(a, kTileRows);                                          \
+    return cudaGetLastError();                                                                                  \
+  }
+  MPF_TILE_CASE(8, 8)
+  MPF_TILE_CASE(8, 16)
+  MPF_TILE_CASE(16, 8)
+  MPF_TILE_CASE(16, 16)
+#undef MPF_TILE_CASE
+  return cudaErrorInvalidValue;
 }
 
 static void bwd_geometry(const MpfBwdArgs& a, int V, dim3* grid, dim3* blk) {
   if (bwd_tile(a)) {
+    int ty, tx;
+    tile_shape(a, &ty, &tx);
     *blk = dim3(256, 1, 1);
-    *grid = dim3((a.gc + kTBX - 1) / kTBX, (a.gr + kTileRows - 1) / kTileRows,
-                 a.n_frag_in < 65535 ? a.n_frag_in : 65535);
+    *grid = dim3((a.gc + tx - 1) / tx, (a.gr + kTileRows - 1) / kTileRows, a.n_frag_in < 65535 ? a.n_frag_in : 65535);
     return;
   }
   const int ty = block_dims(a.C, V, blk);
@@ -600,19 +651,9 @@ cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s) {
   bwd_geometry(a, V, &grid, &blk);
   if (bwd_tile(a)) {
     const size_t sm = tile_smem(a);
-    cudaError_t e = cudaSuccess;
-    if (a.k == 2) {
-      e = cudaFuncSetAttribute(mpf_bwd_tile_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      mpf_bwd_tile_kernel<2><<<grid, blk, sm, s>>>(a, kTileRows);
-    } else if (a.k == 3) {
-      e = cudaFuncSetAttribute(mpf_bwd_tile_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      mpf_bwd_tile_kernel<3><<<grid, blk, sm, s>>>(a, kTileRows);
-    } else {
-      e = cudaFuncSetAttribute(mpf_bwd_tile_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      mpf_bwd_tile_kernel<4><<<grid, blk, sm, s>>>(a, kTileRows);
-    }
-    if (e != cudaSuccess) return e;
-    return cudaGetLastError();
+    if (a.k == 2) return launch_tile_k<2>(a, grid, blk, sm, s);
+    if (a.k == 3) return launch_tile_k<3>(a, grid, blk, sm, s);
+    return launch_tile_k<4>(a, grid, blk, sm, s);
   }
   const size_t smem = sizeof(float) * blk.y * a.C;
   if (bwd_slide(a) && !getenv("MPF_BWD_GENERIC")) {
