@@ -49,6 +49,8 @@ __device__ __forceinline__ float act_der(int act, float y) {
   return 1.f;
 }
 
+__device__ __forceinline__ void named_bar_h(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
 // bytes of region0: two h tiles, or the end-of-kernel reduction area if larger
 __host__ __device__ inline size_t head_region0(int C, int Ch) {
   const int nw = kThr / 32;
@@ -107,7 +109,11 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
   const int M = Ch >> 2;  // channels per lane in phase A (Ch % 4 == 0 path)
   const int rot = pa % (M > 0 ? M : 1);
   constexpr int kMC = 8;  // channel slots per lane in phase B (Ch <= 256)
-  constexpr int kMG = 2;  // float4 channel groups per lane in phase B (VEC; Ch <= 256)
+  // VEC phase B: one float4 channel group per lane.  Ch > 128 (more than 32 groups): the
+  // warps pair up — both warps of a pair walk the pair's 16 positions, warp w & 1 taking
+  // channel groups 32 (w & 1) + lane (keeps the accumulators in registers).
+  constexpr int kMG = 1;
+  const bool pairB = VEC && Ch > 128;
   float accW[VEC ? 1 : kMC][NC], accP[VEC ? 1 : kMC], accL[NC];
   float accW4[VEC ? kMG : 1][NC][4], accP4[VEC ? kMG : 1][4];
 #pragma unroll
@@ -278,29 +284,37 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
       __syncwarp();
       // -------------------------------------------------------------- phase B
       float* dh_img = a.dh + ((long long)img * per_img + p0) * Ch;
-      for (int q = 0; q < 8; ++q) {
-        const int p = pw0 + q;
+      if (pairB) named_bar_h(1 + (warp >> 1), 64);  // the partner warp's dz rows are in s_dl
+      const int pb0 = pairB ? (warp & ~1) * 8 : pw0;
+      const int npb = pairB ? 16 : 8;
+      const int gB = VEC ? lane + (pairB ? 32 * (warp & 1) : 0) : 0;  // this lane's float4 group
+      for (int q = 0; q < npb; ++q) {
+        const int p = pb0 + q;
         const int lab = s_lab[p];  // warp-uniform
         if (lab == kLabBeyond) break;  // past the end of the image (and so are the rest)
         const bool act = lab >= 0 && lab < C;
         float dl[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c) dl[c] = act ? s_dl[p * NC + c] : 0.f;
-        if (act && lane == 0) {
+        if (act && lane == 0 && !(pairB && (warp & 1))) {
 #pragma unroll
           for (int c = 0; c < NC; ++c) accL[c] += dl[c];
         }
         float* dh_row = dh_img + (long long)p * Ch;
         if (!act) {  // warp-uniform: padding position or ignored label -> zero delta
+          if (VEC) {
+            if (4 * gB < Ch) reinterpret_cast<float4*>(dh_row)[gB] = make_float4(0.f, 0.f, 0.f, 0.f);
+          } else {
 #pragma unroll
-          for (int m = 0; m < kMC; ++m)
-            if (lane + 32 * m < Ch) dh_row[lane + 32 * m] = 0.f;
+            for (int m = 0; m < kMC; ++m)
+              if (lane + 32 * m < Ch) dh_row[lane + 32 * m] = 0.f;
+          }
           continue;
         }
         if constexpr (VEC) {
 #pragma unroll
           for (int m = 0; m < kMG; ++m) {
-            const int g = lane + 32 * m;
+            const int g = gB;
             if (4 * g < Ch) {
               const float4 hv = reinterpret_cast<const float4*>(hs + p * Ch)[g];
               const float hh[4] = {hv.x, hv.y, hv.z, hv.w};
@@ -356,7 +370,7 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
   if constexpr (VEC) {
 #pragma unroll
     for (int m = 0; m < kMG; ++m) {
-      const int g = lane + 32 * m;
+      const int g = lane + (pairB ? 32 * (warp & 1) : 0);
       if (4 * g < Ch) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -390,15 +404,22 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
   float* out = a.part + (size_t)blockIdx.x * E;
   for (int e = tid; e < E; e += kThr) {
     float s = 0.f;
+    // with paired warps, channel group g was accumulated only by the warps w with
+    // (w & 1) == g / 32, and db_L only by even warps
     if (e < C * Ch) {
       const int c = e / Ch, ch = e % Ch;
-      for (int q = 0; q < kThr / 32; ++q) s += red[(q * Ch + ch) * RW + c];
+      const int own = pairB ? (ch / 4) / 32 : -1;
+      for (int q = 0; q < kThr / 32; ++q)
+        if (own < 0 || (q & 1) == own) s += red[(q * Ch + ch) * RW + c];
     } else if (e < C * Ch + C) {
       const int c = e - C * Ch;
-      for (int q = 0; q < kThr / 32; ++q) s += redL[q * kMaxC + c];
+      for (int q = 0; q < kThr / 32; ++q)
+        if (!pairB || (q & 1) == 0) s += redL[q * kMaxC + c];
     } else {
       const int ch = e - C * Ch - C;
-      for (int q = 0; q < kThr / 32; ++q) s += red[(q * Ch + ch) * RW + C];
+      const int own = pairB ? (ch / 4) / 32 : -1;
+      for (int q = 0; q < kThr / 32; ++q)
+        if (own < 0 || (q & 1) == own) s += red[(q * Ch + ch) * RW + C];
     }
     out[e] = s;
   }
