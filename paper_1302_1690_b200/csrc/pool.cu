@@ -93,7 +93,7 @@ int block_dims(int C, int V, dim3* blk) {
 
 // ----------------------------------------------------------------------------- forward
 template <int K, int V>
-__global__ void __launch_bounds__(256) mpf_fwd_kernel(MpfArgs a) {
+__global__ void __launch_bounds__(256, K <= 3 ? 4 : 2) mpf_fwd_kernel(MpfArgs a) {
   const int cv = threadIdx.x;
   const int X = blockIdx.x * blockDim.y + threadIdx.y;
   const int Xw = K * a.m_c, Yw = K * a.m_r;
@@ -104,32 +104,44 @@ __global__ void __launch_bounds__(256) mpf_fwd_kernel(MpfArgs a) {
   const int C = a.C;
   for (int g = blockIdx.z; g < a.n_frag_in; g += gridDim.z) {
     const float* src = a.y + ((size_t)g * a.gr * a.gc + X) * C + cv * V;
-    // horizontal max of row r over dx = 0..K-1 (first maximum)
-    auto hrow = [&](int r, float (&hv)[V], uint8_t (&ha)[V]) {
+    // raw loads of row r, issued two window rows ahead of their use (ring of two row
+    // buffers) so that two rows of loads are in flight per thread: the loop is
+    // load-latency-bound otherwise
+    auto lrow = [&](int r, Vec<V> (&q)[K]) {
       const float* p = src + (size_t)r * a.gc * C;
-      Vec<V> q = ldv<V>(p);
 #pragma unroll
-      for (int v = 0; v < V; ++v) { hv[v] = q.v[v]; ha[v] = 0; }
-#pragma unroll
-      for (int dx = 1; dx < K; ++dx) {
-        q = ldv<V>(p + dx * C);
-#pragma unroll
-        for (int v = 0; v < V; ++v)
-          if (q.v[v] > hv[v]) { hv[v] = q.v[v]; ha[v] = (uint8_t)dx; }
-      }
+      for (int dx = 0; dx < K; ++dx) q[dx] = ldv<V>(p + dx * C);
     };
     float hm[K][V];
     uint8_t ha[K][V];
+    // horizontal max of a loaded row over dx = 0..K-1 (first maximum) into hm/ha[d]
+    auto hrow = [&](const Vec<V> (&q)[K], int d) {
 #pragma unroll
-    for (int d = 1; d < K; ++d) hrow(y0 + d - 1, hm[d], ha[d]);
+      for (int v = 0; v < V; ++v) { hm[d][v] = q[0].v[v]; ha[d][v] = 0; }
+#pragma unroll
+      for (int dx = 1; dx < K; ++dx)
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+          if (q[dx].v[v] > hm[d][v]) { hm[d][v] = q[dx].v[v]; ha[d][v] = (uint8_t)dx; }
+    };
+    Vec<V> rawA[K], rawB[K];
+#pragma unroll
+    for (int d = 1; d < K; ++d) {
+      lrow(y0 + d - 1, rawA);
+      hrow(rawA, d);
+    }
+    lrow(y0 + K - 1, rawA);
+    if (y0 + 1 < y1) lrow(y0 + K, rawB);
     const size_t frag_base = (size_t)g * K * K;
-    for (int Y = y0; Y < y1; ++Y) {
+    // one output row: consume `cur` (window row Y+K-1), refill it with row Y+K+1
+    auto step = [&](int Y, Vec<V> (&cur)[K]) {
 #pragma unroll
       for (int d = 0; d < K - 1; ++d) {
 #pragma unroll
         for (int v = 0; v < V; ++v) { hm[d][v] = hm[d + 1][v]; ha[d][v] = ha[d + 1][v]; }
       }
-      hrow(Y + K - 1, hm[K - 1], ha[K - 1]);
+      hrow(cur, K - 1);
+      if (Y + 2 < y1) lrow(Y + K + 1, cur);
       float best[V];
       uint8_t arg[V];
 #pragma unroll
@@ -147,6 +159,10 @@ __global__ void __launch_bounds__(256) mpf_fwd_kernel(MpfArgs a) {
       }
       stv<V>(a.out + o, best);
       stidx<V>(a.idx + o, arg);
+    };
+    for (int Y = y0; Y < y1; Y += 2) {
+      step(Y, rawA);
+      if (Y + 1 < y1) step(Y + 1, rawB);
     }
   }
 }
@@ -424,14 +440,22 @@ __global__ void __launch_bounds__(256) mpf_bwd_slide_kernel(MpfBwdArgs a) {
 // every element gathers its K^2 candidates from shared memory in the same fixed (dy, dx)
 // order as the other MPF backward kernels (bitwise-identical results).  No dependent
 // global-load chains remain; the halo re-reads hit L2.
+// Shared-memory layout, channel-vector-major so that every candidate window of an element
+// sits at a compile-time offset from the element's own cell (LDS [base + imm], no
+// per-window address arithmetic); S = cells per channel vector, odd, so that the lanes
+// of a warp (consecutive cv) hit distinct banks:
+//   argmax words  s_id[(cv / 4) * S * 4 + cell * 4 + cv % 4]   (4 cv per 16-byte chunk)
+//   deltas        s_d [cv * S + cell]                          (float4)
+__host__ __device__ constexpr int tile_cells_padded(int wy, int wx) { return (wy * wx) | 1; }
+
 template <int K, int kTBY, int kTBX>
 __global__ void __launch_bounds__(256) mpf_bwd_tile_kernel(MpfBwdArgs a, int rows_per_cta) {
   extern __shared__ __align__(16) uint8_t sm_raw[];
-  constexpr int WY = kTBY + K - 1, WX = kTBX + K - 1;
-  const int C = a.C, CV = C / 4;
-  uint32_t* s_id = reinterpret_cast<uint32_t*>(sm_raw);                   // [WY][WX][CV]
-  float4* s_d = reinterpret_cast<float4*>(sm_raw + ((size_t)WY * WX * CV * 4 + 15) / 16 * 16);  // [WY][WX][CV]
-  float* s_red = reinterpret_cast<float*>(s_d + WY * WX * CV);            // [256 / CV][C]
+  constexpr int WY = kTBY + K - 1, WX = kTBX + K - 1, S = tile_cells_padded(WY, WX);
+  const int C = a.C, CV = C / 4, CVP = (CV + 3) & ~3;
+  uint32_t* s_id = reinterpret_cast<uint32_t*>(sm_raw);                  // [CVP / 4][S][4]
+  float4* s_d = reinterpret_cast<float4*>(sm_raw + (size_t)CVP * S * 4);  // [CV][S]
+  float* s_red = reinterpret_cast<float*>(s_d + (size_t)CV * S);          // [256 / CV][C]
   const int Xw = K * a.m_c, Yw = K * a.m_r;
   const int MM = a.m_r * a.m_c;
   const int X0 = blockIdx.x * kTBX;
@@ -439,50 +463,91 @@ __global__ void __launch_bounds__(256) mpf_bwd_tile_kernel(MpfBwdArgs a, int row
   const int cv = tid % CV, pt = tid / CV, npt = 256 / CV;  // compute mapping (pt < npt)
   float bsum[4] = {0.f, 0.f, 0.f, 0.f};
   const int ybeg = blockIdx.y * rows_per_cta, yend = min(ybeg + rows_per_cta, a.gr);
+  // argmax bytes are staged in 16-byte chunks (4 channel vectors) when C allows it
+  const bool idx16 = C % 16 == 0;
+  const int CI = idx16 ? C / 16 : CV;
+  const int ci = tid % CI, pi = tid / CI, npi = 256 / CI;
+  // per-fragment strides (32-bit: one input fragment's pooled output is < 2^31 elements)
+  const int MMC = MM * C, mcC = a.m_c * C;
+  float4* const s_d_cv = s_d + cv * S;
+  uint32_t* const s_id_cv = s_id + (cv >> 2) * S * 4 + (cv & 3);
   for (int g = blockIdx.z; g < a.n_frag_in; g += gridDim.z) {
-    const size_t fbase = (size_t)g * K * K * MM;
+    const size_t fbase = (size_t)g * K * K * MM * C;
+    const float* dsrc = a.dout + fbase;
+    const uint8_t* isrc = a.idx + fbase;
+    float* const dst_g = a.din + (size_t)g * a.gr * a.gc * C + cv * 4;  // one fragment < 2^31 elements
     for (int Y0 = ybeg; Y0 < yend; Y0 += kTBY) {
       __syncthreads();  // previous tile's shared data fully consumed
       // ---- stage windows wy in [Y0-K+1, Y0+kTBY), wx in [X0-K+1, X0+kTBX)
       // cp.async: global -> shared without a register round trip, so every thread keeps
-      // all of its staging loads in flight; absent windows read as idx 0xFF.., delta 0
-      for (int e = tid; e < WY * WX * CV; e += 256) {
-        const int c4 = e % CV, t = e / CV, wxl = t % WX, wyl = t / WX;
-        const int wy = Y0 - K + 1 + wyl, wx = X0 - K + 1 + wxl;
-        if (wy >= 0 && wy < Yw && wx >= 0 && wx < Xw) {
-          const size_t cell = (fbase + (size_t)((wy % K) * K + (wx % K)) * MM + (wy / K) * a.m_c + wx / K) * C + c4 * 4;
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(s_id + e)),
-                       "l"(a.idx + cell)
-                       : "memory");
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(s_d + e)),
-                       "l"(a.dout + cell)
-                       : "memory");
-        } else {
-          s_id[e] = 0xFFFFFFFFu;
-          s_d[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+      // all of its staging loads in flight; absent windows read as idx 0xFF.., delta 0.
+      // Division-free apart from the compile-time WX and K.
+      if (pt < npt) {
+        for (int t = pt; t < WY * WX; t += npt) {
+          const int wyl = t / WX, wxl = t - wyl * WX;
+          const int wy = Y0 - K + 1 + wyl, wx = X0 - K + 1 + wxl;
+          float4* dst = s_d_cv + t;
+          if ((unsigned)wy < (unsigned)Yw && (unsigned)wx < (unsigned)Xw) {
+            const unsigned uy = wy, ux = wx;
+            const int off = (int)((uy % K) * K + ux % K) * MMC + (int)(uy / K) * mcC + (int)(ux / K) * C + cv * 4;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                         "l"(dsrc + off)
+                         : "memory");
+          } else {
+            *dst = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+      }
+      if (pi < npi) {
+        for (int t = pi; t < WY * WX; t += npi) {
+          const int wyl = t / WX, wxl = t - wyl * WX;
+          const int wy = Y0 - K + 1 + wyl, wx = X0 - K + 1 + wxl;
+          const bool in = (unsigned)wy < (unsigned)Yw && (unsigned)wx < (unsigned)Xw;
+          const unsigned uy = in ? wy : 0, ux = in ? wx : 0;
+          const int off = (int)((uy % K) * K + ux % K) * MMC + (int)(uy / K) * mcC + (int)(ux / K) * C;
+          if (idx16) {
+            uint32_t* dst = s_id + (ci * S + t) * 4;
+            if (in)
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                           "l"(isrc + off + ci * 16)
+                           : "memory");
+            else
+              *reinterpret_cast<uint4*>(dst) = make_uint4(~0u, ~0u, ~0u, ~0u);
+          } else {
+            uint32_t* dst = s_id + ((ci >> 2) * S + t) * 4 + (ci & 3);
+            if (in)
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                           "l"(isrc + off + ci * 4)
+                           : "memory");
+            else
+              *dst = ~0u;
+          }
         }
       }
       asm volatile("cp.async.wait_all;" ::: "memory");
       __syncthreads();
       // ---- gather: element (Y0+ty, X0+tx) sums window (ty+K-1-dy, tx+K-1-dx) where idx == dy*K+dx
       if (pt < npt) {
-        for (int q = pt; q < kTBY * kTBX; q += npt) {
+        for (unsigned q = pt; q < kTBY * kTBX; q += npt) {
           const int ty = q / kTBX, tx = q % kTBX;
           const int Y = Y0 + ty, X = X0 + tx;
           if (Y >= yend || X >= a.gc) continue;
+          const int cell = (ty + K - 1) * WX + (tx + K - 1);
+          const uint32_t* pid = s_id_cv + cell * 4;
+          const float4* pd = s_d_cv + cell;
           float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
           for (int dy = 0; dy < K; ++dy)
 #pragma unroll
             for (int dx = 0; dx < K; ++dx) {
-              const int w = ((ty + K - 1 - dy) * WX + (tx + K - 1 - dx)) * CV + cv;
-              const uint32_t id = s_id[w];
-              const uint32_t want = (uint32_t)(dy * K + dx);
-              const float4 d = s_d[w];
-              if (((id) & 0xFFu) == want) acc[0] += d.x;
-              if (((id >> 8) & 0xFFu) == want) acc[1] += d.y;
-              if (((id >> 16) & 0xFFu) == want) acc[2] += d.z;
-              if (((id >> 24) & 0xFFu) == want) acc[3] += d.w;
+              const int wo = dy * WX + dx;  // compile-time after unrolling
+              // byte v of `x` is zero iff channel v of this window selected (dy, dx)
+              const uint32_t x = pid[-wo * 4] ^ ((uint32_t)(dy * K + dx) * 0x01010101u);
+              const float4 d = pd[-wo];
+              if (!(x & 0xFFu)) acc[0] += d.x;
+              if (!(x & 0xFF00u)) acc[1] += d.y;
+              if (!(x & 0xFF0000u)) acc[2] += d.z;
+              if (!(x & 0xFF000000u)) acc[3] += d.w;
             }
           float o[4];
 #pragma unroll
@@ -490,7 +555,7 @@ __global__ void __launch_bounds__(256) mpf_bwd_tile_kernel(MpfBwdArgs a, int row
             bsum[v] += acc[v];
             o[v] = a.round_tf32 ? tf32_rna(acc[v]) : acc[v];
           }
-          stv<4>(a.din + (((size_t)g * a.gr + Y) * a.gc + X) * C + cv * 4, o);
+          stv<4>(dst_g + (Y * a.gc + X) * C, o);
         }
       }
     }
@@ -578,8 +643,8 @@ constexpr int kTileRows = 64;  // conv-output rows per CTA of the tiled kernel (
 
 // tile shape (rows x cols of conv-output positions per CTA step); MPF_BWD_TILE=RxC overrides
 static size_t tile_bytes(int C, int k, int ty, int tx) {
-  const int CV = C / 4, WY = ty + k - 1, WX = tx + k - 1;
-  return ((size_t)WY * WX * CV * 4 + 15) / 16 * 16 + (size_t)WY * WX * CV * 16 + sizeof(float) * (256 / CV) * C;
+  const int CV = C / 4, CVP = (CV + 3) & ~3, S = tile_cells_padded(ty + k - 1, tx + k - 1);
+  return (size_t)CVP * S * 4 + (size_t)CV * S * 16 + sizeof(float) * (256 / CV) * C;
 }
 
 // Largest tile whose staging fits ~56 KB (4 CTAs per SM): measured best per layer on
