@@ -1071,6 +1071,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
+cudaError_t make_tmap_sw128(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+  return make_map(m, base, cols, rows, box_rows);
+}
+
 bool tc_wgrad_supported(int cin, int cout, int k) {
   if (getenv("MPF_DISABLE_TC")) return false;
   return cin % 4 == 0 && cin >= 8 && cout % 4 == 0 && cout <= 256 && k >= 1 && k <= 8;

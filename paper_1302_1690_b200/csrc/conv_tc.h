@@ -1,5 +1,6 @@
 // conv_tc.h — tensor-core (tcgen05 / TMEM, kind::tf32) implicit-GEMM convolutions.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <stdint.h>
@@ -64,5 +65,7 @@ bool tc_supported(int cin, int cout, int k);
 bool tc_wgrad_supported(int cin, int cout, int k);
 cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s, int* grid_out = nullptr);
 cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits, cudaStream_t s);
+// 2-D fp32 tensor map [rows][cols] (cols contiguous), box {32 cols, box_rows}, SWIZZLE_128B
+cudaError_t make_tmap_sw128(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows);
 
 }  // namespace mpf

@@ -25,6 +25,7 @@
 #include <math.h>
 #include <stdint.h>
 
+#include "head_common.cuh"
 #include "mpf_internal.h"
 #include "tc_ptx.cuh"
 
@@ -35,7 +36,6 @@ namespace {
 constexpr int kTP = 64;  // positions per tile
 constexpr int kThr = 256;
 constexpr int kMaxC = 16;
-constexpr int kLabBeyond = -1, kLabPad = -2;
 
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
@@ -73,8 +73,8 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
   // W_L [C][Ch] (canonical): phase A reads it with 4 distinct addresses per warp, phase B
   // with consecutive channels per lane (conflict-free)
   float* s_w2 = reinterpret_cast<float*>(smem_raw + 128 + head_region0(C, Ch));
-  float* s_b = s_w2 + C * Ch;
-  float* s_dl = s_b + kMaxC;                                  // [kTP][NC]
+  float* s_b = s_w2 + ((C * Ch + 3) & ~3);  // 16-byte aligned (s_dl is read as float4)
+  float* s_dl = s_b + kMaxC;                                  // [kTP][kNCP]
   int* s_lab = reinterpret_cast<int*>(s_dl + kTP * kMaxC);     // [kTP]
   const uint32_t bar0 = ptx::smem_u32(&bars[0]), bar1 = ptx::smem_u32(&bars[1]);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -114,6 +114,8 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
   // channel groups 32 (w & 1) + lane (keeps the accumulators in registers).
   constexpr int kMG = 1;
   const bool pairB = VEC && Ch > 128;
+  // dz rows in shared memory are padded to kNCP classes (float4 reads in phase B)
+  constexpr int kNCP = (NC + 3) & ~3;
   float accW[VEC ? 1 : kMC][NC], accP[VEC ? 1 : kMC], accL[NC];
   float accW4[VEC ? kMG : 1][NC][4], accP4[VEC ? kMG : 1][4];
 #pragma unroll
@@ -136,6 +138,15 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
 #pragma unroll
   for (int c = 0; c < NC; ++c) accL[c] = 0.f;
   __syncthreads();  // s_w is filled (the barrier init sync above precedes nothing else)
+  // VEC: W_L[:, 4g..4g+3] of this lane's phase-B channel group, held in registers
+  constexpr bool kW4Reg = VEC && NC <= 4;
+  float4 w4reg[kW4Reg ? NC : 1];
+  if constexpr (kW4Reg) {
+    const int g = lane + (pairB ? 32 * (warp & 1) : 0);
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      w4reg[c] = 4 * g < Ch ? reinterpret_cast<const float4*>(s_w2 + c * Ch)[g] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   if constexpr (kWReg) {
 #pragma unroll
     for (int m = 0; m < kMC; ++m) {
@@ -155,32 +166,7 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
     const long long p0 = (long long)tt * kTP;
     // ---------------------------------------------------------- phase 0: labels (lanes 0..7)
     if (lane < 8) {
-      const long long pos = p0 + pw0 + lane;
-      int lab = kLabBeyond;
-      if (pos < per_img) {
-        const int gl = (int)(pos / frag_sz);
-        const int rem = (int)(pos - (long long)gl * frag_sz);
-        const int i = rem / a.gc, j = rem - (rem / a.gc) * a.gc;
-        lab = kLabPad;
-        if (i < a.vr && j < a.vc) {
-          lab = 255;
-          if (TRAIN) {
-            // label through the fragment -> pixel map: y = r1 + k1 (r2 + k2 (... + kL i))
-            int yy = i, xx = j, rf = gl;
-            for (int l = a.n_levels - 1; l >= 0; --l) {
-              const int kq = a.pool_k[l];
-              const int d = rf % (kq * kq);
-              rf /= kq * kq;
-              yy = d / kq + kq * yy;
-              xx = d % kq + kq * xx;
-            }
-            if (yy < a.O_H && xx < a.O_W) lab = a.labels[((long long)img * a.O_H + yy) * a.O_W + xx];
-            if (lab != 255 && lab >= C) atomicOr(a.err, 1);
-          } else {
-            lab = 0;
-          }
-        }
-      }
+      const int lab = head_label(a, img, p0 + pw0 + lane, per_img, frag_sz, TRAIN);
       s_lab[pw0 + lane] = lab;
     }
     if (bulk) {
@@ -272,7 +258,7 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
 #pragma unroll
           for (int c = 0; c < NC; ++c)
             if ((c & 3) == qa)
-              s_dl[pa * NC + c] = (c < C) ? inv * (expf(z[c] - lse) - (c == lab ? 1.f : 0.f)) : 0.f;
+              s_dl[pa * kNCP + c] = (c < C) ? inv * (expf(z[c] - lse) - (c == lab ? 1.f : 0.f)) : 0.f;
         }
       }
     }
@@ -294,8 +280,20 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
         if (lab == kLabBeyond) break;  // past the end of the image (and so are the rest)
         const bool act = lab >= 0 && lab < C;
         float dl[NC];
+        if (act) {  // the row of dz: kNCP / 4 broadcast LDS.128
+          const float4* r4 = reinterpret_cast<const float4*>(s_dl + p * kNCP);
 #pragma unroll
-        for (int c = 0; c < NC; ++c) dl[c] = act ? s_dl[p * NC + c] : 0.f;
+          for (int j = 0; j < kNCP / 4; ++j) {
+            const float4 v = r4[j];
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (4 * j + u < NC) dl[4 * j + u] = vv[u];
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < NC; ++c) dl[c] = 0.f;
+        }
         if (act && lane == 0 && !(pairB && (warp & 1))) {
 #pragma unroll
           for (int c = 0; c < NC; ++c) accL[c] += dl[c];
@@ -321,7 +319,7 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
               float sacc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
               for (int c = 0; c < NC; ++c) {
-                const float4 w = reinterpret_cast<const float4*>(s_w2 + c * Ch)[g];
+                const float4 w = kW4Reg ? w4reg[kW4Reg ? c : 0] : reinterpret_cast<const float4*>(s_w2 + c * Ch)[g];
                 const float ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
@@ -426,7 +424,7 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
 }
 
 size_t head_smem(int C, int Ch) {
-  return 128 + head_region0(C, Ch) + sizeof(float) * (C * Ch + kMaxC + kTP * kMaxC) + sizeof(int) * kTP;
+  return 128 + head_region0(C, Ch) + sizeof(float) * (((C * Ch + 3) & ~3) + kMaxC + kTP * kMaxC) + sizeof(int) * kTP;
 }
 
 template <int NC, bool TRAIN, bool TANH>

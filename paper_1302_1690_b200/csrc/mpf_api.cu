@@ -256,6 +256,14 @@ static bool use_tc(const Net* N, const LayerPlan& P, bool dgrad) {
   return tc_supported(dgrad ? P.cout : P.cin, dgrad ? P.cin : P.cout, P.L.k);
 }
 
+// Does the training head run on the tensor cores (head_tc.cu)?  Then the last hidden
+// layer writes h TF32-rounded (an MMA operand), like every other tensor-core input.
+static bool head_tc_used(const Net* N) {
+  if (fwd_round_off()) return false;
+  const int L = N->n_layers - 1;
+  return head_tc_ok(N->classes, N->a[L].C, true, N->cfg.precision == MPF_PREC_TF32);
+}
+
 }  // namespace mpf
 
 using namespace mpf;
@@ -426,7 +434,9 @@ static mpf_status forward_impl(Net* N, const float* d_images, int n, float* d_pr
     const Act& in = N->a[l];
     const Act& o = N->a[l + 1];
     // the consumer of this output rounds? (TF32 operand of a tensor-core conv)
-    const bool next_tc = (l + 1 < N->n_layers - 1) && N->lp[l + 1].L.kind != MPF_POOL && use_tc(N, N->lp[l + 1], false);
+    // (the tensor-core softmax head counts: it reads h as TF32 MMA operand)
+    const bool next_tc = ((l + 1 < N->n_layers - 1) && N->lp[l + 1].L.kind != MPF_POOL && use_tc(N, N->lp[l + 1], false)) ||
+                         (l + 1 == N->n_layers - 1 && head_tc_used(N));
     if (P.L.kind == MPF_POOL) {
       const Act& y = in;
       MpfArgs m;
@@ -650,8 +660,14 @@ static mpf_status backward_impl(Net* N, const uint8_t* d_labels, const float* h_
              launch_loss_rows(scr(N, N->off_rowloss), (long long)h.F * h.gr * h.gc, nlab, n, d_loss, s));
   } else {
     const double pos = (double)n * h.F * h.vr * h.vc;
-    LAUNCH(N, s, "head_loss_delta", L, 6.0 * pos * h.C * N->classes, pos * (8.0 * h.C + 1.0),
-           launch_head2(hd, s));
+    if (head_tc_used(N)) {
+      hd.n_blocks = head_tc_grid((long long)h.F * h.gr * h.gc, n);
+      LAUNCH(N, s, "head_loss_delta", L, 6.0 * pos * h.C * N->classes, pos * (8.0 * h.C + 1.0),
+             launch_head_tc(hd, s));
+    } else {
+      LAUNCH(N, s, "head_loss_delta", L, 6.0 * pos * h.C * N->classes, pos * (8.0 * h.C + 1.0),
+             launch_head2(hd, s));
+    }
     const int E = N->classes * h.C + N->classes + h.C;
     // [dW_L | db_L] are contiguous in the canonical order; db of layer L-1 follows
     LAUNCH(N, s, "head_reduce", L, 0.0, 4.0 * (double)hd.n_blocks * E,

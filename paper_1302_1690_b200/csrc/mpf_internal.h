@@ -191,6 +191,10 @@ int head_loss_parts_per_tile();
 int head_blocks(long long total_tiles);
 bool head_supported(int C, int Ch);
 cudaError_t launch_head2(const HeadArgs& a, cudaStream_t s);
+// tensor-core training head (head_tc.cu): eligibility, its grid (= partial rows), launch
+bool head_tc_ok(int C, int Ch, bool train, bool tf32);
+int head_tc_grid(long long per_img, int n);
+cudaError_t launch_head_tc(const HeadArgs& a, cudaStream_t s);
 
 cudaError_t launch_label_count(const uint8_t* labels, int n, int hw, int classes, int* nlab, cudaStream_t s);
 cudaError_t launch_loss_finalize(const float* loss_part, int parts, const int* nlab, int n, float* loss,

@@ -449,13 +449,13 @@ __global__ void __launch_bounds__(256) mpf_bwd_slide_kernel(MpfBwdArgs a) {
 __host__ __device__ constexpr int tile_cells_padded(int wy, int wx) { return (wy * wx) | 1; }
 
 template <int K, int kTBY, int kTBX>
-__global__ void __launch_bounds__(256) mpf_bwd_tile_kernel(MpfBwdArgs a, int rows_per_cta) {
+__global__ void __launch_bounds__(256) mpf_bwd_tile_kernel(MpfBwdArgs a, int rows_per_cta, int nbuf) {
   extern __shared__ __align__(16) uint8_t sm_raw[];
   constexpr int WY = kTBY + K - 1, WX = kTBX + K - 1, S = tile_cells_padded(WY, WX);
   const int C = a.C, CV = C / 4, CVP = (CV + 3) & ~3;
-  uint32_t* s_id = reinterpret_cast<uint32_t*>(sm_raw);                  // [CVP / 4][S][4]
-  float4* s_d = reinterpret_cast<float4*>(sm_raw + (size_t)CVP * S * 4);  // [CV][S]
-  float* s_red = reinterpret_cast<float*>(s_d + (size_t)CV * S);          // [256 / CV][C]
+  // nbuf staging buffers [argmax words | deltas], then the bias reduction area
+  const size_t buf_bytes = (size_t)CVP * S * 4 + (size_t)CV * S * 16;
+  float* s_red = reinterpret_cast<float*>(sm_raw + nbuf * buf_bytes);  // [256 / CV][C]
   const int Xw = K * a.m_c, Yw = K * a.m_r;
   const int MM = a.m_r * a.m_c;
   const int X0 = blockIdx.x * kTBX;
@@ -469,96 +469,118 @@ __global__ void __launch_bounds__(256) mpf_bwd_tile_kernel(MpfBwdArgs a, int row
   const int ci = tid % CI, pi = tid / CI, npi = 256 / CI;
   // per-fragment strides (32-bit: one input fragment's pooled output is < 2^31 elements)
   const int MMC = MM * C, mcC = a.m_c * C;
-  float4* const s_d_cv = s_d + cv * S;
-  uint32_t* const s_id_cv = s_id + (cv >> 2) * S * 4 + (cv & 3);
-  for (int g = blockIdx.z; g < a.n_frag_in; g += gridDim.z) {
+  // this CTA's tiles: (input fragment g, first row Y0), g-major
+  const int n_yt = yend > ybeg ? (yend - ybeg + kTBY - 1) / kTBY : 0;
+  const int n_g = blockIdx.z < a.n_frag_in ? (a.n_frag_in - blockIdx.z + gridDim.z - 1) / gridDim.z : 0;
+  const int n_tiles = n_yt * n_g;
+
+  // ---- stage tile `it` into buffer `buf`: windows wy in [Y0-K+1, Y0+kTBY), wx in
+  // [X0-K+1, X0+kTBX).  cp.async: global -> shared without a register round trip, so
+  // every thread keeps all of its staging loads in flight; absent windows read as idx
+  // 0xFF.., delta 0.  Division-free apart from the compile-time WX and K.
+  auto stage = [&](int it, int buf) {
+    const int g = blockIdx.z + (it / n_yt) * gridDim.z, Y0 = ybeg + (it % n_yt) * kTBY;
     const size_t fbase = (size_t)g * K * K * MM * C;
     const float* dsrc = a.dout + fbase;
     const uint8_t* isrc = a.idx + fbase;
-    float* const dst_g = a.din + (size_t)g * a.gr * a.gc * C + cv * 4;  // one fragment < 2^31 elements
-    for (int Y0 = ybeg; Y0 < yend; Y0 += kTBY) {
-      __syncthreads();  // previous tile's shared data fully consumed
-      // ---- stage windows wy in [Y0-K+1, Y0+kTBY), wx in [X0-K+1, X0+kTBX)
-      // cp.async: global -> shared without a register round trip, so every thread keeps
-      // all of its staging loads in flight; absent windows read as idx 0xFF.., delta 0.
-      // Division-free apart from the compile-time WX and K.
-      if (pt < npt) {
-        for (int t = pt; t < WY * WX; t += npt) {
-          const int wyl = t / WX, wxl = t - wyl * WX;
-          const int wy = Y0 - K + 1 + wyl, wx = X0 - K + 1 + wxl;
-          float4* dst = s_d_cv + t;
-          if ((unsigned)wy < (unsigned)Yw && (unsigned)wx < (unsigned)Xw) {
-            const unsigned uy = wy, ux = wx;
-            const int off = (int)((uy % K) * K + ux % K) * MMC + (int)(uy / K) * mcC + (int)(ux / K) * C + cv * 4;
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-                         "l"(dsrc + off)
-                         : "memory");
-          } else {
-            *dst = make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-        }
-      }
-      if (pi < npi) {
-        for (int t = pi; t < WY * WX; t += npi) {
-          const int wyl = t / WX, wxl = t - wyl * WX;
-          const int wy = Y0 - K + 1 + wyl, wx = X0 - K + 1 + wxl;
-          const bool in = (unsigned)wy < (unsigned)Yw && (unsigned)wx < (unsigned)Xw;
-          const unsigned uy = in ? wy : 0, ux = in ? wx : 0;
-          const int off = (int)((uy % K) * K + ux % K) * MMC + (int)(uy / K) * mcC + (int)(ux / K) * C;
-          if (idx16) {
-            uint32_t* dst = s_id + (ci * S + t) * 4;
-            if (in)
-              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-                           "l"(isrc + off + ci * 16)
-                           : "memory");
-            else
-              *reinterpret_cast<uint4*>(dst) = make_uint4(~0u, ~0u, ~0u, ~0u);
-          } else {
-            uint32_t* dst = s_id + ((ci >> 2) * S + t) * 4 + (ci & 3);
-            if (in)
-              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-                           "l"(isrc + off + ci * 4)
-                           : "memory");
-            else
-              *dst = ~0u;
-          }
-        }
-      }
-      asm volatile("cp.async.wait_all;" ::: "memory");
-      __syncthreads();
-      // ---- gather: element (Y0+ty, X0+tx) sums window (ty+K-1-dy, tx+K-1-dx) where idx == dy*K+dx
-      if (pt < npt) {
-        for (unsigned q = pt; q < kTBY * kTBX; q += npt) {
-          const int ty = q / kTBX, tx = q % kTBX;
-          const int Y = Y0 + ty, X = X0 + tx;
-          if (Y >= yend || X >= a.gc) continue;
-          const int cell = (ty + K - 1) * WX + (tx + K - 1);
-          const uint32_t* pid = s_id_cv + cell * 4;
-          const float4* pd = s_d_cv + cell;
-          float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-          for (int dy = 0; dy < K; ++dy)
-#pragma unroll
-            for (int dx = 0; dx < K; ++dx) {
-              const int wo = dy * WX + dx;  // compile-time after unrolling
-              // byte v of `x` is zero iff channel v of this window selected (dy, dx)
-              const uint32_t x = pid[-wo * 4] ^ ((uint32_t)(dy * K + dx) * 0x01010101u);
-              const float4 d = pd[-wo];
-              if (!(x & 0xFFu)) acc[0] += d.x;
-              if (!(x & 0xFF00u)) acc[1] += d.y;
-              if (!(x & 0xFF0000u)) acc[2] += d.z;
-              if (!(x & 0xFF000000u)) acc[3] += d.w;
-            }
-          float o[4];
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            bsum[v] += acc[v];
-            o[v] = a.round_tf32 ? tf32_rna(acc[v]) : acc[v];
-          }
-          stv<4>(dst_g + (Y * a.gc + X) * C, o);
+    uint32_t* s_id = reinterpret_cast<uint32_t*>(sm_raw + buf * buf_bytes);       // [CVP / 4][S][4]
+    float4* s_d = reinterpret_cast<float4*>(sm_raw + buf * buf_bytes + (size_t)CVP * S * 4);  // [CV][S]
+    if (pt < npt) {
+      float4* s_d_cv = s_d + cv * S;
+      for (int t = pt; t < WY * WX; t += npt) {
+        const int wyl = t / WX, wxl = t - wyl * WX;
+        const int wy = Y0 - K + 1 + wyl, wx = X0 - K + 1 + wxl;
+        float4* dst = s_d_cv + t;
+        if ((unsigned)wy < (unsigned)Yw && (unsigned)wx < (unsigned)Xw) {
+          const unsigned uy = wy, ux = wx;
+          const int off = (int)((uy % K) * K + ux % K) * MMC + (int)(uy / K) * mcC + (int)(ux / K) * C + cv * 4;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                       "l"(dsrc + off)
+                       : "memory");
+        } else {
+          *dst = make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
     }
+    if (pi < npi) {
+      for (int t = pi; t < WY * WX; t += npi) {
+        const int wyl = t / WX, wxl = t - wyl * WX;
+        const int wy = Y0 - K + 1 + wyl, wx = X0 - K + 1 + wxl;
+        const bool in = (unsigned)wy < (unsigned)Yw && (unsigned)wx < (unsigned)Xw;
+        const unsigned uy = in ? wy : 0, ux = in ? wx : 0;
+        const int off = (int)((uy % K) * K + ux % K) * MMC + (int)(uy / K) * mcC + (int)(ux / K) * C;
+        if (idx16) {
+          uint32_t* dst = s_id + (ci * S + t) * 4;
+          if (in)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                         "l"(isrc + off + ci * 16)
+                         : "memory");
+          else
+            *reinterpret_cast<uint4*>(dst) = make_uint4(~0u, ~0u, ~0u, ~0u);
+        } else {
+          uint32_t* dst = s_id + ((ci >> 2) * S + t) * 4 + (ci & 3);
+          if (in)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                         "l"(isrc + off + ci * 4)
+                         : "memory");
+          else
+            *dst = ~0u;
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  // Two buffers: tile it + 1 is in flight while tile it is gathered.
+  if (n_tiles > 0) stage(0, 0);
+  for (int it = 0; it < n_tiles; ++it) {
+    const int buf = nbuf == 2 ? (it & 1) : 0;
+    if (nbuf == 2 && it + 1 < n_tiles) {
+      stage(it + 1, buf ^ 1);  // that buffer was last read by tile it - 1 (barrier below)
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();  // tile it's staging (all threads' copies and fills) is visible
+    const int g = blockIdx.z + (it / n_yt) * gridDim.z, Y0 = ybeg + (it % n_yt) * kTBY;
+    float* const dst_g = a.din + (size_t)g * a.gr * a.gc * C + cv * 4;  // one fragment < 2^31 elements
+    // ---- gather: element (Y0+ty, X0+tx) sums window (ty+K-1-dy, tx+K-1-dx) where idx == dy*K+dx
+    if (pt < npt) {
+      const uint32_t* s_id_cv =
+          reinterpret_cast<const uint32_t*>(sm_raw + buf * buf_bytes) + (cv >> 2) * S * 4 + (cv & 3);
+      const float4* s_d_cv = reinterpret_cast<const float4*>(sm_raw + buf * buf_bytes + (size_t)CVP * S * 4) + cv * S;
+      for (unsigned q = pt; q < kTBY * kTBX; q += npt) {
+        const int ty = q / kTBX, tx = q % kTBX;
+        const int Y = Y0 + ty, X = X0 + tx;
+        if (Y >= yend || X >= a.gc) continue;
+        const int cell = (ty + K - 1) * WX + (tx + K - 1);
+        const uint32_t* pid = s_id_cv + cell * 4;
+        const float4* pd = s_d_cv + cell;
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int dy = 0; dy < K; ++dy)
+#pragma unroll
+          for (int dx = 0; dx < K; ++dx) {
+            const int wo = dy * WX + dx;  // compile-time after unrolling
+            // byte v of `x` is zero iff channel v of this window selected (dy, dx)
+            const uint32_t x = pid[-wo * 4] ^ ((uint32_t)(dy * K + dx) * 0x01010101u);
+            const float4 d = pd[-wo];
+            if (!(x & 0xFFu)) acc[0] += d.x;
+            if (!(x & 0xFF00u)) acc[1] += d.y;
+            if (!(x & 0xFF0000u)) acc[2] += d.z;
+            if (!(x & 0xFF000000u)) acc[3] += d.w;
+          }
+        float o[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          bsum[v] += acc[v];
+          o[v] = a.round_tf32 ? tf32_rna(acc[v]) : acc[v];
+        }
+        stv<4>(dst_g + (Y * a.gc + X) * C, o);
+      }
+    }
+    __syncthreads();  // buffer `buf` fully consumed before it is refilled
+    if (nbuf == 1 && it + 1 < n_tiles) stage(it + 1, 0);
   }
   if (a.bias_part == nullptr) return;
   __syncthreads();
@@ -642,9 +664,18 @@ static bool bwd_slide(const MpfBwdArgs& a) { return a.C % 4 == 0 && a.k >= 2 && 
 constexpr int kTileRows = 64;  // conv-output rows per CTA of the tiled kernel (partials per CTA)
 
 // tile shape (rows x cols of conv-output positions per CTA step); MPF_BWD_TILE=RxC overrides
+static int tile_nbuf() {
+  static const int nb = getenv("MPF_BWD_NBUF") ? (atoi(getenv("MPF_BWD_NBUF")) == 2 ? 2 : 1) : 1;
+  return nb;
+}
+// staging budget per CTA: two buffers at 2 CTAs per SM by default; MPF_BWD_SMEM_KB overrides
+static size_t tile_budget() {
+  static const size_t kb = getenv("MPF_BWD_SMEM_KB") ? (size_t)atoi(getenv("MPF_BWD_SMEM_KB")) : 56 * tile_nbuf();
+  return kb * 1024;
+}
 static size_t tile_bytes(int C, int k, int ty, int tx) {
   const int CV = C / 4, CVP = (CV + 3) & ~3, S = tile_cells_padded(ty + k - 1, tx + k - 1);
-  return (size_t)CVP * S * 4 + (size_t)CV * S * 16 + sizeof(float) * (256 / CV) * C;
+  return tile_nbuf() * ((size_t)CVP * S * 4 + (size_t)CV * S * 16) + sizeof(float) * (256 / CV) * C;
 }
 
 // Largest tile whose staging fits ~56 KB (4 CTAs per SM): measured best per layer on
@@ -654,7 +685,7 @@ static void tile_shape(const MpfBwdArgs& a, int* ty, int* tx) {
   *tx = 8;
   const int cand[3][2] = {{16, 16}, {8, 16}, {8, 8}};
   for (int i = 0; i < 3; ++i)
-    if (tile_bytes(a.C, a.k, cand[i][0], cand[i][1]) <= 56 * 1024) {
+    if (tile_bytes(a.C, a.k, cand[i][0], cand[i][1]) <= tile_budget()) {
       *ty = cand[i][0];
       *tx = cand[i][1];
       break;
@@ -680,7 +711,7 @@ static cudaError_t launch_tile_k(const MpfBwdArgs& a, dim3 grid, dim3 blk, size_
   if (ty == TY && tx == TX) {                                                                                   \
     e = cudaFuncSetAttribute(mpf_bwd_tile_kernel<K, TY, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
     if (e != cudaSuccess) return e;                                                                             \
-    mpf_bwd_tile_kernel<K, TY, TX><<<grid, blk, sm, s>>>(a, kTileRows);                                          \
+    mpf_bwd_tile_kernel<K, TY, TX><<<grid, blk, sm, s>>>(a, kTileRows, tile_nbuf());                                          \
     return cudaGetLastError();                                                                                  \
   }
   MPF_TILE_CASE(8, 8)

@@ -271,18 +271,47 @@ def test_fewer_images_than_capacity():
 
 # ----------------------------------------------------------------- full images, kernel variants
 
-@pytest.mark.parametrize("name", ["cfg3", "cfg5"])
+def _cfg4s():
+    """The cfg4 network (5 classes, FC1 3x3x128 -> 200) on a 126^2 image (33^2 outputs)."""
+    import dataclasses
+    return dataclasses.replace(S.CONFIGS["cfg4"], name="cfg4s", H=126, W=126)
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg5", "cfg4s"])
 def test_full_image_all_pixels_vs_o2(name):
-    """One whole BASELINE image (512^2 / 768^2), every output pixel labelled, TF32 path (the
-    bench configuration) against the literal whole-image oracle O2 in fp64: outputs, loss
-    and every weight/bias gradient within rel L2 5e-3 (R17)."""
-    cfg = S.CONFIGS[name]
+    """One whole BASELINE image (512^2 / 768^2; the cfg4 net on 126^2), every output pixel
+    labelled, TF32 path (the bench configuration) against the literal whole-image oracle
+    O2 in fp64: outputs, loss and every weight/bias gradient within rel L2 5e-3 (R17)."""
+    cfg = _cfg4s() if name == "cfg4s" else S.CONFIGS[name]
     images, labels = S.make_batch(cfg, [11])
     params = S.init_params(cfg)
     g = gpu_step(cfg.layers, cfg.P, images, labels, params, "tf32")
     o = oracle_step(cfg.layers, cfg.P, images.astype(np.float64), labels, params, engine="o2")
     errs = compare_step(cfg.layers, g, o, TOL_TF32, f"{name} full image")
     print(name, "full-image rel L2:", {k: f"{v:.1e}" for k, v in errs.items()})
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg4s"])
+def test_tensor_core_head_vs_o2(name):
+    """The opt-in tensor-core softmax head (MPF_HEAD_TC=1: GEMM1 z = W h and GEMM2
+    dh^T = W^T dz on tcgen05, dz / dW on the FMA pipes) against O2: loss, probabilities
+    and every gradient within rel L2 5e-3; and against the default CUDA-core head."""
+    import os
+    cfg = _cfg4s() if name == "cfg4s" else S.CONFIGS[name]
+    images, labels = S.make_batch(cfg, [3, 4])
+    params = S.init_params(cfg)
+    os.environ["MPF_HEAD_TC"] = "1"
+    try:
+        g = gpu_step(cfg.layers, cfg.P, images, labels, params, "tf32")
+    finally:
+        os.environ.pop("MPF_HEAD_TC", None)
+    d = gpu_step(cfg.layers, cfg.P, images, labels, params, "tf32")
+    o = oracle_step(cfg.layers, cfg.P, images.astype(np.float64), labels, params, engine="o2")
+    compare_step(cfg.layers, g, o, TOL_TF32, f"{name} tensor-core head")
+    # the two heads differ by TF32 rounding of h (an MMA operand) and summation order
+    assert rel_l2(g["loss"], d["loss"]) <= 1e-4
+    for nm, sl in param_slices(cfg.layers):
+        assert rel_l2(g["grad_sum"][sl], d["grad_sum"][sl]) <= 2e-3, nm
 
 
 def _run_variant(env, name="cfg2", n=2, prec="tf32"):
