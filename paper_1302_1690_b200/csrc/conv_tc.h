@@ -67,5 +67,8 @@ cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s, int* grid_out = 
 cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits, cudaStream_t s);
 // 2-D fp32 tensor map [rows][cols] (cols contiguous), box {32 cols, box_rows}, SWIZZLE_128B
 cudaError_t make_tmap_sw128(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows);
+// general fp32 tensor map: dims[0] innermost, strides[i] = bytes between steps of dim i+1
+cudaError_t make_tmap_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                          const uint32_t* box, bool sw128);
 
 }  // namespace mpf

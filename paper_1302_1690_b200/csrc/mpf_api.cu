@@ -472,7 +472,10 @@ static mpf_status forward_impl(Net* N, const float* d_images, int n, float* d_pr
         f.w = N->params + P.w_off; f.bias = N->params + P.b_off; f.k = P.L.k; f.cout = P.cout;
         f.out = out; f.out_gr = o.gr; f.out_gc = o.gc; f.out_vr = o.vr; f.out_vc = o.vc;
         f.act = P.L.act; f.zero_pad = P.out_where == Where::Tape ? 1 : 0; f.round_tf32 = next_tc ? 1 : 0;
-        LAUNCH(N, s, "conv_first_fwd", l, cflops, cbytes, launch_first_conv(f, s));
+        if (tf32 && first_conv_tc_ok(N->cfg.in_channels, P.cout, P.L.k))
+          LAUNCH(N, s, "conv_first_fwd", l, cflops, cbytes, launch_first_conv_tc(f, s));
+        else
+          LAUNCH(N, s, "conv_first_fwd", l, cflops, cbytes, launch_first_conv(f, s));
       } else if (l > 0 && use_tc(N, P, false)) {
         TcConvArgs t{};
         t.x = x; t.n_frag = n * in.F; t.gr = in.gr; t.gc = in.gc; t.cin = P.cin;

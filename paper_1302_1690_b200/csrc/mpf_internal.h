@@ -222,6 +222,9 @@ struct FirstConvArgs {
   int act, zero_pad, round_tf32;
   int n_cog;             // set by the launcher
 };
+// tensor-core first layer forward (conv_first_tc.cu), 3xTF32
+bool first_conv_tc_ok(int cin, int cout, int k);
+cudaError_t launch_first_conv_tc(const FirstConvArgs& a, cudaStream_t s);
 struct FirstWgradArgs {
   const float* img;
   int n, H, W;

@@ -4,8 +4,8 @@ mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || exit 1
 timeout 120 python scripts/run_step.py --workload cfg2 > gpurun_out/quick_cfg2.log 2>&1; echo quick_cfg2 $? >> gpurun_out/status.txt
 grep -q "quick_cfg2 0" gpurun_out/status.txt || exit 1
-if [ -n "$1" ]; then k="-k $1"; else k=""; fi
-timeout 900 python -m pytest tests -m gpu -x -q $k > gpurun_out/gpu_tests.log 2>&1; echo tests $? >> gpurun_out/status.txt
+KEXPR="$1"
+timeout 900 python -m pytest tests -m gpu -x -q ${KEXPR:+-k "$KEXPR"} > gpurun_out/gpu_tests.log 2>&1; echo tests $? >> gpurun_out/status.txt
 shift
 for v in NONE=1 "$@"; do
   for w in cfg4 cfg5; do

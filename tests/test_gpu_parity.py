@@ -291,6 +291,31 @@ def test_full_image_all_pixels_vs_o2(name):
     print(name, "full-image rel L2:", {k: f"{v:.1e}" for k, v in errs.items()})
 
 
+@pytest.mark.parametrize("name", ["cfg2", "cfg4s", "cfg5"])
+def test_tensor_core_first_layer_matches(name):
+    """The opt-in tensor-core first layer (MPF_FIRST_TC=1: column slab, k MMAs with the
+    start moved by kx rows, 3xTF32) against the default fp32 CUDA-core kernel on the same
+    images: the forward is fp32-accurate, so the argmaxes agree and the step matches
+    closely; and against O2 on cfg2."""
+    import os
+    cfg = _cfg4s() if name == "cfg4s" else S.CONFIGS[name]
+    images, labels = S.make_batch(cfg, [5])
+    params = S.init_params(cfg)
+    os.environ["MPF_FIRST_TC"] = "1"
+    try:
+        g = gpu_step(cfg.layers, cfg.P, images, labels, params, "tf32")
+    finally:
+        os.environ.pop("MPF_FIRST_TC", None)
+    d = gpu_step(cfg.layers, cfg.P, images, labels, params, "tf32")
+    assert rel_l2(g["probs"], d["probs"]) <= 1e-3
+    assert rel_l2(g["loss"], d["loss"]) <= 1e-4
+    for nm, sl in param_slices(cfg.layers):
+        assert rel_l2(g["grad_sum"][sl], d["grad_sum"][sl]) <= 5e-3, nm
+    if name == "cfg2":
+        o = oracle_step(cfg.layers, cfg.P, images.astype(np.float64), labels, params, engine="o2")
+        compare_step(cfg.layers, g, o, TOL_TF32, "tensor-core first layer")
+
+
 @pytest.mark.parametrize("name", ["cfg2", "cfg4s"])
 def test_tensor_core_head_vs_o2(name):
     """The opt-in tensor-core softmax head (MPF_HEAD_TC=1: GEMM1 z = W h and GEMM2
