@@ -30,9 +30,21 @@ __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float(r);
 }
 
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// SFU activations, as in the tensor-core epilogues: tanh(v) = 1 - 2 / (2^(2 v log2 e) + 1)
+// (absolute error ~1e-7; tanhf's ~25 instructions were a third of this kernel's issue)
 __device__ __forceinline__ float act_fwd(int act, float v) {
-  if (act == MPF_TANH) return tanhf(v);
-  if (act == MPF_LOGISTIC) return 1.f / (1.f + expf(-v));
+  if (act == MPF_TANH) return fmaf(-2.f, rcp_approx(ex2_approx(2.8853900817779268f * v) + 1.f), 1.f);
+  if (act == MPF_LOGISTIC) return rcp_approx(1.f + ex2_approx(-1.4426950408889634f * v));
   return v;
 }
 
