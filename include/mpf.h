@@ -179,6 +179,10 @@ mpf_status mpf_sgd_step(mpf_net* net, float lr, float grad_scale, void* stream);
  * and h_labels [n, out_rows, out_cols] into the bound staging area, mpf_train_step,
  * and an async copy of the per-image losses to h_loss[n].  If apply_sgd,
  * also mpf_sgd_step(lr, grad_scale).  h_loss is valid after the stream is synchronised.
+ * The uploads run on the net's own copy stream into one of two staging slots (ordered
+ * by events against the compute on `stream`), so back-to-back calls overlap the next
+ * step's upload with this step's kernels.  h_images / h_labels must stay unchanged until
+ * `stream` is synchronised (pinned memory for truly asynchronous copies).
  */
 mpf_status mpf_train_step_host(mpf_net* net, const float* h_images, const uint8_t* h_labels,
                                int32_t n, const float* h_class_w, float* h_loss, int32_t apply_sgd,

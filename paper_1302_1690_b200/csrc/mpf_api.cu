@@ -229,8 +229,13 @@ static void layout_memory(Net* N, int n) {
   N->off_lossp = s; s = align256(s + sizeof(float) * (size_t)N->loss_parts * n);
   N->off_err = s; s = align256(s + 256);
   N->off_rowloss = s; s = align256(s + sizeof(float) * (size_t)h_pos * n);  // fused-head per-position losses
-  N->off_stage_img = s; s = align256(s + sizeof(float) * (size_t)n * N->cfg.in_channels * N->cfg.image_rows * N->cfg.image_cols);
-  N->off_stage_lab = s; s = align256(s + (size_t)n * N->O_H * N->O_W);
+  {  // two staging slots [images | labels] for host-buffer steps
+    const size_t s0 = s;
+    N->off_stage_img = s; s = align256(s + sizeof(float) * (size_t)n * N->cfg.in_channels * N->cfg.image_rows * N->cfg.image_cols);
+    N->off_stage_lab = s; s = align256(s + (size_t)n * N->O_H * N->O_W);
+    N->stage_bytes = s - s0;
+    s += N->stage_bytes;
+  }
   N->off_stage_loss = s; s = align256(s + sizeof(float) * n);
   N->scratch_bytes = s;
   N->n_cap = n;
@@ -294,6 +299,14 @@ mpf_status mpf_net_create(const mpf_config* cfg, const mpf_layer* layers, int32_
 void mpf_net_destroy(mpf_net* net) {
   if (!net) return;
   for (cudaEvent_t e : net->prof.ev) cudaEventDestroy(e);
+  if (net->copy_stream) {
+    cudaStreamSynchronize(net->copy_stream);
+    cudaStreamDestroy(net->copy_stream);
+    for (int i = 0; i < 2; ++i) {
+      cudaEventDestroy(net->ev_copied[i]);
+      cudaEventDestroy(net->ev_free[i]);
+    }
+  }
   delete net;
 }
 
@@ -841,15 +854,34 @@ mpf_status mpf_train_step_host(mpf_net* N, const float* h_images, const uint8_t*
   if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound");
   if (n < 1 || n > N->n_cap) return fail(MPF_ERR_DATA, "n must be in [1, bound n_images]");
   cudaStream_t s = (cudaStream_t)stream;
-  float* d_img = scr(N, N->off_stage_img);
-  uint8_t* d_lab = (uint8_t*)(N->scratch + N->off_stage_lab);
+  // Double-buffered inputs: this step's H2D copies run on a copy stream into staging slot
+  // b, after the step that last read slot b (two calls ago) has finished with it; the
+  // compute stream waits only for its own slot.  Consecutive calls therefore overlap the
+  // next step's upload with this step's kernels (both inside a caller's timing of the
+  // calls), and the results are those of the serial order.
+  if (!N->copy_stream) {
+    MPF_CUDA(cudaStreamCreateWithFlags(&N->copy_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      MPF_CUDA(cudaEventCreateWithFlags(&N->ev_copied[i], cudaEventDisableTiming));
+      MPF_CUDA(cudaEventCreateWithFlags(&N->ev_free[i], cudaEventDisableTiming));
+      MPF_CUDA(cudaEventRecord(N->ev_free[i], s));
+    }
+  }
+  const int b = N->stage_slot;
+  N->stage_slot ^= 1;
+  float* d_img = scr(N, N->off_stage_img + b * N->stage_bytes);
+  uint8_t* d_lab = (uint8_t*)(N->scratch + N->off_stage_lab + b * N->stage_bytes);
   float* d_loss = scr(N, N->off_stage_loss);
   const size_t ib = sizeof(float) * (size_t)n * N->cfg.in_channels * N->cfg.image_rows * N->cfg.image_cols;
   const size_t lb = (size_t)n * N->O_H * N->O_W;
-  MPF_CUDA(cudaMemcpyAsync(d_img, h_images, ib, cudaMemcpyHostToDevice, s));
-  MPF_CUDA(cudaMemcpyAsync(d_lab, h_labels, lb, cudaMemcpyHostToDevice, s));
+  MPF_CUDA(cudaStreamWaitEvent(N->copy_stream, N->ev_free[b], 0));
+  MPF_CUDA(cudaMemcpyAsync(d_img, h_images, ib, cudaMemcpyHostToDevice, N->copy_stream));
+  MPF_CUDA(cudaMemcpyAsync(d_lab, h_labels, lb, cudaMemcpyHostToDevice, N->copy_stream));
+  MPF_CUDA(cudaEventRecord(N->ev_copied[b], N->copy_stream));
+  MPF_CUDA(cudaStreamWaitEvent(s, N->ev_copied[b], 0));
   mpf_status st = mpf_train_step(N, d_img, n, d_lab, h_class_w, d_loss, stream);
   if (st != MPF_OK) return st;
+  MPF_CUDA(cudaEventRecord(N->ev_free[b], s));  // slot b's images / labels are consumed
   if (apply_sgd) {
     st = mpf_sgd_step(N, lr, scale, stream);
     if (st != MPF_OK) return st;
