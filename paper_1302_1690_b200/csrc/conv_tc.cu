@@ -47,6 +47,7 @@ constexpr uint32_t kStageBytes = 32 * 128;  // one epilogue store box: 32 rows x
 struct ConvTcParams {
   int P_tot, gr, gc, out_vr, out_vc;
   int cin, cout, npad, k, shift_rows, n_cc;
+  int last_k8;  // k8 steps of the last channel chunk that hold real channels (1..4)
   int act, round_out, dact;
   const float* bias;
   const float* mul_dact;
@@ -523,11 +524,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t sa = sS + st * p.stage_bytes;
           const uint64_t adesc0 = ptx::sdesc_k_sw128(sa, p.base_mode);
           const uint64_t bdesc0 = ptx::sdesc_k_sw128(sa + p.a_slot_bytes, p.base_mode);
+          // the last channel chunk skips its all-zero k8 steps (e.g. C_in = 200: 7 chunks of
+          // 32, the last holding 8 real channels)
+          const int nk8 = cc == p.n_cc - 1 ? p.last_k8 : 4;
           for (int kx = 0; kx < k; ++kx) {
 #pragma unroll
             for (int acc = 0; acc < NACC; ++acc) {
 #pragma unroll
               for (int k8 = 0; k8 < 4; ++k8) {
+                if (k8 >= nk8) break;  // warp-uniform
                 // descriptor start-address field is (addr >> 4) in the low bits
                 const uint64_t ad = adesc0 + (uint64_t)((((acc * 128 + kx) * 128) + k8 * 32) >> 4);
                 const uint64_t bd = bdesc0 + (uint64_t)((kx * p.b_slot_bytes + k8 * 32) >> 4);
@@ -836,6 +841,7 @@ cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s, int* grid_out) {
   p.k = a.k;
   p.shift_rows = a.shift * (a.gc + 1);
   p.n_cc = (a.cin + kKC - 1) / kKC;
+  p.last_k8 = (a.cin - (p.n_cc - 1) * kKC + 7) / 8;
   p.act = a.act;
   p.round_out = a.round_out;
   p.dact = a.dact;
