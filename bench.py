@@ -228,7 +228,7 @@ def main():
 
     def step(i):
         im, lb = pools[i % 2][0], pools[i % 2][1]
-        net.train_step(im, lb)  # forward + backward (softmax head fused into the last hidden conv)
+        net.train_step(im, lb)  # forward + backward through the C ABI (mpf_train_step)
         D.allreduce_grads(net.grads)
         net.sgd_step(cfg.lr, 1.0 / B)
 

@@ -810,7 +810,8 @@ cudaError_t launch_nacc(const CUtensorMap& A, const CUtensorMap& B, const CUtens
 // MPF_TC_PAIR=1/0 forces a mode.
 bool want_pair(int npad, int K) {
   if (const char* e = getenv("MPF_TC_PAIR")) return atoi(e) != 0;
-  return npad >= 192 || (npad >= 128 && K >= 1536);
+  static const int k_min = getenv("MPF_TC_PAIR_KMIN") ? atoi(getenv("MPF_TC_PAIR_KMIN")) : 1536;
+  return npad >= 192 || (npad >= 128 && K >= k_min);
 }
 
 }  // namespace
