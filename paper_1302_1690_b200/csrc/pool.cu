@@ -600,6 +600,97 @@ __global__ void __launch_bounds__(256) mpf_bwd_tile_kernel(MpfBwdArgs a, int row
   }
 }
 
+// Register-blocked gather for k = 2 (premul deltas, 4-channel vectors): a thread owns a
+// 2 x 2 block of conv-output elements (rows 2i, 2i+1, columns 2j, 2j+1) of one channel
+// vector.  Every candidate window of the block lies in the 3 x 3 window patch rows
+// 2i-1 .. 2i+1, columns 2j-1 .. 2j+1, so the thread loads those 9 windows' argmax words and
+// deltas once (18 independent loads in flight, neighbouring blocks' overlap hits L1) and
+// gathers each element's k^2 candidates from registers in the same fixed (dy, dx) order as
+// the other MPF backward kernels (bitwise-identical results).  No shared-memory staging,
+// no barriers; CTAs stride over groups of consecutive blocks of one row.
+__global__ void __launch_bounds__(256) mpf_bwd_block2_kernel(MpfBwdArgs a, long long n_groups) {
+  extern __shared__ float s_red2[];  // [256 / CV][C]
+  const int C = a.C, CV = C / 4;
+  const int tid = threadIdx.x, cv = tid % CV, sub = tid / CV, nsub = 256 / CV;
+  const int Xw = 2 * a.m_c, Yw = 2 * a.m_r;
+  const int MM = a.m_r * a.m_c;
+  const int MMC = MM * C, mcC = a.m_c * C;
+  const int bj_n = (a.gc + 1) / 2, bi_n = (a.gr + 1) / 2;
+  const int groups_per_row = (bj_n + nsub - 1) / nsub;
+  float bsum[4] = {0.f, 0.f, 0.f, 0.f};
+  if (sub < nsub) {
+    for (long long grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
+      const int gj = (int)(grp % groups_per_row);
+      const long long t = grp / groups_per_row;
+      const int bi = (int)(t % bi_n);
+      const int g = (int)(t / bi_n);
+      const int bj = gj * nsub + sub;
+      if (bj >= bj_n) continue;
+      const float* dsrc = a.dout + (size_t)g * 4 * MMC + cv * 4;
+      const uint8_t* isrc = a.idx + (size_t)g * 4 * MMC + cv * 4;
+      // window patch: rows wy = 2bi - 1 + u, columns wx = 2bj - 1 + v (u, v < 3)
+      uint32_t id[3][3];
+      float4 d[3][3];
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        const int wy = 2 * bi - 1 + u;
+        const bool yok = wy >= 0 && wy < Yw;
+        const int rowoff = yok ? ((wy & 1) * 2) * MMC + (wy >> 1) * mcC : 0;
+#pragma unroll
+        for (int v = 0; v < 3; ++v) {
+          const int wx = 2 * bj - 1 + v;
+          const bool ok = yok && wx >= 0 && wx < Xw;
+          const int off = rowoff + (wx & 1) * MMC + (wx >> 1) * C;
+          id[u][v] = ok ? __ldg(reinterpret_cast<const uint32_t*>(isrc + (ok ? off : 0))) : 0xFFFFFFFFu;
+          d[u][v] = ok ? __ldg(reinterpret_cast<const float4*>(dsrc + (ok ? off : 0))) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      float* dst = a.din + ((size_t)g * a.gr * a.gc) * C + cv * 4;
+#pragma unroll
+      for (int ea = 0; ea < 2; ++ea)
+#pragma unroll
+        for (int eb = 0; eb < 2; ++eb) {
+          const int Y = 2 * bi + ea, X = 2 * bj + eb;
+          if (Y >= a.gr || X >= a.gc) continue;
+          float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+            for (int dx = 0; dx < 2; ++dx) {
+              // window (Y - dy, X - dx) = patch (ea - dy + 1, eb - dx + 1)
+              const uint32_t x = id[ea - dy + 1][eb - dx + 1] ^ ((uint32_t)(dy * 2 + dx) * 0x01010101u);
+              const float4 w = d[ea - dy + 1][eb - dx + 1];
+              if (!(x & 0xFFu)) acc[0] += w.x;
+              if (!(x & 0xFF00u)) acc[1] += w.y;
+              if (!(x & 0xFF0000u)) acc[2] += w.z;
+              if (!(x & 0xFF000000u)) acc[3] += w.w;
+            }
+          float o[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            bsum[q] += acc[q];
+            o[q] = a.round_tf32 ? tf32_rna(acc[q]) : acc[q];
+          }
+          stv<4>(dst + (Y * a.gc + X) * C, o);
+        }
+    }
+  }
+  if (a.bias_part == nullptr) return;
+  if (sub < nsub) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) s_red2[sub * C + cv * 4 + q] = bsum[q];
+  }
+  __syncthreads();
+  if (tid < CV) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float t = 0.f;
+      for (int q2 = 0; q2 < nsub; ++q2) t += s_red2[q2 * C + tid * 4 + q];
+      a.bias_part[(size_t)blockIdx.x * C + tid * 4 + q] = t;
+    }
+  }
+}
+
 // ----------------------------------------------------------------------------- channel sums
 // Generic per-channel partials of a [P][C] tensor (bias gradient of a conv whose delta
 // comes from a dgrad, i.e. a conv followed by another conv).
@@ -657,6 +748,20 @@ cudaError_t launch_mpf_fwd(const MpfArgs& a, cudaStream_t s) {
   return fwd_dispatch<1>(a, s);
 }
 
+// k = 2 register-blocked gather (default for k = 2; MPF_BWD_TILE2=1 keeps the tiled kernel)
+static bool bwd_block2(const MpfBwdArgs& a) {
+  return a.premul && a.k == 2 && a.C % 4 == 0 && a.C <= 1024 && !getenv("MPF_BWD_SLIDE") && !getenv("MPF_BWD_TILE2");
+}
+static long long block2_groups(const MpfBwdArgs& a) {
+  const int nsub = 256 / (a.C / 4);
+  const long long bj_n = (a.gc + 1) / 2, bi_n = (a.gr + 1) / 2;
+  return (long long)a.n_frag_in * bi_n * ((bj_n + nsub - 1) / nsub);
+}
+static int block2_grid(const MpfBwdArgs& a) {
+  const long long g = block2_groups(a);
+  const long long cap = 148LL * 8;  // 8 CTAs of 256 threads per SM
+  return (int)(g < cap ? (g < 1 ? 1 : g) : cap);
+}
 static bool bwd_tile(const MpfBwdArgs& a) {
   return a.premul && a.C % 4 == 0 && a.C <= 1024 && a.k >= 2 && a.k <= 4 && !getenv("MPF_BWD_SLIDE");
 }
@@ -736,12 +841,18 @@ static void bwd_geometry(const MpfBwdArgs& a, int V, dim3* grid, dim3* blk) {
 }
 
 long long mpf_bwd_partials(const MpfBwdArgs& a) {
+  if (bwd_block2(a)) return block2_grid(a);
   dim3 g, b;
   bwd_geometry(a, a.C % 4 == 0 ? 4 : 1, &g, &b);
   return (long long)g.x * g.y * g.z;
 }
 
 cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s) {
+  if (bwd_block2(a)) {
+    const size_t smem = sizeof(float) * (256 / (a.C / 4)) * a.C;
+    mpf_bwd_block2_kernel<<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
+    return cudaGetLastError();
+  }
   const int V = a.C % 4 == 0 ? 4 : 1;
   dim3 grid, blk;
   bwd_geometry(a, V, &grid, &blk);
