@@ -691,6 +691,106 @@ __global__ void __launch_bounds__(256) mpf_bwd_block2_kernel(MpfBwdArgs a, long 
   }
 }
 
+// Register-blocked gather for k = 3: a thread owns a 3 x BW block of conv-output elements of
+// one channel vector; the candidate windows form the 5 x (BW + 2) patch rows 3i-2 .. 3i+2.
+// Output row ea needs patch rows ea .. ea+2, so the patch streams through a ring of 3 rows:
+// rows 0-2 are loaded up front, row ea+3 after output row ea.  BW = 1 (MPF_BWD_BW3=1: 45 window
+// registers) or 3 (default: fewer loads per element; measured 1.84 vs 2.75 ms on cfg5).
+// Same fixed (dy, dx) order as the other MPF backward kernels (bitwise-identical results).
+template <int BW>  // block width in output columns (3: 5 x 5 patch; 1: 5 x 3 patch, fewer registers)
+__global__ void __launch_bounds__(256) mpf_bwd_block3_kernel(MpfBwdArgs a, long long n_groups) {
+  constexpr int K = 3, PW = BW + K - 1;
+  extern __shared__ float s_red3[];  // [256 / CV][C]
+  const int C = a.C, CV = C / 4;
+  const int tid = threadIdx.x, cv = tid % CV, sub = tid / CV, nsub = 256 / CV;
+  const int Xw = K * a.m_c, Yw = K * a.m_r;
+  const int MMC = a.m_r * a.m_c * C, mcC = a.m_c * C;
+  const int bj_n = (a.gc + BW - 1) / BW, bi_n = (a.gr + K - 1) / K;
+  const int groups_per_row = (bj_n + nsub - 1) / nsub;
+  float bsum[4] = {0.f, 0.f, 0.f, 0.f};
+  if (sub < nsub) {
+    for (long long grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
+      const int gj = (int)(grp % groups_per_row);
+      const long long t = grp / groups_per_row;
+      const int bi = (int)(t % bi_n);
+      const int g = (int)(t / bi_n);
+      const int bj = gj * nsub + sub;
+      if (bj >= bj_n) continue;
+      const float* dsrc = a.dout + (size_t)g * K * K * MMC + cv * 4;
+      const uint8_t* isrc = a.idx + (size_t)g * K * K * MMC + cv * 4;
+      int coloff[PW];
+      bool colok[PW];
+#pragma unroll
+      for (int v = 0; v < PW; ++v) {
+        const int wx = BW * bj - (K - 1) + v;
+        colok[v] = wx >= 0 && wx < Xw;
+        coloff[v] = colok[v] ? (wx % K) * MMC + (wx / K) * C : 0;
+      }
+      uint32_t id[K][PW];
+      float4 d[K][PW];
+      auto load_row = [&](int u, uint32_t (&ir)[PW], float4 (&dr)[PW]) {
+        const int wy = K * bi - (K - 1) + u;
+        const bool yok = wy >= 0 && wy < Yw;
+        const int rowoff = yok ? (wy % K) * K * MMC + (wy / K) * mcC : 0;
+#pragma unroll
+        for (int v = 0; v < PW; ++v) {
+          const bool ok = yok && colok[v];
+          const int off = ok ? rowoff + coloff[v] : 0;
+          ir[v] = ok ? __ldg(reinterpret_cast<const uint32_t*>(isrc + off)) : 0xFFFFFFFFu;
+          dr[v] = ok ? __ldg(reinterpret_cast<const float4*>(dsrc + off)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      };
+#pragma unroll
+      for (int u = 0; u < K; ++u) load_row(u, id[u], d[u]);
+      float* dst = a.din + ((size_t)g * a.gr * a.gc) * C + cv * 4;
+#pragma unroll
+      for (int ea = 0; ea < K; ++ea) {
+        const int Y = K * bi + ea;
+#pragma unroll
+        for (int eb = 0; eb < BW; ++eb) {
+          const int X = BW * bj + eb;
+          if (Y >= a.gr || X >= a.gc) continue;
+          float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int dy = 0; dy < K; ++dy)
+#pragma unroll
+            for (int dx = 0; dx < K; ++dx) {
+              const int u = ea - dy + K - 1, v = eb - dx + K - 1;  // patch row / column
+              const uint32_t x = id[u % K][v] ^ ((uint32_t)(dy * K + dx) * 0x01010101u);
+              const float4 w = d[u % K][v];
+              if (!(x & 0xFFu)) acc[0] += w.x;
+              if (!(x & 0xFF00u)) acc[1] += w.y;
+              if (!(x & 0xFF0000u)) acc[2] += w.z;
+              if (!(x & 0xFF000000u)) acc[3] += w.w;
+            }
+          float o[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            bsum[q] += acc[q];
+            o[q] = a.round_tf32 ? tf32_rna(acc[q]) : acc[q];
+          }
+          stv<4>(dst + (Y * a.gc + X) * C, o);
+        }
+        if (ea + K < 2 * K - 1) load_row(ea + K, id[(ea + K) % K], d[(ea + K) % K]);  // replaces patch row ea
+      }
+    }
+  }
+  if (a.bias_part == nullptr) return;
+  if (sub < nsub) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) s_red3[sub * C + cv * 4 + q] = bsum[q];
+  }
+  __syncthreads();
+  if (tid < CV) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float t = 0.f;
+      for (int q2 = 0; q2 < nsub; ++q2) t += s_red3[q2 * C + tid * 4 + q];
+      a.bias_part[(size_t)blockIdx.x * C + tid * 4 + q] = t;
+    }
+  }
+}
+
 // ----------------------------------------------------------------------------- channel sums
 // Generic per-channel partials of a [P][C] tensor (bias gradient of a conv whose delta
 // comes from a dgrad, i.e. a conv followed by another conv).
@@ -748,13 +848,19 @@ cudaError_t launch_mpf_fwd(const MpfArgs& a, cudaStream_t s) {
   return fwd_dispatch<1>(a, s);
 }
 
-// k = 2 register-blocked gather (default for k = 2; MPF_BWD_TILE2=1 keeps the tiled kernel)
+// k = 2, 3 register-blocked gathers (default; MPF_BWD_TILE2=1 keeps the tiled kernel)
 static bool bwd_block2(const MpfBwdArgs& a) {
-  return a.premul && a.k == 2 && a.C % 4 == 0 && a.C <= 1024 && !getenv("MPF_BWD_SLIDE") && !getenv("MPF_BWD_TILE2");
+  return a.premul && (a.k == 2 || a.k == 3) && a.C % 4 == 0 && a.C <= 1024 && !getenv("MPF_BWD_SLIDE") &&
+         !getenv("MPF_BWD_TILE2");
+}
+static int block3_bw() {
+  static const int bw = getenv("MPF_BWD_BW3") ? atoi(getenv("MPF_BWD_BW3")) : 3;
+  return bw == 1 ? 1 : 3;
 }
 static long long block2_groups(const MpfBwdArgs& a) {
   const int nsub = 256 / (a.C / 4);
-  const long long bj_n = (a.gc + 1) / 2, bi_n = (a.gr + 1) / 2;
+  const int bw = a.k == 2 ? 2 : block3_bw();
+  const long long bj_n = (a.gc + bw - 1) / bw, bi_n = (a.gr + a.k - 1) / a.k;
   return (long long)a.n_frag_in * bi_n * ((bj_n + nsub - 1) / nsub);
 }
 static int block2_grid(const MpfBwdArgs& a) {
@@ -850,7 +956,9 @@ long long mpf_bwd_partials(const MpfBwdArgs& a) {
 cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s) {
   if (bwd_block2(a)) {
     const size_t smem = sizeof(float) * (256 / (a.C / 4)) * a.C;
-    mpf_bwd_block2_kernel<<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
+    if (a.k == 2) mpf_bwd_block2_kernel<<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
+    else if (block3_bw() == 3) mpf_bwd_block3_kernel<3><<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
+    else mpf_bwd_block3_kernel<1><<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
     return cudaGetLastError();
   }
   const int V = a.C % 4 == 0 ? 4 : 1;
