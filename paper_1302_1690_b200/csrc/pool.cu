@@ -697,9 +697,9 @@ __global__ void __launch_bounds__(256) mpf_bwd_block2_kernel(MpfBwdArgs a, long 
 // rows 0-2 are loaded up front, row ea+3 after output row ea.  BW = 1 (MPF_BWD_BW3=1: 45 window
 // registers) or 3 (default: fewer loads per element; measured 1.84 vs 2.75 ms on cfg5).
 // Same fixed (dy, dx) order as the other MPF backward kernels (bitwise-identical results).
-template <int BW>  // block width in output columns (3: 5 x 5 patch; 1: 5 x 3 patch, fewer registers)
+template <int K, int BW>  // k and block width in output columns (patch (2k-1) x (BW+k-1))
 __global__ void __launch_bounds__(256) mpf_bwd_block3_kernel(MpfBwdArgs a, long long n_groups) {
-  constexpr int K = 3, PW = BW + K - 1;
+  constexpr int PW = BW + K - 1;
   extern __shared__ float s_red3[];  // [256 / CV][C]
   const int C = a.C, CV = C / 4;
   const int tid = threadIdx.x, cv = tid % CV, sub = tid / CV, nsub = 256 / CV;
@@ -957,8 +957,8 @@ cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s) {
   if (bwd_block2(a)) {
     const size_t smem = sizeof(float) * (256 / (a.C / 4)) * a.C;
     if (a.k == 2) mpf_bwd_block2_kernel<<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
-    else if (block3_bw() == 3) mpf_bwd_block3_kernel<3><<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
-    else mpf_bwd_block3_kernel<1><<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
+    else if (block3_bw() == 3) mpf_bwd_block3_kernel<3, 3><<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
+    else mpf_bwd_block3_kernel<3, 1><<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
     return cudaGetLastError();
   }
   const int V = a.C % 4 == 0 ? 4 : 1;
