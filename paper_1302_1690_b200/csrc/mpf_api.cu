@@ -182,6 +182,7 @@ static void layout_memory(Net* N, int n) {
   N->off_Y = s; s = align256(s + sizeof(float) * maxY);
   N->off_dA = s; s = align256(s + sizeof(float) * maxD);
   N->off_dB = s; s = align256(s + sizeof(float) * maxD);
+  N->off_dC = s; s = align256(s + sizeof(float) * maxD);  // third delta buffer (overlapped wgrads)
   // weight packs
   N->off_wpack = s;
   long long wp = 0;
@@ -299,6 +300,13 @@ mpf_status mpf_net_create(const mpf_config* cfg, const mpf_layer* layers, int32_
 void mpf_net_destroy(mpf_net* net) {
   if (!net) return;
   for (cudaEvent_t e : net->prof.ev) cudaEventDestroy(e);
+  if (net->side_stream) {
+    cudaStreamSynchronize(net->side_stream);
+    cudaStreamDestroy(net->side_stream);
+    cudaEventDestroy(net->ev_ready);
+    cudaEventDestroy(net->ev_join);
+    for (int i = 0; i < 3; ++i) cudaEventDestroy(net->ev_buf[i]);
+  }
   if (net->copy_stream) {
     cudaStreamSynchronize(net->copy_stream);
     cudaStreamDestroy(net->copy_stream);
@@ -642,8 +650,37 @@ static mpf_status backward_impl(Net* N, const uint8_t* d_labels, const float* h_
   // head: dL/dx_hat first, dh, and the softmax FC's gradient + the
   // previous layer's bias gradient as block partials
   const Act& h = N->a[L];
-  float* dcur = scr(N, N->off_dA);
-  float* dother = scr(N, N->off_dB);
+  // Delta buffers rotate among three; a layer's weight gradient reads its delta on the
+  // side stream while the main stream continues with the dgrad and the MPF backward
+  // below it.  Before a producer overwrites a buffer, the main stream waits for the
+  // weight gradient that read it (two producers later).
+  float* dbuf[3] = {scr(N, N->off_dA), scr(N, N->off_dB), scr(N, N->off_dC)};
+  bool pending[3] = {false, false, false};
+  int ci = 0;  // dbuf[ci] holds the current delta
+  float* dcur = dbuf[0];
+  float* dother = dbuf[1];
+  const bool side = !getenv("MPF_NO_SIDE_STREAM");
+  if (side && !N->side_stream) {
+    MPF_CUDA(cudaStreamCreateWithFlags(&N->side_stream, cudaStreamNonBlocking));
+    MPF_CUDA(cudaEventCreateWithFlags(&N->ev_ready, cudaEventDisableTiming));
+    MPF_CUDA(cudaEventCreateWithFlags(&N->ev_join, cudaEventDisableTiming));
+    for (int i = 0; i < 3; ++i) MPF_CUDA(cudaEventCreateWithFlags(&N->ev_buf[i], cudaEventDisableTiming));
+  }
+  cudaStream_t sw = side ? N->side_stream : s;
+  // the next producer writes dbuf[(ci + 1) % 3]: make sure no weight gradient still reads it
+  auto next_out = [&]() -> float* {
+    const int b = (ci + 1) % 3;
+    if (pending[b]) {
+      cudaStreamWaitEvent(s, N->ev_buf[b], 0);
+      pending[b] = false;
+    }
+    return dbuf[b];
+  };
+  auto advance = [&]() {
+    ci = (ci + 1) % 3;
+    dcur = dbuf[ci];
+  };
+  dother = next_out();
   HeadArgs hd{};
   hd.h = act_ptr(N, L);
   hd.gr = h.gr; hd.gc = h.gc; hd.vr = h.vr; hd.vc = h.vc; hd.Ch = h.C; hd.F = h.F;
@@ -723,7 +760,8 @@ static mpf_status backward_impl(Net* N, const uint8_t* d_labels, const float* h_
       mpf_status st = bias_reduce(N, l - 1, bpart, mpf_bwd_partials(m), s);
       if (st != MPF_OK) return st;
       bias_done = true;
-      std::swap(dcur, dother);
+      advance();
+      dother = next_out();
       continue;
     }
     if (!bias_done) {  // delta came from a dgrad (conv followed by conv)
@@ -735,8 +773,16 @@ static mpf_status backward_impl(Net* N, const uint8_t* d_labels, const float* h_
     }
     bias_done = false;
     const float* x = (l == 0) ? N->images : act_ptr(N, l);
-    mpf_status st = wgrad(N, l, x, dcur, n, s);
+    if (sw != s) {  // the weight gradient of layer l on the side stream, after dcur is ready
+      MPF_CUDA(cudaEventRecord(N->ev_ready, s));
+      MPF_CUDA(cudaStreamWaitEvent(sw, N->ev_ready, 0));
+    }
+    mpf_status st = wgrad(N, l, x, dcur, n, sw);
     if (st != MPF_OK) return st;
+    if (sw != s) {
+      MPF_CUDA(cudaEventRecord(N->ev_buf[ci], sw));
+      pending[ci] = true;
+    }
     if (l == 0) break;
     // dgrad: delta of a[l] = full correlation of dcur with the rotated kernel.  When a[l]
     // is a pooled tensor, the epilogue already multiplies by act'(pooled value) of the conv
@@ -782,7 +828,12 @@ static mpf_status backward_impl(Net* N, const uint8_t* d_labels, const float* h_
       LAUNCH(N, s, "dgrad_simt", l, dflops, dbytes, launch_conv_simt(c, s));
     }
     premul = in_is_pool;
-    std::swap(dcur, dother);
+    advance();
+    dother = next_out();
+  }
+  if (sw != s) {  // the gradients are complete when the side stream is
+    MPF_CUDA(cudaEventRecord(N->ev_join, sw));
+    MPF_CUDA(cudaStreamWaitEvent(s, N->ev_join, 0));
   }
   return MPF_OK;
 }

@@ -65,13 +65,16 @@ struct Net {
   // memory plan for n_cap images (bytes)
   int n_cap = 0;
   size_t tape_bytes = 0, scratch_bytes = 0;
-  size_t off_Y = 0, off_dA = 0, off_dB = 0, off_bpart = 0, off_wpack = 0, off_part = 0,
+  size_t off_Y = 0, off_dA = 0, off_dB = 0, off_dC = 0, off_bpart = 0, off_wpack = 0, off_part = 0,
          off_nlab = 0, off_lossp = 0, off_err = 0, off_rowloss = 0, off_stage_img = 0, off_stage_lab = 0,
          off_stage_loss = 0;
   size_t stage_bytes = 0;  // one of the two host-input staging slots (images | labels)
   // host-buffer steps: inputs of step i + 1 are copied on copy_stream into the other
   // staging slot while step i computes (events order the slots' reuse)
   cudaStream_t copy_stream = nullptr;
+  // backward: weight gradients run on side_stream, overlapping the dgrad / MPF-backward chain
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t ev_ready = nullptr, ev_join = nullptr, ev_buf[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   int stage_slot = 0;
   size_t part_floats = 0;  // capacity of the wgrad partial buffer (floats)

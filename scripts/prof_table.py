@@ -8,7 +8,8 @@ for path in sys.argv[1:]:
     d = json.load(open(path))
     ks = sorted(d["kernels"], key=lambda r: -r["total_ms"])
     tot = sum(r["total_ms"] for r in ks)
-    print(f"{path}: step {d['step_ms']:.3f} ms, kernels sum {tot / max(1, ks[0]['launches']):.3f} ms/step")
+    ov = f", overlapped step {d['overlapped_step_ms']:.3f} ms" if "overlapped_step_ms" in d else ""
+    print(f"{path}: step {d['step_ms']:.3f} ms{ov}, kernels sum {tot / max(1, ks[0]['launches']):.3f} ms/step")
     for r in ks[:int(sys.argv[0] and 30)]:
         ms = r["total_ms"] / r["launches"]
         fl = r["flops"] / ms / 1e9 if r["flops"] else 0
