@@ -422,6 +422,20 @@ mpf_status mpf_net_bind(mpf_net* N, void* p, void* g, void* t, void* s, int32_t 
   return MPF_OK;
 }
 
+// The side stream (and its events) used to overlap independent work with the main chain:
+// weight packs in the forward, weight gradients in the backward.  MPF_NO_SIDE_STREAM=1
+// serialises everything on the caller's stream.
+static cudaStream_t side_stream(Net* N, cudaStream_t s) {
+  if (getenv("MPF_NO_SIDE_STREAM")) return s;
+  if (!N->side_stream) {
+    if (cudaStreamCreateWithFlags(&N->side_stream, cudaStreamNonBlocking) != cudaSuccess) return s;
+    cudaEventCreateWithFlags(&N->ev_ready, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&N->ev_join, cudaEventDisableTiming);
+    for (int i = 0; i < 3; ++i) cudaEventCreateWithFlags(&N->ev_buf[i], cudaEventDisableTiming);
+  }
+  return N->side_stream;
+}
+
 // Is the softmax head fused into the forward of the last hidden layer (mpf_train_step)?
 static bool head_fusable(const Net* N) {
   const int L = N->n_layers - 1;
@@ -437,7 +451,14 @@ static mpf_status forward_impl(Net* N, const float* d_images, int n, float* d_pr
                                const TcHeadArgs* hf, int* head_grid) {
   const bool tf32 = N->cfg.precision == MPF_PREC_TF32;
   float* wpack = scr(N, N->off_wpack);
-  // 1. weight packs (tf32-rounded for the tensor-core path)
+  // 1. weight packs (tf32-rounded for the tensor-core path), on the side stream: the first
+  // layer reads the canonical weights, so the packs overlap with it and its pool
+  cudaStream_t sp = side_stream(N, s);
+  if (sp != s) {
+    MPF_CUDA(cudaEventRecord(N->ev_ready, s));  // parameters of this step are final
+    MPF_CUDA(cudaStreamWaitEvent(sp, N->ev_ready, 0));
+  }
+  bool packs_joined = sp == s;
   for (int l = 0; l < N->n_layers; ++l) {
     const LayerPlan& P = N->lp[l];
     if (P.L.kind == MPF_POOL) continue;
@@ -445,10 +466,11 @@ static mpf_status forward_impl(Net* N, const float* d_images, int n, float* d_pr
     // tf32-round a pack only when a tensor-core kernel consumes it; CUDA-core convs use fp32
     const int rf = (l > 0 && l < N->n_layers - 1 && use_tc(N, P, false)) ? 1 : 0;
     const int rd = (l > 0 && use_tc(N, P, true)) ? 1 : 0;
-    LAUNCH(N, s, "pack_weights", l, 0.0, 12.0 * nw,
+    LAUNCH(N, sp, "pack_weights", l, 0.0, 12.0 * nw,
            launch_pack_weights(N->params + P.w_off, P.cout, P.cin, P.L.k, wpack + P.wpack_off,
-                               wpack + P.dpack_off, rf, rd, s));
+                               wpack + P.dpack_off, rf, rd, sp));
   }
+  if (sp != s) MPF_CUDA(cudaEventRecord(N->ev_join, sp));
   // 2. layers (Alg. 1; Alg. 3 for MPF)
   for (int l = 0; l < N->n_layers - 1; ++l) {
     const LayerPlan& P = N->lp[l];
@@ -456,6 +478,12 @@ static mpf_status forward_impl(Net* N, const float* d_images, int n, float* d_pr
     const Act& o = N->a[l + 1];
     // the consumer of this output rounds? (TF32 operand of a tensor-core conv)
     // (the tensor-core softmax head counts: it reads h as TF32 MMA operand)
+    const bool first_simt = l == 0 && first_conv_supported(N->cfg.in_channels, P.cout, P.L.k) &&
+                            !getenv("MPF_DISABLE_FIRST");  // reads the canonical weights
+    if (!packs_joined && P.L.kind != MPF_POOL && !first_simt) {  // the first consumer of a pack
+      MPF_CUDA(cudaStreamWaitEvent(s, N->ev_join, 0));
+      packs_joined = true;
+    }
     const bool next_tc = ((l + 1 < N->n_layers - 1) && N->lp[l + 1].L.kind != MPF_POOL && use_tc(N, N->lp[l + 1], false)) ||
                          (l + 1 == N->n_layers - 1 && head_tc_used(N));
     if (P.L.kind == MPF_POOL) {
@@ -534,6 +562,7 @@ static mpf_status forward_impl(Net* N, const float* d_images, int n, float* d_pr
       }
     }
   }
+  if (!packs_joined) MPF_CUDA(cudaStreamWaitEvent(s, N->ev_join, 0));  // the backward reads the packs
   N->images = d_images;
   N->n_fwd = n;
   N->have_fwd = !hf;  // a fused step has no standalone backward
@@ -659,14 +688,7 @@ static mpf_status backward_impl(Net* N, const uint8_t* d_labels, const float* h_
   int ci = 0;  // dbuf[ci] holds the current delta
   float* dcur = dbuf[0];
   float* dother = dbuf[1];
-  const bool side = !getenv("MPF_NO_SIDE_STREAM");
-  if (side && !N->side_stream) {
-    MPF_CUDA(cudaStreamCreateWithFlags(&N->side_stream, cudaStreamNonBlocking));
-    MPF_CUDA(cudaEventCreateWithFlags(&N->ev_ready, cudaEventDisableTiming));
-    MPF_CUDA(cudaEventCreateWithFlags(&N->ev_join, cudaEventDisableTiming));
-    for (int i = 0; i < 3; ++i) MPF_CUDA(cudaEventCreateWithFlags(&N->ev_buf[i], cudaEventDisableTiming));
-  }
-  cudaStream_t sw = side ? N->side_stream : s;
+  cudaStream_t sw = side_stream(N, s);
   // the next producer writes dbuf[(ci + 1) % 3]: make sure no weight gradient still reads it
   auto next_out = [&]() -> float* {
     const int b = (ci + 1) % 3;
