@@ -975,7 +975,7 @@ struct WgTcParams {
   uint32_t tmem_cols;
 };
 
-template <int dummy>
+template <int MT>  // output channels per tile: 128, or 64 (M = 64 MMA) when C_out <= 64
 __global__ void __launch_bounds__(kThreads, 1)
     wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX, WgTcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1021,8 +1021,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_arrive_expect_tx(barFull + 8 * slot, p.a_bytes + G * p.b_bytes);
         const uint32_t sa = sbase + slot * p.stage_bytes;
         const int row = (int)(pbeg + (long long)st * kWR);
-        for (int j = 0; j < 4; ++j)  // 4 atoms of 32 output channels
-          ptx::tma_load_2d(sa + j * kWR * 128, &tmD, barFull + 8 * slot, mt * 128 + j * 32, row);
+        for (int j = 0; j < MT / 32; ++j)  // atoms of 32 output channels
+          ptx::tma_load_2d(sa + j * kWR * 128, &tmD, barFull + 8 * slot, mt * MT + j * 32, row);
         for (int g = 0; g < G; ++g) {
           const int ng = g0 + g, ky = ng / p.n_cc, cc = ng % p.n_cc;
           ptx::tma_load_2d(sa + p.a_bytes + g * p.b_bytes, &tmX, barFull + 8 * slot, cc * kKC, row + ky * p.gc);
@@ -1030,7 +1030,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    const uint32_t idesc = ptx::idesc_tf32_mn(128, N);
+    const uint32_t idesc = ptx::idesc_tf32_mn(MT, N);
     for (int st = 0; st < n_st; ++st) {
       const int slot = st % p.n_stages_ring;
       ptx::mbar_wait(barFull + 8 * slot, (st / p.n_stages_ring) & 1);
@@ -1050,18 +1050,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     ptx::mma_commit_elect(barT);
   } else {
-    const int q = warp & 3;
-    const int co = mt * 128 + q * 32 + lane;
+    // TMEM lane quarter q; with M = 64 the accumulator rows sit in lanes 0-15 of each
+    // quarter (row r -> lane 32 (r / 16) + r % 16).  The two warps of a quarter split the
+    // 16-column chunks.
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    const int co = MT == 128 ? mt * 128 + q * 32 + lane : mt * 64 + q * 16 + lane;
+    const bool row_ok = (MT == 128 || lane < 16) && co < p.cout;
     ptx::mbar_wait(barT, 0);
     ptx::tc_fence_after();
     const int K = p.k * p.k * p.cin;
-    float* dst = p.part + ((long long)split * p.cout + co) * K;
+    float* dst = p.part + ((long long)split * p.cout + (row_ok ? co : 0)) * K;
     for (int g = 0; g < G; ++g) {
       const int ng = g0 + g, ky = ng / p.n_cc, cc = ng % p.n_cc;
-      for (int c0 = 0; c0 < N; c0 += 16) {
+      for (int c0 = half * 16; c0 < N; c0 += 32) {
         float v[16];
         ptx::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + g * N + c0, v);
-        if (co < p.cout) {
+        if (row_ok) {
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int n = c0 + j, kx = n / 32, ci = cc * kKC + (n % 32);
@@ -1118,8 +1122,9 @@ cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits_out, cudaStream_t 
   p.G = 512 / N;
   if (p.G > p.n_groups) p.G = p.n_groups;
   p.n_sets = (p.n_groups + p.G - 1) / p.G;
-  p.m_tiles = (a.cout + 127) / 128;
-  p.a_bytes = 4 * kWR * 128;
+  const int MT = (a.cout <= 64 && !getenv("MPF_WGRAD_M128")) ? 64 : 128;
+  p.m_tiles = (a.cout + MT - 1) / MT;
+  p.a_bytes = (MT / 32) * kWR * 128;
   p.b_bytes = (kWR + 8) * 128;
   p.stage_bytes = p.a_bytes + p.G * p.b_bytes;
   const size_t budget = 225 * 1024 - 1024 - 256;
@@ -1153,9 +1158,10 @@ cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits_out, cudaStream_t 
   e = make_map(&X, a.x, (uint64_t)a.cin, (uint64_t)p.P_tot, (uint32_t)(kWR + 8), CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   if (e != cudaSuccess) return e;
   const size_t smem = 1024 + (size_t)p.n_stages_ring * p.stage_bytes + 256;
-  e = cudaFuncSetAttribute(wgrad_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = MT == 64 ? wgrad_tc_kernel<64> : wgrad_tc_kernel<128>;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  wgrad_tc_kernel<0><<<splits * per_split_blocks, kThreads, smem, s>>>(D, X, p);
+  kern<<<splits * per_split_blocks, kThreads, smem, s>>>(D, X, p);
   return cudaGetLastError();
 }
 

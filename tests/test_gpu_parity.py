@@ -368,6 +368,16 @@ def test_cta_pair_matches_single_cta_mma():
         assert rel_l2(a["grad_sum"][sl], b["grad_sum"][sl]) <= 1e-5, nm
 
 
+def test_wgrad_m64_matches_m128():
+    """Weight gradients of layers with C_out <= 64 use M = 64 MMAs (accumulator rows in
+    lanes 0-15 of each TMEM quarter); forcing M = 128 (MPF_WGRAD_M128=1) computes the same
+    sums in the same order."""
+    cfg, a = _run_variant({})
+    _, b = _run_variant({"MPF_WGRAD_M128": "1"})
+    for nm, sl in param_slices(cfg.layers):
+        assert rel_l2(a["grad_sum"][sl], b["grad_sum"][sl]) <= 1e-6, nm
+
+
 @pytest.mark.parametrize("name", ["cfg2", "cfg5s"])
 def test_mpf_backward_tiled_equals_sliding_bitwise(name):
     """Shared-memory tiled and register-sliding MPF backward gather the same candidates in
