@@ -257,8 +257,11 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
           const float inv = nl > 0 ? wt / (float)nl : 0.f;
 #pragma unroll
           for (int c = 0; c < NC; ++c)
-            if ((c & 3) == qa)
-              s_dl[pa * kNCP + c] = (c < C) ? inv * (expf(z[c] - lse) - (c == lab ? 1.f : 0.f)) : 0.f;
+            if ((c & 3) == qa) {
+              const float dz = (c < C) ? inv * (expf(z[c] - lse) - (c == lab ? 1.f : 0.f)) : 0.f;
+              s_dl[pa * kNCP + c] = dz;
+              accL[c] += dz;  // db_L: this lane owns class c of its positions
+            }
         }
       }
     }
@@ -294,11 +297,7 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
 #pragma unroll
           for (int c = 0; c < NC; ++c) dl[c] = 0.f;
         }
-        if (act && lane == 0 && !(pairB && (warp & 1))) {
-#pragma unroll
-          for (int c = 0; c < NC; ++c) accL[c] += dl[c];
-        }
-        float* dh_row = dh_img + (long long)p * Ch;
+        float* dh_row = dh_img + p * Ch;  // 32-bit offset: a tile is far below 2^31 elements
         if (!act) {  // warp-uniform: padding position or ignored label -> zero delta
           if (VEC) {
             if (4 * gB < Ch) reinterpret_cast<float4*>(dh_row)[gB] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -392,6 +391,12 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
     }
   }
   float* redL = red + (kThr / 32) * Ch * RW;
+  // db_L: class c was accumulated by the lanes with (lane & 3) == (c & 3); fixed-order
+  // butterfly over the lanes (the other lanes hold zeros for c)
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) accL[c] += __shfl_xor_sync(0xffffffffu, accL[c], o);
   if (lane == 0) {
 #pragma unroll
     for (int c = 0; c < NC; ++c)
@@ -411,8 +416,7 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
         if (own < 0 || (q & 1) == own) s += red[(q * Ch + ch) * RW + c];
     } else if (e < C * Ch + C) {
       const int c = e - C * Ch;
-      for (int q = 0; q < kThr / 32; ++q)
-        if (!pairB || (q & 1) == 0) s += redL[q * kMaxC + c];
+      for (int q = 0; q < kThr / 32; ++q) s += redL[q * kMaxC + c];
     } else {
       const int ch = e - C * Ch - C;
       const int own = pairB ? (ch / 4) / 32 : -1;
