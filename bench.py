@@ -158,7 +158,7 @@ def run_reference(args, cfg, rank, world):
     v = tot / dt
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload_config(cfg, world),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
                              "sample": f"each step: O1 fp64 patch-by-patch fwd+bwd on {per_step} random output "
@@ -354,7 +354,7 @@ def main():
         any_tc = any(r["name"].endswith("_tc") for r in stats)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "tf32" if any_tc else "f32",
+                "scaling": "strong", "vs_baseline": None, "dtype": "tf32" if any_tc else "f32",
                 "data": "synthetic (seeded steel-like images, BASELINE.json shapes)",
                 "config": workload_config(cfg, world), "e2e": e2e, "gpu_launches": launches,
                 "roofline": roof, "cpu_baseline": cpu, "clocks": clocks}
