@@ -239,7 +239,7 @@ def main():
     # One CUDA graph per input pool (the step's ~170 launches, its side-stream fork/join and
     # the gradient allreduce replayed as one launch); eager launches if capture fails.
     graphs = None
-    if not args.no_graph:
+    if not args.no_graph and world == 1:  # (multi-rank: eager, NCCL calls stay outside capture)
         try:
             graphs = []
             for b in range(2):
