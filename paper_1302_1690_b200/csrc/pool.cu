@@ -609,7 +609,6 @@ __global__ void __launch_bounds__(256) mpf_bwd_tile_kernel(MpfBwdArgs a, int row
 // the other MPF backward kernels (bitwise-identical results).  No shared-memory staging,
 // no barriers; CTAs stride over groups of consecutive blocks of one row.
 __global__ void __launch_bounds__(256) mpf_bwd_block2_kernel(MpfBwdArgs a, long long n_groups) {
-  extern __shared__ float s_red2[];  // [256 / CV][C]
   const int C = a.C, CV = C / 4;
   const int tid = threadIdx.x, cv = tid % CV, sub = tid / CV, nsub = 256 / CV;
   const int Xw = 2 * a.m_c, Yw = 2 * a.m_r;
@@ -675,20 +674,12 @@ __global__ void __launch_bounds__(256) mpf_bwd_block2_kernel(MpfBwdArgs a, long 
         }
     }
   }
-  if (a.bias_part == nullptr) return;
-  if (sub < nsub) {
+  // bias partials: one row per (CTA, thread group), summed by the fixed-order reduction
+  // kernel.  No shared memory, so a CTA fits beside a tensor-core CTA on an SM (the weight
+  // gradients run concurrently on the side stream).
+  if (a.bias_part == nullptr || sub >= nsub) return;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) s_red2[sub * C + cv * 4 + q] = bsum[q];
-  }
-  __syncthreads();
-  if (tid < CV) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      float t = 0.f;
-      for (int q2 = 0; q2 < nsub; ++q2) t += s_red2[q2 * C + tid * 4 + q];
-      a.bias_part[(size_t)blockIdx.x * C + tid * 4 + q] = t;
-    }
-  }
+  for (int q = 0; q < 4; ++q) a.bias_part[((size_t)blockIdx.x * nsub + sub) * C + cv * 4 + q] = bsum[q];
 }
 
 // Register-blocked gather for k = 3: a thread owns a 3 x BW block of conv-output elements of
@@ -700,7 +691,6 @@ __global__ void __launch_bounds__(256) mpf_bwd_block2_kernel(MpfBwdArgs a, long 
 template <int K, int BW>  // k and block width in output columns (patch (2k-1) x (BW+k-1))
 __global__ void __launch_bounds__(256) mpf_bwd_block3_kernel(MpfBwdArgs a, long long n_groups) {
   constexpr int PW = BW + K - 1;
-  extern __shared__ float s_red3[];  // [256 / CV][C]
   const int C = a.C, CV = C / 4;
   const int tid = threadIdx.x, cv = tid % CV, sub = tid / CV, nsub = 256 / CV;
   const int Xw = K * a.m_c, Yw = K * a.m_r;
@@ -775,20 +765,12 @@ __global__ void __launch_bounds__(256) mpf_bwd_block3_kernel(MpfBwdArgs a, long 
       }
     }
   }
-  if (a.bias_part == nullptr) return;
-  if (sub < nsub) {
+  // bias partials: one row per (CTA, thread group), summed by the fixed-order reduction
+  // kernel.  No shared memory, so a CTA fits beside a tensor-core CTA on an SM (the weight
+  // gradients run concurrently on the side stream).
+  if (a.bias_part == nullptr || sub >= nsub) return;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) s_red3[sub * C + cv * 4 + q] = bsum[q];
-  }
-  __syncthreads();
-  if (tid < CV) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      float t = 0.f;
-      for (int q2 = 0; q2 < nsub; ++q2) t += s_red3[q2 * C + tid * 4 + q];
-      a.bias_part[(size_t)blockIdx.x * C + tid * 4 + q] = t;
-    }
-  }
+  for (int q = 0; q < 4; ++q) a.bias_part[((size_t)blockIdx.x * nsub + sub) * C + cv * 4 + q] = bsum[q];
 }
 
 // ----------------------------------------------------------------------------- channel sums
@@ -947,7 +929,7 @@ static void bwd_geometry(const MpfBwdArgs& a, int V, dim3* grid, dim3* blk) {
 }
 
 long long mpf_bwd_partials(const MpfBwdArgs& a) {
-  if (bwd_block2(a)) return block2_grid(a);
+  if (bwd_block2(a)) return (long long)block2_grid(a) * (256 / (a.C / 4));
   dim3 g, b;
   bwd_geometry(a, a.C % 4 == 0 ? 4 : 1, &g, &b);
   return (long long)g.x * g.y * g.z;
@@ -955,7 +937,7 @@ long long mpf_bwd_partials(const MpfBwdArgs& a) {
 
 cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s) {
   if (bwd_block2(a)) {
-    const size_t smem = sizeof(float) * (256 / (a.C / 4)) * a.C;
+    const size_t smem = 0;
     if (a.k == 2) mpf_bwd_block2_kernel<<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
     else if (block3_bw() == 3) mpf_bwd_block3_kernel<3, 3><<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
     else mpf_bwd_block3_kernel<3, 1><<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
