@@ -472,10 +472,15 @@ static mpf_status forward_impl(Net* N, const float* d_images, int n, float* d_pr
   }
   if (sp != s) MPF_CUDA(cudaEventRecord(N->ev_join, sp));
   // 2. layers (Alg. 1; Alg. 3 for MPF)
+  bool pool_done = false;  // the first layer's kernel already produced the MPF after it
   for (int l = 0; l < N->n_layers - 1; ++l) {
     const LayerPlan& P = N->lp[l];
     const Act& in = N->a[l];
     const Act& o = N->a[l + 1];
+    if (pool_done) {
+      pool_done = false;
+      continue;
+    }
     // the consumer of this output rounds? (TF32 operand of a tensor-core conv)
     // (the tensor-core softmax head counts: it reads h as TF32 MMA operand)
     const bool first_simt = l == 0 && first_conv_supported(N->cfg.in_channels, P.cout, P.L.k) &&
@@ -521,7 +526,23 @@ static mpf_status forward_impl(Net* N, const float* d_images, int n, float* d_pr
         f.w = N->params + P.w_off; f.bias = N->params + P.b_off; f.k = P.L.k; f.cout = P.cout;
         f.out = out; f.out_gr = o.gr; f.out_gc = o.gc; f.out_vr = o.vr; f.out_vc = o.vc;
         f.act = P.L.act; f.zero_pad = P.out_where == Where::Tape ? 1 : 0; f.round_tf32 = next_tc ? 1 : 0;
-        if (tf32 && first_conv_tc_ok(N->cfg.in_channels, P.cout, P.L.k))
+        const LayerPlan& Pn = N->lp[1];
+        if (P.out_where == Where::ScratchY && Pn.L.kind == MPF_POOL && !hf && N->n_layers > 2 &&
+            first_conv_mpf_supported(P.cout, P.L.k, Pn.L.k) && !(tf32 && first_conv_tc_ok(N->cfg.in_channels, P.cout, P.L.k))) {
+          // conv + activation + MPF (layer 1) in one kernel: the conv output is never stored
+          const Act& po = N->a[2];
+          MpfArgs m{};
+          m.y = nullptr;
+          m.gr = o.gr; m.gc = o.gc; m.vr = o.vr; m.vc = o.vc; m.C = o.C; m.k = Pn.L.k;
+          m.n_frag_in = n * o.F;
+          m.out = tape_val(N, 1);
+          m.idx = tape_idx(N, 1);
+          m.m_r = po.vr; m.m_c = po.vc;
+          m.round_tf32 = (2 < N->n_layers - 1 && use_tc(N, N->lp[2], false)) ? 1 : 0;
+          const double eout = (double)n * po.F * po.vr * po.vc * po.C;
+          LAUNCH(N, s, "conv_first_mpf", l, cflops, 4.0 * in_e + 5.0 * eout, launch_first_conv_mpf(f, m, s));
+          pool_done = true;
+        } else if (tf32 && first_conv_tc_ok(N->cfg.in_channels, P.cout, P.L.k))
           LAUNCH(N, s, "conv_first_fwd", l, cflops, cbytes, launch_first_conv_tc(f, s));
         else
           LAUNCH(N, s, "conv_first_fwd", l, cflops, cbytes, launch_first_conv(f, s));

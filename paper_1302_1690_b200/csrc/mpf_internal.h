@@ -150,6 +150,8 @@ struct MpfArgs {
   int round_tf32;
 };
 cudaError_t launch_mpf_fwd(const MpfArgs& a, cudaStream_t s);
+struct FirstConvArgs;
+cudaError_t launch_first_conv_mpf(const FirstConvArgs& a, const MpfArgs& m, cudaStream_t s);
 
 struct MpfBwdArgs {
   const float* dout;     // delta of the pooled output [n*F_in*k*k][m][m][C]
@@ -245,6 +247,8 @@ struct FirstWgradArgs {
   int n_cog;             // set by the launcher
 };
 bool first_conv_supported(int cin, int cout, int k);
+// first conv + activation + the MPF layer after it in one kernel (conv output never stored)
+bool first_conv_mpf_supported(int cout, int k, int pool_k);
 int first_wgrad_blocks();
 cudaError_t launch_first_conv(FirstConvArgs a, cudaStream_t s);
 cudaError_t launch_first_wgrad(FirstWgradArgs a, cudaStream_t s);

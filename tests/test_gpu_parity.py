@@ -368,6 +368,27 @@ def test_cta_pair_matches_single_cta_mma():
         assert rel_l2(a["grad_sum"][sl], b["grad_sum"][sl]) <= 1e-5, nm
 
 
+@pytest.mark.parametrize("name", ["cfg2", "cfg4s", "cfg5s"])
+def test_first_conv_mpf_fusion_bitwise(name):
+    """The fused first conv + activation + MPF kernel computes the conv
+    outputs and the pooling with exactly the arithmetic of the two separate kernels: the
+    whole training step (pooled values, argmaxes and everything downstream) is bitwise
+    identical with the fusion off (opt-in kernel: MPF_FIRST_FUSION=1)."""
+    import dataclasses
+    if name == "cfg4s":
+        S.CONFIGS["cfg4s"] = _cfg4s()
+    if name == "cfg5s":
+        S.CONFIGS["cfg5s"] = dataclasses.replace(S.CONFIGS["cfg5"], name="cfg5s", H=168, W=168)
+    try:
+        cfg, a = _run_variant({"MPF_FIRST_FUSION": "1"}, name=name)
+        _, b = _run_variant({}, name=name)
+    finally:
+        S.CONFIGS.pop(name, None) if name in ("cfg4s", "cfg5s") else None
+    assert np.array_equal(a["loss"], b["loss"])
+    assert np.array_equal(a["probs"], b["probs"])
+    assert np.array_equal(a["grad_sum"], b["grad_sum"])
+
+
 def test_wgrad_m64_matches_m128():
     """Weight gradients of layers with C_out <= 64 use M = 64 MMAs (accumulator rows in
     lanes 0-15 of each TMEM quarter); forcing M = 128 (MPF_WGRAD_M128=1) computes the same
