@@ -212,6 +212,19 @@ mpf_status mpf_debug_tape(const mpf_net* net, int32_t layer, int32_t what, void*
 mpf_status mpf_debug_scratch(const mpf_net* net, int32_t which, void* d_dst, uint64_t bytes, void* stream);
 
 /* Synchronise `stream` and report device-side data errors (bad labels) and CUDA errors. */
+/*
+ * Per-class loss weights from the labels ("loss function per class because of
+ * the unbalanced dataset"; the inverse-frequency rule of SURVEY §8(f) item 3):
+ *     w_c = N / (C * n_c),  n_c = labelled pixels of class c in d_labels[n][out_rows][out_cols]
+ *     (255 = ignored), N = sum_c n_c.
+ * Counts on the device (exact integer histogram), weights on the host in double, rounded to
+ * float into h_class_w[C]; optionally the counts into h_counts[C].  Synchronises `stream`.
+ * Errors: MPF_ERR_DATA if a class has no labelled pixel (pass explicit weights instead).
+ * The result is meant for mpf_backward_image / mpf_train_step's h_class_w.
+ */
+mpf_status mpf_class_weights_auto(const mpf_net* net, const uint8_t* d_labels, int32_t n, float* h_class_w,
+                                  uint64_t* h_counts, void* stream);
+
 mpf_status mpf_check(mpf_net* net, void* stream);
 
 /*

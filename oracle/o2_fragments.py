@@ -308,3 +308,17 @@ def train_image(layers, params, image, labels, class_w=None, P=None, in_channels
             Fd = new
     flat = np.concatenate([np.concatenate([g[0].ravel(), g[1]]) for g in grads if g is not None])
     return loss, n_lab, flat, probs
+
+
+def auto_class_weights(labels: np.ndarray, C: int) -> Tuple[np.ndarray, np.ndarray]:
+    """Per-class loss weights of the unbalanced-data MCCE (SURVEY §8(f) item 3,
+    the inverse-frequency rule w_c = N / (C n_c) of SPEC.md:417-421).  labels: any shape,
+    uint8, 255 = ignored.  Returns (weights fp64 [C], counts int [C]); raises on an
+    absent class."""
+    lab = np.asarray(labels).reshape(-1)
+    lab = lab[lab < C]
+    counts = np.bincount(lab.astype(np.int64), minlength=C)[:C]
+    if np.any(counts == 0):
+        raise ValueError("auto class weights: a class has no labelled pixel")
+    N = counts.sum()
+    return N / (C * counts.astype(np.float64)), counts

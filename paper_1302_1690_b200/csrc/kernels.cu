@@ -260,6 +260,31 @@ __global__ void label_count_kernel(const uint8_t* __restrict__ labels, int hw, i
   }
 }
 
+// per-class pixel counts over n label maps (255 and labels >= classes are not counted);
+// block histograms in shared memory, integer atomics (exact, order-independent)
+__global__ void class_hist_kernel(const uint8_t* __restrict__ labels, long long total, int classes,
+                                  unsigned long long* counts) {
+  __shared__ unsigned int s_h[256];
+  for (int c = threadIdx.x; c < 256; c += blockDim.x) s_h[c] = 0u;
+  __syncthreads();
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int l = labels[e];
+    if (l < classes) atomicAdd(&s_h[l], 1u);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < classes; c += blockDim.x)
+    if (s_h[c]) atomicAdd(counts + c, (unsigned long long)s_h[c]);
+}
+
+cudaError_t launch_class_hist(const uint8_t* labels, long long total, int classes, unsigned long long* counts,
+                              cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * classes, s);
+  if (e != cudaSuccess) return e;
+  const long long blocks = mpf_min_ll((total + 255) / 256, 148 * 8);
+  class_hist_kernel<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(labels, total, classes, counts);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_label_count(const uint8_t* labels, int n, int hw, int classes, int* nlab, cudaStream_t s) {
   cudaError_t e = cudaMemsetAsync(nlab, 0, sizeof(int) * n, s);
   if (e != cudaSuccess) return e;

@@ -984,6 +984,32 @@ mpf_status mpf_train_step_host(mpf_net* N, const float* h_images, const uint8_t*
   return MPF_OK;
 }
 
+mpf_status mpf_class_weights_auto(const mpf_net* N, const uint8_t* d_labels, int32_t n, float* h_class_w,
+                                  uint64_t* h_counts, void* stream) {
+  if (!N || !d_labels || !h_class_w) return fail(MPF_ERR_ARG, "NULL argument");
+  if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound");
+  if (n < 1) return fail(MPF_ERR_ARG, "n must be >= 1");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int C = N->classes;
+  // the counts go to the loss-partials region of the scratch (free between steps)
+  unsigned long long* d_counts = (unsigned long long*)(N->scratch + N->off_lossp);
+  if (sizeof(unsigned long long) * C > sizeof(float) * (size_t)N->loss_parts * N->n_cap)
+    return fail(MPF_ERR_INTERNAL, "scratch too small for the class histogram");
+  MPF_CUDA(launch_class_hist(d_labels, (long long)n * N->O_H * N->O_W, C, d_counts, s));
+  unsigned long long h[256];
+  MPF_CUDA(cudaMemcpyAsync(h, d_counts, sizeof(unsigned long long) * C, cudaMemcpyDeviceToHost, s));
+  MPF_CUDA(cudaStreamSynchronize(s));
+  unsigned long long tot = 0;
+  for (int c = 0; c < C; ++c) tot += h[c];
+  for (int c = 0; c < C; ++c) {
+    if (h_counts) h_counts[c] = h[c];
+    if (h[c] == 0)
+      return fail(MPF_ERR_DATA, "auto class weights: class " + std::to_string(c) + " has no labelled pixel");
+  }
+  for (int c = 0; c < C; ++c) h_class_w[c] = (float)((double)tot / ((double)C * (double)h[c]));
+  return MPF_OK;
+}
+
 mpf_status mpf_fragments_to_pixels(const mpf_net* N, const float* d_frag, float* d_pix, int32_t n, int32_t C,
                                    void* stream) {
   if (!N || !d_frag || !d_pix) return fail(MPF_ERR_ARG, "NULL argument");

@@ -192,6 +192,16 @@ class MPFNet:
                 "mpf_fragments_to_pixels")
         return out
 
+    def class_weights_auto(self, labels: torch.Tensor, stream=None):
+        """Inverse-frequency class weights w_c = N / (C n_c) of a batch of label maps
+        [n, out_rows, out_cols] (uint8, 255 ignored) and the per-class counts."""
+        C = self.geom.classes
+        w = (ctypes.c_float * C)()
+        cnt = (ctypes.c_uint64 * C)()
+        L.check(self.lib.mpf_class_weights_auto(self.h, _ptr(labels), int(labels.shape[0]), w, cnt,
+                                                _stream_ptr(stream)), "mpf_class_weights_auto")
+        return [float(v) for v in w], [int(v) for v in cnt]
+
     def debug_tape(self, layer: int, what: int, n: int) -> torch.Tensor:
         g = self.geom
         shape = (n * g.frag[layer + 1], g.rows[layer + 1], g.cols[layer + 1], g.chans[layer + 1])

@@ -499,3 +499,21 @@ def test_train_step_default_equals_forward_backward():
     g = gpu_step(cfg.layers, cfg.P, images, labels, params, "tf32")
     assert np.array_equal(loss_t, g["loss"])
     assert np.array_equal(grads_t, g["grad_sum"])
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg5s"])
+def test_auto_class_weights_vs_oracle(name):
+    """mpf_class_weights_auto (device histogram, host formula) against the oracle's plain
+    definition on the same labels: counts bit-exact, weights equal; an absent class is a
+    data error."""
+    import dataclasses
+    cfg = dataclasses.replace(S.CONFIGS["cfg5"], name="cfg5s", H=168, W=168) if name == "cfg5s" else S.CONFIGS[name]
+    images, labels = S.make_batch(cfg, list(range(8)))  # every class present in the batch
+    net = MPFNet(cfg.layers, cfg.P, cfg.H, cfg.W, max_images=8)
+    w, cnt = net.class_weights_auto(torch.tensor(labels, device="cuda"))
+    w_o, cnt_o = o2.auto_class_weights(labels, net.geom.classes)
+    assert cnt == [int(v) for v in cnt_o]
+    assert np.array_equal(np.array(w, dtype=np.float32), w_o.astype(np.float32))
+    with pytest.raises(MpfError) as e:
+        net.class_weights_auto(torch.full_like(torch.tensor(labels, device="cuda"), 0))
+    assert e.value.status == 3

@@ -404,3 +404,25 @@ def test_train_step_formula_and_determinism():
     np.testing.assert_allclose(r["params"], p - 0.01 * r["grad"], rtol=0, atol=0)
     r2 = oracle.train_step(cfg.layers, cfg.P, p, imgs, labs, lr=0.01, threads=3)
     assert np.array_equal(r["grad"], r2["grad"])  # bitwise reproducible
+
+
+def test_golden_auto_class_weights():
+    """SPEC.md:417-421 worked examples of the per-class MCCE weights."""
+    lines = golden_lines("class_weights.txt")
+    pairs = [(lines[i], lines[i + 1]) for i in range(0, len(lines), 2)]
+    for cl, wl in pairs:
+        counts = [int(v) for v in cl.split()[1:]]
+        want = [float(v) for v in wl.split()[1:]]
+        labels = np.concatenate([np.full(n, c, dtype=np.uint8) for c, n in enumerate(counts)] +
+                                [np.full(7, 255, dtype=np.uint8)])  # ignored pixels do not count
+        w, cnt = o2.auto_class_weights(labels, len(counts))
+        assert list(cnt) == counts
+        assert np.allclose(w, want, rtol=0, atol=1e-15)
+    # invariants: positive, finite, sum_c w_c n_c = N (the weighted class mass equals N / C each)
+    rng = np.random.default_rng(5)
+    lab = rng.integers(0, 5, size=(3, 17, 19)).astype(np.uint8)
+    w, cnt = o2.auto_class_weights(lab, 5)
+    assert np.all(w > 0) and np.all(np.isfinite(w))
+    assert np.allclose(w * cnt, cnt.sum() / 5)
+    with pytest.raises(ValueError):
+        o2.auto_class_weights(np.zeros(10, dtype=np.uint8), 2)
