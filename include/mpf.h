@@ -213,6 +213,19 @@ mpf_status mpf_debug_scratch(const mpf_net* net, int32_t which, void* d_dst, uin
 
 /* Synchronise `stream` and report device-side data errors (bad labels) and CUDA errors. */
 /*
+ * Mirror padding for same-size output ("pixels outside of the boundary of
+ * testing images are synthesized by mirroring -- which allows to preserve the size of the
+ * output").  d_in [planes][rows][cols] -> d_out [planes][out_rows]
+ * [out_cols], pixel (yp, xp) = d_in at the reflection of (yp - pad_top, xp - pad_left) about
+ * the border pixels, without repeating the edge (y < 0 -> -y, y >= rows -> 2(rows-1) - y;
+ * reading R20).  For a network of patch P, pad_top = pad_left = floor((P-1)/2) and
+ * out = in + P - 1 give an output grid of exactly rows x cols, output (y, x) being the patch
+ * centred (R7) on pixel (y, x).  Each pad must be smaller than the image.  Async on stream.
+ */
+mpf_status mpf_mirror_pad(const float* d_in, int32_t planes, int32_t rows, int32_t cols, int32_t pad_top,
+                          int32_t pad_left, int32_t out_rows, int32_t out_cols, float* d_out, void* stream);
+
+/*
  * Per-class loss weights from the labels ("loss function per class because of
  * the unbalanced dataset"; the inverse-frequency rule of SURVEY §8(f) item 3):
  *     w_c = N / (C * n_c),  n_c = labelled pixels of class c in d_labels[n][out_rows][out_cols]

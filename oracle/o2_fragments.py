@@ -322,3 +322,12 @@ def auto_class_weights(labels: np.ndarray, C: int) -> Tuple[np.ndarray, np.ndarr
         raise ValueError("auto class weights: a class has no labelled pixel")
     N = counts.sum()
     return N / (C * counts.astype(np.float64)), counts
+
+
+def mirror_pad(image: np.ndarray, P: int) -> np.ndarray:
+    """Same-size output: the image [..., H, W] mirror-padded by floor((P-1)/2)
+    before and P-1-floor((P-1)/2) after each spatial axis, reflecting about the border pixel
+    without repeating it (numpy's 'reflect' mode; reading R20)."""
+    pt = (P - 1) // 2
+    pads = [(0, 0)] * (image.ndim - 2) + [(pt, P - 1 - pt), (pt, P - 1 - pt)]
+    return np.pad(image, pads, mode="reflect")

@@ -241,6 +241,35 @@ cudaError_t launch_wgrad_reduce(const float* pw, const float* pb, int n_split, i
   return cudaGetLastError();
 }
 
+// ============================================================================ mirror padding
+// Same-size output ("pixels outside of the boundary of testing images are
+// synthesized by mirroring -- which allows to preserve the size of the output"): the
+// padded image's pixel (yp, xp) is the original pixel reflected about the border pixel
+// (no repeat of the edge; reading R20): y = yp - pad_top, y < 0 -> -y, y >= H -> 2(H-1) - y.
+// One thread per output float; rows are coalesced (reflection only at the two ends).
+__global__ void mirror_pad_kernel(const float* __restrict__ in, float* __restrict__ out, long long planes, int H, int W,
+                                  int pt, int pl, int Hp, int Wp) {
+  const long long total = planes * Hp * Wp;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int xp = (int)(e % Wp);
+    const long long t = e / Wp;
+    const int yp = (int)(t % Hp);
+    const long long pl_i = t / Hp;
+    int y = yp - pt, x = xp - pl;
+    y = y < 0 ? -y : (y >= H ? 2 * (H - 1) - y : y);
+    x = x < 0 ? -x : (x >= W ? 2 * (W - 1) - x : x);
+    out[e] = in[(pl_i * H + y) * W + x];
+  }
+}
+
+cudaError_t launch_mirror_pad(const float* in, float* out, long long planes, int H, int W, int pt, int pl, int Hp, int Wp,
+                              cudaStream_t s) {
+  const long long total = planes * Hp * Wp;
+  const long long blocks = mpf_min_ll((total + 255) / 256, 148 * 16);
+  mirror_pad_kernel<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(in, out, planes, H, W, pt, pl, Hp, Wp);
+  return cudaGetLastError();
+}
+
 // ============================================================================ small kernels
 // labelled pixels per image: integer partial counts combined with integer atomics
 // (exact, order-independent)

@@ -984,6 +984,19 @@ mpf_status mpf_train_step_host(mpf_net* N, const float* h_images, const uint8_t*
   return MPF_OK;
 }
 
+mpf_status mpf_mirror_pad(const float* d_in, int32_t planes, int32_t rows, int32_t cols, int32_t pad_top,
+                          int32_t pad_left, int32_t out_rows, int32_t out_cols, float* d_out, void* stream) {
+  if (!d_in || !d_out) return fail(MPF_ERR_ARG, "NULL argument");
+  if (planes < 1 || rows < 1 || cols < 1 || pad_top < 0 || pad_left < 0) return fail(MPF_ERR_ARG, "bad sizes");
+  const int pb = out_rows - rows - pad_top, pr = out_cols - cols - pad_left;
+  if (pb < 0 || pr < 0) return fail(MPF_ERR_ARG, "output smaller than input + leading pads");
+  if (pad_top >= rows || pad_left >= cols || pb >= rows || pr >= cols)
+    return fail(MPF_ERR_ARG, "a pad must be smaller than the image (single reflection)");
+  MPF_CUDA(launch_mirror_pad(d_in, d_out, planes, rows, cols, pad_top, pad_left, out_rows, out_cols,
+                             (cudaStream_t)stream));
+  return MPF_OK;
+}
+
 mpf_status mpf_class_weights_auto(const mpf_net* N, const uint8_t* d_labels, int32_t n, float* h_class_w,
                                   uint64_t* h_counts, void* stream) {
   if (!N || !d_labels || !h_class_w) return fail(MPF_ERR_ARG, "NULL argument");

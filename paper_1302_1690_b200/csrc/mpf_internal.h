@@ -208,6 +208,8 @@ int head_tc_grid(long long per_img, int n);
 cudaError_t launch_head_tc(const HeadArgs& a, cudaStream_t s);
 
 cudaError_t launch_label_count(const uint8_t* labels, int n, int hw, int classes, int* nlab, cudaStream_t s);
+cudaError_t launch_mirror_pad(const float* in, float* out, long long planes, int H, int W, int pt, int pl, int Hp, int Wp,
+                              cudaStream_t s);
 cudaError_t launch_class_hist(const uint8_t* labels, long long total, int classes, unsigned long long* counts,
                               cudaStream_t s);
 cudaError_t launch_loss_finalize(const float* loss_part, int parts, const int* nlab, int n, float* loss,

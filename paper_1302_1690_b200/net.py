@@ -27,6 +27,21 @@ def _ptr(t: Optional[torch.Tensor]) -> Optional[ctypes.c_void_p]:
     return ctypes.c_void_p(t.data_ptr())
 
 
+def mirror_pad(images: torch.Tensor, patch: int, stream=None) -> torch.Tensor:
+    """Same-size-output input: images [n, c, H, W] (cuda float32) mirror-padded
+    by floor((P-1)/2) before and the rest of P-1 after each axis (mpf_mirror_pad), so that
+    a net created for (H+P-1) x (W+P-1) images predicts exactly H x W pixels."""
+    from . import _lib as L
+    if images.dtype != torch.float32 or not images.is_cuda or not images.is_contiguous():
+        raise ValueError("images must be a contiguous cuda float32 tensor")
+    n, c, H, W = images.shape
+    pt = (patch - 1) // 2
+    out = torch.empty((n, c, H + patch - 1, W + patch - 1), dtype=torch.float32, device=images.device)
+    L.check(L.lib().mpf_mirror_pad(_ptr(images), n * c, H, W, pt, pt, H + patch - 1, W + patch - 1, _ptr(out),
+                                   _stream_ptr(stream)), "mpf_mirror_pad")
+    return out
+
+
 @dataclass
 class Geometry:
     n_layers: int
@@ -191,6 +206,12 @@ class MPFNet:
         L.check(self.lib.mpf_fragments_to_pixels(self.h, _ptr(frag), _ptr(out), n, channels, _stream_ptr(stream)),
                 "mpf_fragments_to_pixels")
         return out
+
+    def predict(self, images: torch.Tensor, stream=None) -> torch.Tensor:
+        """Per-pixel softmax probabilities [n, classes, out_rows, out_cols] of whole images
+        (forward with the softmax output, then the fragment -> pixel reassembly)."""
+        probs = self.forward(images, want_probs=True, stream=stream)
+        return self.fragments_to_pixels(probs, images.shape[0], self.geom.classes, stream=stream)
 
     def class_weights_auto(self, labels: torch.Tensor, stream=None):
         """Inverse-frequency class weights w_c = N / (C n_c) of a batch of label maps

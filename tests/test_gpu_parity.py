@@ -517,3 +517,36 @@ def test_auto_class_weights_vs_oracle(name):
     with pytest.raises(MpfError) as e:
         net.class_weights_auto(torch.full_like(torch.tensor(labels, device="cuda"), 0))
     assert e.value.status == 3
+
+
+def test_mirror_pad_bit_exact():
+    """mpf_mirror_pad against the oracle's definition (numpy reflect), odd and even P."""
+    from paper_1302_1690_b200.net import mirror_pad
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((2, 1, 37, 29)).astype(np.float32)
+    for P in (14, 44, 45):
+        got = mirror_pad(torch.tensor(x, device="cuda"), P).cpu().numpy()
+        assert np.array_equal(got, o2.mirror_pad(x, P))
+
+
+@pytest.mark.parametrize("name,H", [("cfg1", 24), ("cfg2", 64)])
+def test_same_size_segmentation_vs_o2(name, H):
+    """Segmentation workload: mirror-pad an H x H image by P - 1, run the
+    whole-image forward with softmax and reassemble the pixels: the probability map is
+    exactly H x H and matches the oracle on the same padded image (rel L2 5e-3, TF32)."""
+    from paper_1302_1690_b200.net import mirror_pad
+    cfg = S.CONFIGS[name]
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((2, 1, H, H)).astype(np.float32)
+    params = S.init_params(cfg)
+    xp = mirror_pad(torch.tensor(x, device="cuda"), cfg.P)
+    net = MPFNet(cfg.layers, cfg.P, H + cfg.P - 1, H + cfg.P - 1, max_images=2)
+    net.set_params(params.astype(np.float32))
+    prob = net.predict(xp).cpu().numpy()
+    assert prob.shape == (2, cfg.classes, H, H)
+    xo = o2.mirror_pad(x.astype(np.float64), cfg.P)
+    labels = np.full((2, H, H), 255, dtype=np.uint8)
+    o = oracle_step(cfg.layers, cfg.P, xo, labels, params, engine="o2")
+    want = np.stack(o["probs"])
+    assert want.shape == prob.shape
+    assert rel_l2(prob, want) <= TOL_TF32

@@ -426,3 +426,23 @@ def test_golden_auto_class_weights():
     assert np.allclose(w * cnt, cnt.sum() / 5)
     with pytest.raises(ValueError):
         o2.auto_class_weights(np.zeros(10, dtype=np.uint8), 2)
+
+
+def test_golden_mirror_pad():
+    """PAPER.md:207 / SPEC.md:296 mirror convention on a worked row, and the same-size
+    property: a P-padded image has an output grid of exactly H x W (H - P + 1 after padding)."""
+    lines = golden_lines("mirror_pad.txt")
+    row = np.array([float(v) for v in lines[0].split()[1:]])
+    before, after = (int(v) for v in lines[1].split()[1:])
+    want = [float(v) for v in lines[2].split()[1:]]
+    got = np.pad(row, (before, after), mode="reflect")  # the primitive o2.mirror_pad uses
+    assert list(got) == want
+    img = np.arange(5 * 7, dtype=np.float64).reshape(5, 7)
+    for P in (2, 4, 5):
+        pad = o2.mirror_pad(img, P)
+        assert pad.shape == (5 + P - 1, 7 + P - 1)
+        pt = (P - 1) // 2
+        assert np.array_equal(pad[pt:pt + 5, pt:pt + 7], img)
+        assert pad.shape[0] - P + 1 == 5 and pad.shape[1] - P + 1 == 7
+        if pt > 0:
+            assert np.array_equal(pad[pt - 1, pt:pt + 7], img[1])  # no repeat of the edge row
