@@ -171,6 +171,22 @@ mpf_status mpf_backward_image(mpf_net* net, const uint8_t* d_labels, const float
 mpf_status mpf_train_step(mpf_net* net, const float* d_images, int32_t n, const uint8_t* d_labels,
                           const float* h_class_w, float* d_loss, void* stream);
 
+/*
+ * Armijo-safeguarded gradient step ("stochastic gradient descent safe-guarded
+ * by the Armijo rule").  Computes the loss L0 and gradient
+ * g = grad_scale * sum_images grad (mpf_train_step), then tries theta + alpha d, d = -g, for
+ * alpha = alpha0, alpha0 beta, ... (at most max_backtracks + 1 trials, each a forward-only
+ * loss evaluation: forward + the softmax head's loss, L = grad_scale * sum of the images'
+ * mean losses) until L <= L0 - c alpha ||g||^2.  Accepted: the parameters move to that trial
+ * point; otherwise they stay at theta.  The gradient buffer is zeroed either way.
+ * h_out[5] = {L0, L_final, accepted alpha (0 if rejected), accepted (0/1), evaluations}.
+ * Synchronises `stream` once per trial.  Errors: MPF_ERR_ARG for alpha0 <= 0, beta or c
+ * outside (0, 1), n > 256; MPF_ERR_DATA for a non-finite L0 or ||g||.
+ */
+mpf_status mpf_armijo_step(mpf_net* net, const float* d_images, int32_t n, const uint8_t* d_labels,
+                           const float* h_class_w, float alpha0, float beta, float c, int32_t max_backtracks,
+                           float grad_scale, float* h_out, void* stream);
+
 /* SGD: theta <- theta - lr * grad_scale * g ; g <- 0. */
 mpf_status mpf_sgd_step(mpf_net* net, float lr, float grad_scale, void* stream);
 

@@ -331,3 +331,21 @@ def mirror_pad(image: np.ndarray, P: int) -> np.ndarray:
     pt = (P - 1) // 2
     pads = [(0, 0)] * (image.ndim - 2) + [(pt, P - 1 - pt), (pt, P - 1 - pt)]
     return np.pad(image, pads, mode="reflect")
+
+
+def armijo_step(eval_loss_grad, eval_loss, theta: np.ndarray, alpha0: float, beta: float, c: float,
+                max_backtracks: int):
+    """Armijo-safeguarded gradient step, written out: L0, g at
+    theta; alpha = alpha0, alpha0 beta, ...; accept the first theta - alpha g with
+    L <= L0 - c alpha ||g||^2; else keep theta.  Returns (theta_new, alpha or 0, L, accepted,
+    evaluations)."""
+    L0, g = eval_loss_grad(theta)
+    g2 = float(np.dot(g.ravel(), g.ravel()))
+    alpha = alpha0
+    for it in range(max_backtracks + 1):
+        t = theta - alpha * g
+        L = eval_loss(t)
+        if np.isfinite(L) and L <= L0 - c * alpha * g2:
+            return t, alpha, L, True, it + 1
+        alpha *= beta
+    return theta, 0.0, L0, False, max_backtracks + 1

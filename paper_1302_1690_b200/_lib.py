@@ -21,7 +21,7 @@ MPF_MAX_LAYERS = 24
 # every symbol include/mpf.h declares
 EXPORTS = ("mpf_version", "mpf_last_error", "mpf_net_create", "mpf_net_destroy", "mpf_net_geometry",
            "mpf_net_memory", "mpf_net_bind", "mpf_forward_image", "mpf_backward_image", "mpf_sgd_step",
-           "mpf_train_step", "mpf_train_step_host", "mpf_fragments_to_pixels", "mpf_mirror_pad", "mpf_class_weights_auto",
+           "mpf_train_step", "mpf_train_step_host", "mpf_fragments_to_pixels", "mpf_mirror_pad", "mpf_class_weights_auto", "mpf_armijo_step",
            "mpf_debug_tape", "mpf_debug_scratch", "mpf_check", "mpf_profile_begin",
            "mpf_profile_end")
 
@@ -88,6 +88,9 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
                                         ctypes.c_float, vp]
     lib.mpf_fragments_to_pixels.restype = st
     lib.mpf_fragments_to_pixels.argtypes = [vp, vp, vp, i32, i32, vp]
+    lib.mpf_armijo_step.restype = st
+    lib.mpf_armijo_step.argtypes = [vp, vp, i32, vp, ctypes.POINTER(ctypes.c_float), ctypes.c_float, ctypes.c_float,
+                                    ctypes.c_float, i32, ctypes.c_float, ctypes.POINTER(ctypes.c_float), vp]
     lib.mpf_mirror_pad.restype = st
     lib.mpf_mirror_pad.argtypes = [vp, i32, i32, i32, i32, i32, i32, i32, vp, vp]
     lib.mpf_class_weights_auto.restype = st

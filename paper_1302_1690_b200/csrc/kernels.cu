@@ -241,6 +241,48 @@ cudaError_t launch_wgrad_reduce(const float* pw, const float* pb, int n_split, i
   return cudaGetLastError();
 }
 
+// ============================================================================ Armijo helpers
+// ||g||^2 in double, deterministic: block b sums its contiguous chunk (fixed tree order)
+// into part[b], then one block sums part[0..nb) in order.
+__global__ void sqnorm_part_kernel(const float* __restrict__ g, long long n, long long chunk, double* part) {
+  __shared__ double s[256];
+  const long long b0 = blockIdx.x * chunk, b1 = min(n, b0 + chunk);
+  double t = 0.0;
+  for (long long e = b0 + threadIdx.x; e < b1; e += blockDim.x) t += (double)g[e] * (double)g[e];
+  s[threadIdx.x] = t;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = s[0];
+}
+__global__ void sqnorm_final_kernel(const double* __restrict__ part, int nb, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double t = 0.0;
+    for (int b = 0; b < nb; ++b) t += part[b];
+    *out = t;
+  }
+}
+cudaError_t launch_sqnorm(const float* g, long long n, double* part, int nb, double* out, cudaStream_t s) {
+  const long long chunk = (n + nb - 1) / nb;
+  sqnorm_part_kernel<<<nb, 256, 0, s>>>(g, n, chunk, part);
+  sqnorm_final_kernel<<<1, 32, 0, s>>>(part, nb, out);
+  return cudaGetLastError();
+}
+// theta = theta0 - alpha * scale * g   (the Armijo trial point along d = -g)
+__global__ void armijo_axpy_kernel(float* __restrict__ theta, const float* __restrict__ theta0,
+                                   const float* __restrict__ g, long long n, float step) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    theta[e] = theta0[e] - step * g[e];
+}
+cudaError_t launch_armijo_axpy(float* theta, const float* theta0, const float* g, long long n, float step,
+                               cudaStream_t s) {
+  const long long blocks = mpf_min_ll((n + 255) / 256, 148 * 8);
+  armijo_axpy_kernel<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(theta, theta0, g, n, step);
+  return cudaGetLastError();
+}
+
 // ============================================================================ mirror padding
 // Same-size output ("pixels outside of the boundary of testing images are
 // synthesized by mirroring -- which allows to preserve the size of the output"): the

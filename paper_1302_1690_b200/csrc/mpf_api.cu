@@ -12,6 +12,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <string>
 
 #include "conv_tc.h"
@@ -32,6 +33,8 @@ static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
       return MPF_ERR_CUDA;                                                              \
     }                                                                                   \
   } while (0)
+
+constexpr int kArmijoParts = 592;  // blocks of the deterministic ||g||^2 reduction
 
 static mpf_status fail(mpf_status s, const std::string& m) {
   set_error(m);
@@ -238,6 +241,8 @@ static void layout_memory(Net* N, int n) {
     s += N->stage_bytes;
   }
   N->off_stage_loss = s; s = align256(s + sizeof(float) * n);
+  N->off_theta0 = s; s = align256(s + sizeof(float) * (size_t)N->n_params);  // Armijo: parameters at the base point
+  N->off_armijo = s; s = align256(s + sizeof(double) * (kArmijoParts + 1));
   N->scratch_bytes = s;
   N->n_cap = n;
 }
@@ -687,7 +692,7 @@ static mpf_status bias_reduce(Net* N, int l, const float* part, long long nb, cu
 // Backward.  head_grid > 0: the fused forward already produced dh (first delta buffer),
 // the per-position losses and head_grid CTA partials of (dW_L, db_L, db_{L-1}).
 static mpf_status backward_impl(Net* N, const uint8_t* d_labels, const float* h_class_w, float* d_loss,
-                                cudaStream_t s, int head_grid) {
+                                cudaStream_t s, int head_grid, bool loss_only = false) {
   const int n = N->n_fwd;
   const bool tf32 = N->cfg.precision == MPF_PREC_TF32;
   const int L = N->n_layers - 1;  // the softmax FC
@@ -765,6 +770,12 @@ static mpf_status backward_impl(Net* N, const uint8_t* d_labels, const float* h_
              launch_head2(hd, s));
     }
     const int E = N->classes * h.C + N->classes + h.C;
+    if (loss_only) {  // forward-only loss evaluation (Armijo trial points): no gradients
+      if (d_loss)
+        LAUNCH(N, s, "loss_finalize", L, 0.0, 4.0 * (double)N->loss_parts * n,
+               launch_loss_finalize(lossp, hd.tiles_per_img * head_loss_parts_per_tile(), nlab, n, d_loss, s));
+      return MPF_OK;
+    }
     // [dW_L | db_L] are contiguous in the canonical order; db of layer L-1 follows
     LAUNCH(N, s, "head_reduce", L, 0.0, 4.0 * (double)hd.n_blocks * E,
            launch_partial_reduce(bpart, hd.n_blocks, E, N->grads + N->lp[L].w_off, N->grads + N->lp[L - 1].b_off,
@@ -930,6 +941,82 @@ mpf_status mpf_train_step(mpf_net* N, const float* d_images, int32_t n, const ui
   st = backward_impl(N, d_labels, h_class_w, d_loss, s, grid);
   N->have_fwd = false;  // the tape is consumed (the last hidden layer's output was never stored)
   return st;
+}
+
+// Armijo-safeguarded gradient step ("stochastic gradient descent safe-guarded
+// by the Armijo rule"): g = grad_scale * (sum of the images' gradients),
+// d = -g, alpha = alpha0, alpha0 beta, ... until L(theta + alpha d) <= L(theta) - c alpha ||g||^2
+// with L = grad_scale * (sum of the images' losses); trial points are forward-only loss
+// evaluations (forward + the head's loss).  Accepted: theta moves; exhausted: theta unchanged.
+// The gradient buffer is zeroed either way.  h_out[5] = {L0, L_final, alpha (0 if rejected),
+// accepted, loss evaluations}.  Synchronises the stream once per trial (the line search is a
+// host decision).
+mpf_status mpf_armijo_step(mpf_net* N, const float* d_images, int32_t n, const uint8_t* d_labels,
+                           const float* h_class_w, float alpha0, float beta, float c, int32_t max_backtracks,
+                           float grad_scale, float* h_out, void* stream) {
+  if (!N || !d_images || !d_labels || !h_out) return fail(MPF_ERR_ARG, "NULL argument");
+  if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound");
+  if (n < 1 || n > N->n_cap) return fail(MPF_ERR_DATA, "n must be in [1, bound n_images]");
+  if (!(alpha0 > 0.f) || !(beta > 0.f && beta < 1.f) || !(c > 0.f && c < 1.f) || max_backtracks < 0)
+    return fail(MPF_ERR_ARG, "Armijo parameters: alpha0 > 0, 0 < beta < 1, 0 < c < 1, max_backtracks >= 0");
+  cudaStream_t s = (cudaStream_t)stream;
+  float* d_loss = scr(N, N->off_stage_loss);
+  float h_loss[256];
+  if (n > 256) return fail(MPF_ERR_ARG, "at most 256 images per Armijo step");
+  auto total_loss = [&](double* L) -> mpf_status {
+    MPF_CUDA(cudaMemcpyAsync(h_loss, d_loss, sizeof(float) * n, cudaMemcpyDeviceToHost, s));
+    MPF_CUDA(cudaStreamSynchronize(s));
+    double t = 0.0;
+    for (int i = 0; i < n; ++i) t += h_loss[i];
+    *L = t * grad_scale;
+    return MPF_OK;
+  };
+  // 1. loss and gradient at theta
+  mpf_status st = mpf_train_step(N, d_images, n, d_labels, h_class_w, d_loss, stream);
+  if (st != MPF_OK) return st;
+  double L0 = 0.0, g2 = 0.0;
+  double* d_parts = (double*)(N->scratch + N->off_armijo);
+  MPF_CUDA(launch_sqnorm(N->grads, N->n_params, d_parts, kArmijoParts, d_parts + kArmijoParts, s));
+  MPF_CUDA(cudaMemcpyAsync(&g2, d_parts + kArmijoParts, sizeof(double), cudaMemcpyDeviceToHost, s));
+  st = total_loss(&L0);
+  if (st != MPF_OK) return st;
+  g2 *= (double)grad_scale * grad_scale;
+  if (!std::isfinite(L0) || !std::isfinite(g2)) {
+    MPF_CUDA(cudaMemsetAsync(N->grads, 0, sizeof(float) * N->n_params, s));
+    return fail(MPF_ERR_DATA, "Armijo: non-finite loss or gradient");
+  }
+  // 2. backtracking along d = -g from the saved base point
+  float* theta0 = scr(N, N->off_theta0);
+  MPF_CUDA(cudaMemcpyAsync(theta0, N->params, sizeof(float) * N->n_params, cudaMemcpyDeviceToDevice, s));
+  double alpha = alpha0, L = L0;
+  int evals = 0;
+  bool accepted = false;
+  for (int it = 0; it <= max_backtracks; ++it, alpha *= beta) {
+    MPF_CUDA(launch_armijo_axpy(N->params, theta0, N->grads, N->n_params, (float)(alpha * grad_scale), s));
+    st = forward_impl(N, d_images, n, nullptr, s, nullptr, nullptr);
+    if (st != MPF_OK) return st;
+    st = backward_impl(N, d_labels, h_class_w, d_loss, s, 0, true);
+    if (st != MPF_OK) return st;
+    st = total_loss(&L);
+    if (st != MPF_OK) return st;
+    ++evals;
+    if (std::isfinite(L) && L <= L0 - (double)c * alpha * g2) {
+      accepted = true;
+      break;
+    }
+  }
+  if (!accepted) {
+    MPF_CUDA(cudaMemcpyAsync(N->params, theta0, sizeof(float) * N->n_params, cudaMemcpyDeviceToDevice, s));
+    L = L0;
+  }
+  MPF_CUDA(cudaMemsetAsync(N->grads, 0, sizeof(float) * N->n_params, s));
+  N->have_fwd = false;  // the tape holds a trial point
+  h_out[0] = (float)L0;
+  h_out[1] = (float)L;
+  h_out[2] = accepted ? (float)alpha : 0.f;
+  h_out[3] = accepted ? 1.f : 0.f;
+  h_out[4] = (float)evals;
+  return MPF_OK;
 }
 
 mpf_status mpf_sgd_step(mpf_net* N, float lr, float scale, void* stream) {

@@ -67,7 +67,7 @@ struct Net {
   size_t tape_bytes = 0, scratch_bytes = 0;
   size_t off_Y = 0, off_dA = 0, off_dB = 0, off_dC = 0, off_bpart = 0, off_wpack = 0, off_part = 0,
          off_nlab = 0, off_lossp = 0, off_err = 0, off_rowloss = 0, off_stage_img = 0, off_stage_lab = 0,
-         off_stage_loss = 0;
+         off_stage_loss = 0, off_theta0 = 0, off_armijo = 0;
   size_t stage_bytes = 0;  // one of the two host-input staging slots (images | labels)
   // host-buffer steps: inputs of step i + 1 are copied on copy_stream into the other
   // staging slot while step i computes (events order the slots' reuse)
@@ -208,6 +208,9 @@ int head_tc_grid(long long per_img, int n);
 cudaError_t launch_head_tc(const HeadArgs& a, cudaStream_t s);
 
 cudaError_t launch_label_count(const uint8_t* labels, int n, int hw, int classes, int* nlab, cudaStream_t s);
+cudaError_t launch_sqnorm(const float* g, long long n, double* part, int nb, double* out, cudaStream_t s);
+cudaError_t launch_armijo_axpy(float* theta, const float* theta0, const float* g, long long n, float step,
+                               cudaStream_t s);
 cudaError_t launch_mirror_pad(const float* in, float* out, long long planes, int H, int W, int pt, int pl, int Hp, int Wp,
                               cudaStream_t s);
 cudaError_t launch_class_hist(const uint8_t* labels, long long total, int classes, unsigned long long* counts,

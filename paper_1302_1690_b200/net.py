@@ -207,6 +207,21 @@ class MPFNet:
                 "mpf_fragments_to_pixels")
         return out
 
+    def armijo_step(self, images: torch.Tensor, labels: torch.Tensor, alpha0: float = 0.01, beta: float = 0.5,
+                    c: float = 1e-4, max_backtracks: int = 10, class_w=None, grad_scale: float = None,
+                    stream=None) -> dict:
+        """One Armijo-safeguarded step on a batch (mpf_armijo_step); grad_scale defaults to 1/n."""
+        n = images.shape[0]
+        cw = None
+        if class_w is not None:
+            cw = (ctypes.c_float * self.geom.classes)(*[float(v) for v in class_w])
+        out = (ctypes.c_float * 5)()
+        gs = 1.0 / n if grad_scale is None else float(grad_scale)
+        L.check(self.lib.mpf_armijo_step(self.h, _ptr(images), n, _ptr(labels), cw, float(alpha0), float(beta),
+                                         float(c), int(max_backtracks), gs, out, _stream_ptr(stream)),
+                "mpf_armijo_step")
+        return {"loss0": out[0], "loss": out[1], "alpha": out[2], "accepted": bool(out[3]), "evals": int(out[4])}
+
     def predict(self, images: torch.Tensor, stream=None) -> torch.Tensor:
         """Per-pixel softmax probabilities [n, classes, out_rows, out_cols] of whole images
         (forward with the softmax output, then the fragment -> pixel reassembly)."""

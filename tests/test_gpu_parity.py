@@ -550,3 +550,33 @@ def test_same_size_segmentation_vs_o2(name, H):
     want = np.stack(o["probs"])
     assert want.shape == prob.shape
     assert rel_l2(prob, want) <= TOL_TF32
+
+
+def test_armijo_step_vs_oracle():
+    """mpf_armijo_step: loss at theta, the backtracking sequence and the
+    accepted alpha match the oracle's Armijo rule on O2's loss and gradient (batch of 2 cfg2
+    images, alpha0 large enough to force backtracking); the new parameters match."""
+    cfg = S.CONFIGS["cfg2"]
+    images, labels = S.make_batch(cfg, [0, 1])
+    params = S.init_params(cfg)
+    n = 2
+
+    def eval_lg(theta):
+        o = oracle_step(cfg.layers, cfg.P, images.astype(np.float64), labels, theta, engine="o2")
+        return float(np.sum(o["loss"])) / n, o["grad_sum"] / n
+
+    def eval_l(theta):
+        return eval_lg(theta)[0]
+
+    alpha0, beta, c = 40.0, 0.5, 1e-4
+    t_o, a_o, L_o, ok_o, ev_o = o2.armijo_step(eval_lg, eval_l, params.astype(np.float64), alpha0, beta, c, 8)
+    net = MPFNet(cfg.layers, cfg.P, cfg.H, cfg.W, max_images=n)
+    net.set_params(params.astype(np.float32))
+    r = net.armijo_step(torch.tensor(images, device="cuda"), torch.tensor(labels, device="cuda"), alpha0=alpha0,
+                        beta=beta, c=c, max_backtracks=8)
+    L0_o = eval_l(params.astype(np.float64))
+    assert abs(r["loss0"] - L0_o) <= TOL_TF32 * abs(L0_o)
+    assert r["accepted"] == ok_o and r["evals"] == ev_o and r["alpha"] == np.float32(a_o)
+    assert ev_o >= 2  # the test exercises backtracking
+    assert rel_l2(net.params.cpu().numpy(), t_o) <= TOL_TF32
+    assert np.all(net.grads.cpu().numpy() == 0.0)

@@ -446,3 +446,16 @@ def test_golden_mirror_pad():
         assert pad.shape[0] - P + 1 == 5 and pad.shape[1] - P + 1 == 7
         if pt > 0:
             assert np.array_equal(pad[pt - 1, pt:pt + 7], img[1])  # no repeat of the edge row
+
+
+def test_golden_armijo_quadratic():
+    """SPEC.md:388-396 worked cases of the Armijo rule on L = theta^2."""
+    for line in golden_lines("armijo.txt"):
+        tok = line.split()
+        th, a0, beta = float(tok[2]), float(tok[4]), float(tok[6])
+        want_th, want_a, want_ev = float(tok[9]), float(tok[11]), int(tok[13])
+        f = lambda t: float(np.sum(t * t))  # noqa: E731
+        fg = lambda t: (f(t), 2.0 * t)  # noqa: E731
+        t_new, a, L, ok, ev = o2.armijo_step(fg, f, np.array([th]), a0, beta, 1e-4, 10)
+        assert ok and ev == want_ev and a == want_a and abs(t_new[0] - want_th) < 1e-15
+        assert L <= th * th  # an accepted step never increases the loss
