@@ -349,3 +349,64 @@ def armijo_step(eval_loss_grad, eval_loss, theta: np.ndarray, alpha0: float, bet
             return t, alpha, L, True, it + 1
         alpha *= beta
     return theta, 0.0, L0, False, max_backtracks + 1
+
+
+def lbfgs_two_loop(g: np.ndarray, S: List[np.ndarray], Y: List[np.ndarray]) -> np.ndarray:
+    """r = H_k g by the L-BFGS two-loop recursion ("two-loop recursion
+    direction"; "We use LBFGS"), pairs oldest first, H_k^0 = gamma I with
+    gamma = s_{k-1}^T y_{k-1} / y_{k-1}^T y_{k-1} (1 with no pairs; reading R21)."""
+    q = g.astype(np.float64).copy()
+    a = [0.0] * len(S)
+    for i in reversed(range(len(S))):          # newest to oldest
+        rho = 1.0 / float(np.dot(S[i], Y[i]))
+        a[i] = rho * float(np.dot(S[i], q))
+        q = q - a[i] * Y[i]
+    gamma = float(np.dot(S[-1], Y[-1])) / float(np.dot(Y[-1], Y[-1])) if S else 1.0
+    r = gamma * q
+    for i in range(len(S)):                    # oldest to newest
+        rho = 1.0 / float(np.dot(S[i], Y[i]))
+        b = rho * float(np.dot(Y[i], r))
+        r = r + (a[i] - b) * S[i]
+    return r
+
+
+def lbfgs_step(state: dict, theta: np.ndarray, eval_loss_grad, memory: int, alpha0: float, beta: float, c: float,
+               max_backtracks: int, sy_min: float = 1e-10):
+    """One full-batch L-BFGS iteration, written out:
+
+      (L, g) at theta (kept in `state` from the previous accepted trial);
+      d = -H g by the two-loop recursion; if g^T d >= 0, d = -g (steepest descent);
+      alpha = alpha0 with no pairs, 1 otherwise (reading R21); backtrack alpha <- beta alpha
+      until L(theta + alpha d) <= L + c alpha g^T d (Armijo along d);
+      accepted: s = theta_new - theta, y = g_new - g, the pair kept iff s^T y > sy_min,
+      the oldest dropped beyond `memory`; exhausted: theta unchanged, pairs cleared (R21).
+
+    state: {"S": [...], "Y": [...], "L": float or None, "g": array or None}, updated in place.
+    Returns (theta_new, alpha or 0, L_before, L_after, accepted, evaluations, fallback)."""
+    if state.get("g") is None:
+        state["L"], state["g"] = eval_loss_grad(theta)
+    S, Y = state.setdefault("S", []), state.setdefault("Y", [])
+    L0, g = state["L"], state["g"]
+    d = -lbfgs_two_loop(g, S, Y)
+    gtd = float(np.dot(g, d))
+    fallback = not (gtd < 0.0)
+    if fallback:
+        d = -g
+        gtd = -float(np.dot(g, g))
+    alpha = alpha0 if not S else 1.0
+    for it in range(max_backtracks + 1):
+        t = theta + alpha * d
+        Lt, gt = eval_loss_grad(t)
+        if np.isfinite(Lt) and Lt <= L0 + c * alpha * gtd:
+            s, y = t - theta, gt - g
+            if float(np.dot(s, y)) > sy_min:
+                S.append(s)
+                Y.append(y)
+                if len(S) > memory:
+                    del S[0], Y[0]
+            state["L"], state["g"] = Lt, gt
+            return t, alpha, L0, Lt, True, it + 1, fallback
+        alpha *= beta
+    S.clear()
+    Y.clear()
+    return theta, 0.0, L0, L0, False, max_backtracks + 1, fallback

@@ -459,3 +459,94 @@ def test_golden_armijo_quadratic():
         t_new, a, L, ok, ev = o2.armijo_step(fg, f, np.array([th]), a0, beta, 1e-4, 10)
         assert ok and ev == want_ev and a == want_a and abs(t_new[0] - want_th) < 1e-15
         assert L <= th * th  # an accepted step never increases the loss
+
+
+def _quad(A, bvec):
+    """L = 1/2 t^T A t - b^T t and its gradient."""
+    return lambda t: (0.5 * float(t @ A @ t) - float(bvec @ t), A @ t - bvec)
+
+
+def test_golden_lbfgs_worked_steps():
+    """SPEC.md:397-405 worked cases (tests/golden/lbfgs.txt): the empty-history step is
+    steepest descent at alpha0, and the second direction equals the BFGS inverse-Hessian
+    update written as matrices (an independent form of the two-loop)."""
+    lines = {ln.split()[0]: ln.split() for ln in golden_lines("lbfgs.txt")}
+    f = lambda t: (float(t[0] ** 2 + 4 * t[1] ** 2), np.array([2 * t[0], 8 * t[1]]))  # noqa: E731
+    st = {}
+    t1, a, L0, L1, ok, ev, fb = o2.lbfgs_step(st, np.array([1.0, 1.0]), f, 5, 0.1, 0.5, 1e-4, 10)
+    s1 = lines["step1"]
+    assert ok and not fb and ev == int(s1[7]) and a == float(s1[5])
+    assert np.allclose(t1, [float(s1[2]), float(s1[3])], rtol=0, atol=1e-15)
+    assert abs(float(st["S"][0] @ st["Y"][0]) - float(s1[9])) < 1e-14
+    d2 = -o2.lbfgs_two_loop(st["g"], st["S"], st["Y"])
+    w = lines["dir2"]
+    want = np.array([int(w[1]) / int(w[2]), int(w[3]) / int(w[4])])
+    assert np.allclose(d2, want, rtol=1e-14, atol=0)
+
+
+def test_lbfgs_two_loop_equals_bfgs_matrix_update():
+    """The two-loop product H_k g equals the explicit BFGS recursion
+    H <- (I - rho s y^T) H (I - rho y s^T) + rho s s^T from H0 = gamma I over the same m pairs,
+    and H_k y_newest = s_newest (secant equation), for random pairs with s^T y > 0."""
+    rng = np.random.default_rng(7)
+    n, m = 6, 4
+    M = rng.standard_normal((n, n))
+    A = M @ M.T + n * np.eye(n)
+    S = [rng.standard_normal(n) for _ in range(m)]
+    Y = [A @ s for s in S]
+    gamma = float(S[-1] @ Y[-1]) / float(Y[-1] @ Y[-1])
+    H = gamma * np.eye(n)
+    for s, y in zip(S, Y):
+        rho = 1.0 / float(s @ y)
+        V = np.eye(n) - rho * np.outer(y, s)
+        H = V.T @ H @ V + rho * np.outer(s, s)
+    g = rng.standard_normal(n)
+    assert np.allclose(o2.lbfgs_two_loop(g, S, Y), H @ g, rtol=1e-11, atol=1e-12)
+    assert np.allclose(o2.lbfgs_two_loop(Y[-1], S, Y), S[-1], rtol=1e-11, atol=1e-12)
+    assert np.array_equal(o2.lbfgs_two_loop(g, [], []), g)
+
+
+def test_lbfgs_convex_quadratic_converges():
+    """on a fixed strictly convex 5-variable quadratic the gradient norm
+    drops below 1e-8 within 20 iterations, the loss decreases monotonically, and the history
+    never exceeds `memory` pairs (10, the customary default; the SPEC leaves it open); the
+    minimiser is A^-1 b (closed form)."""
+    rng = np.random.default_rng(11)
+    M = rng.standard_normal((5, 5))
+    A = M @ M.T + np.eye(5)
+    bvec = rng.standard_normal(5)
+    f = _quad(A, bvec)
+    theta, st, losses, memory = np.zeros(5), {}, [], 10
+    for it in range(20):
+        theta, a, L0, L1, ok, ev, fb = o2.lbfgs_step(st, theta, f, memory, 1.0, 0.5, 1e-4, 30)
+        assert ok and L1 <= L0
+        assert len(st["S"]) <= memory
+        losses.append(L1)
+        if np.linalg.norm(st["g"]) < 1e-8:
+            break
+    assert np.linalg.norm(st["g"]) < 1e-8, (it, np.linalg.norm(st["g"]))
+    assert np.allclose(theta, np.linalg.solve(A, bvec), rtol=1e-7, atol=1e-9)
+    assert all(b <= a for a, b in zip(losses, losses[1:]))
+
+
+def test_lbfgs_fallback_and_restart():
+    """Non-descent direction -> steepest descent; an exhausted line search keeps
+    theta and clears the pairs (R21); pairs with s^T y <= 1e-10 are not stored."""
+    f = lambda t: (float(t @ t), 2 * t)  # noqa: E731
+    st = {"S": [np.array([1.0, 0.0])], "Y": [np.array([-1.0, 0.0])], "L": 2.0, "g": np.array([2.0, 2.0])}
+    # with s^T y < 0 the single-pair H is indefinite along e1: H g = (-2 + ..., ...) gives g^T d >= 0
+    d = -o2.lbfgs_two_loop(st["g"], st["S"], st["Y"])
+    assert float(st["g"] @ d) >= 0
+    t, a, L0, L1, ok, ev, fb = o2.lbfgs_step(st, np.array([1.0, 1.0]), f, 3, 0.1, 0.5, 1e-4, 10)
+    # d = -g = (-2, -2); history non-empty -> alpha starts at 1: L(-1, -1) = 2 is rejected,
+    # alpha = 0.5 reaches the minimum (0, 0)
+    assert fb and ok and a == 0.5 and ev == 2 and np.array_equal(t, [0.0, 0.0])
+    # exhausted search: max_backtracks = 0 and a step that overshoots
+    st2 = {}
+    t2, a2, L0, L1, ok2, ev2, fb2 = o2.lbfgs_step(st2, np.array([1.0]), f, 3, 5.0, 0.5, 1e-4, 0)
+    assert not ok2 and a2 == 0.0 and t2[0] == 1.0 and st2["S"] == [] and ev2 == 1
+    # a linear loss has y = 0, so s^T y = 0 and no pair is stored
+    lin = lambda t: (float(np.sum(t)), np.ones_like(t))  # noqa: E731
+    st3 = {}
+    o2.lbfgs_step(st3, np.array([0.0, 0.0]), lin, 3, 0.5, 0.5, 1e-4, 5)
+    assert st3["S"] == []
