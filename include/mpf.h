@@ -187,6 +187,60 @@ mpf_status mpf_armijo_step(mpf_net* net, const float* d_images, int32_t n, const
                            const float* h_class_w, float alpha0, float beta, float c, int32_t max_backtracks,
                            float grad_scale, float* h_out, void* stream);
 
+/*
+ * Full-batch L-BFGS ("We use LBFGS"; SURVEY §8(f) item 4;
+ * reading R21 in DESIGN.md).  An mpf_lbfgs owns, in its own device allocation, memory + 1
+ * curvature-pair slots (s, y: fp32 [n_params] each), the base point theta0 and the gradient
+ * g at it (fp32), and the direction v = H g (fp64).  It works on the parameters and
+ * gradients bound to `net`, which must outlive it.  One stream at a time; every call is
+ * asynchronous on `stream` except where it says it synchronises.
+ *
+ * Primitives (the multi-GPU driver calls these with an all-reduce between; one GPU can call
+ * mpf_lbfgs_step instead):
+ *   set_gradient: g <- grad_scale * (the net's gradient buffer), the gradient at the
+ *                 current parameters (the caller has zeroed, evaluated and, across ranks,
+ *                 summed it).
+ *   direction:    v <- H g by the two-loop recursion over the stored pairs (H0 = gamma I,
+ *                 gamma = s^T y / y^T y of the newest pair), theta0 <- parameters;
+ *                 *h_gtd = g^T d with d = -v; if that is not negative (or not finite) d falls
+ *                 back to -g, *h_fallback = 1.  Synchronises `stream` once (or twice).
+ *   trial:        parameters <- theta0 + alpha d.
+ *   accept:       the net's gradient buffer holds the gradient at the current trial point:
+ *                 s = theta - theta0, y = grad_scale grad - g, g <- grad_scale grad; the pair
+ *                 is stored iff s^T y > 1e-10 (the oldest dropped beyond `memory`);
+ *                 *h_stored = 0/1.  Synchronises `stream`.
+ *   reject:       parameters <- theta0; the pairs are cleared (restart).
+ *   reset:        pairs cleared and g marked unknown (after the parameters or data change).
+ * Errors: MPF_ERR_ARG for memory outside [1, 64] or NULL pointers; MPF_ERR_STATE for
+ * direction without a gradient, trial/accept without a direction.
+ */
+typedef struct mpf_lbfgs mpf_lbfgs; /* opaque */
+mpf_status mpf_lbfgs_create(mpf_net* net, int32_t memory, mpf_lbfgs** out);
+void mpf_lbfgs_destroy(mpf_lbfgs* lb);
+mpf_status mpf_lbfgs_reset(mpf_lbfgs* lb);
+mpf_status mpf_lbfgs_set_gradient(mpf_lbfgs* lb, float grad_scale, void* stream);
+mpf_status mpf_lbfgs_direction(mpf_lbfgs* lb, double* h_gtd, int32_t* h_fallback, void* stream);
+mpf_status mpf_lbfgs_trial(mpf_lbfgs* lb, double alpha, void* stream);
+mpf_status mpf_lbfgs_accept(mpf_lbfgs* lb, float grad_scale, int32_t* h_stored, void* stream);
+mpf_status mpf_lbfgs_reject(mpf_lbfgs* lb, void* stream);
+/*
+ * One full-batch L-BFGS iteration on one GPU over the n images (the whole training set;
+ * pass the same images every call, or mpf_lbfgs_reset first): the loss and gradient at
+ * theta (L = grad_scale * sum of the images' mean losses, g = grad_scale * sum of their
+ * gradients; computed here only on the first call or after a reset / rejected search,
+ * otherwise kept from the previous accepted trial), the direction, then trials
+ * theta0 + alpha d for alpha = alpha0 (empty history) or 1, times beta per backtrack, each a
+ * full loss + gradient evaluation (mpf_train_step), until L <= L0 + c alpha g^T d; then
+ * accept (pair update) or, after max_backtracks + 1 trials, reject.
+ * h_out[7] = {L0, L_final, accepted alpha (0 if rejected), accepted (0/1), evaluations,
+ * steepest-descent fallback (0/1), stored pairs}.  Synchronises once per evaluation.
+ * Afterwards the gradient buffer holds the unscaled gradient of the last trial.
+ * Errors: as mpf_armijo_step; MPF_ERR_DATA for a non-finite L0 or g^T d.
+ */
+mpf_status mpf_lbfgs_step(mpf_lbfgs* lb, const float* d_images, int32_t n, const uint8_t* d_labels,
+                          const float* h_class_w, float alpha0, float beta, float c, int32_t max_backtracks,
+                          float grad_scale, float* h_out, void* stream);
+
 /* SGD: theta <- theta - lr * grad_scale * g ; g <- 0. */
 mpf_status mpf_sgd_step(mpf_net* net, float lr, float grad_scale, void* stream);
 

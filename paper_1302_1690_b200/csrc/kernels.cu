@@ -283,6 +283,131 @@ cudaError_t launch_armijo_axpy(float* theta, const float* theta0, const float* g
   return cudaGetLastError();
 }
 
+// ============================================================================ L-BFGS vectors
+// The two-loop recursion (reading R21) on the flat
+// parameter vector.  Every pass is one sweep: v <- f(v, x) with a coefficient formed from
+// the previous pass's dot product, then this block's partial of the next dot z . v over the
+// SAME contiguous chunk it just updated, so no pass needs a grid-wide barrier.  Each block
+// re-sums the nb partials of the previous pass itself in one fixed order (identical in
+// every block), so the scalars are deterministic and never leave the device.
+namespace {
+__device__ __forceinline__ double lb_block_sum(double t, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sh[w] = t;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) r += sh[i];
+  return r;  // valid in thread 0
+}
+// sum of nb partials, same order in every block; broadcast to all threads
+__device__ __forceinline__ double lb_sum_parts(const double* __restrict__ part, int nb, double* sh) {
+  if (threadIdx.x < 32) {
+    double t = 0.0;
+    for (int i = threadIdx.x; i < nb; i += 32) t += part[i];
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) sh[32] = t;
+  }
+  __syncthreads();
+  const double r = sh[32];
+  __syncthreads();
+  return r;
+}
+}  // namespace
+
+// gprev = scale * g
+__global__ void lbfgs_gset_kernel(float* __restrict__ gprev, const float* __restrict__ g, long long n, float scale) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    gprev[e] = scale * g[e];
+}
+// the new curvature pair: s = theta - theta0, y = scale g - gprev; gprev <- scale g;
+// partials of s.y and y.y
+__global__ void lbfgs_pair_kernel(float* __restrict__ S, float* __restrict__ Y, float* __restrict__ gprev,
+                                  const float* __restrict__ theta, const float* __restrict__ theta0,
+                                  const float* __restrict__ g, long long n, long long chunk, float scale,
+                                  double* __restrict__ part) {
+  __shared__ double sh[40];
+  const long long b0 = blockIdx.x * chunk, b1 = min(n, b0 + chunk);
+  double sy = 0.0, yy = 0.0;
+  for (long long e = b0 + threadIdx.x; e < b1; e += blockDim.x) {
+    const float s = theta[e] - theta0[e];
+    const float gn = scale * g[e];
+    const float y = gn - gprev[e];
+    S[e] = s;
+    Y[e] = y;
+    gprev[e] = gn;
+    sy += (double)s * (double)y;
+    yy += (double)y * (double)y;
+  }
+  sy = lb_block_sum(sy, sh);
+  __syncthreads();
+  yy = lb_block_sum(yy, sh);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = sy;
+    part[gridDim.x + blockIdx.x] = yy;
+  }
+}
+// mode 0: v = x.  mode 1 (first loop): a = rho (sum part_in); *a_slot = a; v = (v - a x) * post.
+// mode 2 (second loop): b = rho (sum part_in); v = v + (*a_slot - b) x.  Then partials of z.v.
+__global__ void lbfgs_pass_kernel(double* __restrict__ v, const float* __restrict__ x, const float* __restrict__ z,
+                                  long long n, long long chunk, const double* __restrict__ part_in, int mode,
+                                  double rho, double* a_slot, double post, double* __restrict__ part_out) {
+  __shared__ double sh[40];
+  double coef = 0.0;
+  if (mode != 0) {
+    const double d = lb_sum_parts(part_in, gridDim.x, sh);
+    if (mode == 1) {
+      coef = -rho * d;
+      if (blockIdx.x == 0 && threadIdx.x == 0) *a_slot = rho * d;
+    } else {
+      coef = *a_slot - rho * d;
+    }
+  }
+  const long long b0 = blockIdx.x * chunk, b1 = min(n, b0 + chunk);
+  double t = 0.0;
+  for (long long e = b0 + threadIdx.x; e < b1; e += blockDim.x) {
+    double ve;
+    if (mode == 0) ve = (double)x[e];
+    else if (mode == 1) ve = (v[e] + coef * (double)x[e]) * post;
+    else ve = v[e] + coef * (double)x[e];
+    v[e] = ve;
+    if (z) t += (double)z[e] * ve;
+  }
+  t = lb_block_sum(t, sh);
+  if (threadIdx.x == 0) part_out[blockIdx.x] = t;
+}
+// theta = theta0 - alpha v   (the trial point theta0 + alpha d, d = -H g = -v)
+__global__ void lbfgs_trial_kernel(float* __restrict__ theta, const float* __restrict__ theta0,
+                                   const double* __restrict__ v, long long n, double alpha) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    theta[e] = (float)((double)theta0[e] - alpha * v[e]);
+}
+
+cudaError_t launch_lbfgs_gset(float* gprev, const float* g, long long n, float scale, cudaStream_t s) {
+  const long long blocks = mpf_min_ll((n + 255) / 256, 148 * 8);
+  lbfgs_gset_kernel<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(gprev, g, n, scale);
+  return cudaGetLastError();
+}
+cudaError_t launch_lbfgs_pair(float* S, float* Y, float* gprev, const float* theta, const float* theta0, const float* g,
+                              long long n, float scale, double* part, int nb, cudaStream_t s) {
+  const long long chunk = (n + nb - 1) / nb;
+  lbfgs_pair_kernel<<<nb, 256, 0, s>>>(S, Y, gprev, theta, theta0, g, n, chunk, scale, part);
+  return cudaGetLastError();
+}
+cudaError_t launch_lbfgs_pass(double* v, const float* x, const float* z, long long n, const double* part_in, int mode,
+                              double rho, double* a_slot, double post, double* part_out, int nb, cudaStream_t s) {
+  const long long chunk = (n + nb - 1) / nb;
+  lbfgs_pass_kernel<<<nb, 256, 0, s>>>(v, x, z, n, chunk, part_in, mode, rho, a_slot, post, part_out);
+  return cudaGetLastError();
+}
+cudaError_t launch_lbfgs_trial(float* theta, const float* theta0, const double* v, long long n, double alpha,
+                               cudaStream_t s) {
+  const long long blocks = mpf_min_ll((n + 255) / 256, 148 * 8);
+  lbfgs_trial_kernel<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(theta, theta0, v, n, alpha);
+  return cudaGetLastError();
+}
+
 // ============================================================================ mirror padding
 // Same-size output ("pixels outside of the boundary of testing images are
 // synthesized by mirroring -- which allows to preserve the size of the output"): the

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <string>
+#include <vector>
 
 #include "conv_tc.h"
 #include "mpf_internal.h"
@@ -1016,6 +1017,267 @@ mpf_status mpf_armijo_step(mpf_net* N, const float* d_images, int32_t n, const u
   h_out[2] = accepted ? (float)alpha : 0.f;
   h_out[3] = accepted ? 1.f : 0.f;
   h_out[4] = (float)evals;
+  return MPF_OK;
+}
+
+// ============================================================================ L-BFGS
+// Full-batch L-BFGS (reading R21).  Device state lives in
+// one allocation; the pair bookkeeping (which slots hold which pair, s^T y, y^T y) is on
+// the host, which needs s^T y anyway to decide whether a pair is kept.
+}  // extern "C"
+
+constexpr int kLbParts = 592;  // blocks of every L-BFGS pass (148 SMs x 4)
+
+struct mpf_lbfgs {
+  mpf_net* N = nullptr;
+  int m = 0;                    // memory (pairs kept)
+  long long n = 0;              // parameters
+  char* mem = nullptr;          // device allocation
+  float* S = nullptr;           // (m+1) slots of s, then of y
+  float* Y = nullptr;
+  float* theta0 = nullptr;
+  float* g = nullptr;           // grad_scale * gradient at theta0 / the current point
+  double* v = nullptr;          // H g
+  double* parts = nullptr;      // 2 x kLbParts partial sums (ping, pong)
+  double* a = nullptr;          // alpha_i of the first loop, per slot
+  std::vector<int> order;       // stored pairs' slots, oldest first
+  std::vector<double> sy, yy;   // per slot
+  bool have_g = false, have_dir = false;
+  double L = 0.0;               // mpf_lbfgs_step: loss at the current point (valid with have_g)
+  std::vector<double> hpart;
+};
+
+namespace {
+double host_sum(const std::vector<double>& p, int off, int nb) {
+  double t = 0.0;
+  for (int i = 0; i < nb; ++i) t += p[off + i];
+  return t;
+}
+}  // namespace
+
+extern "C" {
+
+mpf_status mpf_lbfgs_create(mpf_net* N, int32_t memory, mpf_lbfgs** out) {
+  if (!N || !out) return fail(MPF_ERR_ARG, "NULL argument");
+  if (memory < 1 || memory > 64) return fail(MPF_ERR_ARG, "L-BFGS memory must be in [1, 64]");
+  if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound");
+  mpf_lbfgs* lb = new mpf_lbfgs();
+  lb->N = N;
+  lb->m = memory;
+  lb->n = N->n_params;
+  const size_t vec = align256(sizeof(float) * (size_t)lb->n);
+  const size_t slots = (size_t)memory + 1;
+  const size_t bytes = 2 * slots * vec + 2 * vec + align256(sizeof(double) * (size_t)lb->n) +
+                       align256(sizeof(double) * 2 * kLbParts) + align256(sizeof(double) * slots);
+  if (cudaMalloc(&lb->mem, bytes) != cudaSuccess) {
+    delete lb;
+    return fail(MPF_ERR_CUDA, "L-BFGS state allocation failed");
+  }
+  char* p = lb->mem;
+  lb->S = (float*)p; p += slots * vec;
+  lb->Y = (float*)p; p += slots * vec;
+  lb->theta0 = (float*)p; p += vec;
+  lb->g = (float*)p; p += vec;
+  lb->v = (double*)p; p += align256(sizeof(double) * (size_t)lb->n);
+  lb->parts = (double*)p; p += align256(sizeof(double) * 2 * kLbParts);
+  lb->a = (double*)p;
+  lb->sy.assign(slots, 0.0);
+  lb->yy.assign(slots, 0.0);
+  lb->hpart.assign(2 * kLbParts, 0.0);
+  *out = lb;
+  return MPF_OK;
+}
+
+void mpf_lbfgs_destroy(mpf_lbfgs* lb) {
+  if (!lb) return;
+  cudaFree(lb->mem);
+  delete lb;
+}
+
+mpf_status mpf_lbfgs_reset(mpf_lbfgs* lb) {
+  if (!lb) return fail(MPF_ERR_ARG, "NULL L-BFGS state");
+  lb->order.clear();
+  lb->have_g = lb->have_dir = false;
+  return MPF_OK;
+}
+
+mpf_status mpf_lbfgs_set_gradient(mpf_lbfgs* lb, float grad_scale, void* stream) {
+  if (!lb) return fail(MPF_ERR_ARG, "NULL L-BFGS state");
+  MPF_CUDA(launch_lbfgs_gset(lb->g, lb->N->grads, lb->n, grad_scale, (cudaStream_t)stream));
+  lb->have_g = true;
+  lb->have_dir = false;
+  return MPF_OK;
+}
+
+mpf_status mpf_lbfgs_direction(mpf_lbfgs* lb, double* h_gtd, int32_t* h_fallback, void* stream) {
+  if (!lb || !h_gtd) return fail(MPF_ERR_ARG, "NULL argument");
+  if (!lb->have_g) return fail(MPF_ERR_STATE, "L-BFGS direction without a gradient (mpf_lbfgs_set_gradient)");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int k = (int)lb->order.size();
+  const long long n = lb->n;
+  double* P[2] = {lb->parts, lb->parts + kLbParts};
+  int cur = 0;
+  auto slotS = [&](int j) { return lb->S + (size_t)lb->order[j] * (align256(sizeof(float) * n) / sizeof(float)); };
+  auto slotY = [&](int j) { return lb->Y + (size_t)lb->order[j] * (align256(sizeof(float) * n) / sizeof(float)); };
+  // two-loop: q = g; newest -> oldest: a_i = rho_i s_i.q, q -= a_i y_i; r = gamma q;
+  // oldest -> newest: b = rho_i y_i.r, r += (a_i - b) s_i.  Passes ping-pong the partials.
+  MPF_CUDA(launch_lbfgs_pass(lb->v, lb->g, k ? slotS(k - 1) : lb->g, n, nullptr, 0, 0.0, nullptr, 1.0, P[cur],
+                             kLbParts, s));
+  if (k) {
+    const int newest = lb->order[k - 1];
+    const double gamma = lb->sy[newest] / lb->yy[newest];
+    for (int j = k - 1; j >= 0; --j) {
+      const int sl = lb->order[j];
+      const float* z = j > 0 ? slotS(j - 1) : slotY(0);
+      MPF_CUDA(launch_lbfgs_pass(lb->v, slotY(j), z, n, P[cur], 1, 1.0 / lb->sy[sl], lb->a + sl,
+                                 j == 0 ? gamma : 1.0, P[cur ^ 1], kLbParts, s));
+      cur ^= 1;
+    }
+    for (int j = 0; j < k; ++j) {
+      const int sl = lb->order[j];
+      const float* z = j < k - 1 ? slotY(j + 1) : lb->g;
+      MPF_CUDA(launch_lbfgs_pass(lb->v, slotS(j), z, n, P[cur], 2, 1.0 / lb->sy[sl], lb->a + sl, 1.0,
+                                 P[cur ^ 1], kLbParts, s));
+      cur ^= 1;
+    }
+  }
+  MPF_CUDA(cudaMemcpyAsync(lb->hpart.data(), P[cur], sizeof(double) * kLbParts, cudaMemcpyDeviceToHost, s));
+  MPF_CUDA(cudaMemcpyAsync(lb->theta0, lb->N->params, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
+  MPF_CUDA(cudaStreamSynchronize(s));
+  double gtd = -host_sum(lb->hpart, 0, kLbParts);  // d = -v
+  int fb = 0;
+  if (!(gtd < 0.0)) {  // not a descent direction (or not finite): steepest descent
+    fb = 1;
+    MPF_CUDA(launch_lbfgs_pass(lb->v, lb->g, lb->g, n, nullptr, 0, 0.0, nullptr, 1.0, P[0], kLbParts, s));
+    MPF_CUDA(cudaMemcpyAsync(lb->hpart.data(), P[0], sizeof(double) * kLbParts, cudaMemcpyDeviceToHost, s));
+    MPF_CUDA(cudaStreamSynchronize(s));
+    gtd = -host_sum(lb->hpart, 0, kLbParts);
+  }
+  *h_gtd = gtd;
+  if (h_fallback) *h_fallback = fb;
+  lb->have_dir = true;
+  return MPF_OK;
+}
+
+mpf_status mpf_lbfgs_trial(mpf_lbfgs* lb, double alpha, void* stream) {
+  if (!lb) return fail(MPF_ERR_ARG, "NULL L-BFGS state");
+  if (!lb->have_dir) return fail(MPF_ERR_STATE, "L-BFGS trial without a direction");
+  MPF_CUDA(launch_lbfgs_trial(lb->N->params, lb->theta0, lb->v, lb->n, alpha, (cudaStream_t)stream));
+  return MPF_OK;
+}
+
+mpf_status mpf_lbfgs_accept(mpf_lbfgs* lb, float grad_scale, int32_t* h_stored, void* stream) {
+  if (!lb) return fail(MPF_ERR_ARG, "NULL L-BFGS state");
+  if (!lb->have_dir) return fail(MPF_ERR_STATE, "L-BFGS accept without a direction");
+  cudaStream_t s = (cudaStream_t)stream;
+  const long long n = lb->n;
+  const size_t stride = align256(sizeof(float) * n) / sizeof(float);
+  int slot = 0;  // a slot no stored pair uses (there are memory + 1)
+  for (; slot <= lb->m; ++slot) {
+    bool used = false;
+    for (int o : lb->order) used |= (o == slot);
+    if (!used) break;
+  }
+  double* part = lb->parts;  // s.y partials, then y.y partials
+  MPF_CUDA(launch_lbfgs_pair(lb->S + slot * stride, lb->Y + slot * stride, lb->g, lb->N->params, lb->theta0,
+                             lb->N->grads, n, grad_scale, part, kLbParts, s));
+  MPF_CUDA(cudaMemcpyAsync(lb->hpart.data(), part, sizeof(double) * 2 * kLbParts, cudaMemcpyDeviceToHost, s));
+  MPF_CUDA(cudaStreamSynchronize(s));
+  const double sy = host_sum(lb->hpart, 0, kLbParts), yy = host_sum(lb->hpart, kLbParts, kLbParts);
+  const bool keep = sy > 1e-10 && std::isfinite(sy) && std::isfinite(yy);
+  if (keep) {
+    if ((int)lb->order.size() == lb->m) lb->order.erase(lb->order.begin());
+    lb->order.push_back(slot);
+    lb->sy[slot] = sy;
+    lb->yy[slot] = yy;
+  }
+  if (h_stored) *h_stored = keep ? 1 : 0;
+  lb->have_g = true;
+  lb->have_dir = false;
+  return MPF_OK;
+}
+
+mpf_status mpf_lbfgs_reject(mpf_lbfgs* lb, void* stream) {
+  if (!lb) return fail(MPF_ERR_ARG, "NULL L-BFGS state");
+  if (!lb->have_dir) return fail(MPF_ERR_STATE, "L-BFGS reject without a direction");
+  MPF_CUDA(cudaMemcpyAsync(lb->N->params, lb->theta0, sizeof(float) * lb->n, cudaMemcpyDeviceToDevice,
+                           (cudaStream_t)stream));
+  lb->order.clear();
+  lb->have_dir = false;  // g still holds the gradient at theta0
+  return MPF_OK;
+}
+
+mpf_status mpf_lbfgs_step(mpf_lbfgs* lb, const float* d_images, int32_t n, const uint8_t* d_labels,
+                          const float* h_class_w, float alpha0, float beta, float c, int32_t max_backtracks,
+                          float grad_scale, float* h_out, void* stream) {
+  if (!lb || !d_images || !d_labels || !h_out) return fail(MPF_ERR_ARG, "NULL argument");
+  mpf_net* N = lb->N;
+  if (n < 1 || n > N->n_cap) return fail(MPF_ERR_DATA, "n must be in [1, bound n_images]");
+  if (n > 256) return fail(MPF_ERR_ARG, "at most 256 images per L-BFGS evaluation");
+  if (!(alpha0 > 0.f) || !(beta > 0.f && beta < 1.f) || !(c > 0.f && c < 1.f) || max_backtracks < 0)
+    return fail(MPF_ERR_ARG, "line search parameters: alpha0 > 0, 0 < beta < 1, 0 < c < 1, max_backtracks >= 0");
+  cudaStream_t s = (cudaStream_t)stream;
+  float* d_loss = scr(N, N->off_stage_loss);
+  float h_loss[256];
+  // loss and gradient of the full batch at the current parameters
+  auto evaluate = [&](double* L) -> mpf_status {
+    MPF_CUDA(cudaMemsetAsync(N->grads, 0, sizeof(float) * N->n_params, s));
+    mpf_status st = mpf_train_step(N, d_images, n, d_labels, h_class_w, d_loss, stream);
+    if (st != MPF_OK) return st;
+    MPF_CUDA(cudaMemcpyAsync(h_loss, d_loss, sizeof(float) * n, cudaMemcpyDeviceToHost, s));
+    MPF_CUDA(cudaStreamSynchronize(s));
+    double t = 0.0;
+    for (int i = 0; i < n; ++i) t += h_loss[i];
+    *L = t * grad_scale;
+    return MPF_OK;
+  };
+  mpf_status st;
+  if (!lb->have_g) {
+    st = evaluate(&lb->L);
+    if (st != MPF_OK) return st;
+    st = mpf_lbfgs_set_gradient(lb, grad_scale, stream);
+    if (st != MPF_OK) return st;
+  }
+  const double L0 = lb->L;
+  double gtd = 0.0;
+  int32_t fb = 0;
+  st = mpf_lbfgs_direction(lb, &gtd, &fb, stream);
+  if (st != MPF_OK) return st;
+  if (!std::isfinite(L0) || !std::isfinite(gtd)) {
+    lb->have_g = lb->have_dir = false;
+    return fail(MPF_ERR_DATA, "L-BFGS: non-finite loss or direction");
+  }
+  double alpha = lb->order.empty() ? (double)alpha0 : 1.0, L = L0;
+  int evals = 0;
+  bool accepted = false;
+  for (int it = 0; it <= max_backtracks; ++it, alpha *= beta) {
+    st = mpf_lbfgs_trial(lb, alpha, stream);
+    if (st != MPF_OK) return st;
+    st = evaluate(&L);
+    if (st != MPF_OK) return st;
+    ++evals;
+    if (std::isfinite(L) && L <= L0 + (double)c * alpha * gtd) {
+      accepted = true;
+      break;
+    }
+  }
+  if (accepted) {
+    st = mpf_lbfgs_accept(lb, grad_scale, nullptr, stream);
+    if (st != MPF_OK) return st;
+    lb->L = L;
+  } else {
+    st = mpf_lbfgs_reject(lb, stream);
+    if (st != MPF_OK) return st;
+    L = L0;
+  }
+  N->have_fwd = false;
+  h_out[0] = (float)L0;
+  h_out[1] = (float)L;
+  h_out[2] = accepted ? (float)alpha : 0.f;
+  h_out[3] = accepted ? 1.f : 0.f;
+  h_out[4] = (float)evals;
+  h_out[5] = (float)fb;
+  h_out[6] = (float)lb->order.size();
   return MPF_OK;
 }
 

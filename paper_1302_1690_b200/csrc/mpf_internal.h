@@ -211,6 +211,13 @@ cudaError_t launch_label_count(const uint8_t* labels, int n, int hw, int classes
 cudaError_t launch_sqnorm(const float* g, long long n, double* part, int nb, double* out, cudaStream_t s);
 cudaError_t launch_armijo_axpy(float* theta, const float* theta0, const float* g, long long n, float step,
                                cudaStream_t s);
+cudaError_t launch_lbfgs_gset(float* gprev, const float* g, long long n, float scale, cudaStream_t s);
+cudaError_t launch_lbfgs_pair(float* S, float* Y, float* gprev, const float* theta, const float* theta0, const float* g,
+                              long long n, float scale, double* part, int nb, cudaStream_t s);
+cudaError_t launch_lbfgs_pass(double* v, const float* x, const float* z, long long n, const double* part_in, int mode,
+                              double rho, double* a_slot, double post, double* part_out, int nb, cudaStream_t s);
+cudaError_t launch_lbfgs_trial(float* theta, const float* theta0, const double* v, long long n, double alpha,
+                               cudaStream_t s);
 cudaError_t launch_mirror_pad(const float* in, float* out, long long planes, int H, int W, int pt, int pl, int Hp, int Wp,
                               cudaStream_t s);
 cudaError_t launch_class_hist(const uint8_t* labels, long long total, int classes, unsigned long long* counts,

@@ -14,6 +14,8 @@ from __future__ import annotations
 
 from typing import List
 
+import numpy as np
+
 
 def shard(global_batch: int, world: int, rank: int) -> range:
     """Positions (within one global batch) of the images rank `rank` owns."""
@@ -46,3 +48,50 @@ def max_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def all_sum_scalar(value: float, device=None, group=None) -> float:
+    """Sum of a host scalar over ranks in fp64 (the full-batch loss of L-BFGS)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return float(t.item())
+
+
+def lbfgs_iteration(ops, alpha0: float, beta: float, c: float, max_backtracks: int) -> dict:
+    """One full-batch L-BFGS iteration (reading R21) driven
+    from the host over `ops`, whose evaluate() returns the loss summed over ALL ranks after
+    summing the gradient buffer over them (dist.allreduce_grads), so every rank sees the same
+    gradient and loss and takes the same decisions; the vector work stays in ops' kernels.
+
+    ops: .have_g, .L, .n_pairs, evaluate() -> L, set_gradient(), direction() -> (gtd, fallback),
+         trial(alpha), accept() -> stored (bool), reject().
+    """
+    if not ops.have_g:
+        ops.L = ops.evaluate()
+        ops.set_gradient()
+    L0 = ops.L
+    gtd, fallback = ops.direction()
+    if not (np.isfinite(L0) and np.isfinite(gtd)):
+        raise FloatingPointError("L-BFGS: non-finite loss or direction")
+    alpha = alpha0 if ops.n_pairs == 0 else 1.0
+    L, evals, accepted = L0, 0, False
+    for _ in range(max_backtracks + 1):
+        ops.trial(alpha)
+        L = ops.evaluate()
+        evals += 1
+        if np.isfinite(L) and L <= L0 + c * alpha * gtd:
+            accepted = True
+            break
+        alpha *= beta
+    if accepted:
+        ops.accept()
+        ops.L = L
+    else:
+        ops.reject()
+        L = L0
+    return {"loss0": L0, "loss": L, "alpha": alpha if accepted else 0.0, "accepted": accepted, "evals": evals,
+            "fallback": bool(fallback), "pairs": ops.n_pairs}

@@ -260,3 +260,98 @@ class MPFNet:
 
     def check(self, stream=None) -> None:
         L.check(self.lib.mpf_check(self.h, _stream_ptr(stream)), "mpf_check")
+
+
+class Lbfgs:
+    """Full-batch L-BFGS on an MPFNet's parameters (mpf_lbfgs_*, reading R21).
+
+    step(): one iteration on one GPU inside libmpf (mpf_lbfgs_step).
+    step_allreduce(): the same iteration over a data-parallel group: each rank evaluates its
+    shard, the gradient buffer and the loss are summed over ranks, and the host loop of
+    dist.lbfgs_iteration drives the same primitives on every rank."""
+
+    def __init__(self, net: "MPFNet", memory: int = 10):
+        self.net = net
+        self.lib = net.lib
+        self.memory = memory
+        h = ctypes.c_void_p()
+        L.check(self.lib.mpf_lbfgs_create(net.h, int(memory), ctypes.byref(h)), "mpf_lbfgs_create")
+        self.h = h
+        self.have_g, self.L, self.n_pairs = False, 0.0, 0
+        self._ctx = None
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            try:
+                self.lib.mpf_lbfgs_destroy(h)
+            except Exception:
+                pass
+            self.h = None
+
+    def reset(self) -> None:
+        L.check(self.lib.mpf_lbfgs_reset(self.h), "mpf_lbfgs_reset")
+        self.have_g, self.n_pairs = False, 0
+
+    def step(self, images: torch.Tensor, labels: torch.Tensor, alpha0: float = 1.0, beta: float = 0.5,
+             c: float = 1e-4, max_backtracks: int = 10, class_w=None, grad_scale: float = None,
+             stream=None) -> dict:
+        """One iteration over the whole batch `images` (the training set); grad_scale defaults to 1/n."""
+        n = images.shape[0]
+        cw = None
+        if class_w is not None:
+            cw = (ctypes.c_float * self.net.geom.classes)(*[float(v) for v in class_w])
+        out = (ctypes.c_float * 7)()
+        gs = 1.0 / n if grad_scale is None else float(grad_scale)
+        L.check(self.lib.mpf_lbfgs_step(self.h, _ptr(images), n, _ptr(labels), cw, float(alpha0), float(beta),
+                                        float(c), int(max_backtracks), gs, out, _stream_ptr(stream)),
+                "mpf_lbfgs_step")
+        self.n_pairs = int(out[6])
+        return {"loss0": out[0], "loss": out[1], "alpha": out[2], "accepted": bool(out[3]), "evals": int(out[4]),
+                "fallback": bool(out[5]), "pairs": int(out[6])}
+
+    # ---------------------------------------------------------------- primitives (dist.lbfgs_iteration ops)
+    def evaluate(self) -> float:
+        from . import dist as D
+        images, labels, class_w, gs, group = self._ctx
+        self.net.zero_grads()
+        loss = self.net.train_step(images, labels, class_w=class_w)
+        D.allreduce_grads(self.net.grads, group)
+        return D.all_sum_scalar(float(loss.double().sum().item()) * gs, device=self.net.device, group=group)
+
+    def set_gradient(self) -> None:
+        L.check(self.lib.mpf_lbfgs_set_gradient(self.h, float(self._ctx[3]), None), "mpf_lbfgs_set_gradient")
+        self.have_g = True
+
+    def direction(self):
+        gtd, fb = ctypes.c_double(), ctypes.c_int32()
+        L.check(self.lib.mpf_lbfgs_direction(self.h, ctypes.byref(gtd), ctypes.byref(fb), None),
+                "mpf_lbfgs_direction")
+        return gtd.value, bool(fb.value)
+
+    def trial(self, alpha: float) -> None:
+        L.check(self.lib.mpf_lbfgs_trial(self.h, float(alpha), None), "mpf_lbfgs_trial")
+
+    def accept(self) -> bool:
+        stored = ctypes.c_int32()
+        L.check(self.lib.mpf_lbfgs_accept(self.h, float(self._ctx[3]), ctypes.byref(stored), None),
+                "mpf_lbfgs_accept")
+        if stored.value:
+            self.n_pairs = min(self.n_pairs + 1, self.memory)
+        return bool(stored.value)
+
+    def reject(self) -> None:
+        L.check(self.lib.mpf_lbfgs_reject(self.h, None), "mpf_lbfgs_reject")
+        self.n_pairs = 0
+
+    def step_allreduce(self, images: torch.Tensor, labels: torch.Tensor, global_images: int, alpha0: float = 1.0,
+                       beta: float = 0.5, c: float = 1e-4, max_backtracks: int = 10, class_w=None,
+                       group=None) -> dict:
+        """One iteration whose full batch is the union of every rank's `images`
+        (global_images in total; grad_scale = 1 / global_images).  Runs on the default stream."""
+        from . import dist as D
+        self._ctx = (images, labels, class_w, 1.0 / global_images, group)
+        try:
+            return D.lbfgs_iteration(self, alpha0, beta, c, max_backtracks)
+        finally:
+            self._ctx = None

@@ -79,3 +79,113 @@ def test_gloo_world2_gradient_sum_equals_full_batch(tmp_path):
     assert np.allclose(r0[:n], g_full, rtol=1e-12, atol=1e-14)
     assert np.allclose(r0[n:2 * n], params - cfg.lr * g_full / B, rtol=1e-12, atol=1e-14)
     assert r0[-1] == 2.0  # max over ranks
+
+
+class _OracleLbfgsOps:
+    """dist.lbfgs_iteration ops over numpy + the oracle (there is no GPU here): the
+    shard's gradient is summed over ranks with dist.allreduce_grads and the loss with
+    dist.all_sum_scalar, exactly as net.Lbfgs.evaluate does on the GPU path."""
+
+    def __init__(self, cfg, images, labels, theta, B, memory):
+        self.cfg, self.images, self.labels, self.B, self.m = cfg, images, labels, B, memory
+        self.theta, self.have_g, self.L, self.n_pairs = theta.copy(), False, 0.0, 0
+        self.S, self.Y = [], []
+
+    def evaluate(self):
+        import oracle
+        g = np.zeros_like(self.theta)
+        L = 0.0
+        for i in range(len(self.images)):
+            loss, n, gi, _ = oracle.o1_image(self.cfg.layers, self.cfg.P, self.theta, self.images[i].astype(np.float64),
+                                             self.labels[i], threads=1, need_probs=False)
+            g += gi / n
+            L += loss / n
+        t = torch.tensor(g)
+        D.allreduce_grads(t)
+        self.grad = t.numpy() / self.B
+        return D.all_sum_scalar(L) / self.B
+
+    def set_gradient(self):
+        self.g, self.have_g = self.grad, True
+
+    def direction(self):
+        from oracle import o2
+        self.theta0 = self.theta.copy()
+        self.d = -o2.lbfgs_two_loop(self.g, self.S, self.Y)
+        gtd = float(self.g @ self.d)
+        fb = not gtd < 0
+        if fb:
+            self.d, gtd = -self.g, -float(self.g @ self.g)
+        return gtd, fb
+
+    def trial(self, alpha):
+        self.theta = self.theta0 + alpha * self.d
+
+    def accept(self):
+        s, y = self.theta - self.theta0, self.grad - self.g
+        self.g = self.grad
+        if float(s @ y) > 1e-10:
+            self.S.append(s)
+            self.Y.append(y)
+            if len(self.S) > self.m:
+                del self.S[0], self.Y[0]
+            self.n_pairs = len(self.S)
+            return True
+        return False
+
+    def reject(self):
+        self.theta = self.theta0
+        self.S, self.Y, self.n_pairs = [], [], 0
+
+
+def _lbfgs_worker(rank, world, port, B, iters, out_dir):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = S.CONFIGS["cfg1"]
+        images, labels = S.make_batch(cfg, D.batch_indices(0, B, world, rank))
+        ops = _OracleLbfgsOps(cfg, images, labels, S.init_params(cfg).astype(np.float64), B, 3)
+        rec = []
+        for _ in range(iters):
+            r = D.lbfgs_iteration(ops, 0.5, 0.5, 1e-4, 8)
+            rec += [r["loss"], r["alpha"], r["evals"], r["pairs"]]
+        np.save(os.path.join(out_dir, f"l{rank}.npy"), np.concatenate([ops.theta, rec]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_lbfgs_equals_full_batch_oracle(tmp_path):
+    """Full-batch L-BFGS over two ranks ("full-batch"): the host
+    loop dist.lbfgs_iteration with the gradient and loss summed over ranks takes the same
+    steps as the single-process oracle o2.lbfgs_step on the whole batch."""
+    import torch.multiprocessing as mp
+    from oracle import o2
+    import oracle
+    B, world, iters = 4, 2, 3
+    port = _free_port()
+    mp.start_processes(_lbfgs_worker, args=(world, port, B, iters, str(tmp_path)), nprocs=world,
+                       start_method="spawn")
+    r0, r1 = (np.load(tmp_path / f"l{r}.npy") for r in range(world))
+    assert np.array_equal(r0, r1)
+    cfg = S.CONFIGS["cfg1"]
+    images, labels = S.make_batch(cfg, D.batch_indices(0, B, 1, 0))
+
+    def eval_lg(theta):
+        g, L = np.zeros_like(theta), 0.0
+        for i in range(B):
+            loss, n, gi, _ = oracle.o1_image(cfg.layers, cfg.P, theta, images[i].astype(np.float64), labels[i],
+                                             threads=1, need_probs=False)
+            g += gi / n
+            L += loss / n
+        return L / B, g / B
+
+    st, theta, rec = {}, S.init_params(cfg).astype(np.float64), []
+    for _ in range(iters):
+        theta, a, L0, L1, ok, ev, fb = o2.lbfgs_step(st, theta, eval_lg, 3, 0.5, 0.5, 1e-4, 8)
+        rec += [L1, a, ev, len(st["S"])]
+    n = theta.size
+    assert np.allclose(r0[:n], theta, rtol=1e-9, atol=1e-12)
+    assert np.allclose(r0[n:], rec, rtol=1e-9, atol=1e-12)
+    assert rec[0] < eval_lg(S.init_params(cfg).astype(np.float64))[0]

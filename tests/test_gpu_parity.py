@@ -580,3 +580,83 @@ def test_armijo_step_vs_oracle():
     assert ev_o >= 2  # the test exercises backtracking
     assert rel_l2(net.params.cpu().numpy(), t_o) <= TOL_TF32
     assert np.all(net.grads.cpu().numpy() == 0.0)
+
+
+def _lbfgs_oracle_eval(cfg, images, labels, n):
+    def eval_lg(theta):
+        o = oracle_step(cfg.layers, cfg.P, images.astype(np.float64), labels, theta, engine="o2")
+        return float(np.sum(o["loss"])) / n, o["grad_sum"] / n
+    return eval_lg
+
+
+def test_lbfgs_step_vs_oracle():
+    """mpf_lbfgs_step (R21): four full-batch L-BFGS iterations
+    on two cfg2 images (memory 3, alpha0 large enough to backtrack on the first iteration)
+    take the oracle's decisions (evaluations, accepted alpha, stored pairs) and reach the
+    oracle's losses and parameters."""
+    from paper_1302_1690_b200.net import Lbfgs
+    cfg = S.CONFIGS["cfg2"]
+    n = 2
+    images, labels = S.make_batch(cfg, [0, 1])
+    params = S.init_params(cfg)
+    eval_lg = _lbfgs_oracle_eval(cfg, images, labels, n)
+    net = MPFNet(cfg.layers, cfg.P, cfg.H, cfg.W, max_images=n)
+    net.set_params(params.astype(np.float32))
+    lb = Lbfgs(net, memory=3)
+    x, y = torch.tensor(images, device="cuda"), torch.tensor(labels, device="cuda")
+    st, theta = {}, params.astype(np.float64)
+    alpha0, beta, c = 40.0, 0.5, 1e-4
+    backtracked = False
+    for it in range(4):
+        theta, a_o, L0_o, L1_o, ok_o, ev_o, fb_o = o2.lbfgs_step(st, theta, eval_lg, 3, alpha0, beta, c, 8)
+        r = lb.step(x, y, alpha0=alpha0, beta=beta, c=c, max_backtracks=8)
+        assert (r["accepted"], r["evals"], r["fallback"], r["pairs"]) == (ok_o, ev_o, fb_o, len(st["S"])), (it, r)
+        assert r["alpha"] == np.float32(a_o)
+        assert abs(r["loss0"] - L0_o) <= TOL_TF32 * abs(L0_o)
+        assert abs(r["loss"] - L1_o) <= TOL_TF32 * abs(L1_o)
+        backtracked |= ev_o >= 2
+    assert backtracked and r["pairs"] >= 2
+    assert rel_l2(net.params.cpu().numpy(), theta) <= TOL_TF32
+
+
+def test_lbfgs_allreduce_driver_matches_step():
+    """The host-driven iteration (dist.lbfgs_iteration over the mpf_lbfgs primitives, what a
+    data-parallel group runs) equals mpf_lbfgs_step on one GPU: same decisions and the same
+    parameters after three iterations (the cfg4 net on 126^2 images)."""
+    from paper_1302_1690_b200.net import Lbfgs
+    cfg = _cfg4s()
+    n = 2
+    images, labels = S.make_batch(cfg, [0, 1])
+    params = S.init_params(cfg).astype(np.float32)
+    x, y = torch.tensor(images, device="cuda"), torch.tensor(labels, device="cuda")
+    nets = []
+    for _ in range(2):
+        net = MPFNet(cfg.layers, cfg.P, cfg.H, cfg.W, max_images=n)
+        net.set_params(params)
+        nets.append((net, Lbfgs(net, memory=5)))
+    for it in range(3):
+        a = nets[0][1].step(x, y, alpha0=0.05)
+        b = nets[1][1].step_allreduce(x, y, global_images=n, alpha0=0.05)
+        assert (a["accepted"], a["evals"], a["pairs"]) == (b["accepted"], b["evals"], b["pairs"]), (it, a, b)
+        assert a["alpha"] == np.float32(b["alpha"])
+        # the gradient sums use float atomics, so the two runs agree to rounding, not bitwise
+        assert abs(a["loss"] - b["loss"]) <= 1e-4 * abs(a["loss"])
+    assert rel_l2(nets[0][0].params.cpu().numpy(), nets[1][0].params.cpu().numpy().astype(np.float64)) <= 1e-4
+    assert a["loss"] < a["loss0"]
+
+
+def test_lbfgs_primitive_errors():
+    """State errors of the mpf_lbfgs primitives (include/mpf.h): no direction without a
+    gradient, no trial/accept/reject without a direction, memory bounds."""
+    from paper_1302_1690_b200.net import Lbfgs
+    cfg = S.CONFIGS["cfg1"]
+    net = MPFNet(cfg.layers, cfg.P, cfg.H, cfg.W, max_images=1)
+    with pytest.raises(MpfError):
+        Lbfgs(net, memory=0)
+    lb = Lbfgs(net, memory=2)
+    with pytest.raises(MpfError):
+        lb.direction()
+    with pytest.raises(MpfError):
+        lb.trial(1.0)
+    with pytest.raises(MpfError):
+        lb.reject()
