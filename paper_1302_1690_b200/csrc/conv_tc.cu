@@ -973,6 +973,8 @@ struct WgTcParams {
   uint32_t a_bytes, b_bytes, stage_bytes;
   int n_stages_ring;
   uint32_t tmem_cols;
+  const float* dy;       // A operand straight from global (the TMEM-A variant)
+  uint32_t a_col0;       // TMEM column of the two A slots (TMEM-A variant)
 };
 
 template <int MT>  // output channels per tile: 128, or 64 (M = 64 MMA) when C_out <= 64
@@ -1080,6 +1082,154 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) ptx::tmem_dealloc(tmem, p.tmem_cols);
 }
 
+// The same GEMM with the dY operand in tensor memory (kind::tf32, A from TMEM): with A in
+// shared memory the tensor core re-reads the 4 KB dY tile of every K step once per group
+// (G times) and the shared-memory port, not the MMA, sets the pace.  Here
+// the 8 epilogue warps, idle during the main loop, load dY straight from global memory
+// (lane = output channel, a warp reads one 128-B row of dY per position, coalesced) and
+// write it to one of two TMEM A slots of 64 columns (= the 64 positions of a stage,
+// K-major: lane co, column p); the MMA warp reads A from there and only the X slabs go
+// through shared memory.  Same MMAs per group as wgrad_tc_kernel<128>; the split-K
+// partition can differ (fewer groups per CTA), so the totals agree to rounding (tested).
+// Opt-in (MPF_WGRAD_TS=1): measured on cfg4 at 6.07 / 2.91 / 5.00 ms for FC1 / C3 / C5
+// against 6.38 / 2.80 / 4.52 ms, and only 5.66 / 2.58 / 4.35 ms even with the dY loads
+// removed, i.e. the tensor pipe, not the A re-reads, bounds these GEMMs.
+__global__ void __launch_bounds__(kThreads, 1)
+    wgrad_ts_kernel(const __grid_constant__ CUtensorMap tmX, WgTcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t sbase = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t sBar = sbase + p.n_stages_ring * p.stage_bytes;
+  const uint32_t barFull = sBar, barEmpty = sBar + 8 * p.n_stages_ring, barT = sBar + 16 * p.n_stages_ring;
+  const uint32_t aFull = barT + 8, aEmpty = barT + 24;  // 2 A slots each
+  const uint32_t sTmemSlot = barT + 40;
+  uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (sTmemSlot - ptx::smem_u32(smem_raw)));
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int mt = blockIdx.x % p.m_tiles;
+  const int set = (blockIdx.x / p.m_tiles) % p.n_sets;
+  const int split = blockIdx.x / (p.m_tiles * p.n_sets);
+  const int g0 = (int)((long long)set * p.n_groups / p.n_sets);
+  const int G = (int)((long long)(set + 1) * p.n_groups / p.n_sets) - g0;
+  const int N = 32 * p.k;
+  const long long pbeg = (long long)split * p.chunk_stages * kWR;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmX);
+    for (int i = 0; i < p.n_stages_ring; ++i) {
+      ptx::mbar_init(barFull + 8 * i, 1);
+      ptx::mbar_init(barEmpty + 8 * i, 1);
+    }
+    ptx::mbar_init(barT, 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(aFull + 8 * i, kEpiWarps);
+      ptx::mbar_init(aEmpty + 8 * i, 1);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(sTmemSlot, p.tmem_cols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot_ptr;
+  const int n_st = p.chunk_stages;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int st = 0; st < n_st; ++st) {
+        const int slot = st % p.n_stages_ring;
+        ptx::mbar_wait(barEmpty + 8 * slot, ((st / p.n_stages_ring) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(barFull + 8 * slot, G * p.b_bytes);
+        const uint32_t sa = sbase + slot * p.stage_bytes;
+        const int row = (int)(pbeg + (long long)st * kWR);
+        for (int g = 0; g < G; ++g) {
+          const int ng = g0 + g, ky = ng / p.n_cc, cc = ng % p.n_cc;
+          ptx::tma_load_2d(sa + g * p.b_bytes, &tmX, barFull + 8 * slot, cc * kKC, row + ky * p.gc);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = ptx::idesc_tf32_bmn(128, N);
+    for (int st = 0; st < n_st; ++st) {
+      const int slot = st % p.n_stages_ring, as = st & 1;
+      ptx::mbar_wait(aFull + 8 * as, (st >> 1) & 1);
+      ptx::mbar_wait(barFull + 8 * slot, (st / p.n_stages_ring) & 1);
+      ptx::tc_fence_after();
+      const uint32_t sa = sbase + slot * p.stage_bytes;
+      const uint64_t bd0 = ptx::sdesc_mn_sw128_32b(sa, 128, 512);
+      const uint32_t a0 = tmem + p.a_col0 + as * kWR;
+      for (int g = 0; g < G; ++g) {
+#pragma unroll
+        for (int r8 = 0; r8 < kWR / 8; ++r8) {
+          const uint64_t bd = bd0 + (uint64_t)((g * p.b_bytes + r8 * 1024) >> 4);
+          ptx::mma_tf32_ts_elect(tmem + g * N, a0 + r8 * 8, bd, idesc, (st | r8) != 0);
+        }
+      }
+      ptx::mma_commit_elect(barEmpty + 8 * slot);
+      ptx::mma_commit_elect(aEmpty + 8 * as);
+    }
+    ptx::mma_commit_elect(barT);
+  } else {
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    const int co = mt * 128 + q * 32 + lane;
+    const bool row_ok = co < p.cout;
+    // ---- A producer: dY[p][co] of this stage's 32 positions of `half` -> TMEM lane co
+    {
+      const float* src = p.dy + (row_ok ? co : 0);
+      const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+      // two register buffers: the loads of stage st + 1 are in flight while stage st waits
+      // for its TMEM slot and is written
+      uint32_t r0[32], r1[32];
+      auto load = [&](int st, uint32_t (&r)[32]) {
+        const long long pr = pbeg + (long long)st * kWR + half * 32;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const long long pj = pr + j;
+          r[j] = (row_ok && st < n_st && pj < p.P_tot) ? __float_as_uint(__ldg(src + pj * p.cout)) : 0u;
+        }
+      };
+      auto put = [&](int st, const uint32_t (&r)[32]) {
+        const int as = st & 1;
+        ptx::mbar_wait(aEmpty + 8 * as, ((st >> 1) & 1) ^ 1);
+        ptx::tc_fence_after();
+        ptx::tmem_st32(tmem + lane_addr + p.a_col0 + as * kWR + half * 32, r);
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(aFull + 8 * as);
+      };
+      load(0, r0);
+      for (int st = 0; st < n_st; st += 2) {
+        load(st + 1, r1);
+        put(st, r0);
+        if (st + 1 >= n_st) break;
+        load(st + 2, r0);
+        put(st + 1, r1);
+      }
+    }
+    // ---- epilogue (as wgrad_tc_kernel<128>)
+    ptx::mbar_wait(barT, 0);
+    ptx::tc_fence_after();
+    const int K = p.k * p.k * p.cin;
+    float* dst = p.part + ((long long)split * p.cout + (row_ok ? co : 0)) * K;
+    for (int g = 0; g < G; ++g) {
+      const int ng = g0 + g, ky = ng / p.n_cc, cc = ng % p.n_cc;
+      for (int c0 = half * 16; c0 < N; c0 += 32) {
+        float v[16];
+        ptx::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + g * N + c0, v);
+        if (row_ok) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int n = c0 + j, kx = n / 32, ci = cc * kKC + (n % 32);
+            if (ci < p.cin) dst[(ky * p.k + kx) * p.cin + ci] = n_st > 0 ? v[j] : 0.f;
+          }
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) ptx::tmem_dealloc(tmem, p.tmem_cols);
+}
+
 }  // namespace
 
 cudaError_t make_tmap_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
@@ -1123,8 +1273,16 @@ cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits_out, cudaStream_t 
   if (p.G > p.n_groups) p.G = p.n_groups;
   p.n_sets = (p.n_groups + p.G - 1) / p.G;
   const int MT = (a.cout <= 64 && !getenv("MPF_WGRAD_M128")) ? 64 : 128;
+  // TMEM-A variant (MT = 128): two A slots of kWR columns next to the accumulators
+  const char* tse = getenv("MPF_WGRAD_TS");
+  const bool ts = MT == 128 && N <= 256 && (tse ? atoi(tse) != 0 : false);
+  if (ts) {
+    p.G = (512 - 2 * kWR) / N;
+    if (p.G > p.n_groups) p.G = p.n_groups;
+    p.n_sets = (p.n_groups + p.G - 1) / p.G;
+  }
   p.m_tiles = (a.cout + MT - 1) / MT;
-  p.a_bytes = (MT / 32) * kWR * 128;
+  p.a_bytes = ts ? 0 : (MT / 32) * kWR * 128;
   p.b_bytes = (kWR + 8) * 128;
   p.stage_bytes = p.a_bytes + p.G * p.b_bytes;
   const size_t budget = 225 * 1024 - 1024 - 256;
@@ -1137,8 +1295,10 @@ cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits_out, cudaStream_t 
     p.n_stages_ring = 2;
   }
   uint32_t cols = 32;
-  while (cols < (uint32_t)(p.G * N)) cols <<= 1;
+  while (cols < (uint32_t)(p.G * N + (ts ? 2 * kWR : 0))) cols <<= 1;
   p.tmem_cols = cols;
+  p.a_col0 = (uint32_t)(p.G * N);
+  p.dy = a.dy;
   const long long total_stages = (p.P_tot + kWR - 1) / kWR;
   const int per_split_blocks = p.m_tiles * p.n_sets;
   int splits = num_sms() / per_split_blocks;  // one wave of co-resident CTAs
@@ -1158,6 +1318,12 @@ cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits_out, cudaStream_t 
   e = make_map(&X, a.x, (uint64_t)a.cin, (uint64_t)p.P_tot, (uint32_t)(kWR + 8), CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   if (e != cudaSuccess) return e;
   const size_t smem = 1024 + (size_t)p.n_stages_ring * p.stage_bytes + 256;
+  if (ts) {
+    e = cudaFuncSetAttribute(wgrad_ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    wgrad_ts_kernel<<<splits * per_split_blocks, kThreads, smem, s>>>(X, p);
+    return cudaGetLastError();
+  }
   auto kern = MT == 64 ? wgrad_tc_kernel<64> : wgrad_tc_kernel<128>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
