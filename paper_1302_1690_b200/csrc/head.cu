@@ -37,10 +37,12 @@ constexpr int kTP = 64;  // positions per tile
 constexpr int kThr = 256;
 constexpr int kMaxC = 16;
 
+// Round to TF32, nearest with ties away from zero: the same result as cvt.rna.tf32.f32
+// for every finite value, +-inf and NaN (adding half an ulp of the 10-bit mantissa to
+// the magnitude bits carries into the exponent exactly as rounding up does), in two
+// integer instructions instead of the four of the guarded conversion.
 __device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
 __device__ __forceinline__ float act_der(int act, float y) {
@@ -139,7 +141,7 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
   for (int c = 0; c < NC; ++c) accL[c] = 0.f;
   __syncthreads();  // s_w is filled (the barrier init sync above precedes nothing else)
   // VEC: W_L[:, 4g..4g+3] of this lane's phase-B channel group, held in registers
-  constexpr bool kW4Reg = VEC && NC <= 4;
+  constexpr bool kW4Reg = VEC && NC <= 8;
   float4 w4reg[kW4Reg ? NC : 1];
   if constexpr (kW4Reg) {
     const int g = lane + (pairB ? 32 * (warp & 1) : 0);
@@ -166,7 +168,17 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
     const long long p0 = (long long)tt * kTP;
     // ---------------------------------------------------------- phase 0: labels (lanes 0..7)
     if (lane < 8) {
-      const int lab = head_label(a, img, p0 + pw0 + lane, per_img, frag_sz, TRAIN);
+      int lab;
+      if (TRAIN && a.lab_frag) {  // pre-gathered in head-position order (launch_label_frag)
+        const long long pos = p0 + pw0 + lane;
+        lab = kLabBeyond;
+        if (pos < per_img) {
+          lab = a.lab_frag[(long long)img * per_img + pos];
+          if (lab == kLabFragPad) lab = kLabPad;
+        }
+      } else {
+        lab = head_label(a, img, p0 + pw0 + lane, per_img, frag_sz, TRAIN);
+      }
       s_lab[pw0 + lane] = lab;
     }
     if (bulk) {
@@ -447,6 +459,19 @@ cudaError_t launch_nc(const HeadArgs& a, size_t smem, cudaStream_t s) {
   return launch_k<NC, true, false>(a, smem, s);
 }
 
+// The label of every head position, gathered once per step in position order through
+// the fragment -> pixel map (head_label; R2, R7), so the head reads 64 contiguous bytes
+// per tile instead of decoding the mixed-radix index per position.
+__global__ void label_frag_kernel(HeadArgs a, uint8_t* __restrict__ out, long long per_img, int frag_sz) {
+  const long long total = (long long)a.n * per_img;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int img = (int)(e / per_img);
+    const int lab = head_label(a, img, e - (long long)img * per_img, per_img, frag_sz, true);
+    out[e] = (uint8_t)(lab == kLabPad ? kLabFragPad : lab);
+  }
+}
+
 }  // namespace
 
 int head_tiles_per_image(long long per_img) { return (int)((per_img + kTP - 1) / kTP); }
@@ -471,6 +496,14 @@ cudaError_t launch_head2(const HeadArgs& a, cudaStream_t s) {
     case 5: return launch_nc<5>(a, smem, s);
     default: return a.C <= 8 ? launch_nc<8>(a, smem, s) : launch_nc<16>(a, smem, s);
   }
+}
+
+cudaError_t launch_label_frag(const HeadArgs& a, uint8_t* out, cudaStream_t s) {
+  const long long per_img = (long long)a.F * a.gr * a.gc;
+  const long long total = (long long)a.n * per_img;
+  const long long blocks = (total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16;
+  label_frag_kernel<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(a, out, per_img, a.gr * a.gc);
+  return cudaGetLastError();
 }
 
 }  // namespace mpf

@@ -212,6 +212,7 @@ static void layout_memory(Net* N, int n) {
   const Act& h = N->a[N->n_layers - 1];
   const long long h_pos = h.elems_per_image() / h.C;
   N->loss_parts = head_tiles_per_image(h_pos) * head_loss_parts_per_tile();
+  N->off_labfrag = s; s = align256(s + (size_t)n * h_pos);  // labels in head-position order
   size_t bp = (size_t)head_blocks((long long)head_tiles_per_image(h_pos) * n) *
               ((size_t)N->classes * h.C + N->classes + h.C);
   for (int l = 0; l < N->n_layers - 1; ++l) {
@@ -767,6 +768,10 @@ static mpf_status backward_impl(Net* N, const uint8_t* d_labels, const float* h_
       LAUNCH(N, s, "head_loss_delta", L, 6.0 * pos * h.C * N->classes, pos * (8.0 * h.C + 1.0),
              launch_head_tc(hd, s));
     } else {
+      uint8_t* labf = (uint8_t*)(N->scratch + N->off_labfrag);
+      LAUNCH(N, s, "label_frag", L, 0.0, (double)n * h.F * h.gr * h.gc + (double)n * N->O_H * N->O_W,
+             launch_label_frag(hd, labf, s));
+      hd.lab_frag = labf;
       LAUNCH(N, s, "head_loss_delta", L, 6.0 * pos * h.C * N->classes, pos * (8.0 * h.C + 1.0),
              launch_head2(hd, s));
     }

@@ -67,7 +67,7 @@ struct Net {
   size_t tape_bytes = 0, scratch_bytes = 0;
   size_t off_Y = 0, off_dA = 0, off_dB = 0, off_dC = 0, off_bpart = 0, off_wpack = 0, off_part = 0,
          off_nlab = 0, off_lossp = 0, off_err = 0, off_rowloss = 0, off_stage_img = 0, off_stage_lab = 0,
-         off_stage_loss = 0, off_theta0 = 0, off_armijo = 0;
+         off_stage_loss = 0, off_theta0 = 0, off_armijo = 0, off_labfrag = 0;
   size_t stage_bytes = 0;  // one of the two host-input staging slots (images | labels)
   // host-buffer steps: inputs of step i + 1 are copied on copy_stream into the other
   // staging slot while step i computes (events order the slots' reuse)
@@ -196,8 +196,13 @@ struct HeadArgs {
   int* err;
   int n;
   int round_tf32;
+  const uint8_t* lab_frag;  // training: labels in head-position order (launch_label_frag), or NULL
 };
 int head_tiles_per_image(long long per_img);
+// labels gathered into head-position (fragment-major) order: out[img][pos] = class, 255
+// (ignored / outside the output grid) or kLabFragPad (padding of the fragment grid)
+constexpr int kLabFragPad = 254;
+cudaError_t launch_label_frag(const HeadArgs& a, uint8_t* out, cudaStream_t s);
 int head_loss_parts_per_tile();
 int head_blocks(long long total_tiles);
 bool head_supported(int C, int Ch);
