@@ -88,3 +88,62 @@ def compare_step(layers, g, o, tol, what=""):
     bad = {k: v for k, v in errs.items() if not v <= tol}
     assert not bad, f"{what}: rel L2 above {tol}: {bad} (all: {errs})"
     return errs
+
+
+def _tf32_round(t):
+    """Round to TF32 (nearest, ties away) on the fp32 bit pattern."""
+    import torch
+    b = t.detach().float().contiguous().view(torch.int32)
+    return ((b + 0x1000) & ~0x1FFF).view(torch.float32).to(t.dtype)
+
+
+def rounding_model_grads(layers, params, images, labels, prec):
+    """Expected rounding error of the GPU arithmetic, for deriving per-tensor tolerances on
+    random architectures (reading R22; not a reference for the values): the same network
+    as a dilated-convolution model (every patch output of the whole image, SURVEY.md §4
+    item 4) in CPU torch, fp32 arithmetic, with every convolution operand and every
+    gradient flowing into one rounded to TF32 when prec == "tf32" (tensor-core inputs;
+    fp32 accumulation).  Returns the mean over images of the per-image mean-loss gradient."""
+    import torch
+    import torch.nn.functional as Fn
+
+    class _R(torch.autograd.Function):
+        @staticmethod
+        def forward(ctx, x):
+            return _tf32_round(x)
+
+        @staticmethod
+        def backward(ctx, g):
+            return _tf32_round(g)
+
+    rnd = _R.apply if prec == "tf32" else (lambda v: v)
+    n = images.shape[0]
+    total = np.zeros(len(params))
+    for i in range(n):
+        th = torch.tensor(np.asarray(params, np.float32), requires_grad=True)
+        x = torch.tensor(np.asarray(images[i], np.float32))[None]
+        d, off, c = 1, 0, images.shape[1]
+        for L in layers:
+            if L.kind == S.POOL:
+                x = Fn.max_pool2d(x, L.k, stride=1, dilation=d)
+                d *= L.k
+                continue
+            nw = L.n_out * c * L.k * L.k
+            W = th[off:off + nw].reshape(L.n_out, c, L.k, L.k)
+            b = th[off + nw:off + nw + L.n_out]
+            off += nw + L.n_out
+            c = L.n_out
+            x = Fn.conv2d(rnd(x), rnd(W), b, dilation=d)
+            if L.act == S.TANH:
+                x = torch.tanh(x)
+            elif L.act == S.LOGISTIC:
+                x = torch.sigmoid(x)
+        logp = torch.log_softmax(x[0], dim=0)
+        t = torch.tensor(np.asarray(labels[i]).astype(np.int64))
+        m = t != 255
+        tt = torch.where(m, t, torch.zeros_like(t))
+        nll = -logp.gather(0, tt[None])[0]
+        loss = (nll * m).sum() / m.sum().clamp(min=1)
+        loss.backward()
+        total += th.grad.double().numpy()
+    return total

@@ -57,6 +57,77 @@ def test_random_archs_vs_o2(seed, prec, tol):
     compare_step(layers, g, o, tol, f"random arch seed {seed}")
 
 
+def _wide_arch(rng):
+    """A random net on the tensor-core paths with ragged shapes (input generation only):
+    1-2 pooling levels with k in {2, 3, 4}, one or two convs (k 1-4) before each pool,
+    channel counts that are multiples of 4 but rarely of 16 or 32 (ragged N tiles and
+    channel chunks), 1 or 4 input channels, tanh or logistic hidden activations, an s x s
+    FC, an optional hidden 1x1 FC and the linear softmax FC.  P is built backwards from the
+    head so the geometry is exact."""
+    act = [S.TANH, S.LOGISTIC][int(rng.integers(0, 2))]
+    chans = [16, 20, 24, 36, 44, 52, 68, 100]
+    blocks = []
+    for _ in range(int(rng.integers(1, 3))):
+        convs = [(int(rng.integers(1, 5)), int(rng.choice(chans))) for _ in range(int(rng.integers(1, 3)))]
+        blocks.append((convs, int(rng.choice([2, 3, 4]))))
+    s = int(rng.integers(1, 3))
+    size = s
+    for convs, kp in reversed(blocks):
+        size *= kp
+        for kc, _ in reversed(convs):
+            size += kc - 1
+    layers = []
+    for convs, kp in blocks:
+        layers += [S.C(kc, n, act) for kc, n in convs] + [S.MP(kp)]
+    layers.append(S.F(s, int(rng.choice([16, 40, 100])), act))
+    if rng.uniform() < 0.5:
+        layers.append(S.F(1, int(rng.choice([20, 36])), act))
+    layers.append(S.F(1, int(rng.integers(2, 6)), S.IDENTITY))
+    return tuple(layers), size
+
+
+@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("prec,tol", PRECS)
+def test_wide_random_archs_vs_o2(seed, prec, tol):
+    """Tensor-core convolutions, wgrads, MPF k = 2/3/4 and the head on random ragged
+    shapes (_wide_arch: conv -> conv blocks, 1x1 convs, logistic or tanh, 1 or 4 input
+    channels), 1-2 images of random size spanning several tiles and a ragged tail, against
+    the literal whole-image oracle O2: outputs and loss within the bar, and every W/b
+    gradient within max(bar, 3 x the error of the same arithmetic in a rounding model)
+    (reading R22: these random nets are far less well conditioned than the five configs;
+    e.g. a logistic conv -> conv block loses 5e-3 of the first layer's weight gradient to
+    plain fp32 rounding, in torch as on the GPU)."""
+    from tests.gpu_common import rounding_model_grads
+    rng = np.random.default_rng(900 + seed)
+    layers, P = _wide_arch(rng)
+    cin = 4 if seed % 2 else 1
+    n = int(rng.integers(1, 3))
+    H, W = int(rng.integers(P + 40, P + 140)), int(rng.integers(P + 40, P + 140))
+    images = rng.standard_normal((n, cin, H, W)).astype(np.float32)
+    C = layers[-1].n_out
+    labels = S.random_labels(rng, n, H - P + 1, W - P + 1, C)
+    params = S.init_params(layers, seed, in_channels=cin).astype(np.float32).astype(np.float64)
+    g = gpu_step(layers, P, images, labels, params, prec)
+    probs, losses, grads = [], [], []
+    for i in range(n):
+        ls, cnt, gr, pr = o2.train_image(layers, params, images[i].astype(np.float64), labels[i], P=P,
+                                         in_channels=cin)
+        probs.append(pr)
+        losses.append(ls / cnt if cnt else 0.0)
+        grads.append(gr / cnt if cnt else np.zeros_like(params))
+    want = np.sum(grads, axis=0)
+    model = rounding_model_grads(layers, params, images, labels, prec)
+    what = f"wide arch seed {seed} {prec}: {layers}, P={P}, cin={cin}"
+    assert rel_l2(g["probs"], np.stack(probs)) <= tol, what
+    assert rel_l2(g["loss"], np.array(losses)) <= tol, what
+    bad = {}
+    for nm, sl in param_slices(layers, cin):
+        e, e_model = rel_l2(g["grad_sum"][sl], want[sl]), rel_l2(model[sl], want[sl])
+        if not e <= max(tol, 3.0 * e_model):
+            bad[nm] = (e, e_model)
+    assert not bad, f"{what}: (error, rounding-model error) {bad}"
+
+
 def test_cfg2_batch_vs_o2():
     """configs[1]: 8 images of 128^2, one SGD step on the batch mean, TF32."""
     cfg = S.CONFIGS["cfg2"]
