@@ -135,9 +135,12 @@ __global__ void __launch_bounds__(256) conv_first_fwd_kernel(FirstConvArgs a) {
 constexpr int kWTH = 8, kWTW = 32;  // wgrad tile: 256 positions
 constexpr int kWCO = 8, kWT = 4;    // accumulators per thread: 8 maps x 4 taps
 
-template <int K>
-__global__ void __launch_bounds__(256, 3) conv_first_wgrad_kernel(FirstWgradArgs a) {
+// WT taps per thread: 4, or a whole kernel row (WT = K, K >= 5; 2 CTAs per SM) so each
+// staged delta vector feeds 8 K FMAs instead of 32.
+template <int K, int WT>
+__global__ void __launch_bounds__(256, WT > 4 ? 2 : 3) conv_first_wgrad_kernel(FirstWgradArgs a) {
   extern __shared__ float sm[];
+  constexpr int kWT = WT;
   constexpr int IW = kWTW + K - 1, IH = kWTH + K - 1;
   constexpr int NT = (K * K + kWT - 1) / kWT;  // tap groups
   const int coutp = a.n_cog * kWCO;
@@ -404,10 +407,16 @@ cudaError_t fwd_k(const FirstConvArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int K>
+// the row variant (WT = K) for K >= 5 unless MPF_FIRST_WGRAD_ROW=0
+static bool wgrad_row(int k) {
+  const char* e = getenv("MPF_FIRST_WGRAD_ROW");
+  return k >= 5 && (e ? atoi(e) != 0 : true);
+}
+
+template <int K, int WT>
 size_t wgrad_smem(int n_cog) {
   const int coutp = n_cog * kWCO;
-  constexpr int NT = (K * K + kWT - 1) / kWT;
+  constexpr int NT = (K * K + WT - 1) / WT;
   const int n_streams = 256 / (n_cog * NT);
   const size_t tile = (size_t)kWTH * kWTW * coutp;
   const size_t red = (size_t)n_streams * coutp * K * K;
@@ -415,14 +424,21 @@ size_t wgrad_smem(int n_cog) {
   return sizeof(float) * (bufs > red ? bufs : red);
 }
 
-template <int K>
-cudaError_t wgrad_k(const FirstWgradArgs& a, cudaStream_t s) {
-  const size_t smem = wgrad_smem<K>(a.n_cog);
-  cudaError_t e = cudaFuncSetAttribute(conv_first_wgrad_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+template <int K, int WT>
+cudaError_t wgrad_kw(const FirstWgradArgs& a, cudaStream_t s) {
+  const size_t smem = wgrad_smem<K, WT>(a.n_cog);
+  cudaError_t e = cudaFuncSetAttribute(conv_first_wgrad_kernel<K, WT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  conv_first_wgrad_kernel<K><<<a.n_blocks, 256, smem, s>>>(a);
+  conv_first_wgrad_kernel<K, WT><<<a.n_blocks, 256, smem, s>>>(a);
   return cudaGetLastError();
+}
+template <int K>
+cudaError_t wgrad_k(const FirstWgradArgs& a, cudaStream_t s) {
+  if constexpr (K >= 5) {
+    if (wgrad_row(K)) return wgrad_kw<K, K>(a, s);
+  }
+  return wgrad_kw<K, kWT>(a, s);
 }
 
 }  // namespace
@@ -458,7 +474,8 @@ bool first_conv_supported(int cin, int cout, int k) {
   return n_cog * NT <= 256;
 }
 
-int first_wgrad_blocks() { return 148 * 3; }  // 3 co-resident CTAs per SM overlap staging with compute
+// co-resident CTAs per SM overlap staging with compute: 3 (2 for the row variant)
+int first_wgrad_blocks(int k) { return 148 * (k > 0 && wgrad_row(k) ? 2 : 3); }
 
 cudaError_t launch_first_conv(FirstConvArgs a, cudaStream_t s) {
   a.n_cog = (a.cout + kFCO - 1) / kFCO;

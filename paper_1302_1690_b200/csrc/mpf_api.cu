@@ -204,7 +204,7 @@ static void layout_memory(Net* N, int n) {
   N->part_floats = max_part * (size_t)kMaxSplits;
   {  // the first layer's CUDA-core weight gradient writes one partial per CTA
     const LayerPlan& P0 = N->lp[0];
-    N->part_floats = std::max(N->part_floats, (size_t)first_wgrad_blocks() * P0.cout * P0.L.k * P0.L.k);
+    N->part_floats = std::max(N->part_floats, (size_t)first_wgrad_blocks(0) * P0.cout * P0.L.k * P0.L.k);
   }
   s = align256(s + sizeof(float) * N->part_floats);
   N->off_nlab = s; s = align256(s + sizeof(int) * n);
@@ -639,7 +639,7 @@ static mpf_status wgrad(Net* N, int l, const float* x, const float* dy, int n, c
     FirstWgradArgs f{};
     f.img = x; f.n = n; f.H = N->cfg.image_rows; f.W = N->cfg.image_cols;
     f.dy = dy; f.gr = o.gr; f.gc = o.gc; f.k = P.L.k; f.cout = P.cout;
-    f.part = part; f.n_blocks = first_wgrad_blocks();
+    f.part = part; f.n_blocks = first_wgrad_blocks(P.L.k);
     const int E = P.cout * P.L.k * P.L.k;
     LAUNCH(N, s, "wgrad_first", l, wflops, wbytes, launch_first_wgrad(f, s));
     LAUNCH(N, s, "wgrad_reduce", l, 0.0, 4.0 * (f.n_blocks + 1.0) * E,
