@@ -37,12 +37,10 @@ constexpr int kTP = 64;  // positions per tile
 constexpr int kThr = 256;
 constexpr int kMaxC = 16;
 
-// Round to TF32, nearest with ties away from zero: the same result as cvt.rna.tf32.f32
-// for every finite value, +-inf and NaN (adding half an ulp of the 10-bit mantissa to
-// the magnitude bits carries into the exponent exactly as rounding up does), in two
-// integer instructions instead of the four of the guarded conversion.
 __device__ __forceinline__ float tf32_rna(float x) {
-  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
 }
 
 __device__ __forceinline__ float act_der(int act, float y) {
