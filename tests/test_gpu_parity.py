@@ -277,6 +277,20 @@ def test_bad_label_is_reported():
     assert e.value.status == 3
 
 
+@pytest.mark.parametrize("name", ["cfg2", "cfg4s"])
+def test_nan_weight_propagates_to_loss_and_gradients(name):
+    """A NaN in the first layer's weights must reach the loss and the gradients through
+    every kernel of the step (TF32 rounding, activations, MPF, head), not be rounded or
+    pooled away into finite numbers."""
+    cfg = _cfg4s() if name == "cfg4s" else S.CONFIGS[name]
+    images, labels = S.make_batch(cfg, [0])
+    params = S.init_params(cfg)
+    params[0] = np.nan
+    g = gpu_step(cfg.layers, cfg.P, images, labels, params, "tf32")
+    assert np.all(np.isnan(g["loss"]))
+    assert np.isnan(g["grad_sum"]).any()
+
+
 def test_class_weights_vs_o1():
     cfg = S.CONFIGS["cfg1"]
     images, labels = S.make_batch(cfg, [1])
