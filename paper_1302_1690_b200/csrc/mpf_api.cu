@@ -184,6 +184,7 @@ static void layout_memory(Net* N, int n) {
   N->tape_bytes = std::max<size_t>(tape, 256);
   size_t s = 0;
   N->off_Y = s; s = align256(s + sizeof(float) * maxY);
+  N->y_floats = maxY;
   N->off_dA = s; s = align256(s + sizeof(float) * maxD);
   N->off_dB = s; s = align256(s + sizeof(float) * maxD);
   N->off_dC = s; s = align256(s + sizeof(float) * maxD);  // third delta buffer (overlapped wgrads)
@@ -478,16 +479,33 @@ static mpf_status forward_impl(Net* N, const float* d_images, int n, float* d_pr
                                wpack + P.dpack_off, rf, rd, sp));
   }
   if (sp != s) MPF_CUDA(cudaEventRecord(N->ev_join, sp));
-  // 2. layers (Alg. 1; Alg. 3 for MPF)
-  bool pool_done = false;  // the first layer's kernel already produced the MPF after it
-  for (int l = 0; l < N->n_layers - 1; ++l) {
+  // 2. layers (Alg. 1; Alg. 3 for MPF), for images [i0, i0 + n) of the batch on stream s
+  //    (`layer`), either as one chain or as two lanes (split-batch forward, below)
+  const float* images_all = d_images;
+  auto layer = [&](int l, int i0, int n, cudaStream_t s, bool& pool_done, bool& packs_joined,
+                   bool lane_b) -> mpf_status {
     const LayerPlan& P = N->lp[l];
     const Act& in = N->a[l];
     const Act& o = N->a[l + 1];
     if (pool_done) {
       pool_done = false;
-      continue;
+      return MPF_OK;
     }
+    const float* d_images = images_all + (size_t)i0 * N->cfg.in_channels * N->cfg.image_rows * N->cfg.image_cols;
+    // this lane's slice of a[l] (input) and a[l + 1] (output): images are outermost
+    // scratch Y (a conv output consumed by the MPF right after it) is reused layer after
+    // layer while the two lanes are a layer apart, and the layers' sizes differ: lane B's
+    // slice sits at the END of the buffer so the lanes never overlap
+    auto y_slice = [&](long long e_img) -> size_t {
+      return lane_b ? N->y_floats - (size_t)n * e_img : (size_t)i0 * e_img;
+    };
+    auto in_ptr = [&]() {
+      return N->lp[l - 1].out_where == Where::ScratchY ? scr(N, N->off_Y) + y_slice(in.elems_per_image())
+                                                       : act_ptr(N, l) + (size_t)i0 * in.elems_per_image();
+    };
+    auto out_val = [&](int ll) { return tape_val(N, ll) + (size_t)i0 * N->a[ll + 1].elems_per_image(); };
+    auto out_idx = [&](int ll) { return tape_idx(N, ll) + (size_t)i0 * N->a[ll + 1].elems_per_image(); };
+    auto out_y = [&]() { return scr(N, N->off_Y) + y_slice(o.elems_per_image()); };
     // the consumer of this output rounds? (TF32 operand of a tensor-core conv)
     // (the tensor-core softmax head counts: it reads h as TF32 MMA operand)
     const bool first_simt = l == 0 && first_conv_supported(N->cfg.in_channels, P.cout, P.L.k) &&
@@ -501,18 +519,18 @@ static mpf_status forward_impl(Net* N, const float* d_images, int n, float* d_pr
     if (P.L.kind == MPF_POOL) {
       const Act& y = in;
       MpfArgs m;
-      m.y = act_ptr(N, l);
+      m.y = in_ptr();
       m.gr = y.gr; m.gc = y.gc; m.vr = y.vr; m.vc = y.vc; m.C = y.C; m.k = P.L.k;
       m.n_frag_in = n * y.F;
-      m.out = tape_val(N, l);
-      m.idx = tape_idx(N, l);
+      m.out = out_val(l);
+      m.idx = out_idx(l);
       m.m_r = o.vr; m.m_c = o.vc;
       m.round_tf32 = (l + 1 < N->n_layers - 1 && use_tc(N, N->lp[l + 1], false)) ? 1 : 0;
       const double ein = (double)n * y.F * y.vr * y.vc * y.C, eout = (double)n * o.F * o.vr * o.vc * o.C;
       LAUNCH(N, s, "mpf_fwd", l, 0.0, 4.0 * ein + 5.0 * eout, launch_mpf_fwd(m, s));
     } else {
-      float* out = P.out_where == Where::Tape ? tape_val(N, l) : scr(N, N->off_Y);
-      const float* x = (l == 0) ? d_images : act_ptr(N, l);
+      float* out = P.out_where == Where::Tape ? out_val(l) : out_y();
+      const float* x = (l == 0) ? d_images : in_ptr();
       const double pos_out = (double)n * o.F * o.vr * o.vc;
       const double cflops = 2.0 * pos_out * P.cout * P.L.k * P.L.k * P.cin;
       const double in_e = (l == 0) ? (double)n * N->cfg.in_channels * N->cfg.image_rows * N->cfg.image_cols
@@ -542,8 +560,8 @@ static mpf_status forward_impl(Net* N, const float* d_images, int n, float* d_pr
           m.y = nullptr;
           m.gr = o.gr; m.gc = o.gc; m.vr = o.vr; m.vc = o.vc; m.C = o.C; m.k = Pn.L.k;
           m.n_frag_in = n * o.F;
-          m.out = tape_val(N, 1);
-          m.idx = tape_idx(N, 1);
+          m.out = out_val(1);
+          m.idx = out_idx(1);
           m.m_r = po.vr; m.m_c = po.vc;
           m.round_tf32 = (2 < N->n_layers - 1 && use_tc(N, N->lp[2], false)) ? 1 : 0;
           const double eout = (double)n * po.F * po.vr * po.vc * po.C;
@@ -589,6 +607,38 @@ static mpf_status forward_impl(Net* N, const float* d_images, int n, float* d_pr
         LAUNCH(N, s, "conv_fwd_simt", l, cflops, cbytes, launch_conv_simt(c, s));
       }
     }
+    return MPF_OK;
+  };
+  bool pool_done = false;  // the first layer's kernel already produced the MPF after it
+  // Split-batch forward (opt-in MPF_FWD_SPLIT=1): images [0, nA) on s and [nA, n) on the
+  // side stream, the second lane one layer behind (it waits for lane A's layer l), so an
+  // MPF layer of one lane runs beside a tensor-core convolution of the other.  Same kernels
+  // on image slices: the results are those of the one-chain forward.
+  const char* fse = getenv("MPF_FWD_SPLIT");
+  const bool split = fse && atoi(fse) != 0 && n >= 2 && sp != s && !hf;
+  if (!split) {
+    for (int l = 0; l < N->n_layers - 1; ++l) {
+      mpf_status st = layer(l, 0, n, s, pool_done, packs_joined, false);
+      if (st != MPF_OK) return st;
+    }
+  } else {
+    const int nA = (n + 1) / 2, nB = n - nA;
+    bool pool_done_b = false, packs_joined_b = true;  // lane B follows lane A, which joined the packs
+    if (!packs_joined) {
+      MPF_CUDA(cudaStreamWaitEvent(s, N->ev_join, 0));
+      packs_joined = true;
+    }
+    for (int l = 0; l < N->n_layers - 1; ++l) {
+      if (!N->ev_lane[l]) MPF_CUDA(cudaEventCreateWithFlags(&N->ev_lane[l], cudaEventDisableTiming));
+      mpf_status st = layer(l, 0, nA, s, pool_done, packs_joined, false);
+      if (st != MPF_OK) return st;
+      MPF_CUDA(cudaEventRecord(N->ev_lane[l], s));
+      MPF_CUDA(cudaStreamWaitEvent(sp, N->ev_lane[l], 0));
+      st = layer(l, nA, nB, sp, pool_done_b, packs_joined_b, true);
+      if (st != MPF_OK) return st;
+    }
+    MPF_CUDA(cudaEventRecord(N->ev_ready, sp));
+    MPF_CUDA(cudaStreamWaitEvent(s, N->ev_ready, 0));
   }
   if (!packs_joined) MPF_CUDA(cudaStreamWaitEvent(s, N->ev_join, 0));  // the backward reads the packs
   N->images = d_images;

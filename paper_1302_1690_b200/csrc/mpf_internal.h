@@ -65,6 +65,7 @@ struct Net {
   // memory plan for n_cap images (bytes)
   int n_cap = 0;
   size_t tape_bytes = 0, scratch_bytes = 0;
+  size_t y_floats = 0;  // scratch Y capacity (floats)
   size_t off_Y = 0, off_dA = 0, off_dB = 0, off_dC = 0, off_bpart = 0, off_wpack = 0, off_part = 0,
          off_nlab = 0, off_lossp = 0, off_err = 0, off_rowloss = 0, off_stage_img = 0, off_stage_lab = 0,
          off_stage_loss = 0, off_theta0 = 0, off_armijo = 0, off_labfrag = 0;
@@ -75,6 +76,7 @@ struct Net {
   // backward: weight gradients run on side_stream, overlapping the dgrad / MPF-backward chain
   cudaStream_t side_stream = nullptr;
   cudaEvent_t ev_ready = nullptr, ev_join = nullptr, ev_buf[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev_lane[kMaxL] = {};  // split-batch forward: lane A finished layer l
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   int stage_slot = 0;
   size_t part_floats = 0;  // capacity of the wgrad partial buffer (floats)

@@ -502,6 +502,27 @@ def test_wgrad_tmem_a_matches_smem_a(name):
     assert np.array_equal(a["loss"], b["loss"])
 
 
+@pytest.mark.parametrize("name", ["cfg2", "cfg4s", "cfg5s"])
+def test_split_batch_forward_bitwise(name):
+    """The split-batch forward (MPF_FWD_SPLIT: two image lanes on two streams, one layer
+    apart, lane B's scratch slice at the end of the buffer) runs the same kernels on image
+    slices: outputs, loss and gradients are bitwise those of the one-chain forward."""
+    import dataclasses
+    if name == "cfg4s":
+        S.CONFIGS["cfg4s"] = _cfg4s()
+    if name == "cfg5s":
+        S.CONFIGS["cfg5s"] = dataclasses.replace(S.CONFIGS["cfg5"], name="cfg5s", H=168, W=168)
+    try:
+        cfg, a = _run_variant({"MPF_FWD_SPLIT": "1"}, name=name, n=3)
+        _, b = _run_variant({"MPF_FWD_SPLIT": "0"}, name=name, n=3)
+    finally:
+        S.CONFIGS.pop("cfg4s", None)
+        S.CONFIGS.pop("cfg5s", None)
+    assert np.array_equal(a["probs"], b["probs"])
+    assert np.array_equal(a["loss"], b["loss"])
+    assert np.array_equal(a["grad_sum"], b["grad_sum"])
+
+
 @pytest.mark.parametrize("name", ["cfg2", "cfg5s"])
 def test_mpf_backward_tiled_equals_sliding_bitwise(name):
     """Shared-memory tiled and register-sliding MPF backward gather the same candidates in
