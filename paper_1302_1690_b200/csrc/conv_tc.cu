@@ -704,6 +704,260 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// Narrow layers (k * npad <= 256, e.g. the dgrad into a 16/24/32-map layer): the k taps of a
+// slab row go into ONE MMA of N = k * npad, D_kx[r] = sum_c A[p0 + r][c] W_kx[c] over the
+// 128 slab rows r, instead of k MMAs of N = npad on A shifted by kx rows.  The A operand
+// (4 KB per K step, the shared-memory-bound part of a narrow MMA) is then read
+// once per K step instead of k times.  The shift moves to the epilogue:
+// out[p0 + r] = sum_kx D_kx[r + kx], a sum over TMEM rows r .. r + k - 1 (lane shuffles; rows
+// of the next lane quarter through a small shared exchange), so a tile of 128 accumulator
+// rows yields TR = 128 - (k - 1) outputs and tiles overlap by k - 1 rows.  The last quarter
+// stores its 32 - (k - 1) rows through a second tensor map with that box height, so a tile
+// never writes its neighbour's rows.
+template <int K>
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_tc_ntap_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO3,
+                        ConvTcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t sbase = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t sS = sbase;
+  const uint32_t sC = sS + p.n_stages * p.stage_bytes;
+  const uint32_t sX = sC + p.n_stage * kEpiWarps * kStageBytes;  // [2 halves][4 q][7 taps][8 lanes][16]
+  const uint32_t sBias = sX + 2 * 4 * 7 * 8 * 16 * 4;
+  const uint32_t sBar = sBias + 4 * 256;
+  const uint32_t barFull = sBar, barEmpty = barFull + 8 * p.n_stages;
+  const uint32_t barTfull = barEmpty + 8 * p.n_stages, barTempty = barTfull + 16;
+  const uint32_t sTmemSlot = barTempty + 16;
+  uint8_t* gen = smem_raw - ptx::smem_u32(smem_raw);
+  uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(gen + sTmemSlot);
+  float* s_bias = reinterpret_cast<float*>(gen + sBias);
+  float* s_x = reinterpret_cast<float*>(gen + sX);
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  constexpr int k = K;
+  const int TR = 128 - (k - 1), N = k * p.npad;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+    ptx::prefetch_tmap(&tmO);
+    ptx::prefetch_tmap(&tmO3);
+    for (int i = 0; i < p.n_stages; ++i) {
+      ptx::mbar_init(barFull + 8 * i, 1);
+      ptx::mbar_init(barEmpty + 8 * i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(barTfull + 8 * i, 1);
+      ptx::mbar_init(barTempty + 8 * i, kEpiWarps);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(sTmemSlot, p.tmem_cols);
+  for (int c = threadIdx.x; c < 256; c += kThreads) s_bias[c] = (p.bias && c < p.cout) ? p.bias[c] : 0.f;
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot_ptr;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int it = 0;
+      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+        const int p0 = tile * TR;
+        for (int ky = 0; ky < k; ++ky) {
+          for (int cc = 0; cc < p.n_cc; ++cc, ++it) {
+            const int st = it % p.n_stages;
+            ptx::mbar_wait(barEmpty + 8 * st, ((it / p.n_stages) & 1) ^ 1);
+            ptx::mbar_arrive_expect_tx(barFull + 8 * st, p.a_slot_bytes + k * p.b_slot_bytes);
+            const uint32_t sa = sS + st * p.stage_bytes;
+            ptx::tma_load_2d(sa, &tmA, barFull + 8 * st, cc * kKC, p0 + p.shift_rows + ky * p.gc);
+            for (int kx = 0; kx < k; ++kx)
+              ptx::tma_load_2d(sa + p.a_slot_bytes + kx * p.b_slot_bytes, &tmB, barFull + 8 * st,
+                               (ky * k + kx) * p.cin + cc * kKC, 0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    const uint32_t idesc = ptx::idesc_tf32(128, N);
+    int it = 0, lt = 0;
+    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++lt) {
+      const int buf = lt & 1;
+      ptx::mbar_wait(barTempty + 8 * buf, ((lt >> 1) & 1) ^ 1);
+      ptx::tc_fence_after();
+      const uint32_t dbase = tmem + buf * N;
+      for (int ky = 0; ky < k; ++ky) {
+        for (int cc = 0; cc < p.n_cc; ++cc, ++it) {
+          const int st = it % p.n_stages;
+          ptx::mbar_wait(barFull + 8 * st, (it / p.n_stages) & 1);
+          ptx::tc_fence_after();
+          const uint32_t sa = sS + st * p.stage_bytes;
+          const uint64_t adesc0 = ptx::sdesc_k_sw128(sa, p.base_mode);
+          const uint64_t bdesc0 = ptx::sdesc_k_sw128(sa + p.a_slot_bytes, p.base_mode);
+          const int nk8 = cc == p.n_cc - 1 ? p.last_k8 : 4;
+#pragma unroll
+          for (int k8 = 0; k8 < 4; ++k8) {
+            if (k8 >= nk8) break;
+            const uint64_t ad = adesc0 + (uint64_t)((k8 * 32) >> 4);
+            const uint64_t bd = bdesc0 + (uint64_t)((k8 * 32) >> 4);
+            ptx::mma_tf32_elect(dbase, ad, bd, idesc, (ky | cc | k8) != 0);
+          }
+          ptx::mma_commit_elect(barEmpty + 8 * st);
+        }
+      }
+      ptx::mma_commit_elect(barTfull + 8 * buf);
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (warps 2..9)
+    // The two warps of a lane quarter take alternate 16-column slices of every 32-column
+    // chunk and share one swizzled staging box per chunk; the four warps of a half exchange
+    // the first k - 1 rows of their quarter (taps 1 .. k-1) for the previous quarter.
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    const int per_frag = p.gr * p.gc;
+    float* xq = s_x + ((half * 4 + q) * 7) * 8 * 16;
+    const float* xn = s_x + ((half * 4 + q + 1) * 7) * 8 * 16;
+    int lt = 0, sb = 0;
+    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++lt) {
+      const int buf = lt & 1;
+      ptx::mbar_wait(barTfull + 8 * buf, (lt >> 1) & 1);
+      ptx::tc_fence_after();
+      const int p0 = tile * TR;
+      const int r = q * 32 + lane;  // accumulator row = output row of this thread
+      const int pos = p0 + r;
+      bool valid = false;
+      if (r < TR && pos < p.P_tot) {
+        const int rr = pos % per_frag;
+        const int y = rr / p.gc, x = rr - (rr / p.gc) * p.gc;
+        valid = y < p.out_vr && x < p.out_vc;
+      }
+      const float* md = (p.mul_dact && valid) ? p.mul_dact + (size_t)pos * p.cout : nullptr;
+      const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + buf * N;
+      for (int c0 = 0; c0 < p.npad; c0 += 32) {
+        const int cs = c0 + 16 * half;
+        float o[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) o[j] = 0.f;
+        if (cs < p.npad) {
+          uint32_t v[K][16];
+#pragma unroll
+          for (int kx = 0; kx < K; ++kx)
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                : "=r"(v[kx][0]), "=r"(v[kx][1]), "=r"(v[kx][2]), "=r"(v[kx][3]), "=r"(v[kx][4]), "=r"(v[kx][5]),
+                  "=r"(v[kx][6]), "=r"(v[kx][7]), "=r"(v[kx][8]), "=r"(v[kx][9]), "=r"(v[kx][10]), "=r"(v[kx][11]),
+                  "=r"(v[kx][12]), "=r"(v[kx][13]), "=r"(v[kx][14]), "=r"(v[kx][15])
+                : "r"(trow + kx * p.npad + cs));
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) o[j] = __uint_as_float(v[0][j]);
+#pragma unroll
+          for (int kx = 1; kx < K; ++kx) {
+            // rows 0 .. kx-1 of this quarter serve the previous quarter's last lanes
+            if (lane < kx && q > 0) {
+#pragma unroll
+              for (int j4 = 0; j4 < 4; ++j4)
+                *reinterpret_cast<float4*>(xq + ((kx - 1) * 8 + lane) * 16 + 4 * j4) =
+                    make_float4(__uint_as_float(v[kx][4 * j4]), __uint_as_float(v[kx][4 * j4 + 1]),
+                                __uint_as_float(v[kx][4 * j4 + 2]), __uint_as_float(v[kx][4 * j4 + 3]));
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float t = __shfl_down_sync(0xffffffffu, __uint_as_float(v[kx][j]), kx);
+              if (lane + kx < 32) o[j] += t;
+            }
+          }
+        }
+        named_bar(1 + half, 128);  // every quarter's exchange rows are written
+        if (cs < p.npad && q < 3) {
+#pragma unroll
+          for (int kx = 1; kx < K; ++kx) {
+            if (lane + kx >= 32) {
+              const float* src = xn + ((kx - 1) * 8 + (lane + kx - 32)) * 16;
+#pragma unroll
+              for (int j4 = 0; j4 < 4; ++j4) {
+                const float4 t = *reinterpret_cast<const float4*>(src + 4 * j4);
+                o[4 * j4] += t.x; o[4 * j4 + 1] += t.y; o[4 * j4 + 2] += t.z; o[4 * j4 + 3] += t.w;
+              }
+            }
+          }
+        }
+        // the rest of the epilogue on this warp's 16 columns
+        float mdv[16];
+        if (md) {
+          if (cs + 16 <= p.cout) {
+#pragma unroll
+            for (int j4 = 0; j4 < 4; ++j4) {
+              const float4 t = __ldg(reinterpret_cast<const float4*>(md + cs) + j4);
+              mdv[4 * j4] = t.x; mdv[4 * j4 + 1] = t.y; mdv[4 * j4 + 2] = t.z; mdv[4 * j4 + 3] = t.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) mdv[j] = (cs + j < p.cout) ? __ldg(md + cs + j) : 0.f;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) o[j] += s_bias[(cs + j) & 255];
+        if (p.act == MPF_TANH) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) o[j] = fast_tanh(o[j]);
+        } else if (p.act == MPF_LOGISTIC) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) o[j] = fast_logistic(o[j]);
+        }
+        if (md) {
+          if (p.dact == MPF_TANH) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) o[j] *= fmaf(-mdv[j], mdv[j], 1.f);
+          } else if (p.dact == MPF_LOGISTIC) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) o[j] *= mdv[j] * (1.f - mdv[j]);
+          }
+        }
+        if (p.round_out) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) o[j] = tf32r(o[j]);
+        }
+        if (!valid) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) o[j] = 0.f;
+        }
+        // shared staging box of the quarter (half 0's slot): half h fills columns 16h..16h+15
+        const uint32_t sbuf = sC + (q * p.n_stage + sb) * kStageBytes;
+        if (half == 0 && lane == 0) {  // the store that last used this box has read it
+          if (p.n_stage == 2) ptx::bulk_wait_read<1>();
+          else ptx::bulk_wait_read<0>();
+        }
+        named_bar(3 + q, 64);
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int chunk = half * 4 + jj;
+          const uint32_t a = sbuf + lane * 128 + ((chunk ^ (lane & 7)) * 16);
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(o[4 * jj]), "f"(o[4 * jj + 1]),
+                       "f"(o[4 * jj + 2]), "f"(o[4 * jj + 3])
+                       : "memory");
+        }
+        ptx::fence_proxy_async();
+        named_bar(3 + q, 64);
+        if (half == 0 && lane == 0) {
+          if (q < 3) ptx::tma_store_2d(&tmO, sbuf, c0, p0 + q * 32);
+          else ptx::tma_store_2d(&tmO3, sbuf, c0, p0 + 96);  // rows 96 .. TR-1 only
+          ptx::bulk_commit();
+        }
+        sb = (sb + 1 == p.n_stage) ? 0 : sb + 1;
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(barTempty + 8 * buf);
+    }
+    if (lane == 0) ptx::bulk_wait<0>();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) ptx::tmem_dealloc(tmem, p.tmem_cols);
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_once;
 
@@ -829,7 +1083,97 @@ bool tc_supported(int cin, int cout, int k) {
   return cin % 4 == 0 && cin >= 16 && cout % 4 == 0 && cout >= 4 && cout <= 256 && k >= 1 && k <= 8;
 }
 
+// The multi-tap kernel for narrow layers (k * npad <= 256, npad <= 64) with k >= 5: measured
+// 2.06 vs 2.58 ms on the cfg4 C5x5 dgrad (N = 32), but slower for k <= 4 (cfg5: 1.01 vs
+// 0.75 ms), where the cross-row epilogue outweighs the A reads it saves.
+// MPF_TC_NTAP=1 uses it for every eligible layer, =0 for none.
+static bool use_ntap(const TcConvArgs& a) {
+  const int npad = (a.cout + 15) / 16 * 16;
+  const bool ok = a.head == nullptr && a.k >= 2 && a.k <= 8 && a.k * npad <= 256 && npad <= 64;
+  const char* e = getenv("MPF_TC_NTAP");
+  if (e) return ok && atoi(e) != 0;
+  return ok && a.k >= 5;
+}
+
+static cudaError_t launch_conv_ntap(const TcConvArgs& a, cudaStream_t s, int* grid_out) {
+  ConvTcParams p{};
+  p.P_tot = a.n_frag * a.gr * a.gc;
+  p.gr = a.gr;
+  p.gc = a.gc;
+  p.out_vr = a.out_vr;
+  p.out_vc = a.out_vc;
+  p.cin = a.cin;
+  p.cout = a.cout;
+  p.npad = (a.cout + 15) / 16 * 16;
+  p.k = a.k;
+  p.shift_rows = a.shift * (a.gc + 1);
+  p.n_cc = (a.cin + kKC - 1) / kKC;
+  p.last_k8 = (a.cin - (p.n_cc - 1) * kKC + 7) / 8;
+  p.act = a.act;
+  p.round_out = a.round_out;
+  p.dact = a.dact;
+  p.bias = a.bias;
+  p.mul_dact = a.mul_dact;
+  p.base_mode = base_mode();
+  p.nbox = 1;
+  p.box_rows = 128;
+  p.a_slot_bytes = 128 * 128;
+  p.b_rows = p.npad;
+  p.b_slot_bytes = (uint32_t)(p.npad * 128);
+  p.stage_bytes = p.a_slot_bytes + (uint32_t)a.k * p.b_slot_bytes;
+  const size_t xbytes = 2 * 4 * 7 * 8 * 16 * 4;
+  const size_t base_fixed = 1024 + xbytes + 4 * 256 + 512;
+  const size_t total = 227 * 1024;
+  int ns = 0, nst = 0;
+  for (int cand_ns = 2; cand_ns >= 1 && !ns; --cand_ns) {
+    const size_t budget = total - base_fixed - (size_t)cand_ns * kEpiWarps * kStageBytes;
+    int cand = (int)(budget / p.stage_bytes);
+    if (cand > 6) cand = 6;
+    if (cand >= 3 || (cand_ns == 1 && cand >= 2)) {
+      ns = cand_ns;
+      nst = cand;
+    }
+  }
+  if (!ns) return cudaErrorInvalidConfiguration;
+  p.n_stage = ns;
+  p.n_stages = nst;
+  const int N = a.k * p.npad;
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(2 * N)) cols <<= 1;
+  p.tmem_cols = cols;
+  const int TR = 128 - (a.k - 1);
+  p.n_tiles = (p.P_tot + TR - 1) / TR;
+  const size_t smem = base_fixed + (size_t)ns * kEpiWarps * kStageBytes + (size_t)nst * p.stage_bytes;
+  const int grid = p.n_tiles < num_sms() ? p.n_tiles : num_sms();
+  if (grid_out) *grid_out = grid;
+  CUtensorMap A, B, O, O3;
+  cudaError_t e = make_map(&A, a.x, (uint64_t)a.cin, (uint64_t)p.P_tot, 128u);
+  if (e != cudaSuccess) return e;
+  e = make_map(&B, a.w, (uint64_t)a.k * a.k * a.cin, (uint64_t)a.cout, (uint32_t)p.b_rows);
+  if (e != cudaSuccess) return e;
+  e = make_map(&O, a.out, (uint64_t)a.cout, (uint64_t)p.P_tot, 32u);
+  if (e != cudaSuccess) return e;
+  e = make_map(&O3, a.out, (uint64_t)a.cout, (uint64_t)p.P_tot, (uint32_t)(32 - (a.k - 1)));
+  if (e != cudaSuccess) return e;
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e2 != cudaSuccess) return e2;
+    kern<<<grid, kThreads, smem, s>>>(A, B, O, O3, p);
+    return cudaGetLastError();
+  };
+  switch (a.k) {
+    case 2: return go(conv_tc_ntap_kernel<2>);
+    case 3: return go(conv_tc_ntap_kernel<3>);
+    case 4: return go(conv_tc_ntap_kernel<4>);
+    case 5: return go(conv_tc_ntap_kernel<5>);
+    case 6: return go(conv_tc_ntap_kernel<6>);
+    case 7: return go(conv_tc_ntap_kernel<7>);
+    default: return go(conv_tc_ntap_kernel<8>);
+  }
+}
+
 cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s, int* grid_out) {
+  if (use_ntap(a)) return launch_conv_ntap(a, s, grid_out);
   ConvTcParams p{};
   p.P_tot = a.n_frag * a.gr * a.gc;
   p.gr = a.gr;
