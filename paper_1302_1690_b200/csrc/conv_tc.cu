@@ -836,6 +836,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + buf * N;
       for (int c0 = 0; c0 < p.npad; c0 += 32) {
         const int cs = c0 + 16 * half;
+        // the act' operand (a global load) is issued first so it lands while TMEM is read
+        float mdv[16];
+        if (md) {
+          if (cs + 16 <= p.cout) {
+#pragma unroll
+            for (int j4 = 0; j4 < 4; ++j4) {
+              const float4 t = __ldg(reinterpret_cast<const float4*>(md + cs) + j4);
+              mdv[4 * j4] = t.x; mdv[4 * j4 + 1] = t.y; mdv[4 * j4 + 2] = t.z; mdv[4 * j4 + 3] = t.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) mdv[j] = (cs + j < p.cout) ? __ldg(md + cs + j) : 0.f;
+          }
+        }
         float o[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) o[j] = 0.f;
@@ -884,19 +898,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         // the rest of the epilogue on this warp's 16 columns
-        float mdv[16];
-        if (md) {
-          if (cs + 16 <= p.cout) {
-#pragma unroll
-            for (int j4 = 0; j4 < 4; ++j4) {
-              const float4 t = __ldg(reinterpret_cast<const float4*>(md + cs) + j4);
-              mdv[4 * j4] = t.x; mdv[4 * j4 + 1] = t.y; mdv[4 * j4 + 2] = t.z; mdv[4 * j4 + 3] = t.w;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) mdv[j] = (cs + j < p.cout) ? __ldg(md + cs + j) : 0.f;
-          }
-        }
 #pragma unroll
         for (int j = 0; j < 16; ++j) o[j] += s_bias[(cs + j) & 255];
         if (p.act == MPF_TANH) {
