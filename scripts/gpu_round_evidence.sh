@@ -10,3 +10,4 @@ done
 for w in cfg3 cfg4 cfg5; do
   timeout 600 python bench.py --workload $w --steps 5 --no-e2e --no-cpu-baseline --profile-json gpurun_out/live_$w.json > gpurun_out/live_$w.log 2>&1; echo live_$w $? >> gpurun_out/status.txt
 done
+timeout 300 python scripts/api_tour.py > gpurun_out/api_tour.log 2>&1; echo api_tour $? >> gpurun_out/status.txt
