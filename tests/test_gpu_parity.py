@@ -784,3 +784,38 @@ def test_lbfgs_primitive_errors():
         lb.trial(1.0)
     with pytest.raises(MpfError):
         lb.reject()
+
+
+def test_abi_argument_and_state_errors():
+    """Every entry point validates before touching the device (include/mpf.h error
+    behaviour): NULL pointers -> MPF_ERR_ARG, n outside [1, bound] -> MPF_ERR_DATA, a
+    backward without a forward -> MPF_ERR_STATE, line-search parameters out of range ->
+    MPF_ERR_ARG; the net stays usable afterwards."""
+    import ctypes
+    from paper_1302_1690_b200 import _lib as L
+    from paper_1302_1690_b200.net import Lbfgs
+    cfg = S.CONFIGS["cfg1"]
+    images, labels = S.make_batch(cfg, [0, 1])
+    net = MPFNet(cfg.layers, cfg.P, cfg.H, cfg.W, max_images=1)
+    net.set_params(S.init_params(cfg).astype(np.float32))
+    x1 = torch.tensor(images[:1], device="cuda")
+    x2 = torch.tensor(images, device="cuda")
+    y1 = torch.tensor(labels[:1], device="cuda")
+    lib = net.lib
+    assert lib.mpf_forward_image(net.h, None, 1, None, None) == L.MPF_ERR_ARG
+    assert lib.mpf_forward_image(net.h, ctypes.c_void_p(x1.data_ptr()), 0, None, None) == L.MPF_ERR_DATA
+    assert lib.mpf_forward_image(net.h, ctypes.c_void_p(x2.data_ptr()), 2, None, None) == L.MPF_ERR_DATA
+    fresh = MPFNet(cfg.layers, cfg.P, cfg.H, cfg.W, max_images=1)
+    with pytest.raises(MpfError) as e:
+        fresh.backward(y1)
+    assert e.value.status == L.MPF_ERR_STATE
+    with pytest.raises(MpfError) as e:
+        net.armijo_step(x1, y1, beta=1.5)
+    assert e.value.status == L.MPF_ERR_ARG
+    with pytest.raises(MpfError) as e:
+        Lbfgs(net).step(x1, y1, alpha0=0.0)
+    assert e.value.status == L.MPF_ERR_ARG
+    # still usable: a normal step matches a fresh net's
+    loss = net.train_step(x1, y1)
+    fresh.set_params(S.init_params(cfg).astype(np.float32))
+    assert np.array_equal(loss.cpu().numpy(), fresh.train_step(x1, y1).cpu().numpy())
