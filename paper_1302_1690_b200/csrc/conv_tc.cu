@@ -714,7 +714,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 // rows yields TR = 128 - (k - 1) outputs and tiles overlap by k - 1 rows.  The last quarter
 // stores its 32 - (k - 1) rows through a second tensor map with that box height, so a tile
 // never writes its neighbour's rows.
-template <int K>
+// MC: a cluster of two CTAs runs tiles 2u and 2u + 1 in lockstep; each CTA loads half of the
+// k weight taps of a stage and multicasts them to both, halving the weight stream from L2
+// (the k = 5 dgrad was starved by it: 20 of its 36 KB per stage are weights, re-read for
+// every 124-row tile).  A stage slot is refilled only after BOTH CTAs' MMAs released it.
+template <int K, bool MC>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_tc_ntap_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO3,
@@ -744,7 +748,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::prefetch_tmap(&tmO3);
     for (int i = 0; i < p.n_stages; ++i) {
       ptx::mbar_init(barFull + 8 * i, 1);
-      ptx::mbar_init(barEmpty + 8 * i, 1);
+      ptx::mbar_init(barEmpty + 8 * i, MC ? 2 : 1);
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(barTfull + 8 * i, 1);
@@ -755,15 +759,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) ptx::tmem_alloc(sTmemSlot, p.tmem_cols);
   for (int c = threadIdx.x; c < 256; c += kThreads) s_bias[c] = (p.bias && c < p.cout) ? p.bias[c] : 0.f;
   ptx::tc_fence_before();
-  __syncthreads();
+  if (MC) ptx::cluster_sync_all();  // the peer's barriers exist before anything is multicast
+  else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot_ptr;
+  const int rank = MC ? (int)ptx::cluster_rank() : 0;
+  const int first = MC ? (int)(blockIdx.x >> 1) * 2 + rank : (int)blockIdx.x;
+  const int stride = MC ? (int)(gridDim.x >> 1) * 2 : (int)gridDim.x;
+  // MC: both CTAs of the cluster run the same number of units (tile 2u + 1 may lie past the
+  // end: its loads read zeros and its stores are clipped)
+  const int n_iter_tiles = MC ? (p.n_tiles + 1) / 2 * 2 : p.n_tiles;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       int it = 0;
-      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+      for (int tile = first; tile < n_iter_tiles; tile += stride) {
         const int p0 = tile * TR;
         for (int ky = 0; ky < k; ++ky) {
           for (int cc = 0; cc < p.n_cc; ++cc, ++it) {
@@ -772,9 +783,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_arrive_expect_tx(barFull + 8 * st, p.a_slot_bytes + k * p.b_slot_bytes);
             const uint32_t sa = sS + st * p.stage_bytes;
             ptx::tma_load_2d(sa, &tmA, barFull + 8 * st, cc * kKC, p0 + p.shift_rows + ky * p.gc);
-            for (int kx = 0; kx < k; ++kx)
-              ptx::tma_load_2d(sa + p.a_slot_bytes + kx * p.b_slot_bytes, &tmB, barFull + 8 * st,
-                               (ky * k + kx) * p.cin + cc * kKC, 0);
+            for (int kx = 0; kx < k; ++kx) {
+              if (MC) {
+                if ((kx & 1) == rank)
+                  ptx::tma_load_2d_mc(sa + p.a_slot_bytes + kx * p.b_slot_bytes, &tmB, barFull + 8 * st,
+                                      (ky * k + kx) * p.cin + cc * kKC, 0, (uint16_t)3);
+              } else {
+                ptx::tma_load_2d(sa + p.a_slot_bytes + kx * p.b_slot_bytes, &tmB, barFull + 8 * st,
+                                 (ky * k + kx) * p.cin + cc * kKC, 0);
+              }
+            }
           }
         }
       }
@@ -783,7 +801,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ MMA issuer
     const uint32_t idesc = ptx::idesc_tf32(128, N);
     int it = 0, lt = 0;
-    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++lt) {
+    for (int tile = first; tile < n_iter_tiles; tile += stride, ++lt) {
       const int buf = lt & 1;
       ptx::mbar_wait(barTempty + 8 * buf, ((lt >> 1) & 1) ^ 1);
       ptx::tc_fence_after();
@@ -804,7 +822,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t bd = bdesc0 + (uint64_t)((k8 * 32) >> 4);
             ptx::mma_tf32_elect(dbase, ad, bd, idesc, (ky | cc | k8) != 0);
           }
-          ptx::mma_commit_elect(barEmpty + 8 * st);
+          if (MC) ptx::mma_commit_mc_elect(barEmpty + 8 * st, (uint16_t)3);  // frees the slot in both CTAs
+          else ptx::mma_commit_elect(barEmpty + 8 * st);
         }
       }
       ptx::mma_commit_elect(barTfull + 8 * buf);
@@ -819,7 +838,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* xq = s_x + ((half * 4 + q) * 7) * 8 * 16;
     const float* xn = s_x + ((half * 4 + q + 1) * 7) * 8 * 16;
     int lt = 0, sb = 0;
-    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++lt) {
+    for (int tile = first; tile < n_iter_tiles; tile += stride, ++lt) {
       const int buf = lt & 1;
       ptx::mbar_wait(barTfull + 8 * buf, (lt >> 1) & 1);
       ptx::tc_fence_after();
@@ -955,7 +974,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) ptx::bulk_wait<0>();
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  if (MC) ptx::cluster_sync_all();  // the peer may still multicast into / arrive on our smem
+  else __syncthreads();
   if (warp == 1) ptx::tmem_dealloc(tmem, p.tmem_cols);
 }
 
@@ -1156,21 +1176,46 @@ static cudaError_t launch_conv_ntap(const TcConvArgs& a, cudaStream_t s, int* gr
   if (e != cudaSuccess) return e;
   e = make_map(&O3, a.out, (uint64_t)a.cout, (uint64_t)p.P_tot, (uint32_t)(32 - (a.k - 1)));
   if (e != cudaSuccess) return e;
+  // weight multicast across a cluster of two (MPF_TC_NTAP_MC=0 turns it off)
+  const char* mce = getenv("MPF_TC_NTAP_MC");
+  const bool mc = (mce ? atoi(mce) != 0 : true) && p.n_tiles >= 2;
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e2 != cudaSuccess) return e2;
-    kern<<<grid, kThreads, smem, s>>>(A, B, O, O3, p);
+    if (!mc) {
+      kern<<<grid, kThreads, smem, s>>>(A, B, O, O3, p);
+    } else {
+      const int units = (p.n_tiles + 1) / 2;
+      const int pairs = units < num_sms() / 2 ? units : num_sms() / 2;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(2 * pairs, 1, 1);
+      cfg.blockDim = dim3(kThreads, 1, 1);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      e2 = cudaLaunchKernelEx(&cfg, kern, A, B, O, O3, p);
+      if (e2 != cudaSuccess) return e2;
+    }
     return cudaGetLastError();
   };
+#define MPF_NTAP_CASE(KK) \
+  case KK: return mc ? go(conv_tc_ntap_kernel<KK, true>) : go(conv_tc_ntap_kernel<KK, false>);
   switch (a.k) {
-    case 2: return go(conv_tc_ntap_kernel<2>);
-    case 3: return go(conv_tc_ntap_kernel<3>);
-    case 4: return go(conv_tc_ntap_kernel<4>);
-    case 5: return go(conv_tc_ntap_kernel<5>);
-    case 6: return go(conv_tc_ntap_kernel<6>);
-    case 7: return go(conv_tc_ntap_kernel<7>);
-    default: return go(conv_tc_ntap_kernel<8>);
+    MPF_NTAP_CASE(2)
+    MPF_NTAP_CASE(3)
+    MPF_NTAP_CASE(4)
+    MPF_NTAP_CASE(5)
+    MPF_NTAP_CASE(6)
+    MPF_NTAP_CASE(7)
+    default: return mc ? go(conv_tc_ntap_kernel<8, true>) : go(conv_tc_ntap_kernel<8, false>);
   }
+#undef MPF_NTAP_CASE
 }
 
 cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s, int* grid_out) {
