@@ -203,10 +203,19 @@ def main():
     import torch.distributed as dist
     from paper_1302_1690_b200 import dist as D
     from paper_1302_1690_b200.net import MPFNet
+    # MPF_BENCH_FUNCTIONAL_1GPU=1: a functional check of the multi-rank code path on a box with
+    # one GPU (every rank on cuda:0, gloo instead of NCCL); its numbers are meaningless and it
+    # is never used for a reported value
+    one_gpu_check = os.environ.get("MPF_BENCH_FUNCTIONAL_1GPU") == "1"
+    if one_gpu_check:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu_check:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     B = cfg.global_batch
     if B % world:
         raise SystemExit(f"global batch {B} not divisible by {world} ranks")
