@@ -287,6 +287,58 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
       const int pb0 = pairB ? (warp & ~1) * 8 : pw0;
       const int npb = pairB ? 16 : 8;
       const int gB = VEC ? lane + (pairB ? 32 * (warp & 1) : 0) : 0;  // this lane's float4 group
+      if constexpr (VEC) {
+        // float4 channel group gB per lane; lanes past the last group (Ch < 4 * 64) compute on
+        // group 0 and skip their stores, so the loop body has no divergent branch; their
+        // accumulators are never written out (the partials below test 4 * g < Ch).  Row
+        // pointers advance by one position per iteration (no per-position address math).
+        const bool lane_on = 4 * gB < Ch;
+        const int stride4 = Ch >> 2;
+        float4* dh4 = reinterpret_cast<float4*>(dh_img + pb0 * Ch) + (lane_on ? gB : 0);
+        const float4* h4 = reinterpret_cast<const float4*>(hs + pb0 * Ch) + (lane_on ? gB : 0);
+        const float4* w4s = reinterpret_cast<const float4*>(s_w2) + (lane_on ? gB : 0);
+        for (int q = 0; q < npb; ++q, dh4 += stride4, h4 += stride4) {
+          const int lab = s_lab[pb0 + q];  // warp-uniform
+          if (lab == kLabBeyond) break;    // past the end of the image (and so are the rest)
+          if (!(lab >= 0 && lab < C)) {    // padding position or ignored label -> zero delta
+            if (lane_on) *dh4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            continue;
+          }
+          float dl[NC];
+          {  // the row of dz: kNCP / 4 broadcast LDS.128
+            const float4* r4 = reinterpret_cast<const float4*>(s_dl + (pb0 + q) * kNCP);
+#pragma unroll
+            for (int j = 0; j < kNCP / 4; ++j) {
+              const float4 v = r4[j];
+              const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (4 * j + u < NC) dl[4 * j + u] = vv[u];
+            }
+          }
+          const float4 hv = *h4;
+          const float hh[4] = {hv.x, hv.y, hv.z, hv.w};
+          float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            const float4 w = kW4Reg ? w4reg[kW4Reg ? c : 0] : w4s[c * stride4];
+            const float ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              sacc[u] = fmaf(ww[u], dl[c], sacc[u]);
+              accW4[0][c][u] = fmaf(dl[c], hh[u], accW4[0][c][u]);
+            }
+          }
+          float d[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            d[u] = sacc[u] * (TANH ? fmaf(-hh[u], hh[u], 1.f) : act_der(a.hidden_act, hh[u]));
+            accP4[0][u] += d[u];
+            if (a.round_tf32) d[u] = tf32_rna(d[u]);
+          }
+          if (lane_on) *dh4 = make_float4(d[0], d[1], d[2], d[3]);
+        }
+      } else
       for (int q = 0; q < npb; ++q) {
         const int p = pb0 + q;
         const int lab = s_lab[p];  // warp-uniform
