@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(256) mpf_bwd_tile_kernel(MpfBwdArgs a, int row
 // gathers each element's k^2 candidates from registers in the same fixed (dy, dx) order as
 // the other MPF backward kernels (bitwise-identical results).  No shared-memory staging,
 // no barriers; CTAs stride over groups of consecutive blocks of one row.
-__global__ void __launch_bounds__(256) mpf_bwd_block2_kernel(MpfBwdArgs a, long long n_groups) {
+__global__ void __launch_bounds__(256, 3) mpf_bwd_block2_kernel(MpfBwdArgs a, long long n_groups) {
   const int C = a.C, CV = C / 4;
   const int tid = threadIdx.x, cv = tid % CV, sub = tid / CV, nsub = 256 / CV;
   const int Xw = 2 * a.m_c, Yw = 2 * a.m_r;
@@ -618,11 +618,26 @@ __global__ void __launch_bounds__(256) mpf_bwd_block2_kernel(MpfBwdArgs a, long 
   const int groups_per_row = (bj_n + nsub - 1) / nsub;
   float bsum[4] = {0.f, 0.f, 0.f, 0.f};
   if (sub < nsub) {
+    // (g, bi, gj) of group grp, advanced by gridDim.x with carries instead of divisions
+    int gj = (int)(blockIdx.x % groups_per_row), bi, g;
+    {
+      const long long t = blockIdx.x / groups_per_row;
+      bi = (int)(t % bi_n);
+      g = (int)(t / bi_n);
+    }
+    const int st_gj = (int)(gridDim.x % groups_per_row);
+    const long long st_t = gridDim.x / groups_per_row;
+    const int st_bi = (int)(st_t % bi_n), st_g = (int)(st_t / bi_n);
     for (long long grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
-      const int gj = (int)(grp % groups_per_row);
-      const long long t = grp / groups_per_row;
-      const int bi = (int)(t % bi_n);
-      const int g = (int)(t / bi_n);
+      if (grp != blockIdx.x) {
+        gj += st_gj;
+        int cb = st_bi;
+        if (gj >= groups_per_row) { gj -= groups_per_row; ++cb; }
+        bi += cb;
+        int cg = st_g;
+        if (bi >= bi_n) { bi -= bi_n; ++cg; }
+        g += cg;
+      }
       const int bj = gj * nsub + sub;
       if (bj >= bj_n) continue;
       const float* dsrc = a.dout + (size_t)g * 4 * MMC + cv * 4;
