@@ -25,9 +25,11 @@ namespace mpf {
 
 namespace {
 
+// TF32 rounding (nearest-even, finite-saturating: one F2FP instruction on sm_100a; the guarded
+// cvt.rna form takes four) of an MMA operand
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  asm("cvt.rn.satfinite.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
 

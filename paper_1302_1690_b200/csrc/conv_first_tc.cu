@@ -42,9 +42,11 @@ constexpr int kFW0 = kFBld, kFE0 = kFBld + 1, kFS0 = kFE0 + kFEpi;  // MMA warp,
 constexpr int kFThreads = 32 * (kFS0 + kFSt);
 constexpr int kFRaw = 4, kFPre = 3;          // raw image ring, prefetch distance (tiles)
 
+// TF32 rounding (nearest-even, finite-saturating: one F2FP instruction on sm_100a; the guarded
+// cvt.rna form takes four) of an MMA operand
 __device__ __forceinline__ float tf32_rna_f(float x) {
   uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  asm("cvt.rn.satfinite.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
 __device__ __forceinline__ float ex2a(float x) {

@@ -78,9 +78,11 @@ __device__ __forceinline__ void twait(uint32_t bar, uint32_t parity, unsigned lo
   acc += (unsigned long long)(clock64() - t0);
 }
 
+// TF32 rounding (nearest-even, finite-saturating: one F2FP instruction on sm_100a; the guarded
+// cvt.rna form takes four) of an MMA operand
 __device__ __forceinline__ float tf32r(float x) {
   uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  asm("cvt.rn.satfinite.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
 // tanh(v) = 1 - 2 / (exp(2v) + 1): two MUFU ops, absolute error ~1e-7 (far below the

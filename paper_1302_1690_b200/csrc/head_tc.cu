@@ -41,9 +41,11 @@ constexpr int kHSm = 4;                   // softmax warps
 constexpr int kHThreads = 64 + 32 * (kHDh + kHSm);
 constexpr int kHMaxCh = 256;
 
+// TF32 rounding (nearest-even, finite-saturating: one F2FP instruction on sm_100a; the guarded
+// cvt.rna form takes four) of an MMA operand
 __device__ __forceinline__ float tf32_rna_h(float x) {
   uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  asm("cvt.rn.satfinite.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
 

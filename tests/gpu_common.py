@@ -91,7 +91,8 @@ def compare_step(layers, g, o, tol, what=""):
 
 
 def _tf32_round(t):
-    """Round to TF32 (nearest, ties away) on the fp32 bit pattern."""
+    """Round to TF32 on the fp32 bit pattern (nearest, ties away; the GPU rounds ties to even,
+    which makes no difference to an error model)."""
     import torch
     b = t.detach().float().contiguous().view(torch.int32)
     return ((b + 0x1000) & ~0x1FFF).view(torch.float32).to(t.dtype)
