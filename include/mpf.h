@@ -189,11 +189,13 @@ mpf_status mpf_armijo_step(mpf_net* net, const float* d_images, int32_t n, const
 
 /*
  * Full-batch L-BFGS ("We use LBFGS"; SURVEY §8(f) item 4;
- * reading R21 in DESIGN.md).  An mpf_lbfgs owns, in its own device allocation, memory + 1
- * curvature-pair slots (s, y: fp32 [n_params] each), the base point theta0 and the gradient
- * g at it (fp32), and the direction v = H g (fp64).  It works on the parameters and
- * gradients bound to `net`, which must outlive it.  One stream at a time; every call is
- * asynchronous on `stream` except where it says it synchronises.
+ * reading R21 in DESIGN.md).  An mpf_lbfgs keeps, in a caller-owned device buffer of
+ * mpf_lbfgs_state_bytes() bytes (256-byte aligned, e.g. a torch tensor; it must outlive the
+ * handle), memory + 1 curvature-pair slots (s, y: fp32 [n_params] each), the base point
+ * theta0 and the gradient g at it (fp32), and the direction v = H g (fp64); the handle holds
+ * host bookkeeping only.  It works on the parameters and gradients bound to `net`, which
+ * must outlive it.  One stream at a time; every call is asynchronous on `stream` except
+ * where it says it synchronises.
  *
  * Primitives (the multi-GPU driver calls these with an all-reduce between; one GPU can call
  * mpf_lbfgs_step instead):
@@ -211,11 +213,13 @@ mpf_status mpf_armijo_step(mpf_net* net, const float* d_images, int32_t n, const
  *                 *h_stored = 0/1.  Synchronises `stream`.
  *   reject:       parameters <- theta0; the pairs are cleared (restart).
  *   reset:        pairs cleared and g marked unknown (after the parameters or data change).
- * Errors: MPF_ERR_ARG for memory outside [1, 64] or NULL pointers; MPF_ERR_STATE for
- * direction without a gradient, trial/accept without a direction.
+ * Errors: MPF_ERR_ARG for memory outside [1, 64], NULL pointers, a misaligned or too small
+ * state buffer; MPF_ERR_STATE for direction without a gradient, trial/accept without a
+ * direction.
  */
 typedef struct mpf_lbfgs mpf_lbfgs; /* opaque */
-mpf_status mpf_lbfgs_create(mpf_net* net, int32_t memory, mpf_lbfgs** out);
+mpf_status mpf_lbfgs_state_bytes(const mpf_net* net, int32_t memory, uint64_t* bytes);
+mpf_status mpf_lbfgs_create(mpf_net* net, int32_t memory, void* d_state, uint64_t state_bytes, mpf_lbfgs** out);
 void mpf_lbfgs_destroy(mpf_lbfgs* lb);
 mpf_status mpf_lbfgs_reset(mpf_lbfgs* lb);
 mpf_status mpf_lbfgs_set_gradient(mpf_lbfgs* lb, float grad_scale, void* stream);

@@ -22,7 +22,7 @@ MPF_MAX_LAYERS = 24
 EXPORTS = ("mpf_version", "mpf_last_error", "mpf_net_create", "mpf_net_destroy", "mpf_net_geometry",
            "mpf_net_memory", "mpf_net_bind", "mpf_forward_image", "mpf_backward_image", "mpf_sgd_step",
            "mpf_train_step", "mpf_train_step_host", "mpf_fragments_to_pixels", "mpf_mirror_pad", "mpf_class_weights_auto", "mpf_armijo_step",
-           "mpf_lbfgs_create", "mpf_lbfgs_destroy", "mpf_lbfgs_reset", "mpf_lbfgs_set_gradient", "mpf_lbfgs_direction",
+           "mpf_lbfgs_state_bytes", "mpf_lbfgs_create", "mpf_lbfgs_destroy", "mpf_lbfgs_reset", "mpf_lbfgs_set_gradient", "mpf_lbfgs_direction",
            "mpf_lbfgs_trial", "mpf_lbfgs_accept", "mpf_lbfgs_reject", "mpf_lbfgs_step",
            "mpf_debug_tape", "mpf_debug_scratch", "mpf_check", "mpf_profile_begin",
            "mpf_profile_end")
@@ -93,8 +93,10 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.mpf_armijo_step.restype = st
     lib.mpf_armijo_step.argtypes = [vp, vp, i32, vp, ctypes.POINTER(ctypes.c_float), ctypes.c_float, ctypes.c_float,
                                     ctypes.c_float, i32, ctypes.c_float, ctypes.POINTER(ctypes.c_float), vp]
+    lib.mpf_lbfgs_state_bytes.restype = st
+    lib.mpf_lbfgs_state_bytes.argtypes = [vp, i32, u64p]
     lib.mpf_lbfgs_create.restype = st
-    lib.mpf_lbfgs_create.argtypes = [vp, i32, ctypes.POINTER(vp)]
+    lib.mpf_lbfgs_create.argtypes = [vp, i32, vp, ctypes.c_uint64, ctypes.POINTER(vp)]
     lib.mpf_lbfgs_destroy.restype = None
     lib.mpf_lbfgs_destroy.argtypes = [vp]
     lib.mpf_lbfgs_reset.restype = st

@@ -1087,7 +1087,7 @@ struct mpf_lbfgs {
   mpf_net* N = nullptr;
   int m = 0;                    // memory (pairs kept)
   long long n = 0;              // parameters
-  char* mem = nullptr;          // device allocation
+  char* mem = nullptr;          // caller-owned device state (mpf_lbfgs_state_bytes)
   float* S = nullptr;           // (m+1) slots of s, then of y
   float* Y = nullptr;
   float* theta0 = nullptr;
@@ -1112,22 +1112,33 @@ double host_sum(const std::vector<double>& p, int off, int nb) {
 
 extern "C" {
 
-mpf_status mpf_lbfgs_create(mpf_net* N, int32_t memory, mpf_lbfgs** out) {
-  if (!N || !out) return fail(MPF_ERR_ARG, "NULL argument");
+static size_t lbfgs_bytes(long long n, int memory) {
+  const size_t vec = align256(sizeof(float) * (size_t)n);
+  const size_t slots = (size_t)memory + 1;
+  return 2 * slots * vec + 2 * vec + align256(sizeof(double) * (size_t)n) + align256(sizeof(double) * 2 * kLbParts) +
+         align256(sizeof(double) * slots);
+}
+
+mpf_status mpf_lbfgs_state_bytes(const mpf_net* N, int32_t memory, uint64_t* bytes) {
+  if (!N || !bytes) return fail(MPF_ERR_ARG, "NULL argument");
+  if (memory < 1 || memory > 64) return fail(MPF_ERR_ARG, "L-BFGS memory must be in [1, 64]");
+  *bytes = lbfgs_bytes(N->n_params, memory);
+  return MPF_OK;
+}
+
+mpf_status mpf_lbfgs_create(mpf_net* N, int32_t memory, void* d_state, uint64_t state_bytes, mpf_lbfgs** out) {
+  if (!N || !out || !d_state) return fail(MPF_ERR_ARG, "NULL argument");
   if (memory < 1 || memory > 64) return fail(MPF_ERR_ARG, "L-BFGS memory must be in [1, 64]");
   if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound");
+  if (((uintptr_t)d_state & 255) != 0) return fail(MPF_ERR_ARG, "L-BFGS state must be 256-byte aligned");
+  if (state_bytes < lbfgs_bytes(N->n_params, memory)) return fail(MPF_ERR_ARG, "L-BFGS state buffer too small");
   mpf_lbfgs* lb = new mpf_lbfgs();
   lb->N = N;
   lb->m = memory;
   lb->n = N->n_params;
   const size_t vec = align256(sizeof(float) * (size_t)lb->n);
   const size_t slots = (size_t)memory + 1;
-  const size_t bytes = 2 * slots * vec + 2 * vec + align256(sizeof(double) * (size_t)lb->n) +
-                       align256(sizeof(double) * 2 * kLbParts) + align256(sizeof(double) * slots);
-  if (cudaMalloc(&lb->mem, bytes) != cudaSuccess) {
-    delete lb;
-    return fail(MPF_ERR_CUDA, "L-BFGS state allocation failed");
-  }
+  lb->mem = (char*)d_state;
   char* p = lb->mem;
   lb->S = (float*)p; p += slots * vec;
   lb->Y = (float*)p; p += slots * vec;
@@ -1143,11 +1154,7 @@ mpf_status mpf_lbfgs_create(mpf_net* N, int32_t memory, mpf_lbfgs** out) {
   return MPF_OK;
 }
 
-void mpf_lbfgs_destroy(mpf_lbfgs* lb) {
-  if (!lb) return;
-  cudaFree(lb->mem);
-  delete lb;
-}
+void mpf_lbfgs_destroy(mpf_lbfgs* lb) { delete lb; }  // the state buffer belongs to the caller
 
 mpf_status mpf_lbfgs_reset(mpf_lbfgs* lb) {
   if (!lb) return fail(MPF_ERR_ARG, "NULL L-BFGS state");

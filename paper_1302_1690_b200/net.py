@@ -274,8 +274,13 @@ class Lbfgs:
         self.net = net
         self.lib = net.lib
         self.memory = memory
+        nb = ctypes.c_uint64()
+        L.check(self.lib.mpf_lbfgs_state_bytes(net.h, int(memory), ctypes.byref(nb)), "mpf_lbfgs_state_bytes")
+        # device state allocated by PyTorch and lent to the library (like the net's buffers)
+        self.state = torch.empty(nb.value, dtype=torch.uint8, device=net.device)
         h = ctypes.c_void_p()
-        L.check(self.lib.mpf_lbfgs_create(net.h, int(memory), ctypes.byref(h)), "mpf_lbfgs_create")
+        L.check(self.lib.mpf_lbfgs_create(net.h, int(memory), _ptr(self.state), nb.value, ctypes.byref(h)),
+                "mpf_lbfgs_create")
         self.h = h
         self.have_g, self.L, self.n_pairs = False, 0.0, 0
         self._ctx = None
