@@ -503,6 +503,33 @@ def test_wgrad_tmem_a_matches_smem_a(name):
 
 
 @pytest.mark.parametrize("name", ["cfg2", "cfg4s", "cfg5s"])
+def test_multitap_conv_matches_standard(name):
+    """The multi-tap tensor-core conv (one N = k npad MMA per slab row, cross-row tap sum in
+    the epilogue) forced on every eligible layer (MPF_TC_NTAP=1; default only for k >= 5)
+    against the standard kernel (MPF_TC_NTAP=0): the same sums in a different order, so
+    outputs agree to fp32 rounding and gradients to TF32 rounding; and its weight multicast across a
+    cluster of two (MPF_TC_NTAP_MC) changes only how the taps reach shared memory: bitwise."""
+    import dataclasses
+    if name == "cfg4s":
+        S.CONFIGS["cfg4s"] = _cfg4s()
+    if name == "cfg5s":
+        S.CONFIGS["cfg5s"] = dataclasses.replace(S.CONFIGS["cfg5"], name="cfg5s", H=168, W=168)
+    try:
+        cfg, a = _run_variant({"MPF_TC_NTAP": "1", "MPF_TC_NTAP_MC": "1"}, name=name)
+        _, b = _run_variant({"MPF_TC_NTAP": "1", "MPF_TC_NTAP_MC": "0"}, name=name)
+        _, c = _run_variant({"MPF_TC_NTAP": "0"}, name=name)
+    finally:
+        S.CONFIGS.pop("cfg4s", None)
+        S.CONFIGS.pop("cfg5s", None)
+    assert np.array_equal(a["grad_sum"], b["grad_sum"]) and np.array_equal(a["probs"], b["probs"])
+    # the tap sum order differs, and the deltas are TF32-rounded operands of the next MMA: a
+    # few values round one TF32 ulp (2^-11) apart, which the early layers' sums carry
+    assert rel_l2(a["probs"], c["probs"]) <= 1e-5
+    for nm, sl in param_slices(cfg.layers):
+        assert rel_l2(a["grad_sum"][sl], c["grad_sum"][sl]) <= 1e-3, nm
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg4s", "cfg5s"])
 def test_split_batch_forward_bitwise(name):
     """The split-batch forward (MPF_FWD_SPLIT: two image lanes on two streams, one layer
     apart, lane B's scratch slice at the end of the buffer) runs the same kernels on image
