@@ -299,10 +299,17 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
         float4* dh4 = reinterpret_cast<float4*>(dh_img + pb0 * Ch) + (lane_on ? gB : 0);
         const float4* h4 = reinterpret_cast<const float4*>(hs + pb0 * Ch) + (lane_on ? gB : 0);
         const float4* w4s = reinterpret_cast<const float4*>(s_w2) + (lane_on ? gB : 0);
-        for (int q = 0; q < npb; ++q, dh4 += stride4, h4 += stride4) {
-          const int lab = s_lab[pb0 + q];  // warp-uniform
-          if (lab == kLabBeyond) break;    // past the end of the image (and so are the rest)
-          if (!(lab >= 0 && lab < C)) {    // padding position or ignored label -> zero delta
+        // which of the npb positions are labelled (bit q) and how many lie before the end of
+        // the image: one shared load and two ballots instead of a load and tests per position
+        unsigned act_mask, in_mask;
+        {
+          const int lq = lane < npb ? s_lab[pb0 + lane] : kLabBeyond;
+          act_mask = __ballot_sync(0xffffffffu, lq >= 0 && lq < C);
+          in_mask = __ballot_sync(0xffffffffu, lq != kLabBeyond);
+        }
+        const int nq = __popc(in_mask);  // positions past the image end come last
+        for (int q = 0; q < nq; ++q, dh4 += stride4, h4 += stride4) {
+          if (!((act_mask >> q) & 1u)) {  // padding position or ignored label -> zero delta
             if (lane_on) *dh4 = make_float4(0.f, 0.f, 0.f, 0.f);
             continue;
           }
