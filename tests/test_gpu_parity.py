@@ -842,6 +842,16 @@ def test_abi_argument_and_state_errors():
     with pytest.raises(MpfError) as e:
         Lbfgs(net).step(x1, y1, alpha0=0.0)
     assert e.value.status == L.MPF_ERR_ARG
+    # the L-BFGS state buffer is caller-owned: too small or misaligned is an argument error
+    nb = ctypes.c_uint64()
+    assert lib.mpf_lbfgs_state_bytes(net.h, 4, ctypes.byref(nb)) == L.MPF_OK and nb.value > 0
+    buf = torch.empty(nb.value + 512, dtype=torch.uint8, device="cuda")
+    h = ctypes.c_void_p()
+    assert lib.mpf_lbfgs_create(net.h, 4, ctypes.c_void_p(buf.data_ptr()), nb.value - 1, ctypes.byref(h)) == L.MPF_ERR_ARG
+    assert lib.mpf_lbfgs_create(net.h, 4, ctypes.c_void_p(buf.data_ptr() + 4), nb.value, ctypes.byref(h)) == L.MPF_ERR_ARG
+    assert lib.mpf_lbfgs_create(net.h, 0, ctypes.c_void_p(buf.data_ptr()), nb.value, ctypes.byref(h)) == L.MPF_ERR_ARG
+    assert lib.mpf_lbfgs_create(net.h, 4, ctypes.c_void_p(buf.data_ptr()), nb.value, ctypes.byref(h)) == L.MPF_OK
+    lib.mpf_lbfgs_destroy(h)
     # still usable: a normal step matches a fresh net's
     loss = net.train_step(x1, y1)
     fresh.set_params(S.init_params(cfg).astype(np.float32))
