@@ -260,6 +260,120 @@ __global__ void __launch_bounds__(256, WT > 4 ? 2 : 3) conv_first_wgrad_kernel(F
   }
 }
 
+// Row-streamed variant (K >= 5, default): the tile is TH x 32 positions with TH = the number
+// of thread streams, and stream s owns tile row s, so a thread walks 32 consecutive
+// positions of one row: its kernel-row window img[y + ky][x .. x + K - 1] slides by one
+// column per position (one shared load instead of K, no per-tap address math), while the
+// delta vector of each position feeds 8 K FMAs.  Same sums in the same per-CTA order as the
+// other variant within a thread, then the same fixed-order reductions.
+template <int K>
+__global__ void __launch_bounds__(256, 2) conv_first_wgrad_rows_kernel(FirstWgradArgs a, int TH) {
+  extern __shared__ float sm[];
+  constexpr int IW = kWTW + K - 1;
+  const int IH = TH + K - 1;
+  const int coutp = a.n_cog * kWCO;
+  const int IMG = (IH * IW + 3) / 4 * 4;
+  const int buf_floats = IMG + TH * kWTW * coutp;
+  float* s_red = sm;
+  const bool async = coutp == a.cout;
+  const int per_stream = a.n_cog * K;
+  const int stream = threadIdx.x / per_stream, r = threadIdx.x % per_stream;
+  const int cog = r % a.n_cog, ky = r / a.n_cog;
+  const bool active = stream < TH;
+  float acc[kWCO][K];
+#pragma unroll
+  for (int o = 0; o < kWCO; ++o)
+#pragma unroll
+    for (int u = 0; u < K; ++u) acc[o][u] = 0.f;
+  const int tiles_x = (a.gc + kWTW - 1) / kWTW, tiles_y = (a.gr + TH - 1) / TH;
+  const long long total = (long long)a.n * tiles_x * tiles_y;
+  auto stage = [&](long long tile, int b) {
+    float* s_img = sm + b * buf_floats;
+    float* s_dy = s_img + IMG;
+    const int tx_ = (int)(tile % tiles_x);
+    const long long t2 = tile / tiles_x;
+    const int ty_ = (int)(t2 % tiles_y), img = (int)(t2 / tiles_y);
+    const int y0 = ty_ * TH, x0 = tx_ * kWTW;
+    for (int e = threadIdx.x; e < IH * IW; e += blockDim.x) {
+      const int iy = e / IW, ix = e % IW;
+      const int gy = y0 + iy, gx = x0 + ix;
+      const bool in = gy < a.H && gx < a.W;
+      const float* src = a.img + (in ? ((size_t)img * a.H + gy) * a.W + gx : 0);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(s_img + e)),
+                   "l"(src), "r"(in ? 4 : 0)
+                   : "memory");
+    }
+    if (async) {
+      const int vec = coutp / 4;
+      for (int e = threadIdx.x; e < TH * kWTW * vec; e += blockDim.x) {
+        const int v4 = e % vec, p = e / vec;
+        const int y = y0 + p / kWTW, x = x0 + p % kWTW;
+        const bool in = y < a.gr && x < a.gc;
+        const float* src = a.dy + (in ? (((size_t)img * a.gr + y) * a.gc + x) * a.cout + 4 * v4 : 0);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(s_dy + p * coutp + 4 * v4)),
+                     "l"(src), "r"(in ? 16 : 0)
+                     : "memory");
+      }
+    } else {
+      for (int e = threadIdx.x; e < TH * kWTW * coutp; e += blockDim.x) {
+        const int co = e % coutp, p = e / coutp;
+        const int y = y0 + p / kWTW, x = x0 + p % kWTW;
+        float v = 0.f;
+        if (co < a.cout && y < a.gr && x < a.gc) v = a.dy[(((size_t)img * a.gr + y) * a.gc + x) * a.cout + co];
+        s_dy[e] = v;
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (blockIdx.x < total) stage(blockIdx.x, 0);
+  int it = 0;
+  for (long long tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+    if (tile + gridDim.x < total) stage(tile + gridDim.x, (it + 1) & 1);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    const float* s_img = sm + (it & 1) * buf_floats;
+    const float* s_dy = s_img + IMG;
+    if (active) {
+      const float* irow = s_img + (stream + ky) * IW;
+      const float* drow = s_dy + (stream * kWTW) * coutp + cog * kWCO;
+      float win[K];
+#pragma unroll
+      for (int u = 0; u < K; ++u) win[u] = irow[u];
+#pragma unroll 8
+      for (int px = 0; px < kWTW; ++px) {
+        const float4* dp = reinterpret_cast<const float4*>(drow + px * coutp);
+        const float4 d0 = dp[0], d1 = dp[1];
+        const float dv[kWCO] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+#pragma unroll
+        for (int o = 0; o < kWCO; ++o)
+#pragma unroll
+          for (int u = 0; u < K; ++u) acc[o][u] = fmaf(dv[o], win[u], acc[o][u]);
+#pragma unroll
+        for (int u = 0; u + 1 < K; ++u) win[u] = win[u + 1];
+        win[K - 1] = irow[px + K];  // the last read (px = 31) lands in the row's halo
+      }
+    }
+    __syncthreads();
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  const int KK = K * K;
+  if (active) {
+#pragma unroll
+    for (int o = 0; o < kWCO; ++o)
+#pragma unroll
+      for (int u = 0; u < K; ++u) s_red[(stream * coutp + cog * kWCO + o) * KK + ky * K + u] = acc[o][u];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < a.cout * KK; e += blockDim.x) {
+    float s = 0.f;
+    for (int q = 0; q < TH; ++q) s += s_red[q * coutp * KK + e];
+    a.part[(size_t)blockIdx.x * a.cout * KK + e] = s;
+  }
+}
+
 // ------------------------------------------------------------------ fused conv + MPF
 // First convolution + activation + the MaxPoolingFragment layer after it (Alg. 1 then
 // Alg. 3) in one pass: the conv outputs of a 16 x 16 tile of
@@ -438,6 +552,20 @@ cudaError_t wgrad_kw(const FirstWgradArgs& a, cudaStream_t s) {
 template <int K>
 cudaError_t wgrad_k(const FirstWgradArgs& a, cudaStream_t s) {
   if constexpr (K >= 5) {
+    static const bool rows = getenv("MPF_FIRST_WGRAD_ROWS") ? atoi(getenv("MPF_FIRST_WGRAD_ROWS")) != 0 : true;
+    if (rows && wgrad_row(K)) {  // row-streamed tiles: TH = thread streams rows of 32
+      const int coutp = a.n_cog * kWCO;
+      const int TH = 256 / (a.n_cog * K);
+      const size_t img = ((size_t)(TH + K - 1) * (kWTW + K - 1) + 3) / 4 * 4;
+      const size_t bufs = 2 * (img + (size_t)TH * kWTW * coutp);
+      const size_t red = (size_t)TH * coutp * K * K;
+      const size_t smem = sizeof(float) * (bufs > red ? bufs : red);
+      cudaError_t e = cudaFuncSetAttribute(conv_first_wgrad_rows_kernel<K>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      conv_first_wgrad_rows_kernel<K><<<a.n_blocks, 256, smem, s>>>(a, TH);
+      return cudaGetLastError();
+    }
     if (wgrad_row(K)) return wgrad_kw<K, K>(a, s);
   }
   return wgrad_kw<K, kWT>(a, s);
