@@ -74,9 +74,11 @@ __global__ void __launch_bounds__(256) conv_first_fwd_kernel(FirstConvArgs a) {
     if (gy < a.H && gx < a.W) v = a.img[((size_t)img * a.H + gy) * a.W + gx];
     s_img[e] = v;
   }
-  for (int e = threadIdx.x; e < K * K * coutp; e += blockDim.x) {
-    const int co = e % coutp, t = e / coutp;
-    s_w[e] = co < a.cout ? a.w[co * K * K + t] : 0.f;  // canonical W[co][0][ky][kx]
+  {  // canonical W[co][0][ky][kx] -> s_w[tap][coutp]; blockDim = 64 n_cog = 8 coutp, so a
+     // thread keeps one co and steps taps by blockDim / coutp (no division per element)
+    const int co = threadIdx.x % coutp, tstep = blockDim.x / coutp;
+    const bool real = co < a.cout;
+    for (int t = threadIdx.x / coutp; t < K * K; t += tstep) s_w[t * coutp + co] = real ? a.w[co * K * K + t] : 0.f;
   }
   for (int e = threadIdx.x; e < coutp; e += blockDim.x) s_b[e] = e < a.cout ? a.bias[e] : 0.f;
   __syncthreads();
