@@ -305,7 +305,18 @@ __global__ void __launch_bounds__(256, 2) conv_first_wgrad_rows_kernel(FirstWgra
                    "l"(src), "r"(in ? 4 : 0)
                    : "memory");
     }
-    if (async) {
+    if (async && 256 % (coutp / 4) == 0) {  // a thread keeps one 16-B column: no division per copy
+      const int vec = coutp / 4, v4 = threadIdx.x % vec, pstep = blockDim.x / vec;
+      for (int p = threadIdx.x / vec; p < TH * kWTW; p += pstep) {
+        const int y = y0 + p / kWTW, x = x0 + p % kWTW;
+        const bool in = y < a.gr && x < a.gc;
+        const float* src = a.dy + (in ? (((size_t)img * a.gr + y) * a.gc + x) * a.cout + 4 * v4 : 0);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(s_dy + p * coutp + 4 * v4)),
+                     "l"(src), "r"(in ? 16 : 0)
+                     : "memory");
+      }
+    } else if (async) {
       const int vec = coutp / 4;
       for (int e = threadIdx.x; e < TH * kWTW * vec; e += blockDim.x) {
         const int v4 = e % vec, p = e / vec;
