@@ -355,7 +355,8 @@ def main():
     # there includes waiting for SMs held by its neighbour.  Per-kernel durations come from
     # the same number of steps run right after it with the weight gradients serialised on
     # the main stream, one CUDA-event pair per launch on its stream.
-    os.environ["MPF_NO_SIDE_STREAM"] = "1"
+    from paper_1302_1690_b200 import _lib as L
+    net.set_flags(L.MPF_FLAG_SERIAL)
     try:
         if world > 1:
             dist.barrier()
@@ -370,7 +371,7 @@ def main():
         stats = net.profile_end()
         ser_ms = p0.elapsed_time(p1)
     finally:
-        os.environ.pop("MPF_NO_SIDE_STREAM", None)
+        net.set_flags(0)
     peaks, src = _peaks()
     stats.sort(key=lambda r: -r["total_ms"])
     launches = sum(r["launches"] for r in stats)

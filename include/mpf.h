@@ -77,9 +77,36 @@ typedef struct {
   int32_t image_cols;   /* W */
   int32_t max_images;   /* largest n passed to forward/backward */
   int32_t precision;    /* MPF_PREC_* */
-  int32_t deterministic;/* reserved: every reduction is already fixed-order */
+  uint32_t flags;       /* MPF_FLAG_* kernel-selection flags; 0 = the measured defaults */
   int32_t debug_keep;   /* 1: keep every conv output on the tape (mpf_debug_tape), for parity tests */
 } mpf_config;
+
+/*
+ * Kernel-selection flags (mpf_config.flags; changeable later with mpf_net_set_flags).  The
+ * default (0) is the configuration DESIGN.md §5 measured fastest; every flag selects an
+ * alternative that computes the same sums (bitwise, or to fp32 summation order where the
+ * tile shape changes the order; parity-tested), for A/B measurements and tests:
+ *   SERIAL      one stream: the weight packs and weight gradients do not overlap the main
+ *               chain on the side stream (results bitwise identical: fixed-order reductions).
+ *   TC_SINGLE   tensor-core convolutions without CTA pairs (M = 128 per CTA).
+ *   TC_PAIR     CTA pairs (cta_group::2, M = 256) wherever they fit.
+ *   NTAP_ON     the multi-tap convolution on every eligible narrow layer (default: k >= 5).
+ *   NTAP_OFF    never the multi-tap convolution.
+ *   NTAP_NO_MC  multi-tap convolution without the cluster weight multicast.
+ *   WGRAD_M128  M = 128 weight-gradient tiles also for C_out <= 64 (default M = 64).
+ *   ROLE_TIMERS per-warp-role cycle counters of the tensor-core convolutions printed to
+ *               stderr after every launch (synchronises; profiling only).
+ */
+enum {
+  MPF_FLAG_SERIAL = 1u << 0,
+  MPF_FLAG_TC_SINGLE = 1u << 1,
+  MPF_FLAG_TC_PAIR = 1u << 2,
+  MPF_FLAG_NTAP_ON = 1u << 3,
+  MPF_FLAG_NTAP_OFF = 1u << 4,
+  MPF_FLAG_NTAP_NO_MC = 1u << 5,
+  MPF_FLAG_WGRAD_M128 = 1u << 6,
+  MPF_FLAG_ROLE_TIMERS = 1u << 7
+};
 
 /* Geometry of the padded uniform-fragment layout.
  * Activation l = 0..n_layers (a[0] = zero-padded image, a[l+1] = output of layer l). */
@@ -118,6 +145,10 @@ mpf_status mpf_net_create(const mpf_config* cfg, const mpf_layer* layers, int32_
 void mpf_net_destroy(mpf_net* net);
 
 mpf_status mpf_net_geometry(const mpf_net* net, mpf_geometry* out);
+
+/* Replace the net's MPF_FLAG_* flags (takes effect at the next call that launches work).
+ * MPF_ERR_ARG for unknown bits or for NTAP_ON with NTAP_OFF / TC_PAIR with TC_SINGLE. */
+mpf_status mpf_net_set_flags(mpf_net* net, uint32_t flags);
 
 /*
  * Device bytes the caller must provide for n_images images (n_images <= max_images):
@@ -159,14 +190,9 @@ mpf_status mpf_backward_image(mpf_net* net, const uint8_t* d_labels, const float
 
 /*
  * Forward + backward of n images in one call (the training step of PAPER.md:210 without
- * the update): same results as mpf_forward_image followed by mpf_backward_image (up to
- * fp32 summation order), but the softmax head (last FC + softmax + MCCE + dL/dx_hat,
- * PAPER.md:110-113, 197) runs inside the epilogue of the last hidden layer's tensor-core
- * convolution, so that layer's activations never reach device memory.  Gradients are
- * ADDED to the bound buffer; d_loss[n] (device, may be NULL) receives the per-image mean
- * losses.  Afterwards there is no tape to run mpf_backward_image on (MPF_ERR_STATE).
- * Falls back to the unfused sequence when the head cannot be fused (non-tensor-core last
- * hidden layer, > 8 classes).
+ * the update): exactly mpf_forward_image (no softmax output) followed by
+ * mpf_backward_image.  Gradients are ADDED to the bound buffer; d_loss[n] (device, may be
+ * NULL) receives the per-image mean losses.
  */
 mpf_status mpf_train_step(mpf_net* net, const float* d_images, int32_t n, const uint8_t* d_labels,
                           const float* h_class_w, float* d_loss, void* stream);
@@ -181,7 +207,8 @@ mpf_status mpf_train_step(mpf_net* net, const float* d_images, int32_t n, const 
  * point; otherwise they stay at theta.  The gradient buffer is zeroed either way.
  * h_out[5] = {L0, L_final, accepted alpha (0 if rejected), accepted (0/1), evaluations}.
  * Synchronises `stream` once per trial.  Errors: MPF_ERR_ARG for alpha0 <= 0, beta or c
- * outside (0, 1), n > 256; MPF_ERR_DATA for a non-finite L0 or ||g||.
+ * outside (0, 1), n > 256; MPF_ERR_DATA for a non-finite L0 or ||g||.  The gradient
+ * buffer is zeroed before the gradient pass, so leftover content does not enter g.
  */
 mpf_status mpf_armijo_step(mpf_net* net, const float* d_images, int32_t n, const uint8_t* d_labels,
                            const float* h_class_w, float alpha0, float beta, float c, int32_t max_backtracks,
@@ -231,8 +258,10 @@ mpf_status mpf_lbfgs_reject(mpf_lbfgs* lb, void* stream);
  * One full-batch L-BFGS iteration on one GPU over the n images (the whole training set;
  * pass the same images every call, or mpf_lbfgs_reset first): the loss and gradient at
  * theta (L = grad_scale * sum of the images' mean losses, g = grad_scale * sum of their
- * gradients; computed here only on the first call or after a reset / rejected search,
- * otherwise kept from the previous accepted trial), the direction, then trials
+ * gradients; evaluated here on the first call, after mpf_lbfgs_reset, and after
+ * mpf_lbfgs_set_gradient (which leaves the loss unknown); otherwise kept: from the
+ * previous accepted trial, or, after a rejected search, those at the restored theta0),
+ * the direction, then trials
  * theta0 + alpha d for alpha = alpha0 (empty history) or 1, times beta per backtrack, each a
  * full loss + gradient evaluation (mpf_train_step), until L <= L0 + c alpha g^T d; then
  * accept (pair update) or, after max_backtracks + 1 trials, reject.
@@ -281,11 +310,6 @@ enum { MPF_TAPE_VALUE = 0, MPF_TAPE_ARGMAX = 1 };
 mpf_status mpf_debug_tape(const mpf_net* net, int32_t layer, int32_t what, void* d_dst,
                           void* stream);
 
-/* Debug copy of a scratch region (which = 0: fused-head per-position losses, 1: first
- * delta buffer (dh after mpf_train_step), 2: head / bias partials); parity tests only. */
-mpf_status mpf_debug_scratch(const mpf_net* net, int32_t which, void* d_dst, uint64_t bytes, void* stream);
-
-/* Synchronise `stream` and report device-side data errors (bad labels) and CUDA errors. */
 /*
  * Mirror padding for same-size output ("pixels outside of the boundary of
  * testing images are synthesized by mirroring -- which allows to preserve the size of the
@@ -312,6 +336,7 @@ mpf_status mpf_mirror_pad(const float* d_in, int32_t planes, int32_t rows, int32
 mpf_status mpf_class_weights_auto(const mpf_net* net, const uint8_t* d_labels, int32_t n, float* h_class_w,
                                   uint64_t* h_counts, void* stream);
 
+/* Synchronise `stream` and report device-side data errors (bad labels) and CUDA errors. */
 mpf_status mpf_check(mpf_net* net, void* stream);
 
 /*

@@ -17,14 +17,24 @@ MPF_TANH, MPF_IDENTITY, MPF_LOGISTIC = 0, 1, 2
 MPF_PREC_TF32, MPF_PREC_FP32 = 0, 1
 MPF_TAPE_VALUE, MPF_TAPE_ARGMAX = 0, 1
 MPF_MAX_LAYERS = 24
+# kernel-selection flags (mpf_config.flags / mpf_net_set_flags; include/mpf.h)
+MPF_FLAG_SERIAL = 1 << 0
+MPF_FLAG_TC_SINGLE = 1 << 1
+MPF_FLAG_TC_PAIR = 1 << 2
+MPF_FLAG_NTAP_ON = 1 << 3
+MPF_FLAG_NTAP_OFF = 1 << 4
+MPF_FLAG_NTAP_NO_MC = 1 << 5
+MPF_FLAG_WGRAD_M128 = 1 << 6
+MPF_FLAG_ROLE_TIMERS = 1 << 7
 
 # every symbol include/mpf.h declares
 EXPORTS = ("mpf_version", "mpf_last_error", "mpf_net_create", "mpf_net_destroy", "mpf_net_geometry",
+           "mpf_net_set_flags",
            "mpf_net_memory", "mpf_net_bind", "mpf_forward_image", "mpf_backward_image", "mpf_sgd_step",
            "mpf_train_step", "mpf_train_step_host", "mpf_fragments_to_pixels", "mpf_mirror_pad", "mpf_class_weights_auto", "mpf_armijo_step",
            "mpf_lbfgs_state_bytes", "mpf_lbfgs_create", "mpf_lbfgs_destroy", "mpf_lbfgs_reset", "mpf_lbfgs_set_gradient", "mpf_lbfgs_direction",
            "mpf_lbfgs_trial", "mpf_lbfgs_accept", "mpf_lbfgs_reject", "mpf_lbfgs_step",
-           "mpf_debug_tape", "mpf_debug_scratch", "mpf_check", "mpf_profile_begin",
+           "mpf_debug_tape", "mpf_check", "mpf_profile_begin",
            "mpf_profile_end")
 
 
@@ -35,7 +45,7 @@ class MpfLayer(ctypes.Structure):
 class MpfConfig(ctypes.Structure):
     _fields_ = [("in_channels", ctypes.c_int32), ("patch", ctypes.c_int32), ("image_rows", ctypes.c_int32),
                 ("image_cols", ctypes.c_int32), ("max_images", ctypes.c_int32), ("precision", ctypes.c_int32),
-                ("deterministic", ctypes.c_int32), ("debug_keep", ctypes.c_int32)]
+                ("flags", ctypes.c_uint32), ("debug_keep", ctypes.c_int32)]
 
 
 _L1 = MPF_MAX_LAYERS + 1
@@ -73,6 +83,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.mpf_net_destroy.argtypes = [vp]
     lib.mpf_net_geometry.restype = st
     lib.mpf_net_geometry.argtypes = [vp, ctypes.POINTER(MpfGeometry)]
+    lib.mpf_net_set_flags.restype = st
+    lib.mpf_net_set_flags.argtypes = [vp, ctypes.c_uint32]
     lib.mpf_net_memory.restype = st
     lib.mpf_net_memory.argtypes = [vp, i32, u64p, u64p, u64p, u64p]
     lib.mpf_net_bind.restype = st
@@ -121,8 +133,6 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
                                            vp]
     lib.mpf_debug_tape.restype = st
     lib.mpf_debug_tape.argtypes = [vp, i32, i32, vp, vp]
-    lib.mpf_debug_scratch.restype = st
-    lib.mpf_debug_scratch.argtypes = [vp, i32, vp, ctypes.c_uint64, vp]
     lib.mpf_check.restype = st
     lib.mpf_check.argtypes = [vp, vp]
     lib.mpf_profile_begin.restype = st

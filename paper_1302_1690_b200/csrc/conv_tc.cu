@@ -34,6 +34,7 @@
 #include "conv_tc.h"
 #include "tc_ptx.cuh"
 #include "mpf_internal.h"
+#include "numerics.cuh"
 
 namespace mpf {
 
@@ -60,12 +61,8 @@ struct ConvTcParams {
   uint32_t tmem_cols;
   int n_tiles;   // tiles of M_CTA (single) or 2 x M_CTA (pair) positions
   int b_rows;    // weight rows per B slot (npad, or npad/2 per CTA of a pair)
-  unsigned long long* prof;  // optional role-timing counters (MPF_TC_PROF)
-  int per_img;               // positions per image (head mode)
-  TcHeadArgs hd;             // head mode only
+  unsigned long long* prof;  // optional role-timing counters (MPF_FLAG_ROLE_TIMERS)
 };
-
-constexpr int kHC = 8;  // max classes of the fused head
 
 // mbarrier wait that adds the cycles spent waiting to a counter when profiling
 __device__ __forceinline__ void twait(uint32_t bar, uint32_t parity, unsigned long long& acc, bool on) {
@@ -78,334 +75,13 @@ __device__ __forceinline__ void twait(uint32_t bar, uint32_t parity, unsigned lo
   acc += (unsigned long long)(clock64() - t0);
 }
 
-// TF32 rounding (nearest-even, finite-saturating: one F2FP instruction on sm_100a; the guarded
-// cvt.rna form takes four) of an MMA operand
-__device__ __forceinline__ float tf32r(float x) {
-  uint32_t r;
-  asm("cvt.rn.satfinite.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
-// tanh(v) = 1 - 2 / (exp(2v) + 1): two MUFU ops, absolute error ~1e-7 (far below the
-// TF32 rounding of every tensor-core operand), saturates correctly at +-inf.
-__device__ __forceinline__ float ex2_approx(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ float rcp_approx(float x) {
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-// branch-free SFU tanh: 1 - 2 / (2^(2 v log2 e) + 1); saturates to +-1 at +-inf
-__device__ __forceinline__ float fast_tanh(float v) {
-  return fmaf(-2.f, rcp_approx(ex2_approx(2.8853900817779268f * v) + 1.f), 1.f);
-}
-__device__ __forceinline__ float fast_logistic(float v) { return rcp_approx(1.f + ex2_approx(-1.4426950408889634f * v)); }
-
-// ----------------------------------------------------------------------------- fused head
-// Per-thread accumulators of the fused softmax head (persist over the CTA's tiles).
-struct HeadAcc {
-  float w[4][kHC];  // dW_L[c][column c0(jj) + lane] for the warp's 32-column chunks jj
-  float pb[4];      // db_h[column]
-  float l[kHC];     // db_L[c] (rows of half-0 warps)
-  __device__ void zero() {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      pb[j] = 0.f;
-#pragma unroll
-      for (int c = 0; c < kHC; ++c) w[j][c] = 0.f;
-    }
-#pragma unroll
-    for (int c = 0; c < kHC; ++c) l[c] = 0.f;
-  }
-};
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-// 32 columns c0.. of this thread's accumulator row -> h = act(acc + bias)
-__device__ __forceinline__ void load_h32(uint32_t taddr, int c0, int npad, int act, const float* s_bias, float (&h)[32]) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr + c0));
-  if (c0 + 16 < npad) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr + c0 + 16));
-  } else {
-#pragma unroll
-    for (int j = 16; j < 32; ++j) r[j] = 0u;
-  }
-  ptx::tmem_ld_wait();
-#pragma unroll
-  for (int j = 0; j < 32; ++j) h[j] = __uint_as_float(r[j]) + s_bias[c0 + j];
-  if (act == MPF_TANH) {
-#pragma unroll
-    for (int j = 0; j < 32; ++j) h[j] = fast_tanh(h[j]);
-  } else if (act == MPF_LOGISTIC) {
-#pragma unroll
-    for (int j = 0; j < 32; ++j) h[j] = fast_logistic(h[j]);
-  }
-}
-
-// swizzled staging box (TMA SWIZZLE_128B pattern): element (row, col) of a 32x32 fp32 box
-__device__ __forceinline__ uint32_t box_addr(uint32_t base, int row, int col) {
-  return base + row * 128 + ((((col >> 2) ^ (row & 7))) << 4) + ((col & 3) << 2);
-}
-
-// Softmax FC + MCCE + dL/dz + dh for the 128 rows x npad columns of every accumulator of a
-// tile, fused into the forward epilogue of the last hidden
-// layer: the TMEM accumulator (pre-activation of h) is read twice — pass 1 for the logits,
-// pass 2 for dh = (W_L^T dz) act'(h) — and h itself never reaches HBM.  The two warps of a
-// TMEM lane quarter own alternate 32-column chunks: their partial logits meet in shared
-// memory (named barrier per quarter).  dW_L and db_h are column sums over the rows of a
-// chunk: each chunk of h (then of dh) passes through the swizzled staging box, where lane j
-// sums column j (fixed order).  Per-position losses go to row_loss (reduced per image in
-// a fixed order afterwards).
-template <int NACC>
-__device__ __forceinline__ void head_epilogue(const ConvTcParams& p, const CUtensorMap* tmO, uint8_t* gen,
-                                              uint32_t tmem, int buf, int p0, int q, int half, int ew, int lane,
-                                              uint32_t sC, int& sb, const float* s_bias, uint32_t sWL, uint32_t sZ,
-                                              uint32_t sDL, HeadAcc& H) {
-  const TcHeadArgs& hd = p.hd;
-  const int C = hd.C;
-  const float* s_wl = reinterpret_cast<const float*>(gen + sWL);
-  const float* s_bl = s_wl + kHC * 256;
-  float* s_z = reinterpret_cast<float*>(gen + sZ) + q * 32 * kHC;
-  float* s_dl = reinterpret_cast<float*>(gen + sDL) + q * 32 * kHC;
-  const int per_frag = p.gr * p.gc;
-  for (int acc = 0; acc < NACC; ++acc) {
-    const int row0 = p0 + acc * 128 + q * 32;
-    const int pos = row0 + lane;
-    bool valid = false;
-    int lab = 255, img = 0;
-    if (pos < p.P_tot) {
-      img = pos / p.per_img;
-      const int rem = pos - img * p.per_img;
-      const int gl = rem / per_frag, r2 = rem - gl * per_frag;
-      const int i = r2 / p.gc, j = r2 - i * p.gc;
-      valid = i < p.out_vr && j < p.out_vc;
-      if (valid) {
-        // label through the fragment -> pixel map: y = r1 + k1 (r2 + k2 (... + kL i))
-        int yy = i, xx = j, rf = gl;
-        for (int l = hd.n_levels - 1; l >= 0; --l) {
-          const int kq = hd.pool_k[l];
-          const int d = rf % (kq * kq);
-          rf /= kq * kq;
-          yy = d / kq + kq * yy;
-          xx = d % kq + kq * xx;
-        }
-        if (yy < hd.O_H && xx < hd.O_W) lab = hd.labels[((long long)img * hd.O_H + yy) * hd.O_W + xx];
-        if (lab != 255 && lab >= C && half == 0) atomicOr(hd.err, 1);
-      }
-    }
-    const bool act = valid && lab < C;
-    const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + buf * (NACC * p.npad) + acc * p.npad;
-    // ---- pass 1: partial logits over this warp's chunks
-    float zp[kHC];
-#pragma unroll
-    for (int c = 0; c < kHC; ++c) zp[c] = 0.f;
-    for (int c0 = 32 * half; c0 < p.npad; c0 += 64) {
-      float h[32];
-      load_h32(taddr, c0, p.npad, p.act, s_bias, h);
-      const int nj4 = (c0 + 32 <= p.npad) ? 8 : 4;  // the last chunk may hold only 16 columns
-#pragma unroll
-      for (int c = 0; c < kHC; ++c) {
-        if (c < C) {
-          const float4* w4 = reinterpret_cast<const float4*>(s_wl + c * p.npad + c0);
-#pragma unroll
-          for (int j4 = 0; j4 < 8; ++j4) {
-            if (j4 >= nj4) break;
-            const float4 w = w4[j4];
-            zp[c] = fmaf(w.x, h[4 * j4], fmaf(w.y, h[4 * j4 + 1], fmaf(w.z, h[4 * j4 + 2], fmaf(w.w, h[4 * j4 + 3], zp[c]))));
-          }
-        }
-      }
-    }
-    if (half == 1) {
-#pragma unroll
-      for (int c = 0; c < kHC; ++c) s_z[lane * kHC + c] = zp[c];
-    }
-    named_bar(1 + q, 64);
-    if (half == 0) {
-      float dl[kHC], lossv = 0.f;
-#pragma unroll
-      for (int c = 0; c < kHC; ++c) dl[c] = 0.f;
-      if (act) {
-        float z[kHC];
-        float mx = -INFINITY;
-#pragma unroll
-        for (int c = 0; c < kHC; ++c) {
-          z[c] = zp[c] + s_z[lane * kHC + c] + s_bl[c];
-          if (c < C) mx = fmaxf(mx, z[c]);
-        }
-        float se = 0.f;
-#pragma unroll
-        for (int c = 0; c < kHC; ++c)
-          if (c < C) se += expf(z[c] - mx);
-        const float lse = mx + logf(se);
-        const int nl = hd.nlab[img];
-        const float wt = hd.cw[lab];
-        float zt = 0.f;
-#pragma unroll
-        for (int c = 0; c < kHC; ++c)
-          if (c == lab) zt = z[c];
-        lossv = wt * (lse - zt);
-        const float inv = nl > 0 ? wt / (float)nl : 0.f;
-#pragma unroll
-        for (int c = 0; c < kHC; ++c) dl[c] = c < C ? inv * (expf(z[c] - lse) - (c == lab ? 1.f : 0.f)) : 0.f;
-      }
-#pragma unroll
-      for (int c = 0; c < kHC; ++c) {
-        s_dl[lane * kHC + c] = dl[c];
-        H.l[c] += dl[c];
-      }
-      if (pos < p.P_tot) hd.row_loss[pos] = lossv;
-    }
-    named_bar(1 + q, 64);
-    float dl[kHC];
-#pragma unroll
-    for (int c = 0; c < kHC; ++c) dl[c] = s_dl[lane * kHC + c];
-    // ---- pass 2: dh, dW_L, db_h; dh leaves through the TMA store
-    int jj = 0;
-    for (int c0 = 32 * half; c0 < p.npad; c0 += 64, ++jj) {
-      float h[32];
-      load_h32(taddr, c0, p.npad, p.act, s_bias, h);
-      const uint32_t sbuf = sC + (ew * p.n_stage + sb) * kStageBytes;
-      if (lane == 0) {  // the store that last used this box has finished reading it
-        if (p.n_stage == 2) ptx::bulk_wait_read<1>();
-        else ptx::bulk_wait_read<0>();
-      }
-      __syncwarp();
-#pragma unroll
-      for (int j4 = 0; j4 < 8; ++j4) {
-        const uint32_t a = sbuf + lane * 128 + ((j4 ^ (lane & 7)) * 16);
-        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(h[4 * j4]), "f"(h[4 * j4 + 1]),
-                     "f"(h[4 * j4 + 2]), "f"(h[4 * j4 + 3])
-                     : "memory");
-      }
-      __syncwarp();
-      // dW_L[c][c0 + lane] += sum over the 32 rows of dz[row][c] * h[row][lane] (fixed row order)
-      {
-        float wacc[kHC];
-#pragma unroll
-        for (int c = 0; c < kHC; ++c) wacc[c] = 0.f;
-        const float* dlrow = s_dl;
-        for (int r = 0; r < 32; ++r) {
-          float hv;
-          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(hv) : "r"(box_addr(sbuf, r, lane)));
-#pragma unroll
-          for (int c = 0; c < kHC; ++c) wacc[c] = fmaf(dlrow[r * kHC + c], hv, wacc[c]);
-        }
-#pragma unroll
-        if (c0 + lane < p.npad) {
-#pragma unroll
-          for (int c = 0; c < kHC; ++c) H.w[jj & 3][c] += wacc[c];
-        }
-      }
-      __syncwarp();
-      float v[32];
-      const int nj4 = (c0 + 32 <= p.npad) ? 8 : 4;
-#pragma unroll
-      for (int j4 = 0; j4 < 8; ++j4) {
-        float s4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int c = 0; c < kHC; ++c) {
-          if (c < C && j4 < nj4) {
-            const float4 w = reinterpret_cast<const float4*>(s_wl + c * p.npad + c0)[j4];
-            s4[0] = fmaf(w.x, dl[c], s4[0]);
-            s4[1] = fmaf(w.y, dl[c], s4[1]);
-            s4[2] = fmaf(w.z, dl[c], s4[2]);
-            s4[3] = fmaf(w.w, dl[c], s4[3]);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float hv = h[4 * j4 + u];
-          const float der = p.act == MPF_TANH ? fmaf(-hv, hv, 1.f) : (p.act == MPF_LOGISTIC ? hv * (1.f - hv) : 1.f);
-          float d = act ? s4[u] * der : 0.f;
-          if (hd.round_dh) d = tf32r(d);
-          v[4 * j4 + u] = d;
-        }
-      }
-#pragma unroll
-      for (int j4 = 0; j4 < 8; ++j4) {
-        const uint32_t a = sbuf + lane * 128 + ((j4 ^ (lane & 7)) * 16);
-        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v[4 * j4]), "f"(v[4 * j4 + 1]),
-                     "f"(v[4 * j4 + 2]), "f"(v[4 * j4 + 3])
-                     : "memory");
-      }
-      __syncwarp();
-      {  // db_h[c0 + lane] += column sum of dh (fixed row order)
-        float sacc = 0.f;
-        for (int r = 0; r < 32; ++r) {
-          float dv;
-          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(dv) : "r"(box_addr(sbuf, r, lane)));
-          sacc += dv;
-        }
-        if (c0 + lane < p.npad) H.pb[jj & 3] += sacc;
-      }
-      ptx::fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) {
-        ptx::tma_store_2d(tmO, sbuf, c0, row0);
-        ptx::bulk_commit();
-      }
-      sb = (sb + 1 == p.n_stage) ? 0 : sb + 1;
-    }
-  }
-}
-
-// End of the persistent loop: combine the epilogue threads' head accumulators into one
-// partial per CTA, part[blockIdx.x] = [dW_L (C x Ch) | db_L (C) | db_h (Ch)], fixed order.
-__device__ __forceinline__ void head_partials(const ConvTcParams& p, uint8_t* gen, uint32_t sScratch, int q, int half,
-                                              int lane, const HeadAcc& H) {
-  const int C = p.hd.C, Ch = p.cout;
-  float* red = reinterpret_cast<float*>(gen + sScratch);   // [4][npad][kHC + 1]
-  float* redL = red + 4 * p.npad * (kHC + 1);              // [4][32][kHC]
-  named_bar(5, 32 * kEpiWarps);  // every epilogue warp is past its last tile
-  int jj = 0;
-  for (int c0 = 32 * half; c0 < p.npad; c0 += 64, ++jj) {
-    const int ch = c0 + lane;
-    if (ch >= p.npad) continue;  // the last chunk may hold only 16 columns
-#pragma unroll
-    for (int c = 0; c < kHC; ++c) red[(q * p.npad + ch) * (kHC + 1) + c] = H.w[jj & 3][c];
-    red[(q * p.npad + ch) * (kHC + 1) + kHC] = H.pb[jj & 3];
-  }
-  if (half == 0) {
-#pragma unroll
-    for (int c = 0; c < kHC; ++c) redL[(q * 32 + lane) * kHC + c] = H.l[c];
-  }
-  named_bar(5, 32 * kEpiWarps);
-  const int E = C * Ch + C + Ch;
-  float* out = p.hd.part + (size_t)blockIdx.x * E;
-  const int t = (q + 4 * half) * 32 + lane;  // 0..255 over the epilogue warps
-  for (int e = t; e < E; e += 32 * kEpiWarps) {
-    float s = 0.f;
-    if (e < C * Ch) {
-      const int c = e / Ch, ch = e % Ch;
-      for (int qq = 0; qq < 4; ++qq) s += red[(qq * p.npad + ch) * (kHC + 1) + c];
-    } else if (e < C * Ch + C) {
-      const int c = e - C * Ch;
-      for (int qq = 0; qq < 4; ++qq)
-        for (int l = 0; l < 32; ++l) s += redL[(qq * 32 + l) * kHC + c];
-    } else {
-      const int ch = e - C * Ch - C;
-      for (int qq = 0; qq < 4; ++qq) s += red[(qq * p.npad + ch) * (kHC + 1) + kHC];
-    }
-    out[e] = s;
-  }
-}
 
 // PAIR: a cluster of two CTAs on one TPC runs tcgen05 cta_group::2 MMAs (M = 256):
 // each CTA stages its own positions (A) and HALF of every weight tile (B), the leader
 // issues the MMAs, every accumulator lands in the TMEM of the CTA that owns its rows.
-template <int NACC, bool PAIR, bool HEAD>
+template <int NACC, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmO, ConvTcParams p) {
@@ -420,10 +96,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t barFull = sBar, barEmpty = barFull + 8 * p.n_stages;
   const uint32_t barTfull = barEmpty + 8 * p.n_stages, barTempty = barTfull + 16;
   const uint32_t sTmemSlot = barTempty + 16;
-  // head mode: W_L [kHC][npad], b_L, the logit exchange and dz rows of each lane quarter
-  const uint32_t sWL = (sTmemSlot + 16 + 15) & ~15u;
-  const uint32_t sZ = sWL + 4 * kHC * 256 + 64;   // [4][32][kHC]
-  const uint32_t sDL = sZ + 4 * 4 * 32 * kHC;      // [4][32][kHC]
   uint8_t* gen = smem_raw - ptx::smem_u32(smem_raw);  // generic pointer of shared address 0
   uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(gen + sTmemSlot);
   float* s_bias = reinterpret_cast<float*>(gen + sBias);
@@ -462,14 +134,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     else ptx::tmem_alloc(sTmemSlot, p.tmem_cols);
   }
   for (int c = threadIdx.x; c < 256; c += kThreads) s_bias[c] = (p.bias && c < p.cout) ? p.bias[c] : 0.f;
-  if (HEAD) {
-    float* s_wl = reinterpret_cast<float*>(gen + sWL);
-    for (int e = threadIdx.x; e < kHC * p.npad; e += kThreads) {
-      const int c = e / p.npad, ch = e % p.npad;
-      s_wl[e] = (c < p.hd.C && ch < p.cout) ? p.hd.wL[c * p.cout + ch] : 0.f;
-    }
-    for (int c = threadIdx.x; c < kHC; c += kThreads) s_wl[kHC * 256 + c] = c < p.hd.C ? p.hd.bL[c] : 0.f;
-  }
   ptx::tc_fence_before();
   if (PAIR) ptx::cluster_sync_all();  // barrier inits and TMEM allocation visible to the peer
   else __syncthreads();
@@ -558,16 +222,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ew = warp - 2;
     const int per_frag = p.gr * p.gc;
     int lt = 0, sb = 0;
-    HeadAcc hacc;
-    if (HEAD) hacc.zero();
     for (int tile = unit0; tile < p.n_tiles; tile += n_units, ++lt) {
       const int buf = lt & 1;
       twait(barTfull + 8 * buf, (lt >> 1) & 1, pc[7], prof_on);
       ptx::tc_fence_after();
       const int p0 = tile * tile_pos + my_off;
-      if constexpr (HEAD) {
-        head_epilogue<NACC>(p, &tmO, gen, tmem, buf, p0, q, half, ew, lane, sC, sb, s_bias, sWL, sZ, sDL, hacc);
-      } else
       for (int acc = 0; acc < NACC; ++acc) {
         const int row0 = p0 + acc * 128 + q * 32;
         const int pos = row0 + lane;
@@ -643,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (p.round_out) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = tf32r(v[j]);
+            for (int j = 0; j < 32; ++j) v[j] = tf32_rn(v[j]);
           }
           if (!valid) {
 #pragma unroll
@@ -689,7 +348,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (lane == 0) ptx::bulk_wait<0>();
-    if constexpr (HEAD) head_partials(p, gen, sS, q, half, lane, hacc);
   }
   if (prof_on && (warp >= 2 || lane == 0)) {
     const int slot_total = warp == 0 ? 2 : (warp == 1 ? 6 : 8);
@@ -939,7 +597,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (p.round_out) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) o[j] = tf32r(o[j]);
+          for (int j = 0; j < 16; ++j) o[j] = tf32_rn(o[j]);
         }
         if (!valid) {
 #pragma unroll
@@ -1011,10 +669,8 @@ cudaError_t make_map(CUtensorMap* m, const void* base, uint64_t cols, uint64_t r
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-int base_mode() {
-  const char* e = getenv("MPF_TC_BASE_MODE");
-  return e ? atoi(e) : 0;  // measured: the swizzle is address-based, base offset 0
-}
+// UMMA descriptor base-offset mode: measured, the swizzle is address-based, base offset 0
+int base_mode() { return 0; }
 
 int g_num_sms = 0;
 int num_sms() {
@@ -1028,8 +684,8 @@ int num_sms() {
 }
 
 unsigned long long* g_prof = nullptr;
-unsigned long long* prof_counters() {
-  if (!getenv("MPF_TC_PROF")) return nullptr;
+unsigned long long* prof_counters(uint32_t flags) {
+  if (!(flags & MPF_FLAG_ROLE_TIMERS)) return nullptr;
   if (!g_prof && cudaMalloc(&g_prof, 16 * sizeof(unsigned long long)) != cudaSuccess) g_prof = nullptr;
   if (g_prof) cudaMemset(g_prof, 0, 16 * sizeof(unsigned long long));
   return g_prof;
@@ -1050,10 +706,10 @@ void prof_report(const ConvTcParams& p, int nacc, bool pair, int grid) {
           h[1] / ctas / 256e6, h[5] / ctas / 256e6, h[9] / ctas / 256e6, h[8] / ctas / 256e6);
 }
 
-template <int NACC, bool PAIR, bool HEAD = false>
+template <int NACC, bool PAIR>
 cudaError_t launch_nacc(const CUtensorMap& A, const CUtensorMap& B, const CUtensorMap& O, ConvTcParams& p,
                         size_t smem, cudaStream_t s) {
-  auto kern = conv_tc_kernel<NACC, PAIR, HEAD>;
+  auto kern = conv_tc_kernel<NACC, PAIR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (!PAIR) {
@@ -1084,37 +740,28 @@ cudaError_t launch_nacc(const CUtensorMap& A, const CUtensorMap& B, const CUtens
 // CTA-pair policy: the pair halves the weight stream per SM, which pays only for wide,
 // deep layers (N >= 192, or N >= 128 with K >= 1536); everywhere else the single-CTA MMA
 // measured as fast or faster (per-layer A/B on cfg4/cfg5).
-// MPF_TC_PAIR=1/0 forces a mode.
-bool want_pair(int npad, int K) {
-  if (const char* e = getenv("MPF_TC_PAIR")) return atoi(e) != 0;
-  static const int k_min = getenv("MPF_TC_PAIR_KMIN") ? atoi(getenv("MPF_TC_PAIR_KMIN")) : 1536;
-  return npad >= 192 || (npad >= 128 && K >= k_min);
+// MPF_FLAG_TC_PAIR / MPF_FLAG_TC_SINGLE force a mode.
+bool want_pair(int npad, int K, uint32_t flags) {
+  if (flags & MPF_FLAG_TC_SINGLE) return false;
+  if (flags & MPF_FLAG_TC_PAIR) return true;
+  return npad >= 192 || (npad >= 128 && K >= 1536);
 }
 
 }  // namespace
 
-constexpr size_t kHeadSmem = 4 * kHC * 256 + 64 + 2 * 4 * 4 * 32 * kHC + 64;
-
-bool tc_head_supported(int C, int Ch, int act) {
-  if (getenv("MPF_NO_HEAD_FUSION")) return false;
-  return C >= 2 && C <= kHC && Ch >= 16 && Ch <= 256 && Ch % 4 == 0 &&
-         (act == MPF_TANH || act == MPF_LOGISTIC || act == MPF_IDENTITY);
-}
-
 bool tc_supported(int cin, int cout, int k) {
-  if (getenv("MPF_DISABLE_TC")) return false;
   return cin % 4 == 0 && cin >= 16 && cout % 4 == 0 && cout >= 4 && cout <= 256 && k >= 1 && k <= 8;
 }
 
 // The multi-tap kernel for narrow layers (k * npad <= 256, npad <= 64) with k >= 5: measured
 // 2.06 vs 2.58 ms on the cfg4 C5x5 dgrad (N = 32), but slower for k <= 4 (cfg5: 1.01 vs
 // 0.75 ms), where the cross-row epilogue outweighs the A reads it saves.
-// MPF_TC_NTAP=1 uses it for every eligible layer, =0 for none.
+// MPF_FLAG_NTAP_ON uses it for every eligible layer, MPF_FLAG_NTAP_OFF for none.
 static bool use_ntap(const TcConvArgs& a) {
   const int npad = (a.cout + 15) / 16 * 16;
-  const bool ok = a.head == nullptr && a.k >= 2 && a.k <= 8 && a.k * npad <= 256 && npad <= 64;
-  const char* e = getenv("MPF_TC_NTAP");
-  if (e) return ok && atoi(e) != 0;
+  const bool ok = a.k >= 2 && a.k <= 8 && a.k * npad <= 256 && npad <= 64;
+  if (a.flags & MPF_FLAG_NTAP_OFF) return false;
+  if (a.flags & MPF_FLAG_NTAP_ON) return ok;
   return ok && a.k >= 5;
 }
 
@@ -1178,9 +825,8 @@ static cudaError_t launch_conv_ntap(const TcConvArgs& a, cudaStream_t s, int* gr
   if (e != cudaSuccess) return e;
   e = make_map(&O3, a.out, (uint64_t)a.cout, (uint64_t)p.P_tot, (uint32_t)(32 - (a.k - 1)));
   if (e != cudaSuccess) return e;
-  // weight multicast across a cluster of two (MPF_TC_NTAP_MC=0 turns it off)
-  const char* mce = getenv("MPF_TC_NTAP_MC");
-  const bool mc = (mce ? atoi(mce) != 0 : true) && p.n_tiles >= 2;
+  // weight multicast across a cluster of two (MPF_FLAG_NTAP_NO_MC turns it off)
+  const bool mc = !(a.flags & MPF_FLAG_NTAP_NO_MC) && p.n_tiles >= 2;
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e2 != cudaSuccess) return e2;
@@ -1241,20 +887,10 @@ cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s, int* grid_out) {
   p.bias = a.bias;
   p.mul_dact = a.mul_dact;
   p.base_mode = base_mode();
-  p.prof = prof_counters();
-  const bool head = a.head != nullptr;
-  if (head) {
-    p.hd = *a.head;
-    p.per_img = a.head->F * a.gr * a.gc;
-  }
+  p.prof = prof_counters(a.flags);
   int nacc = 256 / p.npad;  // two accumulator sets in 512 TMEM columns
   if (nacc > 4) nacc = 4;
   if (nacc < 1) nacc = 1;
-  if (head && nacc > 2) nacc = 2;  // the fused head epilogue is heavier per row
-  if (const char* e = getenv("MPF_TC_NACC_MAX")) {  // tuning knob
-    const int m = atoi(e);
-    if (m >= 1 && nacc > m) nacc = m;
-  }
   auto set_nacc = [&](int na) {
     const int rows_needed = na * 128 + a.k - 1;
     p.nbox = (rows_needed + 255) / 256;
@@ -1264,7 +900,7 @@ cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s, int* grid_out) {
   set_nacc(nacc);
   // shared memory: stages of [A slab | k weight taps] (2..4, as many as fit), epilogue
   // staging (two boxes per warp when 3 stages still fit, else one)
-  const size_t base_fixed = 1024 + 4 * 256 + 512 + (head ? kHeadSmem : 0);
+  const size_t base_fixed = 1024 + 4 * 256 + 512;
   const size_t total = 227 * 1024;
   int ns = 0, nst = 0;
   auto plan_smem = [&](bool pr) {
@@ -1285,7 +921,7 @@ cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s, int* grid_out) {
   };
   // keep the preferred mode and give up accumulator depth first (a smaller A slab lets two
   // stages fit: measured faster than switching mode); then try the other mode
-  bool pair = want_pair(p.npad, a.k * a.k * a.cin);
+  bool pair = want_pair(p.npad, a.k * a.k * a.cin, a.flags);
   bool ok = false;
   for (int na = nacc; na >= 1 && !ok; --na) {
     set_nacc(na);
@@ -1312,8 +948,6 @@ cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s, int* grid_out) {
   p.tmem_cols = cols;
   p.n_tiles = (p.P_tot + (pair ? 2 : 1) * m_cta - 1) / ((pair ? 2 : 1) * m_cta);
   const size_t smem = fixed + (size_t)nst * p.stage_bytes;
-  if (head && (size_t)nst * p.stage_bytes < sizeof(float) * (4 * (size_t)p.npad * (kHC + 1) + 4 * 32 * kHC))
-    return cudaErrorInvalidConfiguration;  // the head partials reuse the stage area
   const int pairs = p.n_tiles < num_sms() / 2 ? p.n_tiles : num_sms() / 2;
   if (grid_out) *grid_out = pair ? 2 * pairs : (p.n_tiles < num_sms() ? p.n_tiles : num_sms());
   CUtensorMap A, B, O;
@@ -1323,10 +957,6 @@ cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s, int* grid_out) {
   if (e != cudaSuccess) return e;
   e = make_map(&O, a.out, (uint64_t)a.cout, (uint64_t)p.P_tot, 32u);
   if (e != cudaSuccess) return e;
-  if (head) {
-    if (pair) return nacc == 1 ? launch_nacc<1, true, true>(A, B, O, p, smem, s) : launch_nacc<2, true, true>(A, B, O, p, smem, s);
-    return nacc == 1 ? launch_nacc<1, false, true>(A, B, O, p, smem, s) : launch_nacc<2, false, true>(A, B, O, p, smem, s);
-  }
   if (pair) {
     switch (nacc) {
       case 1: return launch_nacc<1, true>(A, B, O, p, smem, s);
@@ -1365,8 +995,6 @@ struct WgTcParams {
   uint32_t a_bytes, b_bytes, stage_bytes;
   int n_stages_ring;
   uint32_t tmem_cols;
-  const float* dy;       // A operand straight from global (the TMEM-A variant)
-  uint32_t a_col0;       // TMEM column of the two A slots (TMEM-A variant)
 };
 
 template <int MT>  // output channels per tile: 128, or 64 (M = 64 MMA) when C_out <= 64
@@ -1474,180 +1102,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) ptx::tmem_dealloc(tmem, p.tmem_cols);
 }
 
-// The same GEMM with the dY operand in tensor memory (kind::tf32, A from TMEM): with A in
-// shared memory the tensor core re-reads the 4 KB dY tile of every K step once per group
-// (G times) and the shared-memory port, not the MMA, sets the pace.  Here
-// the 8 epilogue warps, idle during the main loop, load dY straight from global memory
-// (lane = output channel, a warp reads one 128-B row of dY per position, coalesced) and
-// write it to one of two TMEM A slots of 64 columns (= the 64 positions of a stage,
-// K-major: lane co, column p); the MMA warp reads A from there and only the X slabs go
-// through shared memory.  Same MMAs per group as wgrad_tc_kernel<128>; the split-K
-// partition can differ (fewer groups per CTA), so the totals agree to rounding (tested).
-// Opt-in (MPF_WGRAD_TS=1): measured on cfg4 at 6.07 / 2.91 / 5.00 ms for FC1 / C3 / C5
-// against 6.38 / 2.80 / 4.52 ms, and only 5.66 / 2.58 / 4.35 ms even with the dY loads
-// removed, i.e. the tensor pipe, not the A re-reads, bounds these GEMMs.
-__global__ void __launch_bounds__(kThreads, 1)
-    wgrad_ts_kernel(const __grid_constant__ CUtensorMap tmX, WgTcParams p) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  const uint32_t sbase = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
-  const uint32_t sBar = sbase + p.n_stages_ring * p.stage_bytes;
-  const uint32_t barFull = sBar, barEmpty = sBar + 8 * p.n_stages_ring, barT = sBar + 16 * p.n_stages_ring;
-  const uint32_t aFull = barT + 8, aEmpty = barT + 24;  // 2 A slots each
-  const uint32_t sTmemSlot = barT + 40;
-  uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (sTmemSlot - ptx::smem_u32(smem_raw)));
-  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-  const int mt = blockIdx.x % p.m_tiles;
-  const int set = (blockIdx.x / p.m_tiles) % p.n_sets;
-  const int split = blockIdx.x / (p.m_tiles * p.n_sets);
-  const int g0 = (int)((long long)set * p.n_groups / p.n_sets);
-  const int G = (int)((long long)(set + 1) * p.n_groups / p.n_sets) - g0;
-  const int N = 32 * p.k;
-  const long long pbeg = (long long)split * p.chunk_stages * kWR;
-
-  if (warp == 0 && lane == 0) {
-    ptx::prefetch_tmap(&tmX);
-    for (int i = 0; i < p.n_stages_ring; ++i) {
-      ptx::mbar_init(barFull + 8 * i, 1);
-      ptx::mbar_init(barEmpty + 8 * i, 1);
-    }
-    ptx::mbar_init(barT, 1);
-    for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(aFull + 8 * i, kEpiWarps);
-      ptx::mbar_init(aEmpty + 8 * i, 1);
-    }
-    ptx::fence_mbar_init();
-  }
-  if (warp == 1) ptx::tmem_alloc(sTmemSlot, p.tmem_cols);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = *tmem_slot_ptr;
-  const int n_st = p.chunk_stages;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      for (int st = 0; st < n_st; ++st) {
-        const int slot = st % p.n_stages_ring;
-        ptx::mbar_wait(barEmpty + 8 * slot, ((st / p.n_stages_ring) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(barFull + 8 * slot, G * p.b_bytes);
-        const uint32_t sa = sbase + slot * p.stage_bytes;
-        const int row = (int)(pbeg + (long long)st * kWR);
-        for (int g = 0; g < G; ++g) {
-          const int ng = g0 + g, ky = ng / p.n_cc, cc = ng % p.n_cc;
-          ptx::tma_load_2d(sa + g * p.b_bytes, &tmX, barFull + 8 * slot, cc * kKC, row + ky * p.gc);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    const uint32_t idesc = ptx::idesc_tf32_bmn(128, N);
-    for (int st = 0; st < n_st; ++st) {
-      const int slot = st % p.n_stages_ring, as = st & 1;
-      ptx::mbar_wait(aFull + 8 * as, (st >> 1) & 1);
-      ptx::mbar_wait(barFull + 8 * slot, (st / p.n_stages_ring) & 1);
-      ptx::tc_fence_after();
-      const uint32_t sa = sbase + slot * p.stage_bytes;
-      const uint64_t bd0 = ptx::sdesc_mn_sw128_32b(sa, 128, 512);
-      const uint32_t a0 = tmem + p.a_col0 + as * kWR;
-      for (int g = 0; g < G; ++g) {
-#pragma unroll
-        for (int r8 = 0; r8 < kWR / 8; ++r8) {
-          const uint64_t bd = bd0 + (uint64_t)((g * p.b_bytes + r8 * 1024) >> 4);
-          ptx::mma_tf32_ts_elect(tmem + g * N, a0 + r8 * 8, bd, idesc, (st | r8) != 0);
-        }
-      }
-      ptx::mma_commit_elect(barEmpty + 8 * slot);
-      ptx::mma_commit_elect(aEmpty + 8 * as);
-    }
-    ptx::mma_commit_elect(barT);
-  } else {
-    const int q = warp & 3, half = (warp - 2) >> 2;
-    const int co = mt * 128 + q * 32 + lane;
-    const bool row_ok = co < p.cout;
-    // ---- A producer: dY[p][co] of this stage's 32 positions of `half` -> TMEM lane co
-    {
-      const float* src = p.dy + (row_ok ? co : 0);
-      const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-      // two register buffers: the loads of stage st + 1 are in flight while stage st waits
-      // for its TMEM slot and is written
-      uint32_t r0[32], r1[32];
-      auto load = [&](int st, uint32_t (&r)[32]) {
-        const long long pr = pbeg + (long long)st * kWR + half * 32;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const long long pj = pr + j;
-          r[j] = (row_ok && st < n_st && pj < p.P_tot) ? __float_as_uint(__ldg(src + pj * p.cout)) : 0u;
-        }
-      };
-      auto put = [&](int st, const uint32_t (&r)[32]) {
-        const int as = st & 1;
-        ptx::mbar_wait(aEmpty + 8 * as, ((st >> 1) & 1) ^ 1);
-        ptx::tc_fence_after();
-        ptx::tmem_st32(tmem + lane_addr + p.a_col0 + as * kWR + half * 32, r);
-        ptx::tmem_st_wait();
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(aFull + 8 * as);
-      };
-      load(0, r0);
-      for (int st = 0; st < n_st; st += 2) {
-        load(st + 1, r1);
-        put(st, r0);
-        if (st + 1 >= n_st) break;
-        load(st + 2, r0);
-        put(st + 1, r1);
-      }
-    }
-    // ---- epilogue (as wgrad_tc_kernel<128>)
-    ptx::mbar_wait(barT, 0);
-    ptx::tc_fence_after();
-    const int K = p.k * p.k * p.cin;
-    float* dst = p.part + ((long long)split * p.cout + (row_ok ? co : 0)) * K;
-    for (int g = 0; g < G; ++g) {
-      const int ng = g0 + g, ky = ng / p.n_cc, cc = ng % p.n_cc;
-      for (int c0 = half * 16; c0 < N; c0 += 32) {
-        float v[16];
-        ptx::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + g * N + c0, v);
-        if (row_ok) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int n = c0 + j, kx = n / 32, ci = cc * kKC + (n % 32);
-            if (ci < p.cin) dst[(ky * p.k + kx) * p.cin + ci] = n_st > 0 ? v[j] : 0.f;
-          }
-        }
-      }
-    }
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 1) ptx::tmem_dealloc(tmem, p.tmem_cols);
-}
-
 }  // namespace
 
-cudaError_t make_tmap_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
-                          const uint32_t* box, bool sw128) {
-  cudaError_t e = get_encoder();
-  if (e != cudaSuccess) return e;
-  cuuint64_t d[5], st[4];
-  cuuint32_t bx[5], es[5];
-  for (int i = 0; i < rank; ++i) {
-    d[i] = dims[i];
-    bx[i] = box[i];
-    es[i] = 1;
-    if (i + 1 < rank) st[i] = strides[i];
-  }
-  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(base), d, st, bx, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
-}
-
-cudaError_t make_tmap_sw128(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
-  return make_map(m, base, cols, rows, box_rows);
-}
-
 bool tc_wgrad_supported(int cin, int cout, int k) {
-  if (getenv("MPF_DISABLE_TC")) return false;
   return cin % 4 == 0 && cin >= 8 && cout % 4 == 0 && cout <= 256 && k >= 1 && k <= 8;
 }
 
@@ -1664,17 +1121,9 @@ cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits_out, cudaStream_t 
   p.G = 512 / N;
   if (p.G > p.n_groups) p.G = p.n_groups;
   p.n_sets = (p.n_groups + p.G - 1) / p.G;
-  const int MT = (a.cout <= 64 && !getenv("MPF_WGRAD_M128")) ? 64 : 128;
-  // TMEM-A variant (MT = 128): two A slots of kWR columns next to the accumulators
-  const char* tse = getenv("MPF_WGRAD_TS");
-  const bool ts = MT == 128 && N <= 256 && (tse ? atoi(tse) != 0 : false);
-  if (ts) {
-    p.G = (512 - 2 * kWR) / N;
-    if (p.G > p.n_groups) p.G = p.n_groups;
-    p.n_sets = (p.n_groups + p.G - 1) / p.G;
-  }
+  const int MT = (a.cout <= 64 && !(a.flags & MPF_FLAG_WGRAD_M128)) ? 64 : 128;
   p.m_tiles = (a.cout + MT - 1) / MT;
-  p.a_bytes = ts ? 0 : (MT / 32) * kWR * 128;
+  p.a_bytes = (MT / 32) * kWR * 128;
   p.b_bytes = (kWR + 8) * 128;
   p.stage_bytes = p.a_bytes + p.G * p.b_bytes;
   const size_t budget = 225 * 1024 - 1024 - 256;
@@ -1687,10 +1136,8 @@ cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits_out, cudaStream_t 
     p.n_stages_ring = 2;
   }
   uint32_t cols = 32;
-  while (cols < (uint32_t)(p.G * N + (ts ? 2 * kWR : 0))) cols <<= 1;
+  while (cols < (uint32_t)(p.G * N)) cols <<= 1;
   p.tmem_cols = cols;
-  p.a_col0 = (uint32_t)(p.G * N);
-  p.dy = a.dy;
   const long long total_stages = (p.P_tot + kWR - 1) / kWR;
   const int per_split_blocks = p.m_tiles * p.n_sets;
   int splits = num_sms() / per_split_blocks;  // one wave of co-resident CTAs
@@ -1710,12 +1157,6 @@ cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits_out, cudaStream_t 
   e = make_map(&X, a.x, (uint64_t)a.cin, (uint64_t)p.P_tot, (uint32_t)(kWR + 8), CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   if (e != cudaSuccess) return e;
   const size_t smem = 1024 + (size_t)p.n_stages_ring * p.stage_bytes + 256;
-  if (ts) {
-    e = cudaFuncSetAttribute(wgrad_ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    wgrad_ts_kernel<<<splits * per_split_blocks, kThreads, smem, s>>>(X, p);
-    return cudaGetLastError();
-  }
   auto kern = MT == 64 ? wgrad_tc_kernel<64> : wgrad_tc_kernel<128>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

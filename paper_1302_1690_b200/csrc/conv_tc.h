@@ -5,6 +5,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include "../../include/mpf.h"
+
 namespace mpf {
 
 constexpr int kMaxSplits = 296;  // split-K partial slots of the weight-gradient GEMMs (2 x 148 SMs)
@@ -28,28 +30,8 @@ struct TcConvArgs {
   int zero_pad;       // (SIMT path) write zeros outside the valid region; the TC path always does
   const float* mul_dact;  // nullable: multiply by act'(mul_dact[same position])
   int dact;
-  const struct TcHeadArgs* head;  // nullable: fuse the softmax head into this (forward) conv
+  uint32_t flags;     // MPF_FLAG_* kernel selection (mpf.h)
 };
-
-// Softmax head fused into the epilogue of the forward conv that produces the last hidden
-// layer h: instead of h the kernel writes
-// dh = (W_L^T dz) * act'(h) to `out`, per-position losses to row_loss, and per-CTA
-// partials [grid][C*Ch + C + Ch] = (dW_L, db_L, db_h) to part.
-struct TcHeadArgs {
-  const float* wL;       // [C][Ch] softmax FC weights (canonical 1x1)
-  const float* bL;       // [C]
-  int C;
-  const uint8_t* labels; // [n][O_H][O_W], 255 = ignore
-  int O_H, O_W, F, n_levels;
-  int pool_k[24];
-  const int* nlab;       // [n] labelled pixels per image
-  float cw[16];          // class weights
-  float* row_loss;       // [positions] w_t (lse - z_t) of labelled valid positions, else 0
-  float* part;           // [grid][C*Ch + C + Ch]
-  int* err;              // label >= C flag
-  int round_dh;          // round dh to tf32 (operand of the FC1 dgrad / wgrad MMAs)
-};
-bool tc_head_supported(int C, int Ch, int act);
 
 // Weight gradient: part[s][co][(ky*k+kx)*cin+ci] = sum_{p in split s} dy[p][co] * x[p+(ky,kx)][ci]
 struct TcWgradArgs {
@@ -59,16 +41,11 @@ struct TcWgradArgs {
   int cin, cout, k;
   float* part;
   size_t part_cap_floats;
+  uint32_t flags;     // MPF_FLAG_* kernel selection (mpf.h)
 };
 
 bool tc_supported(int cin, int cout, int k);
 bool tc_wgrad_supported(int cin, int cout, int k);
 cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s, int* grid_out = nullptr);
 cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits, cudaStream_t s);
-// 2-D fp32 tensor map [rows][cols] (cols contiguous), box {32 cols, box_rows}, SWIZZLE_128B
-cudaError_t make_tmap_sw128(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows);
-// general fp32 tensor map: dims[0] innermost, strides[i] = bytes between steps of dim i+1
-cudaError_t make_tmap_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
-                          const uint32_t* box, bool sw128);
-
 }  // namespace mpf

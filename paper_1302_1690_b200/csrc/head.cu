@@ -27,6 +27,7 @@
 
 #include "head_common.cuh"
 #include "mpf_internal.h"
+#include "numerics.cuh"
 #include "tc_ptx.cuh"
 
 namespace mpf {
@@ -37,13 +38,6 @@ constexpr int kTP = 64;  // positions per tile
 constexpr int kThr = 256;
 constexpr int kMaxC = 16;
 
-// TF32 rounding (nearest-even, finite-saturating: one F2FP instruction on sm_100a; the guarded
-// cvt.rna form takes four) of an MMA operand
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rn.satfinite.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
 
 __device__ __forceinline__ float act_der(int act, float y) {
   if (act == MPF_TANH) return 1.f - y * y;
@@ -343,7 +337,7 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
           for (int u = 0; u < 4; ++u) {
             d[u] = sacc[u] * (TANH ? fmaf(-hh[u], hh[u], 1.f) : act_der(a.hidden_act, hh[u]));
             accP4[0][u] += d[u];
-            if (a.round_tf32) d[u] = tf32_rna(d[u]);
+            if (a.round_tf32) d[u] = tf32_rn_sat(d[u]);
           }
           if (lane_on) *dh4 = make_float4(d[0], d[1], d[2], d[3]);
         }
@@ -402,7 +396,7 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
               for (int u = 0; u < 4; ++u) {
                 d[u] = sacc[u] * (TANH ? fmaf(-hh[u], hh[u], 1.f) : act_der(a.hidden_act, hh[u]));
                 accP4[m][u] += d[u];
-                if (a.round_tf32) d[u] = tf32_rna(d[u]);
+                if (a.round_tf32) d[u] = tf32_rn_sat(d[u]);
               }
               reinterpret_cast<float4*>(dh_row)[g] = make_float4(d[0], d[1], d[2], d[3]);
             }
@@ -423,7 +417,7 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
             }
             const float d = sacc * (TANH ? fmaf(-hv, hv, 1.f) : act_der(a.hidden_act, hv));
             accP[VEC ? 0 : m] += d;
-            dh_row[ch] = a.round_tf32 ? tf32_rna(d) : d;
+            dh_row[ch] = a.round_tf32 ? tf32_rn_sat(d) : d;
           }
         }
       }

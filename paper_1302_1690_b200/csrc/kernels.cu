@@ -10,18 +10,12 @@
 #include <stdint.h>
 
 #include "mpf_internal.h"
+#include "numerics.cuh"
 
 namespace mpf {
 
 static inline long long mpf_min_ll(long long a, long long b) { return a < b ? a : b; }
 
-// TF32 rounding (nearest-even, finite-saturating: one F2FP instruction on sm_100a; the guarded
-// cvt.rna form takes four) of an MMA operand
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rn.satfinite.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
 
 __device__ __forceinline__ float act_fwd(int act, float v) {
   if (act == MPF_TANH) return tanhf(v);
@@ -103,7 +97,7 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(ConvArgs a, int tiles_x)
       v = acc[o] + (a.bias ? a.bias[co] : 0.f);
       v = act_fwd(a.act, v);
       if (a.mul_dact) v *= act_der(a.dact, a.mul_dact[base + co]);
-      if (a.round_tf32) v = tf32_rna(v);
+      if (a.round_tf32) v = tf32_rn(v);
     }
     a.out[base + co] = v;
   }
@@ -508,27 +502,6 @@ __global__ void loss_finalize_kernel(const float* __restrict__ part, int parts, 
   if (threadIdx.x == 0) loss[img] = nlab[img] > 0 ? s[0] / (float)nlab[img] : 0.f;
 }
 
-__global__ void loss_rows_kernel(const float* __restrict__ rl, long long per_img, const int* __restrict__ nlab,
-                                 float* loss) {
-  __shared__ float s[1024];
-  const int img = blockIdx.x;
-  float t = 0.f;
-  for (long long i = threadIdx.x; i < per_img; i += 1024) t += rl[(long long)img * per_img + i];
-  s[threadIdx.x] = t;
-  __syncthreads();
-  for (int w = 512; w > 0; w >>= 1) {
-    if (threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) loss[img] = nlab[img] > 0 ? s[0] / (float)nlab[img] : 0.f;
-}
-
-cudaError_t launch_loss_rows(const float* row_loss, long long per_img, const int* nlab, int n, float* loss,
-                             cudaStream_t s) {
-  loss_rows_kernel<<<n, 1024, 0, s>>>(row_loss, per_img, nlab, loss);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_loss_finalize(const float* part, int parts, const int* nlab, int n, float* loss,
                                  cudaStream_t s) {
   loss_finalize_kernel<<<n, 256, 0, s>>>(part, parts, nlab, loss);
@@ -562,8 +535,8 @@ __global__ void pack_kernel(const float* __restrict__ w, int cout, int cin, int 
     const int ci = (int)(t % cin);
     const int co = (int)(t / cin);
     const float v = w[e];
-    wp[(((long long)co * k + ky) * k + kx) * cin + ci] = round_fwd ? tf32_rna(v) : v;
-    if (dp) dp[(((long long)ci * k + (k - 1 - ky)) * k + (k - 1 - kx)) * cout + co] = round_dgrad ? tf32_rna(v) : v;
+    wp[(((long long)co * k + ky) * k + kx) * cin + ci] = round_fwd ? tf32_rn(v) : v;
+    if (dp) dp[(((long long)ci * k + (k - 1 - ky)) * k + (k - 1 - kx)) * cout + co] = round_dgrad ? tf32_rn(v) : v;
   }
 }
 

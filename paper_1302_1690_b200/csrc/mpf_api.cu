@@ -235,7 +235,6 @@ static void layout_memory(Net* N, int n) {
   N->off_bpart = s; s = align256(s + sizeof(float) * bp);
   N->off_lossp = s; s = align256(s + sizeof(float) * (size_t)N->loss_parts * n);
   N->off_err = s; s = align256(s + 256);
-  N->off_rowloss = s; s = align256(s + sizeof(float) * (size_t)h_pos * n);  // fused-head per-position losses
   {  // two staging slots [images | labels] for host-buffer steps
     const size_t s0 = s;
     N->off_stage_img = s; s = align256(s + sizeof(float) * (size_t)n * N->cfg.in_channels * N->cfg.image_rows * N->cfg.image_cols);
@@ -262,20 +261,9 @@ static const float* act_ptr(const Net* N, int l) {
   return nullptr;
 }
 
-static bool fwd_round_off() { return getenv("MPF_DEBUG_FWD_FP32") != nullptr; }
-
 static bool use_tc(const Net* N, const LayerPlan& P, bool dgrad) {
-  if (!dgrad && fwd_round_off()) return false;
   if (N->cfg.precision != MPF_PREC_TF32) return false;
   return tc_supported(dgrad ? P.cout : P.cin, dgrad ? P.cin : P.cout, P.L.k);
-}
-
-// Does the training head run on the tensor cores (head_tc.cu)?  Then the last hidden
-// layer writes h TF32-rounded (an MMA operand), like every other tensor-core input.
-static bool head_tc_used(const Net* N) {
-  if (fwd_round_off()) return false;
-  const int L = N->n_layers - 1;
-  return head_tc_ok(N->classes, N->a[L].C, true, N->cfg.precision == MPF_PREC_TF32);
 }
 
 }  // namespace mpf
@@ -295,7 +283,12 @@ mpf_status mpf_net_create(const mpf_config* cfg, const mpf_layer* layers, int32_
   N->cfg = *cfg;
   N->n_layers = n_layers;
   for (int l = 0; l < n_layers; ++l) N->lp[l].L = layers[l];
-  mpf_status st = plan(N);
+  mpf_status st = mpf_net_set_flags(N, cfg->flags);
+  if (st != MPF_OK) {
+    delete N;
+    return st;
+  }
+  st = plan(N);
   if (st != MPF_OK) {
     delete N;
     return st;
@@ -431,10 +424,10 @@ mpf_status mpf_net_bind(mpf_net* N, void* p, void* g, void* t, void* s, int32_t 
 }
 
 // The side stream (and its events) used to overlap independent work with the main chain:
-// weight packs in the forward, weight gradients in the backward.  MPF_NO_SIDE_STREAM=1
+// weight packs in the forward, weight gradients in the backward.  MPF_FLAG_SERIAL
 // serialises everything on the caller's stream.
 static cudaStream_t side_stream(Net* N, cudaStream_t s) {
-  if (getenv("MPF_NO_SIDE_STREAM")) return s;
+  if (N->cfg.flags & MPF_FLAG_SERIAL) return s;
   if (!N->side_stream) {
     if (cudaStreamCreateWithFlags(&N->side_stream, cudaStreamNonBlocking) != cudaSuccess) return s;
     cudaEventCreateWithFlags(&N->ev_ready, cudaEventDisableTiming);
@@ -444,21 +437,10 @@ static cudaStream_t side_stream(Net* N, cudaStream_t s) {
   return N->side_stream;
 }
 
-// Is the softmax head fused into the forward of the last hidden layer (mpf_train_step)?
-static bool head_fusable(const Net* N) {
-  const int L = N->n_layers - 1;
-  const LayerPlan& P = N->lp[L - 1];
-  return L >= 2 && P.L.kind != MPF_POOL && use_tc(N, P, false) &&
-         tc_head_supported(N->classes, P.cout, P.L.act);
-}
-
-// Forward (Alg. 1 per layer, Alg. 3 for MPF).  With `hf`, the last hidden layer's conv
-// runs with the fused softmax head: it writes dh into the first delta buffer instead of
-// its output, plus per-position losses and per-CTA head partials (*head_grid CTAs).
-static mpf_status forward_impl(Net* N, const float* d_images, int n, float* d_probs, cudaStream_t s,
-                               const TcHeadArgs* hf, int* head_grid) {
-  const bool tf32 = N->cfg.precision == MPF_PREC_TF32;
+// Forward (Alg. 1 per layer, Alg. 3 for MPF) of n images on stream s.
+static mpf_status forward_impl(Net* N, const float* d_images, int n, float* d_probs, cudaStream_t s) {
   float* wpack = scr(N, N->off_wpack);
+  const uint32_t flags = N->cfg.flags;
   // 1. weight packs (tf32-rounded for the tensor-core path), on the side stream: the first
   // layer reads the canonical weights, so the packs overlap with it and its pool
   cudaStream_t sp = side_stream(N, s);
@@ -479,171 +461,87 @@ static mpf_status forward_impl(Net* N, const float* d_images, int n, float* d_pr
                                wpack + P.dpack_off, rf, rd, sp));
   }
   if (sp != s) MPF_CUDA(cudaEventRecord(N->ev_join, sp));
-  // 2. layers (Alg. 1; Alg. 3 for MPF), for images [i0, i0 + n) of the batch on stream s
-  //    (`layer`), either as one chain or as two lanes (split-batch forward, below)
-  const float* images_all = d_images;
-  auto layer = [&](int l, int i0, int n, cudaStream_t s, bool& pool_done, bool& packs_joined,
-                   bool lane_b) -> mpf_status {
+  // 2. layers (Alg. 1; Alg. 3 for MPF)
+  for (int l = 0; l < N->n_layers - 1; ++l) {
     const LayerPlan& P = N->lp[l];
     const Act& in = N->a[l];
     const Act& o = N->a[l + 1];
-    if (pool_done) {
-      pool_done = false;
-      return MPF_OK;
-    }
-    const float* d_images = images_all + (size_t)i0 * N->cfg.in_channels * N->cfg.image_rows * N->cfg.image_cols;
-    // this lane's slice of a[l] (input) and a[l + 1] (output): images are outermost
-    // scratch Y (a conv output consumed by the MPF right after it) is reused layer after
-    // layer while the two lanes are a layer apart, and the layers' sizes differ: lane B's
-    // slice sits at the END of the buffer so the lanes never overlap
-    auto y_slice = [&](long long e_img) -> size_t {
-      return lane_b ? N->y_floats - (size_t)n * e_img : (size_t)i0 * e_img;
-    };
-    auto in_ptr = [&]() {
-      return N->lp[l - 1].out_where == Where::ScratchY ? scr(N, N->off_Y) + y_slice(in.elems_per_image())
-                                                       : act_ptr(N, l) + (size_t)i0 * in.elems_per_image();
-    };
-    auto out_val = [&](int ll) { return tape_val(N, ll) + (size_t)i0 * N->a[ll + 1].elems_per_image(); };
-    auto out_idx = [&](int ll) { return tape_idx(N, ll) + (size_t)i0 * N->a[ll + 1].elems_per_image(); };
-    auto out_y = [&]() { return scr(N, N->off_Y) + y_slice(o.elems_per_image()); };
-    // the consumer of this output rounds? (TF32 operand of a tensor-core conv)
-    // (the tensor-core softmax head counts: it reads h as TF32 MMA operand)
-    const bool first_simt = l == 0 && first_conv_supported(N->cfg.in_channels, P.cout, P.L.k) &&
-                            !getenv("MPF_DISABLE_FIRST");  // reads the canonical weights
+    const bool first_simt = l == 0 && first_conv_supported(N->cfg.in_channels, P.cout, P.L.k);  // canonical weights
     if (!packs_joined && P.L.kind != MPF_POOL && !first_simt) {  // the first consumer of a pack
       MPF_CUDA(cudaStreamWaitEvent(s, N->ev_join, 0));
       packs_joined = true;
     }
-    const bool next_tc = ((l + 1 < N->n_layers - 1) && N->lp[l + 1].L.kind != MPF_POOL && use_tc(N, N->lp[l + 1], false)) ||
-                         (l + 1 == N->n_layers - 1 && head_tc_used(N));
+    // the consumer of this output rounds? (TF32 operand of a tensor-core conv)
+    const bool next_tc = (l + 1 < N->n_layers - 1) && N->lp[l + 1].L.kind != MPF_POOL && use_tc(N, N->lp[l + 1], false);
     if (P.L.kind == MPF_POOL) {
       const Act& y = in;
       MpfArgs m;
-      m.y = in_ptr();
+      m.y = act_ptr(N, l);
       m.gr = y.gr; m.gc = y.gc; m.vr = y.vr; m.vc = y.vc; m.C = y.C; m.k = P.L.k;
       m.n_frag_in = n * y.F;
-      m.out = out_val(l);
-      m.idx = out_idx(l);
+      m.out = tape_val(N, l);
+      m.idx = tape_idx(N, l);
       m.m_r = o.vr; m.m_c = o.vc;
       m.round_tf32 = (l + 1 < N->n_layers - 1 && use_tc(N, N->lp[l + 1], false)) ? 1 : 0;
       const double ein = (double)n * y.F * y.vr * y.vc * y.C, eout = (double)n * o.F * o.vr * o.vc * o.C;
       LAUNCH(N, s, "mpf_fwd", l, 0.0, 4.0 * ein + 5.0 * eout, launch_mpf_fwd(m, s));
+      continue;
+    }
+    float* out = P.out_where == Where::Tape ? tape_val(N, l) : scr(N, N->off_Y);
+    const float* x = (l == 0) ? d_images : act_ptr(N, l);
+    const double pos_out = (double)n * o.F * o.vr * o.vc;
+    const double cflops = 2.0 * pos_out * P.cout * P.L.k * P.L.k * P.cin;
+    const double in_e = (l == 0) ? (double)n * N->cfg.in_channels * N->cfg.image_rows * N->cfg.image_cols
+                                 : (double)n * in.F * in.vr * in.vc * in.C;
+    const double cbytes = 4.0 * (in_e + pos_out * P.cout);
+    if (first_simt) {
+      FirstConvArgs f{};
+      f.img = d_images; f.n = n; f.H = N->cfg.image_rows; f.W = N->cfg.image_cols;
+      f.w = N->params + P.w_off; f.bias = N->params + P.b_off; f.k = P.L.k; f.cout = P.cout;
+      f.out = out; f.out_gr = o.gr; f.out_gc = o.gc; f.out_vr = o.vr; f.out_vc = o.vc;
+      f.act = P.L.act; f.zero_pad = P.out_where == Where::Tape ? 1 : 0; f.round_tf32 = next_tc ? 1 : 0;
+      LAUNCH(N, s, "conv_first_fwd", l, cflops, cbytes, launch_first_conv(f, s));
+    } else if (l > 0 && use_tc(N, P, false)) {
+      TcConvArgs t{};
+      t.x = x; t.n_frag = n * in.F; t.gr = in.gr; t.gc = in.gc; t.cin = P.cin;
+      t.w = wpack + P.wpack_off; t.bias = N->params + P.b_off; t.k = P.L.k; t.cout = P.cout;
+      t.out = out; t.out_vr = o.vr; t.out_vc = o.vc; t.act = P.L.act; t.shift = 0;
+      t.round_out = next_tc ? 1 : 0; t.mul_dact = nullptr;
+      t.zero_pad = P.out_where == Where::Tape ? 1 : 0;  // tape tensors are read whole by the TC wgrad
+      t.flags = flags;
+      LAUNCH(N, s, "conv_fwd_tc", l, cflops, cbytes, launch_conv_tc(t, s));
     } else {
-      float* out = P.out_where == Where::Tape ? out_val(l) : out_y();
-      const float* x = (l == 0) ? d_images : in_ptr();
-      const double pos_out = (double)n * o.F * o.vr * o.vc;
-      const double cflops = 2.0 * pos_out * P.cout * P.L.k * P.L.k * P.cin;
-      const double in_e = (l == 0) ? (double)n * N->cfg.in_channels * N->cfg.image_rows * N->cfg.image_cols
-                                   : (double)n * in.F * in.vr * in.vc * in.C;
-      const double cbytes = 4.0 * (in_e + pos_out * P.cout);
-      if (hf && l == N->n_layers - 2) {  // last hidden layer + fused softmax head
-        TcConvArgs t{};
-        t.x = x; t.n_frag = n * in.F; t.gr = in.gr; t.gc = in.gc; t.cin = P.cin;
-        t.w = wpack + P.wpack_off; t.bias = N->params + P.b_off; t.k = P.L.k; t.cout = P.cout;
-        t.out = scr(N, N->off_dA); t.out_vr = o.vr; t.out_vc = o.vc; t.act = P.L.act; t.shift = 0;
-        t.round_out = 0; t.mul_dact = nullptr; t.head = hf;
-        const double pos = (double)n * o.F * o.vr * o.vc;
-        LAUNCH(N, s, "conv_fwd_head_tc", l, cflops + 6.0 * pos * P.cout * N->classes,
-               4.0 * (in_e + pos * P.cout) + pos, launch_conv_tc(t, s, head_grid));
-      } else if (l == 0 && first_conv_supported(N->cfg.in_channels, P.cout, P.L.k) && !getenv("MPF_DISABLE_FIRST")) {
-        FirstConvArgs f{};
-        f.img = d_images; f.n = n; f.H = N->cfg.image_rows; f.W = N->cfg.image_cols;
-        f.w = N->params + P.w_off; f.bias = N->params + P.b_off; f.k = P.L.k; f.cout = P.cout;
-        f.out = out; f.out_gr = o.gr; f.out_gc = o.gc; f.out_vr = o.vr; f.out_vc = o.vc;
-        f.act = P.L.act; f.zero_pad = P.out_where == Where::Tape ? 1 : 0; f.round_tf32 = next_tc ? 1 : 0;
-        const LayerPlan& Pn = N->lp[1];
-        if (P.out_where == Where::ScratchY && Pn.L.kind == MPF_POOL && !hf && N->n_layers > 2 &&
-            first_conv_mpf_supported(P.cout, P.L.k, Pn.L.k) && !(tf32 && first_conv_tc_ok(N->cfg.in_channels, P.cout, P.L.k))) {
-          // conv + activation + MPF (layer 1) in one kernel: the conv output is never stored
-          const Act& po = N->a[2];
-          MpfArgs m{};
-          m.y = nullptr;
-          m.gr = o.gr; m.gc = o.gc; m.vr = o.vr; m.vc = o.vc; m.C = o.C; m.k = Pn.L.k;
-          m.n_frag_in = n * o.F;
-          m.out = out_val(1);
-          m.idx = out_idx(1);
-          m.m_r = po.vr; m.m_c = po.vc;
-          m.round_tf32 = (2 < N->n_layers - 1 && use_tc(N, N->lp[2], false)) ? 1 : 0;
-          const double eout = (double)n * po.F * po.vr * po.vc * po.C;
-          LAUNCH(N, s, "conv_first_mpf", l, cflops, 4.0 * in_e + 5.0 * eout, launch_first_conv_mpf(f, m, s));
-          pool_done = true;
-        } else if (tf32 && first_conv_tc_ok(N->cfg.in_channels, P.cout, P.L.k))
-          LAUNCH(N, s, "conv_first_fwd", l, cflops, cbytes, launch_first_conv_tc(f, s));
-        else
-          LAUNCH(N, s, "conv_first_fwd", l, cflops, cbytes, launch_first_conv(f, s));
-      } else if (l > 0 && use_tc(N, P, false)) {
-        TcConvArgs t{};
-        t.x = x; t.n_frag = n * in.F; t.gr = in.gr; t.gc = in.gc; t.cin = P.cin;
-        t.w = wpack + P.wpack_off; t.bias = N->params + P.b_off; t.k = P.L.k; t.cout = P.cout;
-        t.out = out; t.out_vr = o.vr; t.out_vc = o.vc; t.act = P.L.act; t.shift = 0;
-        t.round_out = next_tc ? 1 : 0; t.mul_dact = nullptr;
-        t.zero_pad = P.out_where == Where::Tape ? 1 : 0;  // tape tensors are read whole by the TC wgrad
-        LAUNCH(N, s, "conv_fwd_tc", l, cflops, cbytes, launch_conv_tc(t, s));
+      ConvArgs c{};
+      c.in = x;
+      c.in_F = in.F;
+      c.image_mode = l == 0;
+      if (l == 0) {
+        c.in_gr = N->cfg.image_rows; c.in_gc = N->cfg.image_cols;
+        c.in_vr = N->cfg.image_rows; c.in_vc = N->cfg.image_cols;
       } else {
-        ConvArgs c{};
-        c.in = x;
-        c.in_F = in.F;
-        c.image_mode = l == 0;
-        if (l == 0) {
-          c.in_gr = N->cfg.image_rows; c.in_gc = N->cfg.image_cols;
-          c.in_vr = N->cfg.image_rows; c.in_vc = N->cfg.image_cols;
-        } else {
-          c.in_gr = in.gr; c.in_gc = in.gc; c.in_vr = in.vr; c.in_vc = in.vc;
-        }
-        c.off_y = c.off_x = 0;
-        c.cin = P.cin;
-        c.w = wpack + P.wpack_off;
-        c.bias = N->params + P.b_off;
-        c.k = P.L.k;
-        c.cout = P.cout;
-        c.out = out;
-        c.out_gr = o.gr; c.out_gc = o.gc; c.out_vr = o.vr; c.out_vc = o.vc;
-        c.act = P.L.act;
-        c.mul_dact = nullptr;
-        c.dact = 0;
-        c.zero_pad = P.out_where == Where::Tape ? 1 : 0;
-        c.round_tf32 = next_tc ? 1 : 0;
-        c.n_frag_total = n * in.F;
-        LAUNCH(N, s, "conv_fwd_simt", l, cflops, cbytes, launch_conv_simt(c, s));
+        c.in_gr = in.gr; c.in_gc = in.gc; c.in_vr = in.vr; c.in_vc = in.vc;
       }
+      c.off_y = c.off_x = 0;
+      c.cin = P.cin;
+      c.w = wpack + P.wpack_off;
+      c.bias = N->params + P.b_off;
+      c.k = P.L.k;
+      c.cout = P.cout;
+      c.out = out;
+      c.out_gr = o.gr; c.out_gc = o.gc; c.out_vr = o.vr; c.out_vc = o.vc;
+      c.act = P.L.act;
+      c.mul_dact = nullptr;
+      c.dact = 0;
+      c.zero_pad = P.out_where == Where::Tape ? 1 : 0;
+      c.round_tf32 = next_tc ? 1 : 0;
+      c.n_frag_total = n * in.F;
+      LAUNCH(N, s, "conv_fwd_simt", l, cflops, cbytes, launch_conv_simt(c, s));
     }
-    return MPF_OK;
-  };
-  bool pool_done = false;  // the first layer's kernel already produced the MPF after it
-  // Split-batch forward (opt-in MPF_FWD_SPLIT=1): images [0, nA) on s and [nA, n) on the
-  // side stream, the second lane one layer behind (it waits for lane A's layer l), so an
-  // MPF layer of one lane runs beside a tensor-core convolution of the other.  Same kernels
-  // on image slices: the results are those of the one-chain forward.
-  const char* fse = getenv("MPF_FWD_SPLIT");
-  const bool split = fse && atoi(fse) != 0 && n >= 2 && sp != s && !hf;
-  if (!split) {
-    for (int l = 0; l < N->n_layers - 1; ++l) {
-      mpf_status st = layer(l, 0, n, s, pool_done, packs_joined, false);
-      if (st != MPF_OK) return st;
-    }
-  } else {
-    const int nA = (n + 1) / 2, nB = n - nA;
-    bool pool_done_b = false, packs_joined_b = true;  // lane B follows lane A, which joined the packs
-    if (!packs_joined) {
-      MPF_CUDA(cudaStreamWaitEvent(s, N->ev_join, 0));
-      packs_joined = true;
-    }
-    for (int l = 0; l < N->n_layers - 1; ++l) {
-      if (!N->ev_lane[l]) MPF_CUDA(cudaEventCreateWithFlags(&N->ev_lane[l], cudaEventDisableTiming));
-      mpf_status st = layer(l, 0, nA, s, pool_done, packs_joined, false);
-      if (st != MPF_OK) return st;
-      MPF_CUDA(cudaEventRecord(N->ev_lane[l], s));
-      MPF_CUDA(cudaStreamWaitEvent(sp, N->ev_lane[l], 0));
-      st = layer(l, nA, nB, sp, pool_done_b, packs_joined_b, true);
-      if (st != MPF_OK) return st;
-    }
-    MPF_CUDA(cudaEventRecord(N->ev_ready, sp));
-    MPF_CUDA(cudaStreamWaitEvent(s, N->ev_ready, 0));
   }
   if (!packs_joined) MPF_CUDA(cudaStreamWaitEvent(s, N->ev_join, 0));  // the backward reads the packs
   N->images = d_images;
   N->n_fwd = n;
-  N->have_fwd = !hf;  // a fused step has no standalone backward
+  N->have_fwd = true;
   // 3. optional softmax output
   if (d_probs) {
     const int L = N->n_layers - 1;
@@ -671,7 +569,7 @@ mpf_status mpf_forward_image(mpf_net* N, const float* d_images, int32_t n, float
   if (!N || !d_images) return fail(MPF_ERR_ARG, "NULL argument");
   if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound (mpf_net_bind)");
   if (n < 1 || n > N->n_cap) return fail(MPF_ERR_DATA, "n must be in [1, bound n_images]");
-  return forward_impl(N, d_images, n, d_probs, (cudaStream_t)stream, nullptr, nullptr);
+  return forward_impl(N, d_images, n, d_probs, (cudaStream_t)stream);
 }
 
 static mpf_status wgrad(Net* N, int l, const float* x, const float* dy, int n, cudaStream_t s) {
@@ -685,7 +583,7 @@ static mpf_status wgrad(Net* N, int l, const float* x, const float* dy, int n, c
   const double in_e = (l == 0) ? (double)n * N->cfg.in_channels * N->cfg.image_rows * N->cfg.image_cols
                                : (double)n * in.F * in.vr * in.vc * in.C;
   const double wbytes = 4.0 * (in_e + (double)positions * P.cout);
-  if (l == 0 && first_conv_supported(N->cfg.in_channels, P.cout, P.L.k) && !getenv("MPF_DISABLE_FIRST")) {
+  if (l == 0 && first_conv_supported(N->cfg.in_channels, P.cout, P.L.k)) {
     FirstWgradArgs f{};
     f.img = x; f.n = n; f.H = N->cfg.image_rows; f.W = N->cfg.image_cols;
     f.dy = dy; f.gr = o.gr; f.gc = o.gc; f.k = P.L.k; f.cout = P.cout;
@@ -702,6 +600,7 @@ static mpf_status wgrad(Net* N, int l, const float* x, const float* dy, int n, c
     t.cin = P.cin; t.cout = P.cout; t.k = P.L.k;
     t.part = part;
     t.part_cap_floats = N->part_floats;
+    t.flags = N->cfg.flags;
     int splits = 0;
     LAUNCH(N, s, "wgrad_tc", l, wflops, wbytes, launch_wgrad_tc(t, &splits, s));
     const long long K = (long long)P.L.k * P.L.k * P.cin;
@@ -741,18 +640,17 @@ static mpf_status bias_reduce(Net* N, int l, const float* part, long long nb, cu
   return MPF_OK;
 }
 
-// Backward.  head_grid > 0: the fused forward already produced dh (first delta buffer),
-// the per-position losses and head_grid CTA partials of (dW_L, db_L, db_{L-1}).
+// Backward (loss first, then Alg. 4 / Alg. 2 layer by layer).  loss_only: the head's loss
+// only (Armijo trial points), no gradients.
 static mpf_status backward_impl(Net* N, const uint8_t* d_labels, const float* h_class_w, float* d_loss,
-                                cudaStream_t s, int head_grid, bool loss_only = false) {
+                                cudaStream_t s, bool loss_only = false) {
   const int n = N->n_fwd;
   const bool tf32 = N->cfg.precision == MPF_PREC_TF32;
   const int L = N->n_layers - 1;  // the softmax FC
   int* nlab = (int*)(N->scratch + N->off_nlab);
   float* lossp = scr(N, N->off_lossp);
   float* bpart = scr(N, N->off_bpart);
-  if (head_grid == 0)
-    LAUNCH(N, s, "label_count", -1, 0.0, (double)n * N->O_H * N->O_W,
+  LAUNCH(N, s, "label_count", -1, 0.0, (double)n * N->O_H * N->O_W,
            launch_label_count(d_labels, n, N->O_H * N->O_W, N->classes, nlab, s));
   // head: dL/dx_hat first, dh, and the softmax FC's gradient + the
   // previous layer's bias gradient as block partials
@@ -803,28 +701,14 @@ static mpf_status backward_impl(Net* N, const uint8_t* d_labels, const float* h_
   hd.err = (int*)(N->scratch + N->off_err);
   hd.n = n;
   hd.round_tf32 = tf32 ? 1 : 0;
-  if (head_grid > 0) {  // fused: partials from the conv epilogue, losses per position
-    const int E = N->classes * h.C + N->classes + h.C;
-    LAUNCH(N, s, "head_reduce", L, 0.0, 4.0 * (double)head_grid * E,
-           launch_partial_reduce(bpart, head_grid, E, N->grads + N->lp[L].w_off, N->grads + N->lp[L - 1].b_off,
-                                 N->classes * h.C + N->classes, s));
-    if (d_loss)
-      LAUNCH(N, s, "loss_rows", L, 0.0, 4.0 * (double)n * h.F * h.gr * h.gc,
-             launch_loss_rows(scr(N, N->off_rowloss), (long long)h.F * h.gr * h.gc, nlab, n, d_loss, s));
-  } else {
+  {
     const double pos = (double)n * h.F * h.vr * h.vc;
-    if (head_tc_used(N)) {
-      hd.n_blocks = head_tc_grid((long long)h.F * h.gr * h.gc, n);
-      LAUNCH(N, s, "head_loss_delta", L, 6.0 * pos * h.C * N->classes, pos * (8.0 * h.C + 1.0),
-             launch_head_tc(hd, s));
-    } else {
-      uint8_t* labf = (uint8_t*)(N->scratch + N->off_labfrag);
-      LAUNCH(N, s, "label_frag", L, 0.0, (double)n * h.F * h.gr * h.gc + (double)n * N->O_H * N->O_W,
-             launch_label_frag(hd, labf, s));
-      hd.lab_frag = labf;
-      LAUNCH(N, s, "head_loss_delta", L, 6.0 * pos * h.C * N->classes, pos * (8.0 * h.C + 1.0),
-             launch_head2(hd, s));
-    }
+    uint8_t* labf = (uint8_t*)(N->scratch + N->off_labfrag);
+    LAUNCH(N, s, "label_frag", L, 0.0, (double)n * h.F * h.gr * h.gc + (double)n * N->O_H * N->O_W,
+           launch_label_frag(hd, labf, s));
+    hd.lab_frag = labf;
+    LAUNCH(N, s, "head_loss_delta", L, 6.0 * pos * h.C * N->classes, pos * (8.0 * h.C + 1.0),
+           launch_head2(hd, s));
     const int E = N->classes * h.C + N->classes + h.C;
     if (loss_only) {  // forward-only loss evaluation (Armijo trial points): no gradients
       if (d_loss)
@@ -914,6 +798,7 @@ static mpf_status backward_impl(Net* N, const uint8_t* d_labels, const float* h_
       t.zero_pad = 1;
       t.mul_dact = md;
       t.dact = mdact;
+      t.flags = N->cfg.flags;
       LAUNCH(N, s, "dgrad_tc", l, dflops, dbytes, launch_conv_tc(t, s));
     } else {
       ConvArgs c{};
@@ -953,7 +838,7 @@ mpf_status mpf_backward_image(mpf_net* N, const uint8_t* d_labels, const float* 
   if (!N || !d_labels) return fail(MPF_ERR_ARG, "NULL argument");
   if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound");
   if (!N->have_fwd) return fail(MPF_ERR_STATE, "mpf_backward_image before mpf_forward_image");
-  return backward_impl(N, d_labels, h_class_w, d_loss, (cudaStream_t)stream, 0);
+  return backward_impl(N, d_labels, h_class_w, d_loss, (cudaStream_t)stream);
 }
 
 mpf_status mpf_train_step(mpf_net* N, const float* d_images, int32_t n, const uint8_t* d_labels,
@@ -962,41 +847,9 @@ mpf_status mpf_train_step(mpf_net* N, const float* d_images, int32_t n, const ui
   if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound (mpf_net_bind)");
   if (n < 1 || n > N->n_cap) return fail(MPF_ERR_DATA, "n must be in [1, bound n_images]");
   cudaStream_t s = (cudaStream_t)stream;
-  // The fused head is opt-in (MPF_HEAD_FUSION=1): measured slower than the separate head
-  // pass on cfg4/cfg5 (11.5 ms vs 4.7 + 4.4 ms; the per-row head work makes the conv
-  // epilogue the bottleneck), so the default is forward + backward.
-  const char* hfe = getenv("MPF_HEAD_FUSION");
-  if (!head_fusable(N) || !(hfe && atoi(hfe) != 0)) {  // unfused: plain forward + backward
-    mpf_status st = forward_impl(N, d_images, n, nullptr, s, nullptr, nullptr);
-    if (st != MPF_OK) return st;
-    return backward_impl(N, d_labels, h_class_w, d_loss, s, 0);
-  }
-  int* nlab = (int*)(N->scratch + N->off_nlab);
-  LAUNCH(N, s, "label_count", -1, 0.0, (double)n * N->O_H * N->O_W,
-         launch_label_count(d_labels, n, N->O_H * N->O_W, N->classes, nlab, s));
-  const int L = N->n_layers - 1;
-  TcHeadArgs hf{};
-  hf.wL = N->params + N->lp[L].w_off;
-  hf.bL = N->params + N->lp[L].b_off;
-  hf.C = N->classes;
-  hf.labels = d_labels;
-  hf.O_H = N->O_H; hf.O_W = N->O_W;
-  hf.F = N->a[L].F;
-  hf.n_levels = N->n_levels;
-  for (int i = 0; i < N->n_levels; ++i) hf.pool_k[i] = N->pool_k[i];
-  hf.nlab = nlab;
-  for (int c = 0; c < 16; ++c) hf.cw[c] = (h_class_w && c < N->classes) ? h_class_w[c] : 1.f;
-  hf.row_loss = scr(N, N->off_rowloss);
-  hf.part = scr(N, N->off_bpart);
-  hf.err = (int*)(N->scratch + N->off_err);
-  hf.round_dh = N->cfg.precision == MPF_PREC_TF32 ? 1 : 0;
-  int grid = 0;
-  mpf_status st = forward_impl(N, d_images, n, nullptr, s, &hf, &grid);
+  mpf_status st = forward_impl(N, d_images, n, nullptr, s);
   if (st != MPF_OK) return st;
-  if (grid <= 0) return fail(MPF_ERR_INTERNAL, "fused head launch reported no CTAs");
-  st = backward_impl(N, d_labels, h_class_w, d_loss, s, grid);
-  N->have_fwd = false;  // the tape is consumed (the last hidden layer's output was never stored)
-  return st;
+  return backward_impl(N, d_labels, h_class_w, d_loss, s);
 }
 
 // Armijo-safeguarded gradient step ("stochastic gradient descent safe-guarded
@@ -1027,7 +880,9 @@ mpf_status mpf_armijo_step(mpf_net* N, const float* d_images, int32_t n, const u
     *L = t * grad_scale;
     return MPF_OK;
   };
-  // 1. loss and gradient at theta
+  // 1. loss and gradient at theta (the buffer is zeroed first: leftovers, e.g. the last
+  // trial's gradient of mpf_lbfgs_step, must not enter g)
+  MPF_CUDA(cudaMemsetAsync(N->grads, 0, sizeof(float) * N->n_params, s));
   mpf_status st = mpf_train_step(N, d_images, n, d_labels, h_class_w, d_loss, stream);
   if (st != MPF_OK) return st;
   double L0 = 0.0, g2 = 0.0;
@@ -1049,9 +904,9 @@ mpf_status mpf_armijo_step(mpf_net* N, const float* d_images, int32_t n, const u
   bool accepted = false;
   for (int it = 0; it <= max_backtracks; ++it, alpha *= beta) {
     MPF_CUDA(launch_armijo_axpy(N->params, theta0, N->grads, N->n_params, (float)(alpha * grad_scale), s));
-    st = forward_impl(N, d_images, n, nullptr, s, nullptr, nullptr);
+    st = forward_impl(N, d_images, n, nullptr, s);
     if (st != MPF_OK) return st;
-    st = backward_impl(N, d_labels, h_class_w, d_loss, s, 0, true);
+    st = backward_impl(N, d_labels, h_class_w, d_loss, s, true);
     if (st != MPF_OK) return st;
     st = total_loss(&L);
     if (st != MPF_OK) return st;
@@ -1098,7 +953,8 @@ struct mpf_lbfgs {
   std::vector<int> order;       // stored pairs' slots, oldest first
   std::vector<double> sy, yy;   // per slot
   bool have_g = false, have_dir = false;
-  double L = 0.0;               // mpf_lbfgs_step: loss at the current point (valid with have_g)
+  bool have_L = false;          // L is the loss at the point of g (set only by mpf_lbfgs_step)
+  double L = 0.0;               // mpf_lbfgs_step: loss at the current point (valid with have_L)
   std::vector<double> hpart;
 };
 
@@ -1159,7 +1015,7 @@ void mpf_lbfgs_destroy(mpf_lbfgs* lb) { delete lb; }  // the state buffer belong
 mpf_status mpf_lbfgs_reset(mpf_lbfgs* lb) {
   if (!lb) return fail(MPF_ERR_ARG, "NULL L-BFGS state");
   lb->order.clear();
-  lb->have_g = lb->have_dir = false;
+  lb->have_g = lb->have_dir = lb->have_L = false;
   return MPF_OK;
 }
 
@@ -1168,6 +1024,7 @@ mpf_status mpf_lbfgs_set_gradient(mpf_lbfgs* lb, float grad_scale, void* stream)
   MPF_CUDA(launch_lbfgs_gset(lb->g, lb->N->grads, lb->n, grad_scale, (cudaStream_t)stream));
   lb->have_g = true;
   lb->have_dir = false;
+  lb->have_L = false;  // a caller-supplied gradient: its loss is not known here
   return MPF_OK;
 }
 
@@ -1294,11 +1151,14 @@ mpf_status mpf_lbfgs_step(mpf_lbfgs* lb, const float* d_images, int32_t n, const
     return MPF_OK;
   };
   mpf_status st;
-  if (!lb->have_g) {
-    st = evaluate(&lb->L);
+  if (!lb->have_g || !lb->have_L) {  // first call, after a reset or after a caller-supplied gradient
+    double L0 = 0.0;
+    st = evaluate(&L0);
     if (st != MPF_OK) return st;
     st = mpf_lbfgs_set_gradient(lb, grad_scale, stream);
     if (st != MPF_OK) return st;
+    lb->L = L0;
+    lb->have_L = true;
   }
   const double L0 = lb->L;
   double gtd = 0.0;
@@ -1306,7 +1166,7 @@ mpf_status mpf_lbfgs_step(mpf_lbfgs* lb, const float* d_images, int32_t n, const
   st = mpf_lbfgs_direction(lb, &gtd, &fb, stream);
   if (st != MPF_OK) return st;
   if (!std::isfinite(L0) || !std::isfinite(gtd)) {
-    lb->have_g = lb->have_dir = false;
+    lb->have_g = lb->have_dir = lb->have_L = false;
     return fail(MPF_ERR_DATA, "L-BFGS: non-finite loss or direction");
   }
   double alpha = lb->order.empty() ? (double)alpha0 : 1.0, L = L0;
@@ -1465,11 +1325,14 @@ mpf_status mpf_debug_tape(const mpf_net* N, int32_t layer, int32_t what, void* d
   return MPF_OK;
 }
 
-mpf_status mpf_debug_scratch(const mpf_net* N, int32_t which, void* d_dst, uint64_t bytes, void* stream) {
-  if (!N || !d_dst || !N->bound) return fail(MPF_ERR_ARG, "NULL argument or unbound net");
-  const size_t off = which == 0 ? N->off_rowloss : (which == 1 ? N->off_dA : N->off_bpart);
-  if (off + bytes > N->scratch_bytes) return fail(MPF_ERR_ARG, "range outside the scratch buffer");
-  MPF_CUDA(cudaMemcpyAsync(d_dst, N->scratch + off, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+mpf_status mpf_net_set_flags(mpf_net* N, uint32_t flags) {
+  if (!N) return fail(MPF_ERR_ARG, "NULL net");
+  const uint32_t known = MPF_FLAG_SERIAL | MPF_FLAG_TC_SINGLE | MPF_FLAG_TC_PAIR | MPF_FLAG_NTAP_ON | MPF_FLAG_NTAP_OFF |
+                         MPF_FLAG_NTAP_NO_MC | MPF_FLAG_WGRAD_M128 | MPF_FLAG_ROLE_TIMERS;
+  if (flags & ~known) return fail(MPF_ERR_ARG, "unknown MPF_FLAG_* bits");
+  if ((flags & MPF_FLAG_NTAP_ON) && (flags & MPF_FLAG_NTAP_OFF)) return fail(MPF_ERR_ARG, "NTAP_ON with NTAP_OFF");
+  if ((flags & MPF_FLAG_TC_PAIR) && (flags & MPF_FLAG_TC_SINGLE)) return fail(MPF_ERR_ARG, "TC_PAIR with TC_SINGLE");
+  N->cfg.flags = flags;
   return MPF_OK;
 }
 

@@ -67,7 +67,7 @@ struct Net {
   size_t tape_bytes = 0, scratch_bytes = 0;
   size_t y_floats = 0;  // scratch Y capacity (floats)
   size_t off_Y = 0, off_dA = 0, off_dB = 0, off_dC = 0, off_bpart = 0, off_wpack = 0, off_part = 0,
-         off_nlab = 0, off_lossp = 0, off_err = 0, off_rowloss = 0, off_stage_img = 0, off_stage_lab = 0,
+         off_nlab = 0, off_lossp = 0, off_err = 0, off_stage_img = 0, off_stage_lab = 0,
          off_stage_loss = 0, off_theta0 = 0, off_armijo = 0, off_labfrag = 0;
   size_t stage_bytes = 0;  // one of the two host-input staging slots (images | labels)
   // host-buffer steps: inputs of step i + 1 are copied on copy_stream into the other
@@ -76,7 +76,6 @@ struct Net {
   // backward: weight gradients run on side_stream, overlapping the dgrad / MPF-backward chain
   cudaStream_t side_stream = nullptr;
   cudaEvent_t ev_ready = nullptr, ev_join = nullptr, ev_buf[3] = {nullptr, nullptr, nullptr};
-  cudaEvent_t ev_lane[kMaxL] = {};  // split-batch forward: lane A finished layer l
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   int stage_slot = 0;
   size_t part_floats = 0;  // capacity of the wgrad partial buffer (floats)
@@ -152,8 +151,6 @@ struct MpfArgs {
   int round_tf32;
 };
 cudaError_t launch_mpf_fwd(const MpfArgs& a, cudaStream_t s);
-struct FirstConvArgs;
-cudaError_t launch_first_conv_mpf(const FirstConvArgs& a, const MpfArgs& m, cudaStream_t s);
 
 struct MpfBwdArgs {
   const float* dout;     // delta of the pooled output [n*F_in*k*k][m][m][C]
@@ -209,11 +206,6 @@ int head_loss_parts_per_tile();
 int head_blocks(long long total_tiles);
 bool head_supported(int C, int Ch);
 cudaError_t launch_head2(const HeadArgs& a, cudaStream_t s);
-// tensor-core training head (head_tc.cu): eligibility, its grid (= partial rows), launch
-bool head_tc_ok(int C, int Ch, bool train, bool tf32);
-int head_tc_grid(long long per_img, int n);
-cudaError_t launch_head_tc(const HeadArgs& a, cudaStream_t s);
-
 cudaError_t launch_label_count(const uint8_t* labels, int n, int hw, int classes, int* nlab, cudaStream_t s);
 cudaError_t launch_sqnorm(const float* g, long long n, double* part, int nb, double* out, cudaStream_t s);
 cudaError_t launch_armijo_axpy(float* theta, const float* theta0, const float* g, long long n, float step,
@@ -231,9 +223,6 @@ cudaError_t launch_class_hist(const uint8_t* labels, long long total, int classe
                               cudaStream_t s);
 cudaError_t launch_loss_finalize(const float* loss_part, int parts, const int* nlab, int n, float* loss,
                                  cudaStream_t s);
-// per-image loss = sum of per-position losses (fixed order) / n_lab (fused head)
-cudaError_t launch_loss_rows(const float* row_loss, long long per_img, const int* nlab, int n, float* loss,
-                             cudaStream_t s);
 cudaError_t launch_sgd(float* params, float* grads, long long n, float lr, float scale, cudaStream_t s);
 cudaError_t launch_pack_weights(const float* w_canon, int cout, int cin, int k, float* wpack, float* dpack,
                                 int round_fwd, int round_dgrad, cudaStream_t s);
@@ -254,9 +243,6 @@ struct FirstConvArgs {
   int act, zero_pad, round_tf32;
   int n_cog;             // set by the launcher
 };
-// tensor-core first layer forward (conv_first_tc.cu), 3xTF32
-bool first_conv_tc_ok(int cin, int cout, int k);
-cudaError_t launch_first_conv_tc(const FirstConvArgs& a, cudaStream_t s);
 struct FirstWgradArgs {
   const float* img;
   int n, H, W;
@@ -268,8 +254,6 @@ struct FirstWgradArgs {
   int n_cog;             // set by the launcher
 };
 bool first_conv_supported(int cin, int cout, int k);
-// first conv + activation + the MPF layer after it in one kernel (conv output never stored)
-bool first_conv_mpf_supported(int cout, int k, int pool_k);
 int first_wgrad_blocks(int k);  // k = 0: the largest grid (partial-buffer sizing)
 cudaError_t launch_first_conv(FirstConvArgs a, cudaStream_t s);
 cudaError_t launch_first_wgrad(FirstWgradArgs a, cudaStream_t s);

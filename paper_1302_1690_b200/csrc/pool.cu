@@ -26,18 +26,12 @@
 #include <stdlib.h>
 
 #include "mpf_internal.h"
+#include "numerics.cuh"
 
 namespace mpf {
 
 namespace {
 
-// TF32 rounding (nearest-even, finite-saturating: one F2FP instruction on sm_100a; the guarded
-// cvt.rna form takes four) of an MMA operand
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rn.satfinite.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
 
 __device__ __forceinline__ float act_der(int act, float y) {
   if (act == MPF_TANH) return 1.f - y * y;
@@ -157,7 +151,7 @@ __global__ void __launch_bounds__(256, K <= 3 ? 4 : 2) mpf_fwd_kernel(MpfArgs a)
       const size_t o = (((frag_base + r * K + c) * a.m_r + i) * a.m_c + j) * C + cv * V;
       if (a.round_tf32) {
 #pragma unroll
-        for (int v = 0; v < V; ++v) best[v] = tf32_rna(best[v]);
+        for (int v = 0; v < V; ++v) best[v] = tf32_rn(best[v]);
       }
       stv<V>(a.out + o, best);
       stidx<V>(a.idx + o, arg);
@@ -209,7 +203,7 @@ __global__ void __launch_bounds__(256) mpf_fwd_generic_kernel(MpfArgs a) {
       const size_t o = ((((size_t)g * K * K + r * K + c) * a.m_r + i) * a.m_c + j) * a.C + cv * V;
       if (a.round_tf32) {
 #pragma unroll
-        for (int v = 0; v < V; ++v) best[v] = tf32_rna(best[v]);
+        for (int v = 0; v < V; ++v) best[v] = tf32_rn(best[v]);
       }
       stv<V>(a.out + o, best);
       stidx<V>(a.idx + o, arg);
@@ -290,7 +284,7 @@ __global__ void __launch_bounds__(256) mpf_bwd_kernel(MpfBwdArgs a) {
         for (int v = 0; v < V; ++v) {
           const float dv = hit[v] ? (a.premul ? acc[v] : acc[v] * act_der(a.act, val[v])) : 0.f;
           bsum[v] += dv;
-          o[v] = a.round_tf32 ? tf32_rna(dv) : dv;
+          o[v] = a.round_tf32 ? tf32_rn(dv) : dv;
         }
         stv<V>(a.din + (((size_t)g * a.gr + Y) * a.gc + X) * C + cv * V, o);
       }
@@ -308,128 +302,6 @@ __global__ void __launch_bounds__(256) mpf_bwd_kernel(MpfBwdArgs a) {
       float t = 0.f;
       for (int q = 0; q < (int)blockDim.y; ++q) t += s_red[q * C + cv * V + v];
       a.bias_part[blin * C + cv * V + v] = t;
-    }
-  }
-}
-
-// Sliding-window gather for K in {2,3,4} and 4-channel vectors: a thread keeps the
-// argmax bytes of the K window rows that can select its current row (K x K uchar4 in
-// registers), loads one new window row per output row, and fetches delta + pooled
-// value only for matching windows with predicated loads (no branches between the
-// independent loads).
-__device__ __forceinline__ float4 ldg4_pred(const float* p, bool pred) {
-  float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
-      "@q ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];\n\t}"
-      : "+f"(r.x), "+f"(r.y), "+f"(r.z), "+f"(r.w)
-      : "l"(p), "r"((int)pred));
-  return r;
-}
-__device__ __forceinline__ uint32_t ldg_u32_pred(const uint8_t* p, bool pred) {
-  uint32_t r = 0xFFFFFFFFu;  // matches no window index (indices < K^2 <= 16)
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
-      "@q ld.global.nc.u32 %0, [%1];\n\t}"
-      : "+r"(r)
-      : "l"(p), "r"((int)pred));
-  return r;
-}
-
-constexpr int kBandB = 32;  // output rows per thread (backward, sliding)
-
-template <int K>
-__global__ void __launch_bounds__(256) mpf_bwd_slide_kernel(MpfBwdArgs a) {
-  extern __shared__ float s_red[];  // [blockDim.y][C]
-  const int cv = threadIdx.x;
-  const int X = blockIdx.x * blockDim.y + threadIdx.y;
-  const int Xw = K * a.m_c, Yw = K * a.m_r;
-  const int y0 = blockIdx.y * kBandB, y1 = min(y0 + kBandB, a.gr);
-  const int C = a.C;
-  const int MM = a.m_r * a.m_c;  // cells per output fragment
-  float bsum[4] = {0.f, 0.f, 0.f, 0.f};
-  if (X < a.gc) {
-    // column part of the cell index for each dx (window column wx = X - dx)
-    int colpart[K];
-    bool cval[K];
-#pragma unroll
-    for (int dx = 0; dx < K; ++dx) {
-      const int wx = X - dx;
-      cval[dx] = wx >= 0 && wx < Xw;
-      colpart[dx] = cval[dx] ? (wx % K) * MM + wx / K : 0;
-    }
-    for (int g = blockIdx.z; g < a.n_frag_in; g += gridDim.z) {
-      const size_t fbase = (size_t)g * K * K * MM;  // first cell of the input fragment's k^2 outputs
-      auto rowpart = [&](int wy) { return (wy % K) * K * MM + (wy / K) * a.m_c; };
-      auto load_row = [&](int wy, uint32_t (&idr)[K]) {
-        const bool rv = wy >= 0 && wy < Yw;
-        const int rp = rv ? rowpart(wy) : 0;
-#pragma unroll
-        for (int dx = 0; dx < K; ++dx)
-          idr[dx] = ldg_u32_pred(a.idx + (fbase + rp + colpart[dx]) * C + cv * 4, rv && cval[dx]);
-      };
-      uint32_t id[K][K];  // id[dy][dx]: window row Y - dy
-#pragma unroll
-      for (int dy = 0; dy < K; ++dy) load_row(y0 - dy, id[dy]);
-      for (int Y = y0; Y < y1; ++Y) {
-        // prefetch the argmax row of the next output row while this row's deltas load
-        uint32_t nxt[K];
-        load_row(Y + 1, nxt);
-        float acc[4] = {0.f, 0.f, 0.f, 0.f}, val[4] = {0.f, 0.f, 0.f, 0.f};
-        bool hit[4] = {false, false, false, false};
-#pragma unroll
-        for (int dy = 0; dy < K; ++dy) {
-          const int wy = Y - dy;
-          const int rp = (wy >= 0) ? rowpart(wy) : 0;
-#pragma unroll
-          for (int dx = 0; dx < K; ++dx) {
-            const uint32_t want = (uint32_t)(dy * K + dx);
-            const uint32_t w = id[dy][dx];
-            bool m[4];
-            bool any = false;
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              m[v] = ((w >> (8 * v)) & 0xFFu) == want;
-              any |= m[v];
-            }
-            const size_t cell = (fbase + rp + colpart[dx]) * C + cv * 4;
-            const float4 d = ldg4_pred(a.dout + cell, any);
-            // premul: the delta already carries act'(y) (applied by the producing dgrad)
-            const float4 pv = ldg4_pred(a.pooled + cell, any && !a.premul);
-            const float dd[4] = {d.x, d.y, d.z, d.w}, pp[4] = {pv.x, pv.y, pv.z, pv.w};
-#pragma unroll
-            for (int v = 0; v < 4; ++v)
-              if (m[v]) { acc[v] += dd[v]; val[v] = pp[v]; hit[v] = true; }
-          }
-        }
-        float o[4];
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const float dv = hit[v] ? (a.premul ? acc[v] : acc[v] * act_der(a.act, val[v])) : 0.f;
-          bsum[v] += dv;
-          o[v] = a.round_tf32 ? tf32_rna(dv) : dv;
-        }
-        stv<4>(a.din + (((size_t)g * a.gr + Y) * a.gc + X) * C + cv * 4, o);
-#pragma unroll
-        for (int dy = K - 1; dy > 0; --dy)
-#pragma unroll
-          for (int dx = 0; dx < K; ++dx) id[dy][dx] = id[dy - 1][dx];
-#pragma unroll
-        for (int dx = 0; dx < K; ++dx) id[0][dx] = nxt[dx];
-      }
-    }
-  }
-  if (a.bias_part == nullptr) return;
-#pragma unroll
-  for (int v = 0; v < 4; ++v) s_red[threadIdx.y * C + cv * 4 + v] = bsum[v];
-  __syncthreads();
-  if (threadIdx.y == 0) {
-    const size_t blin = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      float t = 0.f;
-      for (int q = 0; q < (int)blockDim.y; ++q) t += s_red[q * C + cv * 4 + v];
-      a.bias_part[blin * C + cv * 4 + v] = t;
     }
   }
 }
@@ -576,7 +448,7 @@ __global__ void __launch_bounds__(256) mpf_bwd_tile_kernel(MpfBwdArgs a, int row
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
           bsum[v] += acc[v];
-          o[v] = a.round_tf32 ? tf32_rna(acc[v]) : acc[v];
+          o[v] = a.round_tf32 ? tf32_rn(acc[v]) : acc[v];
         }
         stv<4>(dst_g + (Y * a.gc + X) * C, o);
       }
@@ -685,7 +557,7 @@ __global__ void __launch_bounds__(256, 3) mpf_bwd_block2_kernel(MpfBwdArgs a, lo
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             bsum[q] += acc[q];
-            o[q] = a.round_tf32 ? tf32_rna(acc[q]) : acc[q];
+            o[q] = a.round_tf32 ? tf32_rn(acc[q]) : acc[q];
           }
           stv<4>(dst + (Y * a.gc + X) * C, o);
         }
@@ -774,7 +646,7 @@ __global__ void __launch_bounds__(256) mpf_bwd_block3_kernel(MpfBwdArgs a, long 
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             bsum[q] += acc[q];
-            o[q] = a.round_tf32 ? tf32_rna(acc[q]) : acc[q];
+            o[q] = a.round_tf32 ? tf32_rn(acc[q]) : acc[q];
           }
           stv<4>(dst + (Y * a.gc + X) * C, o);
         }
@@ -847,18 +719,13 @@ cudaError_t launch_mpf_fwd(const MpfArgs& a, cudaStream_t s) {
   return fwd_dispatch<1>(a, s);
 }
 
-// k = 2, 3 register-blocked gathers (default; MPF_BWD_TILE2=1 keeps the tiled kernel)
+// k = 2, 3: register-blocked gathers
 static bool bwd_block2(const MpfBwdArgs& a) {
-  return a.premul && (a.k == 2 || a.k == 3) && a.C % 4 == 0 && a.C <= 1024 && !getenv("MPF_BWD_SLIDE") &&
-         !getenv("MPF_BWD_TILE2");
-}
-static int block3_bw() {
-  static const int bw = getenv("MPF_BWD_BW3") ? atoi(getenv("MPF_BWD_BW3")) : 3;
-  return bw == 1 ? 1 : 3;
+  return a.premul && (a.k == 2 || a.k == 3) && a.C % 4 == 0 && a.C <= 1024;
 }
 static long long block2_groups(const MpfBwdArgs& a) {
   const int nsub = 256 / (a.C / 4);
-  const int bw = a.k == 2 ? 2 : block3_bw();
+  const int bw = a.k == 2 ? 2 : 3;
   const long long bj_n = (a.gc + bw - 1) / bw, bi_n = (a.gr + a.k - 1) / a.k;
   return (long long)a.n_frag_in * bi_n * ((bj_n + nsub - 1) / nsub);
 }
@@ -867,22 +734,16 @@ static int block2_grid(const MpfBwdArgs& a) {
   const long long cap = 148LL * 8;  // 8 CTAs of 256 threads per SM
   return (int)(g < cap ? (g < 1 ? 1 : g) : cap);
 }
+// k = 4 (and k = 2, 3 with C > 1024): the shared-memory tiled gather
 static bool bwd_tile(const MpfBwdArgs& a) {
-  return a.premul && a.C % 4 == 0 && a.C <= 1024 && a.k >= 2 && a.k <= 4 && !getenv("MPF_BWD_SLIDE");
+  return a.premul && a.C % 4 == 0 && a.C <= 1024 && a.k >= 2 && a.k <= 4;
 }
-static bool bwd_slide(const MpfBwdArgs& a) { return a.C % 4 == 0 && a.k >= 2 && a.k <= 4; }
 constexpr int kTileRows = 64;  // conv-output rows per CTA of the tiled kernel (partials per CTA)
 
-// tile shape (rows x cols of conv-output positions per CTA step); MPF_BWD_TILE=RxC overrides
-static int tile_nbuf() {
-  static const int nb = getenv("MPF_BWD_NBUF") ? (atoi(getenv("MPF_BWD_NBUF")) == 2 ? 2 : 1) : 1;
-  return nb;
-}
-// staging budget per CTA: two buffers at 2 CTAs per SM by default; MPF_BWD_SMEM_KB overrides
-static size_t tile_budget() {
-  static const size_t kb = getenv("MPF_BWD_SMEM_KB") ? (size_t)atoi(getenv("MPF_BWD_SMEM_KB")) : 56 * tile_nbuf();
-  return kb * 1024;
-}
+// tile shape (rows x cols of conv-output positions per CTA step); one staging buffer
+static int tile_nbuf() { return 1; }
+// staging budget per CTA (4 CTAs per SM)
+static size_t tile_budget() { return 56 * 1024; }
 static size_t tile_bytes(int C, int k, int ty, int tx) {
   const int CV = C / 4, CVP = (CV + 3) & ~3, S = tile_cells_padded(ty + k - 1, tx + k - 1);
   return tile_nbuf() * ((size_t)CVP * S * 4 + (size_t)CV * S * 16) + sizeof(float) * (256 / CV) * C;
@@ -900,10 +761,6 @@ static void tile_shape(const MpfBwdArgs& a, int* ty, int* tx) {
       *tx = cand[i][1];
       break;
     }
-  if (const char* e = getenv("MPF_BWD_TILE")) {
-    int r = 8, c = 8;
-    if (sscanf(e, "%dx%d", &r, &c) == 2 && (r == 8 || r == 16) && (c == 8 || c == 16)) { *ty = r; *tx = c; }
-  }
 }
 
 static size_t tile_smem(const MpfBwdArgs& a) {
@@ -941,7 +798,7 @@ static void bwd_geometry(const MpfBwdArgs& a, int V, dim3* grid, dim3* blk) {
     return;
   }
   const int ty = block_dims(a.C, V, blk);
-  const int band = bwd_slide(a) ? kBandB : kBand;
+  const int band = kBand;
   *grid = dim3((a.gc + ty - 1) / ty, (a.gr + band - 1) / band, a.n_frag_in < 65535 ? a.n_frag_in : 65535);
 }
 
@@ -956,8 +813,7 @@ cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s) {
   if (bwd_block2(a)) {
     const size_t smem = 0;
     if (a.k == 2) mpf_bwd_block2_kernel<<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
-    else if (block3_bw() == 3) mpf_bwd_block3_kernel<3, 3><<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
-    else mpf_bwd_block3_kernel<3, 1><<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
+    else mpf_bwd_block3_kernel<3, 3><<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
     return cudaGetLastError();
   }
   const int V = a.C % 4 == 0 ? 4 : 1;
@@ -970,11 +826,7 @@ cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s) {
     return launch_tile_k<4>(a, grid, blk, sm, s);
   }
   const size_t smem = sizeof(float) * blk.y * a.C;
-  if (bwd_slide(a) && !getenv("MPF_BWD_GENERIC")) {
-    if (a.k == 2) mpf_bwd_slide_kernel<2><<<grid, blk, smem, s>>>(a);
-    else if (a.k == 3) mpf_bwd_slide_kernel<3><<<grid, blk, smem, s>>>(a);
-    else mpf_bwd_slide_kernel<4><<<grid, blk, smem, s>>>(a);
-  } else if (V == 4)
+  if (V == 4)
     mpf_bwd_kernel<4><<<grid, blk, smem, s>>>(a);
   else
     mpf_bwd_kernel<1><<<grid, blk, smem, s>>>(a);

@@ -79,13 +79,13 @@ class MPFNet:
 
     def __init__(self, layers: Sequence, patch: int, image_rows: int, image_cols: int, max_images: int,
                  in_channels: int = 1, precision: str = "tf32", device: Optional[torch.device] = None,
-                 debug_keep: bool = False):
+                 debug_keep: bool = False, flags: int = 0):
         if not torch.cuda.is_available():
             raise RuntimeError("MPFNet needs a CUDA device (there is no CPU fallback)")
         self.lib = L.lib()
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         cfg = L.MpfConfig(in_channels, patch, image_rows, image_cols, max_images,
-                          L.MPF_PREC_TF32 if precision == "tf32" else L.MPF_PREC_FP32, 1,
+                          L.MPF_PREC_TF32 if precision == "tf32" else L.MPF_PREC_FP32, int(flags),
                           1 if debug_keep else 0)
         self.layers = tuple(layers)
         self.patch = patch
@@ -124,6 +124,10 @@ class MPFNet:
             except Exception:
                 pass
             self.h = None
+
+    def set_flags(self, flags: int) -> None:
+        """Kernel-selection flags (MPF_FLAG_*, include/mpf.h); 0 = the measured defaults."""
+        L.check(self.lib.mpf_net_set_flags(self.h, int(flags)), "mpf_net_set_flags")
 
     # ------------------------------------------------------------------ parameters
     def set_params(self, flat) -> None:
@@ -169,8 +173,8 @@ class MPFNet:
         return loss
 
     def train_step(self, images: torch.Tensor, labels: torch.Tensor, class_w=None, stream=None) -> torch.Tensor:
-        """Forward + backward in one C call (mpf_train_step: the softmax head is fused into the
-        last hidden layer's tensor-core epilogue).  Gradients are added; returns losses [n]."""
+        """Forward + backward in one C call (mpf_train_step).  Gradients are added; returns
+        losses [n]."""
         if images.dtype != torch.float32 or not images.is_cuda or not images.is_contiguous():
             raise ValueError("images must be a contiguous cuda float32 tensor")
         if labels.dtype != torch.uint8 or not labels.is_cuda or not labels.is_contiguous():
@@ -210,7 +214,8 @@ class MPFNet:
     def armijo_step(self, images: torch.Tensor, labels: torch.Tensor, alpha0: float = 0.01, beta: float = 0.5,
                     c: float = 1e-4, max_backtracks: int = 10, class_w=None, grad_scale: float = None,
                     stream=None) -> dict:
-        """One Armijo-safeguarded step on a batch (mpf_armijo_step); grad_scale defaults to 1/n."""
+        """One Armijo-safeguarded step on a batch (mpf_armijo_step; it zeroes the gradient buffer
+        before its gradient pass and again at the end); grad_scale defaults to 1/n."""
         n = images.shape[0]
         cw = None
         if class_w is not None:
@@ -325,35 +330,36 @@ class Lbfgs:
         return D.all_sum_scalar(float(loss.double().sum().item()) * gs, device=self.net.device, group=group)
 
     def set_gradient(self) -> None:
-        L.check(self.lib.mpf_lbfgs_set_gradient(self.h, float(self._ctx[3]), None), "mpf_lbfgs_set_gradient")
+        L.check(self.lib.mpf_lbfgs_set_gradient(self.h, float(self._ctx[3]), _stream_ptr(None)),
+                "mpf_lbfgs_set_gradient")
         self.have_g = True
 
     def direction(self):
         gtd, fb = ctypes.c_double(), ctypes.c_int32()
-        L.check(self.lib.mpf_lbfgs_direction(self.h, ctypes.byref(gtd), ctypes.byref(fb), None),
+        L.check(self.lib.mpf_lbfgs_direction(self.h, ctypes.byref(gtd), ctypes.byref(fb), _stream_ptr(None)),
                 "mpf_lbfgs_direction")
         return gtd.value, bool(fb.value)
 
     def trial(self, alpha: float) -> None:
-        L.check(self.lib.mpf_lbfgs_trial(self.h, float(alpha), None), "mpf_lbfgs_trial")
+        L.check(self.lib.mpf_lbfgs_trial(self.h, float(alpha), _stream_ptr(None)), "mpf_lbfgs_trial")
 
     def accept(self) -> bool:
         stored = ctypes.c_int32()
-        L.check(self.lib.mpf_lbfgs_accept(self.h, float(self._ctx[3]), ctypes.byref(stored), None),
+        L.check(self.lib.mpf_lbfgs_accept(self.h, float(self._ctx[3]), ctypes.byref(stored), _stream_ptr(None)),
                 "mpf_lbfgs_accept")
         if stored.value:
             self.n_pairs = min(self.n_pairs + 1, self.memory)
         return bool(stored.value)
 
     def reject(self) -> None:
-        L.check(self.lib.mpf_lbfgs_reject(self.h, None), "mpf_lbfgs_reject")
+        L.check(self.lib.mpf_lbfgs_reject(self.h, _stream_ptr(None)), "mpf_lbfgs_reject")
         self.n_pairs = 0
 
     def step_allreduce(self, images: torch.Tensor, labels: torch.Tensor, global_images: int, alpha0: float = 1.0,
                        beta: float = 0.5, c: float = 1e-4, max_backtracks: int = 10, class_w=None,
                        group=None) -> dict:
         """One iteration whose full batch is the union of every rank's `images`
-        (global_images in total; grad_scale = 1 / global_images).  Runs on the default stream."""
+        (global_images in total; grad_scale = 1 / global_images).  Runs on the current stream."""
         from . import dist as D
         self._ctx = (images, labels, class_w, 1.0 / global_images, group)
         try:

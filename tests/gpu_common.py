@@ -91,11 +91,12 @@ def compare_step(layers, g, o, tol, what=""):
 
 
 def _tf32_round(t):
-    """Round to TF32 on the fp32 bit pattern (nearest, ties away; the GPU rounds ties to even,
-    which makes no difference to an error model)."""
+    """Round to TF32 on the fp32 bit pattern, nearest with ties to even, as the GPU's
+    cvt.rn.tf32 does (finite inputs: the rounding model sees no Inf/NaN)."""
     import torch
     b = t.detach().float().contiguous().view(torch.int32)
-    return ((b + 0x1000) & ~0x1FFF).view(torch.float32).to(t.dtype)
+    lsb = (b >> 13) & 1
+    return ((b + 0x0FFF + lsb) & ~0x1FFF).view(torch.float32).to(t.dtype)
 
 
 def rounding_model_grads(layers, params, images, labels, prec):
@@ -148,3 +149,62 @@ def rounding_model_grads(layers, params, images, labels, prec):
         loss.backward()
         total += th.grad.double().numpy()
     return total
+
+
+def o2_image_worker(args):
+    """One image through the literal whole-image oracle O2 in a worker process (spawned: the
+    parent holds a CUDA context).  args = (layers, params, image [cin, H, W] fp64, labels,
+    P, want_idx).  Returns (loss_sum, n_lab, grad_sum, probs, idx) with idx the O2 argmax
+    tensors of every pool layer (a list per layer of [C, nh, nw] uint8 per output fragment)
+    when want_idx, else None."""
+    layers, params, image, labels, P, want_idx = args
+    ls, cnt, g, pr = o2.train_image(layers, params, image, labels, P=P)
+    idx = None
+    if want_idx:
+        _, idxs = o2.forward_dense(layers, params, image)
+        idx = [None if ix is None else [m.astype(np.uint8) for m in ix] for ix in idxs]
+    return ls, cnt, g, pr, idx
+
+
+def o2_images_parallel(layers, params, images, labels, P, want_idx=()):
+    """O2 on several images in parallel worker processes (BLAS threads split between them)."""
+    import concurrent.futures as cf
+    import multiprocessing as mp
+    import os
+    n = images.shape[0]
+    cores = len(os.sched_getaffinity(0))
+    old = {k: os.environ.get(k) for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS")}
+    for k in old:
+        os.environ[k] = str(max(1, cores // n))
+    try:
+        with cf.ProcessPoolExecutor(max_workers=n, mp_context=mp.get_context("spawn")) as ex:
+            jobs = [ex.submit(o2_image_worker, (layers, params, images[i].astype(np.float64), labels[i], P,
+                                                i in want_idx)) for i in range(n)]
+            return [j.result() for j in jobs]
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def argmax_flips(net, layers, o2_idx, n_frag_images):
+    """Per pool layer: pooled cells whose GPU argmax (tape of the last forward, image 0)
+    differs from O2's argmax on its own fp64 forward, over O2's ragged fragment extents
+    (reading R16: end to end, TF32 rounding can flip near-ties; reported, not asserted).
+    Returns {layer: (flips, cells)}."""
+    from paper_1302_1690_b200 import MPF_TAPE_ARGMAX
+    out = {}
+    for l, ly in enumerate(layers):
+        if ly.kind != S.POOL:
+            continue
+        gpu = net.debug_tape(l, MPF_TAPE_ARGMAX, n_frag_images).cpu().numpy()  # [n*F, rows, cols, C]
+        flips = cells = 0
+        for f, m in enumerate(o2_idx[l]):
+            C_, nh, nw = m.shape
+            g = gpu[f, :nh, :nw, :].transpose(2, 0, 1)
+            flips += int(np.count_nonzero(g != m))
+            cells += m.size
+        out[l] = (flips, cells)
+    return out

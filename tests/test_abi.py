@@ -34,7 +34,7 @@ def _create(cfg_name=None, layers=None, P=None, H=None, W=None, n=1, expect=L.MP
     if cfg_name:
         c = S.CONFIGS[cfg_name]
         layers, P, H, W = c.layers, c.P, c.H, c.W
-    cfg = L.MpfConfig(1, P, H, W, n, L.MPF_PREC_TF32, 1, 0)
+    cfg = L.MpfConfig(1, P, H, W, n, L.MPF_PREC_TF32, 0, 0)
     h = ctypes.c_void_p()
     st = lib.mpf_net_create(ctypes.byref(cfg), layers_to_c(layers), len(layers), ctypes.byref(h))
     assert st == expect, lib.mpf_last_error()
@@ -122,3 +122,19 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".h", ".cpp", ".cuh")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "o1_patch" not in txt, f
+
+
+def test_kernel_selection_flags_are_validated():
+    """mpf_config.flags / mpf_net_set_flags (host only): unknown bits and contradictory
+    pairs are argument errors, at create and later; valid flags are accepted."""
+    lib = L.lib()
+    c = S.CONFIGS["cfg2"]
+    for bad in (1 << 20, L.MPF_FLAG_NTAP_ON | L.MPF_FLAG_NTAP_OFF, L.MPF_FLAG_TC_PAIR | L.MPF_FLAG_TC_SINGLE):
+        cfg = L.MpfConfig(1, c.P, c.H, c.W, 1, L.MPF_PREC_TF32, bad, 0)
+        h = ctypes.c_void_p()
+        assert lib.mpf_net_create(ctypes.byref(cfg), layers_to_c(c.layers), len(c.layers), ctypes.byref(h)) == L.MPF_ERR_ARG
+    h, _ = _create("cfg2")
+    assert lib.mpf_net_set_flags(h, L.MPF_FLAG_SERIAL | L.MPF_FLAG_NTAP_OFF | L.MPF_FLAG_WGRAD_M128) == L.MPF_OK
+    assert lib.mpf_net_set_flags(h, 1 << 30) == L.MPF_ERR_ARG
+    assert lib.mpf_net_set_flags(h, 0) == L.MPF_OK
+    lib.mpf_net_destroy(h)
