@@ -330,10 +330,12 @@ def test_o1_equals_o2_random_archs(seed):
 
 # ----------------------------------------------------------------- library special case
 
-def _torch_dilated(layers, params, img, lab, cw=None):
+def _torch_dilated(layers, params, img, lab, cw=None, tie="first"):
     """fp64 torch: conv2d(dilation = prod of earlier pool k) + max_pool2d(k, stride 1,
     dilation) reproduces every patch output; autograd gives the
-    gradient.  Independent of both oracles."""
+    gradient.  Independent of both oracles.  torch's CPU max pooling keeps the first
+    maximum of a window in row-major order (strict >), i.e. reading R6; tie="last" pools
+    the spatially flipped tensor instead, which routes every tie to its last maximum."""
     import torch
     import torch.nn.functional as Fn
     th = torch.tensor(params, dtype=torch.float64, requires_grad=True)
@@ -341,7 +343,10 @@ def _torch_dilated(layers, params, img, lab, cw=None):
     d, off, c = 1, 0, 1
     for L in layers:
         if L.kind == POOL:
-            x = Fn.max_pool2d(x, L.k, stride=1, dilation=d)
+            if tie == "first":
+                x = Fn.max_pool2d(x, L.k, stride=1, dilation=d)
+            else:
+                x = torch.flip(Fn.max_pool2d(torch.flip(x, (2, 3)), L.k, stride=1, dilation=d), (2, 3))
             d *= L.k
         else:
             n = L.n_out * c * L.k * L.k
@@ -383,6 +388,31 @@ def test_oracles_match_torch_dilated(name, H):
         pix = rng.choice(O * O, 24, replace=False)
         _, _, _, p1 = oracle.o1_image(cfg.layers, cfg.P, params, img, None, pix=pix, need_grad=False)
         np.testing.assert_allclose(p1, pt.reshape(cfg.classes, -1)[:, pix].T, atol=1e-12)
+
+
+def test_tie_rule_first_maximum_pinned():
+    """Reading R6 (first maximum in row-major scan, strict >) pinned in both oracles: with the
+    first layer's weights zero every conv output is tanh(b), so every pooling block is an
+    exact tie and the rule alone decides where the deltas go.  O1 (its `>` in the block
+    scan) and O2 (numpy argmax) must equal torch's first-maximum pooling, and the
+    last-maximum routing must give a clearly different gradient (so `>=` would fail)."""
+    cfg = S.CONFIGS["cfg1"]
+    rng = np.random.default_rng(23)
+    H = 22
+    img = rng.standard_normal((H, H))
+    O = H - cfg.P + 1
+    lab = S.random_labels(rng, 1, O, O, cfg.classes, ignore_frac=0.0)[0]
+    params = S.init_params(cfg)
+    n0 = cfg.layers[0].n_out * cfg.layers[0].k ** 2
+    params[:n0] = 0.0                                    # W of the first conv: all ties below
+    lt, gt, pt = _torch_dilated(cfg.layers, params, img, lab)
+    _, gl, _ = _torch_dilated(cfg.layers, params, img, lab, tie="last")
+    l1, n1, g1, p1 = oracle.o1_image(cfg.layers, cfg.P, params, img, lab)
+    l2, n2, g2, p2 = o2.train_image(cfg.layers, params, img, lab, P=cfg.P)
+    w0 = slice(0, n0)
+    assert np.linalg.norm(gt[w0] - gl[w0]) > 0.1 * np.linalg.norm(gt[w0])  # the rule matters here
+    for g, n in ((g1, n1), (g2, n2)):
+        assert np.linalg.norm(g / n - gt) <= 1e-10 * np.linalg.norm(gt)
 
 
 # ----------------------------------------------------------------- SGD / determinism
