@@ -211,7 +211,10 @@ def main():
         local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # under torchrun the process group is created at every world size (world 1 included:
+    # the NCCL path then runs on one rank, which tests/test_bench_launch.py exercises)
+    use_dist = world > 1 or ("LOCAL_RANK" in os.environ and "MASTER_ADDR" in os.environ)
+    if use_dist:
         if one_gpu_check:
             dist.init_process_group("gloo")
         else:
@@ -231,24 +234,37 @@ def main():
     counts = []  # labelled pixels of each global batch (all ranks)
     for p in pools:
         c = torch.tensor([float((p[3] != 255).sum())], device=dev, dtype=torch.float64)
-        if world > 1:
+        if use_dist:
             dist.all_reduce(c)
         counts.append(float(c.item()))
     stream = torch.cuda.current_stream(dev)
+    # the gradient exchange (a7): one NCCL all-reduce per bucket, started by the library's
+    # gradient-ready hook as soon as the backward has produced that bucket, so it overlaps
+    # the rest of the backward; waited for before the SGD step
+    buckets = None
+    if use_dist and not one_gpu_check:
+        buckets = D.BucketAllReduce(net.grads)
+        net.set_grad_hook(buckets)
+
+    def exchange():
+        if buckets is not None:
+            buckets.wait()
+        else:
+            D.allreduce_grads(net.grads)
 
     def step(i):
         im, lb = pools[i % 2][0], pools[i % 2][1]
         net.train_step(im, lb)  # forward + backward through the C ABI (mpf_train_step)
-        D.allreduce_grads(net.grads)
+        exchange()
         net.sgd_step(cfg.lr, 1.0 / B)
 
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize(dev)
     # One CUDA graph per input pool (the step's ~170 launches, its side-stream fork/join and
-    # the gradient allreduce replayed as one launch); eager launches if capture fails.
+    # the bucketed NCCL all-reduces replayed as one launch); eager launches if capture fails.
     graphs = None
-    if not args.no_graph and world == 1:  # (multi-rank: eager, NCCL calls stay outside capture)
+    if not args.no_graph and not one_gpu_check:
         try:
             graphs = []
             for b in range(2):
@@ -275,7 +291,7 @@ def main():
             torch.cuda.synchronize(dev)
             t_eager = c0.elapsed_time(c1)
             tg = torch.tensor([t_graph, t_eager], device=dev, dtype=torch.float64)
-            if world > 1:
+            if use_dist:
                 dist.all_reduce(tg, op=dist.ReduceOp.MAX)
             if tg[0].item() > 0.97 * tg[1].item():  # a clear win only (the calibration is short)
                 graphs = None
@@ -299,7 +315,7 @@ def main():
     clk = ClockSampler(bus)
     clk.start()
     time.sleep(0.3)
-    if world > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -308,12 +324,12 @@ def main():
         timed_step(i)
     e1.record(stream)
     torch.cuda.synchronize(dev)
-    if world > 1:
+    if use_dist:
         dist.barrier()
     ms = e0.elapsed_time(e1)
     clocks = clk.stop()
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
-    if world > 1:
+    if use_dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     total_px = sum(counts[i % 2] for i in range(args.steps))
@@ -327,14 +343,14 @@ def main():
 
         def hstep(i):
             hi, hl = h_pools[i % 2]
-            net.train_step_host(hi, hl, h_loss, apply_sgd=(world == 1), lr=cfg.lr, grad_scale=1.0 / B)
-            if world > 1:
-                D.allreduce_grads(net.grads)
+            net.train_step_host(hi, hl, h_loss, apply_sgd=not use_dist, lr=cfg.lr, grad_scale=1.0 / B)
+            if use_dist:
+                exchange()
                 net.sgd_step(cfg.lr, 1.0 / B)
 
         for i in range(max(1, args.warmup)):
             hstep(i)
-        if world > 1:
+        if use_dist:
             dist.barrier()
         torch.cuda.synchronize(dev)
         h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -344,7 +360,7 @@ def main():
         h1.record(stream)
         torch.cuda.synchronize(dev)
         hms = torch.tensor([h0.elapsed_time(h1)], device=dev, dtype=torch.float64)
-        if world > 1:
+        if use_dist:
             dist.all_reduce(hms, op=dist.ReduceOp.MAX)
         e2e = {"value": total_px / (float(hms.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h_pools[0][0].numel() * 4 + h_pools[0][1].numel()),
@@ -358,7 +374,7 @@ def main():
     from paper_1302_1690_b200 import _lib as L
     net.set_flags(L.MPF_FLAG_SERIAL)
     try:
-        if world > 1:
+        if use_dist:
             dist.barrier()
         torch.cuda.synchronize(dev)
         net.profile_begin(200 * max(1, args.steps) + 100)
@@ -416,7 +432,7 @@ def main():
                 "gpu_launches": launches,
                 "roofline": roof, "cpu_baseline": cpu, "clocks": clocks}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
 
 

@@ -274,6 +274,22 @@ mpf_status mpf_lbfgs_step(mpf_lbfgs* lb, const float* d_images, int32_t n, const
                           const float* h_class_w, float alpha0, float beta, float c, int32_t max_backtracks,
                           float grad_scale, float* h_out, void* stream);
 
+/*
+ * Gradient-ready hook for data-parallel training (Alg. 2's sum extended over ranks): when
+ * set, mpf_backward_image / mpf_train_step call fn(user, layer, offset, count, stream) on
+ * the calling host thread right after they have enqueued the weight gradient of conv/FC
+ * layer `layer`.  At that point, in the order of `stream` (a cudaStream_t as void*: the
+ * net's side stream, or the caller's stream under MPF_FLAG_SERIAL), the gradient entries
+ * [offset, offset + count) of the bound buffer — every W and b of layers `layer` .. L not
+ * yet reported — are final, so the caller can start a collective on that bucket (e.g. an
+ * NCCL all-reduce ordered after `stream`) while the backward continues below.  Buckets come
+ * in decreasing offset order and cover the whole buffer exactly once per backward.  Work
+ * the callback enqueues on `stream` itself is joined into the caller's stream before the
+ * backward returns; work on other streams is the caller's to join.  fn = NULL removes it.
+ */
+typedef void (*mpf_grad_ready_fn)(void* user, int32_t layer, int64_t offset, int64_t count, void* stream);
+mpf_status mpf_net_set_grad_hook(mpf_net* net, mpf_grad_ready_fn fn, void* user);
+
 /* SGD: theta <- theta - lr * grad_scale * g ; g <- 0. */
 mpf_status mpf_sgd_step(mpf_net* net, float lr, float grad_scale, void* stream);
 

@@ -29,13 +29,18 @@ MPF_FLAG_ROLE_TIMERS = 1 << 7
 
 # every symbol include/mpf.h declares
 EXPORTS = ("mpf_version", "mpf_last_error", "mpf_net_create", "mpf_net_destroy", "mpf_net_geometry",
-           "mpf_net_set_flags",
+           "mpf_net_set_flags", "mpf_net_set_grad_hook",
            "mpf_net_memory", "mpf_net_bind", "mpf_forward_image", "mpf_backward_image", "mpf_sgd_step",
            "mpf_train_step", "mpf_train_step_host", "mpf_fragments_to_pixels", "mpf_mirror_pad", "mpf_class_weights_auto", "mpf_armijo_step",
            "mpf_lbfgs_state_bytes", "mpf_lbfgs_create", "mpf_lbfgs_destroy", "mpf_lbfgs_reset", "mpf_lbfgs_set_gradient", "mpf_lbfgs_direction",
            "mpf_lbfgs_trial", "mpf_lbfgs_accept", "mpf_lbfgs_reject", "mpf_lbfgs_step",
            "mpf_debug_tape", "mpf_check", "mpf_profile_begin",
            "mpf_profile_end")
+
+
+# void (*mpf_grad_ready_fn)(void* user, int32_t layer, int64_t offset, int64_t count, void* stream)
+GRAD_READY_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
+                                 ctypes.c_void_p)
 
 
 class MpfLayer(ctypes.Structure):
@@ -85,6 +90,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.mpf_net_geometry.argtypes = [vp, ctypes.POINTER(MpfGeometry)]
     lib.mpf_net_set_flags.restype = st
     lib.mpf_net_set_flags.argtypes = [vp, ctypes.c_uint32]
+    lib.mpf_net_set_grad_hook.restype = st
+    lib.mpf_net_set_grad_hook.argtypes = [vp, GRAD_READY_FN, vp]
     lib.mpf_net_memory.restype = st
     lib.mpf_net_memory.argtypes = [vp, i32, u64p, u64p, u64p, u64p]
     lib.mpf_net_bind.restype = st

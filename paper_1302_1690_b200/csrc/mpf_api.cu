@@ -726,6 +726,7 @@ static mpf_status backward_impl(Net* N, const uint8_t* d_labels, const float* h_
   }
   // remaining layers in reverse.  Invariant: dcur holds the delta of a[l+1] at the
   // pre-activation (CONV/FC output) or the value (pooled output).
+  long long hook_end = N->n_params;  // gradient entries [hook_end, n_params) already reported
   bool bias_done = true;  // layer L-1's bias came from the head
   bool premul = false;    // dcur already carries act' of the conv feeding the next pool
   float* wpack = scr(N, N->off_wpack);
@@ -776,6 +777,10 @@ static mpf_status backward_impl(Net* N, const uint8_t* d_labels, const float* h_
     if (sw != s) {
       MPF_CUDA(cudaEventRecord(N->ev_buf[ci], sw));
       pending[ci] = true;
+    }
+    if (N->grad_hook) {  // every W / b of layers l .. L is final in the order of sw
+      N->grad_hook(N->grad_hook_user, l, P.w_off, hook_end - P.w_off, (void*)sw);
+      hook_end = P.w_off;
     }
     if (l == 0) break;
     // dgrad: delta of a[l] = full correlation of dcur with the rotated kernel.  When a[l]
@@ -1322,6 +1327,13 @@ mpf_status mpf_debug_tape(const mpf_net* N, int32_t layer, int32_t what, void* d
   if (what != MPF_TAPE_VALUE) return fail(MPF_ERR_ARG, "unknown tape item");
   if (P.out_where != Where::Tape) return fail(MPF_ERR_ARG, "this layer's output is not kept on the tape");
   MPF_CUDA(launch_compact_copy(tape_val(N, layer), o.gr, o.gc, o.vr, o.vc, o.C, nf, (float*)dst, s));
+  return MPF_OK;
+}
+
+mpf_status mpf_net_set_grad_hook(mpf_net* N, mpf_grad_ready_fn fn, void* user) {
+  if (!N) return fail(MPF_ERR_ARG, "NULL net");
+  N->grad_hook = fn;
+  N->grad_hook_user = user;
   return MPF_OK;
 }
 

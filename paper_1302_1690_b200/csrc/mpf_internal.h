@@ -78,6 +78,9 @@ struct Net {
   cudaEvent_t ev_ready = nullptr, ev_join = nullptr, ev_buf[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   int stage_slot = 0;
+  // data-parallel gradient buckets (mpf_net_set_grad_hook)
+  mpf_grad_ready_fn grad_hook = nullptr;
+  void* grad_hook_user = nullptr;
   size_t part_floats = 0;  // capacity of the wgrad partial buffer (floats)
   size_t bpart_floats = 0; // capacity of the bias / head partial buffer (floats)
   int loss_parts = 0;      // loss partials per image

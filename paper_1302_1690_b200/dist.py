@@ -39,6 +39,50 @@ def allreduce_grads(grads, group=None) -> None:
         dist.all_reduce(grads, op=dist.ReduceOp.SUM, group=group)
 
 
+def grad_buckets(layers, w_offset, n_params):
+    """The gradient buckets one backward reports through mpf_net_set_grad_hook, in order:
+    (layer, offset, count) for every conv/FC layer from the last hidden one down to the
+    first; each covers the W / b entries of its layer and of every higher layer not yet
+    reported (the softmax FC goes with the last hidden layer), so together they tile
+    [0, n_params) exactly once."""
+    out, end = [], n_params
+    convs = [l for l, ly in enumerate(layers) if ly.kind != 1]  # 1 = POOL
+    for l in reversed(convs[:-1]):
+        out.append((l, int(w_offset[l]), end - int(w_offset[l])))
+        end = int(w_offset[l])
+    return out
+
+
+class BucketAllReduce:
+    """Data-parallel gradient exchange overlapped with the backward: installed as the net's
+    gradient-ready hook, it starts one all-reduce(SUM) per bucket on the stream that
+    produced it (async, so the backward below keeps running), and wait() makes the current
+    stream wait for all of them before the SGD step.  Same sum as allreduce_grads (the
+    buckets tile the buffer).  On a CPU tensor (gloo tests) stream_ptr is ignored."""
+
+    def __init__(self, grads, group=None):
+        self.grads = grads
+        self.group = group
+        self.works = []
+        self.calls = []
+
+    def __call__(self, layer, offset, count, stream_ptr=None):
+        import torch
+        import torch.distributed as dist
+        self.calls.append((layer, offset, count))
+        view = self.grads[offset:offset + count]
+        if self.grads.is_cuda and stream_ptr is not None:
+            with torch.cuda.stream(torch.cuda.ExternalStream(stream_ptr, device=self.grads.device)):
+                self.works.append(dist.all_reduce(view, op=dist.ReduceOp.SUM, group=self.group, async_op=True))
+        else:
+            self.works.append(dist.all_reduce(view, op=dist.ReduceOp.SUM, group=self.group, async_op=True))
+
+    def wait(self):
+        for w in self.works:
+            w.wait()
+        self.works.clear()
+
+
 def max_over_ranks(value: float, device=None) -> float:
     """Max of a host scalar over ranks (device timing rule: max over ranks)."""
     import torch

@@ -125,6 +125,21 @@ class MPFNet:
                 pass
             self.h = None
 
+    def set_grad_hook(self, fn) -> None:
+        """fn(layer, offset, count, stream_ptr) is called during every backward as soon as the
+        gradient entries [offset, offset + count) are final in the order of the CUDA stream
+        stream_ptr (mpf_net_set_grad_hook; the data-parallel bucketed all-reduce of
+        dist.BucketAllReduce).  None removes it."""
+        if fn is None:
+            self._hook = None
+            L.check(self.lib.mpf_net_set_grad_hook(self.h, L.GRAD_READY_FN(), None), "mpf_net_set_grad_hook")
+            return
+
+        def _cb(user, layer, offset, count, stream):
+            fn(int(layer), int(offset), int(count), stream)
+        self._hook = L.GRAD_READY_FN(_cb)  # kept alive as long as the library may call it
+        L.check(self.lib.mpf_net_set_grad_hook(self.h, self._hook, None), "mpf_net_set_grad_hook")
+
     def set_flags(self, flags: int) -> None:
         """Kernel-selection flags (MPF_FLAG_*, include/mpf.h); 0 = the measured defaults."""
         L.check(self.lib.mpf_net_set_flags(self.h, int(flags)), "mpf_net_set_flags")

@@ -189,3 +189,63 @@ def test_gloo_world2_lbfgs_equals_full_batch_oracle(tmp_path):
     assert np.allclose(r0[:n], theta, rtol=1e-9, atol=1e-12)
     assert np.allclose(r0[n:], rec, rtol=1e-9, atol=1e-12)
     assert rec[0] < eval_lg(S.init_params(cfg).astype(np.float64))[0]
+
+
+def _w_offsets(layers):
+    off, out = 0, []
+    shapes = iter(S.param_shapes(layers))
+    for ly in layers:
+        if ly.kind == S.POOL:
+            out.append(-1)
+            continue
+        (w, b) = next(shapes)
+        out.append(off)
+        off += int(np.prod(w)) + b
+    return out, off
+
+
+def test_grad_buckets_tile_the_buffer():
+    """The buckets mpf_net_set_grad_hook reports (dist.grad_buckets) cover every gradient
+    entry exactly once, in decreasing offset order, the softmax FC with the last hidden
+    layer (include/mpf.h; the same plan the library's backward follows)."""
+    for name in S.CONFIGS:
+        cfg = S.CONFIGS[name]
+        woff, n = _w_offsets(cfg.layers)
+        b = D.grad_buckets(cfg.layers, woff, n)
+        cover = np.zeros(n, int)
+        for l, o, c in b:
+            cover[o:o + c] += 1
+        assert np.all(cover == 1), name
+        assert [o for _, o, _ in b] == sorted([o for _, o, _ in b], reverse=True)
+        assert b[-1][1] == 0 and b[0][0] == len(cfg.layers) - 2
+
+
+def _bucket_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = S.CONFIGS["cfg4"]
+        woff, n = _w_offsets(cfg.layers)
+        g = torch.tensor(np.random.default_rng(rank).standard_normal(n))
+        full = g.clone()
+        D.allreduce_grads(full)
+        br = D.BucketAllReduce(g)
+        for l, o, c in D.grad_buckets(cfg.layers, woff, n):  # what the library's backward calls
+            br(l, o, c, None)
+        br.wait()
+        np.save(os.path.join(out_dir, f"b{rank}.npy"), np.stack([g.numpy(), full.numpy()]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_bucketed_allreduce_equals_flat(tmp_path):
+    """Per-bucket all-reduces started from the gradient-ready hook (dist.BucketAllReduce)
+    give exactly the flat all-reduce of the whole buffer (fp64, two ranks)."""
+    import torch.multiprocessing as mp
+    port = _free_port()
+    mp.start_processes(_bucket_worker, args=(2, port, str(tmp_path)), nprocs=2, start_method="spawn")
+    for r in range(2):
+        g, full = np.load(tmp_path / f"b{r}.npy")
+        assert np.array_equal(g, full)
