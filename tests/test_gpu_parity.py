@@ -281,9 +281,11 @@ def test_bad_label_is_reported():
 @pytest.mark.parametrize("name,bad,which", [("cfg2", np.nan, 0), ("cfg4s", np.nan, 0), ("cfg2", np.inf, 1),
                                            ("cfg4s", -np.inf, 1)])
 def test_nan_weight_propagates_to_loss_and_gradients(name, bad, which):
-    """A NaN in the first layer's weights, or an Inf in a tensor-core layer's weights, must
-    reach the loss and the gradients through every kernel of the step (TF32 rounding keeps
-    Inf, activations, MPF, head), not be rounded or pooled away into finite numbers."""
+    """A NaN in the first layer's weights must reach the loss and the gradients through every
+    kernel of the step; an Inf in a tensor-core layer's weights must reach the gradients (its
+    TF32 operand rounding keeps Inf; clamping it to the largest finite TF32 would hide it).
+    The loss may stay finite with an Inf weight: tanh saturates at +-inf in exact arithmetic
+    too, but the delta propagated through that weight is non-finite."""
     cfg = _cfg4s() if name == "cfg4s" else S.CONFIGS[name]
     images, labels = S.make_batch(cfg, [0])
     params = S.init_params(cfg)
@@ -291,7 +293,8 @@ def test_nan_weight_propagates_to_loss_and_gradients(name, bad, which):
     woff = [sl.start for nm, sl in param_slices(cfg.layers) if nm == f"W{conv[which]}"][0]
     params[woff] = bad
     g = gpu_step(cfg.layers, cfg.P, images, labels, params, "tf32")
-    assert not np.isfinite(g["loss"]).any()
+    if np.isnan(bad):
+        assert not np.isfinite(g["loss"]).any()
     assert not np.isfinite(g["grad_sum"]).all()
 
 
