@@ -48,4 +48,9 @@ bool tc_supported(int cin, int cout, int k);
 bool tc_wgrad_supported(int cin, int cout, int k);
 cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s, int* grid_out = nullptr);
 cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits, cudaStream_t s);
+// fp32 tensor map: dims[0] innermost, strides[i] = bytes between steps of dim i+1; zero fill
+// out of bounds on loads, clipped stores
+cudaError_t make_tmap_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                          const uint32_t* box, bool sw128);
+
 }  // namespace mpf

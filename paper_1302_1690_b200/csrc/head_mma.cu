@@ -1,0 +1,411 @@
+// head_mma.cu — the training softmax head (last FC + per-pixel softmax + class-weighted MCCE +
+// dL/dx_hat, and the back-propagation through that FC: "first dL/dx_hat",
+// 197 MCCE per pixel, 252 per-class weights; readings R8, R9, R15) with its three small
+// contractions on the warp-level tensor cores (mma.sync m16n8k8, TF32 operands, fp32
+// accumulate), in one pass over the last hidden activation h:
+//
+//   GEMM1  z[pos][c]    = sum_ch h[pos][ch] W_L[c][ch]        (+ b_L; softmax; dz)
+//   GEMM3  dW_L[c][ch] += sum_pos dz[pos][c] h[pos][ch]        (Alg. 2: sum over all fragments)
+//   GEMM2  dh[pos][ch]  = (sum_c dz[pos][c] W_L[c][ch]) act'(h[pos][ch])
+//
+// with db_L = sum dz and db_prev = sum dh.  Every product is split 3xTF32 (a_hi b_hi +
+// a_hi b_lo + a_lo b_hi, x_lo = x - tf32(x)), so the head keeps fp32-level accuracy (its
+// FMA form was exact fp32).  The FMA form (head.cu) needs ~3000 FMAs + ~200 other warp
+// instructions per position and ran instruction-bound at ~53 % of HBM; here the MMAs take
+// ~900 tensor instructions per 64-position tile and the kernel streams h in / dh out.
+//
+// Schedule (persistent CTAs, one per SM, 8 warps): tiles of 64 positions of one image.  A
+// tile of h arrives by TMA as ceil(Ch/32) SWIZZLE_128B boxes [64 positions][32 channels]
+// (3-D map [n][per_img][Ch]: rows past the image end and channels past Ch read as zeros and
+// are clipped on store), three tiles in flight.  Per tile: labels -> GEMM1 (warp = 16
+// positions x half of K, partial logits combined in shared memory) -> softmax / loss / dz
+// (warps 0-3) -> GEMM3 (warp = two 16-channel tiles, accumulators live across tiles) ->
+// GEMM2 + act' + TF32 rounding written IN PLACE over the h tile -> TMA store of dh.  All
+// sums have a fixed order (deterministic; loss and bias partials as in head.cu).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "conv_tc.h"
+#include "head_common.cuh"
+#include "mpf_internal.h"
+#include "numerics.cuh"
+#include "tc_ptx.cuh"
+
+namespace mpf {
+
+namespace {
+
+constexpr int kMT = 64;          // positions per tile
+constexpr int kMThr = 256;       // 8 warps
+constexpr int kMStages = 3;      // h tiles in flight
+constexpr int kBoxBytes = kMT * 128;  // one [64 x 32 fp32] SW128 box
+constexpr int kWS = 260;         // row stride of the split W_L copies (conflict-free fragment reads)
+
+struct HeadMmaParams {
+  int C, Ch, nchunk, nkt, nmt3;  // classes, channels, 32-ch boxes, 8-ch K/N tiles, 16-ch M tiles
+  int tpi;                       // tiles per image
+  long long total;               // tiles
+  long long per_img;             // positions per image (fragment-major, padded grid)
+  const float* wL;               // [C][Ch]
+  const float* bL;               // [C]
+  const uint8_t* lab_frag;       // [n][per_img] (launch_label_frag)
+  const int* nlab;               // [n]
+  float cw[16];
+  int act;                       // activation of h
+  int round;                     // TF32-round dh (operand of the FC1 dgrad / wgrad MMAs)
+  float* loss_part;              // [n][tpi][8]
+  float* part;                   // [grid][C*Ch + C + Ch]
+};
+
+// byte offset of (row r, channel c) inside a tile: box c/32, TMA SWIZZLE_128B pattern
+__device__ __forceinline__ uint32_t swz(int r, int c) {
+  return (uint32_t)((c >> 5) * kBoxBytes + r * 128 + ((((c & 31) >> 2) ^ (r & 7)) << 4) + ((c & 3) << 2));
+}
+
+// 3xTF32 split: x = hi + lo (exact), both as TF32 operands
+__device__ __forceinline__ void split3(float x, uint32_t& hi, uint32_t& lo) {
+  const float h = tf32_rn(x);
+  hi = __float_as_uint(h);
+  lo = __float_as_uint(tf32_rn(x - h));
+}
+
+__device__ __forceinline__ float act_der_m(int act, float y) {
+  if (act == MPF_TANH) return fmaf(-y, y, 1.f);
+  if (act == MPF_LOGISTIC) return y * (1.f - y);
+  return 1.f;
+}
+
+template <bool TANH>
+__global__ void __launch_bounds__(kMThr, 1)
+    head_mma_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmD, HeadMmaParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t s0 = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
+  uint8_t* g0 = smem_raw + (s0 - ptx::smem_u32(smem_raw));  // generic address of s0
+  const uint32_t stage_bytes = (uint32_t)p.nchunk * kBoxBytes;
+  // [stages | W_L hi [8][kWS] | W_L lo [8][kWS] | zp [64][8] | dz [64][8] | lab [64] | dbL [4][8] | bars]
+  const uint32_t oW = kMStages * stage_bytes;
+  uint32_t* s_whi = reinterpret_cast<uint32_t*>(g0 + oW);
+  uint32_t* s_wlo = s_whi + 8 * kWS;
+  float* s_zp = reinterpret_cast<float*>(s_wlo + 8 * kWS);
+  float* s_dz = s_zp + kMT * 8;
+  int* s_lab = reinterpret_cast<int*>(s_dz + kMT * 8);
+  float* s_dbl = reinterpret_cast<float*>(s_lab + kMT);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_dbl + 32);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const int g = lane >> 2, t = lane & 3;
+  const int C = p.C, Ch = p.Ch;
+
+  for (int e = tid; e < 8 * 256; e += kMThr) {
+    const int c = e >> 8, ch = e & 255;
+    uint32_t hi, lo;
+    split3((c < C && ch < Ch) ? p.wL[c * Ch + ch] : 0.f, hi, lo);
+    s_whi[c * kWS + ch] = hi;
+    s_wlo[c * kWS + ch] = lo;
+  }
+  if (tid == 0) {
+    ptx::prefetch_tmap(&tmH);
+    ptx::prefetch_tmap(&tmD);
+    for (int s = 0; s < kMStages; ++s) ptx::mbar_init(ptx::smem_u32(&bars[s]), 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto issue = [&](long long tile, int st) {
+    const int img = (int)(tile / p.tpi), p0 = (int)(tile % p.tpi) * kMT;
+    const uint32_t bar = ptx::smem_u32(&bars[st]);
+    ptx::mbar_arrive_expect_tx(bar, stage_bytes);
+    for (int c = 0; c < p.nchunk; ++c) ptx::tma_load_3d(s0 + st * stage_bytes + c * kBoxBytes, &tmH, bar, 32 * c, p0, img);
+  };
+  if (tid == 0)
+    for (int s = 0; s < 2; ++s) {
+      const long long tile = blockIdx.x + (long long)s * gridDim.x;
+      if (tile < p.total) issue(tile, s);
+    }
+
+  // GEMM2's B fragments (constant): N-tiles nt = warp + 8 j; b0 = W[t][8 nt + g], b1 = W[t + 4][8 nt + g]
+  uint32_t bW[4][4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int ch = 8 * (warp + 8 * j) + g;
+    const bool ok = ch < 256;
+    bW[j][0] = ok ? s_whi[t * kWS + ch] : 0u;
+    bW[j][1] = ok ? s_whi[(t + 4) * kWS + ch] : 0u;
+    bW[j][2] = ok ? s_wlo[t * kWS + ch] : 0u;
+    bW[j][3] = ok ? s_wlo[(t + 4) * kWS + ch] : 0u;
+  }
+  const float bl0 = 2 * t < C ? p.bL[2 * t] : 0.f, bl1 = 2 * t + 1 < C ? p.bL[2 * t + 1] : 0.f;
+  float accW[2][4], accP[4][2], accL[2] = {0.f, 0.f};
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) accW[j][u] = 0.f;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) accP[j][0] = accP[j][1] = 0.f;
+
+  const int mt = warp & 3, kh = warp >> 2;
+  const int khalf = (p.nkt + 1) >> 1;
+  const int ks0 = kh ? khalf : 0, ks1 = kh ? p.nkt : khalf;
+  int it = 0;
+  for (long long tile = blockIdx.x; tile < p.total; tile += gridDim.x, ++it) {
+    const int st = it % kMStages;
+    const int img = (int)(tile / p.tpi), tt = (int)(tile % p.tpi), p0 = tt * kMT;
+    if (tid < kMT) {
+      const long long pos = (long long)p0 + tid;
+      int lab = kLabBeyond;
+      if (pos < p.per_img) {
+        lab = p.lab_frag[(long long)img * p.per_img + pos];
+        if (lab == kLabFragPad) lab = kLabPad;
+      }
+      s_lab[tid] = lab;
+    }
+    ptx::mbar_wait(ptx::smem_u32(&bars[st]), (uint32_t)((it / kMStages) & 1));
+    __syncthreads();  // labels visible; the previous tile's zp / dz are no longer read
+    uint8_t* hb = g0 + st * stage_bytes;
+
+    // ---------------------------------------------------------------- GEMM1: logits
+    const int r0 = 16 * mt + g, r1 = r0 + 8;
+    float z[4];
+    {
+      float z0[4] = {0.f, 0.f, 0.f, 0.f}, z1[4] = {0.f, 0.f, 0.f, 0.f}, z2[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int ks = ks0; ks < ks1; ++ks) {
+        const int k0 = 8 * ks;
+        uint32_t ah[4], al[4];
+        split3(*reinterpret_cast<const float*>(hb + swz(r0, k0 + t)), ah[0], al[0]);
+        split3(*reinterpret_cast<const float*>(hb + swz(r1, k0 + t)), ah[1], al[1]);
+        split3(*reinterpret_cast<const float*>(hb + swz(r0, k0 + t + 4)), ah[2], al[2]);
+        split3(*reinterpret_cast<const float*>(hb + swz(r1, k0 + t + 4)), ah[3], al[3]);
+        const uint32_t bh0 = s_whi[g * kWS + k0 + t], bh1 = s_whi[g * kWS + k0 + t + 4];
+        const uint32_t bo0 = s_wlo[g * kWS + k0 + t], bo1 = s_wlo[g * kWS + k0 + t + 4];
+        ptx::mma_m16n8k8_tf32(z0, ah, bh0, bh1);
+        ptx::mma_m16n8k8_tf32(z1, ah, bo0, bo1);
+        ptx::mma_m16n8k8_tf32(z2, al, bh0, bh1);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) z[u] = z0[u] + (z1[u] + z2[u]);
+    }
+    if (kh == 1) {
+      *reinterpret_cast<float2*>(s_zp + r0 * 8 + 2 * t) = make_float2(z[0], z[1]);
+      *reinterpret_cast<float2*>(s_zp + r1 * 8 + 2 * t) = make_float2(z[2], z[3]);
+    }
+    __syncthreads();
+
+    // ---------------------------------------------------------------- softmax, loss, dz
+    float lossv = 0.f;
+    if (kh == 0) {
+      const int nl = p.nlab[img];
+#pragma unroll
+      for (int hr = 0; hr < 2; ++hr) {
+        const int row = hr ? r1 : r0;
+        const float2 zp = *reinterpret_cast<const float2*>(s_zp + row * 8 + 2 * t);
+        const float za = z[2 * hr] + zp.x + bl0, zb = z[2 * hr + 1] + zp.y + bl1;
+        const int ca = 2 * t, cb = 2 * t + 1;
+        float m = fmaxf(ca < C ? za : -INFINITY, cb < C ? zb : -INFINITY);
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+        float se = (ca < C ? expf(za - m) : 0.f) + (cb < C ? expf(zb - m) : 0.f);
+        se += __shfl_xor_sync(0xffffffffu, se, 1);
+        se += __shfl_xor_sync(0xffffffffu, se, 2);
+        const float lse = m + logf(se);
+        const int lab = s_lab[row];
+        const bool active = lab >= 0 && lab < C;
+        float da = 0.f, db = 0.f;
+        if (active) {
+          const float wt = p.cw[lab];
+          const float inv = nl > 0 ? wt / (float)nl : 0.f;
+          if (ca < C) da = inv * (expf(za - lse) - (ca == lab ? 1.f : 0.f));
+          if (cb < C) db = inv * (expf(zb - lse) - (cb == lab ? 1.f : 0.f));
+          if (ca == lab) lossv += wt * (lse - za);
+          if (cb == lab) lossv += wt * (lse - zb);
+        }
+        *reinterpret_cast<float2*>(s_dz + row * 8 + 2 * t) = make_float2(da, db);
+        accL[0] += da;
+        accL[1] += db;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lossv += __shfl_xor_sync(0xffffffffu, lossv, o);
+    if (lane == 0) p.loss_part[((long long)img * p.tpi + tt) * (kMThr / 32) + warp] = lossv;
+    __syncthreads();  // dz complete
+
+    // ---------------------------------------------------------------- GEMM3: dW_L^T += h^T dz
+    // warp: channel tiles w and w + 8 (channels 16 mt3 + g, + 8), K = the 64 positions
+#pragma unroll 2
+    for (int kst = 0; kst < kMT / 8; ++kst) {
+      const int k0 = 8 * kst;
+      uint32_t bh0, bo0, bh1, bo1;
+      split3(s_dz[(k0 + t) * 8 + g], bh0, bo0);
+      split3(s_dz[(k0 + t + 4) * 8 + g], bh1, bo1);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int mt3 = warp + 8 * j;
+        if (mt3 >= p.nmt3) break;  // warp-uniform
+        const int c0 = 16 * mt3 + g, c1 = c0 + 8;
+        uint32_t ah[4], al[4];
+        split3(*reinterpret_cast<const float*>(hb + swz(k0 + t, c0)), ah[0], al[0]);
+        split3(*reinterpret_cast<const float*>(hb + swz(k0 + t, c1)), ah[1], al[1]);
+        split3(*reinterpret_cast<const float*>(hb + swz(k0 + t + 4, c0)), ah[2], al[2]);
+        split3(*reinterpret_cast<const float*>(hb + swz(k0 + t + 4, c1)), ah[3], al[3]);
+        ptx::mma_m16n8k8_tf32(accW[j], ah, bh0, bh1);
+        ptx::mma_m16n8k8_tf32(accW[j], ah, bo0, bo1);
+        ptx::mma_m16n8k8_tf32(accW[j], al, bh0, bh1);
+      }
+    }
+    // refill: the dh store of the previous tile (this stage's predecessor in the ring) has
+    // had two phases to read its source; tile it + 2 goes into that stage
+    if (tid == 0) {
+      ptx::bulk_wait_read<0>();
+      const long long nt2 = tile + 2LL * gridDim.x;
+      if (nt2 < p.total) issue(nt2, (it + 2) % kMStages);
+    }
+    __syncthreads();  // GEMM3 has read every h before GEMM2 overwrites it with dh
+
+    // ---------------------------------------------------------------- GEMM2: dh = dz W_L, act'
+    uint32_t adh[4][4], adl[4][4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int q0 = 16 * m + g, q1 = q0 + 8;
+      split3(s_dz[q0 * 8 + t], adh[m][0], adl[m][0]);
+      split3(s_dz[q1 * 8 + t], adh[m][1], adl[m][1]);
+      split3(s_dz[q0 * 8 + t + 4], adh[m][2], adl[m][2]);
+      split3(s_dz[q1 * 8 + t + 4], adh[m][3], adl[m][3]);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int nt = warp + 8 * j;
+      if (nt >= p.nkt) break;  // warp-uniform
+      const int ch = 8 * nt + 2 * t;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        float d[4] = {0.f, 0.f, 0.f, 0.f};
+        ptx::mma_m16n8k8_tf32(d, adh[m], bW[j][0], bW[j][1]);
+        ptx::mma_m16n8k8_tf32(d, adh[m], bW[j][2], bW[j][3]);
+        ptx::mma_m16n8k8_tf32(d, adl[m], bW[j][0], bW[j][1]);
+        const int q0 = 16 * m + g, q1 = q0 + 8;
+        float2* h0 = reinterpret_cast<float2*>(hb + swz(q0, ch));
+        float2* h1 = reinterpret_cast<float2*>(hb + swz(q1, ch));
+        const float2 hv0 = *h0, hv1 = *h1;
+        const int la = s_lab[q0], lb = s_lab[q1];
+        const bool a0 = la >= 0 && la < C, a1 = lb >= 0 && lb < C;
+        float e[4];
+        e[0] = a0 ? d[0] * (TANH ? fmaf(-hv0.x, hv0.x, 1.f) : act_der_m(p.act, hv0.x)) : 0.f;
+        e[1] = a0 ? d[1] * (TANH ? fmaf(-hv0.y, hv0.y, 1.f) : act_der_m(p.act, hv0.y)) : 0.f;
+        e[2] = a1 ? d[2] * (TANH ? fmaf(-hv1.x, hv1.x, 1.f) : act_der_m(p.act, hv1.x)) : 0.f;
+        e[3] = a1 ? d[3] * (TANH ? fmaf(-hv1.y, hv1.y, 1.f) : act_der_m(p.act, hv1.y)) : 0.f;
+        accP[j][0] += e[0] + e[2];
+        accP[j][1] += e[1] + e[3];
+        if (p.round) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) e[u] = tf32_rn_sat(e[u]);
+        }
+        *h0 = make_float2(e[0], e[1]);
+        *h1 = make_float2(e[2], e[3]);
+      }
+    }
+    ptx::fence_proxy_async();  // dh in shared memory is visible to the TMA store
+    __syncthreads();
+    if (tid == 0) {
+      for (int c = 0; c < p.nchunk; ++c) ptx::tma_store_3d(&tmD, s0 + st * stage_bytes + c * kBoxBytes, 32 * c, p0, img);
+      ptx::bulk_commit();
+    }
+  }
+  if (tid == 0) ptx::bulk_wait<0>();
+
+  // ------------------------------------------------------------------ block partials
+  const int E = C * Ch + C + Ch;
+  float* out = p.part + (size_t)blockIdx.x * E;
+  // dW_L[c][ch]: each (class, channel) is owned by exactly one thread of one warp
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int mt3 = warp + 8 * j;
+    if (mt3 >= p.nmt3) break;
+    const int c0 = 16 * mt3 + g, c1 = c0 + 8, ca = 2 * t, cb = 2 * t + 1;
+    if (ca < C && c0 < Ch) out[ca * Ch + c0] = accW[j][0];
+    if (cb < C && c0 < Ch) out[cb * Ch + c0] = accW[j][1];
+    if (ca < C && c1 < Ch) out[ca * Ch + c1] = accW[j][2];
+    if (cb < C && c1 < Ch) out[cb * Ch + c1] = accW[j][3];
+  }
+  // db_prev[ch]: the 8 lanes of equal t hold channels 8 nt + 2t, + 1 (fixed-order butterfly)
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      float v = accP[j][u];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      const int nt = warp + 8 * j, ch = 8 * nt + 2 * t + u;
+      if (g == 0 && nt < p.nkt && ch < Ch) out[C * Ch + C + ch] = v;
+    }
+  }
+  // db_L[c]: warps 0-3 hold classes 2t, 2t + 1 of their 16 positions per tile
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    float v = accL[u];
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    v += __shfl_xor_sync(0xffffffffu, v, 8);
+    v += __shfl_xor_sync(0xffffffffu, v, 16);
+    if (kh == 0 && g == 0) s_dbl[warp * 8 + 2 * t + u] = v;
+  }
+  __syncthreads();
+  if (tid < C) out[C * Ch + tid] = ((s_dbl[tid] + s_dbl[8 + tid]) + s_dbl[16 + tid]) + s_dbl[24 + tid];
+}
+
+size_t head_mma_smem(int Ch) {
+  const int nchunk = (Ch + 31) / 32;
+  return 1024 + (size_t)kMStages * nchunk * kBoxBytes + 2 * 8 * kWS * 4 + 2 * kMT * 8 * 4 + kMT * 4 + 32 * 4 +
+         kMStages * 8 + 64;
+}
+
+}  // namespace
+
+bool head_mma_ok(int C, int Ch, bool train) {
+  return train && C >= 2 && C <= 8 && Ch >= 4 && Ch <= 256 && Ch % 4 == 0;
+}
+
+int head_mma_grid(long long per_img, int n) {
+  const long long tiles = (long long)n * ((per_img + kMT - 1) / kMT);
+  const long long g = tiles < 148 ? tiles : 148;
+  return (int)(g < 1 ? 1 : g);
+}
+
+cudaError_t launch_head_mma(const HeadArgs& a, cudaStream_t s) {
+  HeadMmaParams p{};
+  p.C = a.C;
+  p.Ch = a.Ch;
+  p.nchunk = (a.Ch + 31) / 32;
+  p.nkt = (a.Ch + 7) / 8;
+  p.nmt3 = (a.Ch + 15) / 16;
+  p.per_img = (long long)a.F * a.gr * a.gc;
+  p.tpi = (int)((p.per_img + kMT - 1) / kMT);
+  p.total = (long long)a.n * p.tpi;
+  p.wL = a.w;
+  p.bL = a.b;
+  p.lab_frag = a.lab_frag;
+  p.nlab = a.nlab;
+  for (int c = 0; c < 16; ++c) p.cw[c] = a.cw[c];
+  p.act = a.hidden_act;
+  p.round = a.round_tf32;
+  p.loss_part = a.loss_part;
+  p.part = a.part;
+  if (a.tiles_per_img != p.tpi || !a.lab_frag) return cudaErrorInvalidValue;
+  CUtensorMap H, D;
+  const uint64_t dims[3] = {(uint64_t)a.Ch, (uint64_t)p.per_img, (uint64_t)a.n};
+  const uint64_t strides[2] = {(uint64_t)a.Ch * 4, (uint64_t)p.per_img * a.Ch * 4};
+  const uint32_t box[3] = {32, kMT, 1};
+  cudaError_t e = make_tmap_f32(&H, a.h, 3, dims, strides, box, true);
+  if (e != cudaSuccess) return e;
+  e = make_tmap_f32(&D, a.dh, 3, dims, strides, box, true);
+  if (e != cudaSuccess) return e;
+  const size_t smem = head_mma_smem(a.Ch);
+  const int grid = a.n_blocks;
+  auto kern = a.hidden_act == MPF_TANH ? head_mma_kernel<true> : head_mma_kernel<false>;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kMThr, smem, s>>>(H, D, p);
+  return cudaGetLastError();
+}
+
+}  // namespace mpf
