@@ -39,7 +39,7 @@ namespace {
 
 constexpr int kMT = 64;          // positions per tile
 constexpr int kMThr = 256;       // 8 warps
-constexpr int kMStages = 3;      // h tiles in flight
+constexpr int kMStages = 2;      // h tiles in flight (plus one dh tile)
 constexpr int kBoxBytes = kMT * 128;  // one [64 x 32 fp32] SW128 box
 constexpr int kWS = 260;         // row stride of the split W_L copies (conflict-free fragment reads)
 
@@ -84,15 +84,17 @@ __global__ void __launch_bounds__(kMThr, 1)
   const uint32_t s0 = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* g0 = smem_raw + (s0 - ptx::smem_u32(smem_raw));  // generic address of s0
   const uint32_t stage_bytes = (uint32_t)p.nchunk * kBoxBytes;
-  // [stages | W_L hi [8][kWS] | W_L lo [8][kWS] | zp [64][8] | dz [64][8] | lab [64] | dbL [4][8] | bars]
-  const uint32_t oW = kMStages * stage_bytes;
-  uint32_t* s_whi = reinterpret_cast<uint32_t*>(g0 + oW);
+  // [h stages x2 | dh tile | W_L hi [8][kWS] | W_L lo [8][kWS] | z partials [8 warps][64][8] |
+  //  dz [64][8] | lab [64] | db_L partials [64][8] | bars]
+  const uint32_t sDh = s0 + kMStages * stage_bytes;
+  uint8_t* dhb = g0 + kMStages * stage_bytes;
+  uint32_t* s_whi = reinterpret_cast<uint32_t*>(dhb + stage_bytes);
   uint32_t* s_wlo = s_whi + 8 * kWS;
   float* s_zp = reinterpret_cast<float*>(s_wlo + 8 * kWS);
-  float* s_dz = s_zp + kMT * 8;
+  float* s_dz = s_zp + 8 * kMT * 8;
   int* s_lab = reinterpret_cast<int*>(s_dz + kMT * 8);
   float* s_dbl = reinterpret_cast<float*>(s_lab + kMT);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_dbl + 32);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_dbl + kMT * 8);
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const int g = lane >> 2, t = lane & 3;
@@ -119,11 +121,15 @@ __global__ void __launch_bounds__(kMThr, 1)
     ptx::mbar_arrive_expect_tx(bar, stage_bytes);
     for (int c = 0; c < p.nchunk; ++c) ptx::tma_load_3d(s0 + st * stage_bytes + c * kBoxBytes, &tmH, bar, 32 * c, p0, img);
   };
-  if (tid == 0)
-    for (int s = 0; s < 2; ++s) {
-      const long long tile = blockIdx.x + (long long)s * gridDim.x;
-      if (tile < p.total) issue(tile, s);
-    }
+  // label of position tid of a tile, issued one tile ahead (kept in a register)
+  auto fetch_label = [&](long long tile) -> int {
+    if (tile >= p.total) return kLabBeyond;
+    const int img = (int)(tile / p.tpi);
+    const long long pos = (long long)(tile % p.tpi) * kMT + tid;
+    return pos < p.per_img ? (int)__ldg(p.lab_frag + (long long)img * p.per_img + pos) : kLabBeyond;
+  };
+  if (tid == 0 && blockIdx.x < p.total) issue(blockIdx.x, 0);
+  int lab_next = tid < kMT ? fetch_label(blockIdx.x) : kLabBeyond;
 
   // GEMM2's B fragments (constant): N-tiles nt = warp + 8 j; b0 = W[t][8 nt + g], b1 = W[t + 4][8 nt + g]
   uint32_t bW[4][4];
@@ -136,133 +142,132 @@ __global__ void __launch_bounds__(kMThr, 1)
     bW[j][2] = ok ? s_wlo[t * kWS + ch] : 0u;
     bW[j][3] = ok ? s_wlo[(t + 4) * kWS + ch] : 0u;
   }
-  const float bl0 = 2 * t < C ? p.bL[2 * t] : 0.f, bl1 = 2 * t + 1 < C ? p.bL[2 * t + 1] : 0.f;
-  float accW[2][4], accP[4][2], accL[2] = {0.f, 0.f};
+  // accumulators living across tiles: dW_L^T (two 16-channel tiles x three split products),
+  // db_prev (four 8-channel tiles x two channels), db_L (threads 0-63: eight classes)
+  float accW[2][3][4], accP[4][2], accL[8];
 #pragma unroll
   for (int j = 0; j < 2; ++j)
 #pragma unroll
-    for (int u = 0; u < 4; ++u) accW[j][u] = 0.f;
+    for (int q = 0; q < 3; ++q)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) accW[j][q][u] = 0.f;
 #pragma unroll
   for (int j = 0; j < 4; ++j) accP[j][0] = accP[j][1] = 0.f;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) accL[c] = 0.f;
+  float blc[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) blc[c] = c < C ? p.bL[c] : 0.f;
 
-  const int mt = warp & 3, kh = warp >> 2;
-  const int khalf = (p.nkt + 1) >> 1;
-  const int ks0 = kh ? khalf : 0, ks1 = kh ? p.nkt : khalf;
   int it = 0;
   for (long long tile = blockIdx.x; tile < p.total; tile += gridDim.x, ++it) {
-    const int st = it % kMStages;
+    const int st = it & 1;
     const int img = (int)(tile / p.tpi), tt = (int)(tile % p.tpi), p0 = tt * kMT;
     if (tid < kMT) {
-      const long long pos = (long long)p0 + tid;
-      int lab = kLabBeyond;
-      if (pos < p.per_img) {
-        lab = p.lab_frag[(long long)img * p.per_img + pos];
-        if (lab == kLabFragPad) lab = kLabPad;
-      }
-      s_lab[tid] = lab;
+      s_lab[tid] = lab_next == kLabFragPad ? kLabPad : lab_next;
+      lab_next = fetch_label(tile + gridDim.x);  // in flight during this tile
     }
-    ptx::mbar_wait(ptx::smem_u32(&bars[st]), (uint32_t)((it / kMStages) & 1));
-    __syncthreads();  // labels visible; the previous tile's zp / dz are no longer read
-    uint8_t* hb = g0 + st * stage_bytes;
+    ptx::mbar_wait(ptx::smem_u32(&bars[st]), (uint32_t)((it >> 1) & 1));
+    __syncthreads();  // labels and h visible; the other stage's h is no longer read
+    if (tid == 0 && tile + gridDim.x < p.total) issue(tile + gridDim.x, st ^ 1);
+    const uint8_t* hb = g0 + st * stage_bytes;
 
-    // ---------------------------------------------------------------- GEMM1: logits
-    const int r0 = 16 * mt + g, r1 = r0 + 8;
-    float z[4];
+    // ------------------------------------------------ GEMM1: partial logits, K split over warps
     {
-      float z0[4] = {0.f, 0.f, 0.f, 0.f}, z1[4] = {0.f, 0.f, 0.f, 0.f}, z2[4] = {0.f, 0.f, 0.f, 0.f};
-      for (int ks = ks0; ks < ks1; ++ks) {
+      float za[4][3][4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) za[m][q][u] = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int ks = warp + 8 * i;
+        if (ks >= p.nkt) break;  // warp-uniform
         const int k0 = 8 * ks;
-        uint32_t ah[4], al[4];
-        split3(*reinterpret_cast<const float*>(hb + swz(r0, k0 + t)), ah[0], al[0]);
-        split3(*reinterpret_cast<const float*>(hb + swz(r1, k0 + t)), ah[1], al[1]);
-        split3(*reinterpret_cast<const float*>(hb + swz(r0, k0 + t + 4)), ah[2], al[2]);
-        split3(*reinterpret_cast<const float*>(hb + swz(r1, k0 + t + 4)), ah[3], al[3]);
         const uint32_t bh0 = s_whi[g * kWS + k0 + t], bh1 = s_whi[g * kWS + k0 + t + 4];
         const uint32_t bo0 = s_wlo[g * kWS + k0 + t], bo1 = s_wlo[g * kWS + k0 + t + 4];
-        ptx::mma_m16n8k8_tf32(z0, ah, bh0, bh1);
-        ptx::mma_m16n8k8_tf32(z1, ah, bo0, bo1);
-        ptx::mma_m16n8k8_tf32(z2, al, bh0, bh1);
-      }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) z[u] = z0[u] + (z1[u] + z2[u]);
-    }
-    if (kh == 1) {
-      *reinterpret_cast<float2*>(s_zp + r0 * 8 + 2 * t) = make_float2(z[0], z[1]);
-      *reinterpret_cast<float2*>(s_zp + r1 * 8 + 2 * t) = make_float2(z[2], z[3]);
+        for (int m = 0; m < 4; ++m) {
+          const int r0 = 16 * m + g, r1 = r0 + 8;
+          uint32_t ah[4], al[4];
+          split3(*reinterpret_cast<const float*>(hb + swz(r0, k0 + t)), ah[0], al[0]);
+          split3(*reinterpret_cast<const float*>(hb + swz(r1, k0 + t)), ah[1], al[1]);
+          split3(*reinterpret_cast<const float*>(hb + swz(r0, k0 + t + 4)), ah[2], al[2]);
+          split3(*reinterpret_cast<const float*>(hb + swz(r1, k0 + t + 4)), ah[3], al[3]);
+          ptx::mma_m16n8k8_tf32(za[m][0], ah, bh0, bh1);
+          ptx::mma_m16n8k8_tf32(za[m][1], ah, bo0, bo1);
+          ptx::mma_m16n8k8_tf32(za[m][2], al, bh0, bh1);
+        }
+      }
+      float* zp = s_zp + warp * kMT * 8;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int r0 = 16 * m + g, r1 = r0 + 8;
+        float s[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s[u] = za[m][0][u] + (za[m][1][u] + za[m][2][u]);
+        *reinterpret_cast<float2*>(zp + r0 * 8 + 2 * t) = make_float2(s[0], s[1]);
+        *reinterpret_cast<float2*>(zp + r1 * 8 + 2 * t) = make_float2(s[2], s[3]);
+      }
     }
     __syncthreads();
 
-    // ---------------------------------------------------------------- softmax, loss, dz
+    // ------------------------------------------------ softmax, loss, dz (thread = position)
     float lossv = 0.f;
-    if (kh == 0) {
-      const int nl = p.nlab[img];
+    if (tid < kMT) {
+      float z[8];
 #pragma unroll
-      for (int hr = 0; hr < 2; ++hr) {
-        const int row = hr ? r1 : r0;
-        const float2 zp = *reinterpret_cast<const float2*>(s_zp + row * 8 + 2 * t);
-        const float za = z[2 * hr] + zp.x + bl0, zb = z[2 * hr + 1] + zp.y + bl1;
-        const int ca = 2 * t, cb = 2 * t + 1;
-        float m = fmaxf(ca < C ? za : -INFINITY, cb < C ? zb : -INFINITY);
-        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
-        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
-        float se = (ca < C ? expf(za - m) : 0.f) + (cb < C ? expf(zb - m) : 0.f);
-        se += __shfl_xor_sync(0xffffffffu, se, 1);
-        se += __shfl_xor_sync(0xffffffffu, se, 2);
-        const float lse = m + logf(se);
-        const int lab = s_lab[row];
-        const bool active = lab >= 0 && lab < C;
-        float da = 0.f, db = 0.f;
-        if (active) {
-          const float wt = p.cw[lab];
-          const float inv = nl > 0 ? wt / (float)nl : 0.f;
-          if (ca < C) da = inv * (expf(za - lse) - (ca == lab ? 1.f : 0.f));
-          if (cb < C) db = inv * (expf(zb - lse) - (cb == lab ? 1.f : 0.f));
-          if (ca == lab) lossv += wt * (lse - za);
-          if (cb == lab) lossv += wt * (lse - zb);
-        }
-        *reinterpret_cast<float2*>(s_dz + row * 8 + 2 * t) = make_float2(da, db);
-        accL[0] += da;
-        accL[1] += db;
+      for (int c = 0; c < 8; ++c) z[c] = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {  // fixed order over the K partials
+        const float4 a = *reinterpret_cast<const float4*>(s_zp + (w * kMT + tid) * 8);
+        const float4 b = *reinterpret_cast<const float4*>(s_zp + (w * kMT + tid) * 8 + 4);
+        z[0] += a.x; z[1] += a.y; z[2] += a.z; z[3] += a.w;
+        z[4] += b.x; z[5] += b.y; z[6] += b.z; z[7] += b.w;
       }
+      float m = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        z[c] += blc[c];
+        if (c < C) m = fmaxf(m, z[c]);
+      }
+      float se = 0.f;
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < C) se += expf(z[c] - m);
+      const float lse = m + logf(se);
+      const int lab = s_lab[tid];
+      float d[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) d[c] = 0.f;
+      if (lab >= 0 && lab < C) {
+        const int nl = p.nlab[img];
+        const float wt = p.cw[lab];
+        const float inv = nl > 0 ? wt / (float)nl : 0.f;
+        float zt = 0.f;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if (c < C) d[c] = inv * (expf(z[c] - lse) - (c == lab ? 1.f : 0.f));
+          if (c == lab) zt = z[c];
+        }
+        lossv = wt * (lse - zt);
+      }
+      *reinterpret_cast<float4*>(s_dz + tid * 8) = make_float4(d[0], d[1], d[2], d[3]);
+      *reinterpret_cast<float4*>(s_dz + tid * 8 + 4) = make_float4(d[4], d[5], d[6], d[7]);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) accL[c] += d[c];
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) lossv += __shfl_xor_sync(0xffffffffu, lossv, o);
     if (lane == 0) p.loss_part[((long long)img * p.tpi + tt) * (kMThr / 32) + warp] = lossv;
-    __syncthreads();  // dz complete
+    if (tid == 0) ptx::bulk_wait_read<0>();  // the previous tile's dh store has read the dh tile
+    __syncthreads();  // dz complete; the dh tile is free
 
-    // ---------------------------------------------------------------- GEMM3: dW_L^T += h^T dz
-    // warp: channel tiles w and w + 8 (channels 16 mt3 + g, + 8), K = the 64 positions
-#pragma unroll 2
-    for (int kst = 0; kst < kMT / 8; ++kst) {
-      const int k0 = 8 * kst;
-      uint32_t bh0, bo0, bh1, bo1;
-      split3(s_dz[(k0 + t) * 8 + g], bh0, bo0);
-      split3(s_dz[(k0 + t + 4) * 8 + g], bh1, bo1);
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int mt3 = warp + 8 * j;
-        if (mt3 >= p.nmt3) break;  // warp-uniform
-        const int c0 = 16 * mt3 + g, c1 = c0 + 8;
-        uint32_t ah[4], al[4];
-        split3(*reinterpret_cast<const float*>(hb + swz(k0 + t, c0)), ah[0], al[0]);
-        split3(*reinterpret_cast<const float*>(hb + swz(k0 + t, c1)), ah[1], al[1]);
-        split3(*reinterpret_cast<const float*>(hb + swz(k0 + t + 4, c0)), ah[2], al[2]);
-        split3(*reinterpret_cast<const float*>(hb + swz(k0 + t + 4, c1)), ah[3], al[3]);
-        ptx::mma_m16n8k8_tf32(accW[j], ah, bh0, bh1);
-        ptx::mma_m16n8k8_tf32(accW[j], ah, bo0, bo1);
-        ptx::mma_m16n8k8_tf32(accW[j], al, bh0, bh1);
-      }
-    }
-    // refill: the dh store of the previous tile (this stage's predecessor in the ring) has
-    // had two phases to read its source; tile it + 2 goes into that stage
-    if (tid == 0) {
-      ptx::bulk_wait_read<0>();
-      const long long nt2 = tile + 2LL * gridDim.x;
-      if (nt2 < p.total) issue(nt2, (it + 2) % kMStages);
-    }
-    __syncthreads();  // GEMM3 has read every h before GEMM2 overwrites it with dh
-
-    // ---------------------------------------------------------------- GEMM2: dh = dz W_L, act'
+    // ------------------------------------------------ GEMM3 (dW_L^T += h^T dz) and GEMM2 (dh)
+    // interleaved: step kst does one K step of GEMM3 for the warp's two channel tiles and two
+    // of the warp's (N-tile, M-tile) units of GEMM2, so independent MMA chains overlap
     uint32_t adh[4][4], adl[4][4];
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
@@ -273,41 +278,63 @@ __global__ void __launch_bounds__(kMThr, 1)
       split3(s_dz[q1 * 8 + t + 4], adh[m][3], adl[m][3]);
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int nt = warp + 8 * j;
-      if (nt >= p.nkt) break;  // warp-uniform
-      const int ch = 8 * nt + 2 * t;
+    for (int kst = 0; kst < kMT / 8; ++kst) {
+      {  // GEMM3, positions 8 kst .. 8 kst + 7
+        const int k0 = 8 * kst;
+        uint32_t bh0, bo0, bh1, bo1;
+        split3(s_dz[(k0 + t) * 8 + g], bh0, bo0);
+        split3(s_dz[(k0 + t + 4) * 8 + g], bh1, bo1);
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        float d[4] = {0.f, 0.f, 0.f, 0.f};
-        ptx::mma_m16n8k8_tf32(d, adh[m], bW[j][0], bW[j][1]);
-        ptx::mma_m16n8k8_tf32(d, adh[m], bW[j][2], bW[j][3]);
-        ptx::mma_m16n8k8_tf32(d, adl[m], bW[j][0], bW[j][1]);
-        const int q0 = 16 * m + g, q1 = q0 + 8;
-        float2* h0 = reinterpret_cast<float2*>(hb + swz(q0, ch));
-        float2* h1 = reinterpret_cast<float2*>(hb + swz(q1, ch));
-        const float2 hv0 = *h0, hv1 = *h1;
-        const int la = s_lab[q0], lb = s_lab[q1];
-        const bool a0 = la >= 0 && la < C, a1 = lb >= 0 && lb < C;
-        float e[4];
-        e[0] = a0 ? d[0] * (TANH ? fmaf(-hv0.x, hv0.x, 1.f) : act_der_m(p.act, hv0.x)) : 0.f;
-        e[1] = a0 ? d[1] * (TANH ? fmaf(-hv0.y, hv0.y, 1.f) : act_der_m(p.act, hv0.y)) : 0.f;
-        e[2] = a1 ? d[2] * (TANH ? fmaf(-hv1.x, hv1.x, 1.f) : act_der_m(p.act, hv1.x)) : 0.f;
-        e[3] = a1 ? d[3] * (TANH ? fmaf(-hv1.y, hv1.y, 1.f) : act_der_m(p.act, hv1.y)) : 0.f;
-        accP[j][0] += e[0] + e[2];
-        accP[j][1] += e[1] + e[3];
-        if (p.round) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) e[u] = tf32_rn_sat(e[u]);
+        for (int j = 0; j < 2; ++j) {
+          const int mt3 = warp + 8 * j;
+          if (mt3 < p.nmt3) {  // warp-uniform
+            const int c0 = 16 * mt3 + g, c1 = c0 + 8;
+            uint32_t ah[4], al[4];
+            split3(*reinterpret_cast<const float*>(hb + swz(k0 + t, c0)), ah[0], al[0]);
+            split3(*reinterpret_cast<const float*>(hb + swz(k0 + t, c1)), ah[1], al[1]);
+            split3(*reinterpret_cast<const float*>(hb + swz(k0 + t + 4, c0)), ah[2], al[2]);
+            split3(*reinterpret_cast<const float*>(hb + swz(k0 + t + 4, c1)), ah[3], al[3]);
+            ptx::mma_m16n8k8_tf32(accW[j][0], ah, bh0, bh1);
+            ptx::mma_m16n8k8_tf32(accW[j][1], ah, bo0, bo1);
+            ptx::mma_m16n8k8_tf32(accW[j][2], al, bh0, bh1);
+          }
         }
-        *h0 = make_float2(e[0], e[1]);
-        *h1 = make_float2(e[2], e[3]);
+      }
+#pragma unroll
+      for (int uu = 0; uu < 2; ++uu) {  // GEMM2 unit (j, m) = (kst / 2, 2 (kst % 2) + uu)
+        const int j = kst >> 1, m = 2 * (kst & 1) + uu;
+        const int nt = warp + 8 * j;
+        if (nt < p.nkt) {  // warp-uniform
+          const int ch = 8 * nt + 2 * t;
+          float d[4] = {0.f, 0.f, 0.f, 0.f};
+          ptx::mma_m16n8k8_tf32(d, adh[m], bW[j][0], bW[j][1]);
+          ptx::mma_m16n8k8_tf32(d, adh[m], bW[j][2], bW[j][3]);
+          ptx::mma_m16n8k8_tf32(d, adl[m], bW[j][0], bW[j][1]);
+          const int q0 = 16 * m + g, q1 = q0 + 8;
+          const float2 hv0 = *reinterpret_cast<const float2*>(hb + swz(q0, ch));
+          const float2 hv1 = *reinterpret_cast<const float2*>(hb + swz(q1, ch));
+          const int la = s_lab[q0], lb = s_lab[q1];
+          const bool a0 = la >= 0 && la < C, a1 = lb >= 0 && lb < C;
+          float e[4];
+          e[0] = a0 ? d[0] * (TANH ? fmaf(-hv0.x, hv0.x, 1.f) : act_der_m(p.act, hv0.x)) : 0.f;
+          e[1] = a0 ? d[1] * (TANH ? fmaf(-hv0.y, hv0.y, 1.f) : act_der_m(p.act, hv0.y)) : 0.f;
+          e[2] = a1 ? d[2] * (TANH ? fmaf(-hv1.x, hv1.x, 1.f) : act_der_m(p.act, hv1.x)) : 0.f;
+          e[3] = a1 ? d[3] * (TANH ? fmaf(-hv1.y, hv1.y, 1.f) : act_der_m(p.act, hv1.y)) : 0.f;
+          accP[j][0] += e[0] + e[2];
+          accP[j][1] += e[1] + e[3];
+          if (p.round) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) e[u] = tf32_rn_sat(e[u]);
+          }
+          *reinterpret_cast<float2*>(dhb + swz(q0, ch)) = make_float2(e[0], e[1]);
+          *reinterpret_cast<float2*>(dhb + swz(q1, ch)) = make_float2(e[2], e[3]);
+        }
       }
     }
     ptx::fence_proxy_async();  // dh in shared memory is visible to the TMA store
     __syncthreads();
     if (tid == 0) {
-      for (int c = 0; c < p.nchunk; ++c) ptx::tma_store_3d(&tmD, s0 + st * stage_bytes + c * kBoxBytes, 32 * c, p0, img);
+      for (int c = 0; c < p.nchunk; ++c) ptx::tma_store_3d(&tmD, sDh + c * kBoxBytes, 32 * c, p0, img);
       ptx::bulk_commit();
     }
   }
@@ -322,10 +349,13 @@ __global__ void __launch_bounds__(kMThr, 1)
     const int mt3 = warp + 8 * j;
     if (mt3 >= p.nmt3) break;
     const int c0 = 16 * mt3 + g, c1 = c0 + 8, ca = 2 * t, cb = 2 * t + 1;
-    if (ca < C && c0 < Ch) out[ca * Ch + c0] = accW[j][0];
-    if (cb < C && c0 < Ch) out[cb * Ch + c0] = accW[j][1];
-    if (ca < C && c1 < Ch) out[ca * Ch + c1] = accW[j][2];
-    if (cb < C && c1 < Ch) out[cb * Ch + c1] = accW[j][3];
+    float v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = accW[j][0][u] + (accW[j][1][u] + accW[j][2][u]);
+    if (ca < C && c0 < Ch) out[ca * Ch + c0] = v[0];
+    if (cb < C && c0 < Ch) out[cb * Ch + c0] = v[1];
+    if (ca < C && c1 < Ch) out[ca * Ch + c1] = v[2];
+    if (cb < C && c1 < Ch) out[cb * Ch + c1] = v[3];
   }
   // db_prev[ch]: the 8 lanes of equal t hold channels 8 nt + 2t, + 1 (fixed-order butterfly)
 #pragma unroll
@@ -340,29 +370,29 @@ __global__ void __launch_bounds__(kMThr, 1)
       if (g == 0 && nt < p.nkt && ch < Ch) out[C * Ch + C + ch] = v;
     }
   }
-  // db_L[c]: warps 0-3 hold classes 2t, 2t + 1 of their 16 positions per tile
+  // db_L[c]: threads 0-63 hold the eight classes of their positions; fixed-order sum
+  if (tid < kMT) {
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    float v = accL[u];
-    v += __shfl_xor_sync(0xffffffffu, v, 4);
-    v += __shfl_xor_sync(0xffffffffu, v, 8);
-    v += __shfl_xor_sync(0xffffffffu, v, 16);
-    if (kh == 0 && g == 0) s_dbl[warp * 8 + 2 * t + u] = v;
+    for (int c = 0; c < 8; ++c) s_dbl[tid * 8 + c] = accL[c];
   }
   __syncthreads();
-  if (tid < C) out[C * Ch + tid] = ((s_dbl[tid] + s_dbl[8 + tid]) + s_dbl[16 + tid]) + s_dbl[24 + tid];
+  if (tid < C) {
+    float v = 0.f;
+    for (int q = 0; q < kMT; ++q) v += s_dbl[q * 8 + tid];
+    out[C * Ch + tid] = v;
+  }
 }
 
 size_t head_mma_smem(int Ch) {
   const int nchunk = (Ch + 31) / 32;
-  return 1024 + (size_t)kMStages * nchunk * kBoxBytes + 2 * 8 * kWS * 4 + 2 * kMT * 8 * 4 + kMT * 4 + 32 * 4 +
-         kMStages * 8 + 64;
+  return 1024 + (size_t)(kMStages + 1) * nchunk * kBoxBytes + 2 * 8 * kWS * 4 + 8 * kMT * 8 * 4 + kMT * 8 * 4 +
+         kMT * 4 + kMT * 8 * 4 + kMStages * 8 + 64;
 }
 
 }  // namespace
 
 bool head_mma_ok(int C, int Ch, bool train) {
-  return train && C >= 2 && C <= 8 && Ch >= 4 && Ch <= 256 && Ch % 4 == 0;
+  return train && C >= 2 && C <= 8 && Ch >= 4 && Ch <= 224 && Ch % 4 == 0;
 }
 
 int head_mma_grid(long long per_img, int n) {
