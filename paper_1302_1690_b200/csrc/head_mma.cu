@@ -39,7 +39,7 @@ namespace {
 
 constexpr int kMT = 64;          // positions per tile
 constexpr int kMThr = 256;       // 8 warps
-constexpr int kMStages = 2;      // h tiles in flight (plus one dh tile)
+constexpr int kMaxStages = 6;    // h tiles in the ring (stages - 1 loads in flight)
 constexpr int kBoxBytes = kMT * 128;  // one [64 x 32 fp32] SW128 box
 constexpr int kWS = 260;         // row stride of the split W_L copies (conflict-free fragment reads)
 
@@ -57,6 +57,8 @@ struct HeadMmaParams {
   int round;                     // TF32-round dh (operand of the FC1 dgrad / wgrad MMAs)
   float* loss_part;              // [n][tpi][8]
   float* part;                   // [grid][C*Ch + C + Ch]
+  float* dh;                     // [n][per_img][Ch]
+  int n_stages;                  // h tiles in the ring
 };
 
 // byte offset of (row r, channel c) inside a tile: box c/32, TMA SWIZZLE_128B pattern
@@ -79,16 +81,15 @@ __device__ __forceinline__ float act_der_m(int act, float y) {
 
 template <bool TANH>
 __global__ void __launch_bounds__(kMThr, 1)
-    head_mma_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmD, HeadMmaParams p) {
+    head_mma_kernel(const __grid_constant__ CUtensorMap tmH, HeadMmaParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t s0 = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* g0 = smem_raw + (s0 - ptx::smem_u32(smem_raw));  // generic address of s0
   const uint32_t stage_bytes = (uint32_t)p.nchunk * kBoxBytes;
-  // [h stages x2 | dh tile | W_L hi [8][kWS] | W_L lo [8][kWS] | z partials [8 warps][64][8] |
-  //  dz [64][8] | lab [64] | db_L partials [64][8] | bars]
-  const uint32_t sDh = s0 + kMStages * stage_bytes;
-  uint8_t* dhb = g0 + kMStages * stage_bytes;
-  uint32_t* s_whi = reinterpret_cast<uint32_t*>(dhb + stage_bytes);
+  // [h stages | W_L hi [8][kWS] | W_L lo [8][kWS] | z partials [8 warps][64][8] | dz [64][8] |
+  //  lab [64] | db_L partials [64][8] | bars]
+  const int S = p.n_stages;
+  uint32_t* s_whi = reinterpret_cast<uint32_t*>(g0 + S * stage_bytes);
   uint32_t* s_wlo = s_whi + 8 * kWS;
   float* s_zp = reinterpret_cast<float*>(s_wlo + 8 * kWS);
   float* s_dz = s_zp + 8 * kMT * 8;
@@ -109,8 +110,7 @@ __global__ void __launch_bounds__(kMThr, 1)
   }
   if (tid == 0) {
     ptx::prefetch_tmap(&tmH);
-    ptx::prefetch_tmap(&tmD);
-    for (int s = 0; s < kMStages; ++s) ptx::mbar_init(ptx::smem_u32(&bars[s]), 1);
+    for (int s = 0; s < S; ++s) ptx::mbar_init(ptx::smem_u32(&bars[s]), 1);
     ptx::fence_mbar_init();
   }
   __syncthreads();
@@ -128,7 +128,11 @@ __global__ void __launch_bounds__(kMThr, 1)
     const long long pos = (long long)(tile % p.tpi) * kMT + tid;
     return pos < p.per_img ? (int)__ldg(p.lab_frag + (long long)img * p.per_img + pos) : kLabBeyond;
   };
-  if (tid == 0 && blockIdx.x < p.total) issue(blockIdx.x, 0);
+  if (tid == 0)
+    for (int s = 0; s + 1 < S; ++s) {  // S - 1 tiles in flight
+      const long long tile = blockIdx.x + (long long)s * gridDim.x;
+      if (tile < p.total) issue(tile, s);
+    }
   int lab_next = tid < kMT ? fetch_label(blockIdx.x) : kLabBeyond;
 
   // GEMM2's B fragments (constant): N-tiles nt = warp + 8 j; b0 = W[t][8 nt + g], b1 = W[t + 4][8 nt + g]
@@ -161,15 +165,18 @@ __global__ void __launch_bounds__(kMThr, 1)
 
   int it = 0;
   for (long long tile = blockIdx.x; tile < p.total; tile += gridDim.x, ++it) {
-    const int st = it & 1;
+    const int st = it % S;
     const int img = (int)(tile / p.tpi), tt = (int)(tile % p.tpi), p0 = tt * kMT;
     if (tid < kMT) {
       s_lab[tid] = lab_next == kLabFragPad ? kLabPad : lab_next;
       lab_next = fetch_label(tile + gridDim.x);  // in flight during this tile
     }
-    ptx::mbar_wait(ptx::smem_u32(&bars[st]), (uint32_t)((it >> 1) & 1));
-    __syncthreads();  // labels and h visible; the other stage's h is no longer read
-    if (tid == 0 && tile + gridDim.x < p.total) issue(tile + gridDim.x, st ^ 1);
+    ptx::mbar_wait(ptx::smem_u32(&bars[st]), (uint32_t)((it / S) & 1));
+    __syncthreads();  // labels and h visible; the previous tile's stage is no longer read
+    if (tid == 0) {  // refill that stage with the tile S - 1 ahead
+      const long long nt = tile + (long long)(S - 1) * gridDim.x;
+      if (nt < p.total) issue(nt, (it + S - 1) % S);
+    }
     const uint8_t* hb = g0 + st * stage_bytes;
 
     // ------------------------------------------------ GEMM1: partial logits, K split over warps
@@ -262,12 +269,15 @@ __global__ void __launch_bounds__(kMThr, 1)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) lossv += __shfl_xor_sync(0xffffffffu, lossv, o);
     if (lane == 0) p.loss_part[((long long)img * p.tpi + tt) * (kMThr / 32) + warp] = lossv;
-    if (tid == 0) ptx::bulk_wait_read<0>();  // the previous tile's dh store has read the dh tile
-    __syncthreads();  // dz complete; the dh tile is free
+    __syncthreads();  // dz complete
 
     // ------------------------------------------------ GEMM3 (dW_L^T += h^T dz) and GEMM2 (dh)
     // interleaved: step kst does one K step of GEMM3 for the warp's two channel tiles and two
-    // of the warp's (N-tile, M-tile) units of GEMM2, so independent MMA chains overlap
+    // of the warp's (N-tile, M-tile) units of GEMM2, so independent MMA chains overlap.  dh
+    // goes straight to global memory (each fragment row is one full 32-byte sector), so no
+    // shared memory waits on a store and every stage is free for loads in flight.
+    float* dh_img = p.dh + ((long long)img * p.per_img + p0) * Ch;
+    const int nrow = (int)min((long long)kMT, p.per_img - p0);
     uint32_t adh[4][4], adl[4][4];
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
@@ -326,19 +336,14 @@ __global__ void __launch_bounds__(kMThr, 1)
 #pragma unroll
             for (int u = 0; u < 4; ++u) e[u] = tf32_rn_sat(e[u]);
           }
-          *reinterpret_cast<float2*>(dhb + swz(q0, ch)) = make_float2(e[0], e[1]);
-          *reinterpret_cast<float2*>(dhb + swz(q1, ch)) = make_float2(e[2], e[3]);
+          if (ch < Ch) {
+            if (q0 < nrow) *reinterpret_cast<float2*>(dh_img + (long long)q0 * Ch + ch) = make_float2(e[0], e[1]);
+            if (q1 < nrow) *reinterpret_cast<float2*>(dh_img + (long long)q1 * Ch + ch) = make_float2(e[2], e[3]);
+          }
         }
       }
     }
-    ptx::fence_proxy_async();  // dh in shared memory is visible to the TMA store
-    __syncthreads();
-    if (tid == 0) {
-      for (int c = 0; c < p.nchunk; ++c) ptx::tma_store_3d(&tmD, sDh + c * kBoxBytes, 32 * c, p0, img);
-      ptx::bulk_commit();
-    }
   }
-  if (tid == 0) ptx::bulk_wait<0>();
 
   // ------------------------------------------------------------------ block partials
   const int E = C * Ch + C + Ch;
@@ -383,16 +388,20 @@ __global__ void __launch_bounds__(kMThr, 1)
   }
 }
 
-size_t head_mma_smem(int Ch) {
-  const int nchunk = (Ch + 31) / 32;
-  return 1024 + (size_t)(kMStages + 1) * nchunk * kBoxBytes + 2 * 8 * kWS * 4 + 8 * kMT * 8 * 4 + kMT * 8 * 4 +
-         kMT * 4 + kMT * 8 * 4 + kMStages * 8 + 64;
+size_t head_mma_fixed_smem() {
+  return 1024 + 2 * 8 * kWS * 4 + 8 * kMT * 8 * 4 + kMT * 8 * 4 + kMT * 4 + kMT * 8 * 4 + kMaxStages * 8 + 64;
+}
+// as many h stages as fit (at most kMaxStages): S - 1 tiles of loads in flight per SM
+int head_mma_stages(int Ch) {
+  const size_t stage = (size_t)((Ch + 31) / 32) * kBoxBytes;
+  int s = (int)((225 * 1024 - head_mma_fixed_smem()) / stage);
+  return s > kMaxStages ? kMaxStages : s;
 }
 
 }  // namespace
 
 bool head_mma_ok(int C, int Ch, bool train) {
-  return train && C >= 2 && C <= 8 && Ch >= 4 && Ch <= 224 && Ch % 4 == 0;
+  return train && C >= 2 && C <= 8 && Ch >= 4 && Ch <= 256 && Ch % 4 == 0 && head_mma_stages(Ch) >= 3;
 }
 
 int head_mma_grid(long long per_img, int n) {
@@ -420,21 +429,22 @@ cudaError_t launch_head_mma(const HeadArgs& a, cudaStream_t s) {
   p.round = a.round_tf32;
   p.loss_part = a.loss_part;
   p.part = a.part;
+  p.dh = a.dh;
+  p.n_stages = head_mma_stages(a.Ch);
+  if (p.n_stages < 3) return cudaErrorInvalidConfiguration;
   if (a.tiles_per_img != p.tpi || !a.lab_frag) return cudaErrorInvalidValue;
-  CUtensorMap H, D;
+  CUtensorMap H;
   const uint64_t dims[3] = {(uint64_t)a.Ch, (uint64_t)p.per_img, (uint64_t)a.n};
   const uint64_t strides[2] = {(uint64_t)a.Ch * 4, (uint64_t)p.per_img * a.Ch * 4};
   const uint32_t box[3] = {32, kMT, 1};
   cudaError_t e = make_tmap_f32(&H, a.h, 3, dims, strides, box, true);
   if (e != cudaSuccess) return e;
-  e = make_tmap_f32(&D, a.dh, 3, dims, strides, box, true);
-  if (e != cudaSuccess) return e;
-  const size_t smem = head_mma_smem(a.Ch);
+  const size_t smem = head_mma_fixed_smem() + (size_t)p.n_stages * p.nchunk * kBoxBytes;
   const int grid = a.n_blocks;
   auto kern = a.hidden_act == MPF_TANH ? head_mma_kernel<true> : head_mma_kernel<false>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<grid, kMThr, smem, s>>>(H, D, p);
+  kern<<<grid, kMThr, smem, s>>>(H, p);
   return cudaGetLastError();
 }
 
