@@ -66,11 +66,13 @@ __device__ __forceinline__ uint32_t swz(int r, int c) {
   return (uint32_t)((c >> 5) * kBoxBytes + r * 128 + ((((c & 31) >> 2) ^ (r & 7)) << 4) + ((c & 3) << 2));
 }
 
-// 3xTF32 split: x = hi + lo (exact), both as TF32 operands
+// 3xTF32 split: x = hi + lo, hi the TF32 rounding of x (one F2FP), lo = x - hi exactly in
+// fp32 (the MMA reads only its top 19 bits: the dropped part is ~2^-22 |x|).  Non-finite
+// inputs give non-finite products (NaN stays NaN; Inf becomes MAX_TF32 + Inf in lo).
 __device__ __forceinline__ void split3(float x, uint32_t& hi, uint32_t& lo) {
-  const float h = tf32_rn(x);
+  const float h = tf32_rn_sat(x);
   hi = __float_as_uint(h);
-  lo = __float_as_uint(tf32_rn(x - h));
+  lo = __float_as_uint(x - h);
 }
 
 __device__ __forceinline__ float act_der_m(int act, float y) {
@@ -79,7 +81,7 @@ __device__ __forceinline__ float act_der_m(int act, float y) {
   return 1.f;
 }
 
-template <bool TANH>
+template <bool TANH, bool X3>
 __global__ void __launch_bounds__(kMThr, 1)
     head_mma_kernel(const __grid_constant__ CUtensorMap tmH, HeadMmaParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -204,8 +206,10 @@ __global__ void __launch_bounds__(kMThr, 1)
           split3(*reinterpret_cast<const float*>(hb + swz(r0, k0 + t + 4)), ah[2], al[2]);
           split3(*reinterpret_cast<const float*>(hb + swz(r1, k0 + t + 4)), ah[3], al[3]);
           ptx::mma_m16n8k8_tf32(za[m][0], ah, bh0, bh1);
-          ptx::mma_m16n8k8_tf32(za[m][1], ah, bo0, bo1);
-          ptx::mma_m16n8k8_tf32(za[m][2], al, bh0, bh1);
+          if (X3) {
+            ptx::mma_m16n8k8_tf32(za[m][1], ah, bo0, bo1);
+            ptx::mma_m16n8k8_tf32(za[m][2], al, bh0, bh1);
+          }
         }
       }
       float* zp = s_zp + warp * kMT * 8;
@@ -305,8 +309,10 @@ __global__ void __launch_bounds__(kMThr, 1)
             split3(*reinterpret_cast<const float*>(hb + swz(k0 + t + 4, c0)), ah[2], al[2]);
             split3(*reinterpret_cast<const float*>(hb + swz(k0 + t + 4, c1)), ah[3], al[3]);
             ptx::mma_m16n8k8_tf32(accW[j][0], ah, bh0, bh1);
-            ptx::mma_m16n8k8_tf32(accW[j][1], ah, bo0, bo1);
-            ptx::mma_m16n8k8_tf32(accW[j][2], al, bh0, bh1);
+            if (X3) {
+              ptx::mma_m16n8k8_tf32(accW[j][1], ah, bo0, bo1);
+              ptx::mma_m16n8k8_tf32(accW[j][2], al, bh0, bh1);
+            }
           }
         }
       }
@@ -318,8 +324,10 @@ __global__ void __launch_bounds__(kMThr, 1)
           const int ch = 8 * nt + 2 * t;
           float d[4] = {0.f, 0.f, 0.f, 0.f};
           ptx::mma_m16n8k8_tf32(d, adh[m], bW[j][0], bW[j][1]);
-          ptx::mma_m16n8k8_tf32(d, adh[m], bW[j][2], bW[j][3]);
-          ptx::mma_m16n8k8_tf32(d, adl[m], bW[j][0], bW[j][1]);
+          if (X3) {
+            ptx::mma_m16n8k8_tf32(d, adh[m], bW[j][2], bW[j][3]);
+            ptx::mma_m16n8k8_tf32(d, adl[m], bW[j][0], bW[j][1]);
+          }
           const int q0 = 16 * m + g, q1 = q0 + 8;
           const float2 hv0 = *reinterpret_cast<const float2*>(hb + swz(q0, ch));
           const float2 hv1 = *reinterpret_cast<const float2*>(hb + swz(q1, ch));
@@ -441,7 +449,9 @@ cudaError_t launch_head_mma(const HeadArgs& a, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   const size_t smem = head_mma_fixed_smem() + (size_t)p.n_stages * p.nchunk * kBoxBytes;
   const int grid = a.n_blocks;
-  auto kern = a.hidden_act == MPF_TANH ? head_mma_kernel<true> : head_mma_kernel<false>;
+  const bool x3 = !a.head_1x;
+  auto kern = a.hidden_act == MPF_TANH ? (x3 ? head_mma_kernel<true, true> : head_mma_kernel<true, false>)
+                                       : (x3 ? head_mma_kernel<false, true> : head_mma_kernel<false, false>);
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<grid, kMThr, smem, s>>>(H, p);
