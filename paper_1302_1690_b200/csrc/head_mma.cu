@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include "conv_tc.h"
 #include "head_common.cuh"
@@ -59,6 +60,7 @@ struct HeadMmaParams {
   float* part;                   // [grid][C*Ch + C + Ch]
   float* dh;                     // [n][per_img][Ch]
   int n_stages;                  // h tiles in the ring
+  unsigned long long* prof;      // optional phase cycle counters (MPF_FLAG_ROLE_TIMERS)
 };
 
 // byte offset of (row r, channel c) inside a tile: box c/32, TMA SWIZZLE_128B pattern
@@ -166,6 +168,15 @@ __global__ void __launch_bounds__(kMThr, 1)
   for (int c = 0; c < 8; ++c) blc[c] = c < C ? p.bL[c] : 0.f;
 
   int it = 0;
+  unsigned long long pc[6] = {0, 0, 0, 0, 0, 0};
+  long long tq = clock64();
+  auto tick = [&](int i) {
+    if (p.prof) {
+      const long long t2 = clock64();
+      pc[i] += (unsigned long long)(t2 - tq);
+      tq = t2;
+    }
+  };
   for (long long tile = blockIdx.x; tile < p.total; tile += gridDim.x, ++it) {
     const int st = it % S;
     const int img = (int)(tile / p.tpi), tt = (int)(tile % p.tpi), p0 = tt * kMT;
@@ -173,8 +184,11 @@ __global__ void __launch_bounds__(kMThr, 1)
       s_lab[tid] = lab_next == kLabFragPad ? kLabPad : lab_next;
       lab_next = fetch_label(tile + gridDim.x);  // in flight during this tile
     }
+    tick(5);
     ptx::mbar_wait(ptx::smem_u32(&bars[st]), (uint32_t)((it / S) & 1));
+    tick(0);
     __syncthreads();  // labels and h visible; the previous tile's stage is no longer read
+    tick(1);
     if (tid == 0) {  // refill that stage with the tile S - 1 ahead
       const long long nt = tile + (long long)(S - 1) * gridDim.x;
       if (nt < p.total) issue(nt, (it + S - 1) % S);
@@ -223,7 +237,9 @@ __global__ void __launch_bounds__(kMThr, 1)
         *reinterpret_cast<float2*>(zp + r1 * 8 + 2 * t) = make_float2(s[2], s[3]);
       }
     }
+    tick(2);
     __syncthreads();
+    tick(1);
 
     // ------------------------------------------------ softmax, loss, dz (thread = position)
     float lossv = 0.f;
@@ -273,7 +289,9 @@ __global__ void __launch_bounds__(kMThr, 1)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) lossv += __shfl_xor_sync(0xffffffffu, lossv, o);
     if (lane == 0) p.loss_part[((long long)img * p.tpi + tt) * (kMThr / 32) + warp] = lossv;
+    tick(3);
     __syncthreads();  // dz complete
+    tick(1);
 
     // ------------------------------------------------ GEMM3 (dW_L^T += h^T dz) and GEMM2 (dh)
     // interleaved: step kst does one K step of GEMM3 for the warp's two channel tiles and two
@@ -353,6 +371,9 @@ __global__ void __launch_bounds__(kMThr, 1)
     }
   }
 
+  tick(4);
+  if (p.prof)
+    for (int i = 0; i < 6; ++i) atomicAdd(p.prof + i, pc[i]);
   // ------------------------------------------------------------------ block partials
   const int E = C * Ch + C + Ch;
   float* out = p.part + (size_t)blockIdx.x * E;
@@ -454,7 +475,20 @@ cudaError_t launch_head_mma(const HeadArgs& a, cudaStream_t s) {
                                        : (x3 ? head_mma_kernel<false, true> : head_mma_kernel<false, false>);
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  static unsigned long long* prof = nullptr;
+  if (a.prof_on) {
+    if (!prof) cudaMalloc(&prof, 8 * sizeof(unsigned long long));
+    cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), s);
+    p.prof = prof;
+  }
   kern<<<grid, kMThr, smem, s>>>(H, p);
+  if (a.prof_on) {
+    unsigned long long h[8];
+    cudaMemcpy(h, prof, sizeof(h), cudaMemcpyDeviceToHost);
+    const double d = (double)grid * kMThr;
+    fprintf(stderr, "[head-prof] Ch=%d tiles=%lld grid=%d stages=%d | per thread Mcyc: wait %.3f sync %.3f gemm1 %.3f softmax %.3f gemm32 %.3f top %.3f\n",
+            a.Ch, p.total, grid, p.n_stages, h[0] / d / 1e6, h[1] / d / 1e6, h[2] / d / 1e6, h[3] / d / 1e6, h[4] / d / 1e6, h[5] / d / 1e6);
+  }
   return cudaGetLastError();
 }
 

@@ -709,6 +709,7 @@ static mpf_status backward_impl(Net* N, const uint8_t* d_labels, const float* h_
     hd.lab_frag = labf;
     if (head_mma_ok(N->classes, h.C, true) && !(N->cfg.flags & MPF_FLAG_HEAD_FMA)) {  // the three head contractions on mma.sync (3xTF32)
       hd.head_1x = (N->cfg.flags & (1u << 9)) ? 1 : 0;
+      hd.prof_on = (N->cfg.flags & MPF_FLAG_ROLE_TIMERS) ? 1 : 0;
       hd.n_blocks = head_mma_grid((long long)h.F * h.gr * h.gc, n);
       LAUNCH(N, s, "head_loss_delta", L, 6.0 * pos * h.C * N->classes, pos * (8.0 * h.C + 1.0),
              launch_head_mma(hd, s));
