@@ -39,7 +39,7 @@ namespace mpf {
 namespace {
 
 constexpr int kMT = 64;          // positions per tile
-constexpr int kMThr = 256;       // 8 warps
+constexpr int kMThr = 512;       // 16 warps
 constexpr int kMaxStages = 6;    // h tiles in the ring (stages - 1 loads in flight)
 constexpr int kBoxBytes = kMT * 128;  // one [64 x 32 fp32] SW128 box
 constexpr int kWS = 260;         // row stride of the split W_L copies (conflict-free fragment reads)
@@ -60,7 +60,6 @@ struct HeadMmaParams {
   float* part;                   // [grid][C*Ch + C + Ch]
   float* dh;                     // [n][per_img][Ch]
   int n_stages;                  // h tiles in the ring
-  unsigned long long* prof;      // optional phase cycle counters (MPF_FLAG_ROLE_TIMERS)
 };
 
 // byte offset of (row r, channel c) inside a tile: box c/32, TMA SWIZZLE_128B pattern
@@ -83,23 +82,24 @@ __device__ __forceinline__ float act_der_m(int act, float y) {
   return 1.f;
 }
 
-template <bool TANH, bool X3>
-__global__ void __launch_bounds__(kMThr, 1)
-    head_mma_kernel(const __grid_constant__ CUtensorMap tmH, HeadMmaParams p) {
+template <bool TANH>
+__global__ void __launch_bounds__(kMThr, 1) head_mma_kernel(const __grid_constant__ CUtensorMap tmH, HeadMmaParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t s0 = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* g0 = smem_raw + (s0 - ptx::smem_u32(smem_raw));  // generic address of s0
   const uint32_t stage_bytes = (uint32_t)p.nchunk * kBoxBytes;
-  // [h stages | W_L hi [8][kWS] | W_L lo [8][kWS] | z partials [8 warps][64][8] | dz [64][8] |
-  //  lab [64] | db_L partials [64][8] | bars]
+  // [h stages | W_L hi [8][kWS] | W_L lo [8][kWS] | z partials [4 K-quarters][64][8] | dz [64][8] |
+  //  lab [64] | db_L partials [64][8] | cw [16] | nlab | bars]
   const int S = p.n_stages;
   uint32_t* s_whi = reinterpret_cast<uint32_t*>(g0 + S * stage_bytes);
   uint32_t* s_wlo = s_whi + 8 * kWS;
   float* s_zp = reinterpret_cast<float*>(s_wlo + 8 * kWS);
-  float* s_dz = s_zp + 8 * kMT * 8;
+  float* s_dz = s_zp + 4 * kMT * 8;
   int* s_lab = reinterpret_cast<int*>(s_dz + kMT * 8);
   float* s_dbl = reinterpret_cast<float*>(s_lab + kMT);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_dbl + kMT * 8);
+  float* s_cw = s_dbl + kMT * 8;
+  int* s_nl = reinterpret_cast<int*>(s_cw + 16);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_nl + 2);
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const int g = lane >> 2, t = lane & 3;
@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(kMThr, 1)
     s_whi[c * kWS + ch] = hi;
     s_wlo[c * kWS + ch] = lo;
   }
+  if (tid < 16) s_cw[tid] = p.cw[tid];
   if (tid == 0) {
     ptx::prefetch_tmap(&tmH);
     for (int s = 0; s < S; ++s) ptx::mbar_init(ptx::smem_u32(&bars[s]), 1);
@@ -125,10 +126,12 @@ __global__ void __launch_bounds__(kMThr, 1)
     ptx::mbar_arrive_expect_tx(bar, stage_bytes);
     for (int c = 0; c < p.nchunk; ++c) ptx::tma_load_3d(s0 + st * stage_bytes + c * kBoxBytes, &tmH, bar, 32 * c, p0, img);
   };
-  // label of position tid of a tile, issued one tile ahead (kept in a register)
-  auto fetch_label = [&](long long tile) -> int {
+  // label of position tid of a tile (threads 0-63) and the image's labelled-pixel count
+  // (thread 64), issued one tile ahead and kept in a register
+  auto fetch = [&](long long tile) -> int {
     if (tile >= p.total) return kLabBeyond;
     const int img = (int)(tile / p.tpi);
+    if (tid == kMT) return __ldg(p.nlab + img);
     const long long pos = (long long)(tile % p.tpi) * kMT + tid;
     return pos < p.per_img ? (int)__ldg(p.lab_frag + (long long)img * p.per_img + pos) : kLabBeyond;
   };
@@ -137,146 +140,103 @@ __global__ void __launch_bounds__(kMThr, 1)
       const long long tile = blockIdx.x + (long long)s * gridDim.x;
       if (tile < p.total) issue(tile, s);
     }
-  int lab_next = tid < kMT ? fetch_label(blockIdx.x) : kLabBeyond;
+  int pre = tid <= kMT ? fetch(blockIdx.x) : 0;
 
-  // GEMM2's B fragments (constant): N-tiles nt = warp + 8 j; b0 = W[t][8 nt + g], b1 = W[t + 4][8 nt + g]
-  uint32_t bW[4][4];
+  // GEMM2's B fragments (constant): N-tiles nt = warp + 16 j; b0 = W[t][8 nt + g], b1 = W[t + 4][8 nt + g]
+  uint32_t bW[2][4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int ch = 8 * (warp + 8 * j) + g;
-    const bool ok = ch < 256;
-    bW[j][0] = ok ? s_whi[t * kWS + ch] : 0u;
-    bW[j][1] = ok ? s_whi[(t + 4) * kWS + ch] : 0u;
-    bW[j][2] = ok ? s_wlo[t * kWS + ch] : 0u;
-    bW[j][3] = ok ? s_wlo[(t + 4) * kWS + ch] : 0u;
+  for (int j = 0; j < 2; ++j) {
+    const int ch = 8 * (warp + 16 * j) + g;
+    bW[j][0] = s_whi[t * kWS + ch];
+    bW[j][1] = s_whi[(t + 4) * kWS + ch];
+    bW[j][2] = s_wlo[t * kWS + ch];
+    bW[j][3] = s_wlo[(t + 4) * kWS + ch];
   }
-  // accumulators living across tiles: dW_L^T (two 16-channel tiles x three split products),
-  // db_prev (four 8-channel tiles x two channels), db_L (threads 0-63: eight classes)
-  float accW[2][3][4], accP[4][2], accL[8];
-#pragma unroll
-  for (int j = 0; j < 2; ++j)
-#pragma unroll
-    for (int q = 0; q < 3; ++q)
-#pragma unroll
-      for (int u = 0; u < 4; ++u) accW[j][q][u] = 0.f;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) accP[j][0] = accP[j][1] = 0.f;
+  // accumulators living across tiles: dW_L^T of channel tile `warp`, db_prev of the warp's two
+  // 8-channel tiles, db_L (threads 0-63: eight classes)
+  float accW[4] = {0.f, 0.f, 0.f, 0.f}, accP[2][2] = {{0.f, 0.f}, {0.f, 0.f}}, accL[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) accL[c] = 0.f;
   float blc[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) blc[c] = c < C ? p.bL[c] : 0.f;
+  const int mt = warp & 3, kq = warp >> 2;  // GEMM1: M tile, K quarter
 
   int it = 0;
-  unsigned long long pc[6] = {0, 0, 0, 0, 0, 0};
-  long long tq = clock64();
-  auto tick = [&](int i) {
-    if (p.prof) {
-      const long long t2 = clock64();
-      pc[i] += (unsigned long long)(t2 - tq);
-      tq = t2;
-    }
-  };
   for (long long tile = blockIdx.x; tile < p.total; tile += gridDim.x, ++it) {
     const int st = it % S;
     const int img = (int)(tile / p.tpi), tt = (int)(tile % p.tpi), p0 = tt * kMT;
-    if (tid < kMT) {
-      s_lab[tid] = lab_next == kLabFragPad ? kLabPad : lab_next;
-      lab_next = fetch_label(tile + gridDim.x);  // in flight during this tile
-    }
-    tick(5);
+    if (tid < kMT) s_lab[tid] = pre == kLabFragPad ? kLabPad : pre;
+    if (tid == kMT) s_nl[0] = pre;
+    if (tid <= kMT) pre = fetch(tile + gridDim.x);  // in flight during this tile
     ptx::mbar_wait(ptx::smem_u32(&bars[st]), (uint32_t)((it / S) & 1));
-    tick(0);
     __syncthreads();  // labels and h visible; the previous tile's stage is no longer read
-    tick(1);
     if (tid == 0) {  // refill that stage with the tile S - 1 ahead
       const long long nt = tile + (long long)(S - 1) * gridDim.x;
       if (nt < p.total) issue(nt, (it + S - 1) % S);
     }
     const uint8_t* hb = g0 + st * stage_bytes;
 
-    // ------------------------------------------------ GEMM1: partial logits, K split over warps
+    // ------------------------------------------------ GEMM1: partial logits (M tile x K quarter)
     {
-      float za[4][3][4];
-#pragma unroll
-      for (int m = 0; m < 4; ++m)
-#pragma unroll
-        for (int q = 0; q < 3; ++q)
-#pragma unroll
-          for (int u = 0; u < 4; ++u) za[m][q][u] = 0.f;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int ks = warp + 8 * i;
-        if (ks >= p.nkt) break;  // warp-uniform
+      float za[4] = {0.f, 0.f, 0.f, 0.f};
+      const int r0 = 16 * mt + g, r1 = r0 + 8;
+      for (int ks = kq; ks < p.nkt; ks += 4) {
         const int k0 = 8 * ks;
+        uint32_t ah[4], al[4];
+        split3(*reinterpret_cast<const float*>(hb + swz(r0, k0 + t)), ah[0], al[0]);
+        split3(*reinterpret_cast<const float*>(hb + swz(r1, k0 + t)), ah[1], al[1]);
+        split3(*reinterpret_cast<const float*>(hb + swz(r0, k0 + t + 4)), ah[2], al[2]);
+        split3(*reinterpret_cast<const float*>(hb + swz(r1, k0 + t + 4)), ah[3], al[3]);
         const uint32_t bh0 = s_whi[g * kWS + k0 + t], bh1 = s_whi[g * kWS + k0 + t + 4];
         const uint32_t bo0 = s_wlo[g * kWS + k0 + t], bo1 = s_wlo[g * kWS + k0 + t + 4];
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          const int r0 = 16 * m + g, r1 = r0 + 8;
-          uint32_t ah[4], al[4];
-          split3(*reinterpret_cast<const float*>(hb + swz(r0, k0 + t)), ah[0], al[0]);
-          split3(*reinterpret_cast<const float*>(hb + swz(r1, k0 + t)), ah[1], al[1]);
-          split3(*reinterpret_cast<const float*>(hb + swz(r0, k0 + t + 4)), ah[2], al[2]);
-          split3(*reinterpret_cast<const float*>(hb + swz(r1, k0 + t + 4)), ah[3], al[3]);
-          ptx::mma_m16n8k8_tf32(za[m][0], ah, bh0, bh1);
-          if (X3) {
-            ptx::mma_m16n8k8_tf32(za[m][1], ah, bo0, bo1);
-            ptx::mma_m16n8k8_tf32(za[m][2], al, bh0, bh1);
-          }
-        }
+        ptx::mma_m16n8k8_tf32(za, al, bh0, bh1);
+        ptx::mma_m16n8k8_tf32(za, ah, bo0, bo1);
+        ptx::mma_m16n8k8_tf32(za, ah, bh0, bh1);
       }
-      float* zp = s_zp + warp * kMT * 8;
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int r0 = 16 * m + g, r1 = r0 + 8;
-        float s[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) s[u] = za[m][0][u] + (za[m][1][u] + za[m][2][u]);
-        *reinterpret_cast<float2*>(zp + r0 * 8 + 2 * t) = make_float2(s[0], s[1]);
-        *reinterpret_cast<float2*>(zp + r1 * 8 + 2 * t) = make_float2(s[2], s[3]);
-      }
+      float* zp = s_zp + kq * kMT * 8;
+      *reinterpret_cast<float2*>(zp + r0 * 8 + 2 * t) = make_float2(za[0], za[1]);
+      *reinterpret_cast<float2*>(zp + r1 * 8 + 2 * t) = make_float2(za[2], za[3]);
     }
-    tick(2);
     __syncthreads();
-    tick(1);
 
     // ------------------------------------------------ softmax, loss, dz (thread = position)
     float lossv = 0.f;
     if (tid < kMT) {
       float z[8];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) z[c] = 0.f;
+      for (int c = 0; c < 8; ++c) z[c] = blc[c];
 #pragma unroll
-      for (int w = 0; w < 8; ++w) {  // fixed order over the K partials
-        const float4 a = *reinterpret_cast<const float4*>(s_zp + (w * kMT + tid) * 8);
-        const float4 b = *reinterpret_cast<const float4*>(s_zp + (w * kMT + tid) * 8 + 4);
+      for (int q = 0; q < 4; ++q) {  // fixed order over the K quarters
+        const float4 a = *reinterpret_cast<const float4*>(s_zp + (q * kMT + tid) * 8);
+        const float4 b = *reinterpret_cast<const float4*>(s_zp + (q * kMT + tid) * 8 + 4);
         z[0] += a.x; z[1] += a.y; z[2] += a.z; z[3] += a.w;
         z[4] += b.x; z[5] += b.y; z[6] += b.z; z[7] += b.w;
       }
       float m = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        z[c] += blc[c];
-        if (c < C) m = fmaxf(m, z[c]);
-      }
-      float se = 0.f;
-#pragma unroll
       for (int c = 0; c < 8; ++c)
-        if (c < C) se += expf(z[c] - m);
+        if (c < C) m = fmaxf(m, z[c]);
+      float ex[8], se = 0.f;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        ex[c] = c < C ? expf(z[c] - m) : 0.f;
+        se += ex[c];
+      }
       const float lse = m + logf(se);
       const int lab = s_lab[tid];
       float d[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) d[c] = 0.f;
       if (lab >= 0 && lab < C) {
-        const int nl = p.nlab[img];
-        const float wt = p.cw[lab];
+        const int nl = s_nl[0];
+        const float wt = s_cw[lab];
         const float inv = nl > 0 ? wt / (float)nl : 0.f;
+        const float rs = 1.f / se;
         float zt = 0.f;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          if (c < C) d[c] = inv * (expf(z[c] - lse) - (c == lab ? 1.f : 0.f));
+          if (c < C) d[c] = inv * (ex[c] * rs - (c == lab ? 1.f : 0.f));
           if (c == lab) zt = z[c];
         }
         lossv = wt * (lse - zt);
@@ -286,67 +246,51 @@ __global__ void __launch_bounds__(kMThr, 1)
 #pragma unroll
       for (int c = 0; c < 8; ++c) accL[c] += d[c];
     }
+    if (warp < kMThr / 32 / 2) {  // loss partials: warps 0-1 hold the positions, 2-7 write zeros
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) lossv += __shfl_xor_sync(0xffffffffu, lossv, o);
-    if (lane == 0) p.loss_part[((long long)img * p.tpi + tt) * (kMThr / 32) + warp] = lossv;
-    tick(3);
+      for (int o = 16; o > 0; o >>= 1) lossv += __shfl_xor_sync(0xffffffffu, lossv, o);
+      if (lane == 0) p.loss_part[((long long)img * p.tpi + tt) * 8 + warp] = lossv;
+    }
     __syncthreads();  // dz complete
-    tick(1);
 
     // ------------------------------------------------ GEMM3 (dW_L^T += h^T dz) and GEMM2 (dh)
-    // interleaved: step kst does one K step of GEMM3 for the warp's two channel tiles and two
-    // of the warp's (N-tile, M-tile) units of GEMM2, so independent MMA chains overlap.  dh
-    // goes straight to global memory (each fragment row is one full 32-byte sector), so no
-    // shared memory waits on a store and every stage is free for loads in flight.
+    // interleaved: step kst does one K step of GEMM3 for the warp's channel tile and one of
+    // the warp's (N-tile, M-tile) units of GEMM2, so independent MMA chains overlap.  dh goes
+    // straight to global memory (each fragment row is one full 32-byte sector).
     float* dh_img = p.dh + ((long long)img * p.per_img + p0) * Ch;
     const int nrow = (int)min((long long)kMT, p.per_img - p0);
-    uint32_t adh[4][4], adl[4][4];
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      const int q0 = 16 * m + g, q1 = q0 + 8;
-      split3(s_dz[q0 * 8 + t], adh[m][0], adl[m][0]);
-      split3(s_dz[q1 * 8 + t], adh[m][1], adl[m][1]);
-      split3(s_dz[q0 * 8 + t + 4], adh[m][2], adl[m][2]);
-      split3(s_dz[q1 * 8 + t + 4], adh[m][3], adl[m][3]);
-    }
 #pragma unroll
     for (int kst = 0; kst < kMT / 8; ++kst) {
-      {  // GEMM3, positions 8 kst .. 8 kst + 7
+      if (warp < p.nmt3) {  // GEMM3, positions 8 kst .. 8 kst + 7 (warp-uniform)
         const int k0 = 8 * kst;
         uint32_t bh0, bo0, bh1, bo1;
         split3(s_dz[(k0 + t) * 8 + g], bh0, bo0);
         split3(s_dz[(k0 + t + 4) * 8 + g], bh1, bo1);
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int mt3 = warp + 8 * j;
-          if (mt3 < p.nmt3) {  // warp-uniform
-            const int c0 = 16 * mt3 + g, c1 = c0 + 8;
-            uint32_t ah[4], al[4];
-            split3(*reinterpret_cast<const float*>(hb + swz(k0 + t, c0)), ah[0], al[0]);
-            split3(*reinterpret_cast<const float*>(hb + swz(k0 + t, c1)), ah[1], al[1]);
-            split3(*reinterpret_cast<const float*>(hb + swz(k0 + t + 4, c0)), ah[2], al[2]);
-            split3(*reinterpret_cast<const float*>(hb + swz(k0 + t + 4, c1)), ah[3], al[3]);
-            ptx::mma_m16n8k8_tf32(accW[j][0], ah, bh0, bh1);
-            if (X3) {
-              ptx::mma_m16n8k8_tf32(accW[j][1], ah, bo0, bo1);
-              ptx::mma_m16n8k8_tf32(accW[j][2], al, bh0, bh1);
-            }
-          }
-        }
+        const int c0 = 16 * warp + g, c1 = c0 + 8;
+        uint32_t ah[4], al[4];
+        split3(*reinterpret_cast<const float*>(hb + swz(k0 + t, c0)), ah[0], al[0]);
+        split3(*reinterpret_cast<const float*>(hb + swz(k0 + t, c1)), ah[1], al[1]);
+        split3(*reinterpret_cast<const float*>(hb + swz(k0 + t + 4, c0)), ah[2], al[2]);
+        split3(*reinterpret_cast<const float*>(hb + swz(k0 + t + 4, c1)), ah[3], al[3]);
+        ptx::mma_m16n8k8_tf32(accW, al, bh0, bh1);
+        ptx::mma_m16n8k8_tf32(accW, ah, bo0, bo1);
+        ptx::mma_m16n8k8_tf32(accW, ah, bh0, bh1);
       }
-#pragma unroll
-      for (int uu = 0; uu < 2; ++uu) {  // GEMM2 unit (j, m) = (kst / 2, 2 (kst % 2) + uu)
-        const int j = kst >> 1, m = 2 * (kst & 1) + uu;
-        const int nt = warp + 8 * j;
+      {  // GEMM2 unit (j, m) = (kst / 4, kst % 4)
+        const int j = kst >> 2, m = kst & 3;
+        const int nt = warp + 16 * j;
         if (nt < p.nkt) {  // warp-uniform
-          const int ch = 8 * nt + 2 * t;
-          float d[4] = {0.f, 0.f, 0.f, 0.f};
-          ptx::mma_m16n8k8_tf32(d, adh[m], bW[j][0], bW[j][1]);
-          if (X3) {
-            ptx::mma_m16n8k8_tf32(d, adh[m], bW[j][2], bW[j][3]);
-            ptx::mma_m16n8k8_tf32(d, adl[m], bW[j][0], bW[j][1]);
-          }
           const int q0 = 16 * m + g, q1 = q0 + 8;
+          uint32_t ah[4], al[4];
+          split3(s_dz[q0 * 8 + t], ah[0], al[0]);
+          split3(s_dz[q1 * 8 + t], ah[1], al[1]);
+          split3(s_dz[q0 * 8 + t + 4], ah[2], al[2]);
+          split3(s_dz[q1 * 8 + t + 4], ah[3], al[3]);
+          float d[4] = {0.f, 0.f, 0.f, 0.f};
+          ptx::mma_m16n8k8_tf32(d, al, bW[j][0], bW[j][1]);
+          ptx::mma_m16n8k8_tf32(d, ah, bW[j][2], bW[j][3]);
+          ptx::mma_m16n8k8_tf32(d, ah, bW[j][0], bW[j][1]);
+          const int ch = 8 * nt + 2 * t;
           const float2 hv0 = *reinterpret_cast<const float2*>(hb + swz(q0, ch));
           const float2 hv1 = *reinterpret_cast<const float2*>(hb + swz(q1, ch));
           const int la = s_lab[q0], lb = s_lab[q1];
@@ -371,36 +315,26 @@ __global__ void __launch_bounds__(kMThr, 1)
     }
   }
 
-  tick(4);
-  if (p.prof)
-    for (int i = 0; i < 6; ++i) atomicAdd(p.prof + i, pc[i]);
   // ------------------------------------------------------------------ block partials
   const int E = C * Ch + C + Ch;
   float* out = p.part + (size_t)blockIdx.x * E;
-  // dW_L[c][ch]: each (class, channel) is owned by exactly one thread of one warp
-#pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const int mt3 = warp + 8 * j;
-    if (mt3 >= p.nmt3) break;
-    const int c0 = 16 * mt3 + g, c1 = c0 + 8, ca = 2 * t, cb = 2 * t + 1;
-    float v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = accW[j][0][u] + (accW[j][1][u] + accW[j][2][u]);
-    if (ca < C && c0 < Ch) out[ca * Ch + c0] = v[0];
-    if (cb < C && c0 < Ch) out[cb * Ch + c0] = v[1];
-    if (ca < C && c1 < Ch) out[ca * Ch + c1] = v[2];
-    if (cb < C && c1 < Ch) out[cb * Ch + c1] = v[3];
+  if (warp < p.nmt3) {  // dW_L[c][ch]: each (class, channel) is owned by exactly one thread
+    const int c0 = 16 * warp + g, c1 = c0 + 8, ca = 2 * t, cb = 2 * t + 1;
+    if (ca < C && c0 < Ch) out[ca * Ch + c0] = accW[0];
+    if (cb < C && c0 < Ch) out[cb * Ch + c0] = accW[1];
+    if (ca < C && c1 < Ch) out[ca * Ch + c1] = accW[2];
+    if (cb < C && c1 < Ch) out[cb * Ch + c1] = accW[3];
   }
   // db_prev[ch]: the 8 lanes of equal t hold channels 8 nt + 2t, + 1 (fixed-order butterfly)
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
+  for (int j = 0; j < 2; ++j) {
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       float v = accP[j][u];
       v += __shfl_xor_sync(0xffffffffu, v, 4);
       v += __shfl_xor_sync(0xffffffffu, v, 8);
       v += __shfl_xor_sync(0xffffffffu, v, 16);
-      const int nt = warp + 8 * j, ch = 8 * nt + 2 * t + u;
+      const int nt = warp + 16 * j, ch = 8 * nt + 2 * t + u;
       if (g == 0 && nt < p.nkt && ch < Ch) out[C * Ch + C + ch] = v;
     }
   }
@@ -418,7 +352,8 @@ __global__ void __launch_bounds__(kMThr, 1)
 }
 
 size_t head_mma_fixed_smem() {
-  return 1024 + 2 * 8 * kWS * 4 + 8 * kMT * 8 * 4 + kMT * 8 * 4 + kMT * 4 + kMT * 8 * 4 + kMaxStages * 8 + 64;
+  return 1024 + 2 * 8 * kWS * 4 + 4 * kMT * 8 * 4 + kMT * 8 * 4 + kMT * 4 + kMT * 8 * 4 + 16 * 4 + 8 + kMaxStages * 8 +
+         64;
 }
 // as many h stages as fit (at most kMaxStages): S - 1 tiles of loads in flight per SM
 int head_mma_stages(int Ch) {
@@ -470,25 +405,9 @@ cudaError_t launch_head_mma(const HeadArgs& a, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   const size_t smem = head_mma_fixed_smem() + (size_t)p.n_stages * p.nchunk * kBoxBytes;
   const int grid = a.n_blocks;
-  const bool x3 = !a.head_1x;
-  auto kern = a.hidden_act == MPF_TANH ? (x3 ? head_mma_kernel<true, true> : head_mma_kernel<true, false>)
-                                       : (x3 ? head_mma_kernel<false, true> : head_mma_kernel<false, false>);
+  auto kern = a.hidden_act == MPF_TANH ? head_mma_kernel<true> : head_mma_kernel<false>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  static unsigned long long* prof = nullptr;
-  if (a.prof_on) {
-    if (!prof) cudaMalloc(&prof, 8 * sizeof(unsigned long long));
-    cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), s);
-    p.prof = prof;
-  }
-  kern<<<grid, kMThr, smem, s>>>(H, p);
-  if (a.prof_on) {
-    unsigned long long h[8];
-    cudaMemcpy(h, prof, sizeof(h), cudaMemcpyDeviceToHost);
-    const double d = (double)grid * kMThr;
-    fprintf(stderr, "[head-prof] Ch=%d tiles=%lld grid=%d stages=%d | per thread Mcyc: wait %.3f sync %.3f gemm1 %.3f softmax %.3f gemm32 %.3f top %.3f\n",
-            a.Ch, p.total, grid, p.n_stages, h[0] / d / 1e6, h[1] / d / 1e6, h[2] / d / 1e6, h[3] / d / 1e6, h[4] / d / 1e6, h[5] / d / 1e6);
-  }
   return cudaGetLastError();
 }
 

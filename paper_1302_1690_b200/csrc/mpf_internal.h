@@ -199,8 +199,6 @@ struct HeadArgs {
   int n;
   int round_tf32;
   const uint8_t* lab_frag;  // training: labels in head-position order (launch_label_frag), or NULL
-  int head_1x;           // (experiment) 1xTF32 products in the mma.sync head
-  int prof_on;           // phase timers (MPF_FLAG_ROLE_TIMERS)
 };
 int head_tiles_per_image(long long per_img);
 // labels gathered into head-position (fragment-major) order: out[img][pos] = class, 255
