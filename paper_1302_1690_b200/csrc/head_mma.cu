@@ -26,7 +26,6 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
-#include <stdio.h>
 
 #include "conv_tc.h"
 #include "head_common.cuh"
@@ -408,6 +407,7 @@ cudaError_t launch_head_mma(const HeadArgs& a, cudaStream_t s) {
   auto kern = a.hidden_act == MPF_TANH ? head_mma_kernel<true> : head_mma_kernel<false>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  kern<<<grid, kMThr, smem, s>>>(H, p);
   return cudaGetLastError();
 }
 
