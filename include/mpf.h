@@ -96,7 +96,6 @@ typedef struct {
  *   WGRAD_M128  M = 128 weight-gradient tiles also for C_out <= 64 (default M = 64).
  *   ROLE_TIMERS per-warp-role cycle counters of the tensor-core convolutions printed to
  *               stderr after every launch (synchronises; profiling only).
- *   HEAD_FMA    the training head on the FMA pipes (head.cu) instead of mma.sync 3xTF32.
  */
 enum {
   MPF_FLAG_SERIAL = 1u << 0,
@@ -106,8 +105,7 @@ enum {
   MPF_FLAG_NTAP_OFF = 1u << 4,
   MPF_FLAG_NTAP_NO_MC = 1u << 5,
   MPF_FLAG_WGRAD_M128 = 1u << 6,
-  MPF_FLAG_ROLE_TIMERS = 1u << 7,
-  MPF_FLAG_HEAD_FMA = 1u << 8
+  MPF_FLAG_ROLE_TIMERS = 1u << 7
 };
 
 /* Geometry of the padded uniform-fragment layout.

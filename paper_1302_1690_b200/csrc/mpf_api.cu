@@ -707,14 +707,8 @@ static mpf_status backward_impl(Net* N, const uint8_t* d_labels, const float* h_
     LAUNCH(N, s, "label_frag", L, 0.0, (double)n * h.F * h.gr * h.gc + (double)n * N->O_H * N->O_W,
            launch_label_frag(hd, labf, s));
     hd.lab_frag = labf;
-    if (head_mma_ok(N->classes, h.C, true) && !(N->cfg.flags & MPF_FLAG_HEAD_FMA)) {  // the three head contractions on mma.sync (3xTF32)
-      hd.n_blocks = head_mma_grid((long long)h.F * h.gr * h.gc, n);
-      LAUNCH(N, s, "head_loss_delta", L, 6.0 * pos * h.C * N->classes, pos * (8.0 * h.C + 1.0),
-             launch_head_mma(hd, s));
-    } else {
-      LAUNCH(N, s, "head_loss_delta", L, 6.0 * pos * h.C * N->classes, pos * (8.0 * h.C + 1.0),
-             launch_head2(hd, s));
-    }
+    LAUNCH(N, s, "head_loss_delta", L, 6.0 * pos * h.C * N->classes, pos * (8.0 * h.C + 1.0),
+           launch_head2(hd, s));
     const int E = N->classes * h.C + N->classes + h.C;
     if (loss_only) {  // forward-only loss evaluation (Armijo trial points): no gradients
       if (d_loss)
@@ -1346,7 +1340,7 @@ mpf_status mpf_net_set_grad_hook(mpf_net* N, mpf_grad_ready_fn fn, void* user) {
 mpf_status mpf_net_set_flags(mpf_net* N, uint32_t flags) {
   if (!N) return fail(MPF_ERR_ARG, "NULL net");
   const uint32_t known = MPF_FLAG_SERIAL | MPF_FLAG_TC_SINGLE | MPF_FLAG_TC_PAIR | MPF_FLAG_NTAP_ON | MPF_FLAG_NTAP_OFF |
-                         MPF_FLAG_NTAP_NO_MC | MPF_FLAG_WGRAD_M128 | MPF_FLAG_ROLE_TIMERS | MPF_FLAG_HEAD_FMA;
+                         MPF_FLAG_NTAP_NO_MC | MPF_FLAG_WGRAD_M128 | MPF_FLAG_ROLE_TIMERS;
   if (flags & ~known) return fail(MPF_ERR_ARG, "unknown MPF_FLAG_* bits");
   if ((flags & MPF_FLAG_NTAP_ON) && (flags & MPF_FLAG_NTAP_OFF)) return fail(MPF_ERR_ARG, "NTAP_ON with NTAP_OFF");
   if ((flags & MPF_FLAG_TC_PAIR) && (flags & MPF_FLAG_TC_SINGLE)) return fail(MPF_ERR_ARG, "TC_PAIR with TC_SINGLE");

@@ -209,12 +209,6 @@ int head_loss_parts_per_tile();
 int head_blocks(long long total_tiles);
 bool head_supported(int C, int Ch);
 cudaError_t launch_head2(const HeadArgs& a, cudaStream_t s);
-// training head on the warp-level tensor cores (head_mma.cu): eligibility, grid (= partial
-// rows), launch (needs lab_frag)
-bool head_mma_ok(int C, int Ch, bool train);
-int head_mma_grid(long long per_img, int n);
-cudaError_t launch_head_mma(const HeadArgs& a, cudaStream_t s);
-
 cudaError_t launch_label_count(const uint8_t* labels, int n, int hw, int classes, int* nlab, cudaStream_t s);
 cudaError_t launch_sqnorm(const float* g, long long n, double* part, int nb, double* out, cudaStream_t s);
 cudaError_t launch_armijo_axpy(float* theta, const float* theta0, const float* g, long long n, float step,
