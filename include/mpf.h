@@ -88,7 +88,7 @@ typedef struct {
  * tile shape changes the order; parity-tested), for A/B measurements and tests:
  *   SERIAL      one stream: the weight packs and weight gradients do not overlap the main
  *               chain on the side stream (results bitwise identical: fixed-order reductions).
- *   TC_SINGLE   tensor-core convolutions without CTA pairs (M = 128 per CTA).
+ *   TC_SINGLE   tensor-core convolutions and weight gradients without CTA pairs (M = 128 per CTA).
  *   TC_PAIR     CTA pairs (cta_group::2, M = 256) wherever they fit.
  *   NTAP_ON     the multi-tap convolution on every eligible narrow layer (default: k >= 5).
  *   NTAP_OFF    never the multi-tap convolution.

@@ -1102,6 +1102,130 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) ptx::tmem_dealloc(tmem, p.tmem_cols);
 }
 
+
+// The weight gradient of a layer with 128 < C_out <= 256 (FC1 of the cfg4 net, C_out = 200)
+// on CTA pairs: tcgen05.mma.cta_group::2 with M = 256 output channels (CTA r stages the dY
+// tile of channels 128 r .. 128 r + 127) and N = 2 x 32 k: the two halves of N come from the
+// two CTAs' shared memory at the same offset, so each CTA stages the X slab of ONE group
+// (ky, channel chunk) and one MMA covers the taps of two groups.  Against two M = 128 CTAs
+// (one per channel half) this reads each X slab once per pair instead of twice and doubles
+// the work per A fetch (N 96 -> 192 for k = 3), so the shared-memory port feeds a fuller
+// tensor pipe.  Same sums per group as wgrad_tc_kernel in the same K order.
+struct WgPairParams {
+  int P_tot, gc, cin, cout, k, n_cc, n_groups, n_pairs, G2, n_sets;
+  int chunk_stages;
+  float* part;
+  uint32_t a_bytes, b_bytes, stage_bytes;
+  int n_stages_ring;
+  uint32_t tmem_cols;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    wgrad_tc_pair_kernel(const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX,
+                         WgPairParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t sbase = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t sBar = sbase + p.n_stages_ring * p.stage_bytes;
+  const uint32_t barFull = sBar, barEmpty = sBar + 8 * p.n_stages_ring, barT = sBar + 16 * p.n_stages_ring;
+  const uint32_t sTmemSlot = barT + 8;
+  uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (sTmemSlot - ptx::smem_u32(smem_raw)));
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_rank();
+  const bool leader = rank == 0;
+  // cluster -> (group-pair set, split); neighbouring clusters share a split (L2 reuse)
+  const int cl = (int)(blockIdx.x >> 1);
+  const int set = cl % p.n_sets, split = cl / p.n_sets;
+  const int q0 = (int)((long long)set * p.n_pairs / p.n_sets);
+  const int G2 = (int)((long long)(set + 1) * p.n_pairs / p.n_sets) - q0;
+  const int N = 32 * p.k, N2 = 2 * N;
+  const long long pbeg = (long long)split * p.chunk_stages * kWR;
+  const uint32_t barFullL = ptx::mapa(barFull, 0);
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmD);
+    ptx::prefetch_tmap(&tmX);
+    for (int i = 0; i < p.n_stages_ring; ++i) {
+      ptx::mbar_init(barFull + 8 * i, 1);
+      ptx::mbar_init(barEmpty + 8 * i, 1);
+    }
+    ptx::mbar_init(barT, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc_pair(sTmemSlot, p.tmem_cols);
+  ptx::tc_fence_before();
+  ptx::cluster_sync_all();  // barrier inits and TMEM allocation visible to the peer
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot_ptr;
+  const int n_st = p.chunk_stages;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int st = 0; st < n_st; ++st) {
+        const int slot = st % p.n_stages_ring;
+        ptx::mbar_wait(barEmpty + 8 * slot, ((st / p.n_stages_ring) & 1) ^ 1);
+        if (leader) ptx::mbar_arrive_expect_tx(barFull + 8 * slot, 2u * (p.a_bytes + G2 * p.b_bytes));
+        const uint32_t sa = sbase + slot * p.stage_bytes;
+        const uint32_t bar = barFullL + 8 * slot;
+        const int row = (int)(pbeg + (long long)st * kWR);
+        for (int j = 0; j < 4; ++j)  // this CTA's 128 output channels: 4 atoms of 32
+          ptx::tma_load_2d_pair(sa + j * kWR * 128, &tmD, bar, 128 * (int)rank + 32 * j, row);
+        for (int gp = 0; gp < G2; ++gp) {
+          int ng = 2 * (q0 + gp) + (int)rank;
+          if (ng >= p.n_groups) ng = 0;  // odd group count: the pair's second half is discarded
+          const int ky = ng / p.n_cc, cc = ng % p.n_cc;
+          ptx::tma_load_2d_pair(sa + p.a_bytes + gp * p.b_bytes, &tmX, bar, cc * kKC, row + ky * p.gc);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = ptx::idesc_tf32_mn(256, N2);
+    for (int st = 0; leader && st < n_st; ++st) {
+      const int slot = st % p.n_stages_ring;
+      ptx::mbar_wait(barFull + 8 * slot, (st / p.n_stages_ring) & 1);
+      ptx::tc_fence_after();
+      const uint32_t sa = sbase + slot * p.stage_bytes;
+      const uint64_t ad0 = ptx::sdesc_mn_sw128_32b(sa, kWR * 128, 512);
+      const uint64_t bd0 = ptx::sdesc_mn_sw128_32b(sa + p.a_bytes, 128, 512);
+      for (int gp = 0; gp < G2; ++gp) {
+#pragma unroll
+        for (int r8 = 0; r8 < kWR / 8; ++r8) {
+          const uint64_t ad = ad0 + (uint64_t)((r8 * 1024) >> 4);
+          const uint64_t bd = bd0 + (uint64_t)((gp * p.b_bytes + r8 * 1024) >> 4);
+          ptx::mma_tf32_pair_elect(tmem + gp * N2, ad, bd, idesc, (st | r8) != 0);
+        }
+      }
+      ptx::mma_commit_pair_elect(barEmpty + 8 * slot, 3);  // frees the slot in both CTAs
+    }
+    if (leader) ptx::mma_commit_pair_elect(barT, 3);
+  } else {
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    const int co = 128 * (int)rank + q * 32 + lane;
+    const bool row_ok = co < p.cout;
+    ptx::mbar_wait(barT, 0);
+    ptx::tc_fence_after();
+    const int K = p.k * p.k * p.cin;
+    float* dst = p.part + ((long long)split * p.cout + (row_ok ? co : 0)) * K;
+    for (int gp = 0; gp < G2; ++gp) {
+      for (int c0 = half * 16; c0 < N2; c0 += 32) {
+        float v[16];
+        ptx::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + gp * N2 + c0, v);
+        const int ng = 2 * (q0 + gp) + (c0 >= N ? 1 : 0);
+        if (row_ok && ng < p.n_groups) {
+          const int ky = ng / p.n_cc, cc = ng % p.n_cc;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int n = (c0 % N) + j, kx = n / 32, ci = cc * kKC + (n % 32);
+            if (ci < p.cin) dst[(ky * p.k + kx) * p.cin + ci] = n_st > 0 ? v[j] : 0.f;
+          }
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync_all();  // the peer may still signal our barriers until here
+  if (warp == 1) ptx::tmem_dealloc_pair(tmem, p.tmem_cols);
+}
+
 }  // namespace
 
 cudaError_t make_tmap_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
@@ -1126,7 +1250,73 @@ bool tc_wgrad_supported(int cin, int cout, int k) {
   return cin % 4 == 0 && cin >= 8 && cout % 4 == 0 && cout <= 256 && k >= 1 && k <= 8;
 }
 
+static bool wgrad_pair_ok(const TcWgradArgs& a) {
+  return !(a.flags & MPF_FLAG_TC_SINGLE) && a.cout > 128 && a.cout <= 256 && 64 * a.k <= 256 && a.k * a.cin > 32;
+}
+
+static cudaError_t launch_wgrad_pair(const TcWgradArgs& a, int* splits_out, cudaStream_t s) {
+  WgPairParams p{};
+  p.P_tot = a.n_frag * a.gr * a.gc;
+  p.gc = a.gc;
+  p.cin = a.cin;
+  p.cout = a.cout;
+  p.k = a.k;
+  p.n_cc = (a.cin + kKC - 1) / kKC;
+  p.n_groups = a.k * p.n_cc;
+  p.n_pairs = (p.n_groups + 1) / 2;
+  const int N2 = 64 * a.k;
+  p.G2 = 512 / N2;
+  if (p.G2 > p.n_pairs) p.G2 = p.n_pairs;
+  p.n_sets = (p.n_pairs + p.G2 - 1) / p.G2;
+  p.a_bytes = 4 * kWR * 128;
+  p.b_bytes = (kWR + 8) * 128;
+  p.stage_bytes = p.a_bytes + p.G2 * p.b_bytes;
+  const size_t budget = 225 * 1024 - 1024 - 256;
+  p.n_stages_ring = (int)(budget / p.stage_bytes);
+  if (p.n_stages_ring > 4) p.n_stages_ring = 4;
+  if (p.n_stages_ring < 2) return cudaErrorInvalidConfiguration;
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(p.G2 * N2)) cols <<= 1;
+  p.tmem_cols = cols;
+  const long long total_stages = (p.P_tot + kWR - 1) / kWR;
+  int splits = num_sms() / (2 * p.n_sets);
+  if (splits > kMaxSplits) splits = kMaxSplits;
+  if (splits < 1) splits = 1;
+  const size_t K = (size_t)a.k * a.k * a.cin;
+  while (splits > 1 && (size_t)splits * (a.cout * K + a.cout) > a.part_cap_floats) --splits;
+  if (splits > total_stages) splits = (int)total_stages;
+  p.chunk_stages = (int)((total_stages + splits - 1) / splits);
+  splits = (int)((total_stages + p.chunk_stages - 1) / p.chunk_stages);
+  p.part = a.part;
+  *splits_out = splits;
+  CUtensorMap D, X;
+  cudaError_t e = make_map(&D, a.dy, (uint64_t)a.cout, (uint64_t)p.P_tot, (uint32_t)kWR,
+                           CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  if (e != cudaSuccess) return e;
+  e = make_map(&X, a.x, (uint64_t)a.cin, (uint64_t)p.P_tot, (uint32_t)(kWR + 8), CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  if (e != cudaSuccess) return e;
+  const size_t smem = 1024 + (size_t)p.n_stages_ring * p.stage_bytes + 256;
+  e = cudaFuncSetAttribute(wgrad_tc_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * splits * p.n_sets, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, wgrad_tc_pair_kernel, D, X, p);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits_out, cudaStream_t s) {
+  if (wgrad_pair_ok(a)) return launch_wgrad_pair(a, splits_out, s);
   WgTcParams p{};
   p.P_tot = a.n_frag * a.gr * a.gc;
   p.gc = a.gc;

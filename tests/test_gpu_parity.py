@@ -402,13 +402,15 @@ def _run_variant(flags, name="cfg2", n=2, prec="tf32"):
     return cfg, g
 
 
-def test_cta_pair_matches_single_cta_mma():
-    """The cta_group::2 (M = 256) and single-CTA (M = 128) tensor-core convolutions compute
-    the same sums in the same K order: identical results up to fp32 accumulation order
-    inside the tensor core."""
+@pytest.mark.parametrize("name", ["cfg2", "cfg4s"])
+def test_cta_pair_matches_single_cta_mma(name):
+    """The cta_group::2 (M = 256) and single-CTA (M = 128) tensor-core convolutions and weight
+    gradients (cfg4s: FC1's C_out = 200 wgrad on CTA pairs, N = two groups' taps) compute the
+    same sums in the same K order: identical results up to fp32 accumulation order inside
+    the tensor core."""
     from paper_1302_1690_b200 import _lib as L
-    cfg, a = _run_variant(L.MPF_FLAG_TC_PAIR)
-    _, b = _run_variant(L.MPF_FLAG_TC_SINGLE)
+    cfg, a = _run_variant(L.MPF_FLAG_TC_PAIR, name=name)
+    _, b = _run_variant(L.MPF_FLAG_TC_SINGLE, name=name)
     assert rel_l2(a["probs"], b["probs"]) <= 1e-6
     for nm, sl in param_slices(cfg.layers):
         assert rel_l2(a["grad_sum"][sl], b["grad_sum"][sl]) <= 1e-5, nm
