@@ -93,7 +93,8 @@ typedef struct {
  *   NTAP_ON     the multi-tap convolution on every eligible narrow layer (default: k >= 5).
  *   NTAP_OFF    never the multi-tap convolution.
  *   NTAP_NO_MC  multi-tap convolution without the cluster weight multicast.
- *   WGRAD_M128  M = 128 weight-gradient tiles also for C_out <= 64 (default M = 64).
+ *   WGRAD_M128  C_out <= 64 weight gradients with C_out on M (M = 128 tiles) instead of the
+ *               default swapped roles (M = 128 rows of (tap, input channel), N = C_out).
  *   ROLE_TIMERS per-warp-role cycle counters of the tensor-core convolutions printed to
  *               stderr after every launch (synchronises; profiling only).
  */

@@ -1226,6 +1226,134 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) ptx::tmem_dealloc_pair(tmem, p.tmem_cols);
 }
 
+
+// The weight gradient of a narrow layer (C_out <= 64) with the roles swapped: M = 128 rows
+// = 4 "atoms" of 32 input channels, each atom one tap (ky, kx) of one channel chunk, read
+// straight out of the X slab of its (ky, chunk) group (an atom is the slab shifted by kx
+// rows: the slab trick on the M side), N = C_out (the dY tile, MN-major), K = positions.
+// With C_out on M (wgrad_tc_kernel<64>) an M = 64 MMA uses half of the tensor datapath;
+// here every MMA has M = 128 and the whole tap set of a position split fits in TMEM
+// (T M-tiles x N <= 512 columns), so one CTA per split reads dY and X once.  M-tiles: for
+// every group, runs of 4 consecutive taps (LBO = one 128-B row); the k mod 4 remaining taps
+// are tiled across groups (LBO = one slab), the last tile possibly partial (its phantom
+// atoms read other shared memory and are discarded).  Same products as wgrad_tc_kernel,
+// summed in the same K order per split.
+constexpr int kSwapMaxTiles = 16;
+struct WgSwapParams {
+  int P_tot, gc, cin, cout, npad, k, n_cc, n_groups, n_tiles;
+  int chunk_stages;
+  float* part;
+  uint32_t a_bytes, b_bytes, stage_bytes;  // a = the dY tile, b = one X slab
+  int n_stages_ring;
+  uint32_t tmem_cols;
+  // per M-tile: first atom (group, tap) and the atom stride (0: taps of one group, 1: groups)
+  int t_group[kSwapMaxTiles], t_tap[kSwapMaxTiles], t_across[kSwapMaxTiles];
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    wgrad_tc_swap_kernel(const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX,
+                         WgSwapParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t sbase = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
+  // ring of stages [X slabs of every group | dY tile], then 3 spare slabs (phantom atoms of a
+  // partial M-tile read there), then the barriers
+  const uint32_t sBar = sbase + p.n_stages_ring * p.stage_bytes + 3 * p.b_bytes;
+  const uint32_t barFull = sBar, barEmpty = sBar + 8 * p.n_stages_ring, barT = sBar + 16 * p.n_stages_ring;
+  const uint32_t sTmemSlot = barT + 8;
+  uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (sTmemSlot - ptx::smem_u32(smem_raw)));
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int split = blockIdx.x;
+  const long long pbeg = (long long)split * p.chunk_stages * kWR;
+  const uint32_t slabs_bytes = (uint32_t)p.n_groups * p.b_bytes;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmD);
+    ptx::prefetch_tmap(&tmX);
+    for (int i = 0; i < p.n_stages_ring; ++i) {
+      ptx::mbar_init(barFull + 8 * i, 1);
+      ptx::mbar_init(barEmpty + 8 * i, 1);
+    }
+    ptx::mbar_init(barT, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(sTmemSlot, p.tmem_cols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot_ptr;
+  const int n_st = p.chunk_stages;
+  const int n_datoms = (p.npad + 31) / 32;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int st = 0; st < n_st; ++st) {
+        const int slot = st % p.n_stages_ring;
+        ptx::mbar_wait(barEmpty + 8 * slot, ((st / p.n_stages_ring) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(barFull + 8 * slot, p.a_bytes + slabs_bytes);
+        const uint32_t sa = sbase + slot * p.stage_bytes;
+        const int row = (int)(pbeg + (long long)st * kWR);
+        for (int g = 0; g < p.n_groups; ++g) {
+          const int ky = g / p.n_cc, cc = g % p.n_cc;
+          ptx::tma_load_2d(sa + g * p.b_bytes, &tmX, barFull + 8 * slot, cc * kKC, row + ky * p.gc);
+        }
+        for (int j = 0; j < n_datoms; ++j)
+          ptx::tma_load_2d(sa + slabs_bytes + j * kWR * 128, &tmD, barFull + 8 * slot, j * 32, row);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = ptx::idesc_tf32_mn(128, p.npad);
+    for (int st = 0; st < n_st; ++st) {
+      const int slot = st % p.n_stages_ring;
+      ptx::mbar_wait(barFull + 8 * slot, (st / p.n_stages_ring) & 1);
+      ptx::tc_fence_after();
+      const uint32_t sa = sbase + slot * p.stage_bytes;
+      const uint64_t bd0 = ptx::sdesc_mn_sw128_32b(sa + slabs_bytes, kWR * 128, 512);
+      for (int t = 0; t < p.n_tiles; ++t) {
+        const uint32_t a0 = sa + p.t_group[t] * p.b_bytes + p.t_tap[t] * 128;
+        const uint64_t ad0 = ptx::sdesc_mn_sw128_32b(a0, p.t_across[t] ? p.b_bytes : 128u, 512);
+#pragma unroll
+        for (int r8 = 0; r8 < kWR / 8; ++r8) {
+          const uint64_t ad = ad0 + (uint64_t)((r8 * 1024) >> 4);
+          const uint64_t bd = bd0 + (uint64_t)((r8 * 1024) >> 4);
+          ptx::mma_tf32_elect(tmem + t * p.npad, ad, bd, idesc, (st | r8) != 0);
+        }
+      }
+      ptx::mma_commit_elect(barEmpty + 8 * slot);
+    }
+    ptx::mma_commit_elect(barT);
+  } else {
+    // TMEM lane quarter q = atom q of every M-tile; lane = input channel within the atom's chunk;
+    // the two warps of a quarter split the C_out columns in 16-column halves
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    ptx::mbar_wait(barT, 0);
+    ptx::tc_fence_after();
+    const int K = p.k * p.k * p.cin;
+    for (int t = 0; t < p.n_tiles; ++t) {
+      const int g = p.t_across[t] ? p.t_group[t] + q : p.t_group[t];
+      const int kx = p.t_across[t] ? p.t_tap[t] : p.t_tap[t] + q;
+      const bool atom_ok = g < p.n_groups && kx < p.k;  // warp-uniform
+      const int ky = atom_ok ? g / p.n_cc : 0, cc = atom_ok ? g % p.n_cc : 0;
+      const int ci = cc * kKC + lane;
+      const bool ok = atom_ok && ci < p.cin;
+      float* dst = p.part + (long long)split * p.cout * K + (ky * p.k + kx) * p.cin + (ok ? ci : 0);
+      for (int c0 = half * 16; c0 < p.npad; c0 += 32) {
+        float v[16];
+        ptx::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + t * p.npad + c0, v);
+        if (ok) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int co = c0 + j;
+            if (co < p.cout) dst[(long long)co * K] = n_st > 0 ? v[j] : 0.f;
+          }
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) ptx::tmem_dealloc(tmem, p.tmem_cols);
+}
+
 }  // namespace
 
 cudaError_t make_tmap_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
@@ -1315,8 +1443,74 @@ static cudaError_t launch_wgrad_pair(const TcWgradArgs& a, int* splits_out, cuda
   return cudaGetLastError();
 }
 
+// the swapped-role plan for C_out <= 64: returns the number of M-tiles (0 = not applicable)
+static int wgrad_swap_plan(const TcWgradArgs& a, WgSwapParams* p) {
+  if ((a.flags & MPF_FLAG_WGRAD_M128) || a.cout > 64) return 0;
+  const int n_cc = (a.cin + kKC - 1) / kKC, G = a.k * n_cc, npad = (a.cout + 15) / 16 * 16;
+  int T = 0;
+  for (int g = 0; g < G; ++g)
+    for (int t0 = 0; t0 + 4 <= a.k; t0 += 4) {
+      if (T == kSwapMaxTiles) return 0;
+      p->t_group[T] = g; p->t_tap[T] = t0; p->t_across[T] = 0; ++T;
+    }
+  for (int kx = a.k / 4 * 4; kx < a.k; ++kx)
+    for (int g0 = 0; g0 < G; g0 += 4) {
+      if (T == kSwapMaxTiles) return 0;
+      p->t_group[T] = g0; p->t_tap[T] = kx; p->t_across[T] = 1; ++T;
+    }
+  if (T * npad > 512) return 0;
+  p->n_tiles = T;
+  p->npad = npad;
+  p->n_cc = n_cc;
+  p->n_groups = G;
+  return T;
+}
+
+static cudaError_t launch_wgrad_swap(const TcWgradArgs& a, WgSwapParams& p, int* splits_out, cudaStream_t s) {
+  p.P_tot = a.n_frag * a.gr * a.gc;
+  p.gc = a.gc;
+  p.cin = a.cin;
+  p.cout = a.cout;
+  p.k = a.k;
+  p.a_bytes = (uint32_t)((p.npad + 31) / 32) * kWR * 128;
+  p.b_bytes = (kWR + 8) * 128;
+  p.stage_bytes = (uint32_t)p.n_groups * p.b_bytes + p.a_bytes;
+  const size_t budget = 225 * 1024 - 1024 - 256 - 3 * p.b_bytes;
+  p.n_stages_ring = (int)(budget / p.stage_bytes);
+  if (p.n_stages_ring > 4) p.n_stages_ring = 4;
+  if (p.n_stages_ring < 2) return cudaErrorInvalidConfiguration;
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(p.n_tiles * p.npad)) cols <<= 1;
+  p.tmem_cols = cols;
+  const long long total_stages = (p.P_tot + kWR - 1) / kWR;
+  int splits = num_sms();
+  if (splits > kMaxSplits) splits = kMaxSplits;
+  const size_t K = (size_t)a.k * a.k * a.cin;
+  while (splits > 1 && (size_t)splits * (a.cout * K + a.cout) > a.part_cap_floats) --splits;
+  if (splits > total_stages) splits = (int)total_stages;
+  p.chunk_stages = (int)((total_stages + splits - 1) / splits);
+  splits = (int)((total_stages + p.chunk_stages - 1) / p.chunk_stages);
+  p.part = a.part;
+  *splits_out = splits;
+  CUtensorMap D, X;
+  cudaError_t e = make_map(&D, a.dy, (uint64_t)a.cout, (uint64_t)p.P_tot, (uint32_t)kWR,
+                           CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  if (e != cudaSuccess) return e;
+  e = make_map(&X, a.x, (uint64_t)a.cin, (uint64_t)p.P_tot, (uint32_t)(kWR + 8), CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  if (e != cudaSuccess) return e;
+  const size_t smem = 1024 + (size_t)p.n_stages_ring * p.stage_bytes + 3 * p.b_bytes + 256;
+  e = cudaFuncSetAttribute(wgrad_tc_swap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  wgrad_tc_swap_kernel<<<splits, kThreads, smem, s>>>(D, X, p);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits_out, cudaStream_t s) {
   if (wgrad_pair_ok(a)) return launch_wgrad_pair(a, splits_out, s);
+  {
+    WgSwapParams sp{};
+    if (wgrad_swap_plan(a, &sp)) return launch_wgrad_swap(a, sp, splits_out, s);
+  }
   WgTcParams p{};
   p.P_tot = a.n_frag * a.gr * a.gc;
   p.gc = a.gc;

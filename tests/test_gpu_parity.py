@@ -416,15 +416,17 @@ def test_cta_pair_matches_single_cta_mma(name):
         assert rel_l2(a["grad_sum"][sl], b["grad_sum"][sl]) <= 1e-5, nm
 
 
-def test_wgrad_m64_matches_m128():
-    """Weight gradients of layers with C_out <= 64 use M = 64 MMAs (accumulator rows in
-    lanes 0-15 of each TMEM quarter); forcing M = 128 (MPF_FLAG_WGRAD_M128) computes the
-    same sums in the same order."""
+@pytest.mark.parametrize("name", ["cfg2", "cfg5s", "cfg4s"])
+def test_wgrad_swapped_matches_m128(name):
+    """Weight gradients of layers with C_out <= 64 run with the roles swapped (M = 128 rows of
+    (tap, input channel) atoms cut from the X slabs, N = C_out); forcing the C_out-on-M
+    kernel with M = 128 tiles (MPF_FLAG_WGRAD_M128) computes the same products; the split-K
+    partition differs, so the sums agree to fp32 rounding."""
     from paper_1302_1690_b200 import _lib as L
-    cfg, a = _run_variant(0)
-    _, b = _run_variant(L.MPF_FLAG_WGRAD_M128)
+    cfg, a = _run_variant(0, name=name)
+    _, b = _run_variant(L.MPF_FLAG_WGRAD_M128, name=name)
     for nm, sl in param_slices(cfg.layers):
-        assert rel_l2(a["grad_sum"][sl], b["grad_sum"][sl]) <= 1e-6, nm
+        assert rel_l2(a["grad_sum"][sl], b["grad_sum"][sl]) <= 1e-5, nm
 
 
 @pytest.mark.parametrize("name", ["cfg2", "cfg4s", "cfg5s"])
