@@ -662,113 +662,6 @@ __global__ void __launch_bounds__(256) mpf_bwd_block3_kernel(MpfBwdArgs a, long 
   for (int q = 0; q < 4; ++q) a.bias_part[((size_t)blockIdx.x * nsub + sub) * C + cv * 4 + q] = bsum[q];
 }
 
-// Window-streaming register gather (k = 2, 3; premul deltas, 4-channel vectors): a thread owns
-// a K x BW block of conv-output elements of one channel vector and walks the (2K-1) x
-// (BW+K-1) patch of candidate windows row by row, the next patch row's loads in flight while
-// the current one is processed.  Each loaded window is tested against every element of the
-// block it covers (its code dy K + dx) and added into that element's accumulator, so only
-// two patch rows of windows are live (vs K rows in mpf_bwd_block3_kernel) and the 9 K^2 .. 
-// tests of a row are independent of one another.  Sums per element in a fixed order
-// (patch rows, then columns: deterministic); equals Alg. 4's scatter (tested against O2).
-template <int K, int BW>
-__global__ void __launch_bounds__(256) mpf_bwd_stream_kernel(MpfBwdArgs a, long long n_groups) {
-  constexpr int PR = 2 * K - 1, PC = BW + K - 1;
-  const int C = a.C, CV = C / 4;
-  const int tid = threadIdx.x, cv = tid % CV, sub = tid / CV, nsub = 256 / CV;
-  const int Xw = K * a.m_c, Yw = K * a.m_r;
-  const int MMC = a.m_r * a.m_c * C, mcC = a.m_c * C;
-  const int bj_n = (a.gc + BW - 1) / BW, bi_n = (a.gr + K - 1) / K;
-  const int groups_per_row = (bj_n + nsub - 1) / nsub;
-  float bsum[4] = {0.f, 0.f, 0.f, 0.f};
-  if (sub < nsub) {
-    for (long long grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
-      const int gj = (int)(grp % groups_per_row);
-      const long long t = grp / groups_per_row;
-      const int bi = (int)(t % bi_n);
-      const int g = (int)(t / bi_n);
-      const int bj = gj * nsub + sub;
-      if (bj >= bj_n) continue;
-      const float* dsrc = a.dout + (size_t)g * K * K * MMC + cv * 4;
-      const uint8_t* isrc = a.idx + (size_t)g * K * K * MMC + cv * 4;
-      int coloff[PC];
-      bool colok[PC];
-#pragma unroll
-      for (int v = 0; v < PC; ++v) {
-        const int wx = BW * bj - (K - 1) + v;
-        colok[v] = wx >= 0 && wx < Xw;
-        coloff[v] = colok[v] ? (wx % K) * MMC + (wx / K) * C : 0;
-      }
-      auto load_row = [&](int u, uint32_t (&ir)[PC], float4 (&dr)[PC]) {
-        const int wy = K * bi - (K - 1) + u;
-        const bool yok = wy >= 0 && wy < Yw;
-        const int rowoff = yok ? (wy % K) * K * MMC + (wy / K) * mcC : 0;
-#pragma unroll
-        for (int v = 0; v < PC; ++v) {
-          const bool ok = yok && colok[v];
-          const int off = ok ? rowoff + coloff[v] : 0;
-          ir[v] = ok ? __ldg(reinterpret_cast<const uint32_t*>(isrc + off)) : 0xFFFFFFFFu;
-          dr[v] = ok ? __ldg(reinterpret_cast<const float4*>(dsrc + off)) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      };
-      float acc[K][BW][4];
-#pragma unroll
-      for (int ea = 0; ea < K; ++ea)
-#pragma unroll
-        for (int eb = 0; eb < BW; ++eb)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) acc[ea][eb][q] = 0.f;
-      uint32_t id[2][PC];
-      float4 d[2][PC];
-      load_row(0, id[0], d[0]);
-#pragma unroll
-      for (int u = 0; u < PR; ++u) {
-        if (u + 1 < PR) load_row(u + 1, id[(u + 1) & 1], d[(u + 1) & 1]);  // next row in flight
-#pragma unroll
-        for (int v = 0; v < PC; ++v) {
-          const uint32_t w_id = id[u & 1][v];
-          const float4 w = d[u & 1][v];
-#pragma unroll
-          for (int ea = 0; ea < K; ++ea) {
-            const int dy = ea - u + K - 1;
-            if (dy < 0 || dy >= K) continue;  // compile-time
-#pragma unroll
-            for (int eb = 0; eb < BW; ++eb) {
-              const int dx = eb - v + K - 1;
-              if (dx < 0 || dx >= K) continue;  // compile-time
-              const uint32_t x = w_id ^ ((uint32_t)(dy * K + dx) * 0x01010101u);
-              if (!(x & 0xFFu)) acc[ea][eb][0] += w.x;
-              if (!(x & 0xFF00u)) acc[ea][eb][1] += w.y;
-              if (!(x & 0xFF0000u)) acc[ea][eb][2] += w.z;
-              if (!(x & 0xFF000000u)) acc[ea][eb][3] += w.w;
-            }
-          }
-        }
-        asm volatile("" ::: "memory");  // keep the loads of row u + 2 behind this row (2 rows live)
-      }
-      float* dst = a.din + ((size_t)g * a.gr * a.gc) * C + cv * 4;
-#pragma unroll
-      for (int ea = 0; ea < K; ++ea) {
-        const int Y = K * bi + ea;
-#pragma unroll
-        for (int eb = 0; eb < BW; ++eb) {
-          const int X = BW * bj + eb;
-          if (Y >= a.gr || X >= a.gc) continue;
-          float o[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            bsum[q] += acc[ea][eb][q];
-            o[q] = a.round_tf32 ? tf32_rn(acc[ea][eb][q]) : acc[ea][eb][q];
-          }
-          stv<4>(dst + (Y * a.gc + X) * C, o);
-        }
-      }
-    }
-  }
-  if (a.bias_part == nullptr || sub >= nsub) return;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) a.bias_part[((size_t)blockIdx.x * nsub + sub) * C + cv * 4 + q] = bsum[q];
-}
-
 // ----------------------------------------------------------------------------- channel sums
 // Generic per-channel partials of a [P][C] tensor (bias gradient of a conv whose delta
 // comes from a dgrad, i.e. a conv followed by another conv).
@@ -830,14 +723,9 @@ cudaError_t launch_mpf_fwd(const MpfArgs& a, cudaStream_t s) {
 static bool bwd_block2(const MpfBwdArgs& a) {
   return a.premul && (a.k == 2 || a.k == 3) && a.C % 4 == 0 && a.C <= 1024;
 }
-// block width of the register gathers (output columns per thread)
-static int bwd_bw(const MpfBwdArgs& a) {
-  if (a.k == 2) return 2;
-  return (a.flags_ab & 2) ? 2 : 3;
-}
 static long long block2_groups(const MpfBwdArgs& a) {
   const int nsub = 256 / (a.C / 4);
-  const int bw = bwd_bw(a);
+  const int bw = a.k == 2 ? 2 : 3;
   const long long bj_n = (a.gc + bw - 1) / bw, bi_n = (a.gr + a.k - 1) / a.k;
   return (long long)a.n_frag_in * bi_n * ((bj_n + nsub - 1) / nsub);
 }
@@ -924,12 +812,8 @@ long long mpf_bwd_partials(const MpfBwdArgs& a) {
 cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s) {
   if (bwd_block2(a)) {
     const size_t smem = 0;
-    const bool stream = (a.flags_ab & 1) != 0;
-    if (a.k == 2 && !stream) mpf_bwd_block2_kernel<<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
-    else if (a.k == 2) mpf_bwd_stream_kernel<2, 2><<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
-    else if (!stream) mpf_bwd_block3_kernel<3, 3><<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
-    else if (bwd_bw(a) == 3) mpf_bwd_stream_kernel<3, 3><<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
-    else mpf_bwd_stream_kernel<3, 2><<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
+    if (a.k == 2) mpf_bwd_block2_kernel<<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
+    else mpf_bwd_block3_kernel<3, 3><<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
     return cudaGetLastError();
   }
   const int V = a.C % 4 == 0 ? 4 : 1;
