@@ -97,6 +97,8 @@ typedef struct {
  *               default swapped roles (M = 128 rows of (tap, input channel), N = C_out).
  *   ROLE_TIMERS per-warp-role cycle counters of the tensor-core convolutions printed to
  *               stderr after every launch (synchronises; profiling only).
+ *   FUSE_FIRST_POOL  the first conv + activation + the MPF layer after it in one kernel
+ *               (the conv output never reaches device memory; bitwise equal).
  */
 enum {
   MPF_FLAG_SERIAL = 1u << 0,
@@ -106,7 +108,8 @@ enum {
   MPF_FLAG_NTAP_OFF = 1u << 4,
   MPF_FLAG_NTAP_NO_MC = 1u << 5,
   MPF_FLAG_WGRAD_M128 = 1u << 6,
-  MPF_FLAG_ROLE_TIMERS = 1u << 7
+  MPF_FLAG_ROLE_TIMERS = 1u << 7,
+  MPF_FLAG_FUSE_FIRST_POOL = 1u << 8
 };
 
 /* Geometry of the padded uniform-fragment layout.

@@ -377,6 +377,139 @@ __global__ void __launch_bounds__(256, 2) conv_first_wgrad_rows_kernel(FirstWgra
   }
 }
 
+// ------------------------------------------------------------------ fused conv + MPF
+// First convolution + activation + the MaxPoolingFragment layer after it (Alg. 1 then
+// Alg. 3) in one pass: the conv outputs of a 16 x 16 tile of
+// pool windows plus a P - 1 halo are computed into shared memory with exactly the
+// arithmetic of conv_first_fwd_kernel (same FMA order, same SFU activation), and pooled
+// there with exactly the rule of mpf_fwd_kernel (row-major first maximum) — so the pooled
+// values and argmax bytes equal the two-kernel path bit for bit, while the conv output
+// (the largest tensor of the network) never reaches HBM.
+constexpr int kCT = 16;  // conv outputs per tile side: (16 - P + 1)^2 pool windows, one
+                         // 4-wide strip per thread for 4 map groups (no idle second round)
+
+template <int K, int P>
+__global__ void __launch_bounds__(256, 3) conv_first_mpf_kernel(FirstConvArgs a, MpfArgs m) {
+  extern __shared__ float smf[];
+  constexpr int kPT = kCT - P + 1;                       // pool windows per tile side
+  constexpr int RY = kCT, RX = kCT;                      // conv outputs needed by the tile
+  constexpr int NS = (RX + kFPX - 1) / kFPX;             // 4-wide strips per conv row
+  constexpr int IW = NS * kFPX + K - 1, IH = RY + K - 1;  // image tile
+  constexpr int IMG = (IH * IW + 3) / 4 * 4;
+  const int coutp = a.n_cog * kFCO;
+  float* s_img = smf;                    // [IH][IW]
+  float* s_w = smf + IMG;                // [K*K][coutp]
+  float* s_b = s_w + K * K * coutp;      // [coutp]
+  float* s_y = s_b + coutp;              // [RY][RX][coutp]
+  const int img = blockIdx.z;
+  const int wy0 = blockIdx.y * kPT, wx0 = blockIdx.x * kPT;  // first window = first conv output
+  for (int e = threadIdx.x; e < IH * IW; e += blockDim.x) {
+    const int iy = e / IW, ix = e % IW;
+    const int gy = wy0 + iy, gx = wx0 + ix;
+    float v = 0.f;
+    if (gy < a.H && gx < a.W) v = a.img[((size_t)img * a.H + gy) * a.W + gx];
+    s_img[e] = v;
+  }
+  for (int e = threadIdx.x; e < K * K * coutp; e += blockDim.x) {
+    const int co = e % coutp, t = e / coutp;
+    s_w[e] = co < a.cout ? a.w[co * K * K + t] : 0.f;
+  }
+  for (int e = threadIdx.x; e < coutp; e += blockDim.x) s_b[e] = e < a.cout ? a.bias[e] : 0.f;
+  __syncthreads();
+  // ---- conv outputs of the tile (4 positions x 8 maps per thread, as conv_first_fwd_kernel)
+  const int cog = threadIdx.x % a.n_cog, strip0 = threadIdx.x / a.n_cog, nstrip = blockDim.x / a.n_cog;
+  for (int strip = strip0; strip < RY * NS; strip += nstrip) {
+    const int ty = strip / NS, tx = (strip % NS) * kFPX;
+    float acc[kFPX][kFCO];
+#pragma unroll
+    for (int q = 0; q < kFPX; ++q)
+#pragma unroll
+      for (int o = 0; o < kFCO; ++o) acc[q][o] = 0.f;
+#pragma unroll
+    for (int ky = 0; ky < K; ++ky) {
+      float row[kFPX + K - 1];
+#pragma unroll
+      for (int i = 0; i < kFPX + K - 1; ++i) row[i] = s_img[(ty + ky) * IW + tx + i];
+#pragma unroll
+      for (int kx = 0; kx < K; ++kx) {
+        const float4* wp = reinterpret_cast<const float4*>(s_w + (ky * K + kx) * coutp + cog * kFCO);
+        const float4 w0 = wp[0], w1 = wp[1];
+        const float wv[kFCO] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+        for (int q = 0; q < kFPX; ++q)
+#pragma unroll
+          for (int o = 0; o < kFCO; ++o) acc[q][o] = fmaf(row[q + kx], wv[o], acc[q][o]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kFPX; ++q) {
+      if (tx + q >= RX) continue;
+      float* dst = s_y + (ty * RX + tx + q) * coutp + cog * kFCO;
+#pragma unroll
+      for (int o = 0; o < kFCO; ++o) dst[o] = act_fwd(a.act, acc[q][o] + s_b[cog * kFCO + o]);
+    }
+  }
+  __syncthreads();
+  // ---- MPF forward of the tile's windows (first maximum in row-major order, R6)
+  const int C = a.cout, CV = C / 4;
+  const int Yw = P * m.m_r, Xw = P * m.m_c;
+  for (int e = threadIdx.x; e < kPT * kPT * CV; e += blockDim.x) {
+    const int cv = e % CV, w = e / CV, ty = w / kPT, tx = w % kPT;
+    const int wy = wy0 + ty, wx = wx0 + tx;
+    if (wy >= Yw || wx >= Xw) continue;
+    float best[4];
+    uint8_t arg[4];
+#pragma unroll
+    for (int dy = 0; dy < P; ++dy) {
+      float hm[4];
+      uint8_t ha[4];
+#pragma unroll
+      for (int dx = 0; dx < P; ++dx) {
+        const float4 v = *reinterpret_cast<const float4*>(s_y + ((ty + dy) * RX + tx + dx) * coutp + cv * 4);
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (dx == 0 || vv[u] > hm[u]) { hm[u] = vv[u]; ha[u] = (uint8_t)dx; }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (dy == 0 || hm[u] > best[u]) { best[u] = hm[u]; arg[u] = (uint8_t)(dy * P + ha[u]); }
+    }
+    if (m.round_tf32) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) best[u] = tf32_rn(best[u]);
+    }
+    const int f = (wy % P) * P + (wx % P);
+    const size_t o = ((((size_t)img * P * P + f) * m.m_r + wy / P) * m.m_c + wx / P) * C + cv * 4;
+    *reinterpret_cast<float4*>(m.out + o) = make_float4(best[0], best[1], best[2], best[3]);
+    *reinterpret_cast<uchar4*>(m.idx + o) = make_uchar4(arg[0], arg[1], arg[2], arg[3]);
+  }
+}
+
+template <int K, int P>
+cudaError_t fused_kp(FirstConvArgs a, const MpfArgs& m, cudaStream_t s) {
+  a.n_cog = (a.cout + kFCO - 1) / kFCO;
+  const int coutp = a.n_cog * kFCO;
+  constexpr int RY = kCT, RX = kCT, NS = (RX + kFPX - 1) / kFPX;
+  constexpr int IW = NS * kFPX + K - 1, IH = RY + K - 1, IMG = (IH * IW + 3) / 4 * 4;
+  const size_t smem = sizeof(float) * (IMG + K * K * coutp + coutp + (size_t)RY * RX * coutp);
+  cudaError_t e = cudaFuncSetAttribute(conv_first_mpf_kernel<K, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  constexpr int kPT = kCT - P + 1;
+  dim3 grid((P * m.m_c + kPT - 1) / kPT, (P * m.m_r + kPT - 1) / kPT, a.n);
+  conv_first_mpf_kernel<K, P><<<grid, 256, smem, s>>>(a, m);
+  return cudaGetLastError();
+}
+
+template <int K>
+cudaError_t fused_k(const FirstConvArgs& a, const MpfArgs& m, cudaStream_t s) {
+  if (m.k == 2) return fused_kp<K, 2>(a, m, s);
+  if (m.k == 3) return fused_kp<K, 3>(a, m, s);
+  return cudaErrorInvalidValue;
+}
+
+
 template <int K>
 size_t fwd_smem(int coutp) {
   return sizeof(float) * (((kFTH + K - 1) * (kFTW + K - 1) + 3) / 4 * 4 + K * K * coutp + coutp);
@@ -438,6 +571,29 @@ cudaError_t wgrad_k(const FirstWgradArgs& a, cudaStream_t s) {
 }
 
 }  // namespace
+
+// Fused first conv + MPF (SURVEY §8(f) 1 for the first layer): C_out a multiple of 8 (float4
+// pooling, 8-map groups), pool 2 or 3.  Opt-in (MPF_FLAG_FUSE_FIRST_POOL): bitwise equal to
+// the two kernels but measured slower -- 1.66 vs 0.97 + 0.42 ms on cfg4, 0.60 vs 0.23 + 0.21 ms
+// on cfg5: the halo (14-31 % more conv outputs), the per-tile weight staging and the
+// serialised conv -> pool phases of a CTA cost more than the conv output's HBM round trip
+// saves.
+bool first_conv_mpf_supported(int cout, int k, int pool_k) {
+  return cout % 8 == 0 && cout <= 32 && k >= 2 && k <= 8 && (pool_k == 2 || pool_k == 3);
+}
+
+cudaError_t launch_first_conv_mpf(const FirstConvArgs& a, const MpfArgs& m, cudaStream_t s) {
+  switch (a.k) {
+    case 2: return fused_k<2>(a, m, s);
+    case 3: return fused_k<3>(a, m, s);
+    case 4: return fused_k<4>(a, m, s);
+    case 5: return fused_k<5>(a, m, s);
+    case 6: return fused_k<6>(a, m, s);
+    case 7: return fused_k<7>(a, m, s);
+    case 8: return fused_k<8>(a, m, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
 
 bool first_conv_supported(int cin, int cout, int k) {
   if (cin != 1 || cout < 1 || cout > 32 || k < 2 || k > 8) return false;

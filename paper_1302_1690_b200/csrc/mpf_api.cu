@@ -462,6 +462,7 @@ static mpf_status forward_impl(Net* N, const float* d_images, int n, float* d_pr
   }
   if (sp != s) MPF_CUDA(cudaEventRecord(N->ev_join, sp));
   // 2. layers (Alg. 1; Alg. 3 for MPF)
+  bool pool_done = false;  // the first layer's kernel already produced the MPF after it
   for (int l = 0; l < N->n_layers - 1; ++l) {
     const LayerPlan& P = N->lp[l];
     const Act& in = N->a[l];
@@ -473,6 +474,10 @@ static mpf_status forward_impl(Net* N, const float* d_images, int n, float* d_pr
     }
     // the consumer of this output rounds? (TF32 operand of a tensor-core conv)
     const bool next_tc = (l + 1 < N->n_layers - 1) && N->lp[l + 1].L.kind != MPF_POOL && use_tc(N, N->lp[l + 1], false);
+    if (P.L.kind == MPF_POOL && pool_done) {  // produced by the fused first conv + MPF
+      pool_done = false;
+      continue;
+    }
     if (P.L.kind == MPF_POOL) {
       const Act& y = in;
       MpfArgs m;
@@ -500,7 +505,25 @@ static mpf_status forward_impl(Net* N, const float* d_images, int n, float* d_pr
       f.w = N->params + P.w_off; f.bias = N->params + P.b_off; f.k = P.L.k; f.cout = P.cout;
       f.out = out; f.out_gr = o.gr; f.out_gc = o.gc; f.out_vr = o.vr; f.out_vc = o.vc;
       f.act = P.L.act; f.zero_pad = P.out_where == Where::Tape ? 1 : 0; f.round_tf32 = next_tc ? 1 : 0;
-      LAUNCH(N, s, "conv_first_fwd", l, cflops, cbytes, launch_first_conv(f, s));
+      const LayerPlan& Pn = N->lp[1];
+      if ((flags & MPF_FLAG_FUSE_FIRST_POOL) && P.out_where == Where::ScratchY && Pn.L.kind == MPF_POOL &&
+          N->n_layers > 2 && first_conv_mpf_supported(P.cout, P.L.k, Pn.L.k)) {
+        // conv + activation + MPF (layer 1) in one kernel: the conv output is never stored
+        const Act& po = N->a[2];
+        MpfArgs m{};
+        m.y = nullptr;
+        m.gr = o.gr; m.gc = o.gc; m.vr = o.vr; m.vc = o.vc; m.C = o.C; m.k = Pn.L.k;
+        m.n_frag_in = n * o.F;
+        m.out = tape_val(N, 1);
+        m.idx = tape_idx(N, 1);
+        m.m_r = po.vr; m.m_c = po.vc;
+        m.round_tf32 = (2 < N->n_layers - 1 && use_tc(N, N->lp[2], false)) ? 1 : 0;
+        const double eout = (double)n * po.F * po.vr * po.vc * po.C;
+        LAUNCH(N, s, "conv_first_mpf", l, cflops, 4.0 * in_e + 5.0 * eout, launch_first_conv_mpf(f, m, s));
+        pool_done = true;
+      } else {
+        LAUNCH(N, s, "conv_first_fwd", l, cflops, cbytes, launch_first_conv(f, s));
+      }
     } else if (l > 0 && use_tc(N, P, false)) {
       TcConvArgs t{};
       t.x = x; t.n_frag = n * in.F; t.gr = in.gr; t.gc = in.gc; t.cin = P.cin;
@@ -1340,7 +1363,7 @@ mpf_status mpf_net_set_grad_hook(mpf_net* N, mpf_grad_ready_fn fn, void* user) {
 mpf_status mpf_net_set_flags(mpf_net* N, uint32_t flags) {
   if (!N) return fail(MPF_ERR_ARG, "NULL net");
   const uint32_t known = MPF_FLAG_SERIAL | MPF_FLAG_TC_SINGLE | MPF_FLAG_TC_PAIR | MPF_FLAG_NTAP_ON | MPF_FLAG_NTAP_OFF |
-                         MPF_FLAG_NTAP_NO_MC | MPF_FLAG_WGRAD_M128 | MPF_FLAG_ROLE_TIMERS;
+                         MPF_FLAG_NTAP_NO_MC | MPF_FLAG_WGRAD_M128 | MPF_FLAG_ROLE_TIMERS | MPF_FLAG_FUSE_FIRST_POOL;
   if (flags & ~known) return fail(MPF_ERR_ARG, "unknown MPF_FLAG_* bits");
   if ((flags & MPF_FLAG_NTAP_ON) && (flags & MPF_FLAG_NTAP_OFF)) return fail(MPF_ERR_ARG, "NTAP_ON with NTAP_OFF");
   if ((flags & MPF_FLAG_TC_PAIR) && (flags & MPF_FLAG_TC_SINGLE)) return fail(MPF_ERR_ARG, "TC_PAIR with TC_SINGLE");

@@ -257,6 +257,10 @@ struct FirstWgradArgs {
   int n_cog;             // set by the launcher
 };
 bool first_conv_supported(int cin, int cout, int k);
+// first conv + activation + the MPF layer after it in one kernel (conv output never stored)
+bool first_conv_mpf_supported(int cout, int k, int pool_k);
+struct MpfArgs;
+cudaError_t launch_first_conv_mpf(const FirstConvArgs& a, const MpfArgs& m, cudaStream_t s);
 int first_wgrad_blocks(int k);  // k = 0: the largest grid (partial-buffer sizing)
 cudaError_t launch_first_conv(FirstConvArgs a, cudaStream_t s);
 cudaError_t launch_first_wgrad(FirstWgradArgs a, cudaStream_t s);

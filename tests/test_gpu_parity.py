@@ -449,6 +449,20 @@ def test_multitap_conv_matches_standard(name):
         assert rel_l2(a["grad_sum"][sl], c["grad_sum"][sl]) <= 1e-3, nm
 
 
+@pytest.mark.parametrize("name", ["cfg2", "cfg4s", "cfg5s"])
+def test_first_conv_mpf_fusion_bitwise(name):
+    """The fused first conv + activation + MPF kernel (MPF_FLAG_FUSE_FIRST_POOL)
+    computes the conv outputs and the pooling with exactly the arithmetic of the two separate
+    kernels: the whole training step (pooled values, argmaxes and everything downstream) is
+    bitwise identical with the fusion off."""
+    from paper_1302_1690_b200 import _lib as L
+    _, a = _run_variant(L.MPF_FLAG_FUSE_FIRST_POOL, name=name)
+    _, b = _run_variant(0, name=name)
+    assert np.array_equal(a["loss"], b["loss"])
+    assert np.array_equal(a["probs"], b["probs"])
+    assert np.array_equal(a["grad_sum"], b["grad_sum"])
+
+
 @pytest.mark.parametrize("name", ["cfg2", "cfg5s"])
 def test_serial_schedule_is_bitwise_identical(name):
     """MPF_FLAG_SERIAL (weight packs and weight gradients on the caller's stream instead of the
