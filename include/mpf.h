@@ -92,7 +92,8 @@ typedef struct {
  *   TC_PAIR     CTA pairs (cta_group::2, M = 256) wherever they fit.
  *   NTAP_ON     the multi-tap convolution on every eligible narrow layer (default: k >= 5).
  *   NTAP_OFF    never the multi-tap convolution.
- *   NTAP_NO_MC  multi-tap convolution without the cluster weight multicast.
+ *   NTAP_NO_MC  no cluster multicast: neither the multi-tap convolution's weights nor the
+ *               weight gradients' dY tile (bitwise identical results).
  *   WGRAD_M128  C_out <= 64 weight gradients with C_out on M (M = 128 tiles) instead of the
  *               default swapped roles (M = 128 rows of (tap, input channel), N = C_out).
  *   ROLE_TIMERS per-warp-role cycle counters of the tensor-core convolutions printed to

@@ -997,7 +997,10 @@ struct WgTcParams {
   uint32_t tmem_cols;
 };
 
-template <int MT>  // output channels per tile: 128, or 64 (M = 64 MMA) when C_out <= 64
+// CS > 1: the CS group sets of one split run as a cluster; each CTA loads 1/CS of the dY
+// tile and multicasts it to all of them (the tile is read from L2 once per split instead of
+// CS times), and a stage slot is refilled only when every CTA's MMAs have released it.
+template <int MT, int CS>  // MT: output channels per tile, 128, or 64 (M = 64 MMA) when C_out <= 64
 __global__ void __launch_bounds__(kThreads, 1)
     wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX, WgTcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1023,17 +1026,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::prefetch_tmap(&tmX);
     for (int i = 0; i < p.n_stages_ring; ++i) {
       ptx::mbar_init(barFull + 8 * i, 1);
-      ptx::mbar_init(barEmpty + 8 * i, 1);
+      ptx::mbar_init(barEmpty + 8 * i, CS);
     }
     ptx::mbar_init(barT, 1);
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc(sTmemSlot, p.tmem_cols);
   ptx::tc_fence_before();
-  __syncthreads();
+  if (CS > 1) ptx::cluster_sync_all();  // every CTA's barriers exist before anything is multicast
+  else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot_ptr;
   const int n_st = p.chunk_stages;
+  const int rank = CS > 1 ? (int)ptx::cluster_rank() : 0;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -1043,8 +1048,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_arrive_expect_tx(barFull + 8 * slot, p.a_bytes + G * p.b_bytes);
         const uint32_t sa = sbase + slot * p.stage_bytes;
         const int row = (int)(pbeg + (long long)st * kWR);
-        for (int j = 0; j < MT / 32; ++j)  // atoms of 32 output channels
-          ptx::tma_load_2d(sa + j * kWR * 128, &tmD, barFull + 8 * slot, mt * MT + j * 32, row);
+        for (int j = 0; j < MT / 32; ++j) {  // atoms of 32 output channels
+          if (CS > 1) {
+            if (j % CS == rank)
+              ptx::tma_load_2d_mc(sa + j * kWR * 128, &tmD, barFull + 8 * slot, mt * MT + j * 32, row,
+                                  (uint16_t)((1u << CS) - 1u));
+          } else {
+            ptx::tma_load_2d(sa + j * kWR * 128, &tmD, barFull + 8 * slot, mt * MT + j * 32, row);
+          }
+        }
         for (int g = 0; g < G; ++g) {
           const int ng = g0 + g, ky = ng / p.n_cc, cc = ng % p.n_cc;
           ptx::tma_load_2d(sa + p.a_bytes + g * p.b_bytes, &tmX, barFull + 8 * slot, cc * kKC, row + ky * p.gc);
@@ -1068,7 +1080,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mma_tf32_elect(tmem + g * N, ad, bd, idesc, (st | r8) != 0);
         }
       }
-      ptx::mma_commit_elect(barEmpty + 8 * slot);
+      if (CS > 1) ptx::mma_commit_mc_elect(barEmpty + 8 * slot, (uint16_t)((1u << CS) - 1u));  // frees the slot in every CTA
+      else ptx::mma_commit_elect(barEmpty + 8 * slot);
     }
     ptx::mma_commit_elect(barT);
   } else {
@@ -1098,7 +1111,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  if (CS > 1) ptx::cluster_sync_all();  // peers may still multicast into / arrive on our smem
+  else __syncthreads();
   if (warp == 1) ptx::tmem_dealloc(tmem, p.tmem_cols);
 }
 
@@ -1559,10 +1573,33 @@ cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits_out, cudaStream_t 
   e = make_map(&X, a.x, (uint64_t)a.cin, (uint64_t)p.P_tot, (uint32_t)(kWR + 8), CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   if (e != cudaSuccess) return e;
   const size_t smem = 1024 + (size_t)p.n_stages_ring * p.stage_bytes + 256;
-  auto kern = MT == 64 ? wgrad_tc_kernel<64> : wgrad_tc_kernel<128>;
+  // the group sets of a split share the dY tile through a cluster multicast (m_tiles == 1)
+  const int cs = (p.m_tiles == 1 && p.n_sets >= 2 && p.n_sets <= 4 && !(a.flags & MPF_FLAG_NTAP_NO_MC)) ? p.n_sets : 1;
+  auto pick = [&]() {
+    if (MT == 64) return cs == 2 ? wgrad_tc_kernel<64, 2> : cs == 3 ? wgrad_tc_kernel<64, 3> : cs == 4 ? wgrad_tc_kernel<64, 4> : wgrad_tc_kernel<64, 1>;
+    return cs == 2 ? wgrad_tc_kernel<128, 2> : cs == 3 ? wgrad_tc_kernel<128, 3> : cs == 4 ? wgrad_tc_kernel<128, 4> : wgrad_tc_kernel<128, 1>;
+  };
+  auto kern = pick();
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<splits * per_split_blocks, kThreads, smem, s>>>(D, X, p);
+  if (cs == 1) {
+    kern<<<splits * per_split_blocks, kThreads, smem, s>>>(D, X, p);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(splits * per_split_blocks, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, D, X, p);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
