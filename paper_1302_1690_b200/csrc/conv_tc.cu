@@ -1573,10 +1573,10 @@ cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits_out, cudaStream_t 
   e = make_map(&X, a.x, (uint64_t)a.cin, (uint64_t)p.P_tot, (uint32_t)(kWR + 8), CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   if (e != cudaSuccess) return e;
   const size_t smem = 1024 + (size_t)p.n_stages_ring * p.stage_bytes + 256;
-  // the two group sets of a split share the dY tile through a cluster multicast (m_tiles == 1):
-  // measured on cfg4's C3x3 96->128 weight gradient 2.96 -> 2.65 ms; with four sets (C5x5
-  // 64->96) the four-way lockstep of uneven sets cost more than it saved (5.0 -> 9.2 ms)
-  const int cs = (p.m_tiles == 1 && p.n_sets == 2 && !(a.flags & MPF_FLAG_NTAP_NO_MC)) ? 2 : 1;
+  // pairs of group sets of a split share the dY tile through a cluster multicast (m_tiles == 1):
+  // measured on cfg4's C3x3 96->128 weight gradient 2.96 -> 2.65 ms; one cluster of all four
+  // sets of C5x5 64->96 was slower (5.0 -> 9.2 ms: four-way lockstep of uneven sets)
+  const int cs = (p.m_tiles == 1 && p.n_sets % 2 == 0 && !(a.flags & MPF_FLAG_NTAP_NO_MC)) ? 2 : 1;
   auto pick = [&]() {
     if (MT == 64) return cs == 2 ? wgrad_tc_kernel<64, 2> : cs == 3 ? wgrad_tc_kernel<64, 3> : cs == 4 ? wgrad_tc_kernel<64, 4> : wgrad_tc_kernel<64, 1>;
     return cs == 2 ? wgrad_tc_kernel<128, 2> : cs == 3 ? wgrad_tc_kernel<128, 3> : cs == 4 ? wgrad_tc_kernel<128, 4> : wgrad_tc_kernel<128, 1>;
