@@ -81,7 +81,11 @@ __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.syn
 // PAIR: a cluster of two CTAs on one TPC runs tcgen05 cta_group::2 MMAs (M = 256):
 // each CTA stages its own positions (A) and HALF of every weight tile (B), the leader
 // issues the MMAs, every accumulator lands in the TMEM of the CTA that owns its rows.
-template <int NACC, bool PAIR>
+// MC (single-CTA tiles only): a cluster of two CTAs runs tiles 2u and 2u + 1 in lockstep;
+// each loads half of the k weight taps of a stage and multicasts them to both (the weight
+// stream from L2 per SM halves), and a stage slot is refilled only when both CTAs' MMAs
+// have released it.
+template <int NACC, bool PAIR, bool MC = false>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmO, ConvTcParams p) {
@@ -106,9 +110,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int M_CTA = NACC * 128;
   const uint32_t rank = PAIR ? ptx::cluster_rank() : 0u;
   const bool leader = rank == 0;
-  // tiles: one per CTA, or one per pair (2 x M_CTA positions, CTA r owns the r-th half)
-  const int unit0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  static_assert(!(PAIR && MC), "multicast is for single-CTA tiles");
+  const int mrank = MC ? (int)ptx::cluster_rank() : 0;
+  // tiles: one per CTA, or one per pair (2 x M_CTA positions, CTA r owns the r-th half); MC:
+  // both CTAs of a cluster iterate over the same number of tiles (tile 2u + 1 may lie past
+  // the end: its loads read zeros and its stores are clipped)
+  const int unit0 = PAIR ? (int)(blockIdx.x >> 1) : (MC ? (int)(blockIdx.x >> 1) * 2 + mrank : (int)blockIdx.x);
   const int n_units = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int tile_end = MC ? (p.n_tiles + 1) / 2 * 2 : p.n_tiles;
   const int tile_pos = PAIR ? 2 * M_CTA : M_CTA;
   const int my_off = (int)rank * M_CTA;
   // the pair's full barriers and the TMEM-empty barriers live in the leader
@@ -121,7 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::prefetch_tmap(&tmO);
     for (int i = 0; i < p.n_stages; ++i) {
       ptx::mbar_init(barFull + 8 * i, 1);
-      ptx::mbar_init(barEmpty + 8 * i, 1);
+      ptx::mbar_init(barEmpty + 8 * i, MC ? 2 : 1);
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(barTfull + 8 * i, 1);
@@ -135,7 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   for (int c = threadIdx.x; c < 256; c += kThreads) s_bias[c] = (p.bias && c < p.cout) ? p.bias[c] : 0.f;
   ptx::tc_fence_before();
-  if (PAIR) ptx::cluster_sync_all();  // barrier inits and TMEM allocation visible to the peer
+  if (PAIR || MC) ptx::cluster_sync_all();  // barrier inits and TMEM allocation visible to the peer
   else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot_ptr;
@@ -149,7 +158,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int it = 0;
       const uint32_t npair = PAIR ? 2u : 1u;
-      for (int tile = unit0; tile < p.n_tiles; tile += n_units) {
+      for (int tile = unit0; tile < tile_end; tile += n_units) {
         const int p0 = tile * tile_pos + my_off;
         for (int ky = 0; ky < k; ++ky) {
           for (int cc = 0; cc < p.n_cc; ++cc, ++it) {
@@ -167,7 +176,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint32_t sb = sa + p.a_slot_bytes + kx * p.b_slot_bytes;
               const int c0 = (ky * k + kx) * p.cin + cc * kKC;
               if (PAIR) ptx::tma_load_2d_pair(sb, &tmB, bar, c0, (int)rank * p.b_rows);
-              else ptx::tma_load_2d(sb, &tmB, bar, c0, 0);
+              else if (MC) {
+                if ((kx & 1) == mrank) ptx::tma_load_2d_mc(sb, &tmB, bar, c0, 0, (uint16_t)3);
+              } else ptx::tma_load_2d(sb, &tmB, bar, c0, 0);
             }
           }
         }
@@ -177,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ MMA issuer (leader)
     const uint32_t idesc = ptx::idesc_tf32(PAIR ? 256 : 128, p.npad);
     int it = 0, lt = 0;
-    for (int tile = unit0; leader && tile < p.n_tiles; tile += n_units, ++lt) {
+    for (int tile = unit0; leader && tile < tile_end; tile += n_units, ++lt) {
       const int buf = lt & 1;
       twait(barTempty + 8 * buf, ((lt >> 1) & 1) ^ 1, pc[3], prof_on);  // the epilogue drained this set
       ptx::tc_fence_after();
@@ -209,6 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           if (PAIR) ptx::mma_commit_pair_elect(barEmpty + 8 * st, 3);  // frees the stage in both CTAs
+          else if (MC) ptx::mma_commit_mc_elect(barEmpty + 8 * st, (uint16_t)3);
           else ptx::mma_commit_elect(barEmpty + 8 * st);
         }
       }
@@ -222,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ew = warp - 2;
     const int per_frag = p.gr * p.gc;
     int lt = 0, sb = 0;
-    for (int tile = unit0; tile < p.n_tiles; tile += n_units, ++lt) {
+    for (int tile = unit0; tile < tile_end; tile += n_units, ++lt) {
       const int buf = lt & 1;
       twait(barTfull + 8 * buf, (lt >> 1) & 1, pc[7], prof_on);
       ptx::tc_fence_after();
@@ -356,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (pc[i]) atomicAdd(p.prof + i, pc[i]);
   }
   ptx::tc_fence_before();
-  if (PAIR) ptx::cluster_sync_all();  // the peer may still signal our barriers until here
+  if (PAIR || MC) ptx::cluster_sync_all();  // the peer may still signal our barriers until here
   else __syncthreads();
   if (warp == 1) {
     if (PAIR) ptx::tmem_dealloc_pair(tmem, p.tmem_cols);
@@ -706,19 +718,21 @@ void prof_report(const ConvTcParams& p, int nacc, bool pair, int grid) {
           h[1] / ctas / 256e6, h[5] / ctas / 256e6, h[9] / ctas / 256e6, h[8] / ctas / 256e6);
 }
 
-template <int NACC, bool PAIR>
+template <int NACC, bool PAIR, bool MC = false>
 cudaError_t launch_nacc(const CUtensorMap& A, const CUtensorMap& B, const CUtensorMap& O, ConvTcParams& p,
                         size_t smem, cudaStream_t s) {
-  auto kern = conv_tc_kernel<NACC, PAIR>;
+  auto kern = conv_tc_kernel<NACC, PAIR, MC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if (!PAIR) {
+  if (!PAIR && !MC) {
     const int grid = p.n_tiles < num_sms() ? p.n_tiles : num_sms();
     kern<<<grid, kThreads, smem, s>>>(A, B, O, p);
     prof_report(p, NACC, PAIR, grid);
     return cudaGetLastError();
   }
-  const int pairs = p.n_tiles < num_sms() / 2 ? p.n_tiles : num_sms() / 2;
+  // pairs of CTAs: a cta_group::2 pair per tile, or (MC) two single-CTA tiles in lockstep
+  const int units = MC ? (p.n_tiles + 1) / 2 : p.n_tiles;
+  const int pairs = units < num_sms() / 2 ? units : num_sms() / 2;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pairs, 1, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
@@ -963,6 +977,14 @@ cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s, int* grid_out) {
       case 2: return launch_nacc<2, true>(A, B, O, p, smem, s);
       case 3: return launch_nacc<3, true>(A, B, O, p, smem, s);
       default: return launch_nacc<4, true>(A, B, O, p, smem, s);
+    }
+  }
+  if (!(a.flags & MPF_FLAG_NTAP_NO_MC) && a.k >= 2 && p.n_tiles >= 2) {  // weight taps multicast over two CTAs
+    switch (nacc) {
+      case 1: return launch_nacc<1, false, true>(A, B, O, p, smem, s);
+      case 2: return launch_nacc<2, false, true>(A, B, O, p, smem, s);
+      case 3: return launch_nacc<3, false, true>(A, B, O, p, smem, s);
+      default: return launch_nacc<4, false, true>(A, B, O, p, smem, s);
     }
   }
   switch (nacc) {
