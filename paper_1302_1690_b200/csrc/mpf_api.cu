@@ -772,7 +772,6 @@ static mpf_status backward_impl(Net* N, const uint8_t* d_labels, const float* h_
       m.round_tf32 = tf32 ? 1 : 0;
       m.bias_part = bpart;
       m.premul = premul ? 1 : 0;
-      m.minb4 = (N->cfg.flags >> 9) & 1u;
       premul = false;
       const double ein = (double)n * in.F * in.vr * in.vc * in.C, eout = (double)n * o.F * o.vr * o.vc * o.C;
       LAUNCH(N, s, "mpf_bwd", l, 0.0, (m.premul ? 5.0 : 9.0) * eout + 4.0 * ein, launch_mpf_bwd(m, s));
@@ -1364,7 +1363,7 @@ mpf_status mpf_net_set_grad_hook(mpf_net* N, mpf_grad_ready_fn fn, void* user) {
 mpf_status mpf_net_set_flags(mpf_net* N, uint32_t flags) {
   if (!N) return fail(MPF_ERR_ARG, "NULL net");
   const uint32_t known = MPF_FLAG_SERIAL | MPF_FLAG_TC_SINGLE | MPF_FLAG_TC_PAIR | MPF_FLAG_NTAP_ON | MPF_FLAG_NTAP_OFF |
-                         MPF_FLAG_NTAP_NO_MC | MPF_FLAG_WGRAD_M128 | MPF_FLAG_ROLE_TIMERS | MPF_FLAG_FUSE_FIRST_POOL | (1u << 9);
+                         MPF_FLAG_NTAP_NO_MC | MPF_FLAG_WGRAD_M128 | MPF_FLAG_ROLE_TIMERS | MPF_FLAG_FUSE_FIRST_POOL;
   if (flags & ~known) return fail(MPF_ERR_ARG, "unknown MPF_FLAG_* bits");
   if ((flags & MPF_FLAG_NTAP_ON) && (flags & MPF_FLAG_NTAP_OFF)) return fail(MPF_ERR_ARG, "NTAP_ON with NTAP_OFF");
   if ((flags & MPF_FLAG_TC_PAIR) && (flags & MPF_FLAG_TC_SINGLE)) return fail(MPF_ERR_ARG, "TC_PAIR with TC_SINGLE");

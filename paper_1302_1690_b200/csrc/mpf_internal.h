@@ -166,7 +166,6 @@ struct MpfBwdArgs {
   int round_tf32;
   float* bias_part;      // nullable: [mpf_bwd_partials(a)][C] per-block sums of din (bias gradient)
   int premul;            // 1: dout already carries act'(y) (the producing dgrad applied it); pooled unused
-  int minb4;             // (A/B) k = 2 gather at 4 CTAs per SM
 };
 cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s);
 long long mpf_bwd_partials(const MpfBwdArgs& a);

@@ -482,8 +482,7 @@ __global__ void __launch_bounds__(256) mpf_bwd_tile_kernel(MpfBwdArgs a, int row
 // gathers each element's k^2 candidates from registers in the same fixed (dy, dx) order as
 // the other MPF backward kernels (bitwise-identical results).  No shared-memory staging,
 // no barriers; CTAs stride over groups of consecutive blocks of one row.
-template <int MINB>
-__global__ void __launch_bounds__(256, MINB) mpf_bwd_block2_kernel(MpfBwdArgs a, long long n_groups) {
+__global__ void __launch_bounds__(256, 3) mpf_bwd_block2_kernel(MpfBwdArgs a, long long n_groups) {
   const int C = a.C, CV = C / 4;
   const int tid = threadIdx.x, cv = tid % CV, sub = tid / CV, nsub = 256 / CV;
   const int Xw = 2 * a.m_c, Yw = 2 * a.m_r;
@@ -813,8 +812,7 @@ long long mpf_bwd_partials(const MpfBwdArgs& a) {
 cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s) {
   if (bwd_block2(a)) {
     const size_t smem = 0;
-    if (a.k == 2 && a.minb4) mpf_bwd_block2_kernel<4><<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
-    else if (a.k == 2) mpf_bwd_block2_kernel<3><<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
+    if (a.k == 2) mpf_bwd_block2_kernel<<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
     else mpf_bwd_block3_kernel<3, 3><<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
     return cudaGetLastError();
   }
