@@ -100,8 +100,6 @@ typedef struct {
  *               stderr after every launch (synchronises; profiling only).
  *   FUSE_FIRST_POOL  the first conv + activation + the MPF layer after it in one kernel
  *               (the conv output never reaches device memory; bitwise equal).
- *   NO_PDL      launch the kernels without programmatic dependent launch (by default each
- *               kernel's prologue overlaps the tail of the previous one on the same stream).
  */
 enum {
   MPF_FLAG_SERIAL = 1u << 0,
@@ -112,8 +110,7 @@ enum {
   MPF_FLAG_NTAP_NO_MC = 1u << 5,
   MPF_FLAG_WGRAD_M128 = 1u << 6,
   MPF_FLAG_ROLE_TIMERS = 1u << 7,
-  MPF_FLAG_FUSE_FIRST_POOL = 1u << 8,
-  MPF_FLAG_NO_PDL = 1u << 9
+  MPF_FLAG_FUSE_FIRST_POOL = 1u << 8
 };
 
 /* Geometry of the padded uniform-fragment layout.

@@ -21,7 +21,6 @@
 
 #include "mpf_internal.h"
 #include "numerics.cuh"
-#include "tc_ptx.cuh"
 
 namespace mpf {
 
@@ -43,7 +42,6 @@ constexpr int kFCO = 8;              // maps per thread
 // blockDim.x = 64 strips x n_cog channel groups
 template <int K>
 __global__ void __launch_bounds__(256) conv_first_fwd_kernel(FirstConvArgs a) {
-  ptx::pdl_entry();
   extern __shared__ float sm[];
   constexpr int IW = kFTW + K - 1, IH = kFTH + K - 1;
   const int coutp = a.n_cog * kFCO;
@@ -135,7 +133,6 @@ constexpr int kWCO = 8, kWT = 4;    // accumulators per thread: 8 maps x 4 taps
 // staged delta vector feeds 8 K FMAs instead of 32.
 template <int K, int WT>
 __global__ void __launch_bounds__(256, WT > 4 ? 2 : 3) conv_first_wgrad_kernel(FirstWgradArgs a) {
-  ptx::pdl_entry();
   extern __shared__ float sm[];
   constexpr int kWT = WT;
   constexpr int IW = kWTW + K - 1, IH = kWTH + K - 1;
@@ -263,7 +260,6 @@ __global__ void __launch_bounds__(256, WT > 4 ? 2 : 3) conv_first_wgrad_kernel(F
 // other variant within a thread, then the same fixed-order reductions.
 template <int K>
 __global__ void __launch_bounds__(256, 2) conv_first_wgrad_rows_kernel(FirstWgradArgs a, int TH) {
-  ptx::pdl_entry();
   extern __shared__ float sm[];
   constexpr int IW = kWTW + K - 1;
   const int IH = TH + K - 1;
@@ -394,7 +390,6 @@ constexpr int kCT = 16;  // conv outputs per tile side: (16 - P + 1)^2 pool wind
 
 template <int K, int P>
 __global__ void __launch_bounds__(256, 3) conv_first_mpf_kernel(FirstConvArgs a, MpfArgs m) {
-  ptx::pdl_entry();
   extern __shared__ float smf[];
   constexpr int kPT = kCT - P + 1;                       // pool windows per tile side
   constexpr int RY = kCT, RX = kCT;                      // conv outputs needed by the tile
@@ -503,7 +498,7 @@ cudaError_t fused_kp(FirstConvArgs a, const MpfArgs& m, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   constexpr int kPT = kCT - P + 1;
   dim3 grid((P * m.m_c + kPT - 1) / kPT, (P * m.m_r + kPT - 1) / kPT, a.n);
-  return launch_ex(conv_first_mpf_kernel<K, P>, grid, dim3(256), smem, s, 1, a, m);
+  conv_first_mpf_kernel<K, P><<<grid, 256, smem, s>>>(a, m);
   return cudaGetLastError();
 }
 
@@ -528,7 +523,7 @@ cudaError_t fwd_k(const FirstConvArgs& a, cudaStream_t s) {
                                        (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((a.out_gc + kFTW - 1) / kFTW, (a.out_gr + kFTH - 1) / kFTH, a.n);
-  return launch_ex(conv_first_fwd_kernel<K>, grid, dim3(64 * a.n_cog), smem, s, 1, a);
+  conv_first_fwd_kernel<K><<<grid, 64 * a.n_cog, smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -552,7 +547,7 @@ cudaError_t wgrad_kw(const FirstWgradArgs& a, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(conv_first_wgrad_kernel<K, WT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_ex(conv_first_wgrad_kernel<K, WT>, dim3(a.n_blocks), dim3(256), smem, s, 1, a);
+  conv_first_wgrad_kernel<K, WT><<<a.n_blocks, 256, smem, s>>>(a);
   return cudaGetLastError();
 }
 template <int K>
@@ -568,7 +563,7 @@ cudaError_t wgrad_k(const FirstWgradArgs& a, cudaStream_t s) {
       cudaError_t e = cudaFuncSetAttribute(conv_first_wgrad_rows_kernel<K>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
-      return launch_ex(conv_first_wgrad_rows_kernel<K>, dim3(a.n_blocks), dim3(256), smem, s, 1, a, TH);
+      conv_first_wgrad_rows_kernel<K><<<a.n_blocks, 256, smem, s>>>(a, TH);
       return cudaGetLastError();
     }
   }

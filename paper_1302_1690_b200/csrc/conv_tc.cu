@@ -142,16 +142,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (PAIR) ptx::tmem_alloc_pair(sTmemSlot, p.tmem_cols);
     else ptx::tmem_alloc(sTmemSlot, p.tmem_cols);
   }
+  for (int c = threadIdx.x; c < 256; c += kThreads) s_bias[c] = (p.bias && c < p.cout) ? p.bias[c] : 0.f;
   ptx::tc_fence_before();
   if (PAIR || MC) ptx::cluster_sync_all();  // barrier inits and TMEM allocation visible to the peer
   else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot_ptr;
-  // this CTA holds its TMEM: let the next kernel launch; wait for the previous one's results
-  ptx::pdl_trigger();
-  ptx::pdl_wait();
-  for (int c = threadIdx.x; c < 256; c += kThreads) s_bias[c] = (p.bias && c < p.cout) ? p.bias[c] : 0.f;
-  __syncthreads();
 
   const int k = p.k;
   const bool prof_on = p.prof != nullptr;
@@ -433,16 +429,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc(sTmemSlot, p.tmem_cols);
+  for (int c = threadIdx.x; c < 256; c += kThreads) s_bias[c] = (p.bias && c < p.cout) ? p.bias[c] : 0.f;
   ptx::tc_fence_before();
   if (MC) ptx::cluster_sync_all();  // the peer's barriers exist before anything is multicast
   else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot_ptr;
-  // this CTA holds its TMEM: let the next kernel launch; wait for the previous one's results
-  ptx::pdl_trigger();
-  ptx::pdl_wait();
-  for (int c = threadIdx.x; c < 256; c += kThreads) s_bias[c] = (p.bias && c < p.cout) ? p.bias[c] : 0.f;
-  __syncthreads();
   const int rank = MC ? (int)ptx::cluster_rank() : 0;
   const int first = MC ? (int)(blockIdx.x >> 1) * 2 + rank : (int)blockIdx.x;
   const int stride = MC ? (int)(gridDim.x >> 1) * 2 : (int)gridDim.x;
@@ -734,14 +726,26 @@ cudaError_t launch_nacc(const CUtensorMap& A, const CUtensorMap& B, const CUtens
   if (e != cudaSuccess) return e;
   if (!PAIR && !MC) {
     const int grid = p.n_tiles < num_sms() ? p.n_tiles : num_sms();
-    e = launch_ex(kern, dim3(grid), dim3(kThreads), smem, s, 1, A, B, O, p);
+    kern<<<grid, kThreads, smem, s>>>(A, B, O, p);
     prof_report(p, NACC, PAIR, grid);
-    return e;
+    return cudaGetLastError();
   }
   // pairs of CTAs: a cta_group::2 pair per tile, or (MC) two single-CTA tiles in lockstep
   const int units = MC ? (p.n_tiles + 1) / 2 : p.n_tiles;
   const int pairs = units < num_sms() / 2 ? units : num_sms() / 2;
-  e = launch_ex(kern, dim3(2 * pairs), dim3(kThreads), smem, s, 2, A, B, O, p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, A, B, O, p);
   if (e != cudaSuccess) return e;
   prof_report(p, NACC, PAIR, 2 * pairs);
   return cudaGetLastError();
@@ -840,10 +844,27 @@ static cudaError_t launch_conv_ntap(const TcConvArgs& a, cudaStream_t s, int* gr
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e2 != cudaSuccess) return e2;
-    if (!mc) return launch_ex(kern, dim3(grid), dim3(kThreads), smem, s, 1, A, B, O, O3, p);
-    const int units = (p.n_tiles + 1) / 2;
-    const int pairs = units < num_sms() / 2 ? units : num_sms() / 2;
-    return launch_ex(kern, dim3(2 * pairs), dim3(kThreads), smem, s, 2, A, B, O, O3, p);
+    if (!mc) {
+      kern<<<grid, kThreads, smem, s>>>(A, B, O, O3, p);
+    } else {
+      const int units = (p.n_tiles + 1) / 2;
+      const int pairs = units < num_sms() / 2 ? units : num_sms() / 2;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(2 * pairs, 1, 1);
+      cfg.blockDim = dim3(kThreads, 1, 1);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      e2 = cudaLaunchKernelEx(&cfg, kern, A, B, O, O3, p);
+      if (e2 != cudaSuccess) return e2;
+    }
+    return cudaGetLastError();
   };
 #define MPF_NTAP_CASE(KK) \
   case KK: return mc ? go(conv_tc_ntap_kernel<KK, true>) : go(conv_tc_ntap_kernel<KK, false>);
@@ -1038,9 +1059,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot_ptr;
-  // this CTA holds its TMEM: let the next kernel launch; wait for the previous one's results
-  ptx::pdl_trigger();
-  ptx::pdl_wait();
   const int n_st = p.chunk_stages;
   const int rank = CS > 1 ? (int)ptx::cluster_rank() : 0;
 
@@ -1174,9 +1192,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::cluster_sync_all();  // barrier inits and TMEM allocation visible to the peer
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot_ptr;
-  // this CTA holds its TMEM: let the next kernel launch; wait for the previous one's results
-  ptx::pdl_trigger();
-  ptx::pdl_wait();
   const int n_st = p.chunk_stages;
 
   if (warp == 0) {
@@ -1302,9 +1317,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot_ptr;
-  // this CTA holds its TMEM: let the next kernel launch; wait for the previous one's results
-  ptx::pdl_trigger();
-  ptx::pdl_wait();
   const int n_st = p.chunk_stages;
   const int n_datoms = (p.npad + 31) / 32;
 
@@ -1450,7 +1462,21 @@ static cudaError_t launch_wgrad_pair(const TcWgradArgs& a, int* splits_out, cuda
   const size_t smem = 1024 + (size_t)p.n_stages_ring * p.stage_bytes + 256;
   e = cudaFuncSetAttribute(wgrad_tc_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_ex(wgrad_tc_pair_kernel, dim3(2 * splits * p.n_sets), dim3(kThreads), smem, s, 2, D, X, p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * splits * p.n_sets, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, wgrad_tc_pair_kernel, D, X, p);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
 }
 
 // the swapped-role plan for C_out <= 64: returns the number of M-tiles (0 = not applicable)
@@ -1511,7 +1537,8 @@ static cudaError_t launch_wgrad_swap(const TcWgradArgs& a, WgSwapParams& p, int*
   const size_t smem = 1024 + (size_t)p.n_stages_ring * p.stage_bytes + 3 * p.b_bytes + 256;
   e = cudaFuncSetAttribute(wgrad_tc_swap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_ex(wgrad_tc_swap_kernel, dim3(splits), dim3(kThreads), smem, s, 1, D, X, p);
+  wgrad_tc_swap_kernel<<<splits, kThreads, smem, s>>>(D, X, p);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits_out, cudaStream_t s) {
@@ -1579,7 +1606,25 @@ cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits_out, cudaStream_t 
   auto kern = pick();
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_ex(kern, dim3(splits * per_split_blocks), dim3(kThreads), smem, s, cs, D, X, p);
+  if (cs == 1) {
+    kern<<<splits * per_split_blocks, kThreads, smem, s>>>(D, X, p);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(splits * per_split_blocks, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, D, X, p);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
 }
 
 }  // namespace mpf

@@ -59,7 +59,6 @@ __host__ __device__ inline size_t head_region0(int C, int Ch) {
 // W_L row fetch per 4 channels), which halves the instruction count per element.
 template <int NC, bool TRAIN, bool TANH, bool VEC>
 __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
-  ptx::pdl_entry();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int C = a.C, Ch = a.Ch;
   const size_t tile_bytes = (size_t)kTP * Ch * sizeof(float);
@@ -502,7 +501,7 @@ cudaError_t launch_k(const HeadArgs& a, size_t smem, cudaStream_t s) {
   auto kern = (a.Ch % 4 == 0) ? head_kernel<NC, TRAIN, TANH, true> : head_kernel<NC, TRAIN, TANH, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_ex(kern, dim3(a.n_blocks), dim3(kThr), smem, s, 1, a);
+  kern<<<a.n_blocks, kThr, smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -517,7 +516,6 @@ cudaError_t launch_nc(const HeadArgs& a, size_t smem, cudaStream_t s) {
 // the fragment -> pixel map (head_label; R2, R7), so the head reads 64 contiguous bytes
 // per tile instead of decoding the mixed-radix index per position.
 __global__ void label_frag_kernel(HeadArgs a, uint8_t* __restrict__ out, long long per_img, int frag_sz) {
-  ptx::pdl_entry();
   const long long total = (long long)a.n * per_img;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
@@ -557,7 +555,7 @@ cudaError_t launch_label_frag(const HeadArgs& a, uint8_t* out, cudaStream_t s) {
   const long long per_img = (long long)a.F * a.gr * a.gc;
   const long long total = (long long)a.n * per_img;
   const long long blocks = (total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16;
-  return launch_ex(label_frag_kernel, dim3((unsigned)(blocks < 1 ? 1 : blocks)), dim3(256), 0, s, 1, a, out, per_img, a.gr * a.gc);
+  label_frag_kernel<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(a, out, per_img, a.gr * a.gc);
   return cudaGetLastError();
 }
 

@@ -11,7 +11,6 @@
 
 #include "mpf_internal.h"
 #include "numerics.cuh"
-#include "tc_ptx.cuh"
 
 namespace mpf {
 
@@ -39,7 +38,6 @@ constexpr int kTW = 16, kTH = 16, kCOT = 8, kCIC = 8;
 
 template <int IMG>
 __global__ void __launch_bounds__(256) conv_simt_kernel(ConvArgs a, int tiles_x) {
-  ptx::pdl_entry();
   extern __shared__ float sm[];
   const int k = a.k;
   const int IW = kTW + k - 1, IH = kTH + k - 1;
@@ -113,10 +111,10 @@ cudaError_t launch_conv_simt(const ConvArgs& a, cudaStream_t s) {
   const size_t smem = sizeof(float) * (kCIC * IH * IW + kCOT * a.k * a.k * kCIC);
   if (a.image_mode) {
     cudaFuncSetAttribute(conv_simt_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    return launch_ex(conv_simt_kernel<1>, grid, dim3(256), smem, s, 1, a, tiles_x);
+    conv_simt_kernel<1><<<grid, 256, smem, s>>>(a, tiles_x);
   } else {
     cudaFuncSetAttribute(conv_simt_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    return launch_ex(conv_simt_kernel<0>, grid, dim3(256), smem, s, 1, a, tiles_x);
+    conv_simt_kernel<0><<<grid, 256, smem, s>>>(a, tiles_x);
   }
   return cudaGetLastError();
 }
@@ -130,7 +128,6 @@ constexpr int kWP = 32;  // positions per smem stage
 template <int IMG>
 __global__ void __launch_bounds__(256) wgrad_simt_kernel(WgradArgs a, long long chunk, int co_tiles,
                                                           long long P_total) {
-  ptx::pdl_entry();
   __shared__ float s_d[kWP][17];
   __shared__ float s_x[kWP][17];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -204,15 +201,14 @@ cudaError_t launch_wgrad_simt(const WgradArgs& a, cudaStream_t s) {
   const long long chunk = (P_total + a.n_split - 1) / a.n_split;
   dim3 grid(co_tiles * k_tiles, a.n_split);
   if (a.image_mode)
-    return launch_ex(wgrad_simt_kernel<1>, grid, dim3(256), 0, s, 1, a, chunk, co_tiles, P_total);
+    wgrad_simt_kernel<1><<<grid, 256, 0, s>>>(a, chunk, co_tiles, P_total);
   else
-    return launch_ex(wgrad_simt_kernel<0>, grid, dim3(256), 0, s, 1, a, chunk, co_tiles, P_total);
+    wgrad_simt_kernel<0><<<grid, 256, 0, s>>>(a, chunk, co_tiles, P_total);
   return cudaGetLastError();
 }
 
 __global__ void wgrad_reduce_kernel(const float* __restrict__ pw, const float* __restrict__ pb, int n_split,
                                     int cout, int cin, int k, float* gw, float* gb) {
-  ptx::pdl_entry();
   const int K = k * k * cin;
   const long long total = (long long)cout * K + (pb ? cout : 0);
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
@@ -237,7 +233,7 @@ cudaError_t launch_wgrad_reduce(const float* pw, const float* pb, int n_split, i
                                 float* gw, float* gb, cudaStream_t s) {
   const long long total = (long long)cout * k * k * cin + (pb ? cout : 0);
   int blocks = (int)mpf_min_ll((total + 255) / 256, 4096);
-  return launch_ex(wgrad_reduce_kernel, dim3(blocks), dim3(256), 0, s, 1, pw, pb, n_split, cout, cin, k, gw, gb);
+  wgrad_reduce_kernel<<<blocks, 256, 0, s>>>(pw, pb, n_split, cout, cin, k, gw, gb);
   return cudaGetLastError();
 }
 
@@ -441,7 +437,6 @@ cudaError_t launch_mirror_pad(const float* in, float* out, long long planes, int
 // labelled pixels per image: integer partial counts combined with integer atomics
 // (exact, order-independent)
 __global__ void label_count_kernel(const uint8_t* __restrict__ labels, int hw, int classes, int* nlab) {
-  ptx::pdl_entry();
   __shared__ int s_red[32];
   const int img = blockIdx.y;
   int c = 0;
@@ -487,14 +482,13 @@ cudaError_t launch_label_count(const uint8_t* labels, int n, int hw, int classes
   if (e != cudaSuccess) return e;
   int bx = (hw + 256 * 16 - 1) / (256 * 16);
   if (bx > 64) bx = 64;
-  return launch_ex(label_count_kernel, dim3(bx, n), dim3(256), 0, s, 1, labels, hw, classes, nlab);
+  label_count_kernel<<<dim3(bx, n), 256, 0, s>>>(labels, hw, classes, nlab);
   return cudaGetLastError();
 }
 
 // per-image loss = (sum of the per-tile partials, fixed tree order) / n_lab
 __global__ void loss_finalize_kernel(const float* __restrict__ part, int parts, const int* __restrict__ nlab,
                                      float* loss) {
-  ptx::pdl_entry();
   __shared__ float s[256];
   const int img = blockIdx.x;
   float t = 0.f;
@@ -510,12 +504,11 @@ __global__ void loss_finalize_kernel(const float* __restrict__ part, int parts, 
 
 cudaError_t launch_loss_finalize(const float* part, int parts, const int* nlab, int n, float* loss,
                                  cudaStream_t s) {
-  return launch_ex(loss_finalize_kernel, dim3(n), dim3(256), 0, s, 1, part, parts, nlab, loss);
+  loss_finalize_kernel<<<n, 256, 0, s>>>(part, parts, nlab, loss);
   return cudaGetLastError();
 }
 
 __global__ void sgd_kernel(float* __restrict__ p, float* __restrict__ g, long long n, float step) {
-  ptx::pdl_entry();
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
        e += (long long)gridDim.x * blockDim.x) {
     p[e] -= step * g[e];
@@ -525,14 +518,13 @@ __global__ void sgd_kernel(float* __restrict__ p, float* __restrict__ g, long lo
 
 cudaError_t launch_sgd(float* params, float* grads, long long n, float lr, float scale, cudaStream_t s) {
   const int blocks = (int)mpf_min_ll((n + 255) / 256, 1024);
-  return launch_ex(sgd_kernel, dim3(blocks), dim3(256), 0, s, 1, params, grads, n, lr * scale);
+  sgd_kernel<<<blocks, 256, 0, s>>>(params, grads, n, lr * scale);
   return cudaGetLastError();
 }
 
 // canonical W[co][ci][ky][kx] -> fwd pack [co][ky][kx][ci], dgrad pack [ci][k-1-ky][k-1-kx][co]
 __global__ void pack_kernel(const float* __restrict__ w, int cout, int cin, int k, float* wp, float* dp,
                             int round_fwd, int round_dgrad) {
-  ptx::pdl_entry();
   const long long n = (long long)cout * cin * k * k;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
        e += (long long)gridDim.x * blockDim.x) {
@@ -552,7 +544,7 @@ cudaError_t launch_pack_weights(const float* w, int cout, int cin, int k, float*
                                 int round_dgrad, cudaStream_t s) {
   const long long n = (long long)cout * cin * k * k;
   const int blocks = (int)mpf_min_ll((n + 255) / 256, 1024);
-  return launch_ex(pack_kernel, dim3(blocks), dim3(256), 0, s, 1, w, cout, cin, k, wp, dp, round_fwd, round_dgrad);
+  pack_kernel<<<blocks, 256, 0, s>>>(w, cout, cin, k, wp, dp, round_fwd, round_dgrad);
   return cudaGetLastError();
 }
 

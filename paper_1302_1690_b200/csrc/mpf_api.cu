@@ -22,7 +22,6 @@
 namespace mpf {
 
 static thread_local std::string g_err = "no error";
-bool g_pdl = true;  // programmatic dependent launch of the hot-path kernels (MPF_FLAG_NO_PDL: off)
 void set_error(const std::string& m) { g_err = m; }
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -60,7 +59,6 @@ static void prof_rec(Net* N, cudaStream_t s, int e0, const char* name, int layer
 // every kernel launch of the path goes through LAUNCH (timed when profiling is on)
 #define LAUNCH(N, s, name, layer, flops, bytes, call)            \
   do {                                                           \
-    g_pdl = !((N)->cfg.flags & MPF_FLAG_NO_PDL);                 \
     const int _e0 = prof_mark((N), (s));                         \
     MPF_CUDA(call);                                              \
     prof_rec((N), (s), _e0, (name), (layer), (flops), (bytes));  \
@@ -1365,8 +1363,7 @@ mpf_status mpf_net_set_grad_hook(mpf_net* N, mpf_grad_ready_fn fn, void* user) {
 mpf_status mpf_net_set_flags(mpf_net* N, uint32_t flags) {
   if (!N) return fail(MPF_ERR_ARG, "NULL net");
   const uint32_t known = MPF_FLAG_SERIAL | MPF_FLAG_TC_SINGLE | MPF_FLAG_TC_PAIR | MPF_FLAG_NTAP_ON | MPF_FLAG_NTAP_OFF |
-                         MPF_FLAG_NTAP_NO_MC | MPF_FLAG_WGRAD_M128 | MPF_FLAG_ROLE_TIMERS | MPF_FLAG_FUSE_FIRST_POOL |
-                         MPF_FLAG_NO_PDL;
+                         MPF_FLAG_NTAP_NO_MC | MPF_FLAG_WGRAD_M128 | MPF_FLAG_ROLE_TIMERS | MPF_FLAG_FUSE_FIRST_POOL;
   if (flags & ~known) return fail(MPF_ERR_ARG, "unknown MPF_FLAG_* bits");
   if ((flags & MPF_FLAG_NTAP_ON) && (flags & MPF_FLAG_NTAP_OFF)) return fail(MPF_ERR_ARG, "NTAP_ON with NTAP_OFF");
   if ((flags & MPF_FLAG_TC_PAIR) && (flags & MPF_FLAG_TC_SINGLE)) return fail(MPF_ERR_ARG, "TC_PAIR with TC_SINGLE");

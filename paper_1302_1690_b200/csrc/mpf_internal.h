@@ -96,41 +96,6 @@ struct Net {
   bool have_fwd = false;
 };
 
-// ---------------------------------------------------------------- kernel launch
-// Hot-path kernels are launched with programmatic dependent launch: the next kernel of the
-// stream is scheduled while this one drains (its prologue - barrier init, TMEM allocation,
-// tensor-map prefetch - overlaps the tail), and waits (griddepcontrol.wait, pdl_wait in
-// tc_ptx.cuh) before touching this one's results.  g_pdl = false (MPF_FLAG_NO_PDL, set per
-// call by the entry points) launches them plainly.  cluster > 1 adds a cluster dimension.
-extern bool g_pdl;
-template <typename... KArgs, typename... Args>
-inline cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, int cluster,
-                             Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[2];
-  int na = 0;
-  if (g_pdl) {
-    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[na].val.programmaticStreamSerializationAllowed = 1;
-    ++na;
-  }
-  if (cluster > 1) {
-    attr[na].id = cudaLaunchAttributeClusterDimension;
-    attr[na].val.clusterDim.x = cluster;
-    attr[na].val.clusterDim.y = 1;
-    attr[na].val.clusterDim.z = 1;
-    ++na;
-  }
-  cfg.attrs = attr;
-  cfg.numAttrs = na;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args...);
-  return e != cudaSuccess ? e : cudaGetLastError();
-}
-
 // ---------------------------------------------------------------- kernels (launchers)
 // All launchers enqueue on `s` and return cudaGetLastError().
 

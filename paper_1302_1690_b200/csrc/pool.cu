@@ -27,7 +27,6 @@
 
 #include "mpf_internal.h"
 #include "numerics.cuh"
-#include "tc_ptx.cuh"
 
 namespace mpf {
 
@@ -91,7 +90,6 @@ int block_dims(int C, int V, dim3* blk) {
 // ----------------------------------------------------------------------------- forward
 template <int K, int V>
 __global__ void __launch_bounds__(256, K <= 3 ? 4 : 2) mpf_fwd_kernel(MpfArgs a) {
-  ptx::pdl_entry();
   const int cv = threadIdx.x;
   const int X = blockIdx.x * blockDim.y + threadIdx.y;
   const int Xw = K * a.m_c, Yw = K * a.m_r;
@@ -171,14 +169,13 @@ cudaError_t fwd_launch(const MpfArgs& a, cudaStream_t s) {
   const int ty = block_dims(a.C, V, &blk);
   const int Xw = K * a.m_c, Yw = K * a.m_r;
   dim3 grid((Xw + ty - 1) / ty, (Yw + kBand - 1) / kBand, a.n_frag_in < 65535 ? a.n_frag_in : 65535);
-  return launch_ex(mpf_fwd_kernel<K, V>, grid, blk, 0, s, 1, a);
+  mpf_fwd_kernel<K, V><<<grid, blk, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 // generic k (any pooling factor): plain k x k scan per window
 template <int V>
 __global__ void __launch_bounds__(256) mpf_fwd_generic_kernel(MpfArgs a) {
-  ptx::pdl_entry();
   const int cv = threadIdx.x;
   const int K = a.k;
   const int X = blockIdx.x * blockDim.y + threadIdx.y;
@@ -223,14 +220,13 @@ cudaError_t fwd_dispatch(const MpfArgs& a, cudaStream_t s) {
   const int ty = block_dims(a.C, V, &blk);
   const int Xw = a.k * a.m_c, Yw = a.k * a.m_r;
   dim3 grid((Xw + ty - 1) / ty, (Yw + kBand - 1) / kBand, a.n_frag_in < 65535 ? a.n_frag_in : 65535);
-  return launch_ex(mpf_fwd_generic_kernel<V>, grid, blk, 0, s, 1, a);
+  mpf_fwd_generic_kernel<V><<<grid, blk, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 // ----------------------------------------------------------------------------- backward
 template <int V>
 __global__ void __launch_bounds__(256) mpf_bwd_kernel(MpfBwdArgs a) {
-  ptx::pdl_entry();
   extern __shared__ float s_red[];  // [blockDim.y][C]
   const int cv = threadIdx.x;
   const int K = a.k, KK = K * K;
@@ -328,7 +324,6 @@ __host__ __device__ constexpr int tile_cells_padded(int wy, int wx) { return (wy
 
 template <int K, int kTBY, int kTBX>
 __global__ void __launch_bounds__(256) mpf_bwd_tile_kernel(MpfBwdArgs a, int rows_per_cta, int nbuf) {
-  ptx::pdl_entry();
   extern __shared__ __align__(16) uint8_t sm_raw[];
   constexpr int WY = kTBY + K - 1, WX = kTBX + K - 1, S = tile_cells_padded(WY, WX);
   const int C = a.C, CV = C / 4, CVP = (CV + 3) & ~3;
@@ -488,7 +483,6 @@ __global__ void __launch_bounds__(256) mpf_bwd_tile_kernel(MpfBwdArgs a, int row
 // the other MPF backward kernels (bitwise-identical results).  No shared-memory staging,
 // no barriers; CTAs stride over groups of consecutive blocks of one row.
 __global__ void __launch_bounds__(256, 3) mpf_bwd_block2_kernel(MpfBwdArgs a, long long n_groups) {
-  ptx::pdl_entry();
   const int C = a.C, CV = C / 4;
   const int tid = threadIdx.x, cv = tid % CV, sub = tid / CV, nsub = 256 / CV;
   const int Xw = 2 * a.m_c, Yw = 2 * a.m_r;
@@ -585,7 +579,6 @@ __global__ void __launch_bounds__(256, 3) mpf_bwd_block2_kernel(MpfBwdArgs a, lo
 // Same fixed (dy, dx) order as the other MPF backward kernels (bitwise-identical results).
 template <int K, int BW>  // k and block width in output columns (patch (2k-1) x (BW+k-1))
 __global__ void __launch_bounds__(256) mpf_bwd_block3_kernel(MpfBwdArgs a, long long n_groups) {
-  ptx::pdl_entry();
   constexpr int PW = BW + K - 1;
   const int C = a.C, CV = C / 4;
   const int tid = threadIdx.x, cv = tid % CV, sub = tid / CV, nsub = 256 / CV;
@@ -675,7 +668,6 @@ __global__ void __launch_bounds__(256) mpf_bwd_block3_kernel(MpfBwdArgs a, long 
 template <int V>
 __global__ void __launch_bounds__(256) channel_partial_kernel(const float* __restrict__ dy, long long P, int C,
                                                               long long rows_per_block, float* part) {
-  ptx::pdl_entry();
   extern __shared__ float s_red[];
   const int cv = threadIdx.x;
   const long long r0 = (long long)blockIdx.x * rows_per_block;
@@ -704,7 +696,6 @@ __global__ void __launch_bounds__(256) channel_partial_kernel(const float* __res
 // dst[e] += sum_{b < nb} part[b][e], e < E, in a fixed order (deterministic).
 __global__ void __launch_bounds__(256) partial_reduce_kernel(const float* __restrict__ part, int nb, int E,
                                                              float* dst, float* dst2, int split_at) {
-  ptx::pdl_entry();
   __shared__ float s[256];
   const int e = blockIdx.x;
   float t = 0.f;
@@ -787,7 +778,7 @@ static cudaError_t launch_tile_k(const MpfBwdArgs& a, dim3 grid, dim3 blk, size_
   if (ty == TY && tx == TX) {                                                                                   \
     e = cudaFuncSetAttribute(mpf_bwd_tile_kernel<K, TY, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
     if (e != cudaSuccess) return e;                                                                             \
-    return launch_ex(mpf_bwd_tile_kernel<K, TY, TX>, grid, blk, sm, s, 1, a, kTileRows, tile_nbuf());                      \
+    mpf_bwd_tile_kernel<K, TY, TX><<<grid, blk, sm, s>>>(a, kTileRows, tile_nbuf());                                          \
     return cudaGetLastError();                                                                                  \
   }
   MPF_TILE_CASE(8, 8)
@@ -821,8 +812,8 @@ long long mpf_bwd_partials(const MpfBwdArgs& a) {
 cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s) {
   if (bwd_block2(a)) {
     const size_t smem = 0;
-    if (a.k == 2) return launch_ex(mpf_bwd_block2_kernel, dim3(block2_grid(a)), dim3(256), smem, s, 1, a, block2_groups(a));
-    return launch_ex(mpf_bwd_block3_kernel<3, 3>, dim3(block2_grid(a)), dim3(256), smem, s, 1, a, block2_groups(a));
+    if (a.k == 2) mpf_bwd_block2_kernel<<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
+    else mpf_bwd_block3_kernel<3, 3><<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
     return cudaGetLastError();
   }
   const int V = a.C % 4 == 0 ? 4 : 1;
@@ -836,9 +827,9 @@ cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s) {
   }
   const size_t smem = sizeof(float) * blk.y * a.C;
   if (V == 4)
-    return launch_ex(mpf_bwd_kernel<4>, grid, blk, smem, s, 1, a);
+    mpf_bwd_kernel<4><<<grid, blk, smem, s>>>(a);
   else
-    return launch_ex(mpf_bwd_kernel<1>, grid, blk, smem, s, 1, a);
+    mpf_bwd_kernel<1><<<grid, blk, smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -857,16 +848,16 @@ cudaError_t launch_channel_partial(const float* dy, long long P, int C, float* p
   block_dims(C, V, &blk);
   const size_t smem = sizeof(float) * blk.y * C;
   if (V == 4)
-    return launch_ex(channel_partial_kernel<4>, dim3((unsigned)nb), blk, smem, s, 1, dy, P, C, rows, part);
+    channel_partial_kernel<4><<<(unsigned)nb, blk, smem, s>>>(dy, P, C, rows, part);
   else
-    return launch_ex(channel_partial_kernel<1>, dim3((unsigned)nb), blk, smem, s, 1, dy, P, C, rows, part);
+    channel_partial_kernel<1><<<(unsigned)nb, blk, smem, s>>>(dy, P, C, rows, part);
   return cudaGetLastError();
 }
 
 cudaError_t launch_partial_reduce(const float* part, int nb, int E, float* dst, float* dst2, int split_at,
                                   cudaStream_t s) {
   if (E <= 0) return cudaSuccess;
-  return launch_ex(partial_reduce_kernel, dim3(E), dim3(256), 0, s, 1, part, nb, E, dst, dst2, split_at);
+  partial_reduce_kernel<<<E, 256, 0, s>>>(part, nb, E, dst, dst2, split_at);
   return cudaGetLastError();
 }
 

@@ -52,17 +52,6 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* m, 
       : "memory");
 }
 
-// Programmatic dependent launch (kernels launched with launch_ex, mpf_internal.h): let the
-// next kernel of the stream start launching (its CTAs then wait in pdl_wait), and wait until
-// the previous kernel of the stream has completed and its writes are visible.  Every kernel
-// launched through launch_ex calls pdl_wait() before it reads anything a previous kernel wrote.
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_entry() {
-  pdl_trigger();
-  pdl_wait();
-}
-
 // 3-D TMA tile load global -> shared, completes `bar` with the box's bytes (out-of-bounds
 // elements are zero-filled and still counted).
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1, int c2) {

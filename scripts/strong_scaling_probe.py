@@ -19,8 +19,8 @@ import mpf_synth as S  # noqa: E402
 from paper_1302_1690_b200.net import MPFNet  # noqa: E402
 
 
-def time_step(cfg, n, steps=5, warmup=3, graph=False, flags=0):
-    net = MPFNet(cfg.layers, cfg.P, cfg.H, cfg.W, max_images=n, flags=flags)
+def time_step(cfg, n, steps=5, warmup=3, graph=False):
+    net = MPFNet(cfg.layers, cfg.P, cfg.H, cfg.W, max_images=n)
     net.set_params(S.init_params(cfg).astype(np.float32))
     im, lb = S.make_batch(cfg, list(range(n)))
     img, lab = torch.tensor(im, device="cuda"), torch.tensor(lb, device="cuda")
@@ -52,15 +52,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="cfg4")
     ap.add_argument("--graph", action="store_true", help="time CUDA-graph replays of the step")
-    ap.add_argument("--flags", type=lambda v: int(v, 0), default=0, help="MPF_FLAG_* of the net")
     a = ap.parse_args()
     cfg = S.CONFIGS[a.workload]
     B = cfg.global_batch
-    t_full = time_step(cfg, B, graph=a.graph, flags=a.flags)
-    tag = (" (graph)" if a.graph else "") + (f" flags=0x{a.flags:x}" if a.flags else "")
+    t_full = time_step(cfg, B, graph=a.graph)
     for N in (2, 4, 8):
-        t = time_step(cfg, B // N, graph=a.graph, flags=a.flags)
-        print(f"{a.workload}{tag}: N={N} per-GPU {B // N} images {t:.3f} ms vs "
+        t = time_step(cfg, B // N, graph=a.graph)
+        print(f"{a.workload}{' (graph)' if a.graph else ''}: N={N} per-GPU {B // N} images {t:.3f} ms vs "
               f"{t_full:.3f} ms for {B}: efficiency {t_full / (N * t):.3f}")
 
 
