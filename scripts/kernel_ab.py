@@ -23,12 +23,13 @@ def main():
     ap.add_argument("--match", nargs="*", default=[])
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--json", default="")
+    ap.add_argument("--images", type=int, default=0, help="0 = the config's global batch")
     a = ap.parse_args()
     import torch
     from paper_1302_1690_b200 import _lib as L
     from paper_1302_1690_b200.net import MPFNet
     cfg = S.CONFIGS[a.workload]
-    B = cfg.global_batch
+    B = a.images or cfg.global_batch
     im, lb = S.make_batch(cfg, list(range(B)))
     img, lab = torch.tensor(im, device="cuda"), torch.tensor(lb, device="cuda")
     net = MPFNet(cfg.layers, cfg.P, cfg.H, cfg.W, max_images=B)
