@@ -207,33 +207,63 @@ cudaError_t launch_wgrad_simt(const WgradArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-__global__ void wgrad_reduce_kernel(const float* __restrict__ pw, const float* __restrict__ pb, int n_split,
-                                    int cout, int cin, int k, float* gw, float* gb) {
+// gw (+)= sum_i pw[i] over n_split partials [n_split][cout][K] (K = (ky, kx, ci)), fixed order.
+// A block owns 32 V consecutive partial elements (V = 4: float4 lanes when the partial rows
+// are 16-byte aligned); warp w sums splits w, w + 8, ... (four interleaved accumulators, one
+// coalesced 32 V-float read per split), and the 8 warp sums meet in shared memory in order.
+template <int V>
+__global__ void __launch_bounds__(256) wgrad_reduce_kernel(const float* __restrict__ pw, int n_split, int cout,
+                                                           int cin, int k, float* gw) {
+  __shared__ float red[8][32 * V + 1];
   const int K = k * k * cin;
-  const long long total = (long long)cout * K + (pb ? cout : 0);
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    if (e < (long long)cout * K) {
-      const int co = (int)(e / K), kidx = (int)(e % K);
-      float s = 0.f;
-      for (int i = 0; i < n_split; ++i) s += pw[((long long)i * cout + co) * K + kidx];  // fixed order
-      const int ci = kidx % cin, q = kidx / cin;
-      const int ky = q / k, kx = q % k;
-      gw[(((long long)co * cin + ci) * k + ky) * k + kx] += s;
-    } else {
-      const int co = (int)(e - (long long)cout * K);
-      float s = 0.f;
-      for (int i = 0; i < n_split; ++i) s += pb[(long long)i * cout + co];
-      gb[co] += s;
+  const long long total = (long long)cout * K;
+  const int c = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long long e0 = (blockIdx.x * 32LL + c) * V;
+  float t[4][V];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < V; ++v) t[u][v] = 0.f;
+  if (e0 < total) {
+    auto ld = [&](int i, float (&acc)[V]) {
+      const float* src = pw + (long long)i * total + e0;
+      if constexpr (V == 4) {
+        const float4 q = __ldcg(reinterpret_cast<const float4*>(src));
+        acc[0] += q.x; acc[1] += q.y; acc[2] += q.z; acc[3] += q.w;
+      } else {
+        acc[0] += __ldcg(src);
+      }
+    };
+    int i = w;
+    for (; i + 24 < n_split; i += 32) {
+      ld(i, t[0]); ld(i + 8, t[1]); ld(i + 16, t[2]); ld(i + 24, t[3]);
     }
+    for (; i < n_split; i += 8) ld(i, t[0]);
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v) red[w][c * V + v] = (t[0][v] + t[1][v]) + (t[2][v] + t[3][v]);
+  __syncthreads();
+  for (int j = threadIdx.x; j < 32 * V; j += 256) {
+    const long long e = blockIdx.x * 32LL * V + j;
+    if (e >= total) continue;
+    float s = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += red[q][j];
+    const int co = (int)(e / K), kidx = (int)(e % K);
+    const int ci = kidx % cin, q = kidx / cin;
+    const int ky = q / k, kx = q % k;
+    gw[(((long long)co * cin + ci) * k + ky) * k + kx] += s;
   }
 }
 
-cudaError_t launch_wgrad_reduce(const float* pw, const float* pb, int n_split, int cout, int cin, int k,
-                                float* gw, float* gb, cudaStream_t s) {
-  const long long total = (long long)cout * k * k * cin + (pb ? cout : 0);
-  int blocks = (int)mpf_min_ll((total + 255) / 256, 4096);
-  wgrad_reduce_kernel<<<blocks, 256, 0, s>>>(pw, pb, n_split, cout, cin, k, gw, gb);
+cudaError_t launch_wgrad_reduce(const float* pw, int n_split, int cout, int cin, int k, float* gw,
+                                cudaStream_t s) {
+  const long long total = (long long)cout * k * k * cin;
+  if (total <= 0) return cudaSuccess;
+  if (total % 4 == 0 && ((uintptr_t)pw & 15) == 0)
+    wgrad_reduce_kernel<4><<<(unsigned)((total + 127) / 128), 256, 0, s>>>(pw, n_split, cout, cin, k, gw);
+  else
+    wgrad_reduce_kernel<1><<<(unsigned)((total + 31) / 32), 256, 0, s>>>(pw, n_split, cout, cin, k, gw);
   return cudaGetLastError();
 }
 
@@ -441,14 +471,30 @@ __global__ void label_count_kernel(const uint8_t* __restrict__ labels, int hw, i
   const int img = blockIdx.y;
   int c = 0;
   const uint8_t* L = labels + (long long)img * hw;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < hw; e += gridDim.x * blockDim.x) c += L[e] < classes;
+  const int stride = gridDim.x * blockDim.x;
+  int head = 0;  // bytes before the first 16-byte aligned address
+  if (((uintptr_t)L & 15) != 0) head = min(hw, (int)(16 - ((uintptr_t)L & 15)));
+  const int nv = (hw - head) >> 4;
+  const uint4* V = reinterpret_cast<const uint4*>(L + head);
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += stride) {
+    const uint4 q = __ldg(V + v);
+    const uint32_t wd[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) c += (int)((wd[j] >> (8 * b)) & 255u) < classes;
+  }
+  const int tail0 = head + (nv << 4);
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < head) c += L[g] < classes;
+  if (g < hw - tail0) c += L[tail0 + g] < classes;
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = c;
   __syncthreads();
   if (threadIdx.x == 0) {
     int t = 0;
     for (int w = 0; w < (int)(blockDim.x / 32); ++w) t += s_red[w];
-    atomicAdd(nlab + img, t);
+    if (t) atomicAdd(nlab + img, t);
   }
 }
 
@@ -480,31 +526,58 @@ cudaError_t launch_class_hist(const uint8_t* labels, long long total, int classe
 cudaError_t launch_label_count(const uint8_t* labels, int n, int hw, int classes, int* nlab, cudaStream_t s) {
   cudaError_t e = cudaMemsetAsync(nlab, 0, sizeof(int) * n, s);
   if (e != cudaSuccess) return e;
-  int bx = (hw + 256 * 16 - 1) / (256 * 16);
-  if (bx > 64) bx = 64;
+  if (hw <= 0) return cudaSuccess;
+  // 16 labels per thread per pass; about 4 resident blocks per SM over the whole batch
+  int bx = (int)mpf_min_ll(((long long)hw + 256 * 16 * 2 - 1) / (256 * 16 * 2), (148 * 4 + n - 1) / n);
+  if (bx < 1) bx = 1;
   label_count_kernel<<<dim3(bx, n), 256, 0, s>>>(labels, hw, classes, nlab);
   return cudaGetLastError();
 }
 
-// per-image loss = (sum of the per-tile partials, fixed tree order) / n_lab
-__global__ void loss_finalize_kernel(const float* __restrict__ part, int parts, const int* __restrict__ nlab,
-                                     float* loss) {
+// per-image loss = (sum of the per-tile partials, fixed order) / n_lab.  Grid (chunks, n):
+// block (ch, img) sums parts [ch*len, (ch+1)*len) of its image (fixed tree), writes
+// tmp[img][ch]; the last block of an image (cnt[img], reset afterwards) sums the chunks in order.
+__global__ void __launch_bounds__(256) loss_finalize_kernel(const float* __restrict__ part, int parts, int len,
+                                                            const int* __restrict__ nlab, float* loss, float* tmp,
+                                                            unsigned* cnt) {
   __shared__ float s[256];
-  const int img = blockIdx.x;
+  __shared__ bool last;
+  const int img = blockIdx.y, ch = blockIdx.x, nch = gridDim.x;
+  const int p0 = ch * len, p1 = min(parts, p0 + len);
   float t = 0.f;
-  for (int i = threadIdx.x; i < parts; i += 256) t += part[(long long)img * parts + i];
+  for (int i = p0 + threadIdx.x; i < p1; i += 256) t += part[(long long)img * parts + i];
   s[threadIdx.x] = t;
   __syncthreads();
   for (int w = 128; w > 0; w >>= 1) {
     if (threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x == 0) loss[img] = nlab[img] > 0 ? s[0] / (float)nlab[img] : 0.f;
+  if (nch == 1) {
+    if (threadIdx.x == 0) loss[img] = nlab[img] > 0 ? s[0] / (float)nlab[img] : 0.f;
+    return;
+  }
+  if (threadIdx.x == 0) {
+    tmp[(long long)img * nch + ch] = s[0];
+    __threadfence();
+    last = atomicAdd(cnt + img, 1u) == (unsigned)nch - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  float u = 0.f;
+  for (int q = 0; q < nch; ++q) u += __ldcg(tmp + (long long)img * nch + q);
+  loss[img] = nlab[img] > 0 ? u / (float)nlab[img] : 0.f;
+  cnt[img] = 0u;  // ready for the next launch
 }
 
-cudaError_t launch_loss_finalize(const float* part, int parts, const int* nlab, int n, float* loss,
-                                 cudaStream_t s) {
-  loss_finalize_kernel<<<n, 256, 0, s>>>(part, parts, nlab, loss);
+cudaError_t launch_loss_finalize(const float* part, int parts, const int* nlab, int n, float* loss, float* tmp,
+                                 unsigned* cnt, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int nch = (parts + 2047) / 2048;
+  if (nch > kLossChunks) nch = kLossChunks;
+  if (nch < 1) nch = 1;
+  const int len = (parts + nch - 1) / nch;
+  loss_finalize_kernel<<<dim3(nch, n), 256, 0, s>>>(part, parts, len, nlab, loss, tmp, cnt);
   return cudaGetLastError();
 }
 

@@ -234,7 +234,19 @@ static void layout_memory(Net* N, int n) {
   N->bpart_floats = bp;
   N->off_bpart = s; s = align256(s + sizeof(float) * bp);
   N->off_lossp = s; s = align256(s + sizeof(float) * (size_t)N->loss_parts * n);
+  N->off_lossred = s; s = align256(s + (sizeof(float) * kLossChunks + sizeof(unsigned)) * (size_t)n);
   N->off_err = s; s = align256(s + 256);
+  {  // two-level reduction scratch, one per stream (see launch_partial_reduce)
+    const LayerPlan& P0 = N->lp[0];
+    int E = N->classes * h.C + N->classes + h.C;
+    E = std::max(E, P0.cout * P0.L.k * P0.L.k);
+    for (int l = 0; l < N->n_layers; ++l) E = std::max(E, N->lp[l].cout);
+    N->red_E = E;
+    for (int r = 0; r < 2; ++r) {
+      N->off_red[r] = s;
+      s = align256(s + sizeof(float) * (size_t)kReduceSegments * E + sizeof(unsigned) * ((E + 31) / 32));
+    }
+  }
   {  // two staging slots [images | labels] for host-buffer steps
     const size_t s0 = s;
     N->off_stage_img = s; s = align256(s + sizeof(float) * (size_t)n * N->cfg.in_channels * N->cfg.image_rows * N->cfg.image_cols);
@@ -252,6 +264,14 @@ static void layout_memory(Net* N, int n) {
 static float* tape_val(const Net* N, int l) { return (float*)(N->tape + N->lp[l].tape_val_off); }
 static uint8_t* tape_idx(const Net* N, int l) { return (uint8_t*)(N->tape + N->lp[l].tape_idx_off); }
 static float* scr(const Net* N, size_t off) { return (float*)(N->scratch + off); }
+static ReduceScratch red_scratch(const Net* N, int which) {
+  ReduceScratch r;
+  r.tmp = scr(N, N->off_red[which]);
+  r.tmp_floats = (size_t)kReduceSegments * N->red_E;
+  r.cnt = (unsigned*)(r.tmp + r.tmp_floats);
+  r.n_cnt = (N->red_E + 31) / 32;
+  return r;
+}
 
 // pointer to activation a[l] (l >= 1) as produced in the last forward
 static const float* act_ptr(const Net* N, int l) {
@@ -420,6 +440,11 @@ mpf_status mpf_net_bind(mpf_net* N, void* p, void* g, void* t, void* s, int32_t 
   N->bound = true;
   N->have_fwd = false;
   MPF_CUDA(cudaMemset(N->scratch + N->off_err, 0, 256));
+  MPF_CUDA(cudaMemset(N->scratch + N->off_lossred + sizeof(float) * kLossChunks * n, 0, sizeof(unsigned) * n));
+  for (int r = 0; r < 2; ++r) {  // reduction arrival counters start (and stay) at zero
+    const ReduceScratch rs = red_scratch(N, r);
+    MPF_CUDA(cudaMemset(rs.cnt, 0, sizeof(unsigned) * rs.n_cnt));
+  }
   return MPF_OK;
 }
 
@@ -614,7 +639,7 @@ static mpf_status wgrad(Net* N, int l, const float* x, const float* dy, int n, c
     const int E = P.cout * P.L.k * P.L.k;
     LAUNCH(N, s, "wgrad_first", l, wflops, wbytes, launch_first_wgrad(f, s));
     LAUNCH(N, s, "wgrad_reduce", l, 0.0, 4.0 * (f.n_blocks + 1.0) * E,
-           launch_partial_reduce(part, f.n_blocks, E, N->grads + P.w_off, nullptr, E, s));
+           launch_partial_reduce(part, f.n_blocks, E, N->grads + P.w_off, nullptr, E, red_scratch(N, 1), s));
     return MPF_OK;
   }
   if (l > 0 && N->cfg.precision == MPF_PREC_TF32 && tc_wgrad_supported(P.cin, P.cout, P.L.k)) {
@@ -628,7 +653,7 @@ static mpf_status wgrad(Net* N, int l, const float* x, const float* dy, int n, c
     LAUNCH(N, s, "wgrad_tc", l, wflops, wbytes, launch_wgrad_tc(t, &splits, s));
     const long long K = (long long)P.L.k * P.L.k * P.cin;
     LAUNCH(N, s, "wgrad_reduce", l, 0.0, 4.0 * (splits + 2.0) * (P.cout * Kd),
-           launch_wgrad_reduce(part, nullptr, splits, P.cout, P.cin, P.L.k, N->grads + P.w_off, nullptr, s));
+           launch_wgrad_reduce(part, splits, P.cout, P.cin, P.L.k, N->grads + P.w_off, s));
     return MPF_OK;
   }
   WgradArgs w{};
@@ -651,7 +676,7 @@ static mpf_status wgrad(Net* N, int l, const float* x, const float* dy, int n, c
   w.part_b = part + (size_t)splits * P.cout * K;
   LAUNCH(N, s, "wgrad_simt", l, wflops, wbytes, launch_wgrad_simt(w, s));
   LAUNCH(N, s, "wgrad_reduce", l, 0.0, 4.0 * (splits + 2.0) * (P.cout * Kd),
-         launch_wgrad_reduce(w.part_w, nullptr, splits, P.cout, P.cin, P.L.k, N->grads + P.w_off, nullptr, s));
+         launch_wgrad_reduce(w.part_w, splits, P.cout, P.cin, P.L.k, N->grads + P.w_off, s));
   return MPF_OK;
 }
 
@@ -659,7 +684,7 @@ static mpf_status wgrad(Net* N, int l, const float* x, const float* dy, int n, c
 static mpf_status bias_reduce(Net* N, int l, const float* part, long long nb, cudaStream_t s) {
   const LayerPlan& P = N->lp[l];
   LAUNCH(N, s, "bias_reduce", l, 0.0, 4.0 * (double)nb * P.cout,
-         launch_partial_reduce(part, (int)nb, P.cout, N->grads + P.b_off, nullptr, P.cout, s));
+         launch_partial_reduce(part, (int)nb, P.cout, N->grads + P.b_off, nullptr, P.cout, red_scratch(N, 0), s));
   return MPF_OK;
 }
 
@@ -736,16 +761,18 @@ static mpf_status backward_impl(Net* N, const uint8_t* d_labels, const float* h_
     if (loss_only) {  // forward-only loss evaluation (Armijo trial points): no gradients
       if (d_loss)
         LAUNCH(N, s, "loss_finalize", L, 0.0, 4.0 * (double)N->loss_parts * n,
-               launch_loss_finalize(lossp, hd.tiles_per_img * head_loss_parts_per_tile(), nlab, n, d_loss, s));
+               launch_loss_finalize(lossp, hd.tiles_per_img * head_loss_parts_per_tile(), nlab, n, d_loss,
+                                  scr(N, N->off_lossred), (unsigned*)scr(N, N->off_lossred + sizeof(float) * kLossChunks * N->n_cap), s));
       return MPF_OK;
     }
     // [dW_L | db_L] are contiguous in the canonical order; db of layer L-1 follows
     LAUNCH(N, s, "head_reduce", L, 0.0, 4.0 * (double)hd.n_blocks * E,
            launch_partial_reduce(bpart, hd.n_blocks, E, N->grads + N->lp[L].w_off, N->grads + N->lp[L - 1].b_off,
-                                 N->classes * h.C + N->classes, s));
+                                 N->classes * h.C + N->classes, red_scratch(N, 0), s));
     if (d_loss)
       LAUNCH(N, s, "loss_finalize", L, 0.0, 4.0 * (double)N->loss_parts * n,
-             launch_loss_finalize(lossp, hd.tiles_per_img * head_loss_parts_per_tile(), nlab, n, d_loss, s));
+             launch_loss_finalize(lossp, hd.tiles_per_img * head_loss_parts_per_tile(), nlab, n, d_loss,
+                                  scr(N, N->off_lossred), (unsigned*)scr(N, N->off_lossred + sizeof(float) * kLossChunks * N->n_cap), s));
   }
   // remaining layers in reverse.  Invariant: dcur holds the delta of a[l+1] at the
   // pre-activation (CONV/FC output) or the value (pooled output).

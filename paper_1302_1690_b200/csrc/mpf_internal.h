@@ -69,6 +69,10 @@ struct Net {
   size_t off_Y = 0, off_dA = 0, off_dB = 0, off_dC = 0, off_bpart = 0, off_wpack = 0, off_part = 0,
          off_nlab = 0, off_lossp = 0, off_err = 0, off_stage_img = 0, off_stage_lab = 0,
          off_stage_loss = 0, off_theta0 = 0, off_armijo = 0, off_labfrag = 0;
+  // partial_reduce scratch: [0] main stream (bias / head), [1] side stream (weight gradients)
+  size_t off_red[2] = {0, 0};
+  size_t off_lossred = 0;  // loss_finalize chunk sums + per-image counters
+  int red_E = 0;  // widest reduction (floats per row)
   size_t stage_bytes = 0;  // one of the two host-input staging slots (images | labels)
   // host-buffer steps: inputs of step i + 1 are copied on copy_stream into the other
   // staging slot while step i computes (events order the slots' reuse)
@@ -141,8 +145,8 @@ cudaError_t launch_wgrad_simt(const WgradArgs& a, cudaStream_t s);
 int wgrad_simt_splits(long long positions);
 
 // grads_canon[w_off + ((co*cin+ci)*k+ky)*k+kx] += sum_s part_w[s][co][(ky*k+kx)*cin+ci]; bias likewise.
-cudaError_t launch_wgrad_reduce(const float* part_w, const float* part_b, int n_split, int cout, int cin,
-                                int k, float* grad_w, float* grad_b, cudaStream_t s);
+cudaError_t launch_wgrad_reduce(const float* part_w, int n_split, int cout, int cin, int k, float* gw,
+                                cudaStream_t s);
 
 struct MpfArgs {
   const float* y;        // conv output, grid (gr,gc), valid vr x vc, C channels
@@ -173,9 +177,18 @@ long long mpf_bwd_partials(const MpfBwdArgs& a);
 // per-channel partial sums of a [P][C] tensor: part[channel_partials(P)][C]
 long long channel_partials(long long P);
 cudaError_t launch_channel_partial(const float* dy, long long P, int C, float* part, cudaStream_t s);
-// dst[e] += sum_b part[b][e] for e < split_at, dst2[e - split_at] += ... beyond (fixed order)
+// dst[e] += sum_b part[b][e] for e < split_at, dst2[e - split_at] += ... beyond (fixed order).
+// Scratch of this two-level reduction: up to kReduceSegments x E segment sums and one
+// arrival counter per 32-column chunk (zero between launches); one scratch per stream.
+constexpr int kReduceSegments = 128;
+struct ReduceScratch {
+  float* tmp;
+  size_t tmp_floats;
+  unsigned* cnt;
+  int n_cnt;
+};
 cudaError_t launch_partial_reduce(const float* part, int nb, int E, float* dst, float* dst2, int split_at,
-                                  cudaStream_t s);
+                                  const ReduceScratch& rs, cudaStream_t s);
 
 struct HeadArgs {
   const float* h;        // last hidden activation, grid (gr,gc), valid (vr,vc), Ch channels
@@ -224,8 +237,10 @@ cudaError_t launch_mirror_pad(const float* in, float* out, long long planes, int
                               cudaStream_t s);
 cudaError_t launch_class_hist(const uint8_t* labels, long long total, int classes, unsigned long long* counts,
                               cudaStream_t s);
-cudaError_t launch_loss_finalize(const float* loss_part, int parts, const int* nlab, int n, float* loss,
-                                 cudaStream_t s);
+// loss_finalize scratch: kLossChunks x n chunk sums + n arrival counters (zero between launches)
+constexpr int kLossChunks = 32;
+cudaError_t launch_loss_finalize(const float* loss_part, int parts, const int* nlab, int n, float* loss, float* tmp,
+                                 unsigned* cnt, cudaStream_t s);
 cudaError_t launch_sgd(float* params, float* grads, long long n, float lr, float scale, cudaStream_t s);
 cudaError_t launch_pack_weights(const float* w_canon, int cout, int cin, int k, float* wpack, float* dpack,
                                 int round_fwd, int round_dgrad, cudaStream_t s);

@@ -474,6 +474,38 @@ __global__ void __launch_bounds__(256) mpf_bwd_tile_kernel(MpfBwdArgs a, int row
   }
 }
 
+// Bias partials of the register-blocked gathers (thread = channel vector cv of group sub):
+// for C / 4 <= 32 one row per warp -- leader lane l < C/4 adds the lanes l + j C/4 of its
+// channel vector by shuffles (fixed order) -- else one row per (CTA, group); the fixed-order
+// reduction kernel sums the rows.  No shared memory, so a CTA fits beside a tensor-core CTA
+// on an SM (the weight gradients run concurrently on the side stream).
+__device__ __forceinline__ void write_bias_rows(const MpfBwdArgs& a, const float (&bsum)[4], int sub, int nsub,
+                                                int cv) {
+  if (a.bias_part == nullptr) return;
+  const int C = a.C, CV = C / 4;
+  if (CV <= 32) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float s[4] = {bsum[0], bsum[1], bsum[2], bsum[3]};
+    for (int j = 1; j * CV < 32; ++j) {
+      const int src = lane + j * CV;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float v = __shfl_sync(0xffffffffu, bsum[q], src & 31);
+        if (src < 32) s[q] += v;
+      }
+    }
+    if (lane < CV) {
+      const int cls = (int)(threadIdx.x % CV);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) a.bias_part[((size_t)blockIdx.x * 8 + warp) * C + cls * 4 + q] = s[q];
+    }
+    return;
+  }
+  if (sub >= nsub) return;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) a.bias_part[((size_t)blockIdx.x * nsub + sub) * C + cv * 4 + q] = bsum[q];
+}
+
 // Register-blocked gather for k = 2 (premul deltas, 4-channel vectors): a thread owns a
 // 2 x 2 block of conv-output elements (rows 2i, 2i+1, columns 2j, 2j+1) of one channel
 // vector.  Every candidate window of the block lies in the 3 x 3 window patch rows
@@ -563,12 +595,7 @@ __global__ void __launch_bounds__(256, 3) mpf_bwd_block2_kernel(MpfBwdArgs a, lo
         }
     }
   }
-  // bias partials: one row per (CTA, thread group), summed by the fixed-order reduction
-  // kernel.  No shared memory, so a CTA fits beside a tensor-core CTA on an SM (the weight
-  // gradients run concurrently on the side stream).
-  if (a.bias_part == nullptr || sub >= nsub) return;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) a.bias_part[((size_t)blockIdx.x * nsub + sub) * C + cv * 4 + q] = bsum[q];
+  write_bias_rows(a, bsum, sub, nsub, cv);
 }
 
 // Register-blocked gather for k = 3: a thread owns a 3 x BW block of conv-output elements of
@@ -654,12 +681,7 @@ __global__ void __launch_bounds__(256) mpf_bwd_block3_kernel(MpfBwdArgs a, long 
       }
     }
   }
-  // bias partials: one row per (CTA, thread group), summed by the fixed-order reduction
-  // kernel.  No shared memory, so a CTA fits beside a tensor-core CTA on an SM (the weight
-  // gradients run concurrently on the side stream).
-  if (a.bias_part == nullptr || sub >= nsub) return;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) a.bias_part[((size_t)blockIdx.x * nsub + sub) * C + cv * 4 + q] = bsum[q];
+  write_bias_rows(a, bsum, sub, nsub, cv);
 }
 
 // ----------------------------------------------------------------------------- channel sums
@@ -693,23 +715,60 @@ __global__ void __launch_bounds__(256) channel_partial_kernel(const float* __res
   }
 }
 
-// dst[e] += sum_{b < nb} part[b][e], e < E, in a fixed order (deterministic).
+// dst[e] (+)= sum_b part[b][e] (e >= split_at: dst2[e - split_at]), b in [0, nb), fixed order.
+// Grid (column chunks of 32, S row segments): thread (column c, row lane r) sums rows
+// seg0 + r, seg0 + r + 8, ... of its segment (four interleaved accumulators) with coalesced 128-byte row reads; the 8 lanes
+// meet in shared memory (fixed order) and the block writes tmp[s][e].  The last of the S
+// blocks of a column chunk (counted in cnt[chunk], reset afterwards) sums tmp[0..S) in order.
 __global__ void __launch_bounds__(256) partial_reduce_kernel(const float* __restrict__ part, int nb, int E,
-                                                             float* dst, float* dst2, int split_at) {
-  __shared__ float s[256];
-  const int e = blockIdx.x;
+                                                             float* dst, float* dst2, int split_at, float* tmp,
+                                                             unsigned* cnt, int S) {
+  __shared__ float red[8][33];
+  __shared__ bool last;
+  const int c = threadIdx.x & 31, r = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + c;
+  const int seg = blockIdx.y;
+  const int rows = (nb + S - 1) / S, b0 = seg * rows, b1 = min(nb, b0 + rows);
   float t = 0.f;
-  for (int b = threadIdx.x; b < nb; b += 256) t += part[(size_t)b * E + e];
-  s[threadIdx.x] = t;
+  if (e < E) {  // four independent loads in flight per thread; fixed order
+    float t1 = 0.f, t2 = 0.f, t3 = 0.f;
+    int b = b0 + r;
+    for (; b + 24 < b1; b += 32) {
+      t += part[(size_t)b * E + e];
+      t1 += part[(size_t)(b + 8) * E + e];
+      t2 += part[(size_t)(b + 16) * E + e];
+      t3 += part[(size_t)(b + 24) * E + e];
+    }
+    for (; b < b1; b += 8) t += part[(size_t)b * E + e];
+    t = (t + t1) + (t2 + t3);
+  }
+  red[r][c] = t;
   __syncthreads();
-  for (int w = 128; w > 0; w >>= 1) {
-    if (threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
-    __syncthreads();
+  if (r == 0) {
+    float v = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v += red[q][c];
+    if (e < E) tmp[(size_t)seg * E + e] = v;
   }
-  if (threadIdx.x == 0) {
-    if (e < split_at) dst[e] += s[0];
-    else dst2[e - split_at] += s[0];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(cnt + blockIdx.x, 1u) == (unsigned)S - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  float u = 0.f;
+  if (e < E)
+    for (int q = r; q < S; q += 8) u += __ldcg(tmp + (size_t)q * E + e);
+  red[r][c] = u;
+  __syncthreads();
+  if (r == 0 && e < E) {
+    float v = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v += red[q][c];
+    if (e < split_at) dst[e] += v;
+    else dst2[e - split_at] += v;
   }
+  if (threadIdx.x == 0) cnt[blockIdx.x] = 0u;  // ready for the next launch on this stream
 }
 
 }  // namespace
@@ -803,7 +862,7 @@ static void bwd_geometry(const MpfBwdArgs& a, int V, dim3* grid, dim3* blk) {
 }
 
 long long mpf_bwd_partials(const MpfBwdArgs& a) {
-  if (bwd_block2(a)) return (long long)block2_grid(a) * (256 / (a.C / 4));
+  if (bwd_block2(a)) return (long long)block2_grid(a) * (a.C / 4 <= 32 ? 8 : 256 / (a.C / 4));
   dim3 g, b;
   bwd_geometry(a, a.C % 4 == 0 ? 4 : 1, &g, &b);
   return (long long)g.x * g.y * g.z;
@@ -855,9 +914,14 @@ cudaError_t launch_channel_partial(const float* dy, long long P, int C, float* p
 }
 
 cudaError_t launch_partial_reduce(const float* part, int nb, int E, float* dst, float* dst2, int split_at,
-                                  cudaStream_t s) {
+                                  const ReduceScratch& rs, cudaStream_t s) {
   if (E <= 0) return cudaSuccess;
-  partial_reduce_kernel<<<E, 256, 0, s>>>(part, nb, E, dst, dst2, split_at);
+  int S = (nb + 63) / 64;  // >= 8 rows per thread; the last block then sums S / 8 per thread
+  if (S > kReduceSegments) S = kReduceSegments;
+  if (S < 1) S = 1;
+  const int chunks = (E + 31) / 32;
+  if (chunks > rs.n_cnt || (size_t)S * E > rs.tmp_floats) return cudaErrorInvalidValue;
+  partial_reduce_kernel<<<dim3(chunks, S), 256, 0, s>>>(part, nb, E, dst, dst2, split_at, rs.tmp, rs.cnt, S);
   return cudaGetLastError();
 }
 

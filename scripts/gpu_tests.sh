@@ -1,7 +1,6 @@
 # GPU suite with the per-test printouts (-s: per-tensor errors, argmax flips), smoke(), and
 # one default bench line.  Usage: gpurun -- bash scripts/gpu_tests.sh [pytest -k expr]
 mkdir -p gpurun_out
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/mma_micro scripts/mma_sync_micro.cu && /tmp/mma_micro > gpurun_out/mma_micro.txt 2>&1
 { nproc; free -g; nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv; } > gpurun_out/box.txt 2>&1
 K=${1:+-k "$1"}
 eval timeout 2400 python -m pytest tests -m gpu -q -s -rA $K > gpurun_out/gpu_tests.log 2>&1; echo tests $? >> gpurun_out/status.txt
