@@ -100,6 +100,11 @@ typedef struct {
  *               stderr after every launch (synchronises; profiling only).
  *   FUSE_FIRST_POOL  the first conv + activation + the MPF layer after it in one kernel
  *               (the conv output never reaches device memory; bitwise equal).
+ *   HEAD_LOGITS_OFF  the softmax FC's logits are computed by the head kernel from h instead
+ *               of in the epilogue of the last hidden layer's tensor-core forward (same sums
+ *               to fp32 summation order).  Default: in the epilogue when that layer's
+ *               k^2 C_in >= 512.
+ *   HEAD_LOGITS_ON   in the epilogue whenever the last hidden layer runs on the tensor cores.
  */
 enum {
   MPF_FLAG_SERIAL = 1u << 0,
@@ -110,7 +115,9 @@ enum {
   MPF_FLAG_NTAP_NO_MC = 1u << 5,
   MPF_FLAG_WGRAD_M128 = 1u << 6,
   MPF_FLAG_ROLE_TIMERS = 1u << 7,
-  MPF_FLAG_FUSE_FIRST_POOL = 1u << 8
+  MPF_FLAG_FUSE_FIRST_POOL = 1u << 8,
+  MPF_FLAG_HEAD_LOGITS_OFF = 1u << 9,
+  MPF_FLAG_HEAD_LOGITS_ON = 1u << 10
 };
 
 /* Geometry of the padded uniform-fragment layout.

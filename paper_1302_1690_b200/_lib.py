@@ -27,6 +27,8 @@ MPF_FLAG_NTAP_NO_MC = 1 << 5
 MPF_FLAG_WGRAD_M128 = 1 << 6
 MPF_FLAG_ROLE_TIMERS = 1 << 7
 MPF_FLAG_FUSE_FIRST_POOL = 1 << 8
+MPF_FLAG_HEAD_LOGITS_OFF = 1 << 9
+MPF_FLAG_HEAD_LOGITS_ON = 1 << 10
 
 # every symbol include/mpf.h declares
 EXPORTS = ("mpf_version", "mpf_last_error", "mpf_net_create", "mpf_net_destroy", "mpf_net_geometry",

@@ -62,7 +62,20 @@ struct ConvTcParams {
   int n_tiles;   // tiles of M_CTA (single) or 2 x M_CTA (pair) positions
   int b_rows;    // weight rows per B slot (npad, or npad/2 per CTA of a pair)
   unsigned long long* prof;  // optional role-timing counters (MPF_FLAG_ROLE_TIMERS)
+  // logits of the softmax FC in the epilogue (forward of the last hidden layer, head_z set):
+  // z[p][c] = sum_ch W_L[c][ch] h[p][ch] over the stored (rounded) h, bias excluded
+  const float* head_w;  // canonical W_L [head_C][cout]
+  float* head_z;        // [P_tot][head_C]
+  int head_C;
 };
+constexpr int kMaxHeadC = 16;
+// row stride of W_L in shared memory: whole 32-channel chunks, zero beyond cout (the last
+// chunk of an npad % 32 == 16 layer reads 32 weights; its channels past cout hold act(0))
+__host__ __device__ inline int head_w_ld(int npad) { return (npad + 31) / 32 * 32; }
+// shared bytes of the logits epilogue: W_L [head_C][ld] + two exchange slots [4][32][head_C]
+__host__ __device__ inline uint32_t head_epi_bytes(int head_C, int npad) {
+  return head_C > 0 ? (uint32_t)(4 * head_C * head_w_ld(npad) + 2 * 4 * 32 * 4 * head_C) : 0u;
+}
 
 // mbarrier wait that adds the cycles spent waiting to a counter when profiling
 __device__ __forceinline__ void twait(uint32_t bar, uint32_t parity, unsigned long long& acc, bool on) {
@@ -103,6 +116,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* gen = smem_raw - ptx::smem_u32(smem_raw);  // generic pointer of shared address 0
   uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(gen + sTmemSlot);
   float* s_bias = reinterpret_cast<float*>(gen + sBias);
+  const int HC = p.head_z ? p.head_C : 0;  // logits epilogue (0: off)
+  const int hw_ld = head_w_ld(p.npad);
+  float* s_hw = reinterpret_cast<float*>(gen + sBar + 512);  // W_L [HC][hw_ld], zero-padded
+  float* s_zx = s_hw + HC * hw_ld;                           // [2][4][32][HC] half-1 partials
 
   // warp index via a shuffle: provably warp-uniform, so role branches stay convergent and
   // the MMA warp's descriptor arithmetic lives in uniform registers
@@ -143,6 +160,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     else ptx::tmem_alloc(sTmemSlot, p.tmem_cols);
   }
   for (int c = threadIdx.x; c < 256; c += kThreads) s_bias[c] = (p.bias && c < p.cout) ? p.bias[c] : 0.f;
+  for (int e = threadIdx.x; e < HC * hw_ld; e += kThreads) {
+    const int c = e / hw_ld, ch = e - c * hw_ld;
+    s_hw[e] = ch < p.cout ? p.head_w[c * p.cout + ch] : 0.f;
+  }
   ptx::tc_fence_before();
   if (PAIR || MC) ptx::cluster_sync_all();  // barrier inits and TMEM allocation visible to the peer
   else __syncthreads();
@@ -233,13 +254,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int half = (warp - 2) >> 2;  // which alternate 32-column chunks this warp stores
     const int ew = warp - 2;
     const int per_frag = p.gr * p.gc;
-    int lt = 0, sb = 0;
+    int lt = 0, sb = 0, zslot = 0;
     for (int tile = unit0; tile < tile_end; tile += n_units, ++lt) {
       const int buf = lt & 1;
       twait(barTfull + 8 * buf, (lt >> 1) & 1, pc[7], prof_on);
       ptx::tc_fence_after();
       const int p0 = tile * tile_pos + my_off;
       for (int acc = 0; acc < NACC; ++acc) {
+        float zc[kMaxHeadC];  // this half's logit partials of position row0 + lane
+#pragma unroll
+        for (int c = 0; c < kMaxHeadC; ++c) zc[c] = 0.f;
         const int row0 = p0 + acc * 128 + q * 32;
         const int pos = row0 + lane;
         bool valid = false;
@@ -320,6 +344,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = 0.f;
           }
+          if (HC) {  // logits: W_L rows of this chunk are broadcast reads (same address per warp)
+#pragma unroll
+            for (int c = 0; c < kMaxHeadC; ++c) {
+              if (c >= HC) break;
+              const float4* w4 = reinterpret_cast<const float4*>(s_hw + c * hw_ld + c0);
+              float t = zc[c];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float4 w = w4[j];
+                t = fmaf(w.x, v[4 * j], t);
+                t = fmaf(w.y, v[4 * j + 1], t);
+                t = fmaf(w.z, v[4 * j + 2], t);
+                t = fmaf(w.w, v[4 * j + 3], t);
+              }
+              zc[c] = t;
+            }
+          }
           // staging box (swizzled like the TMA SWIZZLE_128B pattern): 16-B chunk jj of
           // row `lane` lives at lane*128 + ((jj ^ (lane & 7)) * 16)
           const uint32_t sbuf = sC + (ew * p.n_stage + sb) * kStageBytes;
@@ -349,6 +390,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             pc[5] += (unsigned long long)(e2 - e1);   // epilogue math
             pc[9] += (unsigned long long)(e3 - e2);   // staging wait + st.shared + fence + store issue
           }
+        }
+        if (HC) {  // z = half-0 partial + half-1 partial (fixed order), written by half 0
+          float* slot = s_zx + ((zslot * 4 + q) * 32 + lane) * HC;
+          if (half) {
+#pragma unroll
+            for (int c = 0; c < kMaxHeadC; ++c)
+              if (c < HC) slot[c] = zc[c];
+          }
+          named_bar(1 + q, 64);
+          if (!half && row0 + lane < p.P_tot) {
+            float* zo = p.head_z + (size_t)(row0 + lane) * HC;
+#pragma unroll
+            for (int c = 0; c < kMaxHeadC; ++c)
+              if (c < HC) zo[c] = zc[c] + slot[c];
+          }
+          zslot ^= 1;
         }
       }
       // every TMEM read of this accumulator set is complete: hand it back to the MMA warp
@@ -902,6 +959,12 @@ cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s, int* grid_out) {
   p.mul_dact = a.mul_dact;
   p.base_mode = base_mode();
   p.prof = prof_counters(a.flags);
+  if (a.head_z) {
+    if (a.head_C < 1 || a.head_C > kMaxHeadC || !a.head_w) return cudaErrorInvalidValue;
+    p.head_w = a.head_w;
+    p.head_z = a.head_z;
+    p.head_C = a.head_C;
+  }
   int nacc = 256 / p.npad;  // two accumulator sets in 512 TMEM columns
   if (nacc > 4) nacc = 4;
   if (nacc < 1) nacc = 1;
@@ -914,7 +977,7 @@ cudaError_t launch_conv_tc(const TcConvArgs& a, cudaStream_t s, int* grid_out) {
   set_nacc(nacc);
   // shared memory: stages of [A slab | k weight taps] (2..4, as many as fit), epilogue
   // staging (two boxes per warp when 3 stages still fit, else one)
-  const size_t base_fixed = 1024 + 4 * 256 + 512;
+  const size_t base_fixed = 1024 + 4 * 256 + 512 + head_epi_bytes(p.head_z ? p.head_C : 0, p.npad);
   const size_t total = 227 * 1024;
   int ns = 0, nst = 0;
   auto plan_smem = [&](bool pr) {

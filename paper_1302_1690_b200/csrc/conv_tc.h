@@ -31,6 +31,11 @@ struct TcConvArgs {
   const float* mul_dact;  // nullable: multiply by act'(mul_dact[same position])
   int dact;
   uint32_t flags;     // MPF_FLAG_* kernel selection (mpf.h)
+  // forward of the last hidden layer: also write the softmax FC's logits (bias excluded)
+  // z[p][c] = sum_co head_w[c][co] * out[p][co] of the stored output (nullable)
+  const float* head_w;  // [head_C][cout]
+  float* head_z;        // [n_frag * gr * gc][head_C]
+  int head_C;
 };
 
 // Weight gradient: part[s][co][(ky*k+kx)*cin+ci] = sum_{p in split s} dy[p][co] * x[p+(ky,kx)][ci]

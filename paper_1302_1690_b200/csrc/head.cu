@@ -194,43 +194,54 @@ __global__ void __launch_bounds__(kThr, 2) head_kernel(HeadArgs a) {
       float z[NC];
 #pragma unroll
       for (int c = 0; c < NC; ++c) z[c] = 0.f;
-      if (need && VEC) {  // float4 channel groups g = qa, qa + 4, ...
-        const float4* hrow4 = reinterpret_cast<const float4*>(hs + pa * Ch);
-        const int G4 = Ch >> 2;
-        for (int g = qa; g < G4; g += 4) {
-          const float4 hv = hrow4[g];
+      if (a.zpre) {  // logits from the last hidden layer's epilogue: every lane of the position loads them
+        if (need) {
+          const float* zr = a.zpre + ((long long)img * per_img + p0 + pa) * C;
 #pragma unroll
-          for (int c = 0; c < NC; ++c) {
-            const float4 w = reinterpret_cast<const float4*>(s_w2 + c * Ch)[g];
-            z[c] = fmaf(w.x, hv.x, fmaf(w.y, hv.y, fmaf(w.z, hv.z, fmaf(w.w, hv.w, z[c]))));
+          for (int c = 0; c < NC; ++c)
+            if (c < C) z[c] = __ldg(zr + c);
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) z[c] += (c < C) ? s_b[c] : 0.f;
+      } else {  // the logits from h: 4 lanes per position, each over a quarter of the channels
+        if (need && VEC) {  // float4 channel groups g = qa, qa + 4, ...
+          const float4* hrow4 = reinterpret_cast<const float4*>(hs + pa * Ch);
+          const int G4 = Ch >> 2;
+          for (int g = qa; g < G4; g += 4) {
+            const float4 hv = hrow4[g];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+              const float4 w = reinterpret_cast<const float4*>(s_w2 + c * Ch)[g];
+              z[c] = fmaf(w.x, hv.x, fmaf(w.y, hv.y, fmaf(w.z, hv.z, fmaf(w.w, hv.w, z[c]))));
+            }
+          }
+        } else if (need) {  // uniform over the 4 lanes of a position
+          const float* hrow = hs + pa * Ch;
+          if (bulk) {
+            for (int m = 0; m < M; ++m) {
+              int mm = m + rot;
+              if (mm >= M) mm -= M;
+              const int ch = qa + 4 * mm;
+              const float hv = hrow[ch];
+#pragma unroll
+              for (int c = 0; c < NC; ++c) z[c] = fmaf(s_w2[c * Ch + ch], hv, z[c]);
+            }
+          } else {
+            for (int ch = qa; ch < Ch; ch += 4) {
+              const float hv = hrow[ch];
+#pragma unroll
+              for (int c = 0; c < NC; ++c) z[c] = fmaf(s_w2[c * Ch + ch], hv, z[c]);
+            }
           }
         }
-      } else if (need) {  // uniform over the 4 lanes of a position
-        const float* hrow = hs + pa * Ch;
-        if (bulk) {
-          for (int m = 0; m < M; ++m) {
-            int mm = m + rot;
-            if (mm >= M) mm -= M;
-            const int ch = qa + 4 * mm;
-            const float hv = hrow[ch];
+        // 4-lane butterfly (the lanes of one position are lane^1, lane^2: same group);
+        // executed by every lane of the warp
 #pragma unroll
-            for (int c = 0; c < NC; ++c) z[c] = fmaf(s_w2[c * Ch + ch], hv, z[c]);
-          }
-        } else {
-          for (int ch = qa; ch < Ch; ch += 4) {
-            const float hv = hrow[ch];
-#pragma unroll
-            for (int c = 0; c < NC; ++c) z[c] = fmaf(s_w2[c * Ch + ch], hv, z[c]);
-          }
+        for (int c = 0; c < NC; ++c) {
+          z[c] += __shfl_xor_sync(0xffffffffu, z[c], 1);
+          z[c] += __shfl_xor_sync(0xffffffffu, z[c], 2);
+          z[c] += (c < C) ? s_b[c] : 0.f;
         }
-      }
-      // 4-lane butterfly (the lanes of one position are lane^1, lane^2: same group);
-      // executed by every lane of the warp
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        z[c] += __shfl_xor_sync(0xffffffffu, z[c], 1);
-        z[c] += __shfl_xor_sync(0xffffffffu, z[c], 2);
-        z[c] += (c < C) ? s_b[c] : 0.f;
       }
       if (need) {
         float mx = z[0];

@@ -214,6 +214,8 @@ static void layout_memory(Net* N, int n) {
   const long long h_pos = h.elems_per_image() / h.C;
   N->loss_parts = head_tiles_per_image(h_pos) * head_loss_parts_per_tile();
   N->off_labfrag = s; s = align256(s + (size_t)n * h_pos);  // labels in head-position order
+  // the softmax FC's logits from the last hidden layer's forward epilogue, forward -> head
+  N->off_z = s; s = align256(s + sizeof(float) * (size_t)n * h_pos * N->classes);
   size_t bp = (size_t)head_blocks((long long)head_tiles_per_image(h_pos) * n) *
               ((size_t)N->classes * h.C + N->classes + h.C);
   for (int l = 0; l < N->n_layers - 1; ++l) {
@@ -488,6 +490,7 @@ static mpf_status forward_impl(Net* N, const float* d_images, int n, float* d_pr
   if (sp != s) MPF_CUDA(cudaEventRecord(N->ev_join, sp));
   // 2. layers (Alg. 1; Alg. 3 for MPF)
   bool pool_done = false;  // the first layer's kernel already produced the MPF after it
+  bool z_ready = false;    // the last hidden layer's epilogue wrote the logits (off_z)
   for (int l = 0; l < N->n_layers - 1; ++l) {
     const LayerPlan& P = N->lp[l];
     const Act& in = N->a[l];
@@ -557,7 +560,20 @@ static mpf_status forward_impl(Net* N, const float* d_images, int n, float* d_pr
       t.round_out = next_tc ? 1 : 0; t.mul_dact = nullptr;
       t.zero_pad = P.out_where == Where::Tape ? 1 : 0;  // tape tensors are read whole by the TC wgrad
       t.flags = flags;
-      LAUNCH(N, s, "conv_fwd_tc", l, cflops, cbytes, launch_conv_tc(t, s));
+      double zflops = 0.0;
+      // h feeds the softmax FC: its logits come from this epilogue when the K loop per tile is
+      // long enough to hide the extra epilogue work (measured: cfg4 FC1, K = 1152: head 3.5 ->
+      // 2.55 ms, forward unchanged; cfg5 FC1, K = 256: forward +0.05 ms, head -0.01 ms)
+      if (l == N->n_layers - 2 && !(flags & MPF_FLAG_HEAD_LOGITS_OFF) &&
+          ((flags & MPF_FLAG_HEAD_LOGITS_ON) || P.L.k * P.L.k * P.cin >= 512)) {
+        t.head_w = N->params + N->lp[l + 1].w_off;
+        t.head_z = scr(N, N->off_z);
+        t.head_C = N->classes;
+        zflops = 2.0 * pos_out * P.cout * N->classes;
+        z_ready = true;
+      }
+      LAUNCH(N, s, "conv_fwd_tc", l, cflops + zflops, cbytes + 4.0 * pos_out * N->classes * (zflops > 0),
+             launch_conv_tc(t, s));
     } else {
       ConvArgs c{};
       c.in = x;
@@ -590,6 +606,7 @@ static mpf_status forward_impl(Net* N, const float* d_images, int n, float* d_pr
   N->images = d_images;
   N->n_fwd = n;
   N->have_fwd = true;
+  N->z_ready = z_ready;
   // 3. optional softmax output
   if (d_probs) {
     const int L = N->n_layers - 1;
@@ -606,9 +623,10 @@ static mpf_status forward_impl(Net* N, const float* d_images, int n, float* d_pr
     hd.err = (int*)(N->scratch + N->off_err);
     hd.tiles_per_img = head_tiles_per_image((long long)h.F * h.gr * h.gc);
     hd.n_blocks = head_blocks((long long)hd.tiles_per_img * n);
+    hd.zpre = z_ready ? scr(N, N->off_z) : nullptr;
     const double pos = (double)n * h.F * h.vr * h.vc;
-    LAUNCH(N, s, "head_probs", L, 2.0 * pos * h.C * N->classes, pos * (4.0 * h.C + 4.0 * N->classes),
-           launch_head2(hd, s));
+    LAUNCH(N, s, "head_probs", L, hd.zpre ? 0.0 : 2.0 * pos * h.C * N->classes,
+           hd.zpre ? pos * 8.0 * N->classes : pos * (4.0 * h.C + 4.0 * N->classes), launch_head2(hd, s));
   }
   return MPF_OK;
 }
@@ -749,14 +767,15 @@ static mpf_status backward_impl(Net* N, const uint8_t* d_labels, const float* h_
   hd.err = (int*)(N->scratch + N->off_err);
   hd.n = n;
   hd.round_tf32 = tf32 ? 1 : 0;
+  hd.zpre = N->z_ready ? scr(N, N->off_z) : nullptr;
   {
     const double pos = (double)n * h.F * h.vr * h.vc;
     uint8_t* labf = (uint8_t*)(N->scratch + N->off_labfrag);
     LAUNCH(N, s, "label_frag", L, 0.0, (double)n * h.F * h.gr * h.gc + (double)n * N->O_H * N->O_W,
            launch_label_frag(hd, labf, s));
     hd.lab_frag = labf;
-    LAUNCH(N, s, "head_loss_delta", L, 6.0 * pos * h.C * N->classes, pos * (8.0 * h.C + 1.0),
-           launch_head2(hd, s));
+    LAUNCH(N, s, "head_loss_delta", L, (hd.zpre ? 4.0 : 6.0) * pos * h.C * N->classes,
+           pos * (8.0 * h.C + 1.0 + (hd.zpre ? 4.0 * N->classes : 0.0)), launch_head2(hd, s));
     const int E = N->classes * h.C + N->classes + h.C;
     if (loss_only) {  // forward-only loss evaluation (Armijo trial points): no gradients
       if (d_loss)
@@ -1390,10 +1409,13 @@ mpf_status mpf_net_set_grad_hook(mpf_net* N, mpf_grad_ready_fn fn, void* user) {
 mpf_status mpf_net_set_flags(mpf_net* N, uint32_t flags) {
   if (!N) return fail(MPF_ERR_ARG, "NULL net");
   const uint32_t known = MPF_FLAG_SERIAL | MPF_FLAG_TC_SINGLE | MPF_FLAG_TC_PAIR | MPF_FLAG_NTAP_ON | MPF_FLAG_NTAP_OFF |
-                         MPF_FLAG_NTAP_NO_MC | MPF_FLAG_WGRAD_M128 | MPF_FLAG_ROLE_TIMERS | MPF_FLAG_FUSE_FIRST_POOL;
+                         MPF_FLAG_NTAP_NO_MC | MPF_FLAG_WGRAD_M128 | MPF_FLAG_ROLE_TIMERS | MPF_FLAG_FUSE_FIRST_POOL |
+                         MPF_FLAG_HEAD_LOGITS_OFF | MPF_FLAG_HEAD_LOGITS_ON;
   if (flags & ~known) return fail(MPF_ERR_ARG, "unknown MPF_FLAG_* bits");
   if ((flags & MPF_FLAG_NTAP_ON) && (flags & MPF_FLAG_NTAP_OFF)) return fail(MPF_ERR_ARG, "NTAP_ON with NTAP_OFF");
   if ((flags & MPF_FLAG_TC_PAIR) && (flags & MPF_FLAG_TC_SINGLE)) return fail(MPF_ERR_ARG, "TC_PAIR with TC_SINGLE");
+  if ((flags & MPF_FLAG_HEAD_LOGITS_ON) && (flags & MPF_FLAG_HEAD_LOGITS_OFF))
+    return fail(MPF_ERR_ARG, "HEAD_LOGITS_ON with HEAD_LOGITS_OFF");
   N->cfg.flags = flags;
   return MPF_OK;
 }

@@ -72,6 +72,8 @@ struct Net {
   // partial_reduce scratch: [0] main stream (bias / head), [1] side stream (weight gradients)
   size_t off_red[2] = {0, 0};
   size_t off_lossred = 0;  // loss_finalize chunk sums + per-image counters
+  size_t off_z = 0;        // softmax FC logits [n][head positions][classes] (forward -> head)
+  bool z_ready = false;    // the last forward wrote off_z
   int red_E = 0;  // widest reduction (floats per row)
   size_t stage_bytes = 0;  // one of the two host-input staging slots (images | labels)
   // host-buffer steps: inputs of step i + 1 are copied on copy_stream into the other
@@ -212,6 +214,8 @@ struct HeadArgs {
   int n;
   int round_tf32;
   const uint8_t* lab_frag;  // training: labels in head-position order (launch_label_frag), or NULL
+  const float* zpre;        // logits without bias [n][F*gr*gc][C] from the last hidden layer's
+                            // forward epilogue, or NULL (the head computes them from h)
 };
 int head_tiles_per_image(long long per_img);
 // labels gathered into head-position (fragment-major) order: out[img][pos] = class, 255

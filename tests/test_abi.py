@@ -129,7 +129,8 @@ def test_kernel_selection_flags_are_validated():
     pairs are argument errors, at create and later; valid flags are accepted."""
     lib = L.lib()
     c = S.CONFIGS["cfg2"]
-    for bad in (1 << 20, L.MPF_FLAG_NTAP_ON | L.MPF_FLAG_NTAP_OFF, L.MPF_FLAG_TC_PAIR | L.MPF_FLAG_TC_SINGLE):
+    for bad in (1 << 20, L.MPF_FLAG_NTAP_ON | L.MPF_FLAG_NTAP_OFF, L.MPF_FLAG_TC_PAIR | L.MPF_FLAG_TC_SINGLE,
+                L.MPF_FLAG_HEAD_LOGITS_ON | L.MPF_FLAG_HEAD_LOGITS_OFF):
         cfg = L.MpfConfig(1, c.P, c.H, c.W, 1, L.MPF_PREC_TF32, bad, 0)
         h = ctypes.c_void_p()
         assert lib.mpf_net_create(ctypes.byref(cfg), layers_to_c(c.layers), len(c.layers), ctypes.byref(h)) == L.MPF_ERR_ARG

@@ -107,7 +107,13 @@ def test_wide_random_archs_vs_o2(seed, prec, tol):
     C = layers[-1].n_out
     labels = S.random_labels(rng, n, H - P + 1, W - P + 1, C)
     params = S.init_params(layers, seed, in_channels=cin).astype(np.float32).astype(np.float64)
-    g = gpu_step(layers, P, images, labels, params, prec)
+    # even seeds: the logits in the last hidden layer's epilogue on every shape (not only the
+    # default's long K loops)
+    from paper_1302_1690_b200 import _lib as L
+    from paper_1302_1690_b200.net import MPFNet
+    net = MPFNet(layers, P, H, W, max_images=n, in_channels=cin, precision=prec,
+                 flags=L.MPF_FLAG_HEAD_LOGITS_ON if seed % 2 == 0 else 0)
+    g = gpu_step(layers, P, images, labels, params, prec, net=net)
     probs, losses, grads = [], [], []
     for i in range(n):
         ls, cnt, gr, pr = o2.train_image(layers, params, images[i].astype(np.float64), labels[i], P=P,
@@ -447,6 +453,22 @@ def test_multitap_conv_matches_standard(name):
     assert rel_l2(a["probs"], c["probs"]) <= 1e-5
     for nm, sl in param_slices(cfg.layers):
         assert rel_l2(a["grad_sum"][sl], c["grad_sum"][sl]) <= 1e-3, nm
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg4s", "cfg5s"])
+def test_head_logits_in_fc1_epilogue(name):
+    """The softmax FC's logits z = W_L h summed in the last hidden layer's tensor-core
+    epilogue (from the stored h, two fixed-order half sums; MPF_FLAG_HEAD_LOGITS_ON, the
+    default for cfg4's FC1) and by the head kernel itself (MPF_FLAG_HEAD_LOGITS_OFF, 4-lane
+    butterfly): the same products in another order, so probabilities, loss and gradients
+    agree to fp32 rounding."""
+    from paper_1302_1690_b200 import _lib as L
+    cfg, a = _run_variant(L.MPF_FLAG_HEAD_LOGITS_ON, name=name)
+    _, b = _run_variant(L.MPF_FLAG_HEAD_LOGITS_OFF, name=name)
+    assert rel_l2(a["probs"], b["probs"]) <= 1e-5
+    assert rel_l2(a["loss"], b["loss"]) <= 1e-5
+    for nm, sl in param_slices(cfg.layers):
+        assert rel_l2(a["grad_sum"][sl], b["grad_sum"][sl]) <= 1e-4, nm
 
 
 @pytest.mark.parametrize("name", ["cfg2", "cfg4s", "cfg5s"])
