@@ -16,6 +16,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "conv_tc.h"
 #include "mpf_internal.h"
 
@@ -57,8 +59,26 @@ static void prof_rec(Net* N, cudaStream_t s, int e0, const char* name, int layer
   P.used++;
 }
 // every kernel launch of the path goes through LAUNCH (timed when profiling is on)
+// NVTX range per kernel launch (message = the profile name, payload = the layer), so ncu
+// (--nvtx --nvtx-include) and nsys can attribute launches to layers; with no tool attached
+// an NVTX call is a test of a null function pointer.
+struct NvtxRange {
+  NvtxRange(const char* name, int layer) {
+    nvtxEventAttributes_t ea = {};
+    ea.version = NVTX_VERSION;
+    ea.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+    ea.messageType = NVTX_MESSAGE_TYPE_ASCII;
+    ea.message.ascii = name;
+    ea.payloadType = NVTX_PAYLOAD_TYPE_INT32;
+    ea.payload.iValue = layer;
+    nvtxRangePushEx(&ea);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 #define LAUNCH(N, s, name, layer, flops, bytes, call)            \
   do {                                                           \
+    NvtxRange _nv((name), (layer));                              \
     const int _e0 = prof_mark((N), (s));                         \
     MPF_CUDA(call);                                              \
     prof_rec((N), (s), _e0, (name), (layer), (flops), (bytes));  \
@@ -635,6 +655,7 @@ mpf_status mpf_forward_image(mpf_net* N, const float* d_images, int32_t n, float
   if (!N || !d_images) return fail(MPF_ERR_ARG, "NULL argument");
   if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound (mpf_net_bind)");
   if (n < 1 || n > N->n_cap) return fail(MPF_ERR_DATA, "n must be in [1, bound n_images]");
+  NvtxRange nv("mpf_forward_image", n);
   return forward_impl(N, d_images, n, d_probs, (cudaStream_t)stream);
 }
 
@@ -912,6 +933,7 @@ mpf_status mpf_backward_image(mpf_net* N, const uint8_t* d_labels, const float* 
   if (!N || !d_labels) return fail(MPF_ERR_ARG, "NULL argument");
   if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound");
   if (!N->have_fwd) return fail(MPF_ERR_STATE, "mpf_backward_image before mpf_forward_image");
+  NvtxRange nv("mpf_backward_image", N->n_fwd);
   return backward_impl(N, d_labels, h_class_w, d_loss, (cudaStream_t)stream);
 }
 
@@ -921,6 +943,7 @@ mpf_status mpf_train_step(mpf_net* N, const float* d_images, int32_t n, const ui
   if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound (mpf_net_bind)");
   if (n < 1 || n > N->n_cap) return fail(MPF_ERR_DATA, "n must be in [1, bound n_images]");
   cudaStream_t s = (cudaStream_t)stream;
+  NvtxRange nv("mpf_train_step", n);
   mpf_status st = forward_impl(N, d_images, n, nullptr, s);
   if (st != MPF_OK) return st;
   return backward_impl(N, d_labels, h_class_w, d_loss, s);

@@ -154,6 +154,18 @@ class MPFNet:
     def get_params(self) -> torch.Tensor:
         return self.params.clone()
 
+    def save(self, path: str, step: int = 0) -> None:
+        """Checkpoint the parameters with the architecture echo (checkpoint.py)."""
+        from .checkpoint import save_checkpoint
+        save_checkpoint(path, self.layers, self.patch, self.in_channels, self.params.cpu().numpy(), step)
+
+    def load(self, path: str) -> int:
+        """Resume from a checkpoint of the same architecture; returns its step counter."""
+        from .checkpoint import load_checkpoint
+        ck = load_checkpoint(path, self.layers, self.patch, self.in_channels, self.geom.n_params)
+        self.set_params(ck["params"])
+        return ck["step"]
+
     def zero_grads(self) -> None:
         self.grads.zero_()
 

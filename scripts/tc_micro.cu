@@ -67,26 +67,25 @@ int main() {
   const int n_mma = 20000;
   printf("tf32 M=128 cta_group::1, %d MMAs per SM, all 148 SMs; math = 128*N*8/2048 cycles\n", n_mma);
   printf("%5s %6s %6s %6s %10s %10s %8s\n", "N", "a_off", "commit", "2acc", "cyc/mma", "math", "eff");
-  int Ns[] = {32, 64, 96, 128, 208};
-  int Cs[] = {0, 16, 8, 4, 1};
+  // A start-row offset (the slab trick's kx shift) x N, commit every 16 MMAs, two accumulators
+  int Ns[] = {32, 64, 128, 208, 256};
+  int Offs[] = {0, 1, 2, 3, 4, 8};
   for (int ni = 0; ni < 5; ++ni) {
-    for (int off = 0; off <= 0; ++off) {
-      for (int ci = 0; ci < 5; ++ci) {
-        const int two = 1, kv = Cs[ci];
-        micro<<<148, 128, smem>>>(n_mma, Ns[ni], off * 3, 1, two, Cs[ci], d);
-        cudaError_t e = cudaDeviceSynchronize();
-        if (e != cudaSuccess) {
-          printf("error %s\n", cudaGetErrorString(e));
-          return 1;
-        }
-        unsigned long long h[148];
-        cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
-        double avg = 0;
-        for (int i = 0; i < 148; ++i) avg += h[i];
-        avg /= 148.0 * n_mma;
-        const double math = 128.0 * Ns[ni] * 8 / 2048.0;
-        printf("%5d %6d %6d %6d %10.1f %10.1f %7.0f%%\n", Ns[ni], off * 3, kv, two, avg, math, 100 * math / avg);
+    for (int oi = 0; oi < 6; ++oi) {
+      const int two = 1, kv = 16;
+      micro<<<148, 128, smem>>>(n_mma, Ns[ni], Offs[oi], 1, two, kv, d);
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) {
+        printf("error %s\n", cudaGetErrorString(e));
+        return 1;
       }
+      unsigned long long h[148];
+      cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+      double avg = 0;
+      for (int i = 0; i < 148; ++i) avg += h[i];
+      avg /= 148.0 * n_mma;
+      const double math = 128.0 * Ns[ni] * 8 / 2048.0;
+      printf("%5d %6d %6d %6d %10.1f %10.1f %7.0f%%\n", Ns[ni], Offs[oi], kv, two, avg, math, 100 * math / avg);
     }
   }
   return 0;
