@@ -105,6 +105,8 @@ typedef struct {
  *               to fp32 summation order).  Default: in the epilogue when that layer's
  *               k^2 C_in >= 512.
  *   HEAD_LOGITS_ON   in the epilogue whenever the last hidden layer runs on the tensor cores.
+ *   MPF_BWD_BLOCK  the k = 2 MPF backward as one 2 x 2 block per work item instead of bands of
+ *               block rows (bitwise the same deltas).
  */
 enum {
   MPF_FLAG_SERIAL = 1u << 0,
@@ -117,7 +119,8 @@ enum {
   MPF_FLAG_ROLE_TIMERS = 1u << 7,
   MPF_FLAG_FUSE_FIRST_POOL = 1u << 8,
   MPF_FLAG_HEAD_LOGITS_OFF = 1u << 9,
-  MPF_FLAG_HEAD_LOGITS_ON = 1u << 10
+  MPF_FLAG_HEAD_LOGITS_ON = 1u << 10,
+  MPF_FLAG_MPF_BWD_BLOCK = 1u << 11
 };
 
 /* Geometry of the padded uniform-fragment layout.

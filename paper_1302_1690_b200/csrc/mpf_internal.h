@@ -172,6 +172,7 @@ struct MpfBwdArgs {
   int round_tf32;
   float* bias_part;      // nullable: [mpf_bwd_partials(a)][C] per-block sums of din (bias gradient)
   int premul;            // 1: dout already carries act'(y) (the producing dgrad applied it); pooled unused
+  int block_form;        // k = 2: one 2 x 2 block per work item instead of a band (MPF_FLAG_MPF_BWD_BLOCK)
 };
 cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s);
 long long mpf_bwd_partials(const MpfBwdArgs& a);

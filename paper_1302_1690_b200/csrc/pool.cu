@@ -598,6 +598,97 @@ __global__ void __launch_bounds__(256, 3) mpf_bwd_block2_kernel(MpfBwdArgs a, lo
   write_bias_rows(a, bsum, sub, nsub, cv);
 }
 
+// Band form of the k = 2 gather: a thread walks its 2 x 2 block column down a band of
+// kBand2 block rows.  Block row bi needs window patch rows 2bi-1, 2bi, 2bi+1; the next block
+// row's first patch row (2bi+1) is this one's last, so it stays in registers and only two
+// new patch rows (6 windows) are loaded per block instead of 9, with row offsets advanced
+// by one pooled row per step instead of recomputed.  Same candidates in the same (dy, dx)
+// order per element: bitwise the deltas of mpf_bwd_block2_kernel.
+constexpr int kBand2 = 8;
+__global__ void __launch_bounds__(256, 3) mpf_bwd_band2_kernel(MpfBwdArgs a, long long n_units) {
+  const int C = a.C, CV = C / 4;
+  const int tid = threadIdx.x, cv = tid % CV, sub = tid / CV, nsub = 256 / CV;
+  const int Xw = 2 * a.m_c, Yw = 2 * a.m_r;
+  const int MMC = a.m_r * a.m_c * C, mcC = a.m_c * C;
+  const int bj_n = (a.gc + 1) / 2, bi_n = (a.gr + 1) / 2;
+  const int groups_per_row = (bj_n + nsub - 1) / nsub;
+  const int bands = (bi_n + kBand2 - 1) / kBand2;
+  float bsum[4] = {0.f, 0.f, 0.f, 0.f};
+  if (sub < nsub) {
+    for (long long unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
+      const int gj = (int)(unit % groups_per_row);
+      const long long t = unit / groups_per_row;
+      const int band = (int)(t % bands);
+      const int g = (int)(t / bands);
+      const int bj = gj * nsub + sub;
+      if (bj >= bj_n) continue;
+      const int bi0 = band * kBand2, bi1 = min(bi_n, bi0 + kBand2);
+      const float* dsrc = a.dout + (size_t)g * 4 * MMC + cv * 4;
+      const uint8_t* isrc = a.idx + (size_t)g * 4 * MMC + cv * 4;
+      float* dst = a.din + ((size_t)g * a.gr * a.gc) * C + cv * 4;
+      // patch columns wx = 2bj - 1 + v: parity odd, even, odd
+      int coff[3];
+      bool cok[3];
+#pragma unroll
+      for (int v = 0; v < 3; ++v) {
+        const int wx = 2 * bj - 1 + v;
+        cok[v] = wx >= 0 && wx < Xw;
+        coff[v] = cok[v] ? (wx & 1) * MMC + (wx >> 1) * C : 0;
+      }
+      auto load_row = [&](int wy, uint32_t (&ir)[3], float4 (&dr)[3]) {
+        const bool yok = wy >= 0 && wy < Yw;
+        const int rowoff = yok ? (wy & 1) * 2 * MMC + (wy >> 1) * mcC : 0;
+#pragma unroll
+        for (int v = 0; v < 3; ++v) {
+          const bool ok = yok && cok[v];
+          const int off = rowoff + coff[v];
+          ir[v] = ok ? __ldg(reinterpret_cast<const uint32_t*>(isrc + off)) : 0xFFFFFFFFu;
+          dr[v] = ok ? __ldg(reinterpret_cast<const float4*>(dsrc + off)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      };
+      uint32_t id[3][3];
+      float4 d[3][3];
+      load_row(2 * bi0 - 1, id[0], d[0]);
+      for (int bi = bi0; bi < bi1; ++bi) {
+        load_row(2 * bi, id[1], d[1]);
+        load_row(2 * bi + 1, id[2], d[2]);
+#pragma unroll
+        for (int ea = 0; ea < 2; ++ea)
+#pragma unroll
+          for (int eb = 0; eb < 2; ++eb) {
+            const int Y = 2 * bi + ea, X = 2 * bj + eb;
+            if (Y >= a.gr || X >= a.gc) continue;
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+              for (int dx = 0; dx < 2; ++dx) {
+                const uint32_t x = id[ea - dy + 1][eb - dx + 1] ^ ((uint32_t)(dy * 2 + dx) * 0x01010101u);
+                const float4 w = d[ea - dy + 1][eb - dx + 1];
+                if (!(x & 0xFFu)) acc[0] += w.x;
+                if (!(x & 0xFF00u)) acc[1] += w.y;
+                if (!(x & 0xFF0000u)) acc[2] += w.z;
+                if (!(x & 0xFF000000u)) acc[3] += w.w;
+              }
+            float o[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              bsum[q] += acc[q];
+              o[q] = a.round_tf32 ? tf32_rn(acc[q]) : acc[q];
+            }
+            stv<4>(dst + (Y * a.gc + X) * C, o);
+          }
+#pragma unroll
+        for (int v = 0; v < 3; ++v) {  // the last patch row is the next block row's first
+          id[0][v] = id[2][v];
+          d[0][v] = d[2][v];
+        }
+      }
+    }
+  }
+  write_bias_rows(a, bsum, sub, nsub, cv);
+}
+
 // Register-blocked gather for k = 3: a thread owns a 3 x BW block of conv-output elements of
 // one channel vector; the candidate windows form the 5 x (BW + 2) patch rows 3i-2 .. 3i+2.
 // Output row ea needs patch rows ea .. ea+2, so the patch streams through a ring of 3 rows:
@@ -788,8 +879,14 @@ static long long block2_groups(const MpfBwdArgs& a) {
   const long long bj_n = (a.gc + bw - 1) / bw, bi_n = (a.gr + a.k - 1) / a.k;
   return (long long)a.n_frag_in * bi_n * ((bj_n + nsub - 1) / nsub);
 }
+static long long band2_units(const MpfBwdArgs& a) {
+  const int nsub = 256 / (a.C / 4);
+  const long long bj_n = (a.gc + 1) / 2, bi_n = (a.gr + 1) / 2;
+  return (long long)a.n_frag_in * ((bi_n + kBand2 - 1) / kBand2) * ((bj_n + nsub - 1) / nsub);
+}
+static bool use_band2(const MpfBwdArgs& a) { return a.k == 2 && !a.block_form; }
 static int block2_grid(const MpfBwdArgs& a) {
-  const long long g = block2_groups(a);
+  const long long g = use_band2(a) ? band2_units(a) : block2_groups(a);
   const long long cap = 148LL * 8;  // 8 CTAs of 256 threads per SM
   return (int)(g < cap ? (g < 1 ? 1 : g) : cap);
 }
@@ -871,7 +968,8 @@ long long mpf_bwd_partials(const MpfBwdArgs& a) {
 cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s) {
   if (bwd_block2(a)) {
     const size_t smem = 0;
-    if (a.k == 2) mpf_bwd_block2_kernel<<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
+    if (use_band2(a)) mpf_bwd_band2_kernel<<<block2_grid(a), 256, smem, s>>>(a, band2_units(a));
+    else if (a.k == 2) mpf_bwd_block2_kernel<<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
     else mpf_bwd_block3_kernel<3, 3><<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
     return cudaGetLastError();
   }

@@ -471,6 +471,20 @@ def test_head_logits_in_fc1_epilogue(name):
         assert rel_l2(a["grad_sum"][sl], b["grad_sum"][sl]) <= 1e-4, nm
 
 
+@pytest.mark.parametrize("name", ["cfg2", "cfg4s"])
+def test_mpf_bwd_k2_band_matches_blocks(name):
+    """The k = 2 MPF backward walking bands of 2 x 2 blocks (default; the last patch row is
+    reused by the next block row) and one block per work item (MPF_FLAG_MPF_BWD_BLOCK) sum
+    the same candidates in the same order: the forward is untouched and the gradients agree
+    to the grouping of the bias partial sums."""
+    from paper_1302_1690_b200 import _lib as L
+    cfg, a = _run_variant(0, name=name)
+    _, b = _run_variant(L.MPF_FLAG_MPF_BWD_BLOCK, name=name)
+    assert np.array_equal(a["probs"], b["probs"]) and np.array_equal(a["loss"], b["loss"])
+    for nm, sl in param_slices(cfg.layers):
+        assert rel_l2(a["grad_sum"][sl], b["grad_sum"][sl]) <= 1e-5, nm
+
+
 @pytest.mark.parametrize("name", ["cfg2", "cfg4s", "cfg5s"])
 def test_first_conv_mpf_fusion_bitwise(name):
     """The fused first conv + activation + MPF kernel (MPF_FLAG_FUSE_FIRST_POOL)
