@@ -885,6 +885,7 @@ static long long band2_units(const MpfBwdArgs& a) {
   return (long long)a.n_frag_in * ((bi_n + kBand2 - 1) / kBand2) * ((bj_n + nsub - 1) / nsub);
 }
 static bool use_band2(const MpfBwdArgs& a) { return a.k == 2 && !a.block_form; }
+
 static int block2_grid(const MpfBwdArgs& a) {
   const long long g = use_band2(a) ? band2_units(a) : block2_groups(a);
   const long long cap = 148LL * 8;  // 8 CTAs of 256 threads per SM

@@ -472,9 +472,10 @@ def test_head_logits_in_fc1_epilogue(name):
 
 
 @pytest.mark.parametrize("name", ["cfg2", "cfg4s"])
-def test_mpf_bwd_k2_band_matches_blocks(name):
-    """The k = 2 MPF backward walking bands of 2 x 2 blocks (default; the last patch row is
-    reused by the next block row) and one block per work item (MPF_FLAG_MPF_BWD_BLOCK) sum
+def test_mpf_bwd_band_matches_blocks(name):
+    """The k = 2 MPF backward walking bands of 2 x 2 blocks (default; the window row shared
+    by consecutive block rows stays in registers) and one block per work item
+    (MPF_FLAG_MPF_BWD_BLOCK) sum
     the same candidates in the same order: the forward is untouched and the gradients agree
     to the grouping of the bias partial sums."""
     from paper_1302_1690_b200 import _lib as L
