@@ -599,20 +599,19 @@ __global__ void __launch_bounds__(256, 3) mpf_bwd_block2_kernel(MpfBwdArgs a, lo
 }
 
 // Band form of the k = 2 gather: a thread walks its 2 x 2 block column down a band of
-// kBand2 block rows.  Block row bi needs window patch rows 2bi-1, 2bi, 2bi+1; the next block
+// `band` block rows.  Block row bi needs window patch rows 2bi-1, 2bi, 2bi+1; the next block
 // row's first patch row (2bi+1) is this one's last, so it stays in registers and only two
 // new patch rows (6 windows) are loaded per block instead of 9, with row offsets advanced
 // by one pooled row per step instead of recomputed.  Same candidates in the same (dy, dx)
 // order per element: bitwise the deltas of mpf_bwd_block2_kernel.
-constexpr int kBand2 = 8;
-__global__ void __launch_bounds__(256, 3) mpf_bwd_band2_kernel(MpfBwdArgs a, long long n_units) {
+__global__ void __launch_bounds__(256, 3) mpf_bwd_band2_kernel(MpfBwdArgs a, long long n_units, int band_rows) {
   const int C = a.C, CV = C / 4;
   const int tid = threadIdx.x, cv = tid % CV, sub = tid / CV, nsub = 256 / CV;
   const int Xw = 2 * a.m_c, Yw = 2 * a.m_r;
   const int MMC = a.m_r * a.m_c * C, mcC = a.m_c * C;
   const int bj_n = (a.gc + 1) / 2, bi_n = (a.gr + 1) / 2;
   const int groups_per_row = (bj_n + nsub - 1) / nsub;
-  const int bands = (bi_n + kBand2 - 1) / kBand2;
+  const int bands = (bi_n + band_rows - 1) / band_rows;
   float bsum[4] = {0.f, 0.f, 0.f, 0.f};
   if (sub < nsub) {
     for (long long unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
@@ -622,7 +621,7 @@ __global__ void __launch_bounds__(256, 3) mpf_bwd_band2_kernel(MpfBwdArgs a, lon
       const int g = (int)(t / bands);
       const int bj = gj * nsub + sub;
       if (bj >= bj_n) continue;
-      const int bi0 = band * kBand2, bi1 = min(bi_n, bi0 + kBand2);
+      const int bi0 = band * band_rows, bi1 = min(bi_n, bi0 + band_rows);
       const float* dsrc = a.dout + (size_t)g * 4 * MMC + cv * 4;
       const uint8_t* isrc = a.idx + (size_t)g * 4 * MMC + cv * 4;
       float* dst = a.din + ((size_t)g * a.gr * a.gc) * C + cv * 4;
@@ -879,10 +878,21 @@ static long long block2_groups(const MpfBwdArgs& a) {
   const long long bj_n = (a.gc + bw - 1) / bw, bi_n = (a.gr + a.k - 1) / a.k;
   return (long long)a.n_frag_in * bi_n * ((bj_n + nsub - 1) / nsub);
 }
-static long long band2_units(const MpfBwdArgs& a) {
+// block rows per band: long bands (up to 32; measured 8 -> 32: 4.6 -> 4.8-5.2 TB/s on cfg4)
+// while the grid keeps about two waves of 3 CTAs per SM
+static int band2_rows(const MpfBwdArgs& a) {
   const int nsub = 256 / (a.C / 4);
   const long long bj_n = (a.gc + 1) / 2, bi_n = (a.gr + 1) / 2;
-  return (long long)a.n_frag_in * ((bi_n + kBand2 - 1) / kBand2) * ((bj_n + nsub - 1) / nsub);
+  const long long cols = (long long)a.n_frag_in * ((bj_n + nsub - 1) / nsub);
+  long long r = cols * bi_n / (148LL * 6);
+  if (r > 32) r = 32;
+  if (r < 1) r = 1;
+  return (int)r;
+}
+static long long band2_units(const MpfBwdArgs& a) {
+  const int nsub = 256 / (a.C / 4), rows = band2_rows(a);
+  const long long bj_n = (a.gc + 1) / 2, bi_n = (a.gr + 1) / 2;
+  return (long long)a.n_frag_in * ((bi_n + rows - 1) / rows) * ((bj_n + nsub - 1) / nsub);
 }
 static bool use_band2(const MpfBwdArgs& a) { return a.k == 2 && !a.block_form; }
 
@@ -969,7 +979,7 @@ long long mpf_bwd_partials(const MpfBwdArgs& a) {
 cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s) {
   if (bwd_block2(a)) {
     const size_t smem = 0;
-    if (use_band2(a)) mpf_bwd_band2_kernel<<<block2_grid(a), 256, smem, s>>>(a, band2_units(a));
+    if (use_band2(a)) mpf_bwd_band2_kernel<<<block2_grid(a), 256, smem, s>>>(a, band2_units(a), band2_rows(a));
     else if (a.k == 2) mpf_bwd_block2_kernel<<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
     else mpf_bwd_block3_kernel<3, 3><<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
     return cudaGetLastError();
