@@ -21,6 +21,8 @@
 //
 // All index arithmetic is 32-bit per fragment; only final offsets are 64-bit.
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -774,6 +776,152 @@ __global__ void __launch_bounds__(256) mpf_bwd_block3_kernel(MpfBwdArgs a, long 
   write_bias_rows(a, bsum, sub, nsub, cv);
 }
 
+// Scatter form of the MPF backward (k = 3 default; premul deltas).  Alg. 4
+// read forwards: every window routes its delta to the one conv-output element its argmax names,
+// instead of every element testing its k^2 candidate windows (the gathers above spend k^2
+// predicated adds per element and channel; this kernel spends one shared-memory add per window).
+// Windows are grouped into k x k blocks (block (B, bx) = window rows kB .. kB+k-1, columns
+// kbx .. kbx+k-1); a block's targets lie in rows kB .. kB+2k-2 and columns kbx .. kbx+2k-2, so
+// blocks of one block row whose bx differ by 2 never share a target.  A CTA owns an output tile
+// (rows [Y0, Y1), columns [X0, X1), a slice of CS channels) of one input fragment and walks its
+// block rows top to bottom: per block row, the even-bx blocks and then the odd-bx blocks add
+// their deltas into a shared-memory ring of 2k accumulator rows (one thread per (block, channel),
+// no two threads of a phase on one element, no atomics), then output rows kB .. kB+k-1 are
+// complete (no later block row reaches them) and are written out, zeroed and summed into the
+// bias partials.  Windows of the block row above the tile and of the block column left of it
+// (halo) are processed too, keeping only targets inside the tile, so every element receives
+// all its contributions from one CTA in one fixed order: block row, then bx parity, then window
+// (u, v) row-major — deterministic and independent of the tiling.  (The gathers sum in (dy, dx)
+// order instead; the two agree to fp32 rounding.)
+struct ScatterGeo {
+  int CS, n_cs, NBX, n_cx, BR, n_bb, T;  // T = threads = (NBX / 2 + 1) * CS: one block per thread and phase
+  size_t smem;
+  long long units;  // CTAs / n_cs: rows of bias partials
+};
+constexpr int kScatterRing = 8;  // accumulator ring rows (a power of two >= 2k - 1)
+
+template <int K>
+__global__ void __launch_bounds__(1024) mpf_bwd_scatter_kernel(MpfBwdArgs a, ScatterGeo s) {
+  // ring of kRing accumulator rows (slot = row mod kRing; rows kB .. kB+2k-2 of one block row
+  // are distinct slots), each K*NBX + 2K - 1 columns: K columns left of the tile and K - 1
+  // right of it catch the halo blocks' out-of-tile targets (never written out)
+  extern __shared__ __align__(16) float acc[];
+  constexpr int HL = K, kRing = kScatterRing;
+  static_assert(2 * K - 1 <= kRing && (kRing & (kRing - 1)) == 0, "ring too small");
+  const int CS = s.CS, T = s.T, tid = threadIdx.x;  // blockDim.x == T, a multiple of CS
+  const int C = a.C;
+  int u_ = blockIdx.x;
+  const int cs = u_ % s.n_cs; u_ /= s.n_cs;
+  const int cx = u_ % s.n_cx; u_ /= s.n_cx;
+  const int bb = u_ % s.n_bb;
+  const int g = u_ / s.n_bb;
+  const int ch = tid % CS, sub = tid / CS, nsub = T / CS;
+  const int TXo = K * s.NBX, RW = TXo + 2 * K - 1, ROW = RW * CS;  // ring row pitch (floats)
+  const int X0 = TXo * cx, X1 = min(a.gc, X0 + TXo);
+  const int Y0 = K * s.BR * bb, Y1 = min(a.gr, Y0 + K * s.BR);
+  // block (B, bx) has all its k x k windows iff B < m_r and bx < m_c
+  const int bxa = max(0, s.NBX * cx - 1), bxb = min(a.m_c, s.NBX * (cx + 1));
+  const int MMC = a.m_r * a.m_c * C, mcC = a.m_c * C;
+  const float* dsrc = a.dout + (size_t)g * K * K * MMC + cs * CS + ch;
+  const uint8_t* isrc = a.idx + (size_t)g * K * K * MMC + cs * CS + ch;
+  for (int i = tid; i < kRing * ROW; i += T) acc[i] = 0.f;
+  const int Bs = bb > 0 ? Y0 / K - 1 : 0, Be = (Y1 + K - 1) / K;
+  // this thread's block of phase p (bx parity p) in block row B, or -1
+  auto block_of = [&](int B, int p) -> int {
+    const int bx = bxa + ((p - bxa) & 1) + 2 * sub;
+    return (B < a.m_r && B < Be && bx < bxb) ? bx : -1;
+  };
+  auto load = [&](int B, int bx, uint32_t (&id)[K][K], float (&d)[K][K]) {
+    if (bx < 0) return;
+    const int o = B * mcC + bx * C;
+    const uint8_t* ip = isrc + o;
+    const float* dp = dsrc + o;
+#pragma unroll
+    for (int u = 0; u < K; ++u)
+#pragma unroll
+      for (int v = 0; v < K; ++v) {
+        id[u][v] = __ldg(ip + (u * K + v) * MMC);
+        d[u][v] = __ldg(dp + (u * K + v) * MMC);
+      }
+  };
+  auto scatter = [&](int B, int bx, const uint32_t (&id)[K][K], const float (&d)[K][K]) {
+    float* base = acc + (K * bx - X0 + HL) * CS + ch;
+#pragma unroll
+    for (int u = 0; u < K; ++u)
+#pragma unroll
+      for (int v = 0; v < K; ++v) {
+        const int q = (int)id[u][v];
+        const int dy = q / K, dx = q - K * dy;
+        base[((K * B + u + dy) & (kRing - 1)) * ROW + (v + dx) * CS] += d[u][v];
+      }
+  };
+  // write-out mapping: 4-channel vectors, thread (column lane, vector) with a fixed vector
+  const int CV = CS / 4, vq = tid % CV, csub = tid / CV, ncsub = T / CV;
+  float bsum[4] = {0.f, 0.f, 0.f, 0.f};
+  const int W = X1 - X0;
+  float* dst = a.din + ((size_t)g * a.gr * a.gc + X0) * C + cs * CS + vq * 4;
+  // rows kB .. kB+k-1 are complete after block row B (no later block row reaches them): write
+  // out and zero them (the halo block row above the tile only zeroes: its rows belong to the
+  // tile above), bias partials
+  auto write_out = [&](int B) {
+    for (int r = 0; r < K; ++r) {
+      const int rr = K * B + r;
+      if (rr >= Y1) break;
+      float* q = acc + (rr & (kRing - 1)) * ROW + HL * CS + vq * 4;
+      int c0 = 0;
+      if (rr >= Y0) {
+        float* op = dst + ((size_t)rr * a.gc + csub) * C;
+        float* qp = q + csub * CS;
+        const size_t ostep = (size_t)ncsub * C;
+        const int qstep = ncsub * CS;
+        for (int col = csub; col < W; col += ncsub, op += ostep, qp += qstep) {
+          const float4 v = *reinterpret_cast<float4*>(qp);
+          *reinterpret_cast<float4*>(qp) = make_float4(0.f, 0.f, 0.f, 0.f);
+          bsum[0] += v.x; bsum[1] += v.y; bsum[2] += v.z; bsum[3] += v.w;
+          float4 w = v;
+          if (a.round_tf32) { w.x = tf32_rn(v.x); w.y = tf32_rn(v.y); w.z = tf32_rn(v.z); w.w = tf32_rn(v.w); }
+          *reinterpret_cast<float4*>(op) = w;
+        }
+        c0 = W;
+      }
+      // the columns not written out (halo; the whole row above the tile): zero for reuse
+      for (int j = csub; j < RW - c0; j += ncsub) {
+        const int col = j < HL ? j - HL : c0 + j - HL;
+        *reinterpret_cast<float4*>(q + col * CS) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  };
+  uint32_t idA[K][K], idB[K][K];
+  float dA[K][K], dB[K][K];
+  int bxA = block_of(Bs, 0), bxB;
+  load(Bs, bxA, idA, dA);
+  __syncthreads();
+  for (int B = Bs; B < Be; ++B) {
+    // phase 0 (even bx) from set A while phase 1's windows load into set B; then phase 1 from
+    // set B while the next block row's phase 0 loads into set A
+    bxB = block_of(B, 1);
+    load(B, bxB, idB, dB);
+    if (bxA >= 0) scatter(B, bxA, idA, dA);
+    __syncthreads();
+    bxA = block_of(B + 1, 0);
+    load(B + 1, bxA, idA, dA);
+    if (bxB >= 0) scatter(B, bxB, idB, dB);
+    __syncthreads();
+    write_out(B);
+    __syncthreads();
+  }
+  if (a.bias_part == nullptr) return;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) acc[i * T + tid] = bsum[i];  // fixed-order reduction per channel
+  __syncthreads();
+  if (tid < CS) {
+    const int v = tid / 4, i = tid % 4;
+    float t = 0.f;
+    for (int j = 0; j < ncsub; ++j) t += acc[i * T + j * CV + v];
+    a.bias_part[(size_t)(blockIdx.x / s.n_cs) * C + cs * CS + tid] = t;
+  }
+}
+
 // ----------------------------------------------------------------------------- channel sums
 // Generic per-channel partials of a [P][C] tensor (bias gradient of a conv whose delta
 // comes from a dgrad, i.e. a conv followed by another conv).
@@ -969,7 +1117,43 @@ static void bwd_geometry(const MpfBwdArgs& a, int V, dim3* grid, dim3* blk) {
   *grid = dim3((a.gc + ty - 1) / ty, (a.gr + band - 1) / band, a.n_frag_in < 65535 ? a.n_frag_in : 65535);
 }
 
+// k = 3 (premul, C % 4 == 0 or C <= 32): the scatter; MPF_FLAG_MPF_BWD_GATHER keeps the gather
+static bool scatter_geo(const MpfBwdArgs& a, ScatterGeo* s) {
+  if (!(a.k == 3 && a.premul && !a.gather_form)) return false;
+  const int K = a.k, C = a.C;
+  if (C % 4) return false;  // 4-channel write-out vectors
+  int CS = C;
+  if (C > 32) {
+    if (C % 32 == 0) CS = 32;
+    else if (C % 24 == 0) CS = 24;
+    else if (C % 16 == 0) CS = 16;
+    else return false;
+  }
+  s->CS = CS;
+  s->n_cs = C / CS;
+  // widest tile of NBX blocks whose ring fits ~64 KB (three CTAs per SM) within 1024 threads
+  const size_t budget = 64 * 1024 + 512;
+  int nbx_max = (int)((budget / ((size_t)kScatterRing * CS * sizeof(float)) - (2 * K - 1)) / K);
+  while (nbx_max > 1 && (nbx_max / 2 + 1) * CS > 1024) --nbx_max;
+  if (nbx_max < 1 || (nbx_max / 2 + 1) * CS > 1024) return false;
+  const int blk_cols = (a.gc + K - 1) / K, blk_rows = (a.gr + K - 1) / K;
+  s->n_cx = (blk_cols + nbx_max - 1) / nbx_max;
+  s->NBX = (blk_cols + s->n_cx - 1) / s->n_cx;
+  s->T = (s->NBX / 2 + 1) * CS;  // blocks per phase <= NBX / 2 + 1 (the halo block included)
+  const long long per_row = (long long)a.n_frag_in * s->n_cx * s->n_cs;
+  long long br = (blk_rows * per_row + 148LL * 9 - 1) / (148LL * 9);  // about three waves of 3 CTAs/SM
+  if (br < 4) br = 4;
+  if (br > blk_rows) br = blk_rows;
+  s->n_bb = (int)((blk_rows + br - 1) / br);
+  s->BR = (blk_rows + s->n_bb - 1) / s->n_bb;
+  s->smem = sizeof(float) * std::max((size_t)kScatterRing * (K * s->NBX + 2 * K - 1) * CS, (size_t)4 * s->T);
+  s->units = (long long)a.n_frag_in * s->n_bb * s->n_cx;
+  return true;
+}
+
 long long mpf_bwd_partials(const MpfBwdArgs& a) {
+  ScatterGeo sg;
+  if (scatter_geo(a, &sg)) return sg.units;
   if (bwd_block2(a)) return (long long)block2_grid(a) * (a.C / 4 <= 32 ? 8 : 256 / (a.C / 4));
   dim3 g, b;
   bwd_geometry(a, a.C % 4 == 0 ? 4 : 1, &g, &b);
@@ -977,6 +1161,15 @@ long long mpf_bwd_partials(const MpfBwdArgs& a) {
 }
 
 cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s) {
+  ScatterGeo sg;
+  if (scatter_geo(a, &sg)) {
+    if (sg.units * sg.n_cs > 0x7fffffffLL) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(mpf_bwd_scatter_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sg.smem);
+    if (e != cudaSuccess) return e;
+    mpf_bwd_scatter_kernel<3><<<(unsigned)(sg.units * sg.n_cs), sg.T, sg.smem, s>>>(a, sg);
+    return cudaGetLastError();
+  }
   if (bwd_block2(a)) {
     const size_t smem = 0;
     if (use_band2(a)) mpf_bwd_band2_kernel<<<block2_grid(a), 256, smem, s>>>(a, band2_units(a), band2_rows(a));
