@@ -185,6 +185,9 @@ def main():
     ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the timed steps eagerly")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="multi-rank gradient exchange: pushes into peer memory summed by the SGD kernel "
+                         "(default; NCCL if a GPU pair lacks P2P) or bucketed NCCL all-reduces")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-px-per-thread", type=int, default=1)
@@ -238,15 +241,31 @@ def main():
             dist.all_reduce(c)
         counts.append(float(c.item()))
     stream = torch.cuda.current_stream(dev)
-    # the gradient exchange (a7): one NCCL all-reduce per bucket, started by the library's
-    # gradient-ready hook as soon as the backward has produced that bucket, so it overlaps
-    # the rest of the backward; waited for before the SGD step
+    # the gradient exchange (a7).  Default: peer memory — the library's backward pushes each
+    # gradient bucket into every rank's exchange buffer over NVLink as soon as it is final and
+    # the SGD kernel sums the ranks' slots (dist.PeerExchange).  Fallback / --exchange nccl: one
+    # NCCL all-reduce per bucket started by the gradient-ready hook, waited for before the SGD.
     buckets = None
+    peer = None
+    exchange_kind = "local"
     if use_dist and not one_gpu_check:
-        buckets = D.BucketAllReduce(net.grads)
-        net.set_grad_hook(buckets)
+        ok = args.exchange == "peer" and all(
+            r == local or torch.cuda.can_device_access_peer(local, r) for r in range(world))
+        okt = torch.tensor([1 if ok else 0], device=dev, dtype=torch.int32)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        if okt.item():
+            peer = D.PeerExchange(net)
+            exchange_kind = "peer"
+        else:
+            buckets = D.BucketAllReduce(net.grads)
+            net.set_grad_hook(buckets)
+            exchange_kind = "nccl"
+    elif use_dist:
+        exchange_kind = "gloo"
 
     def exchange():
+        if peer is not None:
+            return  # inside the backward (pushes) and the SGD kernel (sum)
         if buckets is not None:
             buckets.wait()
         else:
@@ -428,10 +447,13 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "tf32" if any_tc else "f32",
                 "data": "synthetic (seeded steel-like images, BASELINE.json shapes)",
-                "config": dict(workload_config(cfg, world), cuda_graph=graphs is not None), "e2e": e2e,
+                "config": dict(workload_config(cfg, world), cuda_graph=graphs is not None,
+                               grad_exchange=exchange_kind), "e2e": e2e,
                 "gpu_launches": launches,
                 "roofline": roof, "cpu_baseline": cpu, "clocks": clocks}
         print(json.dumps(line), flush=True)
+    if peer is not None:
+        peer.close()
     if use_dist:
         dist.destroy_process_group()
 

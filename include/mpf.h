@@ -313,6 +313,54 @@ mpf_status mpf_net_set_grad_hook(mpf_net* net, mpf_grad_ready_fn fn, void* user)
 mpf_status mpf_sgd_step(mpf_net* net, float lr, float grad_scale, void* stream);
 
 /*
+ * Data-parallel gradient exchange over peer memory: Alg. 2's sum
+ * over fragments and positions extended over the images of every rank,
+ * without a separate collective.  Each rank owns one exchange buffer that every other rank
+ * can address (NVLink P2P through CUDA IPC: mpf_ipc_export / mpf_ipc_open; or, on one GPU,
+ * plain device pointers).  While attached:
+ *   - the backward copies every gradient bucket, as soon as it is final (the points
+ *     mpf_net_set_grad_hook reports, on the same stream), into this rank's slot of EVERY
+ *     rank's buffer, then raises this rank's flag for that bucket in every buffer (release,
+ *     system scope) — the transfer overlaps the rest of the backward;  with
+ *     push_in_backward = 0 nothing is pushed by the backward and the caller calls
+ *     mpf_exchange_push once after its last backward of the step (micro-batches);
+ *   - mpf_exchange_sgd_step waits (acquire) until every rank's flags carry this step's
+ *     epoch, sums the ranks' slots in rank order 0 .. world-1 (the same fp32 sum on every
+ *     rank, so the parameters stay bitwise identical across ranks), applies
+ *     theta <- theta - lr * grad_scale * sum, zeroes this rank's gradient buffer and advances
+ *     the epoch.  Slots alternate between two parities by epoch, so a rank one step ahead
+ *     never overwrites a slot a slower rank still reads.
+ * A wait that exceeds ~10 s (a rank that never pushes) gives up, leaves theta unchanged and
+ * makes mpf_check return MPF_ERR_INTERNAL.  All calls are asynchronous on `stream`.
+ *
+ * mpf_exchange_bytes: size of one rank's buffer for `world` ranks.  The caller allocates it
+ * on the rank's device, ZERO-FILLED, before any rank attaches (e.g. torch.zeros), and
+ * keeps it alive until every rank has detached.
+ * mpf_exchange_attach: d_bufs[r] = rank r's buffer as addressable from this process
+ * (d_bufs[rank] = the own buffer); host array of `world` pointers, copied.  MPF_ERR_ARG for
+ * rank / world out of range (world <= 64) or NULL pointers; MPF_ERR_STATE if not bound.
+ * mpf_exchange_detach: back to mpf_sgd_step's local update (no device work).
+ */
+mpf_status mpf_exchange_bytes(const mpf_net* net, int32_t world, size_t* bytes);
+mpf_status mpf_exchange_attach(mpf_net* net, int32_t rank, int32_t world, void* const* d_bufs,
+                               int32_t push_in_backward);
+mpf_status mpf_exchange_push(mpf_net* net, void* stream);
+mpf_status mpf_exchange_sgd_step(mpf_net* net, float lr, float grad_scale, void* stream);
+mpf_status mpf_exchange_detach(mpf_net* net);
+
+/*
+ * CUDA IPC for the exchange buffers (legacy cudaIpc*, P2P over NVLink between the processes
+ * of one node).  mpf_ipc_export: 64-byte handle of the allocation containing d_ptr (any
+ * pointer into a cudaMalloc allocation, e.g. a PyTorch tensor) and d_ptr's byte offset in
+ * it.  mpf_ipc_open: maps another process's allocation, *d_ptr = its base + offset.
+ * mpf_ipc_close: unmaps (pass the pointer mpf_ipc_open returned).  MPF_ERR_CUDA on failure
+ * (e.g. expandable-segment allocations, which cudaIpc cannot export).
+ */
+mpf_status mpf_ipc_export(const void* d_ptr, void* handle64, uint64_t* offset);
+mpf_status mpf_ipc_open(const void* handle64, uint64_t offset, void** d_ptr);
+mpf_status mpf_ipc_close(void* d_ptr, uint64_t offset);
+
+/*
  * One end-to-end step on HOST buffers: async copy h_images [n, in_channels, H, W]
  * and h_labels [n, out_rows, out_cols] into the bound staging area, mpf_train_step,
  * and an async copy of the per-image losses to h_loss[n].  If apply_sgd,

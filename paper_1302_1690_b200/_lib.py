@@ -40,7 +40,8 @@ EXPORTS = ("mpf_version", "mpf_last_error", "mpf_net_create", "mpf_net_destroy",
            "mpf_lbfgs_state_bytes", "mpf_lbfgs_create", "mpf_lbfgs_destroy", "mpf_lbfgs_reset", "mpf_lbfgs_set_gradient", "mpf_lbfgs_direction",
            "mpf_lbfgs_trial", "mpf_lbfgs_accept", "mpf_lbfgs_reject", "mpf_lbfgs_step",
            "mpf_debug_tape", "mpf_check", "mpf_profile_begin",
-           "mpf_profile_end")
+           "mpf_profile_end", "mpf_exchange_bytes", "mpf_exchange_attach", "mpf_exchange_push",
+           "mpf_exchange_sgd_step", "mpf_exchange_detach", "mpf_ipc_export", "mpf_ipc_open", "mpf_ipc_close")
 
 
 # void (*mpf_grad_ready_fn)(void* user, int32_t layer, int64_t offset, int64_t count, void* stream)
@@ -151,6 +152,22 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.mpf_profile_begin.argtypes = [vp, i32]
     lib.mpf_profile_end.restype = st
     lib.mpf_profile_end.argtypes = [vp, ctypes.POINTER(MpfKernelStat), i32, ctypes.POINTER(i32)]
+    lib.mpf_exchange_bytes.restype = st
+    lib.mpf_exchange_bytes.argtypes = [vp, i32, u64p]
+    lib.mpf_exchange_attach.restype = st
+    lib.mpf_exchange_attach.argtypes = [vp, i32, i32, ctypes.POINTER(vp), i32]
+    lib.mpf_exchange_push.restype = st
+    lib.mpf_exchange_push.argtypes = [vp, vp]
+    lib.mpf_exchange_sgd_step.restype = st
+    lib.mpf_exchange_sgd_step.argtypes = [vp, ctypes.c_float, ctypes.c_float, vp]
+    lib.mpf_exchange_detach.restype = st
+    lib.mpf_exchange_detach.argtypes = [vp]
+    lib.mpf_ipc_export.restype = st
+    lib.mpf_ipc_export.argtypes = [vp, vp, u64p]
+    lib.mpf_ipc_open.restype = st
+    lib.mpf_ipc_open.argtypes = [vp, ctypes.c_uint64, ctypes.POINTER(vp)]
+    lib.mpf_ipc_close.restype = st
+    lib.mpf_ipc_close.argtypes = [vp, ctypes.c_uint64]
     return lib
 
 

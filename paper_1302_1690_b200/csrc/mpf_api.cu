@@ -6,6 +6,7 @@
 //   loss     (MCCE per pixel, dL/dx_hat first)
 //   backward (Alg. 4 for MPF, Alg. 2 accumulation)
 //   SGD
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -821,6 +822,7 @@ static mpf_status backward_impl(Net* N, const uint8_t* d_labels, const float* h_
   // remaining layers in reverse.  Invariant: dcur holds the delta of a[l+1] at the
   // pre-activation (CONV/FC output) or the value (pooled output).
   long long hook_end = N->n_params;  // gradient entries [hook_end, n_params) already reported
+  int bucket = 0;                    // index of the next gradient bucket (exchange flags)
   bool bias_done = true;  // layer L-1's bias came from the head
   bool premul = false;    // dcur already carries act' of the conv feeding the next pool
   float* wpack = scr(N, N->off_wpack);
@@ -874,10 +876,13 @@ static mpf_status backward_impl(Net* N, const uint8_t* d_labels, const float* h_
       MPF_CUDA(cudaEventRecord(N->ev_buf[ci], sw));
       pending[ci] = true;
     }
-    if (N->grad_hook) {  // every W / b of layers l .. L is final in the order of sw
-      N->grad_hook(N->grad_hook_user, l, P.w_off, hook_end - P.w_off, (void*)sw);
-      hook_end = P.w_off;
-    }
+    // every W / b of layers l .. L is final in the order of sw: one gradient bucket
+    if (N->ex_on && N->ex_in_bwd)  // into every rank's exchange buffer, overlapping the rest
+      MPF_CUDA(launch_exchange_push(N->grads, P.w_off, hook_end - P.w_off, N->ex_own, N->ex_layout, N->ex_rank,
+                                    bucket, sw));
+    if (N->grad_hook) N->grad_hook(N->grad_hook_user, l, P.w_off, hook_end - P.w_off, (void*)sw);
+    hook_end = P.w_off;
+    ++bucket;
     if (l == 0) break;
     // dgrad: delta of a[l] = full correlation of dcur with the rotated kernel.  When a[l]
     // is a pooled tensor, the epilogue already multiplies by act'(pooled value) of the conv
@@ -1306,9 +1311,74 @@ mpf_status mpf_lbfgs_step(mpf_lbfgs* lb, const float* d_images, int32_t n, const
   return MPF_OK;
 }
 
+// gradient buckets one backward reports (conv / FC layers but the softmax FC, which goes with
+// the last hidden layer's bucket)
+static int n_grad_buckets(const mpf_net* N) {
+  int nb = 0;
+  for (int l = 0; l < N->n_layers; ++l) nb += N->lp[l].L.kind != MPF_POOL;
+  return nb > 1 ? nb - 1 : 1;
+}
+
+mpf_status mpf_exchange_bytes(const mpf_net* N, int32_t world, size_t* bytes) {
+  if (!N || !bytes) return fail(MPF_ERR_ARG, "NULL argument");
+  if (world < 1 || world > ExLayout::kMaxWorld) return fail(MPF_ERR_ARG, "world out of range [1, 64]");
+  *bytes = exchange_layout(world, N->n_layers, N->n_params).bytes;
+  return MPF_OK;
+}
+
+mpf_status mpf_exchange_attach(mpf_net* N, int32_t rank, int32_t world, void* const* d_bufs, int32_t push_in_backward) {
+  if (!N || !d_bufs) return fail(MPF_ERR_ARG, "NULL argument");
+  if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound (mpf_net_bind)");
+  if (world < 1 || world > ExLayout::kMaxWorld) return fail(MPF_ERR_ARG, "world out of range [1, 64]");
+  if (rank < 0 || rank >= world) return fail(MPF_ERR_ARG, "rank out of range [0, world)");
+  uint64_t peers[ExLayout::kMaxWorld];
+  for (int r = 0; r < world; ++r) {
+    if (!d_bufs[r]) return fail(MPF_ERR_ARG, "NULL exchange buffer of rank " + std::to_string(r));
+    if ((uintptr_t)d_bufs[r] % 256) return fail(MPF_ERR_ARG, "exchange buffers must be 256-byte aligned");
+    peers[r] = (uint64_t)(uintptr_t)d_bufs[r];
+  }
+  N->ex_layout = exchange_layout(world, N->n_layers, N->n_params);
+  N->ex_own = (char*)d_bufs[rank];
+  N->ex_rank = rank;
+  N->ex_in_bwd = push_in_backward != 0;
+  MPF_CUDA(cudaMemcpy(N->ex_own + ExLayout::kPeers, peers, sizeof(uint64_t) * world, cudaMemcpyHostToDevice));
+  N->ex_on = true;
+  return MPF_OK;
+}
+
+mpf_status mpf_exchange_detach(mpf_net* N) {
+  if (!N) return fail(MPF_ERR_ARG, "NULL net");
+  N->ex_on = false;
+  N->ex_own = nullptr;
+  return MPF_OK;
+}
+
+mpf_status mpf_exchange_push(mpf_net* N, void* stream) {
+  if (!N) return fail(MPF_ERR_ARG, "NULL net");
+  if (!N->ex_on) return fail(MPF_ERR_STATE, "no exchange attached (mpf_exchange_attach)");
+  if (N->ex_in_bwd) return fail(MPF_ERR_STATE, "the backward pushes (attached with push_in_backward = 1)");
+  cudaStream_t s = (cudaStream_t)stream;
+  LAUNCH(N, s, "exchange_push", -1, 0.0, 4.0 * (1 + N->ex_layout.world) * N->n_params,
+         launch_exchange_push(N->grads, 0, N->n_params, N->ex_own, N->ex_layout, N->ex_rank, 0, s));
+  return MPF_OK;
+}
+
+mpf_status mpf_exchange_sgd_step(mpf_net* N, float lr, float scale, void* stream) {
+  if (!N) return fail(MPF_ERR_ARG, "NULL net");
+  if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound");
+  if (!N->ex_on) return fail(MPF_ERR_STATE, "no exchange attached (mpf_exchange_attach)");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nb = N->ex_in_bwd ? n_grad_buckets(N) : 1;
+  LAUNCH(N, s, "exchange_sgd", -1, (1.0 + N->ex_layout.world) * N->n_params,
+         4.0 * (N->ex_layout.world + 3) * N->n_params,
+         launch_exchange_sgd(N->params, N->grads, lr, scale, N->ex_own, N->ex_layout, nb, s));
+  return MPF_OK;
+}
+
 mpf_status mpf_sgd_step(mpf_net* N, float lr, float scale, void* stream) {
   if (!N) return fail(MPF_ERR_ARG, "NULL net");
   if (!N->bound) return fail(MPF_ERR_STATE, "net is not bound");
+  if (N->ex_on) return mpf_exchange_sgd_step(N, lr, scale, stream);
   cudaStream_t s = (cudaStream_t)stream;
   LAUNCH(N, s, "sgd", -1, 2.0 * N->n_params, 16.0 * N->n_params,
          launch_sgd(N->params, N->grads, N->n_params, lr, scale, s));
@@ -1463,6 +1533,55 @@ mpf_status mpf_check(mpf_net* N, void* stream) {
       return fail(MPF_ERR_DATA, "a label >= classes (and != 255) was found; it was ignored");
     }
   }
+  if (N->ex_on) {
+    uint32_t t = 0;
+    MPF_CUDA(cudaMemcpy(&t, N->ex_own + ExLayout::kTimeout, sizeof(t), cudaMemcpyDeviceToHost));
+    if (t)
+      return fail(MPF_ERR_INTERNAL, "gradient exchange: timed out waiting for rank " + std::to_string(t - 1) +
+                                        "; parameters not updated");
+  }
+  return MPF_OK;
+}
+
+// ---------------------------------------------------------------- CUDA IPC (exchange buffers)
+typedef CUresult (*PFN_getAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+mpf_status mpf_ipc_export(const void* d_ptr, void* handle64, uint64_t* offset) {
+  if (!d_ptr || !handle64 || !offset) return fail(MPF_ERR_ARG, "NULL argument");
+  static PFN_getAddressRange get_range = nullptr;
+  if (!get_range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return fail(MPF_ERR_CUDA, "cuMemGetAddressRange entry point not found");
+    get_range = (PFN_getAddressRange)fn;
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, (CUdeviceptr)(uintptr_t)d_ptr) != CUDA_SUCCESS)
+    return fail(MPF_ERR_CUDA, "cuMemGetAddressRange failed (not a device allocation?)");
+  cudaIpcMemHandle_t h;
+  MPF_CUDA(cudaIpcGetMemHandle(&h, (void*)(uintptr_t)base));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(handle64, &h, sizeof(h));
+  *offset = (uint64_t)((uintptr_t)d_ptr - (uintptr_t)base);
+  return MPF_OK;
+}
+
+mpf_status mpf_ipc_open(const void* handle64, uint64_t offset, void** d_ptr) {
+  if (!handle64 || !d_ptr) return fail(MPF_ERR_ARG, "NULL argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  void* base = nullptr;
+  MPF_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  *d_ptr = (char*)base + offset;
+  return MPF_OK;
+}
+
+mpf_status mpf_ipc_close(void* d_ptr, uint64_t offset) {
+  if (!d_ptr) return fail(MPF_ERR_ARG, "NULL argument");
+  MPF_CUDA(cudaIpcCloseMemHandle((char*)d_ptr - offset));
   return MPF_OK;
 }
 

@@ -52,6 +52,15 @@ struct Prof {
   std::vector<ProfRec> recs;
 };
 
+// peer-memory gradient exchange (exchange.cu): byte layout of one rank's buffer
+struct ExLayout {
+  static constexpr size_t kEpoch = 0, kSgdCnt = 8, kTimeout = 12, kPushCnt = 256, kPeers = 512, kFlags = 1024;
+  static constexpr int kMaxWorld = 64;
+  int world = 1, nbmax = 1;
+  long long n_params = 0;
+  size_t slots = 0, bytes = 0;
+};
+
 struct Net {
   mpf_config cfg{};
   Prof prof;
@@ -87,6 +96,11 @@ struct Net {
   // data-parallel gradient buckets (mpf_net_set_grad_hook)
   mpf_grad_ready_fn grad_hook = nullptr;
   void* grad_hook_user = nullptr;
+  // peer-memory gradient exchange (mpf_exchange_attach)
+  bool ex_on = false, ex_in_bwd = true;
+  int ex_rank = 0;
+  char* ex_own = nullptr;
+  ExLayout ex_layout;
   size_t part_floats = 0;  // capacity of the wgrad partial buffer (floats)
   size_t bpart_floats = 0; // capacity of the bias / head partial buffer (floats)
   int loss_parts = 0;      // loss partials per image
@@ -248,6 +262,16 @@ constexpr int kLossChunks = 32;
 cudaError_t launch_loss_finalize(const float* loss_part, int parts, const int* nlab, int n, float* loss, float* tmp,
                                  unsigned* cnt, cudaStream_t s);
 cudaError_t launch_sgd(float* params, float* grads, long long n, float lr, float scale, cudaStream_t s);
+
+// peer-memory gradient exchange (exchange.cu)
+ExLayout exchange_layout(int world, int nbmax, long long n_params);
+// copy grads[off, off+count) into this rank's slot (parity of the coming epoch) of every
+// rank's buffer, then raise flag (rank, bucket) = epoch in every buffer
+cudaError_t launch_exchange_push(const float* grads, long long off, long long count, char* own, const ExLayout& L,
+                                 int rank, int bucket, cudaStream_t s);
+// wait for every rank's flags 0 .. nb-1, theta -= lr*scale*sum_r slot[r] (rank order), g = 0, epoch++
+cudaError_t launch_exchange_sgd(float* params, float* grads, float lr, float scale, char* own, const ExLayout& L,
+                                int nb, cudaStream_t s);
 cudaError_t launch_pack_weights(const float* w_canon, int cout, int cin, int k, float* wpack, float* dpack,
                                 int round_fwd, int round_dgrad, cudaStream_t s);
 cudaError_t launch_frag2pix(const float* frag, float* pix, int n, int C, int F, int fr, int fc, int O_H,

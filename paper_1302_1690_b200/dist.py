@@ -4,11 +4,14 @@ Images are independent units: rank r of N takes the contiguous slice
 [r*B/N, (r+1)*B/N) of every global batch of B images and generates its own images
 from per-image seeds, so no input crosses ranks.  The only exchange is the sum of
 the flat fp32 gradient (Alg. 2's sum over fragments, extended
-over images and ranks), one ``all_reduce(SUM)`` per SGD step on a tensor that
-aliases the bound gradient buffer; every rank then applies the same
-``mpf_sgd_step(lr, 1/B)``.  No compute step is followed by a
-collective inside a kernel here: the exchange is one 0.3-2.2 MB message per
->= 30 ms step, so NCCL over NVLink is the right tool.
+over images and ranks).  Two exchanges implement it:
+- PeerExchange (default in bench.py): the library's backward pushes every gradient bucket
+  into every rank's exchange buffer over NVLink P2P as soon as it is final, and the SGD
+  kernel sums the ranks' slots (rank order) before applying the same
+  ``theta -= lr/B * g`` — the collective fused into the backward's tail and
+  the optimizer;
+- BucketAllReduce / allreduce_grads: NCCL ``all_reduce(SUM)`` per bucket on a tensor that
+  aliases the bound gradient buffer, then ``mpf_sgd_step(lr, 1/B)`` (the baseline).
 """
 from __future__ import annotations
 
@@ -81,6 +84,79 @@ class BucketAllReduce:
         for w in self.works:
             w.wait()
         self.works.clear()
+
+
+def peer_table(records, rank: int, world: int):
+    """Validate the all-gathered exchange records [(rank, handle bytes, offset, bytes), ...] of
+    PeerExchange: one per rank, in rank order, equal buffer sizes.  Returns them sorted."""
+    recs = sorted(records, key=lambda r: r[0])
+    if [r[0] for r in recs] != list(range(world)):
+        raise RuntimeError(f"exchange records do not cover ranks 0..{world - 1}: {[r[0] for r in records]}")
+    sizes = {r[3] for r in recs}
+    if len(sizes) != 1:
+        raise RuntimeError(f"ranks disagree on the exchange buffer size: {sorted(sizes)}")
+    if not 0 <= rank < world:
+        raise ValueError("bad rank")
+    return recs
+
+
+class PeerExchange:
+    """Peer-memory gradient exchange for `net` across the ranks of `group` (include/mpf.h
+    mpf_exchange_*): allocates this rank's zero-filled exchange buffer, exports it through CUDA
+    IPC, all-gathers the handles (a collective, so no rank attaches before every buffer is
+    zeroed), maps the peers' buffers and attaches.  From then on the backward pushes every
+    gradient bucket into every rank's buffer as it completes and net.sgd_step sums the ranks'
+    slots inside the SGD kernel — no separate all-reduce.  The arithmetic (Alg. 2's sum
+    extended over ranks) is all in the library's kernels; this class only
+    moves handles."""
+
+    def __init__(self, net, group=None, push_in_backward: bool = True):
+        import ctypes
+        import torch
+        import torch.distributed as dist
+        from . import _lib as L
+        self.net, self.lib = net, L.lib()
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        nbytes = net.exchange_bytes(self.world)
+        raw = torch.zeros(nbytes + 256, dtype=torch.uint8, device=net.device)
+        shift = (-raw.data_ptr()) % 256
+        self._raw, self.buf = raw, raw[shift:shift + nbytes]
+        torch.cuda.synchronize(net.device)  # zero-filled before any peer can see it
+        handle = (ctypes.c_char * 64)()
+        off = ctypes.c_uint64()
+        L.check(self.lib.mpf_ipc_export(ctypes.c_void_p(self.buf.data_ptr()), handle, ctypes.byref(off)),
+                "mpf_ipc_export")
+        recs = [None] * self.world
+        dist.all_gather_object(recs, (self.rank, bytes(handle), int(off.value), nbytes), group=group)
+        recs = peer_table(recs, self.rank, self.world)
+        self.opened = []
+        ptrs = []
+        for r, h, o, _ in recs:
+            if r == self.rank:
+                ptrs.append(self.buf.data_ptr())
+                continue
+            p = ctypes.c_void_p()
+            hb = (ctypes.c_char * 64).from_buffer_copy(h)
+            L.check(self.lib.mpf_ipc_open(hb, ctypes.c_uint64(o), ctypes.byref(p)), "mpf_ipc_open")
+            self.opened.append((p.value, o))
+            ptrs.append(p.value)
+        net.attach_exchange(self.rank, self.world, ptrs, push_in_backward)
+        self.group = group
+
+    def close(self) -> None:
+        """Detach and unmap (collective: waits until every rank is done with every buffer)."""
+        import ctypes
+        import torch
+        import torch.distributed as dist
+        from . import _lib as L
+        torch.cuda.synchronize(self.net.device)
+        dist.barrier(group=self.group)
+        self.net.detach_exchange()
+        for p, o in self.opened:
+            L.check(self.lib.mpf_ipc_close(ctypes.c_void_p(p), ctypes.c_uint64(o)), "mpf_ipc_close")
+        self.opened = []
+        dist.barrier(group=self.group)
 
 
 def max_over_ranks(value: float, device=None) -> float:

@@ -293,6 +293,26 @@ class MPFNet:
     def check(self, stream=None) -> None:
         L.check(self.lib.mpf_check(self.h, _stream_ptr(stream)), "mpf_check")
 
+    # ---- data-parallel gradient exchange over peer memory (include/mpf.h mpf_exchange_*;
+    # dist.PeerExchange sets it up across processes)
+    def exchange_bytes(self, world: int) -> int:
+        b = ctypes.c_uint64()
+        L.check(self.lib.mpf_exchange_bytes(self.h, int(world), ctypes.byref(b)), "mpf_exchange_bytes")
+        return int(b.value)
+
+    def attach_exchange(self, rank: int, world: int, buf_ptrs, push_in_backward: bool = True) -> None:
+        """buf_ptrs[r]: device address of rank r's zero-filled exchange buffer as seen from
+        this process (buf_ptrs[rank] = this rank's own buffer)."""
+        arr = (ctypes.c_void_p * world)(*[int(p) for p in buf_ptrs])
+        L.check(self.lib.mpf_exchange_attach(self.h, int(rank), int(world), arr, 1 if push_in_backward else 0),
+                "mpf_exchange_attach")
+
+    def exchange_push(self, stream=None) -> None:
+        L.check(self.lib.mpf_exchange_push(self.h, _stream_ptr(stream)), "mpf_exchange_push")
+
+    def detach_exchange(self) -> None:
+        L.check(self.lib.mpf_exchange_detach(self.h), "mpf_exchange_detach")
+
 
 class Lbfgs:
     """Full-batch L-BFGS on an MPFNet's parameters (mpf_lbfgs_*, reading R21).

@@ -30,11 +30,14 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("workload", ["cfg2", "cfg5"])
-def test_torchrun_world1_nccl_path(workload):
+@pytest.mark.parametrize("workload,exchange", [("cfg2", "nccl"), ("cfg5", "nccl"), ("cfg2", "peer"), ("cfg5", "peer")])
+def test_torchrun_world1_nccl_path(workload, exchange):
+    """Both gradient exchanges of the multi-rank path: peer memory (dist.PeerExchange: CUDA IPC
+    export, handle all-gather, pushes in the backward, sum in the SGD kernel; the default) and
+    the bucketed NCCL all-reduce."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "1",
-           "--steps", "3", "--warmup", "3", "--workload", workload, "--no-cpu-baseline"]
+           "--steps", "3", "--warmup", "3", "--workload", workload, "--no-cpu-baseline", "--exchange", exchange]
     env = dict(os.environ, NCCL_DEBUG="WARN")
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
@@ -44,6 +47,7 @@ def test_torchrun_world1_nccl_path(workload):
     print(workload, "torchrun world 1:", {k: line[k] for k in ("value", "ms_per_step", "gpu_launches")},
           line["config"].get("cuda_graph"), r.stderr[-500:])
     assert line["n_gpus"] == 1 and line["config"]["parallelism"] == "dp1" and line["value"] > 0
+    assert line["config"]["grad_exchange"] == exchange
     assert line["e2e"]["value"] > 0
 
 

@@ -249,3 +249,28 @@ def test_gloo_world2_bucketed_allreduce_equals_flat(tmp_path):
     for r in range(2):
         g, full = np.load(tmp_path / f"b{r}.npy")
         assert np.array_equal(g, full)
+
+
+def _peer_table_worker(rank, world, port, out):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    recs = [None] * world
+    # what PeerExchange all-gathers: (rank, 64-byte IPC handle, offset, buffer bytes)
+    dist.all_gather_object(recs, (rank, bytes([rank]) * 64, 256 * rank, 4096))
+    table = D.peer_table(recs, rank, world)
+    np.save(os.path.join(out, f"t{rank}.npy"), np.array([[r, h[0], o, b] for r, h, o, b in table]))
+    dist.destroy_process_group()
+
+
+def test_peer_exchange_records_world2(tmp_path):
+    """The host half of PeerExchange: every rank ends with the same rank-ordered
+    table of buffer handles, and inconsistent records are rejected."""
+    import torch.multiprocessing as mp
+    mp.start_processes(_peer_table_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, start_method="spawn")
+    t0, t1 = np.load(tmp_path / "t0.npy"), np.load(tmp_path / "t1.npy")
+    assert np.array_equal(t0, t1) and t0[:, 0].tolist() == [0, 1] and t0[:, 2].tolist() == [0, 256]
+    with pytest.raises(RuntimeError):
+        D.peer_table([(0, b"", 0, 1), (0, b"", 0, 1)], 0, 2)
+    with pytest.raises(RuntimeError):
+        D.peer_table([(0, b"", 0, 1), (1, b"", 0, 2)], 0, 2)
