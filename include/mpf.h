@@ -107,9 +107,10 @@ typedef struct {
  *   HEAD_LOGITS_ON   in the epilogue whenever the last hidden layer runs on the tensor cores.
  *   MPF_BWD_BLOCK  the k = 2 MPF backward as one 2 x 2 block per work item instead of bands of
  *               block rows (bitwise the same deltas).
- *   MPF_BWD_GATHER the k = 3 MPF backward as the register-blocked gather (each element tests its
- *               k^2 candidate windows) instead of the shared-memory scatter (each window adds
- *               its delta to its argmax element); the same sums in another fp32 order.
+ *   MPF_BWD_SCATTER the k = 3 MPF backward as a shared-memory scatter (each window adds its
+ *               delta to its argmax element) instead of the register-blocked gather (each
+ *               element tests its k^2 candidate windows); the same sums in another fp32
+ *               order.  Faster alone, slower in the overlapped step.
  */
 enum {
   MPF_FLAG_SERIAL = 1u << 0,
@@ -124,7 +125,7 @@ enum {
   MPF_FLAG_HEAD_LOGITS_OFF = 1u << 9,
   MPF_FLAG_HEAD_LOGITS_ON = 1u << 10,
   MPF_FLAG_MPF_BWD_BLOCK = 1u << 11,
-  MPF_FLAG_MPF_BWD_GATHER = 1u << 12
+  MPF_FLAG_MPF_BWD_SCATTER = 1u << 12
 };
 
 /* Geometry of the padded uniform-fragment layout.

@@ -30,7 +30,7 @@ MPF_FLAG_FUSE_FIRST_POOL = 1 << 8
 MPF_FLAG_HEAD_LOGITS_OFF = 1 << 9
 MPF_FLAG_HEAD_LOGITS_ON = 1 << 10
 MPF_FLAG_MPF_BWD_BLOCK = 1 << 11
-MPF_FLAG_MPF_BWD_GATHER = 1 << 12
+MPF_FLAG_MPF_BWD_SCATTER = 1 << 12
 
 # every symbol include/mpf.h declares
 EXPORTS = ("mpf_version", "mpf_last_error", "mpf_net_create", "mpf_net_destroy", "mpf_net_geometry",

@@ -250,7 +250,7 @@ static void layout_memory(Net* N, int n) {
           for (int gf = 0; gf <= 1; ++gf) {
             m.premul = pm;
             m.block_form = bf;
-            m.gather_form = gf;
+            m.scatter_form = gf;
             bp = std::max(bp, (size_t)mpf_bwd_partials(m) * in.C);
           }
     } else {
@@ -846,7 +846,7 @@ static mpf_status backward_impl(Net* N, const uint8_t* d_labels, const float* h_
       m.bias_part = bpart;
       m.premul = premul ? 1 : 0;
       m.block_form = (N->cfg.flags & MPF_FLAG_MPF_BWD_BLOCK) ? 1 : 0;
-      m.gather_form = (N->cfg.flags & MPF_FLAG_MPF_BWD_GATHER) ? 1 : 0;
+      m.scatter_form = (N->cfg.flags & MPF_FLAG_MPF_BWD_SCATTER) ? 1 : 0;
       premul = false;
       const double ein = (double)n * in.F * in.vr * in.vc * in.C, eout = (double)n * o.F * o.vr * o.vc * o.C;
       LAUNCH(N, s, "mpf_bwd", l, 0.0, (m.premul ? 5.0 : 9.0) * eout + 4.0 * ein, launch_mpf_bwd(m, s));
@@ -1510,7 +1510,7 @@ mpf_status mpf_net_set_flags(mpf_net* N, uint32_t flags) {
   const uint32_t known = MPF_FLAG_SERIAL | MPF_FLAG_TC_SINGLE | MPF_FLAG_TC_PAIR | MPF_FLAG_NTAP_ON | MPF_FLAG_NTAP_OFF |
                          MPF_FLAG_NTAP_NO_MC | MPF_FLAG_WGRAD_M128 | MPF_FLAG_ROLE_TIMERS | MPF_FLAG_FUSE_FIRST_POOL |
                          MPF_FLAG_HEAD_LOGITS_OFF | MPF_FLAG_HEAD_LOGITS_ON | MPF_FLAG_MPF_BWD_BLOCK |
-                         MPF_FLAG_MPF_BWD_GATHER;
+                         MPF_FLAG_MPF_BWD_SCATTER;
   if (flags & ~known) return fail(MPF_ERR_ARG, "unknown MPF_FLAG_* bits");
   if ((flags & MPF_FLAG_NTAP_ON) && (flags & MPF_FLAG_NTAP_OFF)) return fail(MPF_ERR_ARG, "NTAP_ON with NTAP_OFF");
   if ((flags & MPF_FLAG_TC_PAIR) && (flags & MPF_FLAG_TC_SINGLE)) return fail(MPF_ERR_ARG, "TC_PAIR with TC_SINGLE");

@@ -187,7 +187,7 @@ struct MpfBwdArgs {
   float* bias_part;      // nullable: [mpf_bwd_partials(a)][C] per-block sums of din (bias gradient)
   int premul;            // 1: dout already carries act'(y) (the producing dgrad applied it); pooled unused
   int block_form;        // k = 2: one 2 x 2 block per work item instead of a band (MPF_FLAG_MPF_BWD_BLOCK)
-  int gather_form;       // k = 3: the register-blocked gather instead of the scatter (MPF_FLAG_MPF_BWD_GATHER)
+  int scatter_form;      // k = 3: the shared-memory scatter instead of the gather (MPF_FLAG_MPF_BWD_SCATTER)
 };
 cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s);
 long long mpf_bwd_partials(const MpfBwdArgs& a);

@@ -800,15 +800,21 @@ struct ScatterGeo {
 };
 constexpr int kScatterRing = 8;  // accumulator ring rows (a power of two >= 2k - 1)
 
-template <int K>
-__global__ void __launch_bounds__(1024) mpf_bwd_scatter_kernel(MpfBwdArgs a, ScatterGeo s) {
+#ifndef MPF_SCATTER_MAXT
+#define MPF_SCATTER_MAXT 1024
+#endif
+template <int K, int CS>
+__global__ void __launch_bounds__(MPF_SCATTER_MAXT, 1024 / MPF_SCATTER_MAXT) mpf_bwd_scatter_kernel(MpfBwdArgs a, ScatterGeo s) {
   // ring of kRing accumulator rows (slot = row mod kRing; rows kB .. kB+2k-2 of one block row
   // are distinct slots), each K*NBX + 2K - 1 columns: K columns left of the tile and K - 1
   // right of it catch the halo blocks' out-of-tile targets (never written out)
   extern __shared__ __align__(16) float acc[];
   constexpr int HL = K, kRing = kScatterRing;
   static_assert(2 * K - 1 <= kRing && (kRing & (kRing - 1)) == 0, "ring too small");
-  const int CS = s.CS, T = s.T, tid = threadIdx.x;  // blockDim.x == T, a multiple of CS
+  // byte offset of the target of a window with argmax q, relative to its block's column in
+  // ring row K*B + u: tab[B mod 8][u][q] (K*B mod 8 depends on B mod 8 only)
+  __shared__ int tab[8 * K * K * K];
+  const int T = s.T, tid = threadIdx.x;  // blockDim.x == T, a multiple of CS
   const int C = a.C;
   int u_ = blockIdx.x;
   const int cs = u_ % s.n_cs; u_ /= s.n_cs;
@@ -817,6 +823,10 @@ __global__ void __launch_bounds__(1024) mpf_bwd_scatter_kernel(MpfBwdArgs a, Sca
   const int g = u_ / s.n_bb;
   const int ch = tid % CS, sub = tid / CS, nsub = T / CS;
   const int TXo = K * s.NBX, RW = TXo + 2 * K - 1, ROW = RW * CS;  // ring row pitch (floats)
+  for (int i = tid; i < 8 * K * K * K; i += T) {
+    const int bm = i / (K * K * K), u = (i / (K * K)) % K, q = i % (K * K);
+    tab[i] = (((K * bm + u + q / K) & (kRing - 1)) * ROW + (q % K) * CS) * (int)sizeof(float);
+  }
   const int X0 = TXo * cx, X1 = min(a.gc, X0 + TXo);
   const int Y0 = K * s.BR * bb, Y1 = min(a.gr, Y0 + K * s.BR);
   // block (B, bx) has all its k x k windows iff B < m_r and bx < m_c
@@ -845,18 +855,19 @@ __global__ void __launch_bounds__(1024) mpf_bwd_scatter_kernel(MpfBwdArgs a, Sca
       }
   };
   auto scatter = [&](int B, int bx, const uint32_t (&id)[K][K], const float (&d)[K][K]) {
-    float* base = acc + (K * bx - X0 + HL) * CS + ch;
+    char* base = reinterpret_cast<char*>(acc + (K * bx - X0 + HL) * CS + ch);
+    const int* tb = tab + (B & 7) * K * K * K;
 #pragma unroll
     for (int u = 0; u < K; ++u)
 #pragma unroll
       for (int v = 0; v < K; ++v) {
-        const int q = (int)id[u][v];
-        const int dy = q / K, dx = q - K * dy;
-        base[((K * B + u + dy) & (kRing - 1)) * ROW + (v + dx) * CS] += d[u][v];
+        float* e = reinterpret_cast<float*>(base + tb[u * K * K + (int)id[u][v]]) + v * CS;
+        *e += d[u][v];
       }
   };
   // write-out mapping: 4-channel vectors, thread (column lane, vector) with a fixed vector
-  const int CV = CS / 4, vq = tid % CV, csub = tid / CV, ncsub = T / CV;
+  constexpr int CV = CS / 4;
+  const int vq = tid % CV, csub = tid / CV, ncsub = T / CV;
   float bsum[4] = {0.f, 0.f, 0.f, 0.f};
   const int W = X1 - X0;
   float* dst = a.din + ((size_t)g * a.gr * a.gc + X0) * C + cs * CS + vq * 4;
@@ -1117,25 +1128,26 @@ static void bwd_geometry(const MpfBwdArgs& a, int V, dim3* grid, dim3* blk) {
   *grid = dim3((a.gc + ty - 1) / ty, (a.gr + band - 1) / band, a.n_frag_in < 65535 ? a.n_frag_in : 65535);
 }
 
-// k = 3 (premul, C % 4 == 0 or C <= 32): the scatter; MPF_FLAG_MPF_BWD_GATHER keeps the gather
+// k = 3 (premul, C a multiple of 16, 24 or 32) under MPF_FLAG_MPF_BWD_SCATTER: the scatter
 static bool scatter_geo(const MpfBwdArgs& a, ScatterGeo* s) {
-  if (!(a.k == 3 && a.premul && !a.gather_form)) return false;
+  if (!(a.k == 3 && a.premul && a.scatter_form)) return false;
   const int K = a.k, C = a.C;
-  if (C % 4) return false;  // 4-channel write-out vectors
-  int CS = C;
-  if (C > 32) {
-    if (C % 32 == 0) CS = 32;
-    else if (C % 24 == 0) CS = 24;
-    else if (C % 16 == 0) CS = 16;
-    else return false;
-  }
+  // channel slice: 32, 24 or 16 channels (compile-time in the kernel)
+  int CS = 0;
+  if (C % 32 == 0) CS = 32;
+  else if (C % 24 == 0) CS = 24;
+  else if (C % 16 == 0) CS = 16;
+  else return false;
   s->CS = CS;
   s->n_cs = C / CS;
   // widest tile of NBX blocks whose ring fits ~64 KB (three CTAs per SM) within 1024 threads
-  const size_t budget = 64 * 1024 + 512;
+#ifndef MPF_SCATTER_BUDGET_KB
+#define MPF_SCATTER_BUDGET_KB 32
+#endif
+  const size_t budget = MPF_SCATTER_BUDGET_KB * 1024 + 512;
   int nbx_max = (int)((budget / ((size_t)kScatterRing * CS * sizeof(float)) - (2 * K - 1)) / K);
-  while (nbx_max > 1 && (nbx_max / 2 + 1) * CS > 1024) --nbx_max;
-  if (nbx_max < 1 || (nbx_max / 2 + 1) * CS > 1024) return false;
+  while (nbx_max > 1 && (nbx_max / 2 + 1) * CS > MPF_SCATTER_MAXT) --nbx_max;
+  if (nbx_max < 1 || (nbx_max / 2 + 1) * CS > MPF_SCATTER_MAXT) return false;
   const int blk_cols = (a.gc + K - 1) / K, blk_rows = (a.gr + K - 1) / K;
   s->n_cx = (blk_cols + nbx_max - 1) / nbx_max;
   s->NBX = (blk_cols + s->n_cx - 1) / s->n_cx;
@@ -1164,10 +1176,11 @@ cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s) {
   ScatterGeo sg;
   if (scatter_geo(a, &sg)) {
     if (sg.units * sg.n_cs > 0x7fffffffLL) return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(mpf_bwd_scatter_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sg.smem);
+    auto kern = sg.CS == 32 ? mpf_bwd_scatter_kernel<3, 32>
+                : sg.CS == 24 ? mpf_bwd_scatter_kernel<3, 24> : mpf_bwd_scatter_kernel<3, 16>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg.smem);
     if (e != cudaSuccess) return e;
-    mpf_bwd_scatter_kernel<3><<<(unsigned)(sg.units * sg.n_cs), sg.T, sg.smem, s>>>(a, sg);
+    kern<<<(unsigned)(sg.units * sg.n_cs), sg.T, sg.smem, s>>>(a, sg);
     return cudaGetLastError();
   }
   if (bwd_block2(a)) {

@@ -488,15 +488,15 @@ def test_mpf_bwd_band_matches_blocks(name):
 
 @pytest.mark.parametrize("prec", ["tf32", "fp32"])
 def test_mpf_bwd_k3_scatter_matches_gather(prec):
-    """k = 3 MPF backward (Alg. 4): the shared-memory scatter (default; every
-    window adds its delta to its argmax element) and the register-blocked gather
-    (MPF_FLAG_MPF_BWD_GATHER; every element tests its 9 candidate windows) add the same deltas
-    in different fixed orders: the forward is untouched, the gradients agree to fp32 rounding,
-    and each form is bitwise reproducible run to run."""
+    """k = 3 MPF backward (Alg. 4): the shared-memory scatter
+    (MPF_FLAG_MPF_BWD_SCATTER; every window adds its delta to its argmax element) and the
+    register-blocked gather (default; every element tests its 9 candidate windows) add the
+    same deltas in different fixed orders: the forward is untouched, the gradients agree to
+    fp32 rounding, and each form is bitwise reproducible run to run."""
     from paper_1302_1690_b200 import _lib as L
-    cfg, a = _run_variant(0, name="cfg5s", prec=prec)
-    _, a2 = _run_variant(0, name="cfg5s", prec=prec)
-    _, b = _run_variant(L.MPF_FLAG_MPF_BWD_GATHER, name="cfg5s", prec=prec)
+    cfg, a = _run_variant(L.MPF_FLAG_MPF_BWD_SCATTER, name="cfg5s", prec=prec)
+    _, a2 = _run_variant(L.MPF_FLAG_MPF_BWD_SCATTER, name="cfg5s", prec=prec)
+    _, b = _run_variant(0, name="cfg5s", prec=prec)
     assert np.array_equal(a["probs"], b["probs"]) and np.array_equal(a["loss"], b["loss"])
     assert np.array_equal(a["grad_sum"], a2["grad_sum"])
     for nm, sl in param_slices(cfg.layers):
