@@ -295,6 +295,24 @@ mpf_status mpf_lbfgs_step(mpf_lbfgs* lb, const float* d_images, int32_t n, const
                           float grad_scale, float* h_out, void* stream);
 
 /*
+ * The backtracking rule of the L-BFGS line search (reading
+ * R21), as mpf_lbfgs_step applies it, for a caller that evaluates the (e.g. rank-summed) loss
+ * itself and drives the mpf_lbfgs_* primitives (paper_1302_1690_b200.dist.lbfgs_iteration).
+ * Host-only (no device, no state).
+ * mpf_line_search_first: *alpha = alpha0 when no curvature pair is stored (n_pairs == 0),
+ *   else 1 (the quasi-Newton step).
+ * mpf_line_search_decide: after trial number trials_done (1-based) at step alpha gave loss
+ *   L_trial: *decision = 1 (accept: L_trial finite and L_trial <= L0 + c * alpha * gtd),
+ *   0 (try *alpha_next = beta * alpha) or -1 (max_backtracks + 1 trials failed: restore the
+ *   start point).  MPF_ERR_ARG for parameters outside 0 < beta < 1, 0 < c < 1,
+ *   max_backtracks >= 0, trials_done >= 1, or NULL outputs.
+ */
+mpf_status mpf_line_search_first(double alpha0, int32_t n_pairs, double* alpha);
+mpf_status mpf_line_search_decide(double L0, double gtd, double c, double beta, double alpha, double L_trial,
+                                  int32_t trials_done, int32_t max_backtracks, int32_t* decision,
+                                  double* alpha_next);
+
+/*
  * Gradient-ready hook for data-parallel training (Alg. 2's sum extended over ranks): when
  * set, mpf_backward_image / mpf_train_step call fn(user, layer, offset, count, stream) on
  * the calling host thread right after they have enqueued the weight gradient of conv/FC

@@ -41,7 +41,8 @@ EXPORTS = ("mpf_version", "mpf_last_error", "mpf_net_create", "mpf_net_destroy",
            "mpf_lbfgs_trial", "mpf_lbfgs_accept", "mpf_lbfgs_reject", "mpf_lbfgs_step",
            "mpf_debug_tape", "mpf_check", "mpf_profile_begin",
            "mpf_profile_end", "mpf_exchange_bytes", "mpf_exchange_attach", "mpf_exchange_push",
-           "mpf_exchange_sgd_step", "mpf_exchange_detach", "mpf_ipc_export", "mpf_ipc_open", "mpf_ipc_close")
+           "mpf_exchange_sgd_step", "mpf_exchange_detach", "mpf_ipc_export", "mpf_ipc_open", "mpf_ipc_close",
+           "mpf_line_search_first", "mpf_line_search_decide")
 
 
 # void (*mpf_grad_ready_fn)(void* user, int32_t layer, int64_t offset, int64_t count, void* stream)
@@ -168,6 +169,11 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.mpf_ipc_open.argtypes = [vp, ctypes.c_uint64, ctypes.POINTER(vp)]
     lib.mpf_ipc_close.restype = st
     lib.mpf_ipc_close.argtypes = [vp, ctypes.c_uint64]
+    dbl, dblp = ctypes.c_double, ctypes.POINTER(ctypes.c_double)
+    lib.mpf_line_search_first.restype = st
+    lib.mpf_line_search_first.argtypes = [dbl, i32, dblp]
+    lib.mpf_line_search_decide.restype = st
+    lib.mpf_line_search_decide.argtypes = [dbl, dbl, dbl, dbl, dbl, dbl, i32, i32, ctypes.POINTER(i32), dblp]
     return lib
 
 

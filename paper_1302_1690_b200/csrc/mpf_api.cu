@@ -1234,6 +1234,28 @@ mpf_status mpf_lbfgs_reject(mpf_lbfgs* lb, void* stream) {
   return MPF_OK;
 }
 
+mpf_status mpf_line_search_first(double alpha0, int32_t n_pairs, double* alpha) {
+  if (!alpha) return fail(MPF_ERR_ARG, "NULL argument");
+  *alpha = n_pairs == 0 ? alpha0 : 1.0;
+  return MPF_OK;
+}
+
+mpf_status mpf_line_search_decide(double L0, double gtd, double c, double beta, double alpha, double L_trial,
+                                  int32_t trials_done, int32_t max_backtracks, int32_t* decision,
+                                  double* alpha_next) {
+  if (!decision || !alpha_next) return fail(MPF_ERR_ARG, "NULL argument");
+  if (!(beta > 0.0 && beta < 1.0) || !(c > 0.0 && c < 1.0) || max_backtracks < 0 || trials_done < 1)
+    return fail(MPF_ERR_ARG, "line search: 0 < beta < 1, 0 < c < 1, max_backtracks >= 0, trials_done >= 1");
+  *alpha_next = alpha;
+  if (std::isfinite(L_trial) && L_trial <= L0 + c * alpha * gtd) *decision = 1;  // Armijo: sufficient decrease
+  else if (trials_done > max_backtracks) *decision = -1;
+  else {
+    *decision = 0;
+    *alpha_next = beta * alpha;
+  }
+  return MPF_OK;
+}
+
 mpf_status mpf_lbfgs_step(mpf_lbfgs* lb, const float* d_images, int32_t n, const uint8_t* d_labels,
                           const float* h_class_w, float alpha0, float beta, float c, int32_t max_backtracks,
                           float grad_scale, float* h_out, void* stream) {
@@ -1277,19 +1299,25 @@ mpf_status mpf_lbfgs_step(mpf_lbfgs* lb, const float* d_images, int32_t n, const
     lb->have_g = lb->have_dir = lb->have_L = false;
     return fail(MPF_ERR_DATA, "L-BFGS: non-finite loss or direction");
   }
-  double alpha = lb->order.empty() ? (double)alpha0 : 1.0, L = L0;
+  double alpha = 0.0, L = L0;
+  mpf_line_search_first(alpha0, (int32_t)lb->order.size(), &alpha);
   int evals = 0;
   bool accepted = false;
-  for (int it = 0; it <= max_backtracks; ++it, alpha *= beta) {
+  for (;;) {
     st = mpf_lbfgs_trial(lb, alpha, stream);
     if (st != MPF_OK) return st;
     st = evaluate(&L);
     if (st != MPF_OK) return st;
     ++evals;
-    if (std::isfinite(L) && L <= L0 + (double)c * alpha * gtd) {
-      accepted = true;
+    int32_t decision = 0;
+    double next = 0.0;
+    st = mpf_line_search_decide(L0, gtd, c, beta, alpha, L, evals, max_backtracks, &decision, &next);
+    if (st != MPF_OK) return st;
+    if (decision != 0) {
+      accepted = decision == 1;
       break;
     }
+    alpha = next;
   }
   if (accepted) {
     st = mpf_lbfgs_accept(lb, grad_scale, nullptr, stream);

@@ -189,7 +189,12 @@ def lbfgs_iteration(ops, alpha0: float, beta: float, c: float, max_backtracks: i
 
     ops: .have_g, .L, .n_pairs, evaluate() -> L, set_gradient(), direction() -> (gtd, fallback),
          trial(alpha), accept() -> stored (bool), reject().
+    The first step length and every accept / backtrack decision come from the library
+    (mpf_line_search_first / mpf_line_search_decide: the rule mpf_lbfgs_step applies).
     """
+    import ctypes
+    from . import _lib as Lb
+    lib = Lb.lib()
     if not ops.have_g:
         ops.L = ops.evaluate()
         ops.set_gradient()
@@ -197,16 +202,22 @@ def lbfgs_iteration(ops, alpha0: float, beta: float, c: float, max_backtracks: i
     gtd, fallback = ops.direction()
     if not (np.isfinite(L0) and np.isfinite(gtd)):
         raise FloatingPointError("L-BFGS: non-finite loss or direction")
-    alpha = alpha0 if ops.n_pairs == 0 else 1.0
+    a = ctypes.c_double()
+    Lb.check(lib.mpf_line_search_first(float(alpha0), int(ops.n_pairs), ctypes.byref(a)), "mpf_line_search_first")
+    alpha = a.value
     L, evals, accepted = L0, 0, False
-    for _ in range(max_backtracks + 1):
+    decision, nxt = ctypes.c_int32(), ctypes.c_double()
+    while True:
         ops.trial(alpha)
         L = ops.evaluate()
         evals += 1
-        if np.isfinite(L) and L <= L0 + c * alpha * gtd:
-            accepted = True
+        Lb.check(lib.mpf_line_search_decide(float(L0), float(gtd), float(c), float(beta), float(alpha), float(L),
+                                            evals, int(max_backtracks), ctypes.byref(decision), ctypes.byref(nxt)),
+                 "mpf_line_search_decide")
+        if decision.value != 0:
+            accepted = decision.value == 1
             break
-        alpha *= beta
+        alpha = nxt.value
     if accepted:
         ops.accept()
         ops.L = L

@@ -139,3 +139,27 @@ def test_kernel_selection_flags_are_validated():
     assert lib.mpf_net_set_flags(h, 1 << 30) == L.MPF_ERR_ARG
     assert lib.mpf_net_set_flags(h, 0) == L.MPF_OK
     lib.mpf_net_destroy(h)
+
+
+def test_line_search_rule_host_only():
+    """mpf_line_search_first / _decide (the backtracking rule of mpf_lbfgs_step, PAPER.md:251,
+    reading R21) on the host: Armijo acceptance L <= L0 + c alpha g'd, backtracking by beta,
+    giving up after max_backtracks + 1 trials, non-finite losses never accepted."""
+    lib = L.lib()
+    a = ctypes.c_double()
+    assert lib.mpf_line_search_first(0.25, 0, ctypes.byref(a)) == 0 and a.value == 0.25
+    assert lib.mpf_line_search_first(0.25, 3, ctypes.byref(a)) == 0 and a.value == 1.0
+
+    def decide(L0, gtd, alpha, Lt, trials, maxb=2, c=0.1, beta=0.5):
+        d, n = ctypes.c_int32(), ctypes.c_double()
+        st = lib.mpf_line_search_decide(L0, gtd, c, beta, alpha, Lt, trials, maxb, ctypes.byref(d), ctypes.byref(n))
+        return st, d.value, n.value
+    # L0 = 1, g'd = -2, alpha = 1, c = 0.1: threshold 0.8
+    assert decide(1.0, -2.0, 1.0, 0.8, 1) == (0, 1, 1.0)       # equality accepts
+    assert decide(1.0, -2.0, 1.0, 0.80001, 1) == (0, 0, 0.5)   # backtrack to beta * alpha
+    assert decide(1.0, -2.0, 0.25, 0.99, 3) == (0, -1, 0.25)   # third trial with max_backtracks 2: give up
+    assert decide(1.0, -2.0, 0.5, 0.95, 2)[1] == 0             # second trial: one more allowed
+    assert decide(1.0, -2.0, 1.0, float("nan"), 1)[1] == 0     # NaN never accepted
+    assert decide(1.0, -2.0, 1.0, float("-inf"), 1)[1] == 0    # nor -inf
+    assert decide(1.0, -2.0, 1.0, 0.5, 1, beta=1.0)[0] == L.MPF_ERR_ARG
+    assert decide(1.0, -2.0, 1.0, 0.5, 0)[0] == L.MPF_ERR_ARG
