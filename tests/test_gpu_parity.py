@@ -843,6 +843,51 @@ def test_bench_step_cfg4_full_images_vs_o2():
     assert not bad, bad
 
 
+def test_bench_step_cfg5_full_batch_vs_o2():
+    """The step bench.py times for cfg5 (BASELINE configs[4]: 8 images of 768^2, every output
+    pixel labelled, k = 3 pools, TF32 tensor cores, mpf_train_step then mpf_sgd_step(lr, 1/8))
+    on the bench's own first batch, against O2 on all 8 images ("cfg5 vs O2 on 8
+    fully labelled images"): per-image losses, every W/b gradient of the batch sum and the SGD
+    update within rel L2 5e-3 (R17), per-pixel outputs of images 0 and 7; argmax flips per pool
+    layer of image 0 reported (R16)."""
+    from tests.gpu_common import argmax_flips, o2_images_parallel
+    cfg = S.CONFIGS["cfg5"]
+    B = cfg.global_batch
+    images, labels = S.make_batch(cfg, list(range(B)))
+    assert np.all(labels != 255)
+    params = S.init_params(cfg)
+    net = MPFNet(cfg.layers, cfg.P, cfg.H, cfg.W, max_images=B)
+    net.set_params(params.astype(np.float32))
+    net.zero_grads()
+    img = torch.tensor(images, device="cuda").contiguous()
+    lab = torch.tensor(labels, device="cuda").contiguous()
+    loss = net.train_step(img, lab)
+    grads = net.grads.clone()
+    p0 = net.params.clone()
+    net.sgd_step(cfg.lr, 1.0 / B)
+    net.check()
+    o = o2_images_parallel(cfg.layers, params, images, labels, cfg.P, want_idx=(0,))
+    flips = argmax_flips(net, cfg.layers, o[0][4], B)
+    theta1 = net.params.cpu().numpy().astype(np.float64)
+    net.set_params(p0)
+    probs = net.fragments_to_pixels(net.forward(img, want_probs=True), B, cfg.classes).cpu().numpy()
+    torch.cuda.synchronize()
+    loss = loss.cpu().numpy()
+    grads = grads.cpu().numpy().astype(np.float64)
+    o_loss = np.array([r[0] / r[1] for r in o])
+    o_grad = sum(r[2] / r[1] for r in o)
+    errs = {"probs0": rel_l2(probs[0], o[0][3]), "probs7": rel_l2(probs[7], o[7][3]), "loss": rel_l2(loss, o_loss)}
+    for nm, sl in param_slices(cfg.layers):
+        errs["g" + nm] = rel_l2(grads[sl], o_grad[sl])
+    errs["sgd_update"] = rel_l2(theta1 - p0.cpu().numpy().astype(np.float64), -cfg.lr * o_grad / B)
+    print("cfg5 bench step vs O2 (8 fully labelled 768^2 images): rel L2",
+          {k: f"{v:.2e}" for k, v in errs.items()})
+    print("cfg5 argmax flips per pool layer (image 0, GPU TF32 vs O2 fp64):",
+          {l: f"{f}/{c} = {f / c:.2e}" for l, (f, c) in flips.items()})
+    bad = {k: v for k, v in errs.items() if not v <= TOL_TF32}
+    assert not bad, bad
+
+
 def _tie_images(rng, n, H, W, block=4):
     """Images of constant block x block tiles with values in {-1, 0, 1}: every window inside
     a tile sees the same inputs, so conv outputs repeat exactly and pooling blocks hold exact
