@@ -254,9 +254,12 @@ def main():
         okt = torch.tensor([1 if ok else 0], device=dev, dtype=torch.int32)
         dist.all_reduce(okt, op=dist.ReduceOp.MIN)
         if okt.item():
-            peer = D.PeerExchange(net)
-            exchange_kind = "peer"
-        else:
+            try:
+                peer = D.PeerExchange(net)
+                exchange_kind = "peer"
+            except RuntimeError as ex:  # every rank sees the same outcome (PeerExchange agrees)
+                print(f"[bench] peer-memory exchange unavailable ({ex}); NCCL all-reduce", file=sys.stderr)
+        if peer is None:
             buckets = D.BucketAllReduce(net.grads)
             net.set_grad_hook(buckets)
             exchange_kind = "nccl"
@@ -280,6 +283,14 @@ def main():
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize(dev)
+    net.check()  # device-side errors (labels, a gradient exchange that timed out) fail the run here
+    if use_dist:  # every rank must hold the same parameters after the exchanged SGD steps
+        cs = net.params.double().sum().reshape(1)
+        lo, hi = cs.clone(), cs.clone()
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+        dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+        if lo.item() != hi.item():
+            raise SystemExit(f"ranks disagree on the parameters after warm-up ({lo.item()} vs {hi.item()})")
     # One CUDA graph per input pool (the step's ~170 launches, its side-stream fork/join and
     # the bucketed NCCL all-reduces replayed as one launch); eager launches if capture fails.
     graphs = None
@@ -351,6 +362,7 @@ def main():
         dist.barrier()
     ms = e0.elapsed_time(e1)
     clocks = clk.stop()
+    net.check()
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
     if use_dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -125,24 +125,42 @@ class PeerExchange:
         torch.cuda.synchronize(net.device)  # zero-filled before any peer can see it
         handle = (ctypes.c_char * 64)()
         off = ctypes.c_uint64()
-        L.check(self.lib.mpf_ipc_export(ctypes.c_void_p(self.buf.data_ptr()), handle, ctypes.byref(off)),
-                "mpf_ipc_export")
+        err = ""
+        if self.lib.mpf_ipc_export(ctypes.c_void_p(self.buf.data_ptr()), handle, ctypes.byref(off)) != L.MPF_OK:
+            err = f"rank {self.rank}: mpf_ipc_export failed: " + self.lib.mpf_last_error().decode(errors="replace")
         recs = [None] * self.world
-        dist.all_gather_object(recs, (self.rank, bytes(handle), int(off.value), nbytes), group=group)
-        recs = peer_table(recs, self.rank, self.world)
+        dist.all_gather_object(recs, (self.rank, bytes(handle), int(off.value), nbytes, err), group=group)
+        bad = [r[4] for r in recs if r[4]]
+        if bad:  # every rank raises (no rank is left waiting in a collective)
+            raise RuntimeError("PeerExchange: " + "; ".join(bad))
+        recs = peer_table([r[:4] for r in recs], self.rank, self.world)
         self.opened = []
-        ptrs = []
+        self.group = group
+        ptrs, err = [], ""
         for r, h, o, _ in recs:
             if r == self.rank:
                 ptrs.append(self.buf.data_ptr())
                 continue
             p = ctypes.c_void_p()
             hb = (ctypes.c_char * 64).from_buffer_copy(h)
-            L.check(self.lib.mpf_ipc_open(hb, ctypes.c_uint64(o), ctypes.byref(p)), "mpf_ipc_open")
+            st = self.lib.mpf_ipc_open(hb, ctypes.c_uint64(o), ctypes.byref(p))
+            if st != L.MPF_OK:
+                err = f"rank {self.rank}: mpf_ipc_open of rank {r}'s buffer failed: " + \
+                    self.lib.mpf_last_error().decode(errors="replace")
+                break
             self.opened.append((p.value, o))
             ptrs.append(p.value)
+        # attach only if every rank mapped every buffer (else nobody attaches: the caller
+        # falls back to another exchange)
+        errs = [None] * self.world
+        dist.all_gather_object(errs, err, group=group)
+        bad = [e for e in errs if e]
+        if bad:
+            for p, o in self.opened:
+                self.lib.mpf_ipc_close(ctypes.c_void_p(p), ctypes.c_uint64(o))
+            self.opened = []
+            raise RuntimeError("PeerExchange: " + "; ".join(bad))
         net.attach_exchange(self.rank, self.world, ptrs, push_in_backward)
-        self.group = group
 
     def close(self) -> None:
         """Detach and unmap (collective: waits until every rank is done with every buffer)."""
