@@ -1340,6 +1340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 constexpr int kSwapMaxTiles = 16;
 struct WgSwapParams {
   int P_tot, gc, cin, cout, npad, k, n_cc, n_groups, n_tiles;
+  int g_lo;  // this pass's first (ky, channel chunk) group: its slabs are groups g_lo .. g_lo + n_groups - 1
   int chunk_stages;
   float* part;
   uint32_t a_bytes, b_bytes, stage_bytes;  // a = the dY tile, b = one X slab
@@ -1392,7 +1393,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t sa = sbase + slot * p.stage_bytes;
         const int row = (int)(pbeg + (long long)st * kWR);
         for (int g = 0; g < p.n_groups; ++g) {
-          const int ky = g / p.n_cc, cc = g % p.n_cc;
+          const int ky = (p.g_lo + g) / p.n_cc, cc = (p.g_lo + g) % p.n_cc;
           ptx::tma_load_2d(sa + g * p.b_bytes, &tmX, barFull + 8 * slot, cc * kKC, row + ky * p.gc);
         }
         for (int j = 0; j < n_datoms; ++j)
@@ -1431,7 +1432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int g = p.t_across[t] ? p.t_group[t] + q : p.t_group[t];
       const int kx = p.t_across[t] ? p.t_tap[t] : p.t_tap[t] + q;
       const bool atom_ok = g < p.n_groups && kx < p.k;  // warp-uniform
-      const int ky = atom_ok ? g / p.n_cc : 0, cc = atom_ok ? g % p.n_cc : 0;
+      const int ky = atom_ok ? (p.g_lo + g) / p.n_cc : 0, cc = atom_ok ? (p.g_lo + g) % p.n_cc : 0;
       const int ci = cc * kKC + lane;
       const bool ok = atom_ok && ci < p.cin;
       float* dst = p.part + (long long)split * p.cout * K + (ky * p.k + kx) * p.cin + (ok ? ci : 0);
@@ -1542,45 +1543,63 @@ static cudaError_t launch_wgrad_pair(const TcWgradArgs& a, int* splits_out, cuda
   return cudaGetLastError();
 }
 
-// the swapped-role plan for C_out <= 64: returns the number of M-tiles (0 = not applicable)
-static int wgrad_swap_plan(const TcWgradArgs& a, WgSwapParams* p) {
-  if ((a.flags & MPF_FLAG_WGRAD_M128) || a.cout > 64) return 0;
-  const int n_cc = (a.cin + kKC - 1) / kKC, G = a.k * n_cc, npad = (a.cout + 15) / 16 * 16;
+// the M-tiles of the swapped-role plan over G groups (local group indices); returns the tile
+// count, or -1 when more than kSwapMaxTiles
+static int swap_tiles(int k, int G, WgSwapParams* p) {
   int T = 0;
   for (int g = 0; g < G; ++g)
-    for (int t0 = 0; t0 + 4 <= a.k; t0 += 4) {
-      if (T == kSwapMaxTiles) return 0;
-      p->t_group[T] = g; p->t_tap[T] = t0; p->t_across[T] = 0; ++T;
+    for (int t0 = 0; t0 + 4 <= k; t0 += 4) {
+      if (T == kSwapMaxTiles) return -1;
+      if (p) { p->t_group[T] = g; p->t_tap[T] = t0; p->t_across[T] = 0; }
+      ++T;
     }
-  for (int kx = a.k / 4 * 4; kx < a.k; ++kx)
+  for (int kx = k / 4 * 4; kx < k; ++kx)
     for (int g0 = 0; g0 < G; g0 += 4) {
-      if (T == kSwapMaxTiles) return 0;
-      p->t_group[T] = g0; p->t_tap[T] = kx; p->t_across[T] = 1; ++T;
+      if (T == kSwapMaxTiles) return -1;
+      if (p) { p->t_group[T] = g0; p->t_tap[T] = kx; p->t_across[T] = 1; }
+      ++T;
     }
-  if (T * npad > 512) return 0;
-  p->n_tiles = T;
-  p->npad = npad;
-  p->n_cc = n_cc;
-  p->n_groups = G;
   return T;
 }
 
-static cudaError_t launch_wgrad_swap(const TcWgradArgs& a, WgSwapParams& p, int* splits_out, cudaStream_t s) {
+static uint32_t swap_stage_bytes(int G, int npad) {
+  return (uint32_t)G * (kWR + 8) * 128 + (uint32_t)((npad + 31) / 32) * kWR * 128;
+}
+static size_t swap_budget() { return 225 * 1024 - 1024 - 256 - 3 * (kWR + 8) * 128; }
+
+// The swapped-role plan: C_out <= 64, or 64 < C_out <= 96 where C_out on M would leave at least
+// a quarter of every M = 128 tile empty.  A pass's tiles must fit TMEM (tiles x npad <= 512
+// columns) with >= 2 pipeline stages of slabs; when all groups' tiles do not, the groups are
+// split into passes (one launch each over the same position splits, with its own slabs and
+// tiles, writing its own (tap, channel) columns of the partials; dY is re-read per pass).
+// Narrow layers (C_out <= 64) keep the single pass.  Returns the groups per pass (0 = not
+// applicable).
+static int wgrad_swap_plan(const TcWgradArgs& a, WgSwapParams* p) {
+  if ((a.flags & MPF_FLAG_WGRAD_M128) || a.cout > 96) return 0;
+  const int n_cc = (a.cin + kKC - 1) / kKC, G = a.k * n_cc, npad = (a.cout + 15) / 16 * 16;
+  int GP = 0;
+  for (int gp = G; gp >= 1 && !GP; --gp) {
+    const int T = swap_tiles(a.k, gp, nullptr);
+    if (T < 1 || T * npad > 512) continue;
+    if (swap_budget() / swap_stage_bytes(gp, npad) < 2) continue;
+    GP = gp;
+  }
+  if (!GP) return 0;
+  if (GP < G && a.cout <= 64) return 0;
+  p->npad = npad;
+  p->n_cc = n_cc;
+  return GP;
+}
+
+static cudaError_t launch_wgrad_swap(const TcWgradArgs& a, WgSwapParams& p, int GP, int* splits_out, cudaStream_t s) {
   p.P_tot = a.n_frag * a.gr * a.gc;
   p.gc = a.gc;
   p.cin = a.cin;
   p.cout = a.cout;
   p.k = a.k;
+  const int G = a.k * p.n_cc;
   p.a_bytes = (uint32_t)((p.npad + 31) / 32) * kWR * 128;
   p.b_bytes = (kWR + 8) * 128;
-  p.stage_bytes = (uint32_t)p.n_groups * p.b_bytes + p.a_bytes;
-  const size_t budget = 225 * 1024 - 1024 - 256 - 3 * p.b_bytes;
-  p.n_stages_ring = (int)(budget / p.stage_bytes);
-  if (p.n_stages_ring > 4) p.n_stages_ring = 4;
-  if (p.n_stages_ring < 2) return cudaErrorInvalidConfiguration;
-  uint32_t cols = 32;
-  while (cols < (uint32_t)(p.n_tiles * p.npad)) cols <<= 1;
-  p.tmem_cols = cols;
   const long long total_stages = (p.P_tot + kWR - 1) / kWR;
   int splits = num_sms();
   if (splits > kMaxSplits) splits = kMaxSplits;
@@ -1597,18 +1616,32 @@ static cudaError_t launch_wgrad_swap(const TcWgradArgs& a, WgSwapParams& p, int*
   if (e != cudaSuccess) return e;
   e = make_map(&X, a.x, (uint64_t)a.cin, (uint64_t)p.P_tot, (uint32_t)(kWR + 8), CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   if (e != cudaSuccess) return e;
-  const size_t smem = 1024 + (size_t)p.n_stages_ring * p.stage_bytes + 3 * p.b_bytes + 256;
-  e = cudaFuncSetAttribute(wgrad_tc_swap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  wgrad_tc_swap_kernel<<<splits, kThreads, smem, s>>>(D, X, p);
-  return cudaGetLastError();
+  for (int g_lo = 0; g_lo < G; g_lo += GP) {  // passes over disjoint groups: disjoint partial columns
+    p.g_lo = g_lo;
+    p.n_groups = std::min(GP, G - g_lo);
+    p.n_tiles = swap_tiles(a.k, p.n_groups, &p);
+    p.stage_bytes = swap_stage_bytes(p.n_groups, p.npad);
+    p.n_stages_ring = (int)(swap_budget() / p.stage_bytes);
+    if (p.n_stages_ring > 4) p.n_stages_ring = 4;
+    if (p.n_stages_ring < 2 || p.n_tiles < 1) return cudaErrorInvalidConfiguration;
+    uint32_t cols = 32;
+    while (cols < (uint32_t)(p.n_tiles * p.npad)) cols <<= 1;
+    p.tmem_cols = cols;
+    const size_t smem = 1024 + (size_t)p.n_stages_ring * p.stage_bytes + 3 * p.b_bytes + 256;
+    e = cudaFuncSetAttribute(wgrad_tc_swap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    wgrad_tc_swap_kernel<<<splits, kThreads, smem, s>>>(D, X, p);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits_out, cudaStream_t s) {
   if (wgrad_pair_ok(a)) return launch_wgrad_pair(a, splits_out, s);
   {
     WgSwapParams sp{};
-    if (wgrad_swap_plan(a, &sp)) return launch_wgrad_swap(a, sp, splits_out, s);
+    if (const int GP = wgrad_swap_plan(a, &sp)) return launch_wgrad_swap(a, sp, GP, splits_out, s);
   }
   WgTcParams p{};
   p.P_tot = a.n_frag * a.gr * a.gc;

@@ -94,6 +94,28 @@ def test_exchange_two_ranks_one_process(push_in_backward):
     assert np.max(np.abs(p0 - ref)) <= 1e-6 * max(1.0, np.max(np.abs(ref)))
 
 
+def test_exchange_three_ranks_scalar_path():
+    """cfg1 (898 parameters: buckets and slots not multiples of 4 floats, the push kernel's
+    scalar path) with three ranks of one image each, two steps."""
+    cfg = S.CONFIGS["cfg1"]
+    world, per, steps = 3, 1, 2
+    nets = _nets(cfg, per, world)
+    bufs = _exchange_buffers(nets, world)
+    for r, net in enumerate(nets):
+        net.attach_exchange(r, world, [b.data_ptr() for b in bufs])
+    for t in range(steps):
+        for (im, lb), net in zip(_shards(cfg, t, world, per), nets):
+            net.train_step(im, lb)
+        for net in nets:
+            net.sgd_step(LR, 1.0 / (world * per))
+    for net in nets:
+        net.check()
+    ps = [net.params.cpu().numpy() for net in nets]
+    assert np.array_equal(ps[0], ps[1]) and np.array_equal(ps[0], ps[2])
+    ref = _reference(cfg, steps, world, per)
+    assert np.max(np.abs(ps[0] - ref)) <= 1e-6 * max(1.0, np.max(np.abs(ref)))
+
+
 def test_exchange_world1_equals_local_sgd():
     """At world 1 the exchange SGD is the local SGD: bitwise the same parameters."""
     cfg = S.CONFIGS["cfg2"]
