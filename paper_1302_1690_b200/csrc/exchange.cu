@@ -94,8 +94,9 @@ __global__ void __launch_bounds__(256) exchange_sgd_kernel(float* __restrict__ p
   const float* slots = reinterpret_cast<const float*>(own + L.slots) + (long long)par * L.world * L.n_params;
   const long long n = L.n_params;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    float s = slots[i];
-    for (int r = 1; r < L.world; ++r) s += slots[(long long)r * n + i];  // rank order, same on every rank
+    // L2 loads (peers wrote these lines over NVLink; no stale L1 copy can be used)
+    float s = __ldcg(slots + i);
+    for (int r = 1; r < L.world; ++r) s += __ldcg(slots + (long long)r * n + i);  // rank order, same on every rank
     p[i] -= step * s;
     g[i] = 0.f;
   }
