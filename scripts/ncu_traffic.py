@@ -37,11 +37,31 @@ def main():
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     table = json.load(open(path)) if os.path.exists(path) else {}
     print(f"{'kernel':18s} {'L':>3s} {'ncu us':>9s} {'DRAM MB':>9s} {'alg MB':>9s} {'DRAM/alg':>8s} {'dram%':>6s} {'tc%':>6s}  name")
-    for (name, layer, ms, flops, nbytes), r in zip(seq, ours):
-        dram = g(r, "dram__bytes_read.sum") + g(r, "dram__bytes_write.sum")
-        us = g(r, "gpu__time_duration.sum") * 1e6
+    # one library launch can be several kernels: the swapped-role weight gradient in passes
+    # (consecutive wgrad_tc_swap_kernel launches) -> merge them into that launch's row
+    merged, i = [], 0
+    extra = len(ours) - len(seq)
+    for name, *_ in seq:
+        if i >= len(ours):
+            break
+        grp = [ours[i]]
+        i += 1
+        while (extra > 0 and name == "wgrad_tc" and i < len(ours) and "wgrad_tc_swap_kernel" in ours[i][ix["Kernel Name"]]
+               and "wgrad_tc_swap_kernel" in grp[0][ix["Kernel Name"]]):
+            grp.append(ours[i])
+            i += 1
+            extra -= 1
+        merged.append(grp)
+    for (name, layer, ms, flops, nbytes), grp in zip(seq, merged):
+        r = grp[0]
+        dram = sum(g(x, "dram__bytes_read.sum") + g(x, "dram__bytes_write.sum") for x in grp)
+        us = sum(g(x, "gpu__time_duration.sum") for x in grp) * 1e6
+        if len(grp) > 1:
+            name_note = f" ({len(grp)} passes)"
+        else:
+            name_note = ""
         table[f"{wl}:{name}:{layer}"] = dram
-        kn = r[ix["Kernel Name"]].split("(")[0].replace("void ", "").replace("mpf::", "")[:40]
+        kn = r[ix["Kernel Name"]].split("(")[0].replace("void ", "").replace("mpf::", "")[:40] + name_note
         print(f"{name:18s} {layer:3d} {us:9.1f} {dram / 1e6:9.1f} {nbytes / 1e6:9.1f} {dram / max(nbytes, 1):8.2f} "
               f"{g(r, 'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed'):6.1f} "
               f"{g(r, 'sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed'):6.1f}  {kn}")
