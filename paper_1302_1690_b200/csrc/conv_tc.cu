@@ -1338,16 +1338,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 // atoms read other shared memory and are discarded).  Same products as wgrad_tc_kernel,
 // summed in the same K order per split.
 constexpr int kSwapMaxTiles = 16;
+constexpr int kSwapMaxPass = 4;
 struct WgSwapParams {
-  int P_tot, gc, cin, cout, npad, k, n_cc, n_groups, n_tiles;
-  int g_lo;  // this pass's first (ky, channel chunk) group: its slabs are groups g_lo .. g_lo + n_groups - 1
+  int P_tot, gc, cin, cout, npad, k, n_cc;
+  int n_pass;  // passes over disjoint (ky, channel chunk) group ranges; CTA = (split, pass)
   int chunk_stages;
   float* part;
-  uint32_t a_bytes, b_bytes, stage_bytes;  // a = the dY tile, b = one X slab
+  uint32_t a_bytes, b_bytes, stage_bytes;  // a = the dY tile, b = one X slab; stage: the largest pass's
   int n_stages_ring;
-  uint32_t tmem_cols;
-  // per M-tile: first atom (group, tap) and the atom stride (0: taps of one group, 1: groups)
-  int t_group[kSwapMaxTiles], t_tap[kSwapMaxTiles], t_across[kSwapMaxTiles];
+  uint32_t tmem_cols;  // the largest pass's
+  // per pass: first group (its slabs are groups g_lo .. g_lo + n_groups - 1) and its M-tiles:
+  // first atom (local group, tap) and the atom stride (0: taps of one group, 1: groups)
+  int g_lo[kSwapMaxPass], n_groups[kSwapMaxPass], n_tiles[kSwapMaxPass];
+  int t_group[kSwapMaxPass][kSwapMaxTiles], t_tap[kSwapMaxPass][kSwapMaxTiles], t_across[kSwapMaxPass][kSwapMaxTiles];
 };
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -1362,9 +1365,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sTmemSlot = barT + 8;
   uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (sTmemSlot - ptx::smem_u32(smem_raw)));
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-  const int split = blockIdx.x;
+  // the passes of one position split are adjacent CTAs: they stream the same dY / X rows at
+  // about the same time, so a pass's re-read of dY is served by L2
+  const int pass = blockIdx.x % p.n_pass, split = blockIdx.x / p.n_pass;
+  const int g_lo = p.g_lo[pass], n_groups = p.n_groups[pass], n_tiles = p.n_tiles[pass];
   const long long pbeg = (long long)split * p.chunk_stages * kWR;
-  const uint32_t slabs_bytes = (uint32_t)p.n_groups * p.b_bytes;
+  const uint32_t slabs_bytes = (uint32_t)n_groups * p.b_bytes;
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmD);
@@ -1392,8 +1398,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_arrive_expect_tx(barFull + 8 * slot, p.a_bytes + slabs_bytes);
         const uint32_t sa = sbase + slot * p.stage_bytes;
         const int row = (int)(pbeg + (long long)st * kWR);
-        for (int g = 0; g < p.n_groups; ++g) {
-          const int ky = (p.g_lo + g) / p.n_cc, cc = (p.g_lo + g) % p.n_cc;
+        for (int g = 0; g < n_groups; ++g) {
+          const int ky = (g_lo + g) / p.n_cc, cc = (g_lo + g) % p.n_cc;
           ptx::tma_load_2d(sa + g * p.b_bytes, &tmX, barFull + 8 * slot, cc * kKC, row + ky * p.gc);
         }
         for (int j = 0; j < n_datoms; ++j)
@@ -1408,9 +1414,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tc_fence_after();
       const uint32_t sa = sbase + slot * p.stage_bytes;
       const uint64_t bd0 = ptx::sdesc_mn_sw128_32b(sa + slabs_bytes, kWR * 128, 512);
-      for (int t = 0; t < p.n_tiles; ++t) {
-        const uint32_t a0 = sa + p.t_group[t] * p.b_bytes + p.t_tap[t] * 128;
-        const uint64_t ad0 = ptx::sdesc_mn_sw128_32b(a0, p.t_across[t] ? p.b_bytes : 128u, 512);
+      for (int t = 0; t < n_tiles; ++t) {
+        const uint32_t a0 = sa + p.t_group[pass][t] * p.b_bytes + p.t_tap[pass][t] * 128;
+        const uint64_t ad0 = ptx::sdesc_mn_sw128_32b(a0, p.t_across[pass][t] ? p.b_bytes : 128u, 512);
 #pragma unroll
         for (int r8 = 0; r8 < kWR / 8; ++r8) {
           const uint64_t ad = ad0 + (uint64_t)((r8 * 1024) >> 4);
@@ -1428,11 +1434,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::mbar_wait(barT, 0);
     ptx::tc_fence_after();
     const int K = p.k * p.k * p.cin;
-    for (int t = 0; t < p.n_tiles; ++t) {
-      const int g = p.t_across[t] ? p.t_group[t] + q : p.t_group[t];
-      const int kx = p.t_across[t] ? p.t_tap[t] : p.t_tap[t] + q;
-      const bool atom_ok = g < p.n_groups && kx < p.k;  // warp-uniform
-      const int ky = atom_ok ? (p.g_lo + g) / p.n_cc : 0, cc = atom_ok ? (p.g_lo + g) % p.n_cc : 0;
+    for (int t = 0; t < n_tiles; ++t) {
+      const int g = p.t_across[pass][t] ? p.t_group[pass][t] + q : p.t_group[pass][t];
+      const int kx = p.t_across[pass][t] ? p.t_tap[pass][t] : p.t_tap[pass][t] + q;
+      const bool atom_ok = g < n_groups && kx < p.k;  // warp-uniform
+      const int ky = atom_ok ? (g_lo + g) / p.n_cc : 0, cc = atom_ok ? (g_lo + g) % p.n_cc : 0;
       const int ci = cc * kKC + lane;
       const bool ok = atom_ok && ci < p.cin;
       float* dst = p.part + (long long)split * p.cout * K + (ky * p.k + kx) * p.cin + (ok ? ci : 0);
@@ -1545,18 +1551,18 @@ static cudaError_t launch_wgrad_pair(const TcWgradArgs& a, int* splits_out, cuda
 
 // the M-tiles of the swapped-role plan over G groups (local group indices); returns the tile
 // count, or -1 when more than kSwapMaxTiles
-static int swap_tiles(int k, int G, WgSwapParams* p) {
+static int swap_tiles(int k, int G, WgSwapParams* p, int pass = 0) {
   int T = 0;
   for (int g = 0; g < G; ++g)
     for (int t0 = 0; t0 + 4 <= k; t0 += 4) {
       if (T == kSwapMaxTiles) return -1;
-      if (p) { p->t_group[T] = g; p->t_tap[T] = t0; p->t_across[T] = 0; }
+      if (p) { p->t_group[pass][T] = g; p->t_tap[pass][T] = t0; p->t_across[pass][T] = 0; }
       ++T;
     }
   for (int kx = k / 4 * 4; kx < k; ++kx)
     for (int g0 = 0; g0 < G; g0 += 4) {
       if (T == kSwapMaxTiles) return -1;
-      if (p) { p->t_group[T] = g0; p->t_tap[T] = kx; p->t_across[T] = 1; }
+      if (p) { p->t_group[pass][T] = g0; p->t_tap[pass][T] = kx; p->t_across[pass][T] = 1; }
       ++T;
     }
   return T;
@@ -1586,6 +1592,7 @@ static int wgrad_swap_plan(const TcWgradArgs& a, WgSwapParams* p) {
   }
   if (!GP) return 0;
   if (GP < G && a.cout <= 64) return 0;
+  if ((G + GP - 1) / GP > kSwapMaxPass) return 0;
   p->npad = npad;
   p->n_cc = n_cc;
   return GP;
@@ -1616,24 +1623,30 @@ static cudaError_t launch_wgrad_swap(const TcWgradArgs& a, WgSwapParams& p, int 
   if (e != cudaSuccess) return e;
   e = make_map(&X, a.x, (uint64_t)a.cin, (uint64_t)p.P_tot, (uint32_t)(kWR + 8), CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   if (e != cudaSuccess) return e;
-  for (int g_lo = 0; g_lo < G; g_lo += GP) {  // passes over disjoint groups: disjoint partial columns
-    p.g_lo = g_lo;
-    p.n_groups = std::min(GP, G - g_lo);
-    p.n_tiles = swap_tiles(a.k, p.n_groups, &p);
-    p.stage_bytes = swap_stage_bytes(p.n_groups, p.npad);
-    p.n_stages_ring = (int)(swap_budget() / p.stage_bytes);
-    if (p.n_stages_ring > 4) p.n_stages_ring = 4;
-    if (p.n_stages_ring < 2 || p.n_tiles < 1) return cudaErrorInvalidConfiguration;
-    uint32_t cols = 32;
-    while (cols < (uint32_t)(p.n_tiles * p.npad)) cols <<= 1;
-    p.tmem_cols = cols;
-    const size_t smem = 1024 + (size_t)p.n_stages_ring * p.stage_bytes + 3 * p.b_bytes + 256;
-    e = cudaFuncSetAttribute(wgrad_tc_swap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    wgrad_tc_swap_kernel<<<splits, kThreads, smem, s>>>(D, X, p);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+  // passes over disjoint groups (disjoint partial columns), launched together
+  p.n_pass = 0;
+  int max_tiles = 0;
+  for (int g_lo = 0; g_lo < G; g_lo += GP) {
+    const int q = p.n_pass++;
+    p.g_lo[q] = g_lo;
+    p.n_groups[q] = std::min(GP, G - g_lo);
+    p.n_tiles[q] = swap_tiles(a.k, p.n_groups[q], &p, q);
+    if (p.n_tiles[q] < 1) return cudaErrorInvalidConfiguration;
+    max_tiles = std::max(max_tiles, p.n_tiles[q]);
   }
+  p.stage_bytes = swap_stage_bytes(std::min(GP, G), p.npad);
+  p.n_stages_ring = (int)(swap_budget() / p.stage_bytes);
+  if (p.n_stages_ring > 4) p.n_stages_ring = 4;
+  if (p.n_stages_ring < 2) return cudaErrorInvalidConfiguration;
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(max_tiles * p.npad)) cols <<= 1;
+  p.tmem_cols = cols;
+  const size_t smem = 1024 + (size_t)p.n_stages_ring * p.stage_bytes + 3 * p.b_bytes + 256;
+  e = cudaFuncSetAttribute(wgrad_tc_swap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  wgrad_tc_swap_kernel<<<splits * p.n_pass, kThreads, smem, s>>>(D, X, p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
   return cudaSuccess;
 }
 
