@@ -328,7 +328,9 @@ mpf_status mpf_line_search_decide(double L0, double gtd, double c, double beta, 
 typedef void (*mpf_grad_ready_fn)(void* user, int32_t layer, int64_t offset, int64_t count, void* stream);
 mpf_status mpf_net_set_grad_hook(mpf_net* net, mpf_grad_ready_fn fn, void* user);
 
-/* SGD: theta <- theta - lr * grad_scale * g ; g <- 0. */
+/* SGD: theta <- theta - lr * grad_scale * g ; g <- 0.  While a peer-memory
+ * exchange is attached (mpf_exchange_attach) this is mpf_exchange_sgd_step: g is the sum of
+ * every rank's gradient. */
 mpf_status mpf_sgd_step(mpf_net* net, float lr, float grad_scale, void* stream);
 
 /*
