@@ -690,15 +690,24 @@ __global__ void __launch_bounds__(256, 3) mpf_bwd_band2_kernel(MpfBwdArgs a, lon
   write_bias_rows(a, bsum, sub, nsub, cv);
 }
 
-// Register-blocked gather for k = 3: a thread owns a 3 x BW block of conv-output elements of
-// one channel vector; the candidate windows form the 5 x (BW + 2) patch rows 3i-2 .. 3i+2.
-// Output row ea needs patch rows ea .. ea+2, so the patch streams through a ring of 3 rows:
-// rows 0-2 are loaded up front, row ea+3 after output row ea.  BW = 1 (MPF_BWD_BW3=1: 45 window
-// registers) or 3 (default: fewer loads per element; measured 1.84 vs 2.75 ms on cfg5).
-// Same fixed (dy, dx) order as the other MPF backward kernels (bitwise-identical results).
-template <int K, int BW>  // k and block width in output columns (patch (2k-1) x (BW+k-1))
-__global__ void __launch_bounds__(256) mpf_bwd_block3_kernel(MpfBwdArgs a, long long n_groups) {
-  constexpr int PW = BW + K - 1;
+// Register-blocked gather for k = 3 (premul deltas, 4-channel vectors): a thread owns a 3 x 3
+// block of conv-output elements of one channel vector; the candidate windows form the 5 x 5
+// patch rows 3i-2 .. 3i+2.  Output row ea needs patch rows ea .. ea+2, so the patch streams
+// through a ring of 3 rows: rows 0-2 are loaded up front, row ea+3 after output row ea.  Same
+// fixed (dy, dx) order as the other MPF backward kernels.  Against the first form of this
+// kernel (bitwise equal deltas, tested before it was removed; cfg5 layer 5 0.86 -> 0.76-0.79 ms,
+// profiles/r2/mpf_bwd_k3_lean_ab_cfg5.log) it has
+//  - 32-bit work-item decoding (the grid-stride loop decoded a 64-bit group index with three
+//    64-bit divisions per block);
+//  - window offsets without division: patch column v of block column bj is window column
+//    3 bj - 2 + v, i.e. offset fragment (v + 1) % 3, cell bj - 1 + (v + 1) / 3 -- compile-time
+//    coefficients times the runtime strides -- and the same for the rows;
+//  - no selects on the loads: a window outside the window grid loads from an in-bounds
+//    address (its row or column offset is replaced by 0) and its argmax word is OR-ed with
+//    0xFFFFFFFF, which no candidate test (byte == dy*3+dx <= 8) accepts, so its delta is
+//    never added.
+__global__ void __launch_bounds__(256, 2) mpf_bwd_k3_kernel(MpfBwdArgs a, int n_groups) {
+  constexpr int K = 3, BW = 3, PW = 5;
   const int C = a.C, CV = C / 4;
   const int tid = threadIdx.x, cv = tid % CV, sub = tid / CV, nsub = 256 / CV;
   const int Xw = K * a.m_c, Yw = K * a.m_r;
@@ -707,42 +716,47 @@ __global__ void __launch_bounds__(256) mpf_bwd_block3_kernel(MpfBwdArgs a, long 
   const int groups_per_row = (bj_n + nsub - 1) / nsub;
   float bsum[4] = {0.f, 0.f, 0.f, 0.f};
   if (sub < nsub) {
-    for (long long grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
-      const int gj = (int)(grp % groups_per_row);
-      const long long t = grp / groups_per_row;
-      const int bi = (int)(t % bi_n);
-      const int g = (int)(t / bi_n);
+    for (int grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
+      const int t = grp / groups_per_row;
+      const int gj = grp - t * groups_per_row;
+      const int g = t / bi_n;
+      const int bi = t - g * bi_n;
       const int bj = gj * nsub + sub;
       if (bj >= bj_n) continue;
-      const float* dsrc = a.dout + (size_t)g * K * K * MMC + cv * 4;
-      const uint8_t* isrc = a.idx + (size_t)g * K * K * MMC + cv * 4;
+      const size_t fbase = (size_t)g * K * K * MMC + cv * 4;
+      const float* dsrc = a.dout + fbase;
+      const uint8_t* isrc = a.idx + fbase;
       int coloff[PW];
-      bool colok[PW];
+      uint32_t colbad[PW];
 #pragma unroll
       for (int v = 0; v < PW; ++v) {
         const int wx = BW * bj - (K - 1) + v;
-        colok[v] = wx >= 0 && wx < Xw;
-        coloff[v] = colok[v] ? (wx % K) * MMC + (wx / K) * C : 0;
+        const bool bad = wx < 0 || wx >= Xw;
+        coloff[v] = bad ? 0 : ((v + 1) % K) * MMC + (bj - 1 + (v + 1) / K) * C;
+        colbad[v] = bad ? 0xFFFFFFFFu : 0u;
       }
       uint32_t id[K][PW];
       float4 d[K][PW];
       auto load_row = [&](int u, uint32_t (&ir)[PW], float4 (&dr)[PW]) {
         const int wy = K * bi - (K - 1) + u;
-        const bool yok = wy >= 0 && wy < Yw;
-        const int rowoff = yok ? (wy % K) * K * MMC + (wy / K) * mcC : 0;
+        const bool bad = wy < 0 || wy >= Yw;
+        const int rowoff = bad ? 0 : ((u + 1) % K) * K * MMC + (bi - 1 + (u + 1) / K) * mcC;
+        const uint32_t rbad = bad ? 0xFFFFFFFFu : 0u;
+        const uint8_t* ip = isrc + rowoff;
+        const float* dp = dsrc + rowoff;
 #pragma unroll
         for (int v = 0; v < PW; ++v) {
-          const bool ok = yok && colok[v];
-          const int off = ok ? rowoff + coloff[v] : 0;
-          ir[v] = ok ? __ldg(reinterpret_cast<const uint32_t*>(isrc + off)) : 0xFFFFFFFFu;
-          dr[v] = ok ? __ldg(reinterpret_cast<const float4*>(dsrc + off)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          ir[v] = __ldg(reinterpret_cast<const uint32_t*>(ip + coloff[v])) | rbad | colbad[v];
+          dr[v] = __ldg(reinterpret_cast<const float4*>(dp + coloff[v]));
         }
       };
 #pragma unroll
       for (int u = 0; u < K; ++u) load_row(u, id[u], d[u]);
-      float* dst = a.din + ((size_t)g * a.gr * a.gc) * C + cv * 4;
+      float* dst = a.din + (size_t)g * a.gr * a.gc * C + cv * 4;
+      const int gcC = a.gc * C;
+      int eoff = K * bi * gcC + BW * bj * C;  // 32-bit element offset inside the fragment
 #pragma unroll
-      for (int ea = 0; ea < K; ++ea) {
+      for (int ea = 0; ea < K; ++ea, eoff += gcC) {
         const int Y = K * bi + ea;
 #pragma unroll
         for (int eb = 0; eb < BW; ++eb) {
@@ -767,7 +781,7 @@ __global__ void __launch_bounds__(256) mpf_bwd_block3_kernel(MpfBwdArgs a, long 
             bsum[q] += acc[q];
             o[q] = a.round_tf32 ? tf32_rn(acc[q]) : acc[q];
           }
-          stv<4>(dst + (Y * a.gc + X) * C, o);
+          stv<4>(dst + eoff + eb * C, o);
         }
         if (ea + K < 2 * K - 1) load_row(ea + K, id[(ea + K) % K], d[(ea + K) % K]);  // replaces patch row ea
       }
@@ -1187,7 +1201,10 @@ cudaError_t launch_mpf_bwd(const MpfBwdArgs& a, cudaStream_t s) {
     const size_t smem = 0;
     if (use_band2(a)) mpf_bwd_band2_kernel<<<block2_grid(a), 256, smem, s>>>(a, band2_units(a), band2_rows(a));
     else if (a.k == 2) mpf_bwd_block2_kernel<<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
-    else mpf_bwd_block3_kernel<3, 3><<<block2_grid(a), 256, smem, s>>>(a, block2_groups(a));
+    else {
+      if (block2_groups(a) > 0x7fffffffLL) return cudaErrorInvalidValue;
+      mpf_bwd_k3_kernel<<<block2_grid(a), 256, smem, s>>>(a, (int)block2_groups(a));
+    }
     return cudaGetLastError();
   }
   const int V = a.C % 4 == 0 ? 4 : 1;
