@@ -1488,6 +1488,24 @@ static bool wgrad_pair_ok(const TcWgradArgs& a) {
   return !(a.flags & MPF_FLAG_TC_SINGLE) && a.cout > 128 && a.cout <= 256 && 64 * a.k <= 256 && a.k * a.cin > 32;
 }
 
+// Split-K count of a tensor-core weight gradient.  The tensor core adds every K step's
+// products into the fp32 accumulator without rounding to nearest, so the error of a sum grows
+// with the length of the accumulation chain: on cfg4's FC1 weight gradient (7.1 M positions)
+// one wave of 24 splits (296 K positions per chain) is 2.06e-3 from the fp64 oracle, 48 / 96 /
+// 192 splits are 1.03e-3 / 5.3e-4 / 3.1e-4 (profiles/r2/wgrad_chain_length_cfg4.log), at
+// 5.07 / 5.05 / 5.11 / 5.29 ms.  Chains are therefore capped at kMaxChain positions: whole
+// extra waves of splits (each ends in an fp32 partial; the fixed-order reduction adds the
+// partials in round-to-nearest fp32), which also keeps the error independent of the batch size.
+constexpr long long kMaxChain = 80 * 1024;
+static int wgrad_splits(int one_wave, long long P_tot) {
+  if (one_wave < 1) one_wave = 1;
+  long long s = one_wave;
+  const long long need = (P_tot + kMaxChain - 1) / kMaxChain;
+  if (need > s) s = (need + one_wave - 1) / one_wave * one_wave;
+  if (s > kMaxSplits) s = one_wave <= kMaxSplits ? (long long)(kMaxSplits / one_wave) * one_wave : kMaxSplits;
+  return (int)s;
+}
+
 static cudaError_t launch_wgrad_pair(const TcWgradArgs& a, int* splits_out, cudaStream_t s) {
   WgPairParams p{};
   p.P_tot = a.n_frag * a.gr * a.gc;
@@ -1513,9 +1531,7 @@ static cudaError_t launch_wgrad_pair(const TcWgradArgs& a, int* splits_out, cuda
   while (cols < (uint32_t)(p.G2 * N2)) cols <<= 1;
   p.tmem_cols = cols;
   const long long total_stages = (p.P_tot + kWR - 1) / kWR;
-  int splits = num_sms() / (2 * p.n_sets);
-  if (splits > kMaxSplits) splits = kMaxSplits;
-  if (splits < 1) splits = 1;
+  int splits = wgrad_splits(num_sms() / (2 * p.n_sets), p.P_tot);  // whole waves of co-resident CTA pairs
   const size_t K = (size_t)a.k * a.k * a.cin;
   while (splits > 1 && (size_t)splits * (a.cout * K + a.cout) > a.part_cap_floats) --splits;
   if (splits > total_stages) splits = (int)total_stages;
@@ -1608,8 +1624,7 @@ static cudaError_t launch_wgrad_swap(const TcWgradArgs& a, WgSwapParams& p, int 
   p.a_bytes = (uint32_t)((p.npad + 31) / 32) * kWR * 128;
   p.b_bytes = (kWR + 8) * 128;
   const long long total_stages = (p.P_tot + kWR - 1) / kWR;
-  int splits = num_sms();
-  if (splits > kMaxSplits) splits = kMaxSplits;
+  int splits = wgrad_splits(num_sms(), p.P_tot);
   const size_t K = (size_t)a.k * a.k * a.cin;
   while (splits > 1 && (size_t)splits * (a.cout * K + a.cout) > a.part_cap_floats) --splits;
   if (splits > total_stages) splits = (int)total_stages;
@@ -1687,9 +1702,7 @@ cudaError_t launch_wgrad_tc(const TcWgradArgs& a, int* splits_out, cudaStream_t 
   p.tmem_cols = cols;
   const long long total_stages = (p.P_tot + kWR - 1) / kWR;
   const int per_split_blocks = p.m_tiles * p.n_sets;
-  int splits = num_sms() / per_split_blocks;  // one wave of co-resident CTAs
-  if (splits > kMaxSplits) splits = kMaxSplits;
-  if (splits < 1) splits = 1;
+  int splits = wgrad_splits(num_sms() / per_split_blocks, p.P_tot);  // whole waves of co-resident CTAs
   const size_t K = (size_t)a.k * a.k * a.cin;
   while (splits > 1 && (size_t)splits * (a.cout * K + a.cout) > a.part_cap_floats) --splits;
   if (splits > total_stages) splits = (int)total_stages;
