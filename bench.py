@@ -447,6 +447,27 @@ def main():
     roof["measured"] = (f"CUDA events per launch over {args.steps} steps with the weight gradients serialised on "
                         f"the main stream ({ser_ms / args.steps:.2f} ms/step), right after the timed loop")
     roof["algorithmic_per_launch"] = dom["flops"] if roof["bound"] != "hbm" else dom["bytes"]
+    # The library counts the positions of the uniform-fragment layout (every fragment padded
+    # to the largest one): a few % more than the dense positions the
+    # paper's sums run over ((H - rf + 1)(W - rf + 1) per image at that layer).  The stricter
+    # fraction counts only those.
+    try:
+        rr, cc, d = cfg.H, cfg.W, 1
+        dense = []
+        for Ly in cfg.layers:
+            rr, cc = rr - (Ly.k - 1) * d, cc - (Ly.k - 1) * d
+            if Ly.kind == S.POOL:
+                d *= Ly.k
+            dense.append(rr * cc)
+        lay = dom["layer"]
+        if 0 <= lay < len(dense):
+            uni = net.geom.frag[lay + 1] * net.geom.rows[lay + 1] * net.geom.cols[lay + 1]
+            roof["dense_positions_per_image"] = dense[lay]
+            roof["uniform_fragment_positions_per_image"] = int(uni)
+            if roof["bound"] != "hbm" and uni >= dense[lay] > 0:
+                roof["frac_dense_positions"] = roof["frac"] * dense[lay] / uni
+    except Exception as ex:  # noqa: BLE001 -- a reporting detail must not fail the run
+        print(f"[bench] dense-position fraction skipped ({ex})", file=sys.stderr)
 
     if args.profile_json and rank == 0:
         with open(args.profile_json, "w") as f:
