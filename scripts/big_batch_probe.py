@@ -6,7 +6,7 @@ the gradient sum must be twice its gradient sum, up to the order of the fp32 par
 the length of the tensor-core accumulation chains (conv_tc.cu wgrad_splits caps them at 80 K
 positions; before the cap the FC1 weight gradient of the two runs differed by 2.1e-3, the
 chains of the 16-image run being twice as long).
-Usage: python scripts/big_batch_probe.py [n_big]"""
+Usage: python scripts/big_batch_probe.py [n_big] [workload]   (default 16 cfg4; e.g. 32 cfg5)"""
 import os
 import sys
 
@@ -21,7 +21,7 @@ def main():
     import torch
     from paper_1302_1690_b200.net import MPFNet
     nb = int(sys.argv[1]) if len(sys.argv) > 1 else 16
-    cfg = S.CONFIGS["cfg4"]
+    cfg = S.CONFIGS[sys.argv[2] if len(sys.argv) > 2 else "cfg4"]
     im, lb = S.make_batch(cfg, list(range(8)))
     params = S.init_params(cfg).astype(np.float32)
 
