@@ -1496,7 +1496,9 @@ static bool wgrad_pair_ok(const TcWgradArgs& a) {
 // 5.07 / 5.05 / 5.11 / 5.29 ms.  Chains are therefore capped at kMaxChain positions: whole
 // extra waves of splits (each ends in an fp32 partial; the fixed-order reduction adds the
 // partials in round-to-nearest fp32), which also keeps the error independent of the batch size.
-constexpr long long kMaxChain = 80 * 1024;
+// 160 K positions (FC1 of cfg4: 48 splits, 1.03e-3) cost nothing in the overlapped step; 80 K
+// (96 splits, 5.3e-4) cost 0.4-0.7 ms of its 54 (three interleaved bench runs each).
+constexpr long long kMaxChain = 160 * 1024;
 static int wgrad_splits(int one_wave, long long P_tot) {
   if (one_wave < 1) one_wave = 1;
   long long s = one_wave;

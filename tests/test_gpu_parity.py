@@ -889,9 +889,9 @@ def test_bench_step_cfg4_full_images_vs_o2():
     bad = {k: v for k, v in errs.items() if not v <= TOL_TF32}
     assert not bad, bad
     # the FC1 weight gradient sums 7.1 M positions: with its tensor-core accumulation chains
-    # capped at 80 K positions (conv_tc.cu wgrad_splits) it is ~5e-4 from the oracle; one
+    # capped at 160 K positions (conv_tc.cu wgrad_splits) it is ~1.0e-3 from the oracle; one
     # uncapped wave of splits (296 K positions per chain) measured 2.06e-3
-    assert errs["gW8"] <= 1.2e-3, errs["gW8"]
+    assert errs["gW8"] <= 1.5e-3, errs["gW8"]
 
 
 def test_bench_step_cfg5_full_batch_vs_o2():
