@@ -3,7 +3,7 @@
 deltas hold 2.8e9 fp32 elements each: beyond 2^31) against the same net bound for 8.  The 16
 images are the bench's 8 images twice, so per-image losses must repeat the 8-image run's and
 the gradient sum must be twice its gradient sum, up to the order of the fp32 partial sums and
-the length of the tensor-core accumulation chains (conv_tc.cu wgrad_splits caps them at 80 K
+the length of the tensor-core accumulation chains (conv_tc.cu wgrad_splits caps them at 160 K
 positions; before the cap the FC1 weight gradient of the two runs differed by 2.1e-3, the
 chains of the 16-image run being twice as long).
 Usage: python scripts/big_batch_probe.py [n_big] [workload]   (default 16 cfg4; e.g. 32 cfg5)"""
